@@ -1,0 +1,390 @@
+"""Plain, slow, fp64 NumPy oracle of the GmGM hot path (arXiv 2407.19892).
+
+TEST INFRASTRUCTURE — not product code.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import or run anything in ``oracle/``.
+
+Citations: ``P:n`` = PAPER.md line n (LaTeX source of arXiv 2407.19892),
+``S:n`` = SPEC.md line n, readings Q1..Q15 / G / T / TOL = DESIGN.md §"Readings".
+
+Pinning (tests/test_oracle_pins.py, ``-m "not gpu"``):
+  matricize / gram_eig      eigh(S) vs SVD route; tr S_l = ||X||_F^2; E_1 = E_2 for
+                            matrices; vec^T(⊕Ψ)vec = Σ tr[S_l Ψ_l] (brute force)
+  grid_sums / marginals     dense Kronecker-sum inverse + stridewise-blockwise trace
+                            (brute force); golden example S:234
+  nll                       dense log-pseudodeterminant NLL on tiny inputs;
+                            convexity (Lemma 4)
+  gradient                  finite differences of nll; single axis closed form
+  solve_eigvals             Lemma 3 on dense ⊕Ψ; isotropic closed form;
+                            Alg. 1 gradient descent (paper_gd_solve) reaches the same grid
+  canonical gauge           grid invariance; PSD; closed form on shifted inputs
+  psi_rows / top_t / thr    dense V diag(λ) V^T + brute-force sort on tiny inputs;
+                            rank-1 closed form; identity-factor all-tie case
+No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "RankError", "matricize", "gram", "gram_eig", "gram_eig_eigh",
+    "grid_sums", "marginals", "marginals_sq2d", "nll", "gradient", "stationarity",
+    "solve_eigvals", "paper_gd_solve", "canonical_gauge", "identifiable",
+    "trace_inconsistency",
+    "kron_sum", "sb_trace", "dense_nll",
+    "psi_rows", "top_t_row", "threshold_row", "sparse_precision",
+]
+
+
+class RankError(ValueError):
+    """k_l exceeds the attainable rank (Cor. 3)."""
+
+
+# ---------------------------------------------------------------------------
+# Gram spectrum — Algorithm 1 lines 1-4, Theorem 1
+# ---------------------------------------------------------------------------
+
+def matricize(x: np.ndarray, axis: int) -> np.ndarray:
+    """l-matricization mat_l[D]: a d_l x d_{\\l} matrix whose row i holds every
+    entry with l-index i.  First axis has the largest stride; the column order
+    does not affect S_l = mat_l mat_l^T."""
+    x = np.asarray(x, dtype=np.float64)
+    return np.moveaxis(x, axis, 0).reshape(x.shape[axis], -1)
+
+
+def gram(x: np.ndarray, axis: int) -> np.ndarray:
+    """Empirical Gram matrix S_l = mat_l[D] mat_l[D]^T, fp64."""
+    m = matricize(x, axis)
+    return m @ m.T
+
+
+def _check_rank(e: np.ndarray, k: int):
+    if not (e[k - 1] > 1e-12 * e[0]):
+        raise RankError(f"E_k={e[k-1]:.3e} <= 1e-12*E_1 ({e[0]:.3e}); k exceeds rank (S:140)")
+
+
+def gram_eig(x: np.ndarray, axis: int, k: int):
+    """Top-k left singular vectors of D_l = mat_l[D] and E = sigma^2 (Alg. 1 lines 3-4,
+    P:910-911: "top k_l left singular vectors of D_l", "(top k_l singular values)^2").
+
+    Returns V (d_l x k, fp64) and E (k, descending).  Single modality: D_l = mat_l.
+    """
+    m = matricize(x, axis)
+    if not 1 <= k <= min(m.shape):
+        raise RankError(f"k={k} not in [1, min(d_l, d_\\l)={min(m.shape)}] (S:116)")
+    u, sig, _ = np.linalg.svd(m, full_matrices=False)
+    e = sig ** 2
+    _check_rank(e, k)
+    return u[:, :k].copy(), e[:k].copy()
+
+
+def gram_eig_eigh(x: np.ndarray, axis: int, k: int):
+    """Independent route (pin only): eigh of the explicitly formed S_l."""
+    s = gram(x, axis)
+    e, v = np.linalg.eigh(s)
+    order = np.argsort(-e, kind="stable")
+    e, v = e[order], v[:, order]
+    _check_rank(e, k)
+    return v[:, :k].copy(), e[:k].copy()
+
+
+# ---------------------------------------------------------------------------
+# Eigenvalue grid — Theorem 2, elementwise form (Lemma 6 proof P:662-668)
+# ---------------------------------------------------------------------------
+
+def grid_sums(lams) -> np.ndarray:
+    """s_j = Σ_l λ_l[j_l] on the full k-grid (the diagonal of ⊕Λ), shape (k_1..k_L);
+    axis 1 outermost, matching ⊕ = Σ I_{<l} ⊗ Λ_l ⊗ I_{>l}."""
+    s = np.zeros(())
+    for lam in lams:
+        s = np.add.outer(s, np.asarray(lam, dtype=np.float64))
+    return s
+
+
+def marginals(lams):
+    """g_l[i] = Σ_{grid points j with j_l = i} 1/s_j — the diagonal of
+    tr^{k<l}_{k>l}[(⊕Λ)^†] in Thm 2, elementwise as in P:667."""
+    s = grid_sums(lams)
+    if s.min() <= 0:
+        raise ValueError("grid sum <= 0: outside the domain (Lemma 4, P:650)")
+    r = 1.0 / s
+    out = []
+    for ax in range(s.ndim):
+        other = tuple(a for a in range(s.ndim) if a != ax)
+        out.append(r.sum(axis=other) if other else r.copy())
+    return out
+
+
+def marginals_sq2d(lams):
+    """Second-order marginals of 1/s^2 used by the Newton oracle: returns
+    (diag list: Σ_{j_l=i} 1/s^2, pair dict {(l,m): Σ_{j_l=i, j_m=j} 1/s^2})."""
+    s = grid_sums(lams)
+    r2 = 1.0 / (s * s)
+    L = s.ndim
+    diag, pair = [], {}
+    for a in range(L):
+        other = tuple(x for x in range(L) if x != a)
+        diag.append(r2.sum(axis=other) if other else r2.copy())
+    for a in range(L):
+        for b in range(a + 1, L):
+            other = tuple(x for x in range(L) if x not in (a, b))
+            pair[(a, b)] = r2.sum(axis=other) if other else r2.copy()
+    return diag, pair
+
+
+def nll(E, lams) -> float:
+    """NLL(λ) = ½ Σ_l e_l^T λ_l − ½ Σ_{grid} log s_j  (constants of P:262
+    dropped, reading Q11)."""
+    s = grid_sums(lams)
+    if s.min() <= 0:
+        return np.inf
+    lin = sum(float(np.dot(np.asarray(e, np.float64), np.asarray(l, np.float64)))
+              for e, l in zip(E, lams))
+    return 0.5 * lin - 0.5 * float(np.log(s).sum())
+
+
+def gradient(E, lams):
+    """∂NLL/∂Λ_l = ½ (E_l − g_l)  (Theorem 2)."""
+    g = marginals(lams)
+    return [0.5 * (np.asarray(e, np.float64) - gl) for e, gl in zip(E, g)]
+
+
+def stationarity(E, lams) -> float:
+    """max_l max_i |E_li − g_li| / max E  (reading Q4)."""
+    g = marginals(lams)
+    emax = max(float(np.max(e)) for e in E)
+    return max(float(np.max(np.abs(np.asarray(e) - gl))) for e, gl in zip(E, g)) / emax
+
+
+def trace_inconsistency(E) -> float:
+    """|P_G(tr E)|: the gradient component along the gauge directions G (reading T).
+    Stationarity in G⊥ needs tr E_l equal across axes for a single modality."""
+    tr = np.array([float(np.sum(e)) for e in E])
+    return float(np.max(np.abs(tr - tr.mean())) / max(abs(tr.mean()), 1e-300))
+
+
+def _gauge_projector(ks):
+    """Orthogonal projector onto G⊥, G = span{(c_l 1_{k_l})_l : Σ c_l = 0} (reading G)."""
+    L = len(ks)
+    n = int(sum(ks))
+    if L == 1:
+        return np.eye(n)
+    cols = []
+    off = np.cumsum([0] + list(ks))
+    for l in range(L - 1):
+        c = np.zeros(n)
+        c[off[l]:off[l + 1]] = 1.0
+        c[off[L - 1]:off[L]] = -1.0
+        cols.append(c)
+    B = np.stack(cols, axis=1)
+    Q, _ = np.linalg.qr(B)
+    return np.eye(n) - Q @ Q.T
+
+
+def _split(vec, ks):
+    off = np.cumsum([0] + list(ks))
+    return [vec[off[i]:off[i + 1]].copy() for i in range(len(ks))]
+
+
+def canonical_gauge(lams):
+    """Gauge 0 (reading G): λ_l ← λ_l − min λ_l + s_min / L, s_min = Σ_l min λ_l.
+    Leaves every grid sum unchanged (shifts sum to 0) and makes each axis'
+    minimum equal, so Ψ_l = V diag(λ_l) V^T is PSD whenever s_min > 0."""
+    L = len(lams)
+    smin = sum(float(np.min(l)) for l in lams)
+    return [np.asarray(l, np.float64) - float(np.min(l)) + smin / L for l in lams]
+
+
+def identifiable(lams):
+    """Gauge-free coordinates (t, λ̃): t = Σ_l mean(λ_l), λ̃_l = λ_l − mean(λ_l)
+    (k-space form of the Greenewald reparameterization; reading G)."""
+    t = sum(float(np.mean(l)) for l in lams)
+    return t, [np.asarray(l, np.float64) - float(np.mean(l)) for l in lams]
+
+
+def solve_eigvals(E, tol: float = 1e-12, max_iter: int = 200, gauge: int = 0):
+    """Eigenvalue MLE: the minimizer of the convex NLL (Lemma 4, existence
+    Lemma 6, uniqueness up to gauge Thm 4).
+
+    The MLE has a plain definition (argmin of NLL), so the oracle computes that
+    definition: projected Newton on G⊥ (Hessian from the 1/s^2 marginals, a library
+    least-squares solve as the primitive), backtracking on NLL with grid feasibility.
+    Start at λ = 1/E (Alg. 1 line 5).  Returns (lams, info dict).
+    gauge 0 → canonical_gauge; gauge 1 → the iterate as reached from 1/E.
+    """
+    E = [np.asarray(e, np.float64) for e in E]
+    ks = [len(e) for e in E]
+    if any(np.any(~np.isfinite(e)) or np.any(e <= 0) for e in E):
+        raise ValueError("E must be finite and > 0 (Thm 4 hypothesis, P:742)")
+    lam = np.concatenate([1.0 / e for e in E])
+    P = _gauge_projector(ks)
+    off = np.cumsum([0] + ks)
+    evec = np.concatenate(E)
+    f = nll(E, _split(lam, ks))
+    it = 0
+    res = stationarity(E, _split(lam, ks))
+    while res > tol and it < max_iter:
+        lams = _split(lam, ks)
+        grad = np.concatenate(gradient(E, lams))
+        diag, pair = marginals_sq2d(lams)
+        n = len(lam)
+        H = np.zeros((n, n))
+        for a in range(len(ks)):
+            H[off[a]:off[a + 1], off[a]:off[a + 1]] = np.diag(0.5 * diag[a])
+        for (a, b), m in pair.items():
+            H[off[a]:off[a + 1], off[b]:off[b + 1]] = 0.5 * m
+            H[off[b]:off[b + 1], off[a]:off[a + 1]] = 0.5 * m.T
+        Hp = P @ H @ P
+        step = -np.linalg.lstsq(Hp, P @ grad, rcond=None)[0]
+        step = P @ step
+        alpha = 1.0
+        while True:
+            cand = lam + alpha * step
+            fc = nll(E, _split(cand, ks))
+            if np.isfinite(fc) and fc <= f + 1e-4 * alpha * float(grad @ step):
+                break
+            alpha *= 0.5
+            if alpha < 1e-12:
+                cand = lam
+                fc = f
+                break
+        if np.array_equal(cand, lam):
+            break
+        lam, f = cand, fc
+        it += 1
+        res = stationarity(E, _split(lam, ks))
+    lams = _split(lam, ks)
+    if gauge == 0:
+        lams = canonical_gauge(lams)
+    info = dict(iterations=it, stationarity=stationarity(E, lams), nll=nll(E, lams),
+                grid_min=float(grid_sums(lams).min()),
+                trace_inconsistency=trace_inconsistency(E))
+    return lams, info
+
+
+def paper_gd_solve(E, max_iter: int = 200000, tol: float = 1e-9, eps_scale: float = 1e-10):
+    """Algorithm 1 step by step, in its order and notation, for tiny problems.
+
+    Λ ← 1/E (line 5); μ ← 1 (line 6); while not converged (line 7; Q4 criterion):
+      Λ' ← Λ − μ·½(E − g(Λ))   (lines 8-9, reading Q1: the printed update omits Λ − μ·)
+      while Σ_l min Λ'_l < ε  (lines 11-12, reading Q3: grid-minimum feasibility) or the
+      NLL does not decrease (reading Q2): μ ← μ/2, recompute Λ' (lines 13-14)
+      Λ ← Λ' (lines 16-17).
+    """
+    E = [np.asarray(e, np.float64) for e in E]
+    lams = [1.0 / e for e in E]
+    eps = eps_scale * max(float(np.max(1.0 / e)) for e in E)
+    mu = 1.0
+    f = nll(E, lams)
+    it = 0
+    while stationarity(E, lams) > tol and it < max_iter:
+        grad = gradient(E, lams)
+        while True:
+            cand = [l - mu * g for l, g in zip(lams, grad)]
+            smin = sum(float(np.min(c)) for c in cand)
+            if smin >= eps:
+                fc = nll(E, cand)
+                if fc <= f:
+                    break
+            mu *= 0.5
+            if mu < 1e-300:
+                return lams, dict(iterations=it, stationarity=stationarity(E, lams))
+        lams, f = cand, fc
+        it += 1
+    return lams, dict(iterations=it, stationarity=stationarity(E, lams))
+
+
+# ---------------------------------------------------------------------------
+# Brute-force dense algebra (pins only): Kronecker sum, sb-trace, dense NLL
+# ---------------------------------------------------------------------------
+
+def kron_sum(mats) -> np.ndarray:
+    """⊕_l Ψ_l = Σ_l I_{d_<l} ⊗ Ψ_l ⊗ I_{d_>l}  (definition)."""
+    ds = [m.shape[0] for m in mats]
+    total = int(np.prod(ds))
+    out = np.zeros((total, total))
+    for l, m in enumerate(mats):
+        a = int(np.prod(ds[:l])) if l else 1
+        b = int(np.prod(ds[l + 1:])) if l + 1 < len(ds) else 1
+        out += np.kron(np.kron(np.eye(a), m), np.eye(b))
+    return out
+
+
+def sb_trace(M: np.ndarray, a: int, b: int, d: int) -> np.ndarray:
+    """Stridewise-blockwise trace: tr^a_b[M]_{ij} = tr[M (I_a ⊗ J^{ij} ⊗ I_b)]."""
+    out = np.zeros((d, d))
+    for i in range(d):
+        for j in range(d):
+            J = np.zeros((d, d))
+            J[i, j] = 1.0
+            out[i, j] = np.trace(M @ np.kron(np.kron(np.eye(a), J), np.eye(b)))
+    return out
+
+
+def dense_nll(S_list, psis, rtol: float = 1e-10) -> float:
+    """Matrix-form NLL ½ Σ tr[S_l Ψ_l] − ½ logdet†(⊕Ψ) (constants dropped)."""
+    om = kron_sum(psis)
+    ev = np.linalg.eigvalsh(om)
+    keep = np.abs(ev) > rtol * np.max(np.abs(ev))
+    return 0.5 * sum(float(np.trace(S @ P)) for S, P in zip(S_list, psis)) \
+        - 0.5 * float(np.log(ev[keep]).sum())
+
+
+# ---------------------------------------------------------------------------
+# Recomposition + sparsification — Alg. 1 lines 18-20
+# ---------------------------------------------------------------------------
+
+def psi_rows(V: np.ndarray, lam: np.ndarray, rows) -> np.ndarray:
+    """Rows of Ψ = V diag(λ) V^T (Cor. of Thm 2), fp64: ψ_i· = (V_i ⊙ λ) V^T."""
+    V = np.asarray(V, np.float64)
+    lam = np.asarray(lam, np.float64)
+    rows = np.asarray(rows, dtype=np.int64)
+    return (V[rows] * lam) @ V.T
+
+
+def top_t_row(psi_row: np.ndarray, i: int, t: int):
+    """Per-vertex top-t (reading Q8/Q9): the t_eff = min(t, n−1) entries j ≠ i with the
+    largest |ψ_ij|, ties → smaller j; returned in ascending-j order (cols, vals)."""
+    n = psi_row.shape[0]
+    te = min(t, n - 1)
+    a = np.abs(psi_row).astype(np.float64)
+    a[i] = -np.inf
+    if te <= 0:
+        return np.zeros(0, np.int64), np.zeros(0)
+    thr = np.partition(a, n - te)[n - te]          # te-th largest magnitude
+    cand = np.nonzero(a >= thr)[0]                 # every entry tied at the boundary too
+    order = np.lexsort((cand, -a[cand]))[:te]      # rank by (−|ψ|, j)
+    sel = np.sort(cand[order])
+    return sel.astype(np.int64), psi_row[sel].astype(np.float64)
+
+
+def threshold_row(psi_row: np.ndarray, i: int, tau: float):
+    """Mode 1: all j ≠ i with |ψ_ij| > τ, ascending j (reading Q15)."""
+    a = np.abs(psi_row)
+    a[i] = -np.inf
+    sel = np.nonzero(a > tau)[0]
+    return sel.astype(np.int64), psi_row[sel].astype(np.float64)
+
+
+def sparse_precision(V, lam, row_begin: int, row_end: int, mode: int = 0, t: int = 10,
+                     tau: float = 0.0, rows=None, block: int = 256):
+    """thresh_{n_l}[V Λ V^T] for rows [row_begin,row_end) (or an explicit ``rows`` list)
+    against all n columns; directed per-row CSR (row_ptr, col, val), ascending columns."""
+    if rows is None:
+        rows = np.arange(row_begin, row_end, dtype=np.int64)
+    rows = np.asarray(rows, np.int64)
+    cols, vals, ptr = [], [], [0]
+    for b0 in range(0, len(rows), block):
+        rb = rows[b0:b0 + block]
+        P = psi_rows(V, lam, rb)
+        for r, i in enumerate(rb):
+            if mode == 0:
+                c, v = top_t_row(P[r], int(i), t)
+            else:
+                c, v = threshold_row(P[r], int(i), tau)
+            cols.append(c)
+            vals.append(v)
+            ptr.append(ptr[-1] + len(c))
+    col = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+    val = np.concatenate(vals) if vals else np.zeros(0)
+    return np.asarray(ptr, np.int64), col, val
