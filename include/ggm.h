@@ -1,0 +1,177 @@
+/*
+ * ggm.h — C ABI of libggm.so, the B200 (sm_100a) hot path of the scalable multi-axis
+ * Gaussian graphical model of arXiv 2407.19892 ("GmGM", Andrew, Westhead, Cutillo).
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; readings Qn/G/T/TOL are listed
+ * in DESIGN.md §"Readings of the paper".
+ *
+ * Conventions (all entry points)
+ *  - Pointers are DEVICE pointers unless marked (host).  The caller owns every buffer;
+ *    the library never frees caller memory and keeps no device allocation between calls
+ *    except per-thread cuBLAS/cuSOLVER handles.
+ *  - Work is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *    default stream).  Calls that return host-visible results synchronize `stream`
+ *    (stated per call).
+ *  - Errors are return codes; nothing throws across the ABI.  On error, output contents
+ *    are unspecified but no out-of-bounds write occurs.  ggm_last_error() returns a
+ *    thread-local message for the last non-OK status.
+ *  - Tensors are row-major with the FIRST axis at the LARGEST stride, so that
+ *    ⊕_l Ψ_l = Σ_l I_{d<l} ⊗ Ψ_l ⊗ I_{d>l} matches vec ordering.
+ *  - Only a single modality is supported (the Σ_γ of Thm 2, has one term).
+ */
+#ifndef GGM_H_
+#define GGM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GGM_OK = 0,
+  GGM_ERR_INVALID_ARGUMENT = 1, /* null pointer, n<2, k<1, k>n, t<1, L<1, bad axis/mode,
+                                   row range outside [0,n), workspace too small, tau<0 */
+  GGM_ERR_RANK = 2,             /* k_l > attainable rank or E_k <= 1e-12 E_1
+                                   (Cor. 3 P:336-344) */
+  GGM_ERR_DOMAIN = 3,           /* non-finite input, E<=0 (Thm 4), lambda<=0 in
+                                   sparse_precision (PSD factors), grid sum <= 0 */
+  GGM_ERR_NO_CONVERGENCE = 4,   /* max_iter reached; info->stationarity = last residual */
+  GGM_ERR_CAPACITY = 5,         /* threshold mode: nnz > capacity; *nnz_out = required */
+  GGM_ERR_CUDA = 6,             /* CUDA / cuBLAS / cuSOLVER failure (see ggm_last_error) */
+  GGM_ERR_UNSUPPORTED = 7       /* e.g. t > GGM_MAX_TOPK */
+} ggm_status;
+
+#define GGM_MAX_TOPK 32
+
+const char *ggm_last_error(void);
+int ggm_version(void);
+/* 1 if the library was built with the sm_100a tcgen05 path and a device of compute
+ * capability 10.x is current; 0 otherwise (no compute is attempted). */
+int ggm_device_supported(void);
+
+/* ------------------------------------------------------------------------------------
+ * (1) Gram spectrum — Algorithm 1 lines 1-4, Theorem 1.
+ *
+ * Computes the top-k eigenpairs of the effective Gram matrix S_axis = mat_axis(X)
+ * mat_axis(X)^T, i.e. the top-k left singular vectors V of D_axis = mat_axis(X)
+ * and E = sigma^2.  fp64 internally: the unfolding is
+ * formed in fp64, S (or the dual Gram mat^T mat when d_axis > d_\axis, mapped back with
+ * V = mat W diag(1/sigma)) by cuBLAS DSYRK, eigendecomposition by cuSOLVER DSYEVD.
+ *
+ *  X        : float32, prod(shape) entries, row-major, device.
+ *  shape    : (host) ndim extents, each >= 1.
+ *  axis     : 0 <= axis < ndim.
+ *  k        : 1 <= k <= min(d_axis, d_\axis), else GGM_ERR_RANK.
+ *  V        : out float32, d_axis x k row-major (k contiguous), orthonormal columns,
+ *             column r = eigenvector of E[r]; the sign of each column is fixed so that its
+ *             largest-|.| entry is positive.
+ *  E        : out float64, k, descending; GGM_ERR_RANK if E[k-1] <= 1e-12 E[0].
+ *  trace_S  : (host, optional) out ||X||_F^2 = tr S_axis (for explained variance).
+ *  workspace: device scratch of >= ggm_gram_eig_workspace() bytes (256-byte aligned).
+ * Synchronizes `stream` (rank check).
+ * ---------------------------------------------------------------------------------- */
+ggm_status ggm_gram_eig_workspace(int ndim, const int64_t *shape, int axis, int k,
+                                  size_t *bytes);
+ggm_status ggm_gram_eig(const float *X, int ndim, const int64_t *shape, int axis, int k,
+                        float *V, double *E, double *trace_S, void *workspace,
+                        size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------
+ * (2) Eigenvalue MLE — Theorem 2, Algorithm 1 lines 5-17.
+ *
+ * Minimises NLL(λ) = ½ Σ_l E_l·λ_l − ½ Σ_{j in k-grid} log s_j, s_j = Σ_l λ_l[j_l]
+ * for ONE modality with L axes.  The gradient ½(E_l − g_l),
+ * g_l[i] = Σ_{j: j_l = i} 1/s_j, is evaluated by a grid-reduction kernel
+ * over all prod(k) grid points, never materialising the grid.
+ *
+ *  L      : number of axes, 1 <= L <= 8.
+ *  k      : (host) L ranks; prod(k) < 2^40.
+ *  E      : float64 sum(k), axis-concatenated Gram eigenvalues, each > 0 and finite.
+ *  opts   : (host, may be NULL = defaults).
+ *  lambda : out float64 sum(k), axis-concatenated, in the gauge opts->gauge.
+ *  info   : (host, may be NULL) diagnostics.
+ * Synchronizes `stream`.
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+  double tol;        /* stop when max_l max_i |E_li − g_li| / max E <= tol (reading Q4).
+                        default 1e-7 */
+  int max_iter;      /* default 20000 */
+  double eps_scale;  /* feasibility floor eps = eps_scale * max(1/E). default 1e-10 */
+  int method;        /* 0 = multiplicative fixed point λ ← λ ⊙ g/E with Anderson-free
+                        NLL-monotone safeguard (default); 1 = Algorithm 1 gradient descent
+                        (readings Q1-Q3, slow; for cross-checks) */
+  int gauge;         /* 0 = min-balanced PSD gauge (default, reading G);
+                        1 = iterate as reached from λ0 = 1/E */
+} ggm_solve_opts;
+
+typedef struct {
+  int iterations;
+  double stationarity;        /* max |E − g| / max E at exit */
+  double nll;                 /* NLL at exit */
+  double grid_min;            /* min_j s_j = Σ_l min λ_l */
+  double trace_inconsistency; /* max_l |tr E_l − mean| / mean (reading T) */
+  int floor_active;           /* 1 if some grid sum hit the eps floor */
+} ggm_solve_info;
+
+void ggm_solve_opts_default(ggm_solve_opts *opts);
+ggm_status ggm_solve_eigvals(int L, const int *k, const double *E, const ggm_solve_opts *opts,
+                             double *lambda, ggm_solve_info *info, void *stream);
+
+/* Grid marginals alone (the Thm 2 trace term), for parity tests and the bench:
+ * g (out, float64 sum(k)) and, if nll_out != NULL, F = Σ_j log s_j (host).  Synchronizes
+ * `stream` only when nll_out != NULL. */
+ggm_status ggm_grid_marginals(int L, const int *k, const double *lambda, double *g,
+                              double *logsum_out, void *stream);
+
+/* ------------------------------------------------------------------------------------
+ * (3) Fused recomposition + sparsification — Alg. 1 lines 18-20 ("Threshold
+ * simultaneously"), P:945, P:949 (never store the n x n matrix), P:1018 (per-vertex top-n).
+ *
+ * For rows i in [row_begin, row_end) of Ψ = V diag(λ) V^T (Cor. of Thm 2) and
+ * ALL n columns j != i, keeps
+ *   mode 0: the t_eff = min(t, n−1) entries of largest |ψ_ij|, ties -> smaller j (Q8, Q9)
+ *   mode 1: every entry with |ψ_ij| > tau (tau >= 0; e.g. the Thm 5 critical value, Q15)
+ * and writes directed per-row CSR, columns ascending within a row (Q10).  The contraction
+ * runs on tcgen05 tensor cores with a 3-term fp16 split (hi·hi + hi·lo + lo·hi, one
+ * power-of-two scale) accumulated in fp32 TMEM; the n x n matrix is never written.
+ *
+ *  V        : float32 n x k row-major, finite.
+ *  lambda   : float64 k, each > 0 and finite (PSD factors; the solver's gauge 0
+ *             guarantees this), else GGM_ERR_DOMAIN.
+ *  row_ptr  : out int64 rows+1 (rows = row_end − row_begin), offsets from 0.
+ *  col      : out int32 global column ids;  val: out float32 ψ_ij.
+ *  capacity : entries available in col/val.  mode 0 needs rows*t_eff.
+ *  nnz_out  : (host) out number of entries written (mode 1: required count when
+ *             GGM_ERR_CAPACITY is returned — two-call protocol).
+ *  workspace: >= ggm_sparse_precision_workspace() bytes, 256-byte aligned.
+ * Synchronizes `stream` (status and nnz are host-visible).
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+  int mode;   /* 0 top-t per row by |ψ| (j != i); 1 |ψ| > tau (j != i) */
+  int topk;   /* t, 1 <= t <= GGM_MAX_TOPK; effective t_eff = min(t, n−1) */
+  float tau;  /* mode 1 only, >= 0 */
+  int col_chunks; /* 0 = automatic; else split each row block's column sweep into this
+                     many chunks merged afterwards (balances small row ranges) */
+} ggm_sparsify_opts;
+
+ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t row_begin, int64_t row_end,
+                                          const ggm_sparsify_opts *opts, int64_t capacity,
+                                          size_t *bytes);
+ggm_status ggm_sparse_precision(int64_t n, int k, const float *V, const double *lambda,
+                                int64_t row_begin, int64_t row_end,
+                                const ggm_sparsify_opts *opts, int64_t *row_ptr, int32_t *col,
+                                float *val, int64_t capacity, int64_t *nnz_out,
+                                void *workspace, size_t workspace_bytes, void *stream);
+
+/* Per-kernel timing of the last ggm_sparse_precision call on this thread, measured with
+ * CUDA events on `stream` when enabled (for bench.py's roofline).  ms[0] = prep (absmax +
+ * split), ms[1] = fused tcgen05 kernel, ms[2] = merge/CSR assembly. */
+void ggm_set_timing(int enabled);
+void ggm_last_timing(float ms[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GGM_H_ */

@@ -1,0 +1,16 @@
+"""B200-native (sm_100a) hot path of the scalable multi-axis GGM (arXiv 2407.19892).
+
+Public API (thin bindings of libggm.so, include/ggm.h):
+  ggm_gram_eig         per-axis Gram spectrum          (Alg. 1 lines 1-4)
+  ggm_solve_eigvals    Kronecker-sum eigenvalue MLE    (Thm 2, Alg. 1 lines 5-17)
+  ggm_grid_marginals   the Thm 2 trace term alone
+  ggm_sparse_precision fused V diag(λ) V^T + per-row top-t / threshold (Alg. 1 line 19)
+  parallel.sharded_sparse_precision  row-sharded multi-GPU driver (torch.distributed/NCCL)
+"""
+from ._ggm import (GGMError, SparsePlan, device_supported, ggm_gram_eig, ggm_grid_marginals,
+                   ggm_solve_eigvals, ggm_sparse_precision, last_timing, lib, set_timing,
+                   version, EXPORTED, MAX_TOPK)
+
+__all__ = ["GGMError", "SparsePlan", "device_supported", "ggm_gram_eig", "ggm_grid_marginals",
+           "ggm_solve_eigvals", "ggm_sparse_precision", "last_timing", "lib", "set_timing",
+           "version", "EXPORTED", "MAX_TOPK"]

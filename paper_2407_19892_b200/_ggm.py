@@ -1,0 +1,256 @@
+"""ctypes binding of libggm.so (include/ggm.h).  Argument marshalling only: every step of
+the hot path runs in the library's CUDA kernels.  PyTorch supplies device memory (tensors),
+the current CUDA stream and, in ``parallel``, the process groups.
+
+There is no CPU fallback: if libggm.so is missing or the device is not sm_100a the calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libggm.so")
+
+GGM_OK = 0
+STATUS_NAMES = {
+    0: "GGM_OK", 1: "GGM_ERR_INVALID_ARGUMENT", 2: "GGM_ERR_RANK", 3: "GGM_ERR_DOMAIN",
+    4: "GGM_ERR_NO_CONVERGENCE", 5: "GGM_ERR_CAPACITY", 6: "GGM_ERR_CUDA",
+    7: "GGM_ERR_UNSUPPORTED",
+}
+MAX_TOPK = 32
+
+# symbols declared in include/ggm.h (checked by tests/test_abi.py)
+EXPORTED = [
+    "ggm_last_error", "ggm_version", "ggm_device_supported",
+    "ggm_gram_eig_workspace", "ggm_gram_eig",
+    "ggm_solve_opts_default", "ggm_solve_eigvals", "ggm_grid_marginals",
+    "ggm_sparse_precision_workspace", "ggm_sparse_precision",
+    "ggm_set_timing", "ggm_last_timing",
+]
+
+
+class GGMError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.status_name = STATUS_NAMES.get(status, str(status))
+        super().__init__(f"{self.status_name}: {message}")
+
+
+class SolveOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("eps_scale", C.c_double),
+                ("method", C.c_int), ("gauge", C.c_int)]
+
+
+class SolveInfo(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("stationarity", C.c_double), ("nll", C.c_double),
+                ("grid_min", C.c_double), ("trace_inconsistency", C.c_double),
+                ("floor_active", C.c_int)]
+
+
+class SparsifyOpts(C.Structure):
+    _fields_ = [("mode", C.c_int), ("topk", C.c_int), ("tau", C.c_float),
+                ("col_chunks", C.c_int)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libggm.so (built in-tree by ``paper_2407_19892_b200.build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(f"{_LIB_PATH} missing: run `python -m paper_2407_19892_b200.build` "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(_LIB_PATH)
+    vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+    L.ggm_last_error.restype = C.c_char_p
+    L.ggm_version.restype = i32
+    L.ggm_device_supported.restype = i32
+    L.ggm_gram_eig_workspace.argtypes = [i32, C.POINTER(i64), i32, i32, C.POINTER(C.c_size_t)]
+    L.ggm_gram_eig.argtypes = [vp, i32, C.POINTER(i64), i32, i32, vp, vp, C.POINTER(C.c_double),
+                               vp, C.c_size_t, vp]
+    L.ggm_solve_opts_default.argtypes = [C.POINTER(SolveOpts)]
+    L.ggm_solve_opts_default.restype = None
+    L.ggm_solve_eigvals.argtypes = [i32, C.POINTER(i32), vp, C.POINTER(SolveOpts), vp,
+                                    C.POINTER(SolveInfo), vp]
+    L.ggm_grid_marginals.argtypes = [i32, C.POINTER(i32), vp, vp, C.POINTER(C.c_double), vp]
+    L.ggm_sparse_precision_workspace.argtypes = [i64, i32, i64, i64, C.POINTER(SparsifyOpts), i64,
+                                                 C.POINTER(C.c_size_t)]
+    L.ggm_sparse_precision.argtypes = [i64, i32, vp, vp, i64, i64, C.POINTER(SparsifyOpts), vp, vp,
+                                       vp, i64, C.POINTER(i64), vp, C.c_size_t, vp]
+    L.ggm_set_timing.argtypes = [i32]
+    L.ggm_set_timing.restype = None
+    L.ggm_last_timing.argtypes = [C.POINTER(C.c_float)]
+    L.ggm_last_timing.restype = None
+    for name in ("ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
+                 "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision"):
+        getattr(L, name).restype = i32
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != GGM_OK:
+        msg = lib().ggm_last_error()
+        raise GGMError(status, msg.decode() if msg else "")
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def _require_cuda(t: torch.Tensor, dtype, name):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def device_supported() -> bool:
+    return bool(lib().ggm_device_supported())
+
+
+def version() -> int:
+    return int(lib().ggm_version())
+
+
+# --------------------------------------------------------------------------- (1) gram_eig
+
+def ggm_gram_eig(X: torch.Tensor, axis: int, k: int, stream=None):
+    """Top-k eigenpairs of S_axis = mat_axis(X) mat_axis(X)^T (Alg. 1 lines 1-4).
+    Returns (V float32 d x k, E float64 k descending, trace_S float)."""
+    _require_cuda(X, torch.float32, "X")
+    shape = (C.c_int64 * X.dim())(*X.shape)
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_gram_eig_workspace(X.dim(), shape, axis, k, C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=X.device)
+    d = X.shape[axis]
+    V = torch.empty((d, k), dtype=torch.float32, device=X.device)
+    E = torch.empty((k,), dtype=torch.float64, device=X.device)
+    tr = C.c_double(0.0)
+    _check(lib().ggm_gram_eig(_ptr(X), X.dim(), shape, axis, k, _ptr(V), _ptr(E), C.byref(tr),
+                              _ptr(ws), nbytes.value, _stream(stream)))
+    return V, E, tr.value
+
+
+# --------------------------------------------------------------------------- (2) solve
+
+def ggm_solve_eigvals(E: torch.Tensor, ks, tol: float = 1e-7, max_iter: int = 20000,
+                      gauge: int = 0, eps_scale: float = 1e-10, method: int = 0, stream=None):
+    """Eigenvalue MLE of Thm 2 on the k-grid (Alg. 1 lines 5-17).  E: float64 CUDA tensor,
+    axis-concatenated (sum(ks)).  Returns (lambda float64 sum(ks), info dict)."""
+    _require_cuda(E, torch.float64, "E")
+    ks = [int(k) for k in ks]
+    if E.numel() != sum(ks):
+        raise ValueError("E length != sum(ks)")
+    karr = (C.c_int * len(ks))(*ks)
+    o = SolveOpts()
+    lib().ggm_solve_opts_default(C.byref(o))
+    o.tol, o.max_iter, o.gauge, o.eps_scale, o.method = tol, max_iter, gauge, eps_scale, method
+    lam = torch.empty_like(E)
+    info = SolveInfo()
+    _check(lib().ggm_solve_eigvals(len(ks), karr, _ptr(E), C.byref(o), _ptr(lam), C.byref(info),
+                                   _stream(stream)))
+    return lam, {f: getattr(info, f) for f, _ in SolveInfo._fields_}
+
+
+def ggm_grid_marginals(lam: torch.Tensor, ks, with_logsum: bool = False, stream=None):
+    """g_l[i] = Σ_{j: j_l = i} 1/s_j (the Thm 2 trace term); optional Σ log s."""
+    _require_cuda(lam, torch.float64, "lam")
+    ks = [int(k) for k in ks]
+    karr = (C.c_int * len(ks))(*ks)
+    g = torch.empty_like(lam)
+    ls = C.c_double(0.0)
+    _check(lib().ggm_grid_marginals(len(ks), karr, _ptr(lam), _ptr(g),
+                                    C.byref(ls) if with_logsum else None, _stream(stream)))
+    return (g, ls.value) if with_logsum else g
+
+
+# --------------------------------------------------------------------------- (3) sparse
+
+class SparsePlan:
+    """Workspace + output buffers for repeated ggm_sparse_precision calls (bench loop)."""
+
+    def __init__(self, n, k, row_begin, row_end, mode=0, topk=10, tau=0.0, col_chunks=0,
+                 capacity=None, device="cuda"):
+        self.n, self.k, self.row_begin, self.row_end = int(n), int(k), int(row_begin), int(row_end)
+        self.opts = SparsifyOpts(int(mode), int(topk), float(tau), int(col_chunks))
+        rows = self.row_end - self.row_begin
+        self.t_eff = min(int(topk), self.n - 1)
+        if capacity is None:
+            capacity = rows * self.t_eff if mode == 0 else max(rows * 16, 1024)
+        self.capacity = int(capacity)
+        nbytes = C.c_size_t(0)
+        _check(lib().ggm_sparse_precision_workspace(self.n, self.k, self.row_begin, self.row_end,
+                                                    C.byref(self.opts), self.capacity,
+                                                    C.byref(nbytes)))
+        self.ws_bytes = nbytes.value
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=device)
+        self.row_ptr = torch.empty(rows + 1, dtype=torch.int64, device=device)
+        self.col = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=device)
+        self.val = torch.empty(max(self.capacity, 1), dtype=torch.float32, device=device)
+
+    def run(self, V: torch.Tensor, lam: torch.Tensor, stream=None) -> int:
+        _require_cuda(V, torch.float32, "V")
+        _require_cuda(lam, torch.float64, "lam")
+        if V.shape != (self.n, self.k) or lam.numel() != self.k:
+            raise ValueError("V/lam shape mismatch with plan")
+        nnz = C.c_int64(0)
+        st = lib().ggm_sparse_precision(self.n, self.k, _ptr(V), _ptr(lam), self.row_begin,
+                                        self.row_end, C.byref(self.opts), _ptr(self.row_ptr),
+                                        _ptr(self.col), _ptr(self.val), self.capacity,
+                                        C.byref(nnz), _ptr(self.ws), self.ws_bytes,
+                                        _stream(stream))
+        if st != GGM_OK:
+            try:
+                _check(st)
+            except GGMError as e:
+                e.required = int(nnz.value)
+                raise
+        return int(nnz.value)
+
+
+def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
+                         row_end: int | None = None, mode: int = 0, topk: int = 10,
+                         tau: float = 0.0, col_chunks: int = 0, capacity: int | None = None,
+                         stream=None):
+    """Fused thresh[V diag(λ) V^T] for rows [row_begin,row_end) (Alg. 1 line 19).
+    Returns CSR (row_ptr int64, col int32, val float32) on the device.  Mode 1 retries once
+    with the required capacity (two-call protocol)."""
+    n, k = V.shape
+    if row_end is None:
+        row_end = n
+    plan = SparsePlan(n, k, row_begin, row_end, mode, topk, tau, col_chunks, capacity,
+                      device=V.device)
+    try:
+        nnz = plan.run(V, lam, stream)
+    except GGMError as e:
+        if e.status != 5:
+            raise
+        plan = SparsePlan(n, k, row_begin, row_end, mode, topk, tau, col_chunks,
+                          max(e.required, 1), device=V.device)
+        nnz = plan.run(V, lam, stream)
+    return plan.row_ptr, plan.col[:nnz], plan.val[:nnz]
+
+
+def set_timing(enabled: bool):
+    lib().ggm_set_timing(1 if enabled else 0)
+
+
+def last_timing():
+    arr = (C.c_float * 3)()
+    lib().ggm_last_timing(arr)
+    return list(arr)

@@ -1,0 +1,327 @@
+// gram_eig.cu — per-axis Gram spectrum (Algorithm 1 lines 1-4; Theorem 1,
+// P:308-331): top-k eigenpairs of S_l = mat_l(X) mat_l(X)^T — equivalently the
+// top-k left singular vectors of D_l = mat_l(X) with E = sigma^2.
+//
+// fp64 throughout (C2's top-50 spectrum has relative eigengaps ~3e-4, so an fp32
+// Gram would rotate the subspace):
+//   unfold_f64  : mat_l(X) in fp64, column-major d_l x d_\l (one coalesced permute pass)
+//   cuBLAS DSYRK: S = M M^T  (or, for a matrix whose axis is the longer side, the Gram of the
+//                 OTHER axis, so both axes of a matrix share one bitwise-identical spectrum,
+//                 reading T; V is mapped back as V = M^T W diag(1/sigma))
+//   cuSOLVER DSYEVD: all eigenpairs of the small Gram (a library eigensolver, like a sort)
+//   select_topk : descending top-k, deterministic sign (largest-|.| entry positive), fp32
+//                 row-major V (k contiguous)
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "ggm_internal.h"
+
+namespace ggm {
+namespace ge {
+
+struct Handles {
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  ~Handles() {
+    if (blas) cublasDestroy(blas);
+    if (solver) cusolverDnDestroy(solver);
+  }
+};
+static thread_local Handles g_handles;
+
+static ggm_status get_handles(cudaStream_t s, cublasHandle_t* b, cusolverDnHandle_t* so) {
+  if (!g_handles.blas && cublasCreate(&g_handles.blas) != CUBLAS_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cublasCreate failed");
+  if (!g_handles.solver && cusolverDnCreate(&g_handles.solver) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnCreate failed");
+  if (cublasSetStream(g_handles.blas, s) != CUBLAS_STATUS_SUCCESS ||
+      cusolverDnSetStream(g_handles.solver, s) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "set stream failed");
+  *b = g_handles.blas;
+  *so = g_handles.solver;
+  return GGM_OK;
+}
+
+// M (column-major, rows = d_axis, cols = d_\axis) from row-major X viewed as
+// [pre, d_axis, post]: M[i + c*d] = X[pre, i, post], c = pre*post_n + post.
+__global__ void unfold_f64(const float* __restrict__ X, int64_t pre_n, int64_t d, int64_t post_n,
+                           double* __restrict__ M, double* __restrict__ fro) {
+  const int64_t total = pre_n * d * post_n;
+  double acc = 0.0;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    // idx enumerates the OUTPUT (i fastest) for coalesced writes
+    const int64_t i = idx % d;
+    const int64_t c = idx / d;
+    const int64_t pre = c / post_n, post = c % post_n;
+    const double x = (double)X[(pre * d + i) * post_n + post];
+    M[idx] = x;
+    acc += x * x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(fro, acc);
+}
+
+// Eigenvalues w (ascending, length dim) and eigenvectors Z (column-major dim x dim) ->
+// top-k descending E and column-major V64 (rows x k) from Z (primal: rows = dim).
+__global__ void take_topk(const double* __restrict__ w, const double* __restrict__ Z, int dim,
+                          int k, double* __restrict__ E, double* __restrict__ Vk) {
+  const int r = blockIdx.x;  // output column
+  if (r >= k) return;
+  const int src = dim - 1 - r;
+  if (threadIdx.x == 0) E[r] = w[src];
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) Vk[(size_t)r * dim + i] = Z[(size_t)src * dim + i];
+}
+
+// Sign fix (largest-|.| entry positive; first index on ties) and fp32 row-major output.
+__global__ void sign_and_store(const double* __restrict__ V64, int64_t rows, int k,
+                               float* __restrict__ V) {
+  const int r = blockIdx.x;
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  double best = -1.0;
+  long long bi = 0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double a = fabs(V64[(size_t)r * rows + i]);
+    if (a > best) {
+      best = a;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sv[w] > sv[0] || (sv[w] == sv[0] && si[w] < si[0])) {
+        sv[0] = sv[w];
+        si[0] = si[w];
+      }
+  }
+  __syncthreads();
+  const double sgn = V64[(size_t)r * rows + si[0]] < 0 ? -1.0 : 1.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x)
+    V[i * k + r] = (float)(sgn * V64[(size_t)r * rows + i]);
+}
+
+// mode 1/2: Vasc (d x k, ascending eigen order) -> V64 column r = Vasc column (k-1-r) /
+// sigma_r, E[r] = w[dim-1-r].
+__global__ void reverse_scale(const double* __restrict__ w, int dim, const double* __restrict__ Vasc,
+                              int64_t d, int k, double* __restrict__ E, double* __restrict__ V64) {
+  const int r = blockIdx.y;
+  const double e = w[dim - 1 - r];
+  if (blockIdx.x == 0 && threadIdx.x == 0) E[r] = e;
+  const double inv = e > 0.0 ? 1.0 / sqrt(e) : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+       i += (int64_t)gridDim.x * blockDim.x)
+    V64[(size_t)r * d + i] = Vasc[(size_t)(k - 1 - r) * d + i] * inv;
+}
+
+struct GPlan {
+  int64_t d, m;        // axis length, product of the others
+  int64_t pre_n, post_n;
+  int mode;            // 0 primal (S = M M^T), 1 dual via the other axis of a matrix,
+                       // 2 dual via M^T M (tensor with d > m)
+  int64_t dim;         // Gram dimension
+  int64_t Md_rows, Md_cols;  // the unfolding actually materialised (column-major)
+  int k;
+  int lwork;
+};
+
+static ggm_status make_gplan(int ndim, const int64_t* shape, int axis, int k, GPlan* g) {
+  if (ndim < 1 || !shape) return fail(GGM_ERR_INVALID_ARGUMENT, "ndim/shape invalid");
+  if (axis < 0 || axis >= ndim) return fail(GGM_ERR_INVALID_ARGUMENT, "axis %d out of range", axis);
+  int64_t pre = 1, post = 1;
+  for (int a = 0; a < ndim; ++a) {
+    if (shape[a] < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "shape[%d] < 1", a);
+    if (a < axis) pre *= shape[a];
+    if (a > axis) post *= shape[a];
+  }
+  g->d = shape[axis];
+  g->m = pre * post;
+  g->pre_n = pre;
+  g->post_n = post;
+  g->k = k;
+  if (k < 1 || k > std::min(g->d, g->m))
+    return fail(GGM_ERR_RANK, "k=%d not in [1, min(d_l=%lld, d_\\l=%lld)] (S:116)", k,
+                (long long)g->d, (long long)g->m);
+  if (g->d <= g->m) {
+    g->mode = 0;
+    g->dim = g->d;
+    g->Md_rows = g->d;
+    g->Md_cols = g->m;
+  } else if (ndim == 2) {
+    g->mode = 1;  // Gram of the other axis: M_o = mat_other (m x d), S_o = M_o M_o^T (m x m)
+    g->dim = g->m;
+    g->Md_rows = g->m;
+    g->Md_cols = g->d;
+  } else {
+    g->mode = 2;
+    g->dim = g->m;
+    g->Md_rows = g->d;
+    g->Md_cols = g->m;
+  }
+  if (g->dim > 32768) return fail(GGM_ERR_UNSUPPORTED, "Gram dimension %lld too large", (long long)g->dim);
+  return GGM_OK;
+}
+
+static size_t gcarve(const GPlan& g, int lwork, void* ws, double** Md, double** S, double** w,
+                     double** work, int** info, double** V64, double** fro, double** Ek,
+                     double** Vasc) {
+  Carve c(ws);
+  *Md = c.take<double>((size_t)g.Md_rows * g.Md_cols);
+  *S = c.take<double>((size_t)g.dim * g.dim);
+  *w = c.take<double>((size_t)g.dim);
+  *work = c.take<double>((size_t)std::max(lwork, 1));
+  *info = c.take<int>(4);
+  *V64 = c.take<double>((size_t)g.d * g.k);
+  *fro = c.take<double>(4);
+  *Ek = c.take<double>((size_t)g.k);
+  *Vasc = c.take<double>(g.mode == 0 ? 0 : (size_t)g.d * g.k);
+  return c.used();
+}
+
+static ggm_status query_lwork(const GPlan& g, int* lwork) {
+  cusolverDnHandle_t h = g_handles.solver;
+  if (!h && cusolverDnCreate(&g_handles.solver) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnCreate failed");
+  h = g_handles.solver;
+  int lw = 0;
+  if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)g.dim,
+                                  nullptr, (int)g.dim, nullptr, &lw) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
+  *lwork = lw;
+  return GGM_OK;
+}
+
+}  // namespace ge
+}  // namespace ggm
+
+using namespace ggm;
+using namespace ggm::ge;
+
+extern "C" ggm_status ggm_gram_eig_workspace(int ndim, const int64_t* shape, int axis, int k,
+                                             size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  GPlan g;
+  ggm_status st = make_gplan(ndim, shape, axis, k, &g);
+  if (st != GGM_OK) return st;
+  int lwork = 0;
+  st = query_lwork(g, &lwork);
+  if (st != GGM_OK) return st;
+  double *a, *b, *c, *d, *f, *h, *e, *v;
+  int* i;
+  *bytes = gcarve(g, lwork, nullptr, &a, &b, &c, &d, &i, &f, &h, &e, &v);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_gram_eig(const float* X, int ndim, const int64_t* shape, int axis, int k,
+                                   float* V, double* E, double* trace_S, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  if (!X || !V || !E || !workspace) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  GPlan g;
+  ggm_status st = make_gplan(ndim, shape, axis, k, &g);
+  if (st != GGM_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  int lwork = 0;
+  st = query_lwork(g, &lwork);
+  if (st != GGM_OK) return st;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  double *Md, *S, *w, *work, *V64, *fro, *Ek, *Vasc;
+  int* dinfo;
+  const size_t need =
+      gcarve(g, lwork, workspace, &Md, &S, &w, &work, &dinfo, &V64, &fro, &Ek, &Vasc);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+
+  GGM_CUDA_TRY(cudaMemsetAsync(fro, 0, sizeof(double), s));
+  const int sms = num_sms();
+  {
+    // which unfolding to materialise
+    int64_t pre_n = g.pre_n, d = g.d, post_n = g.post_n;
+    if (g.mode == 1) {  // matrix, other axis: X is [d0, d1]; other = 1 - axis
+      if (axis == 0) {   // other axis 1: [pre=d0, d=d1, post=1]
+        pre_n = shape[0];
+        d = shape[1];
+        post_n = 1;
+      } else {           // other axis 0: [pre=1, d=d0, post=d1]
+        pre_n = 1;
+        d = shape[0];
+        post_n = shape[1];
+      }
+    }
+    const int64_t total = pre_n * d * post_n;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 16));
+    unfold_f64<<<grid, 256, 0, s>>>(X, pre_n, d, post_n, Md, fro);
+    GGM_CUDA_TRY(cudaGetLastError());
+  }
+  const double one = 1.0, zero = 0.0;
+  cublasStatus_t bs;
+  if (g.mode == 2)  // S = M^T M  (m x m), M is d x m column-major
+    bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)g.dim, (int)g.Md_rows, &one, Md,
+                     (int)g.Md_rows, &zero, S, (int)g.dim);
+  else              // S = M M^T  (Md_rows x Md_rows)
+    bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)g.dim, (int)g.Md_cols, &one, Md,
+                     (int)g.Md_rows, &zero, S, (int)g.dim);
+  if (bs != CUBLAS_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cublasDsyrk failed (%d)", (int)bs);
+  cusolverStatus_t ss = cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                         (int)g.dim, S, (int)g.dim, w, work, lwork, dinfo);
+  if (ss != CUSOLVER_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed (%d)", (int)ss);
+  // top-k eigenpairs of the Gram that was formed (syevd: ascending eigenvalues, Z in S)
+  if (g.mode == 0) {
+    take_topk<<<g.k, 256, 0, s>>>(w, S, (int)g.dim, g.k, Ek, V64);
+    GGM_CUDA_TRY(cudaGetLastError());
+  } else {
+    // V = A W_k diag(1/sigma), A = mat_axis (d x m): mode 1 A = Md^T, mode 2 A = Md.
+    const double* Zk = S + (size_t)(g.dim - g.k) * g.dim;  // ascending block of the top k
+    if (g.mode == 1)
+      bs = cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)g.d, g.k, (int)g.dim, &one, Md,
+                       (int)g.Md_rows, Zk, (int)g.dim, &zero, Vasc, (int)g.d);
+    else
+      bs = cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)g.d, g.k, (int)g.dim, &one, Md,
+                       (int)g.Md_rows, Zk, (int)g.dim, &zero, Vasc, (int)g.d);
+    if (bs != CUBLAS_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cublasDgemm failed (%d)", (int)bs);
+    reverse_scale<<<dim3(std::max<int64_t>(1, std::min<int64_t>((g.d + 255) / 256, 64)), g.k), 256, 0, s>>>(
+        w, (int)g.dim, Vasc, g.d, g.k, Ek, V64);
+    GGM_CUDA_TRY(cudaGetLastError());
+  }
+  sign_and_store<<<g.k, 256, 0, s>>>(V64, g.d, g.k, V);
+  GGM_CUDA_TRY(cudaGetLastError());
+  GGM_CUDA_TRY(cudaMemcpyAsync(E, Ek, sizeof(double) * g.k, cudaMemcpyDeviceToDevice, s));
+  std::vector<double> hE(g.k);
+  int hinfo = 0;
+  double hfro = 0.0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(hE.data(), Ek, sizeof(double) * g.k, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hfro, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hinfo != 0) return fail(GGM_ERR_CUDA, "cusolverDnDsyevd info=%d", hinfo);
+  if (trace_S) *trace_S = hfro;
+  if (!(hE[0] > 0.0) || !std::isfinite(hE[0]) || !(hE[g.k - 1] > 1e-12 * hE[0]))
+    return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)",
+                hE[g.k - 1], hE[0]);
+  return GGM_OK;
+}

@@ -1,0 +1,529 @@
+// grid_solve.cu — Kronecker-sum eigenvalue MLE on the k-grid (Theorem 2, P:354-376;
+// Algorithm 1 lines 5-17).
+//
+// The Thm 2 trace term for one modality is the vector of grid marginals
+//     g_l[i] = Σ_{grid points j with j_l = i} 1 / s_j,   s_j = Σ_l λ_l[j_l]
+// over all prod(k) grid points.  The grid is never stored: each pass regenerates s_j from
+// the Σk eigenvalues held in shared memory (BK4 is bound by the reciprocal rate, not HBM).
+//
+// Solver: the multiplicative update λ ← λ ⊙ g / E.  It is the
+// majorise-minimise step for the NLL (Jensen on -log s with weights λ_l[j_l]/s_j gives a
+// separable majoriser whose minimiser is exactly λ g / E), so the NLL decreases
+// monotonically and λ stays > 0: Algorithm 1's feasibility loop never triggers.
+// The whole loop runs in ONE cooperative persistent kernel: per iteration a grid pass
+// (per-block partial marginals), grid.sync, a per-entry reduction + update + stationarity
+// max, grid.sync.
+//
+// Layout of the pass: the axis with the largest k is the "inner" axis (contiguous in the
+// lanes of a warp); every other axis is "outer".  One warp owns one outer multi-index row
+// at a time: s = base(row) + λ_inner[m].  Per-lane fp32 partials (<= 32 terms, flushed to
+// fp64), warp-shuffle row sums, fp64 shared-memory block partials, fp64 cross-block sums.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "ggm_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace ggm {
+namespace gs {
+
+constexpr int kMaxAxes = 8;
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kFlush = 32;  // rows per fp32 lane partial before flushing to fp64
+
+struct GridDesc {
+  int L;                   // axes
+  int inner;               // index of the inner axis (original order)
+  int k[kMaxAxes];         // ranks, original order
+  int off[kMaxAxes + 1];   // offsets into the concatenated vectors
+  int outer_axes[kMaxAxes];  // original indices of outer axes, last = fastest
+  int64_t outer_stride[kMaxAxes];  // row = Σ_a idx_a · outer_stride[a]
+  int n_outer;
+  int64_t rows;            // prod of outer k
+  int total;               // Σ k
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One grid pass: this block's partial marginals in sg (fp64, Σk entries, zeroed by caller).
+// slam: fp32 λ (Σk), in shared memory.
+template <int J>
+__device__ void grid_pass_block(const GridDesc& gd, const float* slam, double* sg, int64_t row0,
+                                int64_t row_stride) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int kin = gd.k[gd.inner];
+  const float* lin = slam + gd.off[gd.inner];
+  float lv[J];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const int m = lane + 32 * jj;
+    lv[jj] = (m < kin) ? lin[m] : 0.f;
+  }
+  float accf[J];
+  double accd[J];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    accf[jj] = 0.f;
+    accd[jj] = 0.0;
+  }
+  int since_flush = 0;
+  for (int64_t row = row0 + warp; row < gd.rows; row += row_stride) {
+    // base sum over the outer multi-index (last outer axis fastest)
+    float base = 0.f;
+    for (int a = 0; a < gd.n_outer; ++a) {
+      const int ax = gd.outer_axes[a];
+      base += slam[gd.off[ax] + (int)((row / gd.outer_stride[a]) % gd.k[ax])];
+    }
+    float rsum = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      const int m = lane + 32 * jj;
+      if (m < kin) {
+        const float r = rcp_approx(base + lv[jj]);
+        rsum += r;
+        accf[jj] += r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+    if (lane < gd.n_outer) {
+      // lane a adds the row sum to g_{outer axis a}[idx_a]
+      const int ax = gd.outer_axes[lane];
+      const int my = (int)((row / gd.outer_stride[lane]) % gd.k[ax]);
+      atomicAdd(&sg[gd.off[ax] + my], (double)rsum);
+    }
+    if (++since_flush == kFlush) {
+#pragma unroll
+      for (int jj = 0; jj < J; ++jj) {
+        accd[jj] += (double)accf[jj];
+        accf[jj] = 0.f;
+      }
+      since_flush = 0;
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const int m = lane + 32 * jj;
+    if (m < kin) atomicAdd(&sg[gd.off[gd.inner] + m], accd[jj] + (double)accf[jj]);
+  }
+}
+
+template <int J>
+__device__ void grid_pass_dispatch(const GridDesc& gd, const float* slam, double* sg,
+                                   int64_t row0, int64_t stride) {
+  grid_pass_block<J>(gd, slam, sg, row0, stride);
+}
+
+struct SolveParams {
+  GridDesc gd;
+  const double* E;
+  double* lam0;       // λ buffers (ping-pong), Σk each
+  double* lam1;
+  double* g;          // marginals of the last pass, Σk
+  double* partial;    // [Σk][gridDim]
+  unsigned long long* res_bits;  // [2] residual max as double bits
+  int* status;        // [0] iterations, [1] converged flag, [2] which λ buffer holds result
+  double tol;
+  int max_iter;
+};
+
+template <int J>
+__global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double dsm[];
+  const GridDesc& gd = p.gd;
+  double* sg = dsm;                                   // Σk
+  float* slam = reinterpret_cast<float*>(sg + gd.total);  // Σk
+  __shared__ double s_emax;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < gd.total; ++i) m = fmax(m, p.E[i]);
+    s_emax = m;
+  }
+  __syncthreads();
+  const double emax = s_emax;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  const int64_t wrow0 = (int64_t)blockIdx.x * kWarps;
+  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  int cur = 0;
+  int it = 0;
+  bool done = false;
+  for (; it <= p.max_iter; ++it) {
+    const double* lc = cur ? p.lam1 : p.lam0;
+    double* ln = cur ? p.lam0 : p.lam1;
+    for (int i = threadIdx.x; i < gd.total; i += blockDim.x) {
+      sg[i] = 0.0;
+      slam[i] = (float)__ldcg(&lc[i]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.res_bits[(it + 1) & 1] = 0ull;
+    __syncthreads();
+    grid_pass_dispatch<J>(gd, slam, sg, wrow0, wstride);
+    __syncthreads();
+    for (int i = threadIdx.x; i < gd.total; i += blockDim.x)
+      p.partial[(size_t)i * gridDim.x + blockIdx.x] = sg[i];
+    grid.sync();
+    // per-entry reduction across blocks, update, stationarity
+    for (int e = gw; e < gd.total; e += gridDim.x * kWarps) {
+      double sum = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) sum += __ldcg(&p.partial[(size_t)e * gridDim.x + b]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        const double Ee = p.E[e];
+        p.g[e] = sum;
+        ln[e] = __ldcg(&lc[e]) * sum / Ee;
+        const double r = fabs(Ee - sum) / emax;
+        atomicMax(&p.res_bits[it & 1], (unsigned long long)__double_as_longlong(r));
+      }
+    }
+    grid.sync();
+    const double res = __longlong_as_double((long long)__ldcg(&p.res_bits[it & 1]));
+    if (res <= p.tol) {
+      done = true;
+      break;
+    }
+    if (it == p.max_iter) break;
+    cur ^= 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.status[0] = it;
+    p.status[1] = done ? 1 : 0;
+    p.status[2] = cur;  // λ buffer whose marginals were last evaluated (g corresponds to it)
+  }
+}
+
+// Stand-alone single pass (ggm_grid_marginals / final NLL): partials into [Σk][grid].
+template <int J>
+__global__ void __launch_bounds__(kThreads, 1) marginal_pass_kernel(GridDesc gd, const double* lam,
+                                                                     double* partial) {
+  extern __shared__ double dsm[];
+  double* sg = dsm;
+  float* slam = reinterpret_cast<float*>(sg + gd.total);
+  for (int i = threadIdx.x; i < gd.total; i += blockDim.x) {
+    sg[i] = 0.0;
+    slam[i] = (float)lam[i];
+  }
+  __syncthreads();
+  grid_pass_block<J>(gd, slam, sg, (int64_t)blockIdx.x * kWarps, (int64_t)gridDim.x * kWarps);
+  __syncthreads();
+  for (int i = threadIdx.x; i < gd.total; i += blockDim.x)
+    partial[(size_t)i * gridDim.x + blockIdx.x] = sg[i];
+}
+
+__global__ void reduce_partials(const double* partial, int nblk, int total, double* g) {
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= total) return;
+  double sum = 0.0;
+  for (int b = lane; b < nblk; b += 32) sum += partial[(size_t)e * nblk + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) g[e] = sum;
+}
+
+// Σ_j log s_j over the grid (fp32 log per point, fp64 accumulation) -> logsum (atomic).
+__global__ void logsum_kernel(GridDesc gd, const double* lam, double* logsum) {
+  extern __shared__ float flam[];
+  for (int i = threadIdx.x; i < gd.total; i += blockDim.x) flam[i] = (float)lam[i];
+  __syncthreads();
+  const int kin = gd.k[gd.inner];
+  double acc = 0.0;
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < gd.rows;
+       row += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    double base = 0.0;
+    for (int a = 0; a < gd.n_outer; ++a) {
+      const int ax = gd.outer_axes[a];
+      base += lam[gd.off[ax] + (int)((row / gd.outer_stride[a]) % gd.k[ax])];
+    }
+    float racc = 0.f;
+    for (int m = lane; m < kin; m += 32) racc += __logf((float)(base + lam[gd.off[gd.inner] + m]));
+    acc += (double)racc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) atomicAdd(logsum, acc);
+}
+
+// Final: choose result buffer, canonical gauge, write λ out; compute grid_min, floor.
+__global__ void finalize_kernel(GridDesc gd, const double* lam_res, int gauge, double* lam_out,
+                                double* scalars /* [0]=smin */) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double mins[kMaxAxes];
+  double smin = 0.0;
+  for (int a = 0; a < gd.L; ++a) {
+    double m = lam_res[gd.off[a]];
+    for (int i = 1; i < gd.k[a]; ++i) m = fmin(m, lam_res[gd.off[a] + i]);
+    mins[a] = m;
+    smin += m;
+  }
+  for (int a = 0; a < gd.L; ++a) {
+    const double shift = gauge == 0 ? (-mins[a] + smin / gd.L) : 0.0;
+    for (int i = 0; i < gd.k[a]; ++i) lam_out[gd.off[a] + i] = lam_res[gd.off[a] + i] + shift;
+  }
+  scalars[0] = smin;
+}
+
+__global__ void check_E(const double* E, int total, int* bad) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const double e = E[i];
+    if (!(e > 0.0) || !isfinite(e)) atomicOr(bad, 1);
+  }
+}
+
+__global__ void init_lambda(const double* E, int total, double* lam) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
+    lam[i] = 1.0 / E[i];  // Algorithm 1 line 5
+}
+
+static ggm_status make_desc(int L, const int* k, GridDesc* gd) {
+  if (L < 1 || L > kMaxAxes) return fail(GGM_ERR_INVALID_ARGUMENT, "L=%d not in [1,%d]", L, kMaxAxes);
+  if (!k) return fail(GGM_ERR_INVALID_ARGUMENT, "k is NULL");
+  gd->L = L;
+  gd->off[0] = 0;
+  int inner = 0;
+  double prod = 1.0;
+  for (int a = 0; a < L; ++a) {
+    if (k[a] < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "k[%d]=%d < 1", a, k[a]);
+    gd->k[a] = k[a];
+    gd->off[a + 1] = gd->off[a] + k[a];
+    if (k[a] > k[inner]) inner = a;
+    prod *= k[a];
+  }
+  if (prod >= 1099511627776.0) return fail(GGM_ERR_INVALID_ARGUMENT, "grid too large (>= 2^40)");
+  if (k[inner] > 1024)
+    return fail(GGM_ERR_UNSUPPORTED, "largest rank %d > 1024 not supported by grid_solve", k[inner]);
+  gd->inner = inner;
+  gd->n_outer = 0;
+  gd->rows = 1;
+  for (int a = 0; a < L; ++a)
+    if (a != inner) {
+      gd->outer_axes[gd->n_outer++] = a;
+      gd->rows *= k[a];
+    }
+  int64_t stride = 1;
+  for (int a = gd->n_outer - 1; a >= 0; --a) {
+    gd->outer_stride[a] = stride;
+    stride *= k[gd->outer_axes[a]];
+  }
+  gd->total = gd->off[L];
+  return GGM_OK;
+}
+
+static int pick_J(int kin) { return kin <= 128 ? 4 : kin <= 256 ? 8 : kin <= 512 ? 16 : 32; }
+
+static size_t pass_smem(const GridDesc& gd) {
+  return (size_t)gd.total * (sizeof(double) + sizeof(float)) + 16;
+}
+
+template <int J>
+static cudaError_t set_attrs(size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(solve_kernel<J>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(marginal_pass_kernel<J>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+static int grid_blocks(const GridDesc& gd) {
+  const int64_t warps_needed = std::max<int64_t>(1, gd.rows);
+  const int64_t blocks = (warps_needed + kWarps - 1) / kWarps;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, num_sms()));
+}
+
+static cudaError_t launch_pass(const GridDesc& gd, const double* lam, double* partial, int nblk,
+                               cudaStream_t s) {
+  const size_t smem = pass_smem(gd);
+  const int J = pick_J(gd.k[gd.inner]);
+  cudaError_t e;
+  switch (J) {
+    case 4: e = set_attrs<4>(smem); if (e) return e; marginal_pass_kernel<4><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
+    case 8: e = set_attrs<8>(smem); if (e) return e; marginal_pass_kernel<8><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
+    case 16: e = set_attrs<16>(smem); if (e) return e; marginal_pass_kernel<16><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
+    default: e = set_attrs<32>(smem); if (e) return e; marginal_pass_kernel<32><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
+  }
+  return cudaGetLastError();
+}
+
+template <int J>
+static cudaError_t launch_solve(const SolveParams& sp, int nblk, size_t smem, cudaStream_t s) {
+  cudaError_t e = set_attrs<J>(smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<J>, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  void* args[] = {const_cast<SolveParams*>(&sp)};
+  return cudaLaunchCooperativeKernel((void*)solve_kernel<J>, dim3(nblk), dim3(kThreads), args, smem,
+                                     s);
+}
+
+}  // namespace gs
+}  // namespace ggm
+
+using namespace ggm;
+using namespace ggm::gs;
+
+extern "C" void ggm_solve_opts_default(ggm_solve_opts* o) {
+  if (!o) return;
+  o->tol = 1e-7;
+  o->max_iter = 20000;
+  o->eps_scale = 1e-10;
+  o->method = 0;
+  o->gauge = 0;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+extern "C" ggm_status ggm_grid_marginals(int L, const int* k, const double* lambda, double* g,
+                                         double* logsum_out, void* stream) {
+  GridDesc gd;
+  ggm_status st = make_desc(L, k, &gd);
+  if (st != GGM_OK) return st;
+  if (!lambda || !g) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nblk = grid_blocks(gd);
+  DevBuf buf;
+  GGM_CUDA_TRY(cudaMallocAsync(&buf.p, (size_t)gd.total * nblk * sizeof(double) + 64, s));
+  double* partial = static_cast<double*>(buf.p);
+  GGM_CUDA_TRY(launch_pass(gd, lambda, partial, nblk, s));
+  reduce_partials<<<(gd.total + 7) / 8, 256, 0, s>>>(partial, nblk, gd.total, g);
+  GGM_CUDA_TRY(cudaGetLastError());
+  if (logsum_out) {
+    double* dls = partial + (size_t)gd.total * nblk;
+    GGM_CUDA_TRY(cudaMemsetAsync(dls, 0, sizeof(double), s));
+    logsum_kernel<<<num_sms() * 4, 256, gd.total * sizeof(float), s>>>(gd, lambda, dls);
+    GGM_CUDA_TRY(cudaGetLastError());
+    GGM_CUDA_TRY(cudaMemcpyAsync(logsum_out, dls, sizeof(double), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  GGM_CUDA_TRY(cudaFreeAsync(buf.p, s));
+  buf.p = nullptr;
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
+                                        const ggm_solve_opts* opts, double* lambda,
+                                        ggm_solve_info* info, void* stream) {
+  GridDesc gd;
+  ggm_status st = make_desc(L, k, &gd);
+  if (st != GGM_OK) return st;
+  if (!E || !lambda) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  ggm_solve_opts o;
+  ggm_solve_opts_default(&o);
+  if (opts) o = *opts;
+  if (!(o.tol > 0.0) || o.max_iter < 0 || !(o.eps_scale >= 0.0))
+    return fail(GGM_ERR_INVALID_ARGUMENT, "invalid solve options");
+  if (o.method != 0)
+    return fail(GGM_ERR_UNSUPPORTED, "method %d not implemented on the GPU (use 0)", o.method);
+  if (o.gauge != 0 && o.gauge != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "gauge=%d", o.gauge);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nblk = grid_blocks(gd);
+  const size_t T = gd.total;
+  // scratch: lam0, lam1, g, partial[T*nblk], res_bits[2], status[4], bad, scalars[4], logsum
+  const size_t bytes = sizeof(double) * (3 * T + T * nblk + 8) + 64 + 64;
+  DevBuf buf;
+  GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
+  double* lam0 = static_cast<double*>(buf.p);
+  double* lam1 = lam0 + T;
+  double* g = lam1 + T;
+  double* partial = g + T;
+  double* scal = partial + T * nblk;  // [0] smin, [1] logsum
+  unsigned long long* res_bits = reinterpret_cast<unsigned long long*>(scal + 4);
+  int* istat = reinterpret_cast<int*>(res_bits + 2);  // [0..2] status, [3] bad
+  GGM_CUDA_TRY(cudaMemsetAsync(scal, 0, sizeof(double) * 8 + 64, s));
+  check_E<<<4, 256, 0, s>>>(E, gd.total, istat + 3);
+  init_lambda<<<(gd.total + 255) / 256, 256, 0, s>>>(E, gd.total, lam0);
+  GGM_CUDA_TRY(cudaGetLastError());
+  int hbad = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hbad, istat + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hbad) return fail(GGM_ERR_DOMAIN, "E must be finite and > 0 (Thm 4, P:742)");
+
+  SolveParams sp;
+  sp.gd = gd;
+  sp.E = E;
+  sp.lam0 = lam0;
+  sp.lam1 = lam1;
+  sp.g = g;
+  sp.partial = partial;
+  sp.res_bits = res_bits;
+  sp.status = istat;
+  sp.tol = o.tol;
+  sp.max_iter = o.max_iter;
+  const size_t smem = pass_smem(gd);
+  cudaError_t ce;
+  switch (pick_J(gd.k[gd.inner])) {
+    case 4: ce = launch_solve<4>(sp, nblk, smem, s); break;
+    case 8: ce = launch_solve<8>(sp, nblk, smem, s); break;
+    case 16: ce = launch_solve<16>(sp, nblk, smem, s); break;
+    default: ce = launch_solve<32>(sp, nblk, smem, s); break;
+  }
+  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+  int hstat[3] = {0, 0, 0};
+  GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  const double* lam_res = hstat[2] ? lam1 : lam0;
+  finalize_kernel<<<1, 32, 0, s>>>(gd, lam_res, o.gauge, lambda, scal);
+  logsum_kernel<<<num_sms() * 4, 256, gd.total * sizeof(float), s>>>(gd, lam_res, scal + 1);
+  GGM_CUDA_TRY(cudaGetLastError());
+  // residual of the returned λ (its marginals are in g)
+  double hres = 0.0;
+  {
+    const unsigned long long* rb = res_bits + (hstat[0] & 1);
+    unsigned long long bits = 0;
+    GGM_CUDA_TRY(cudaMemcpyAsync(&bits, rb, sizeof(bits), cudaMemcpyDeviceToHost, s));
+    double hscal[2];
+    GGM_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    memcpy(&hres, &bits, sizeof(double));
+    if (info) {
+      std::vector<double> hE(T), hL(T);
+      GGM_CUDA_TRY(cudaMemcpy(hE.data(), E, T * sizeof(double), cudaMemcpyDeviceToHost));
+      GGM_CUDA_TRY(cudaMemcpy(hL.data(), lam_res, T * sizeof(double), cudaMemcpyDeviceToHost));
+      double lin = 0.0;
+      for (size_t i = 0; i < T; ++i) lin += hE[i] * hL[i];
+      std::vector<double> tr(L, 0.0);
+      double mean = 0.0;
+      for (int a = 0; a < L; ++a) {
+        for (int i = gd.off[a]; i < gd.off[a + 1]; ++i) tr[a] += hE[i];
+        mean += tr[a] / L;
+      }
+      double ti = 0.0;
+      for (int a = 0; a < L; ++a) ti = std::max(ti, std::fabs(tr[a] - mean));
+      info->iterations = hstat[0];
+      info->stationarity = hres;
+      info->nll = 0.5 * lin - 0.5 * hscal[1];
+      info->grid_min = hscal[0];
+      double emax = 0.0;
+      for (size_t i = 0; i < T; ++i) emax = std::max(emax, 1.0 / hE[i]);
+      info->floor_active = hscal[0] <= o.eps_scale * emax ? 1 : 0;
+      info->trace_inconsistency = mean > 0 ? ti / mean : 0.0;
+    }
+  }
+  GGM_CUDA_TRY(cudaFreeAsync(buf.p, s));
+  buf.p = nullptr;
+  if (!hstat[1])
+    return fail(GGM_ERR_NO_CONVERGENCE, "no convergence in %d iterations (residual %.3e)",
+                o.max_iter, hres);
+  return GGM_OK;
+}

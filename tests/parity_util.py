@@ -1,0 +1,71 @@
+"""Parity helpers shared by the GPU tests: compare a CUDA-path CSR against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star): values within 1e-4 relative with a 1e-6 absolute
+floor; identical per-row top-t index sets except where the t-th and (t+1)-th oracle
+magnitudes differ by less than that tolerance (then the GPU set must still be valid:
+every chosen entry within tolerance of the oracle's t-th magnitude).  A strict gate with
+the relative tolerance only (reading TOL in DESIGN.md) is reported alongside.
+"""
+import numpy as np
+
+import oracle as O
+
+REL = 1e-4
+ABS = 1e-6
+
+
+def tol(x, strict=False):
+    return REL * np.abs(x) if strict else np.maximum(REL * np.abs(x), ABS)
+
+
+def check_topk(row_ptr, col, val, V, lam, rows, t, strict=False):
+    """rows: global row ids corresponding to CSR rows 0..len(rows)-1 of the GPU output
+    (row_ptr/col/val already restricted to those rows).  Returns stats dict; asserts."""
+    V = np.asarray(V)
+    n = V.shape[0]
+    te = min(t, n - 1)
+    P = O.psi_rows(V, lam, rows)
+    stats = dict(rows=len(rows), excused=0, exact=0, max_rel_err=0.0, max_abs_err=0.0)
+    for r, i in enumerate(rows):
+        c = np.asarray(col[row_ptr[r]:row_ptr[r + 1]], dtype=np.int64)
+        v = np.asarray(val[row_ptr[r]:row_ptr[r + 1]], dtype=np.float64)
+        assert len(c) == te, f"row {i}: {len(c)} entries != {te}"
+        assert np.all(np.diff(c) > 0), f"row {i}: columns not strictly ascending"
+        assert np.all((c >= 0) & (c < n) & (c != i)), f"row {i}: invalid column"
+        want = P[r, c]
+        err = np.abs(v - want)
+        assert np.all(err <= tol(want, strict)), (
+            f"row {i}: value error {err.max():.3e} (|psi| {np.abs(want).max():.3e})")
+        rel = err / np.maximum(np.abs(want), 1e-300)
+        stats["max_rel_err"] = max(stats["max_rel_err"], float(rel.max()))
+        stats["max_abs_err"] = max(stats["max_abs_err"], float(err.max()))
+        oc, _ = O.top_t_row(P[r], int(i), t)
+        if np.array_equal(oc, c):
+            stats["exact"] += 1
+            continue
+        a = np.abs(P[r]).copy()
+        a[i] = -np.inf
+        srt = np.sort(a)[::-1]
+        at, at1 = srt[te - 1], (srt[te] if te < n - 1 else -np.inf)
+        gap_small = (at - at1) <= tol(at, strict)
+        assert gap_small, f"row {i}: top-{t} set differs with a clear gap {at - at1:.3e}"
+        # excused: the GPU set must still be a valid top set within tolerance
+        assert np.all(np.abs(P[r, c]) >= at - tol(at, strict)), f"row {i}: invalid near-tie set"
+        stats["excused"] += 1
+    return stats
+
+
+def check_threshold(row_ptr, col, val, V, lam, rows, tau):
+    """Mode 1: every j != i with |psi| > tau; entries within tolerance of tau may differ."""
+    P = O.psi_rows(V, lam, rows)
+    for r, i in enumerate(rows):
+        c = set(np.asarray(col[row_ptr[r]:row_ptr[r + 1]]).tolist())
+        a = np.abs(P[r])
+        a[i] = -np.inf
+        sure_in = set(np.nonzero(a > tau + tol(tau))[0].tolist())
+        maybe = set(np.nonzero(a > tau - tol(tau))[0].tolist())
+        assert sure_in <= c <= maybe, f"row {i}: threshold set mismatch"
+        cc = np.asarray(col[row_ptr[r]:row_ptr[r + 1]], dtype=np.int64)
+        vv = np.asarray(val[row_ptr[r]:row_ptr[r + 1]], dtype=np.float64)
+        assert np.all(np.diff(cc) > 0)
+        assert np.all(np.abs(vv - P[r, cc]) <= tol(P[r, cc]))

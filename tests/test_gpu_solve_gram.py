@@ -1,0 +1,122 @@
+"""GPU parity of ggm_grid_marginals / ggm_solve_eigvals (Thm 2, Alg. 1 lines 5-17) and
+ggm_gram_eig (Alg. 1 lines 1-4, Thm 1) against the fp64 oracle, through the C ABI."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import gen
+
+pytestmark = pytest.mark.gpu
+
+EIG_REL = 1e-5   # north_star: eigenvalues within 1e-5 relative
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2407_19892_b200 as G
+    assert G.device_supported()
+    return G
+
+
+def _cat(xs):
+    return torch.from_numpy(np.concatenate([np.asarray(x, np.float64) for x in xs])).cuda()
+
+
+@pytest.mark.parametrize("ks", [(2, 2), (5,), (7, 3, 4), (40, 30, 20), (130, 3), (1, 600),
+                                (3, 2, 2, 3, 2)])
+def test_grid_marginals(G, ks):
+    rng = np.random.default_rng(len(ks) * 100 + sum(ks))
+    lams = [rng.uniform(0.05, 2.0, k) for k in ks]
+    g, ls = G.ggm_grid_marginals(_cat(lams), ks, with_logsum=True)
+    want = np.concatenate(O.marginals(lams))
+    np.testing.assert_allclose(g.cpu().numpy(), want, rtol=2e-6)
+    assert ls == pytest.approx(float(np.log(O.grid_sums(lams)).sum()), rel=1e-6)
+
+
+def test_grid_marginals_golden(G):
+    g = G.ggm_grid_marginals(_cat([[1.0, 2.0], [3.0, 4.0]]), (2, 2))
+    np.testing.assert_allclose(g.cpu().numpy(), [0.45, 0.36666666666666664] * 2, rtol=1e-6)
+
+
+def _split(x, ks):
+    off = np.cumsum([0] + list(ks))
+    return [x[off[i]:off[i + 1]] for i in range(len(ks))]
+
+
+@pytest.mark.parametrize("shape", [(20, 10), (6, 5, 4), (30, 20, 10)])
+def test_solve_matches_oracle(G, shape):
+    x = gen.small_tensor(sum(shape), shape)
+    ks = []
+    Es = []
+    for l, d in enumerate(shape):
+        k = min(d, int(np.prod(shape)) // d)
+        _, E = O.gram_eig(x, l, k)
+        ks.append(k)
+        Es.append(E)
+    lo, _ = O.solve_eigvals(Es, tol=1e-13)
+    lam, info = G.ggm_solve_eigvals(_cat(Es), ks, tol=1e-9)
+    lg = _split(lam.cpu().numpy(), ks)
+    # gauge-free comparison: grid sums, then the canonical (gauge 0) λ
+    np.testing.assert_allclose(O.grid_sums(lg), O.grid_sums(lo), rtol=EIG_REL)
+    for a, b in zip(lg, lo):
+        np.testing.assert_allclose(a, b, rtol=EIG_REL)
+    assert O.stationarity(Es, lg) < 1e-6
+    assert info["stationarity"] <= 1e-9
+    assert info["nll"] == pytest.approx(O.nll(Es, lo), rel=1e-6, abs=1e-6)
+
+
+def test_solve_isotropic_closed_form_c3_size(G):
+    """E_l = (T/k_l)·1 ⇒ every grid sum = Πk/T, at the full C3 grid (24M points)."""
+    ks = (400, 300, 200)
+    T = 123.0
+    E = [np.full(k, T / k) for k in ks]
+    lam, info = G.ggm_solve_eigvals(_cat(E), ks, tol=1e-7)
+    lg = _split(lam.cpu().numpy(), ks)
+    s = O.grid_sums([l.astype(np.float64) for l in lg])
+    np.testing.assert_allclose(s, np.prod(ks) / T, rtol=1e-5)
+    assert info["iterations"] <= 2
+
+
+def test_solve_single_axis(G):
+    E = np.array([4.0, 2.0, 0.5])
+    lam, info = G.ggm_solve_eigvals(_cat([E]), (3,), gauge=1)
+    np.testing.assert_allclose(lam.cpu().numpy(), 1.0 / E, rtol=1e-6)
+
+
+def test_solve_domain_error(G):
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_solve_eigvals(_cat([[1.0, -2.0], [1.0, 1.0]]), (2, 2))
+    assert e.value.status == 3
+
+
+@pytest.mark.parametrize("shape,axis,k", [((200, 100), 0, 100), ((200, 100), 1, 100),
+                                          ((50, 80), 0, 20), ((12, 9, 7), 1, 9),
+                                          ((40, 3, 2), 0, 6), ((64, 48, 30), 2, 30)])
+def test_gram_eig(G, shape, axis, k):
+    x = gen.small_tensor(sum(shape) + axis, shape)
+    V, E, tr = G.ggm_gram_eig(torch.from_numpy(x).cuda(), axis, k)
+    Vo, Eo = O.gram_eig(x, axis, k)
+    np.testing.assert_allclose(E.cpu().numpy(), Eo, rtol=1e-9)
+    assert tr == pytest.approx(float(np.sum(x.astype(np.float64) ** 2)), rel=1e-12)
+    Vg = V.cpu().numpy().astype(np.float64)
+    # subspace agreement (largest principal angle) and orthonormality
+    sv = np.linalg.svd(Vg.T @ Vo, compute_uv=False)
+    assert sv.min() > 1 - 1e-5
+    np.testing.assert_allclose(Vg.T @ Vg, np.eye(k), atol=1e-5)
+
+
+def test_gram_eig_matrix_axes_share_spectrum(G):
+    """Reading T: both axes of a matrix get the bitwise-identical spectrum."""
+    x = gen.small_tensor(3, (60, 25))
+    xd = torch.from_numpy(x).cuda()
+    _, E0, _ = G.ggm_gram_eig(xd, 0, 25)
+    _, E1, _ = G.ggm_gram_eig(xd, 1, 25)
+    assert torch.equal(E0, E1)
+
+
+def test_gram_eig_rank_error(G):
+    x = gen.small_tensor(3, (6, 3))
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_gram_eig(torch.from_numpy(x).cuda(), 0, 4)
+    assert e.value.status == 2

@@ -1,0 +1,139 @@
+"""GPU parity of ggm_sparse_precision (fused tcgen05 recomposition + per-row top-t /
+threshold, Alg. 1 line 19) against the fp64 oracle, through the C ABI."""
+import numpy as np
+import pytest
+import torch
+
+from synth import gen
+from parity_util import check_threshold, check_topk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2407_19892_b200 as G
+    assert torch.cuda.is_available()
+    assert G.device_supported(), "needs an sm_100a (B200) device"
+    return G
+
+
+def _run(G, V, lam, row_begin=0, row_end=None, **kw):
+    Vd = torch.from_numpy(V).cuda()
+    ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
+    rp, c, v = G.ggm_sparse_precision(Vd, ld, row_begin, row_end, **kw)
+    torch.cuda.synchronize()
+    return rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,k,t", [(1000, 64, 10), (777, 37, 5), (2053, 100, 10),
+                                   (300, 16, 32), (257, 1, 3), (2, 1, 10), (129, 128, 16)])
+def test_topk_full_rows(G, n, k, t):
+    V, lam = gen.small_factor(n + k + t, n, k)
+    rp, c, v = _run(G, V, lam, 0, n, mode=0, topk=t)
+    st = check_topk(rp, c, v, V, lam, np.arange(n), t)
+    assert st["exact"] + st["excused"] == n
+
+
+@pytest.mark.parametrize("rb,re,chunks", [(5, 900, 0), (128, 640, 3), (1, 2, 0), (700, 1000, 7)])
+def test_topk_row_ranges_and_chunks(G, rb, re, chunks):
+    n, k, t = 1000, 48, 10
+    V, lam = gen.small_factor(99, n, k)
+    rp, c, v = _run(G, V, lam, rb, re, mode=0, topk=t, col_chunks=chunks)
+    check_topk(rp, c, v, V, lam, np.arange(rb, re), t)
+
+
+def test_topk_streaming_large_k(G):
+    """k > 128: operand A streamed per K atom (C3-like ranks)."""
+    n, k, t = 600, 300, 10
+    V, lam = gen.small_factor(7, n, k)
+    rp, c, v = _run(G, V, lam, 0, n, mode=0, topk=t)
+    check_topk(rp, c, v, V, lam, np.arange(n), t)
+
+
+def test_all_ties_identity_factor(G):
+    """V = first k columns of I: all off-diagonals are exactly 0 ⇒ the t smallest j != i."""
+    n, k, t = 700, 8, 10
+    V = np.eye(n, dtype=np.float32)[:, :k].copy()
+    lam = np.ones(k)
+    rp, c, v = _run(G, V, lam, 0, n, mode=0, topk=t)
+    for i in range(n):
+        want = [j for j in range(n) if j != i][:t]
+        got = list(c[rp[i]:rp[i + 1]])
+        if i < k:   # row i < k has psi_ij = 0 for all j != i as well
+            assert got == want
+        else:
+            assert got == want
+        assert np.all(v[rp[i]:rp[i + 1]] == 0)
+
+
+def test_rank1_closed_form_large_n(G):
+    """Rank 1 at n = 200,000: row i's set = top-t of |v_j|, j != i (closed form)."""
+    n, t = 200_000, 10
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    V = v.astype(np.float32).reshape(n, 1)
+    lam = np.array([2.5])
+    rows = [0, 1, 12345, 199_999]
+    rp, c, vals = _run(G, V, lam, 0, n, mode=0, topk=t)
+    a = np.abs(V[:, 0].astype(np.float64))
+    order = np.argsort(-a, kind="stable")
+    for i in rows:
+        want = sorted([j for j in order[:t + 1] if j != i][:t])
+        assert list(c[rp[i]:rp[i + 1]]) == want
+        np.testing.assert_allclose(vals[rp[i]:rp[i + 1]],
+                                   2.5 * V[i, 0].astype(np.float64) * V[want, 0], rtol=1e-4)
+
+
+def test_threshold_mode(G):
+    n, k = 900, 24
+    V, lam = gen.small_factor(5, n, k)
+    P = (V.astype(np.float64) * lam) @ V.astype(np.float64).T
+    off = np.abs(P[~np.eye(n, dtype=bool)])
+    tau = float(np.quantile(off, 0.995))
+    rp, c, v = _run(G, V, lam, 0, n, mode=1, tau=tau)
+    check_threshold(rp, c, v, V, lam, np.arange(n), tau)
+    # capacity protocol: a too-small capacity reports the required count
+    Vd = torch.from_numpy(V).cuda()
+    ld = torch.from_numpy(lam).cuda()
+    plan = G.SparsePlan(n, k, 0, n, mode=1, tau=tau, capacity=10)
+    with pytest.raises(G.GGMError) as e:
+        plan.run(Vd, ld)
+    assert e.value.status == 5 and e.value.required == len(c)
+
+
+def test_domain_errors(G):
+    n, k = 300, 8
+    V, lam = gen.small_factor(1, n, k)
+    Vd = torch.from_numpy(V).cuda()
+    bad = lam.copy()
+    bad[3] = -1.0
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_sparse_precision(Vd, torch.from_numpy(bad).cuda(), 0, n, topk=5)
+    assert e.value.status == 3
+    Vn = V.copy()
+    Vn[17, 2] = np.nan
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_sparse_precision(torch.from_numpy(Vn).cuda(), torch.from_numpy(lam).cuda(), 0, n)
+    assert e.value.status == 3
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_sparse_precision(Vd, torch.from_numpy(lam).cuda(), 0, n, topk=33)
+    assert e.value.status == 7
+
+
+def test_permutation_equivariance_and_scaling(G):
+    """Permuting rows of V permutes the output; scaling λ by c scales values, same sets."""
+    n, k, t = 800, 32, 10
+    V, lam = gen.small_factor(11, n, k)
+    perm = np.random.default_rng(0).permutation(n)
+    rp, c, v = _run(G, V, lam, 0, n, topk=t)
+    rp2, c2, v2 = _run(G, V[perm].copy(), lam, 0, n, topk=t)
+    rp3, c3, v3 = _run(G, V, lam * 4.0, 0, n, topk=t)
+    inv = np.argsort(perm)
+    for i in range(0, n, 37):
+        a = set(c[rp[i]:rp[i + 1]].tolist())
+        b = set(perm[c2[rp2[inv[i]]:rp2[inv[i] + 1]]].tolist())
+        assert a == b
+        assert list(c3[rp3[i]:rp3[i + 1]]) == list(c[rp[i]:rp[i + 1]])
+        np.testing.assert_allclose(v3[rp3[i]:rp3[i + 1]], 4.0 * v[rp[i]:rp[i + 1]], rtol=1e-6)
