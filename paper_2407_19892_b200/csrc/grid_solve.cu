@@ -16,8 +16,9 @@
 //
 // Layout of the pass: the axis with the largest k is the "inner" axis (contiguous in the
 // lanes of a warp); every other axis is "outer".  One warp owns one outer multi-index row
-// at a time: s = base(row) + λ_inner[m].  Per-lane fp32 partials (<= 32 terms, flushed to
-// fp64), warp-shuffle row sums, fp64 shared-memory block partials, fp64 cross-block sums.
+// at a time: s = base(row) + λ_inner[m].  fp64 throughout: SFU-seeded fp64 reciprocals
+// (one Newton step), per-lane accumulators, warp-shuffle row sums, shared-memory block
+// partials and cross-block sums.  The pass is bound by the FP64 + SFU pipes, not HBM.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -37,7 +38,6 @@ namespace gs {
 constexpr int kMaxAxes = 8;
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kFlush = 32;  // rows per fp32 lane partial before flushing to fp64
 
 struct GridDesc {
   int L;                   // axes
@@ -51,50 +51,51 @@ struct GridDesc {
   int total;               // Σ k
 };
 
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // One grid pass: this block's partial marginals in sg (fp64, Σk entries, zeroed by caller).
 // slam: fp32 λ (Σk), in shared memory.
+// Reciprocal of a positive double: MUFU 64-bit approximation (~2^-20 relative, the SFU
+// pipe) refined by one Newton step on the FP64 pipe (error ~2^-40).
+__device__ __forceinline__ double rcp_f64(double s) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  const double e = fma(-s, r, 1.0);
+  return fma(r, e, r);
+}
+
+// One grid pass over this block's share of the outer rows: per-lane fp64 accumulators for
+// the inner axis, warp-shuffle row sums for the outer axes, fp64 shared-memory partials sg.
+// All of s, 1/s and the sums are fp64 (no fixed fp32 rounding of λ or s that would floor
+// the stationarity residual; e.g. the isotropic case, where every s_j is equal, would
+// otherwise carry one identical rounding error in every term).
 template <int J>
-__device__ void grid_pass_block(const GridDesc& gd, const float* slam, double* sg, int64_t row0,
+__device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* sg, int64_t row0,
                                 int64_t row_stride) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int kin = gd.k[gd.inner];
-  const float* lin = slam + gd.off[gd.inner];
-  float lv[J];
+  const int oin = gd.off[gd.inner];
+  double lv[J], acc[J];
 #pragma unroll
   for (int jj = 0; jj < J; ++jj) {
     const int m = lane + 32 * jj;
-    lv[jj] = (m < kin) ? lin[m] : 0.f;
+    lv[jj] = (m < kin) ? slam[oin + m] : 1.0;
+    acc[jj] = 0.0;
   }
-  float accf[J];
-  double accd[J];
-#pragma unroll
-  for (int jj = 0; jj < J; ++jj) {
-    accf[jj] = 0.f;
-    accd[jj] = 0.0;
-  }
-  int since_flush = 0;
   for (int64_t row = row0 + warp; row < gd.rows; row += row_stride) {
-    // base sum over the outer multi-index (last outer axis fastest)
-    float base = 0.f;
+    double base = 0.0;  // Σ over the outer multi-index (last outer axis fastest)
     for (int a = 0; a < gd.n_outer; ++a) {
       const int ax = gd.outer_axes[a];
       base += slam[gd.off[ax] + (int)((row / gd.outer_stride[a]) % gd.k[ax])];
     }
-    float rsum = 0.f;
+    double rsum = 0.0;
 #pragma unroll
     for (int jj = 0; jj < J; ++jj) {
       const int m = lane + 32 * jj;
       if (m < kin) {
-        const float r = rcp_approx(base + lv[jj]);
+        const double r = rcp_f64(base + lv[jj]);
         rsum += r;
-        accf[jj] += r;
+        acc[jj] += r;
       }
     }
 #pragma unroll
@@ -103,28 +104,20 @@ __device__ void grid_pass_block(const GridDesc& gd, const float* slam, double* s
       // lane a adds the row sum to g_{outer axis a}[idx_a]
       const int ax = gd.outer_axes[lane];
       const int my = (int)((row / gd.outer_stride[lane]) % gd.k[ax]);
-      atomicAdd(&sg[gd.off[ax] + my], (double)rsum);
-    }
-    if (++since_flush == kFlush) {
-#pragma unroll
-      for (int jj = 0; jj < J; ++jj) {
-        accd[jj] += (double)accf[jj];
-        accf[jj] = 0.f;
-      }
-      since_flush = 0;
+      atomicAdd(&sg[gd.off[ax] + my], rsum);
     }
   }
 #pragma unroll
   for (int jj = 0; jj < J; ++jj) {
     const int m = lane + 32 * jj;
-    if (m < kin) atomicAdd(&sg[gd.off[gd.inner] + m], accd[jj] + (double)accf[jj]);
+    if (m < kin) atomicAdd(&sg[oin + m], acc[jj]);
   }
 }
 
-template <int J>
-__device__ void grid_pass_dispatch(const GridDesc& gd, const float* slam, double* sg,
-                                   int64_t row0, int64_t stride) {
-  grid_pass_block<J>(gd, slam, sg, row0, stride);
+__device__ __forceinline__ void load_lambda(const double* lam, int total, double* slam,
+                                            bool bypass_l1) {
+  for (int i = threadIdx.x; i < total; i += blockDim.x)
+    slam[i] = bypass_l1 ? __ldcg(&lam[i]) : lam[i];
 }
 
 struct SolveParams {
@@ -145,8 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
   const GridDesc& gd = p.gd;
-  double* sg = dsm;                                   // Σk
-  float* slam = reinterpret_cast<float*>(sg + gd.total);  // Σk
+  double* sg = dsm;               // Σk
+  double* slam = sg + gd.total;   // Σk
   __shared__ double s_emax;
   if (threadIdx.x == 0) {
     double m = 0.0;
@@ -165,13 +158,11 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p)
   for (; it <= p.max_iter; ++it) {
     const double* lc = cur ? p.lam1 : p.lam0;
     double* ln = cur ? p.lam0 : p.lam1;
-    for (int i = threadIdx.x; i < gd.total; i += blockDim.x) {
-      sg[i] = 0.0;
-      slam[i] = (float)__ldcg(&lc[i]);
-    }
+    for (int i = threadIdx.x; i < gd.total; i += blockDim.x) sg[i] = 0.0;
+    load_lambda(lc, gd.total, slam, true);
     if (blockIdx.x == 0 && threadIdx.x == 0) p.res_bits[(it + 1) & 1] = 0ull;
     __syncthreads();
-    grid_pass_dispatch<J>(gd, slam, sg, wrow0, wstride);
+    grid_pass_block<J>(gd, slam, sg, wrow0, wstride);
     __syncthreads();
     for (int i = threadIdx.x; i < gd.total; i += blockDim.x)
       p.partial[(size_t)i * gridDim.x + blockIdx.x] = sg[i];
@@ -212,11 +203,9 @@ __global__ void __launch_bounds__(kThreads, 1) marginal_pass_kernel(GridDesc gd,
                                                                      double* partial) {
   extern __shared__ double dsm[];
   double* sg = dsm;
-  float* slam = reinterpret_cast<float*>(sg + gd.total);
-  for (int i = threadIdx.x; i < gd.total; i += blockDim.x) {
-    sg[i] = 0.0;
-    slam[i] = (float)lam[i];
-  }
+  double* slam = sg + gd.total;
+  for (int i = threadIdx.x; i < gd.total; i += blockDim.x) sg[i] = 0.0;
+  load_lambda(lam, gd.total, slam, false);
   __syncthreads();
   grid_pass_block<J>(gd, slam, sg, (int64_t)blockIdx.x * kWarps, (int64_t)gridDim.x * kWarps);
   __syncthreads();
@@ -235,11 +224,8 @@ __global__ void reduce_partials(const double* partial, int nblk, int total, doub
   if (lane == 0) g[e] = sum;
 }
 
-// Σ_j log s_j over the grid (fp32 log per point, fp64 accumulation) -> logsum (atomic).
+// Σ_j log s_j over the grid (fp64; a one-off diagnostic pass) -> logsum (atomic).
 __global__ void logsum_kernel(GridDesc gd, const double* lam, double* logsum) {
-  extern __shared__ float flam[];
-  for (int i = threadIdx.x; i < gd.total; i += blockDim.x) flam[i] = (float)lam[i];
-  __syncthreads();
   const int kin = gd.k[gd.inner];
   double acc = 0.0;
   const int lane = threadIdx.x & 31;
@@ -250,9 +236,7 @@ __global__ void logsum_kernel(GridDesc gd, const double* lam, double* logsum) {
       const int ax = gd.outer_axes[a];
       base += lam[gd.off[ax] + (int)((row / gd.outer_stride[a]) % gd.k[ax])];
     }
-    float racc = 0.f;
-    for (int m = lane; m < kin; m += 32) racc += __logf((float)(base + lam[gd.off[gd.inner] + m]));
-    acc += (double)racc;
+    for (int m = lane; m < kin; m += 32) acc += log(base + lam[gd.off[gd.inner] + m]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -327,7 +311,7 @@ static ggm_status make_desc(int L, const int* k, GridDesc* gd) {
 static int pick_J(int kin) { return kin <= 128 ? 4 : kin <= 256 ? 8 : kin <= 512 ? 16 : 32; }
 
 static size_t pass_smem(const GridDesc& gd) {
-  return (size_t)gd.total * (sizeof(double) + sizeof(float)) + 16;
+  return (size_t)gd.total * 2 * sizeof(double) + 16;
 }
 
 template <int J>
@@ -411,7 +395,7 @@ extern "C" ggm_status ggm_grid_marginals(int L, const int* k, const double* lamb
   if (logsum_out) {
     double* dls = partial + (size_t)gd.total * nblk;
     GGM_CUDA_TRY(cudaMemsetAsync(dls, 0, sizeof(double), s));
-    logsum_kernel<<<num_sms() * 4, 256, gd.total * sizeof(float), s>>>(gd, lambda, dls);
+    logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(gd, lambda, dls);
     GGM_CUDA_TRY(cudaGetLastError());
     GGM_CUDA_TRY(cudaMemcpyAsync(logsum_out, dls, sizeof(double), cudaMemcpyDeviceToHost, s));
     GGM_CUDA_TRY(cudaStreamSynchronize(s));
@@ -484,7 +468,7 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   GGM_CUDA_TRY(cudaStreamSynchronize(s));
   const double* lam_res = hstat[2] ? lam1 : lam0;
   finalize_kernel<<<1, 32, 0, s>>>(gd, lam_res, o.gauge, lambda, scal);
-  logsum_kernel<<<num_sms() * 4, 256, gd.total * sizeof(float), s>>>(gd, lam_res, scal + 1);
+  logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(gd, lam_res, scal + 1);
   GGM_CUDA_TRY(cudaGetLastError());
   // residual of the returned λ (its marginals are in g)
   double hres = 0.0;

@@ -66,7 +66,7 @@ def ks_sample(rng: np.random.Generator, psis) -> np.ndarray:
     x = w
     for ax, (_, u) in enumerate(decomp):
         x = np.moveaxis(np.tensordot(u, x, axes=([1], [ax])), 0, ax)
-    return x
+    return np.ascontiguousarray(x)
 
 
 def random_factor(rng: np.random.Generator, n: int, k: int):
@@ -92,7 +92,7 @@ def matrix_config(name: str) -> np.ndarray:
         keep = rng.random(counts.shape) < 0.181
         return np.log1p(counts * keep).astype(np.float32)
     psis = [er_precision(rng, d, meta["p"]) for d in meta["shape"]]
-    return ks_sample(rng, psis).astype(np.float32)
+    return np.ascontiguousarray(ks_sample(rng, psis), dtype=np.float32)
 
 
 def config(name: str):
@@ -113,7 +113,7 @@ def small_tensor(seed: int, shape, p: float = 0.3) -> np.ndarray:
     """Small Kronecker-sum Gaussian tensor for brute-force tests (same ER recipe)."""
     rng = np.random.default_rng(seed)
     psis = [er_precision(rng, d, p) for d in shape]
-    return ks_sample(rng, psis).astype(np.float32)
+    return np.ascontiguousarray(ks_sample(rng, psis), dtype=np.float32)
 
 
 def small_factor(seed: int, n: int, k: int):

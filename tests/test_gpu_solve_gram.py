@@ -55,14 +55,14 @@ def test_solve_matches_oracle(G, shape):
         ks.append(k)
         Es.append(E)
     lo, _ = O.solve_eigvals(Es, tol=1e-13)
-    lam, info = G.ggm_solve_eigvals(_cat(Es), ks, tol=1e-9)
+    lam, info = G.ggm_solve_eigvals(_cat(Es), ks, tol=2e-8)
     lg = _split(lam.cpu().numpy(), ks)
     # gauge-free comparison: grid sums, then the canonical (gauge 0) λ
     np.testing.assert_allclose(O.grid_sums(lg), O.grid_sums(lo), rtol=EIG_REL)
     for a, b in zip(lg, lo):
         np.testing.assert_allclose(a, b, rtol=EIG_REL)
     assert O.stationarity(Es, lg) < 1e-6
-    assert info["stationarity"] <= 1e-9
+    assert info["stationarity"] <= 2e-8
     assert info["nll"] == pytest.approx(O.nll(Es, lo), rel=1e-6, abs=1e-6)
 
 
