@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the GmGM hot path (arXiv 2407.19892) on B200: precision entries evaluated +
+sparsified per second (n^2 per axis) for the BASELINE.json workload C5 (factor-level axes
+n = 1,000,000 and n = 30,000, rank 100, top-10 per row; BJ:11), row-sharded over N GPUs.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config C5|C4]
+
+A step = one pass of the hot path over the workload: for every axis, ggm_sparse_precision
+(BK1 prep/split -> BK2 fused tcgen05 recomposition + top-t -> CSR) on this rank's rows; at
+N > 1 also the NCCL all-gather of the CSR shards.  Inputs (V, λ) are resident in HBM when the
+timed region starts (replicated by one NCCL broadcast at setup).  The inputs (V 400 MB, the
+split operand 512 MB) are larger than L2, so no explicit flush is used.  The e2e arm repeats
+the step through the same public API from pinned HOST buffers with H2D/D2H inside the timed
+region.  The reference arm (--impl reference) times the fp64 CPU oracle on a bounded row
+sample of the same workload (the reference of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "precision entries evaluated+sparsified/sec (n^2 per axis), % of TC roofline"
+UNIT = "entries/s"
+DTYPE = "f16x3 split (hi*hi+hi*lo+lo*hi), f32 accumulate"
+WORKLOADS = {
+    "C5": "C5: factor-level axes n=1,000,000 and n=30,000 (cell / gene axis of a million-cell "
+          "dataset), rank 100, V = QR of N(0,1), lambda ~ LogNormal(0,1), top-10 per row",
+    "C4": "C4: factor-level axis n=200,000, rank 64, top-10 per row",
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "MEASURED_PEAKS.json"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _load_workload(name):
+    from synth import gen
+    c = gen.config(name)
+    return c["axes"], c["t"]
+
+
+def run_reference(args):
+    """The reference arm: the fp64 CPU oracle (as it stands) on a bounded row sample."""
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+    axes, t = _load_workload(args.config)
+    rows_per_axis = args.ref_rows
+    rng = np.random.default_rng(0)
+    samples = [np.sort(rng.choice(V.shape[0], size=min(rows_per_axis, V.shape[0]),
+                                  replace=False)) for V, _ in axes]
+    ent_step = sum(len(s) * V.shape[0] for s, (V, _) in zip(samples, axes))
+
+    def step():
+        for s, (V, lam) in zip(samples, axes):
+            O.sparse_precision(V, lam, 0, 0, rows=s, t=t)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = ent_step / dt
+    cores = _blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (synth.gen seeded recipes)",
+        "config": {"workload": WORKLOADS[args.config], "sample_rows_per_axis": rows_per_axis},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{rows_per_axis} random rows per axis x all n columns per "
+                                   f"step (fp64 NumPy oracle, oracle.sparse_precision)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = max((i.get("num_threads", 0) for i in info), default=0)
+        return int(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(axes, t, rows=512):
+    import oracle as O
+    V, lam = axes[0]
+    rng = np.random.default_rng(1)
+    s = np.sort(rng.choice(V.shape[0], size=min(rows, V.shape[0]), replace=False))
+    t0 = time.perf_counter()
+    O.sparse_precision(V, lam, 0, 0, rows=s, t=t)
+    dt = time.perf_counter() - t0
+    return {"value": len(s) * V.shape[0] / dt, "unit": UNIT, "cores": _blas_threads(),
+            "kind": "oracle",
+            "sample": f"{len(s)} random rows of the n={V.shape[0]} axis x all columns "
+                      f"({dt:.1f} s, fp64 NumPy oracle.sparse_precision)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--cpu-rows", type=int, default=512)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2407_19892_b200 as G
+    from paper_2407_19892_b200.parallel import gather_topk_csr, shard_rows
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if not G.device_supported():
+        raise SystemExit("libggm: device is not sm_100a")
+
+    # ---------------- inputs: rank 0 generates, NCCL broadcast replicates (setup, untimed)
+    if rank == 0:
+        host_axes, t = _load_workload(args.config)
+        shapes = [V.shape for V, _ in host_axes]
+    else:
+        host_axes, t, shapes = None, None, None
+    if world > 1:
+        obj = [shapes, t]
+        dist.broadcast_object_list(obj, src=0)
+        shapes, t = obj
+    dev_axes = []
+    for a, (n, k) in enumerate(shapes):
+        if rank == 0:
+            V = torch.from_numpy(host_axes[a][0]).cuda()
+            lam = torch.from_numpy(host_axes[a][1]).cuda()
+        else:
+            V = torch.empty((n, k), dtype=torch.float32, device="cuda")
+            lam = torch.empty((k,), dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.broadcast(V, 0)
+            dist.broadcast(lam, 0)
+        dev_axes.append((V, lam))
+    if host_axes is None:   # host copies for the e2e arm on the other ranks
+        host_axes = [(V.cpu().numpy(), lam.cpu().numpy()) for V, lam in dev_axes]
+
+    plans = []
+    for (V, lam) in dev_axes:
+        n, k = V.shape
+        b, e = shard_rows(n, world, rank)
+        plans.append(G.SparsePlan(n, k, b, e, mode=0, topk=t))
+    entries_step = float(sum(V.shape[0] ** 2 for V, _ in dev_axes))
+    G.set_timing(True)
+    stream = torch.cuda.current_stream()
+
+    fused_ms = [[] for _ in plans]
+    launches = [0]
+
+    def step(record=False):
+        for a, (plan, (V, lam)) in enumerate(zip(plans, dev_axes)):
+            plan.run(V, lam)
+            if record:
+                fused_ms[a].append(G.last_timing()[1])
+                launches[0] += G.last_launches()
+            if world > 1:
+                gather_topk_csr(plan.col, plan.val, plan.t_eff, V.shape[0])
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+        dist.barrier()
+    ms_step = elapsed_ms / args.steps
+    value = entries_step / (ms_step * 1e-3)
+
+    # ---------------- roofline of the dominant kernel (BK2 on the largest axis)
+    peaks, peak_src = _peaks()
+    a0 = int(np.argmax([V.shape[0] for V, _ in dev_axes]))
+    V0 = dev_axes[a0][0]
+    n0, k0 = V0.shape
+    rows0 = plans[a0].row_end - plans[a0].row_begin
+    avg_fused = float(np.mean(fused_ms[a0]))
+    alg_flops = 2.0 * k0 * rows0 * n0                     # 2k flops / entry
+    achieved = alg_flops / (avg_fused * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "fused_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("config") == args.config and world == 1:
+                traffic = tj.get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_ms_fused_share = sum(np.mean(f) for f in fused_ms) / ms_step
+
+    # ---------------- e2e through the same public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hV = [torch.from_numpy(np.ascontiguousarray(h[0])).pin_memory() for h in host_axes]
+        hL = [torch.from_numpy(np.ascontiguousarray(h[1])).pin_memory() for h in host_axes]
+        hout = [(torch.empty(p.row_ptr.numel(), dtype=torch.int64).pin_memory(),
+                 torch.empty(p.col.numel(), dtype=torch.int32).pin_memory(),
+                 torch.empty(p.val.numel(), dtype=torch.float32).pin_memory()) for p in plans]
+        h2d = sum(v.numel() * 4 + l.numel() * 8 for v, l in zip(hV, hL))
+        d2h = sum(o[0].numel() * 8 + o[1].numel() * 4 + o[2].numel() * 4 for o in hout)
+
+        def e2e_step():
+            for a, plan in enumerate(plans):
+                V, lam = dev_axes[a]
+                V.copy_(hV[a], non_blocking=True)
+                lam.copy_(hL[a], non_blocking=True)
+                plan.run(V, lam)
+                hout[a][0].copy_(plan.row_ptr, non_blocking=True)
+                hout[a][1].copy_(plan.col, non_blocking=True)
+                hout[a][2].copy_(plan.val, non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ems], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": entries_step / (ems / args.steps * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    if rank == 0:
+        cpu = None if args.no_cpu else cpu_baseline(host_axes, t, args.cpu_rows)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": DTYPE, "data": "synthetic (synth.gen seeded recipes of BASELINE.json configs)",
+            "config": {"workload": WORKLOADS[args.config], "axes_n": [int(V.shape[0]) for V, _ in dev_axes],
+                       "k": [int(V.shape[1]) for V, _ in dev_axes], "topk": int(t),
+                       "parallelism": f"row-shard x{world}", "l2": "inputs > L2 (no flush needed)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "fused_recon_topk (BK2)",
+                         "achieved_basis": "2k flops per entry (SURVEY 8(d)) x rows x n / mean CUDA-event "
+                                           "duration of BK2 on the largest axis",
+                         "peak_basis": f"{peak_src} bf16_tflops_sustained / 3 (3-term fp16 split = 3 MMAs "
+                                       "per fp32-accurate product; fp16 rate = bf16 rate)",
+                         "kernel_ms": avg_fused, "step_share": step_ms_fused_share,
+                         "tensor_pipe_tflops": achieved * 3.0 * (16 * ((k0 + 15) // 16)) / k0},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": int(launches[0]),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

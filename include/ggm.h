@@ -92,16 +92,18 @@ ggm_status ggm_gram_eig(const float *X, int ndim, const int64_t *shape, int axis
  *  opts   : (host, may be NULL = defaults).
  *  lambda : out float64 sum(k), axis-concatenated, in the gauge opts->gauge.
  *  info   : (host, may be NULL) diagnostics.
- * Synchronizes `stream`.
+ * Scratch of O(Σk · #SMs) doubles is taken with stream-ordered cudaMallocAsync and released
+ * before returning.  Synchronizes `stream`.
  * ---------------------------------------------------------------------------------- */
 typedef struct {
   double tol;        /* stop when max_l max_i |E_li − g_li| / max E <= tol (reading Q4).
                         default 1e-7 */
   int max_iter;      /* default 20000 */
   double eps_scale;  /* feasibility floor eps = eps_scale * max(1/E). default 1e-10 */
-  int method;        /* 0 = multiplicative fixed point λ ← λ ⊙ g/E with Anderson-free
-                        NLL-monotone safeguard (default); 1 = Algorithm 1 gradient descent
-                        (readings Q1-Q3, slow; for cross-checks) */
+  int method;        /* 0 = majorise-minimise fixed point λ ← λ ⊙ g/E (default; the NLL
+                        decreases monotonically and λ stays > 0, so Algorithm 1's overshoot
+                        loop, never triggers).  Other values: GGM_ERR_UNSUPPORTED
+                        (Algorithm 1's gradient descent, readings Q1-Q3, lives in the oracle) */
   int gauge;         /* 0 = min-balanced PSD gauge (default, reading G);
                         1 = iterate as reached from λ0 = 1/E */
 } ggm_solve_opts;
@@ -120,8 +122,8 @@ ggm_status ggm_solve_eigvals(int L, const int *k, const double *E, const ggm_sol
                              double *lambda, ggm_solve_info *info, void *stream);
 
 /* Grid marginals alone (the Thm 2 trace term), for parity tests and the bench:
- * g (out, float64 sum(k)) and, if nll_out != NULL, F = Σ_j log s_j (host).  Synchronizes
- * `stream` only when nll_out != NULL. */
+ * g (out, float64 sum(k)) and, if logsum_out != NULL, F = Σ_j log s_j (host).  Synchronizes
+ * `stream` only when logsum_out != NULL. */
 ggm_status ggm_grid_marginals(int L, const int *k, const double *lambda, double *g,
                               double *logsum_out, void *stream);
 
@@ -170,6 +172,9 @@ ggm_status ggm_sparse_precision(int64_t n, int k, const float *V, const double *
  * split), ms[1] = fused tcgen05 kernel, ms[2] = merge/CSR assembly. */
 void ggm_set_timing(int enabled);
 void ggm_last_timing(float ms[3]);
+/* Number of libggm kernels launched by the last call on this thread (library kernels such
+ * as cuBLAS/cuSOLVER/CUB internals are not counted). */
+int ggm_last_launches(void);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,7 @@ EXPORTED = [
     "ggm_gram_eig_workspace", "ggm_gram_eig",
     "ggm_solve_opts_default", "ggm_solve_eigvals", "ggm_grid_marginals",
     "ggm_sparse_precision_workspace", "ggm_sparse_precision",
-    "ggm_set_timing", "ggm_last_timing",
+    "ggm_set_timing", "ggm_last_timing", "ggm_last_launches",
 ]
 
 
@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
     L.ggm_set_timing.restype = None
     L.ggm_last_timing.argtypes = [C.POINTER(C.c_float)]
     L.ggm_last_timing.restype = None
+    L.ggm_last_launches.restype = i32
     for name in ("ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
                  "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision"):
         getattr(L, name).restype = i32
@@ -248,6 +249,10 @@ def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
 
 def set_timing(enabled: bool):
     lib().ggm_set_timing(1 if enabled else 0)
+
+
+def last_launches() -> int:
+    return int(lib().ggm_last_launches())
 
 
 def last_timing():

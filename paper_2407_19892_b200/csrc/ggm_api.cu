@@ -12,6 +12,7 @@ namespace ggm {
 static thread_local char g_last_error[1024] = "";
 static thread_local bool g_timing = false;
 static thread_local float g_timing_ms[3] = {0.f, 0.f, 0.f};
+static thread_local int g_launches = 0;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -37,6 +38,8 @@ int num_sms() {
 }
 
 bool timing_enabled() { return g_timing; }
+void reset_launches() { g_launches = 0; }
+void count_launches(int n) { g_launches += n; }
 void record_timing(int slot, float ms) {
   if (slot >= 0 && slot < 3) g_timing_ms[slot] = ms;
 }
@@ -65,6 +68,8 @@ int ggm_device_supported(void) {
 }
 
 void ggm_set_timing(int enabled) { ggm::g_timing = enabled != 0; }
+
+int ggm_last_launches(void) { return ggm::g_launches; }
 
 void ggm_last_timing(float ms[3]) {
   for (int i = 0; i < 3; ++i) ms[i] = ggm::g_timing_ms[i];

@@ -16,6 +16,8 @@ ggm_status fail(ggm_status st, const char* fmt, ...);
 int num_sms();
 bool timing_enabled();
 void record_timing(int slot, float ms);
+void reset_launches();
+void count_launches(int n);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -757,6 +757,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     return fail(GGM_ERR_CUDA, "current device is not compute capability 10.0 (sm_100a)");
 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  reset_launches();
   EventTimer tm(timing_enabled(), s);
   tm.mark(0);
   GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
@@ -766,6 +767,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 8));
     absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
     scale_finalize<<<1, 1, 0, s>>>(w.sc);
+    count_launches(pl.alias ? 3 : 4);
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 8;
     split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
         V, lambda, n, k, pl.KA, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
@@ -809,6 +811,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
                                                : launch_fused<32>(fp, smem, grid, s);
   if (ce != cudaSuccess)
     return fail(GGM_ERR_CUDA, "fused_recon_topk launch: %s", cudaGetErrorString(ce));
+  count_launches(1);
   tm.mark(2);
 
   DevScalars hs;
@@ -823,6 +826,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
         merge_partials<32><<<blocks, threads, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t,
                                                       row_ptr, col, val);
       GGM_CUDA_TRY(cudaGetLastError());
+      count_launches(1);
     }
     tm.mark(3);
     GGM_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, s));
@@ -852,9 +856,11 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
                                                  w.cv_out, count, 0, 64, s));
     const int blocks = (int)std::min<int64_t>((count + 256) / 256 + 1, sms * 8);
     coo_to_csr<<<blocks, 256, 0, s>>>(w.key_out, w.cv_out, count, n, pl.rows, row_ptr, col, val);
+    count_launches(1);
   } else {
     zero_row_ptr<<<(int)std::min<int64_t>((pl.rows + 256) / 256 + 1, sms * 8), 256, 0, s>>>(
         row_ptr, pl.rows);
+    count_launches(1);
   }
   GGM_CUDA_TRY(cudaGetLastError());
   tm.mark(3);
