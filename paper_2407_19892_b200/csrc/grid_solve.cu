@@ -127,7 +127,7 @@ struct SolveParams {
   double* lam1;
   double* g;          // marginals of the last pass, Σk
   double* partial;    // [Σk][gridDim]
-  unsigned long long* res_bits;  // [2] residual max as double bits
+  unsigned long long* res_bits;  // [3] residual max as double bits (rotating)
   int* status;        // [0] iterations, [1] converged flag, [2] which λ buffer holds result
   double tol;
   int max_iter;
@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p)
     double* ln = cur ? p.lam0 : p.lam1;
     for (int i = threadIdx.x; i < gd.total; i += blockDim.x) sg[i] = 0.0;
     load_lambda(lc, gd.total, slam, true);
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.res_bits[(it + 1) & 1] = 0ull;
+    // 3 rotating residual slots: slot (it+1)%3 was last read right after the second grid
+    // sync of iteration it-2, which every block has passed by now (a 2-slot scheme would
+    // let block 0 clear a slot a slower block has not read yet).
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.res_bits[(it + 1) % 3] = 0ull;
     __syncthreads();
     grid_pass_block<J>(gd, slam, sg, wrow0, wstride);
     __syncthreads();
@@ -178,11 +181,11 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p)
         p.g[e] = sum;
         ln[e] = __ldcg(&lc[e]) * sum / Ee;
         const double r = fabs(Ee - sum) / emax;
-        atomicMax(&p.res_bits[it & 1], (unsigned long long)__double_as_longlong(r));
+        atomicMax(&p.res_bits[it % 3], (unsigned long long)__double_as_longlong(r));
       }
     }
     grid.sync();
-    const double res = __longlong_as_double((long long)__ldcg(&p.res_bits[it & 1]));
+    const double res = __longlong_as_double((long long)__ldcg(&p.res_bits[it % 3]));
     if (res <= p.tol) {
       done = true;
       break;
@@ -423,7 +426,7 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int nblk = grid_blocks(gd);
   const size_t T = gd.total;
-  // scratch: lam0, lam1, g, partial[T*nblk], res_bits[2], status[4], bad, scalars[4], logsum
+  // scratch: lam0, lam1, g, partial[T*nblk], scalars[4] (smin, logsum), res_bits[3], status[4]
   const size_t bytes = sizeof(double) * (3 * T + T * nblk + 8) + 64 + 64;
   DevBuf buf;
   GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
@@ -433,7 +436,7 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   double* partial = g + T;
   double* scal = partial + T * nblk;  // [0] smin, [1] logsum
   unsigned long long* res_bits = reinterpret_cast<unsigned long long*>(scal + 4);
-  int* istat = reinterpret_cast<int*>(res_bits + 2);  // [0..2] status, [3] bad
+  int* istat = reinterpret_cast<int*>(res_bits + 3);  // [0..2] status, [3] bad
   GGM_CUDA_TRY(cudaMemsetAsync(scal, 0, sizeof(double) * 8 + 64, s));
   check_E<<<4, 256, 0, s>>>(E, gd.total, istat + 3);
   init_lambda<<<(gd.total + 255) / 256, 256, 0, s>>>(E, gd.total, lam0);
@@ -473,7 +476,7 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   // residual of the returned λ (its marginals are in g)
   double hres = 0.0;
   {
-    const unsigned long long* rb = res_bits + (hstat[0] & 1);
+    const unsigned long long* rb = res_bits + (hstat[0] % 3);
     unsigned long long bits = 0;
     GGM_CUDA_TRY(cudaMemcpyAsync(&bits, rb, sizeof(bits), cudaMemcpyDeviceToHost, s));
     double hscal[2];

@@ -54,5 +54,5 @@ def probe_solve(ks, seed=0):
     torch.cuda.synchronize(); dt = (time.time() - t0) / 10
     print(f"   single marginal pass (incl. alloc+reduce): {dt*1e6:.1f} us = {pts/dt:.3e} pts/s", flush=True)
 
-for ks in [(400, 300, 200), (100, 100), (50, 50)]:
+for ks in ([] if "--sparse-only" in sys.argv else [(400, 300, 200), (100, 100), (50, 50)]):
     probe_solve(ks)
