@@ -68,13 +68,27 @@ __device__ __forceinline__ double rcp_f64(double s) {
 // All of s, 1/s and the sums are fp64 (no fixed fp32 rounding of λ or s that would floor
 // the stationarity residual; e.g. the isotropic case, where every s_j is equal, would
 // otherwise carry one identical rounding error in every term).
-template <int J>
-__device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* sg, int64_t row0,
-                                int64_t row_stride) {
+// NOUT = number of outer axes when known at compile time (0, 1, 2 cover L <= 3, i.e. every
+// BASELINE config); -1 = generic.  The per-row bookkeeping (base sum, odometer, outer
+// marginal atomics) is kept out of constant-bank indexing so that it stays small next to the
+// k_inner points of the row.
+template <int J, int NOUT>
+__device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* sg, int64_t gwarp,
+                                int64_t nwarps) {
+  constexpr int NO = NOUT < 0 ? kMaxAxes : (NOUT == 0 ? 1 : NOUT);
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   const int kin = gd.k[gd.inner];
   const int oin = gd.off[gd.inner];
+  const int nout = NOUT < 0 ? gd.n_outer : NOUT;
+  int ko[NO], oo[NO], idx[NO];
+  int64_t so[NO];
+#pragma unroll
+  for (int a = 0; a < NO; ++a) {
+    const bool live = a < nout;
+    ko[a] = live ? gd.k[gd.outer_axes[a]] : 1;
+    oo[a] = live ? gd.off[gd.outer_axes[a]] : 0;
+    so[a] = live ? gd.outer_stride[a] : 1;
+  }
   double lv[J], acc[J];
 #pragma unroll
   for (int jj = 0; jj < J; ++jj) {
@@ -82,12 +96,17 @@ __device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* 
     lv[jj] = (m < kin) ? slam[oin + m] : 1.0;
     acc[jj] = 0.0;
   }
-  for (int64_t row = row0 + warp; row < gd.rows; row += row_stride) {
-    double base = 0.0;  // Σ over the outer multi-index (last outer axis fastest)
-    for (int a = 0; a < gd.n_outer; ++a) {
-      const int ax = gd.outer_axes[a];
-      base += slam[gd.off[ax] + (int)((row / gd.outer_stride[a]) % gd.k[ax])];
-    }
+  // this warp's contiguous range of outer rows; the multi-index advances like an odometer
+  const int64_t per = (gd.rows + nwarps - 1) / nwarps;
+  const int64_t r0 = gwarp * per;
+  const int64_t r1 = min(gd.rows, r0 + per);
+#pragma unroll
+  for (int a = 0; a < NO; ++a) idx[a] = a < nout ? (int)((r0 / so[a]) % ko[a]) : 0;
+  for (int64_t row = r0; row < r1; ++row) {
+    double base = 0.0;
+#pragma unroll
+    for (int a = 0; a < NO; ++a)
+      if (a < nout) base += slam[oo[a] + idx[a]];
     double rsum = 0.0;
 #pragma unroll
     for (int jj = 0; jj < J; ++jj) {
@@ -98,19 +117,41 @@ __device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* 
         acc[jj] += r;
       }
     }
+    if (nout > 0) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-    if (lane < gd.n_outer) {
+      for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
       // lane a adds the row sum to g_{outer axis a}[idx_a]
-      const int ax = gd.outer_axes[lane];
-      const int my = (int)((row / gd.outer_stride[lane]) % gd.k[ax]);
-      atomicAdd(&sg[gd.off[ax] + my], rsum);
+#pragma unroll
+      for (int a = 0; a < NO; ++a)
+        if (a < nout && lane == a) atomicAdd(&sg[oo[a] + idx[a]], rsum);
+      // odometer: last outer axis fastest
+      bool carry = true;
+#pragma unroll
+      for (int a = NO - 1; a >= 0; --a) {
+        if (a < nout && carry) {
+          if (++idx[a] == ko[a])
+            idx[a] = 0;
+          else
+            carry = false;
+        }
+      }
     }
   }
 #pragma unroll
   for (int jj = 0; jj < J; ++jj) {
     const int m = lane + 32 * jj;
     if (m < kin) atomicAdd(&sg[oin + m], acc[jj]);
+  }
+}
+
+template <int J>
+__device__ __forceinline__ void grid_pass(const GridDesc& gd, const double* slam, double* sg,
+                                          int64_t gwarp, int64_t nwarps) {
+  switch (gd.n_outer) {
+    case 0: grid_pass_block<J, 0>(gd, slam, sg, gwarp, nwarps); break;
+    case 1: grid_pass_block<J, 1>(gd, slam, sg, gwarp, nwarps); break;
+    case 2: grid_pass_block<J, 2>(gd, slam, sg, gwarp, nwarps); break;
+    default: grid_pass_block<J, -1>(gd, slam, sg, gwarp, nwarps); break;
   }
 }
 
@@ -123,80 +164,92 @@ __device__ __forceinline__ void load_lambda(const double* lam, int total, double
 struct SolveParams {
   GridDesc gd;
   const double* E;
-  double* lam0;       // λ buffers (ping-pong), Σk each
-  double* lam1;
-  double* g;          // marginals of the last pass, Σk
-  double* partial;    // [Σk][gridDim]
-  unsigned long long* res_bits;  // [3] residual max as double bits (rotating)
-  int* status;        // [0] iterations, [1] converged flag, [2] which λ buffer holds result
+  double* lam_out;    // converged λ (gauge 1: as iterated), Σk
+  double* g;          // marginals at lam_out, Σk
+  double* gacc;       // [3][Σk] rotating global accumulators of the block partials
+  int* status;        // [0] iterations, [1] converged flag
+  double* res_out;    // stationarity of lam_out
   double tol;
   int max_iter;
 };
 
+// Whole MM iteration in one cooperative kernel with ONE grid-wide barrier per iteration:
+// every block keeps its own copy of λ in shared memory; block partial marginals are added
+// atomically into global slot it%3; after grid.sync every block reads the same sums,
+// computes the same residual and the same update (bitwise identical in all blocks).
+// Slot (it+1)%3 is cleared by block 0 during iteration it: its last readers finished before
+// the barrier of iteration it-1, and its next writers start after the barrier of it.
 template <int J>
 __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
   const GridDesc& gd = p.gd;
-  double* sg = dsm;               // Σk
-  double* slam = sg + gd.total;   // Σk
+  const int T = gd.total;
+  double* sg = dsm;        // Σk block partials, then the reduced marginals
+  double* slam = sg + T;   // Σk this block's λ
+  __shared__ double s_red[kWarps];
   __shared__ double s_emax;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) slam[i] = 1.0 / p.E[i];  // Alg. 1 line 5
   if (threadIdx.x == 0) {
     double m = 0.0;
-    for (int i = 0; i < gd.total; ++i) m = fmax(m, p.E[i]);
+    for (int i = 0; i < T; ++i) m = fmax(m, p.E[i]);
     s_emax = m;
   }
-  __syncthreads();
-  const double emax = s_emax;
-  const int64_t wstride = (int64_t)gridDim.x * kWarps;
-  const int64_t wrow0 = (int64_t)blockIdx.x * kWarps;
-  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  int cur = 0;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + wid;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
   int it = 0;
   bool done = false;
-  for (; it <= p.max_iter; ++it) {
-    const double* lc = cur ? p.lam1 : p.lam0;
-    double* ln = cur ? p.lam0 : p.lam1;
-    for (int i = threadIdx.x; i < gd.total; i += blockDim.x) sg[i] = 0.0;
-    load_lambda(lc, gd.total, slam, true);
-    // 3 rotating residual slots: slot (it+1)%3 was last read right after the second grid
-    // sync of iteration it-2, which every block has passed by now (a 2-slot scheme would
-    // let block 0 clear a slot a slower block has not read yet).
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.res_bits[(it + 1) % 3] = 0ull;
+  double res = 0.0;
+  const bool single = gridDim.x == 1;
+  for (;; ++it) {
+    for (int i = threadIdx.x; i < T; i += blockDim.x) sg[i] = 0.0;
+    if (blockIdx.x == 0 && !single)
+      for (int i = threadIdx.x; i < T; i += blockDim.x) p.gacc[(size_t)((it + 1) % 3) * T + i] = 0.0;
     __syncthreads();
-    grid_pass_block<J>(gd, slam, sg, wrow0, wstride);
+    grid_pass<J>(gd, slam, sg, gw, nw);
     __syncthreads();
-    for (int i = threadIdx.x; i < gd.total; i += blockDim.x)
-      p.partial[(size_t)i * gridDim.x + blockIdx.x] = sg[i];
-    grid.sync();
-    // per-entry reduction across blocks, update, stationarity
-    for (int e = gw; e < gd.total; e += gridDim.x * kWarps) {
-      double sum = 0.0;
-      for (int b = lane; b < (int)gridDim.x; b += 32) sum += __ldcg(&p.partial[(size_t)e * gridDim.x + b]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (lane == 0) {
-        const double Ee = p.E[e];
-        p.g[e] = sum;
-        ln[e] = __ldcg(&lc[e]) * sum / Ee;
-        const double r = fabs(Ee - sum) / emax;
-        atomicMax(&p.res_bits[it % 3], (unsigned long long)__double_as_longlong(r));
+    double mr = 0.0;
+    if (single) {  // one block: the block partials are the marginals, no grid barrier
+      for (int i = threadIdx.x; i < T; i += blockDim.x) mr = fmax(mr, fabs(p.E[i] - sg[i]));
+    } else {
+      double* acc = p.gacc + (size_t)(it % 3) * T;
+      for (int i = threadIdx.x; i < T; i += blockDim.x) atomicAdd(&acc[i], sg[i]);
+      grid.sync();
+      // reduced marginals g (identical in every block), stationarity max |E - g| / max E
+      for (int i = threadIdx.x; i < T; i += blockDim.x) {
+        const double gi = __ldcg(&acc[i]);
+        sg[i] = gi;
+        mr = fmax(mr, fabs(p.E[i] - gi));
       }
     }
-    grid.sync();
-    const double res = __longlong_as_double((long long)__ldcg(&p.res_bits[it % 3]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    if (lane == 0) s_red[wid] = mr;
+    __syncthreads();
+    mr = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) mr = fmax(mr, s_red[w]);
+    res = mr / s_emax;
     if (res <= p.tol) {
       done = true;
       break;
     }
     if (it == p.max_iter) break;
-    cur ^= 1;
+    // majorise-minimise update λ <- λ ⊙ g / E
+    for (int i = threadIdx.x; i < T; i += blockDim.x) slam[i] = slam[i] * sg[i] / p.E[i];
+    __syncthreads();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.status[0] = it;
-    p.status[1] = done ? 1 : 0;
-    p.status[2] = cur;  // λ buffer whose marginals were last evaluated (g corresponds to it)
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+      p.lam_out[i] = slam[i];
+      p.g[i] = sg[i];
+    }
+    if (threadIdx.x == 0) {
+      p.status[0] = it;
+      p.status[1] = done ? 1 : 0;
+      *p.res_out = res;
+    }
   }
 }
 
@@ -210,7 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1) marginal_pass_kernel(GridDesc gd,
   for (int i = threadIdx.x; i < gd.total; i += blockDim.x) sg[i] = 0.0;
   load_lambda(lam, gd.total, slam, false);
   __syncthreads();
-  grid_pass_block<J>(gd, slam, sg, (int64_t)blockIdx.x * kWarps, (int64_t)gridDim.x * kWarps);
+  grid_pass<J>(gd, slam, sg, (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
+               (int64_t)gridDim.x * kWarps);
   __syncthreads();
   for (int i = threadIdx.x; i < gd.total; i += blockDim.x)
     partial[(size_t)i * gridDim.x + blockIdx.x] = sg[i];
@@ -332,6 +386,14 @@ static int grid_blocks(const GridDesc& gd) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, num_sms()));
 }
 
+// Blocks for the cooperative solve: enough warps that each owns >= ~8 outer rows (a grid
+// barrier costs microseconds; small grids run in one block).
+static int solve_blocks(const GridDesc& gd) {
+  const double pts = (double)gd.rows * gd.k[gd.inner];
+  const int64_t want = (int64_t)std::ceil(pts / (kWarps * 8.0 * 32.0 * 16.0));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, num_sms()));
+}
+
 static cudaError_t launch_pass(const GridDesc& gd, const double* lam, double* partial, int nblk,
                                cudaStream_t s) {
   const size_t smem = pass_smem(gd);
@@ -424,22 +486,19 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
     return fail(GGM_ERR_UNSUPPORTED, "method %d not implemented on the GPU (use 0)", o.method);
   if (o.gauge != 0 && o.gauge != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "gauge=%d", o.gauge);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int nblk = grid_blocks(gd);
+  const int nblk = solve_blocks(gd);
   const size_t T = gd.total;
-  // scratch: lam0, lam1, g, partial[T*nblk], scalars[4] (smin, logsum), res_bits[3], status[4]
-  const size_t bytes = sizeof(double) * (3 * T + T * nblk + 8) + 64 + 64;
+  // scratch: lam_res, g, gacc[3T], scalars[4] (smin, logsum, res), status[4]
+  const size_t bytes = sizeof(double) * (5 * T + 8) + 64;
   DevBuf buf;
   GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
-  double* lam0 = static_cast<double*>(buf.p);
-  double* lam1 = lam0 + T;
-  double* g = lam1 + T;
-  double* partial = g + T;
-  double* scal = partial + T * nblk;  // [0] smin, [1] logsum
-  unsigned long long* res_bits = reinterpret_cast<unsigned long long*>(scal + 4);
-  int* istat = reinterpret_cast<int*>(res_bits + 3);  // [0..2] status, [3] bad
-  GGM_CUDA_TRY(cudaMemsetAsync(scal, 0, sizeof(double) * 8 + 64, s));
+  double* lam_res = static_cast<double*>(buf.p);
+  double* g = lam_res + T;
+  double* gacc = g + T;
+  double* scal = gacc + 3 * T;  // [0] smin, [1] logsum, [2] residual
+  int* istat = reinterpret_cast<int*>(scal + 4);  // [0] iterations, [1] converged, [3] bad
+  GGM_CUDA_TRY(cudaMemsetAsync(gacc, 0, sizeof(double) * (3 * T + 8) + 64, s));
   check_E<<<4, 256, 0, s>>>(E, gd.total, istat + 3);
-  init_lambda<<<(gd.total + 255) / 256, 256, 0, s>>>(E, gd.total, lam0);
   GGM_CUDA_TRY(cudaGetLastError());
   int hbad = 0;
   GGM_CUDA_TRY(cudaMemcpyAsync(&hbad, istat + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -449,12 +508,11 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   SolveParams sp;
   sp.gd = gd;
   sp.E = E;
-  sp.lam0 = lam0;
-  sp.lam1 = lam1;
+  sp.lam_out = lam_res;
   sp.g = g;
-  sp.partial = partial;
-  sp.res_bits = res_bits;
+  sp.gacc = gacc;
   sp.status = istat;
+  sp.res_out = scal + 2;
   sp.tol = o.tol;
   sp.max_iter = o.max_iter;
   const size_t smem = pass_smem(gd);
@@ -466,23 +524,18 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
     default: ce = launch_solve<32>(sp, nblk, smem, s); break;
   }
   if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
-  int hstat[3] = {0, 0, 0};
+  int hstat[2] = {0, 0};
   GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  const double* lam_res = hstat[2] ? lam1 : lam0;
   finalize_kernel<<<1, 32, 0, s>>>(gd, lam_res, o.gauge, lambda, scal);
   logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(gd, lam_res, scal + 1);
   GGM_CUDA_TRY(cudaGetLastError());
   // residual of the returned λ (its marginals are in g)
   double hres = 0.0;
   {
-    const unsigned long long* rb = res_bits + (hstat[0] % 3);
-    unsigned long long bits = 0;
-    GGM_CUDA_TRY(cudaMemcpyAsync(&bits, rb, sizeof(bits), cudaMemcpyDeviceToHost, s));
-    double hscal[2];
+    double hscal[3];
     GGM_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, s));
     GGM_CUDA_TRY(cudaStreamSynchronize(s));
-    memcpy(&hres, &bits, sizeof(double));
+    hres = hscal[2];
     if (info) {
       std::vector<double> hE(T), hL(T);
       GGM_CUDA_TRY(cudaMemcpy(hE.data(), E, T * sizeof(double), cudaMemcpyDeviceToHost));
