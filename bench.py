@@ -174,6 +174,38 @@ def cpu_baseline(axes, t, rows=512):
                       f"({dt:.1f} s, fp64 NumPy oracle.sparse_precision)"}
 
 
+def stage_timings(G, torch):
+    """§8(a) rows a1-a4 (Gram spectrum + eigenvalue MLE) on the data configs C2 and C3:
+    device time of ggm_gram_eig per axis and of ggm_solve_eigvals (both synchronise)."""
+    from synth import gen
+    out = {}
+    for name in ("C2", "C3"):
+        cfg = gen.config(name)
+        X = torch.from_numpy(cfg["X"]).cuda()
+        ks = cfg["k"]
+        Es, gram_ms = [], []
+        for a, k in enumerate(ks):
+            G.ggm_gram_eig(X, a, k)              # warm-up (handles, workspace sizing)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, E, _ = G.ggm_gram_eig(X, a, k)
+            gram_ms.append((time.perf_counter() - t0) * 1e3)
+            Es.append(E)
+        Ec = torch.cat(Es)
+        G.ggm_solve_eigvals(Ec, ks)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, info = G.ggm_solve_eigvals(Ec, ks)
+        solve_ms = (time.perf_counter() - t0) * 1e3
+        pts = float(np.prod(ks))
+        out[name] = {"gram_eig_ms": gram_ms, "solve_ms": solve_ms,
+                     "solve_iterations": info["iterations"],
+                     "stationarity": info["stationarity"],
+                     "grid_points_per_s": pts * max(info["iterations"], 1) / (solve_ms * 1e-3),
+                     "grid_points": pts}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,6 +217,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=512)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stages", action="store_true",
+                    help="skip the a1-a4 stage timings (gram_eig + solve on C2/C3)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -335,6 +369,7 @@ def main():
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(host_axes, t, args.cpu_rows)
+        stages = None if args.no_stages else stage_timings(G, torch)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -356,6 +391,7 @@ def main():
             "e2e": e2e,
             "clocks": clk,
             "gpu_launches": int(launches[0]),
+            "stages_a1_a4": stages,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -156,6 +156,13 @@ typedef struct {
   float tau;  /* mode 1 only, >= 0 */
   int col_chunks; /* 0 = automatic; else split each row block's column sweep into this
                      many chunks merged afterwards (balances small row ranges) */
+  int symmetric;  /* mode 0 over the FULL axis only (row_begin = 0, row_end = n), k <= 128:
+                     1 = use the symmetric scheme; 0 (automatic) and 2 = plain scheme.
+                     Ψ is symmetric, so each unordered 128x128 block pair is evaluated once
+                     (cyclic window per row block); the transposed direction keeps entries
+                     >= a per-row lower bound of the t-th |ψ| obtained from a strided seed
+                     pass over 1/16 of the columns; per-row candidate buckets are merged,
+                     and any row block whose bucket overflowed is recomputed exactly. */
 } ggm_sparsify_opts;
 
 ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t row_begin, int64_t row_end,
@@ -169,12 +176,18 @@ ggm_status ggm_sparse_precision(int64_t n, int k, const float *V, const double *
 
 /* Per-kernel timing of the last ggm_sparse_precision call on this thread, measured with
  * CUDA events on `stream` when enabled (for bench.py's roofline).  ms[0] = prep (absmax +
- * split), ms[1] = fused tcgen05 kernel, ms[2] = merge/CSR assembly. */
+ * split, + the seed pass in the symmetric scheme), ms[1] = main fused tcgen05 kernel,
+ * ms[2] = merge/CSR assembly. */
 void ggm_set_timing(int enabled);
 void ggm_last_timing(float ms[3]);
 /* Number of libggm kernels launched by the last call on this thread (library kernels such
  * as cuBLAS/cuSOLVER/CUB internals are not counted). */
 int ggm_last_launches(void);
+/* Statistics of the last ggm_sparse_precision call on this thread: out[0] = scheme (0 plain,
+ * 2 symmetric), out[1] = entries evaluated by the main fused kernel (incl. padding),
+ * out[2] = transposed-direction candidates emitted, out[3] = row blocks recomputed after a
+ * candidate-bucket overflow. */
+void ggm_last_stats(double out[4]);
 
 #ifdef __cplusplus
 }

@@ -8,10 +8,10 @@ Public API (thin bindings of libggm.so, include/ggm.h):
   parallel.sharded_sparse_precision  row-sharded multi-GPU driver (torch.distributed/NCCL)
 """
 from ._ggm import (GGMError, SparsePlan, device_supported, ggm_gram_eig, ggm_grid_marginals,
-                   ggm_solve_eigvals, ggm_sparse_precision, last_launches, last_timing, lib,
+                   ggm_solve_eigvals, ggm_sparse_precision, last_launches, last_stats, last_timing, lib,
                    set_timing,
                    version, EXPORTED, MAX_TOPK)
 
 __all__ = ["GGMError", "SparsePlan", "device_supported", "ggm_gram_eig", "ggm_grid_marginals",
-           "ggm_solve_eigvals", "ggm_sparse_precision", "last_launches", "last_timing", "lib", "set_timing",
+           "ggm_solve_eigvals", "ggm_sparse_precision", "last_launches", "last_stats", "last_timing", "lib", "set_timing",
            "version", "EXPORTED", "MAX_TOPK"]

@@ -29,7 +29,7 @@ EXPORTED = [
     "ggm_gram_eig_workspace", "ggm_gram_eig",
     "ggm_solve_opts_default", "ggm_solve_eigvals", "ggm_grid_marginals",
     "ggm_sparse_precision_workspace", "ggm_sparse_precision",
-    "ggm_set_timing", "ggm_last_timing", "ggm_last_launches",
+    "ggm_set_timing", "ggm_last_timing", "ggm_last_launches", "ggm_last_stats",
 ]
 
 
@@ -53,7 +53,7 @@ class SolveInfo(C.Structure):
 
 class SparsifyOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("topk", C.c_int), ("tau", C.c_float),
-                ("col_chunks", C.c_int)]
+                ("col_chunks", C.c_int), ("symmetric", C.c_int)]
 
 
 _lib = None
@@ -89,6 +89,8 @@ def lib() -> C.CDLL:
     L.ggm_last_timing.argtypes = [C.POINTER(C.c_float)]
     L.ggm_last_timing.restype = None
     L.ggm_last_launches.restype = i32
+    L.ggm_last_stats.argtypes = [C.POINTER(C.c_double)]
+    L.ggm_last_stats.restype = None
     for name in ("ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
                  "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision"):
         getattr(L, name).restype = i32
@@ -186,9 +188,10 @@ class SparsePlan:
     """Workspace + output buffers for repeated ggm_sparse_precision calls (bench loop)."""
 
     def __init__(self, n, k, row_begin, row_end, mode=0, topk=10, tau=0.0, col_chunks=0,
-                 capacity=None, device="cuda"):
+                 capacity=None, device="cuda", symmetric=0):
         self.n, self.k, self.row_begin, self.row_end = int(n), int(k), int(row_begin), int(row_end)
-        self.opts = SparsifyOpts(int(mode), int(topk), float(tau), int(col_chunks))
+        self.opts = SparsifyOpts(int(mode), int(topk), float(tau), int(col_chunks),
+                                 int(symmetric))
         rows = self.row_end - self.row_begin
         self.t_eff = min(int(topk), self.n - 1)
         if capacity is None:
@@ -227,7 +230,7 @@ class SparsePlan:
 def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
                          row_end: int | None = None, mode: int = 0, topk: int = 10,
                          tau: float = 0.0, col_chunks: int = 0, capacity: int | None = None,
-                         stream=None):
+                         stream=None, symmetric: int = 0):
     """Fused thresh[V diag(λ) V^T] for rows [row_begin,row_end) (Alg. 1 line 19).
     Returns CSR (row_ptr int64, col int32, val float32) on the device.  Mode 1 retries once
     with the required capacity (two-call protocol)."""
@@ -235,20 +238,27 @@ def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
     if row_end is None:
         row_end = n
     plan = SparsePlan(n, k, row_begin, row_end, mode, topk, tau, col_chunks, capacity,
-                      device=V.device)
+                      device=V.device, symmetric=symmetric)
     try:
         nnz = plan.run(V, lam, stream)
     except GGMError as e:
         if e.status != 5:
             raise
         plan = SparsePlan(n, k, row_begin, row_end, mode, topk, tau, col_chunks,
-                          max(e.required, 1), device=V.device)
+                          max(e.required, 1), device=V.device, symmetric=symmetric)
         nnz = plan.run(V, lam, stream)
     return plan.row_ptr, plan.col[:nnz], plan.val[:nnz]
 
 
 def set_timing(enabled: bool):
     lib().ggm_set_timing(1 if enabled else 0)
+
+
+def last_stats() -> dict:
+    arr = (C.c_double * 4)()
+    lib().ggm_last_stats(arr)
+    return {"scheme": "symmetric" if arr[0] == 2 else "plain", "entries_main": arr[1],
+            "candidates": int(arr[2]), "recomputed_blocks": int(arr[3])}
 
 
 def last_launches() -> int:

@@ -4,18 +4,20 @@
 // TMEM), with the per-row top-t / threshold selection fused into the epilogue so that the
 // n x n matrix is never written ("we eigen-recompose and threshold simultaneously").
 //
-// Kernels (DESIGN.md §"Kernels"):
+// Kernels:
 //   BK1a absmax_check   max_{i,r} |V_ir|·sqrt(λ_r), finiteness / λ>0 flags
 //   BK1b scale_finalize power-of-two scale s = 2^e with max|U|·s <= 2^14
 //   BK1c split_tile     U·s = hi + lo (two fp16 terms) written in the pre-swizzled
 //                       (SWIZZLE_128B, K-major) 128-row block layout the MMA reads
 //   BK2  fused_recon_topk  persistent, warp-specialised: 1 producer warp (bulk async
 //                       copies), 1 MMA-issuer warp (3 MMAs / K-step: hi·hi, hi·lo, lo·hi),
-//                       4 epilogue warps (tcgen05.ld thread = row, register top-t)
-//   BK3  merge_partials / coo_to_csr  column-chunk merge (mode 0) and CSR assembly (mode 1)
+//                       8 epilogue warps (tcgen05.ld thread = row, register top-t).  Three
+//                       tile enumerations ("kinds"): plain (rows x all columns), seed (rows x
+//                       a strided column sample -> per-row lower bounds of the t-th |ψ|) and
+//                       symmetric (each unordered 128x128 block pair once, cyclic window;
+//                       the transposed direction emits candidates above the seed bound)
+//   BK3  merge_partials / merge_sym / coo_to_csr  CSR assembly
 #include <cub/device/device_radix_sort.cuh>
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -37,11 +39,17 @@ constexpr int kTileN = 256;               // N (columns of Ψ per tile; 2 operan
 constexpr int kAtomElems = 64;            // fp16 elements per 128-byte swizzle row
 constexpr int kAtomBytes = kRowsPerBlock * 128;  // one (128-row block, K atom) = 16 KB
 constexpr int kStages = 2;
-constexpr int kThreads = 384;             // 12 warps: 4 role warps + 8 epilogue warps
+#ifndef GGM_THREADS
+#define GGM_THREADS 320
+#endif
+constexpr int kThreads = GGM_THREADS;     // producer(+TMEM alloc), MMA, [idle], 8 epilogue warps
+constexpr int kFirstEpiWarp = kThreads / 32 - 8;
 constexpr int kTmemCols = 512;            // 2 accumulator buffers x 256 columns
 constexpr int kMaxResidentAtoms = 2;
+// A (128 rows x KA atoms x hi/lo) stays resident in shared memory when KA <= 2 (k <= 128)
 constexpr int kEpiWarps = 8;              // epilogue warps (2 per TMEM lane quadrant)
-constexpr int kScratchFloats = 32 * 32;   // per epilogue warp: [32 values][32 lanes]      // A (128 rows x KA atoms x hi/lo) resident if KA<=2
+constexpr int kScratchFloats = 32 * 32;   // per epilogue warp: [32 values][32 lanes]
+constexpr int kSeedStride = 16;           // seed pass samples every 16th column tile
 
 __host__ __device__ inline size_t block_bytes(int KA) { return (size_t)2 * KA * kAtomBytes; }
 
@@ -49,9 +57,11 @@ struct DevScalars {
   unsigned int absmax_bits;  // float bits of max |U|
   int flags;                 // 1 = non-finite V, 2 = lambda <= 0 or non-finite
   int exp2;                  // e: s = 2^e
-  int pad;
+  int cand_overflow;         // kSym: candidate pool exhausted -> exact fallback
   unsigned long long coo_count;
+  unsigned long long cand_alloc;  // kSym: entries reserved from the candidate pool
 };
+constexpr int kCandChunk = 4096;  // candidate-pool reservation granularity (entries)
 
 // ------------------------------------------------------------------ BK1a
 __global__ void absmax_check(const float* __restrict__ V, const double* __restrict__ lam,
@@ -139,6 +149,9 @@ __global__ void split_tile(const float* __restrict__ V, const double* __restrict
 }
 
 // ------------------------------------------------------------------ BK2
+// ------------------------------------------------------------------ BK2
+enum Kind : int { kPlain = 0, kSeed = 1, kSym = 2 };
+
 struct FusedParams {
   const uint8_t* A;  // row-block operand (rows [row_begin,row_end)), tiled layout
   const uint8_t* B;  // column operand (all n rows, padded to 256), tiled layout
@@ -146,19 +159,26 @@ struct FusedParams {
   int KS;            // K steps of 16 actually issued (ceil(k/16))
   int resident;      // 1: A kept in shared memory for a whole row block
   int64_t n, row_begin, rows;
+  int kind;          // Kind
   int RB, NT, C, TPC;
+  int NB;            // kSym: 128-row blocks of the axis (row_begin == 0, rows == n)
   int mode, t;
   float tau;
   const DevScalars* sc;
   int64_t* row_ptr;
   int32_t* col;
   float* val;
-  int32_t* pcol;
+  int32_t* pcol;     // partial per-row lists [C][rows][t] (plain C > 1, kSym: C = 1)
   float* pval;
-  int64_t* coo_key;
+  int64_t* coo_key;  // mode 1 candidates
   float* coo_val;
   unsigned long long* coo_count;
   int64_t capacity;
+  float* thr_out;          // kSeed: per-row t-th largest sampled |ψ| (accumulator units)
+  const float* thr;        // kSym: per-column lower bound (accumulator units, +inf = none)
+  uint32_t* cand_key;      // kSym: candidate pool: target row j (UINT32_MAX = unused slot)
+  uint2* cand_val;         //       (source row i, ψ bits)
+  int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
   int dbg;  // timing experiments only (GGM_DEBUG_EPI): 1 = TMEM loads only, 2 = no epilogue work
 };
 
@@ -169,6 +189,54 @@ __host__ inline size_t fused_smem_bytes(int KA, int resident) {
   size_t a = resident ? block_bytes(KA) : 0;
   return 1024 /*align slack*/ + a + kStages * stage_bytes(resident) + 256 /*barriers*/ +
          kEpiWarps * kScratchFloats * sizeof(float);
+}
+
+// Tile enumeration shared by the producer, MMA and epilogue roles.  A unit is one 128-row
+// block rb (plus a column chunk cc for kPlain); tile s of the unit pairs two 128-column
+// operand blocks K0, K1 (the two N-halves of one 128x256 MMA tile); h1 = second half valid.
+struct TileRef {
+  int K0, K1;
+  bool h1;
+};
+__device__ __forceinline__ int sym_window(int rb, int NB) {
+  // blocks K = rb + d (mod NB), d < W: each unordered pair {I, K} exactly once
+  return (NB & 1) ? (NB + 1) / 2 : NB / 2 + (rb < NB / 2 ? 1 : 0);
+}
+template <int KIND>
+__device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& rb) {
+  if (KIND == kPlain) {
+    rb = u / p.C;
+    const int j0 = (u % p.C) * p.TPC;
+    return min(p.NT, j0 + p.TPC) - j0;
+  }
+  rb = u;
+  if (KIND == kSeed) {
+    const int off = rb % kSeedStride;
+    return off < p.NT ? (p.NT - 1 - off) / kSeedStride + 1 : 0;
+  }
+  return (sym_window(rb, p.NB) + 1) / 2;
+}
+template <int KIND>
+__device__ __forceinline__ TileRef tile_ref(const FusedParams& p, int u, int rb, int s) {
+  TileRef tr;
+  if (KIND == kSym) {
+    // Visit the window [rb, rb + W) starting at X = the last row block of this wave of
+    // units (all CTAs of a wave contain X in their windows), so concurrently running CTAs
+    // stream the same column blocks in lockstep and share them through L2.
+    const int W = sym_window(rb, p.NB);
+    const int X = min(p.NB - 1, u - (int)blockIdx.x + (int)gridDim.x - 1);
+    int delta = (X - rb + p.NB) % p.NB;
+    if (delta >= W) delta = 0;
+    tr.K0 = (rb + (delta + 2 * s) % W) % p.NB;
+    tr.h1 = 2 * s + 1 < W;
+    tr.K1 = tr.h1 ? (rb + (delta + 2 * s + 1) % W) % p.NB : tr.K0;
+    return tr;
+  }
+  const int j = KIND == kPlain ? (u % p.C) * p.TPC + s : rb % kSeedStride + s * kSeedStride;
+  tr.K0 = 2 * j;
+  tr.K1 = 2 * j + 1;
+  tr.h1 = true;
+  return tr;
 }
 
 // Per-thread (= per-row) top-t list kept entirely in registers.  Slots are sorted
@@ -238,15 +306,21 @@ struct TopList {
       idx[MAXT - 1] = j;
     }
   }
+  // Emit slots [0, t) in ascending column order.
+  __device__ __forceinline__ void emit_sorted(int t, int32_t* col, float* val, float sd) const {
+#pragma unroll
+    for (int a = 0; a < MAXT; ++a) {
+      if (a < t) {
+        int rank = 0;
+#pragma unroll
+        for (int b = 0; b < MAXT; ++b)
+          if (b < t && idx[b] < idx[a]) ++rank;
+        col[rank] = idx[a];
+        val[rank] = sval[a] * sd;
+      }
+    }
+  }
 };
-
-// Epilogue role (warps 4-11): TMEM -> registers, fused per-row top-t / threshold.
-// Warp w handles TMEM lane quadrant q = w & 3 (thread = row) and column half h = (w-4) >> 2
-// of every 256-column tile (4 x tcgen05.ld.32x32b.x32 per tile, the next chunk's load in
-// flight while the current chunk is reduced).  Two warps share each row; their partial
-// lists are merged through shared memory at the end of a unit.  Fast path per 32 values:
-// 4 independent FMNMX3 chains of |v| against the row's current t-th magnitude; the rare
-// path stages the chunk in the warp's shared scratch and inserts candidates in column order.
 
 __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
   float m0 = fabsf(v[0]), m1 = fabsf(v[1]), m2 = fabsf(v[2]), m3 = fabsf(v[3]);
@@ -260,51 +334,79 @@ __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
   return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
 }
 
-template <int MAXT>
+// Epilogue role (warps 2-9): TMEM -> registers, fused per-row top-t / threshold.
+// Warp w handles TMEM lane quadrant q = w & 3 (thread = row) and column half h = (w-2) >> 2
+// of every 256-column tile, i.e. one 128-column operand block (4 x tcgen05.ld.32x32b.x32,
+// the next chunk's load in flight while the current chunk is reduced).  Two warps share
+// each row; their partial lists are merged through shared memory at the end of a unit.
+// Fast path per 32 values: 4 independent FMNMX chains of |v| against the row's current t-th
+// magnitude; the rare path stages the chunk in the warp's shared scratch and inserts
+// candidates in column order.  kSym additionally tests each value against its COLUMN's
+// lower bound (the transposed entry ψ_ji = ψ_ij) and appends survivors to row j's bucket.
+template <int MAXT, int KIND>
 __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tmem_base,
-                                              uint64_t* tfull, uint64_t* tempty, int unit0,
-                                              int ustride, int units, int rows_per_unit,
-                                              int row_off, bool remote_arrive, int warp,
+                                              uint64_t* tfull, uint64_t* tempty, int warp,
                                               int lane, float* scratch_all) {
-  const int ew = warp - 4;
+  const int ew = warp - kFirstEpiWarp;  // 0..7; slot of (quadrant q, half h) = h*4 + ((q-first)&3)
   const int q = warp & 3;   // TMEM lane quadrant accessible to this warp
   const int h = ew >> 2;    // column half of each tile
   const int r = q * 32 + lane;
   float* scratch = scratch_all + ew * kScratchFloats;
-  const float scale_down = ldexpf(1.f, -p.sc->exp2);  // ψ = acc · 2^-e · 2^-e
+  const float sd = ldexpf(1.f, -p.sc->exp2);  // ψ = acc · 2^-e · 2^-e
+  const float sd2 = sd * sd;
   const float tau_s = ldexpf(ldexpf(p.tau, p.sc->exp2), p.sc->exp2);
   const float qnan = __int_as_float(0x7fc00000);
   const int t = p.t;
+  const int units = KIND == kPlain ? p.RB * p.C : p.RB;
   int buf = 0;
   uint32_t tphase = 0;
   TopList<MAXT> top;
-  for (int u = unit0; u < units; u += ustride) {
-    const int rb = u / p.C, cc = u % p.C;
-    const int j0 = cc * p.TPC, j1 = min(p.NT, j0 + p.TPC);
-    const int64_t lr = (int64_t)rb * rows_per_unit + row_off + r;
+  // kSym candidates: appended into chunks reserved from a global pool (one atomic per
+  // kCandChunk entries); slots are claimed within the warp by ballot + popc (no atomics)
+  int64_t cbase = 0, cused = kCandChunk;  // current chunk [cbase, cbase + kCandChunk)
+  DevScalars* scw = const_cast<DevScalars*>(p.sc);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    int rb;
+    const int ntiles = unit_tiles<KIND>(p, u, rb);
+
+    const int64_t lr = (int64_t)rb * kRowsPerBlock + r;
     const bool valid = lr < p.rows;
     const int64_t gi = p.row_begin + lr;
     top.init(t);
-    for (int j = j0; j < j1; ++j) {
+    for (int s = 0; s < ntiles; ++s) {
+      const TileRef tr = tile_ref<KIND>(p, u, rb, s);
+      const int Kh = h ? tr.K1 : tr.K0;
+      const bool live = (h == 0 || tr.h1) && p.dbg != 2;
+      const bool emit_cols = KIND == kSym && Kh != rb && p.dbg != 3 && p.dbg != 4;
       mbar_wait(&tfull[buf], tphase);
       tc_fence_after();
       const uint32_t taddr =
           tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTileN + h * (kTileN / 2));
-      const int nchunks = p.dbg == 2 ? 0 : (kTileN / 2) / 32;
+      const int nchunks = live ? (kTileN / 2) / 32 : 0;
       uint32_t vn[32];
       if (nchunks) tmem_ld32_nowait(taddr, vn);
 #pragma unroll 1
       for (int c = 0; c < nchunks; ++c) {
         float v[32];
+        // kSym: this chunk's column bounds (warp-uniform 16-byte loads), issued before the
+        // TMEM wait and the row-direction work so their latency is hidden
+        float4 thc[8];
+        if (emit_cols) {
+          const float4* tp =
+              reinterpret_cast<const float4*>(p.thr + (int64_t)Kh * kRowsPerBlock + c * 32);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) thc[g] = __ldg(tp + g);
+        }
         tmem_wait_ld(vn);
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(vn[e]);
         if (c + 1 < nchunks) tmem_ld32_nowait(taddr + (c + 1) * 32, vn);
+
         if (p.dbg == 1) {
           if (v[0] == 12345.f && v[31] == 54321.f) p.row_ptr[0] = (int64_t)v[7];
           continue;
         }
-        const int64_t col0 = (int64_t)j * kTileN + h * (kTileN / 2) + c * 32;
+        const int64_t col0 = (int64_t)Kh * kRowsPerBlock + c * 32;
         if (((uint64_t)(gi - col0) < 32ull) || (col0 + 32 > p.n)) {
           // diagonal (j == i: not an edge, Q8) and padding columns (j >= n): NaN, ignored
 #pragma unroll
@@ -314,7 +416,74 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
           }
         }
         const float m = max32_abs(v);
+        if (emit_cols) {
+          // transposed direction: ψ_ij is also entry (j, i) of row j, kept if |ψ| >= the
+          // seed lower bound of row j (the true t-th magnitude of row j is >= that bound).
+          // Exact per-column test: max_e(|v_e| - thr_{col0+e}) >= 0, bounds read with
+          // warp-uniform (broadcast) 16-byte loads.
+          float d0 = -INFINITY, d1 = -INFINITY;
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const float4 th = thc[g];
+            d0 = fmaxf(d0, fmaxf(fabsf(v[4 * g + 0]) - th.x, fabsf(v[4 * g + 1]) - th.y));
+            d1 = fmaxf(d1, fmaxf(fabsf(v[4 * g + 2]) - th.z, fabsf(v[4 * g + 3]) - th.w));
+          }
+          if (__any_sync(0xffffffffu, valid && fmaxf(d0, d1) >= 0.f)) {
+            if (cused + 32 * 32 > kCandChunk) {  // reserve a fresh chunk for this chunk's hits
+              unsigned long long b0 = 0;
+              if (lane == 0) b0 = atomicAdd(&scw->cand_alloc, (unsigned long long)kCandChunk);
+              cbase = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+              cused = 0;
+              if (cbase + kCandChunk > p.cand_total) {
+                if (lane == 0) atomicOr(&scw->cand_overflow, 1);  // exact fallback by the host
+                cused = kCandChunk;
+              }
+            }
+            if (cused + 32 * 32 <= kCandChunk) {
+              // per-thread hit mask, warp prefix sum of hit counts, then each thread writes
+              // its own hits (values staged in the warp's scratch for dynamic indexing)
+              uint32_t mask = 0;
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const float4 th = thc[g];
+                mask |= (fabsf(v[4 * g + 0]) >= th.x ? 1u : 0u) << (4 * g + 0);
+                mask |= (fabsf(v[4 * g + 1]) >= th.y ? 1u : 0u) << (4 * g + 1);
+                mask |= (fabsf(v[4 * g + 2]) >= th.z ? 1u : 0u) << (4 * g + 2);
+                mask |= (fabsf(v[4 * g + 3]) >= th.w ? 1u : 0u) << (4 * g + 3);
+              }
+              if (!valid) mask = 0;
+              const int cnt = __popc(mask);
+              int incl = cnt;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              const int total = __shfl_sync(0xffffffffu, incl, 31);
+              if (mask) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) scratch[e * 32 + lane] = v[e];
+              }
+              __syncwarp();
+              int64_t at = cbase + cused + (incl - cnt);
+              while (mask) {
+                const int e = __ffs(mask) - 1;
+                mask &= mask - 1;
+                p.cand_key[at] = (uint32_t)(col0 + e);
+                p.cand_val[at] = make_uint2((unsigned)gi,
+                                            __float_as_uint(scratch[e * 32 + lane] * sd2));
+                ++at;
+              }
+              cused += total;
+              __syncwarp();
+            }
+          }
+        }
         const float thr = p.mode == 0 ? top.thr() : tau_s;
+        if (p.dbg == 4) {
+          if (m == 12345.f) p.row_ptr[0] = 7;
+          continue;
+        }
         if (__any_sync(0xffffffffu, m > thr)) {
           // rare path: stage the chunk, then visit this thread's candidates in column order
           uint32_t mask = 0;
@@ -340,7 +509,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
               mask &= mask - 1;
               if ((int64_t)base < p.capacity) {
                 p.coo_key[base] = lr * p.n + col0 + e;
-                p.coo_val[base] = scratch[e * 32 + lane] * scale_down * scale_down;
+                p.coo_val[base] = scratch[e * 32 + lane] * sd2;
               }
               ++base;
             }
@@ -350,12 +519,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        if (remote_arrive)
-          mbar_arrive_cluster(&tempty[buf], 0);
-        else
-          mbar_arrive(&tempty[buf]);
-      }
+      if (lane == 0) mbar_arrive(&tempty[buf]);
       if (++buf == 2) {
         buf = 0;
         tphase ^= 1;
@@ -364,8 +528,8 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     if (p.mode != 0) continue;
     // merge the two column halves of each row: half 1 publishes (values into its own
     // scratch, columns into the half-0 warp's), half 0 merges and emits.
-    float* pv = scratch_all + (4 + q) * kScratchFloats;
-    float* pc = scratch_all + q * kScratchFloats;
+    float* pv = scratch_all + (4 + ((q - kFirstEpiWarp) & 3)) * kScratchFloats;
+    float* pc = scratch_all + ((q - kFirstEpiWarp) & 3) * kScratchFloats;
     asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
     if (h == 1) {
 #pragma unroll
@@ -383,29 +547,21 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
         if (jx >= 0) top.merge_insert(fabsf(x), x, jx);
       }
       if (valid) {
-        if (p.C == 1) {
+        if (KIND == kSeed) {
+          p.thr_out[lr] = top.thr();  // t-th largest sampled magnitude (-1: fewer than t)
+        } else if (KIND == kPlain && p.C == 1) {
           // the list is full (t <= n-1 real columns scanned); emit in ascending column
-          const int64_t base = lr * t;
-#pragma unroll
-          for (int a = 0; a < MAXT; ++a) {
-            if (a < t) {
-              int rank = 0;
-#pragma unroll
-              for (int b = 0; b < MAXT; ++b)
-                if (b < t && top.idx[b] < top.idx[a]) ++rank;
-              p.col[base + rank] = top.idx[a];
-              p.val[base + rank] = top.sval[a] * scale_down * scale_down;
-            }
-          }
-          p.row_ptr[lr] = base;
-          if (lr == p.rows - 1) p.row_ptr[p.rows] = base + t;
+          top.emit_sorted(t, p.col + lr * t, p.val + lr * t, sd2);
+          p.row_ptr[lr] = lr * t;
+          if (lr == p.rows - 1) p.row_ptr[p.rows] = p.rows * t;
         } else {
+          const int cc = KIND == kPlain ? u % p.C : 0;
           const int64_t base = ((int64_t)cc * p.rows + lr) * t;
 #pragma unroll
           for (int a = 0; a < MAXT; ++a) {
             if (a < t) {
               p.pcol[base + a] = top.idx[a];
-              p.pval[base + a] = top.sval[a] * scale_down * scale_down;
+              p.pval[base + a] = top.sval[a] * sd2;
             }
           }
         }
@@ -415,7 +571,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
   }
 }
 
-template <int MAXT>
+template <int MAXT, int KIND>
 __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -438,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int units = p.RB * p.C;
+  const int units = KIND == kPlain ? p.RB * p.C : p.RB;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -453,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
     mbar_init(aempty, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 0) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -471,8 +627,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
       uint32_t phase = 0;
       int a_iter = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int rb = u / p.C, cc = u % p.C;
-        const int j0 = cc * p.TPC, j1 = min(p.NT, j0 + p.TPC);
+        int rb;
+        const int ntiles = unit_tiles<KIND>(p, u, rb);
         const uint8_t* Ablk = p.A + (size_t)rb * bb;
         if (resident) {
           if (a_iter > 0) mbar_wait(aempty, (a_iter - 1) & 1);
@@ -480,9 +636,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
           bulk_g2s(sA, Ablk, (uint32_t)bb, afull, pol_a);
           ++a_iter;
         }
-        for (int j = j0; j < j1; ++j) {
-          const uint8_t* B0 = p.B + (size_t)(2 * j) * bb;
-          const uint8_t* B1 = B0 + bb;
+        for (int s = 0; s < ntiles; ++s) {
+          const TileRef tr = tile_ref<KIND>(p, u, rb, s);
+          const uint8_t* B0 = p.B + (size_t)tr.K0 * bb;
+          const uint8_t* B1 = p.B + (size_t)tr.K1 * bb;
           for (int a = 0; a < KA; ++a) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* st = sStage + stage * st_bytes;
@@ -494,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
                        &full[stage], pol_a);
               sb = st + 2 * kAtomBytes;
             }
-            // B hi (rows 0-127 | 128-255), then B lo: 256 rows per atom, uniform 1 KB SBO
+            // B hi (block K0 | block K1), then B lo: 256 rows per atom, uniform 1 KB SBO
             bulk_g2s(sb, B0 + (size_t)a * kAtomBytes, kAtomBytes, &full[stage], pol_b);
             bulk_g2s(sb + kAtomBytes, B1 + (size_t)a * kAtomBytes, kAtomBytes, &full[stage],
                      pol_b);
@@ -520,13 +677,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
       uint32_t tphase = 0;
       int a_iter = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int cc = u % p.C;
-        const int j0 = cc * p.TPC, j1 = min(p.NT, j0 + p.TPC);
+        int rb;
+        const int ntiles = unit_tiles<KIND>(p, u, rb);
         if (resident) {
           mbar_wait(afull, a_iter & 1);
           tc_fence_after();
         }
-        for (int j = j0; j < j1; ++j) {
+        for (int s = 0; s < ntiles; ++s) {
           mbar_wait(&tempty[buf], tphase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(buf * kTileN);
@@ -568,211 +725,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
         }
       }
     }
-  } else if (warp >= 4) {
-    epilogue_role<MAXT>(p, tmem_base, tfull, tempty, blockIdx.x, gridDim.x, units,
-                        kRowsPerBlock, 0, false, warp, lane, scratch);
+  } else if (warp >= kFirstEpiWarp) {
+    epilogue_role<MAXT, KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
   }
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
-  }
-}
-
-
-// ------------------------------------------------------------------ BK2, CTA-pair variant
-// Two CTAs of a cluster (one TPC) run one tcgen05.mma.cta_group::2 pipeline: M = 256 rows
-// (128 per CTA, accumulators in each CTA's TMEM), N = 256 columns with each CTA holding HALF
-// of the B tile (128 rows) in its shared memory, so per-CTA operand traffic and smem
-// footprint halve and the pipeline can be 4 stages deep.  The leader (cluster rank 0) issues
-// the MMAs; both CTAs' producers load with tensor-map TMA crediting the leader's full
-// barriers; tcgen05.commit multicasts stage/accumulator releases to both CTAs; the peer's
-// epilogue releases TMEM buffers by remote mbarrier arrival on the leader.
-constexpr int kPairStagesResident = 4;
-constexpr int kPairStagesStreaming = 3;
-
-__host__ __device__ inline size_t pair_stage_bytes(int resident) {
-  return (resident ? 0 : (size_t)2 * kAtomBytes) + (size_t)2 * kAtomBytes;
-}
-__host__ __device__ inline int pair_stages(int resident) {
-  return resident ? kPairStagesResident : kPairStagesStreaming;
-}
-__host__ inline size_t pair_smem_bytes(int KA, int resident) {
-  size_t a = resident ? block_bytes(KA) : 0;
-  return 1024 + a + pair_stages(resident) * pair_stage_bytes(resident) + 256 +
-         kEpiWarps * kScratchFloats * sizeof(float);
-}
-
-template <int MAXT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    fused_recon_topk_pair(const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmB, const FusedParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  const int KA = p.KA;
-  const int resident = p.resident;
-  const int S = pair_stages(resident);
-  const size_t a_bytes = resident ? block_bytes(KA) : 0;
-  const size_t st_bytes = pair_stage_bytes(resident);
-  uint8_t* sA = smem;
-  uint8_t* sStage = smem + a_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + S * st_bytes);
-  uint64_t* full = bars;            // [S]  (leader's are used)
-  uint64_t* empty = bars + 4;       // [S]  (both CTAs)
-  uint64_t* tfull = bars + 8;       // [2]  (both CTAs)
-  uint64_t* tempty = bars + 10;     // [2]  (leader's are used; 8 arrivals)
-  uint64_t* afull = bars + 12;      // leader's used
-  uint64_t* aempty = bars + 13;     // both
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-  float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
-  const int units = p.RB * p.C;  // RB counts 256-row pair blocks here
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 2 * kEpiWarps);
-    }
-    mbar_init(afull, 1);
-    mbar_init(aempty, 1);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const bool skip = p.sc->flags != 0;
-
-  if (!skip && warp == 0) {
-    // ===================== producers (both CTAs): tensor-map TMA into own smem =========
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
-      const uint64_t pol_b = policy_evict_last();
-      const uint64_t pol_a = policy_evict_first();
-      const int lines_per_block = 2 * KA * kRowsPerBlock;  // 128-byte lines per 128-row block
-      int stage = 0;
-      uint32_t phase = 0;
-      int a_iter = 0;
-      for (int u = pair; u < units; u += npairs) {
-        const int rb2 = u / p.C, cc = u % p.C;
-        const int j0 = cc * p.TPC, j1 = min(p.NT, j0 + p.TPC);
-        const int ablk = rb2 * 2 + (int)rank;  // this CTA's 128 rows of the pair block
-        const int aline = ablk * lines_per_block;
-        if (resident) {
-          if (a_iter > 0) mbar_wait(aempty, (a_iter - 1) & 1);
-          if (rank == 0) mbar_arrive_expect_tx(afull, (uint32_t)(2 * block_bytes(KA)));
-          for (int a = 0; a < 2 * KA; ++a)
-            tma_load_2d_pair(sA + (size_t)a * kAtomBytes, &tmA, 0, aline + a * kRowsPerBlock,
-                             afull, pol_a);
-          ++a_iter;
-        }
-        for (int j = j0; j < j1; ++j) {
-          const int bline = (2 * j + (int)rank) * lines_per_block;  // this CTA's half of B
-          for (int a = 0; a < KA; ++a) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], (uint32_t)(2 * st_bytes));
-            uint8_t* st = sStage + stage * st_bytes;
-            uint8_t* sb = st;
-            if (!resident) {
-              tma_load_2d_pair(st, &tmA, 0, aline + a * kRowsPerBlock, &full[stage], pol_a);
-              tma_load_2d_pair(st + kAtomBytes, &tmA, 0, aline + (KA + a) * kRowsPerBlock,
-                               &full[stage], pol_a);
-              sb = st + 2 * kAtomBytes;
-            }
-            tma_load_2d_pair(sb, &tmB, 0, bline + a * kRowsPerBlock, &full[stage], pol_b);
-            tma_load_2d_pair(sb + kAtomBytes, &tmB, 0, bline + (KA + a) * kRowsPerBlock,
-                             &full[stage], pol_b);
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
-      }
-    }
-  } else if (!skip && warp == 1) {
-    // ===================== MMA issuer (leader CTA only) ================================
-    if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32(2 * kRowsPerBlock, kTileN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int buf = 0;
-      uint32_t tphase = 0;
-      int a_iter = 0;
-      for (int u = pair; u < units; u += npairs) {
-        const int cc = u % p.C;
-        const int j0 = cc * p.TPC, j1 = min(p.NT, j0 + p.TPC);
-        if (resident) {
-          mbar_wait(afull, a_iter & 1);
-          tc_fence_after();
-        }
-        for (int j = j0; j < j1; ++j) {
-          mbar_wait(&tempty[buf], tphase ^ 1);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem_base + (uint32_t)(buf * kTileN);
-          for (int a = 0; a < KA; ++a) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            uint8_t* st = sStage + stage * st_bytes;
-            const uint8_t* aHi = resident ? sA + (size_t)a * kAtomBytes : st;
-            const uint8_t* aLo = resident ? sA + (size_t)(KA + a) * kAtomBytes : st + kAtomBytes;
-            const uint8_t* bHi = resident ? st : st + 2 * kAtomBytes;
-            const uint8_t* bLo = bHi + kAtomBytes;
-            const uint32_t aHi_s = smem_u32(aHi), aLo_s = smem_u32(aLo);
-            const uint32_t bHi_s = smem_u32(bHi), bLo_s = smem_u32(bLo);
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              if (a * 4 + ks < p.KS) {
-                const uint32_t off = ks * 32;
-                const uint32_t acc = (a | ks) ? 1u : 0u;
-                mma_f16_ss_pair(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc,
-                                acc);
-                mma_f16_ss_pair(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc,
-                                1u);
-                mma_f16_ss_pair(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc,
-                                1u);
-              }
-            }
-            mma_commit_pair(&empty[stage]);
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          mma_commit_pair(&tfull[buf]);
-          if (++buf == 2) {
-            buf = 0;
-            tphase ^= 1;
-          }
-        }
-        if (resident) {
-          mma_commit_pair(aempty);
-          ++a_iter;
-        }
-      }
-    }
-  } else if (!skip && warp >= 4) {
-    epilogue_role<MAXT>(p, tmem_base, tfull, tempty, pair, npairs, units, 2 * kRowsPerBlock,
-                        (int)rank * kRowsPerBlock, rank != 0, warp, lane, scratch);
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem_base, kTmemCols);
   }
 }
 
@@ -783,59 +742,70 @@ __global__ void merge_partials(const int32_t* __restrict__ pcol, const float* __
                                float* val) {
   const int64_t lr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (lr >= rows) return;
-  float mag[MAXT], sv[MAXT];
-  int id[MAXT];
-#pragma unroll
-  for (int a = 0; a < MAXT; ++a) {
-    mag[a] = -1.f;
-    sv[a] = 0.f;
-    id[a] = INT_MAX;
-  }
+  TopList<MAXT> top;
+  top.init(t);
   for (int c = 0; c < C; ++c) {
     const int64_t base = ((int64_t)c * rows + lr) * t;
     for (int e = 0; e < t; ++e) {
       const int j = pcol[base + e];
       if (j < 0) continue;
       const float v = pval[base + e];
-      const float a = fabsf(v);
-      // insert by (|v| desc, j asc)
-#pragma unroll
-      for (int s = MAXT - 1; s >= 1; --s) {
-        if (s < t) {
-          const bool before_prev = a > mag[s - 1] || (a == mag[s - 1] && j < id[s - 1]);
-          const bool before_cur = a > mag[s] || (a == mag[s] && j < id[s]);
-          if (before_prev) {
-            mag[s] = mag[s - 1];
-            sv[s] = sv[s - 1];
-            id[s] = id[s - 1];
-          } else if (before_cur) {
-            mag[s] = a;
-            sv[s] = v;
-            id[s] = j;
-          }
-        }
-      }
-      if (a > mag[0] || (a == mag[0] && j < id[0])) {
-        mag[0] = a;
-        sv[0] = v;
-        id[0] = j;
-      }
+      top.merge_insert(fabsf(v), v, j);
     }
   }
-  const int64_t base = lr * t;
-#pragma unroll
-  for (int a = 0; a < MAXT; ++a) {
-    if (a < t) {
-      int rank = 0;
-#pragma unroll
-      for (int b = 0; b < MAXT; ++b)
-        if (b < t && id[b] < id[a]) ++rank;
-      col[base + rank] = id[a];
-      val[base + rank] = sv[a];
+  top.emit_sorted(t, col + lr * t, val + lr * t, 1.f);
+  row_ptr[lr] = lr * t;
+  if (lr == rows - 1) row_ptr[rows] = rows * t;
+}
+
+// ------------------------------------------------------------------ BK3 (kSym)
+// Row j's final list = top-t of (its row-direction list over its own cyclic window) ∪
+// (the transposed-direction candidates other blocks emitted for it; sorted by target row,
+// the row's range found by binary search).
+__device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n, uint32_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <int MAXT>
+__global__ void merge_sym(const int32_t* __restrict__ pcol, const float* __restrict__ pval,
+                          const uint32_t* __restrict__ key, const uint2* __restrict__ cv,
+                          int64_t ncand, int64_t n, int t, int64_t* row_ptr, int32_t* col,
+                          float* val) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  TopList<MAXT> top;
+  top.init(t);
+  for (int e = 0; e < t; ++e) {
+    const int c = pcol[j * t + e];
+    if (c >= 0) {
+      const float v = pval[j * t + e];
+      top.merge_insert(fabsf(v), v, c);
     }
   }
-  row_ptr[lr] = base;
-  if (lr == rows - 1) row_ptr[rows] = base + t;
+  const int64_t b0 = lower_bound_u32(key, ncand, (uint32_t)j);
+  const int64_t b1 = lower_bound_u32(key, ncand, (uint32_t)j + 1u);
+  for (int64_t e = b0; e < b1; ++e) {
+    const uint2 x = cv[e];
+    const float v = __uint_as_float(x.y);
+    top.merge_insert(fabsf(v), v, (int)x.x);
+  }
+  top.emit_sorted(t, col + j * t, val + j * t, 1.f);
+  row_ptr[j] = j * t;
+  if (j == n - 1) row_ptr[n] = n * t;
+}
+
+__global__ void fill_f32(float* p, int64_t count, float v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
 }
 
 // ------------------------------------------------------------------ BK3 (mode 1)
@@ -861,13 +831,18 @@ __global__ void zero_row_ptr(int64_t* row_ptr, int64_t rows) {
 }
 
 // ------------------------------------------------------------------ host plan
+
 struct Plan {
   int64_t n, rows, row_begin;
-  int k, KA, KS, t, mode, resident, alias, pair;
+  int k, KA, KS, t, mode, resident, alias;
   int64_t RB, NT, C, TPC;
   int64_t nBblocks, nAblocks;
   int64_t capacity;
   size_t coo_temp_bytes;
+  int sym;       // symmetric scheme (kSeed + kSym + merge_sym)
+  int64_t NB;    // 128-row blocks of the axis
+  int64_t cand_total;  // kSym: candidate pool capacity (entries)
+  size_t sort_temp_bytes;
 };
 
 static int choose_chunks(int64_t RB, int64_t NT, int sms) {
@@ -905,28 +880,41 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   if (o->mode == 1 && !(o->tau >= 0.f && std::isfinite(o->tau)))
     return fail(GGM_ERR_INVALID_ARGUMENT, "tau must be finite and >= 0");
   if (o->col_chunks < 0) return fail(GGM_ERR_INVALID_ARGUMENT, "col_chunks < 0");
+  if (o->symmetric < 0 || o->symmetric > 2)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "symmetric=%d not in {0,1,2}", o->symmetric);
   pl->n = n;
   pl->k = k;
   pl->row_begin = row_begin;
   pl->rows = row_end - row_begin;
   pl->mode = o->mode;
-  pl->t = (int)std::min<int64_t>(o->topk, n - 1);
+  pl->t = (int)std::max<int64_t>(1, std::min<int64_t>(o->topk, n - 1));
   pl->KA = (k + kAtomElems - 1) / kAtomElems;
   pl->KS = (k + 15) / 16;
   pl->resident = pl->KA <= kMaxResidentAtoms ? 1 : 0;
-  // 1-CTA kernel by default (faster end to end); GGM_PAIR=1 selects the
-  // CTA-pair (cta_group::2) kernel, which has the faster MMA pipeline but couples the two
-  // CTAs' epilogues.
-  const char* env = getenv("GGM_PAIR");
-  pl->pair = (env && env[0] == '1') ? 1 : 0;
-  const int rows_per_unit = pl->pair ? 2 * kRowsPerBlock : kRowsPerBlock;
-  pl->alias = (row_begin % rows_per_unit) == 0 ? 1 : 0;
+  pl->alias = (row_begin % kRowsPerBlock) == 0 ? 1 : 0;
   pl->NT = (n + kTileN - 1) / kTileN;
-  pl->RB = (pl->rows + rows_per_unit - 1) / rows_per_unit;
+  pl->RB = (pl->rows + kRowsPerBlock - 1) / kRowsPerBlock;
   pl->nBblocks = pl->NT * 2;
-  pl->nAblocks = pl->alias ? 0 : pl->RB * (rows_per_unit / kRowsPerBlock);
-  const int sms = pl->pair ? num_sms() / 2 : num_sms();
-  int64_t C = o->col_chunks > 0 ? o->col_chunks : (pl->mode == 0 ? choose_chunks(pl->RB, pl->NT, sms) : 1);
+  pl->nAblocks = pl->alias ? 0 : pl->RB;
+  pl->NB = (n + kRowsPerBlock - 1) / kRowsPerBlock;
+  const int sms = num_sms();
+  const bool full_axis = row_begin == 0 && row_end == n;
+  // automatic selection keeps the plain scheme: on B200 the symmetric scheme halves the MMA
+  // work but its transposed-direction epilogue costs about what it saves
+  pl->sym = (o->mode == 0 && o->symmetric == 1 && full_axis && pl->resident) ? 1 : 0;
+  // candidates: ~ t x 16 / 2 per row expected (seed samples 1/16 of the columns, half of
+  // each row's columns come from the transposed direction); regions hold 2x that on average
+  // pool: 2x the expected candidates + one chunk per epilogue warp of partially used space
+  pl->cand_total = pl->sym ? n * 16 * pl->t + (int64_t)sms * kEpiWarps * kCandChunk * 2 : 0;
+  pl->sort_temp_bytes = 0;
+  if (pl->sym) {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint2*)nullptr, (uint2*)nullptr, pl->cand_total);
+    pl->sort_temp_bytes = tb;
+  }
+  int64_t C = o->col_chunks > 0 ? o->col_chunks
+                                : (pl->mode == 0 ? choose_chunks(pl->RB, pl->NT, sms) : 1);
   C = std::max<int64_t>(1, std::min<int64_t>(C, pl->NT));
   pl->TPC = (pl->NT + C - 1) / C;
   pl->C = (pl->NT + pl->TPC - 1) / pl->TPC;  // no empty chunks
@@ -952,6 +940,12 @@ struct Work {
   float* cv_in;
   float* cv_out;
   void* cub_tmp;
+  float* thr;          // kSym: [NB*128]
+  uint32_t* ckey;      // kSym: candidate pool
+  uint2* cval;
+  uint32_t* skey;      // kSym: sorted by target row
+  uint2* sval;
+  void* sort_tmp;
 };
 
 static size_t carve(const Plan& pl, void* ws, Work* w) {
@@ -959,7 +953,8 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->sc = cv.take<DevScalars>(1);
   w->Bop = cv.take<uint8_t>((size_t)pl.nBblocks * block_bytes(pl.KA));
   w->Aop = cv.take<uint8_t>((size_t)pl.nAblocks * block_bytes(pl.KA));
-  const size_t npart = (pl.mode == 0 && pl.C > 1) ? (size_t)pl.C * pl.rows * pl.t : 0;
+  size_t npart = (pl.mode == 0 && pl.C > 1) ? (size_t)pl.C * pl.rows * pl.t : 0;
+  if (pl.sym) npart = std::max(npart, (size_t)pl.n * pl.t);
   w->pcol = cv.take<int32_t>(npart);
   w->pval = cv.take<float>(npart);
   const size_t ncoo = pl.mode == 1 ? (size_t)std::max<int64_t>(pl.capacity, 0) : 0;
@@ -968,6 +963,14 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->cv_in = cv.take<float>(ncoo);
   w->cv_out = cv.take<float>(ncoo);
   w->cub_tmp = cv.take<char>(pl.coo_temp_bytes);
+  const size_t nb = pl.sym ? (size_t)pl.NB : 0;
+  const size_t ct = pl.sym ? (size_t)pl.cand_total : 0;
+  w->thr = cv.take<float>(nb * kRowsPerBlock);
+  w->ckey = cv.take<uint32_t>(ct);
+  w->cval = cv.take<uint2>(ct);
+  w->skey = cv.take<uint32_t>(ct);
+  w->sval = cv.take<uint2>(ct);
+  w->sort_tmp = cv.take<char>(pl.sort_temp_bytes);
   return cv.used();
 }
 
@@ -994,56 +997,52 @@ struct EventTimer {
   }
 };
 
-template <int MAXT>
-static cudaError_t launch_fused(const FusedParams& fp, size_t smem, int grid, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(fused_recon_topk<MAXT>,
+template <int MAXT, int KIND>
+static cudaError_t launch_fused_k(const FusedParams& fp, size_t smem, int grid, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(fused_recon_topk<MAXT, KIND>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fused_recon_topk<MAXT><<<grid, kThreads, smem, st>>>(fp);
+  fused_recon_topk<MAXT, KIND><<<grid, kThreads, smem, st>>>(fp);
   return cudaGetLastError();
 }
+template <int MAXT>
+static cudaError_t launch_fused_t(const FusedParams& fp, size_t smem, int grid, cudaStream_t st) {
+  return fp.kind == kPlain  ? launch_fused_k<MAXT, kPlain>(fp, smem, grid, st)
+         : fp.kind == kSeed ? launch_fused_k<MAXT, kSeed>(fp, smem, grid, st)
+                            : launch_fused_k<MAXT, kSym>(fp, smem, grid, st);
+}
 
-
-// 2-D tensor map over a tiled operand array viewed as lines of 128 bytes (64 x uint16):
-// box = 128 lines = one 16 KB (128-row block, K atom) chunk, no swizzle (the data is already
-// stored in the SWIZZLE_128B canonical layout by split_tile).
-static ggm_status make_line_tmap(CUtensorMap* tm, const void* base, uint64_t lines) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return fail(GGM_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  cuuint64_t dims[2] = {64, (cuuint64_t)std::max<uint64_t>(lines, 128)};
-  cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {64, 128};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides,
-                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(GGM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return GGM_OK;
+static cudaError_t launch_fused(const FusedParams& fp, int t, cudaStream_t s) {
+  const size_t smem = fused_smem_bytes(fp.KA, fp.resident);
+  const int units = fp.kind == kPlain ? fp.RB * fp.C : fp.RB;
+  const int grid = std::max(1, std::min(num_sms(), units));
+  count_launches(1);
+  return t <= 5    ? launch_fused_t<5>(fp, smem, grid, s)
+         : t <= 10 ? launch_fused_t<10>(fp, smem, grid, s)
+         : t <= 16 ? launch_fused_t<16>(fp, smem, grid, s)
+                   : launch_fused_t<32>(fp, smem, grid, s);
 }
 
 template <int MAXT>
-static cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB,
-                               const FusedParams& fp, size_t smem, int grid, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(fused_recon_topk_pair<MAXT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  fused_recon_topk_pair<MAXT><<<grid, kThreads, smem, st>>>(tmA, tmB, fp);
-  return cudaGetLastError();
+static void launch_merge_sym_t(const Work& w, const Plan& pl, int64_t ncand, int64_t* row_ptr,
+                               int32_t* col, float* val, cudaStream_t s) {
+  const int threads = 128;
+  const int blocks = (int)((pl.n + threads - 1) / threads);
+  merge_sym<MAXT><<<blocks, threads, 0, s>>>(w.pcol, w.pval, w.skey, w.sval, ncand, pl.n, pl.t,
+                                             row_ptr, col, val);
 }
+
+static thread_local double g_stats[4] = {0, 0, 0, 0};
 
 }  // namespace sp
 }  // namespace ggm
 
 using namespace ggm;
 using namespace ggm::sp;
+
+extern "C" void ggm_last_stats(double out[4]) {
+  for (int i = 0; i < 4; ++i) out[i] = g_stats[i];
+}
 
 extern "C" ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t row_begin,
                                                      int64_t row_end,
@@ -1056,6 +1055,32 @@ extern "C" ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t r
   Work w;
   *bytes = carve(pl, nullptr, &w);
   return GGM_OK;
+}
+
+static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t row_begin) {
+  FusedParams fp{};
+  fp.B = w.Bop;
+  fp.A = pl.alias ? w.Bop + (size_t)(row_begin / kRowsPerBlock) * block_bytes(pl.KA) : w.Aop;
+  fp.KA = pl.KA;
+  fp.KS = pl.KS;
+  fp.resident = pl.resident;
+  fp.n = n;
+  fp.row_begin = row_begin;
+  fp.rows = pl.rows;
+  fp.kind = kPlain;
+  fp.RB = (int)pl.RB;
+  fp.NT = (int)pl.NT;
+  fp.C = (int)pl.C;
+  fp.TPC = (int)pl.TPC;
+  fp.NB = (int)pl.NB;
+  fp.mode = pl.mode;
+  fp.t = pl.t;
+  fp.sc = w.sc;
+  fp.pcol = w.pcol;
+  fp.pval = w.pval;
+  const char* d = getenv("GGM_DEBUG_EPI");
+  fp.dbg = d ? atoi(d) : 0;
+  return fp;
 }
 
 extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, const double* lambda,
@@ -1085,6 +1110,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   reset_launches();
+  for (double& x : g_stats) x = 0.0;
   EventTimer tm(timing_enabled(), s);
   tm.mark(0);
   GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
@@ -1094,84 +1120,143 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 8));
     absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
     scale_finalize<<<1, 1, 0, s>>>(w.sc);
-    count_launches(pl.alias ? 3 : 4);
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 8;
     split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
         V, lambda, n, k, pl.KA, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
+    count_launches(3);
     if (!pl.alias) {
       const int64_t totA = (int64_t)pl.nAblocks * kRowsPerBlock * pl.KA * 8;  // rows padded
       split_tile<<<(int)std::min<int64_t>((totA + 255) / 256, sms * 16), 256, 0, s>>>(
           V, lambda, n, k, pl.KA, row_begin, (int64_t)pl.nAblocks * kRowsPerBlock, w.sc, w.Aop);
+      count_launches(1);
     }
     GGM_CUDA_TRY(cudaGetLastError());
   }
-  tm.mark(1);
-  FusedParams fp{};
-  fp.B = w.Bop;
-  fp.A = pl.alias ? w.Bop + (size_t)(row_begin / kRowsPerBlock) * block_bytes(pl.KA) : w.Aop;
-  fp.KA = pl.KA;
-  fp.KS = pl.KS;
-  fp.resident = pl.resident;
-  fp.n = n;
-  fp.row_begin = row_begin;
-  fp.rows = pl.rows;
-  fp.RB = (int)pl.RB;
-  fp.NT = (int)pl.NT;
-  fp.C = (int)pl.C;
-  fp.TPC = (int)pl.TPC;
-  fp.mode = pl.mode;
-  fp.t = pl.t;
-  fp.tau = pl.mode == 1 ? opts->tau : 0.f;
-  fp.sc = w.sc;
+  FusedParams fp = base_params(pl, w, n, row_begin);
+  cudaError_t ce;
+  if (pl.sym) {
+    // seed: per-row t-th largest |ψ| over every 16th column tile (a lower bound of the
+    // row's true t-th magnitude), padded rows +inf
+    const int64_t nthr = pl.NB * kRowsPerBlock;
+    fill_f32<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, nthr,
+                                                                               INFINITY);
+    count_launches(1);
+    GGM_CUDA_TRY(cudaMemsetAsync(w.ckey, 0xFF, sizeof(uint32_t) * pl.cand_total, s));
+    FusedParams sp = fp;
+    sp.kind = kSeed;
+    sp.RB = (int)pl.NB;
+    sp.thr_out = w.thr;
+    ce = launch_fused(sp, pl.t, s);
+    if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "seed launch: %s", cudaGetErrorString(ce));
+    tm.mark(1);
+    fp.kind = kSym;
+    fp.RB = (int)pl.NB;
+    fp.thr = w.thr;
+    fp.cand_key = w.ckey;
+    fp.cand_val = w.cval;
+    fp.cand_total = pl.cand_total;
+    ce = launch_fused(fp, pl.t, s);
+    if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "sym launch: %s", cudaGetErrorString(ce));
+    tm.mark(2);
+    // sort the candidate pool by target row (unused slots carry UINT32_MAX -> sorted last)
+    DevScalars hs;
+    GGM_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
+    if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
+    const int hovf = hs.cand_overflow;
+    if (hovf) {
+      // a candidate region filled up: recompute the whole axis with the plain scheme (exact)
+      Plan bp = pl;
+      bp.sym = 0;
+      FusedParams op = base_params(bp, w, n, 0);
+      op.row_ptr = row_ptr;
+      if (pl.C == 1) {
+        op.col = col;
+        op.val = val;
+      }
+      ce = launch_fused(op, pl.t, s);
+      if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "fallback launch: %s", cudaGetErrorString(ce));
+      if (pl.C > 1) {
+        const int blocks = (int)((pl.rows + 127) / 128);
+        if (pl.t <= 5)
+          merge_partials<5><<<blocks, 128, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t, row_ptr, col, val);
+        else if (pl.t <= 10)
+          merge_partials<10><<<blocks, 128, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t, row_ptr, col, val);
+        else if (pl.t <= 16)
+          merge_partials<16><<<blocks, 128, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t, row_ptr, col, val);
+        else
+          merge_partials<32><<<blocks, 128, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t, row_ptr, col, val);
+        count_launches(1);
+      }
+      tm.mark(3);
+      GGM_CUDA_TRY(cudaStreamSynchronize(s));
+      tm.finish();
+      g_stats[0] = 0;
+      g_stats[1] = (double)pl.RB * kRowsPerBlock * pl.NT * kTileN;
+      g_stats[3] = 1;
+      *nnz_out = pl.rows * pl.t;
+      return GGM_OK;
+    }
+    const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
+    if (ncand > 0) {
+      size_t tb = pl.sort_temp_bytes;
+      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
+                                                   ncand, 0, 32, s));
+    }
+    if (pl.t <= 5)
+      launch_merge_sym_t<5>(w, pl, ncand, row_ptr, col, val, s);
+    else if (pl.t <= 10)
+      launch_merge_sym_t<10>(w, pl, ncand, row_ptr, col, val, s);
+    else if (pl.t <= 16)
+      launch_merge_sym_t<16>(w, pl, ncand, row_ptr, col, val, s);
+    else
+      launch_merge_sym_t<32>(w, pl, ncand, row_ptr, col, val, s);
+    count_launches(1);
+    GGM_CUDA_TRY(cudaGetLastError());
+    tm.mark(3);
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    tm.finish();
+    double evaluated = 0.0;  // entries evaluated by the symmetric pass (incl. masked halves)
+    for (int64_t b = 0; b < pl.NB; ++b) {
+      const int64_t W = (pl.NB & 1) ? (pl.NB + 1) / 2 : pl.NB / 2 + (b < pl.NB / 2 ? 1 : 0);
+      evaluated += (double)((W + 1) / 2) * kRowsPerBlock * kTileN;
+    }
+    g_stats[0] = 2;
+    g_stats[1] = evaluated;
+    g_stats[2] = (double)ncand;
+    g_stats[3] = 0;
+    *nnz_out = pl.rows * pl.t;
+    return GGM_OK;
+  }
   fp.row_ptr = row_ptr;
   fp.col = (pl.mode == 0 && pl.C == 1) ? col : nullptr;
   fp.val = (pl.mode == 0 && pl.C == 1) ? val : nullptr;
-  fp.pcol = w.pcol;
-  fp.pval = w.pval;
+  fp.tau = pl.mode == 1 ? opts->tau : 0.f;
   fp.coo_key = w.key_in;
   fp.coo_val = w.cv_in;
   fp.coo_count = &w.sc->coo_count;
   fp.capacity = pl.mode == 1 ? capacity : 0;
-  {
-    const char* d = getenv("GGM_DEBUG_EPI");
-    fp.dbg = d ? atoi(d) : 0;
-  }
-  cudaError_t ce;
-  if (pl.pair) {
-    const int lines_per_block = 2 * pl.KA * kRowsPerBlock;
-    CUtensorMap tmA, tmB;
-    const uint64_t linesB = (uint64_t)pl.nBblocks * lines_per_block;
-    const uint64_t linesA = pl.alias ? linesB - (uint64_t)(row_begin / kRowsPerBlock) * lines_per_block
-                                     : (uint64_t)pl.nAblocks * lines_per_block;
-    ggm_status ts = make_line_tmap(&tmB, w.Bop, linesB);
-    if (ts == GGM_OK) ts = make_line_tmap(&tmA, fp.A, linesA);
-    if (ts != GGM_OK) return ts;
-    const size_t smem = pair_smem_bytes(pl.KA, pl.resident);
-    const int pairs = (int)std::min<int64_t>(sms / 2, pl.RB * pl.C);
-    const int g2 = 2 * pairs;
-    ce = pl.t <= 5    ? launch_pair<5>(tmA, tmB, fp, smem, g2, s)
-         : pl.t <= 10 ? launch_pair<10>(tmA, tmB, fp, smem, g2, s)
-         : pl.t <= 16 ? launch_pair<16>(tmA, tmB, fp, smem, g2, s)
-                      : launch_pair<32>(tmA, tmB, fp, smem, g2, s);
-  } else {
-    const size_t smem = fused_smem_bytes(pl.KA, pl.resident);
-    const int grid = (int)std::min<int64_t>(sms, pl.RB * pl.C);
-    ce = pl.t <= 5    ? launch_fused<5>(fp, smem, grid, s)
-         : pl.t <= 10 ? launch_fused<10>(fp, smem, grid, s)
-         : pl.t <= 16 ? launch_fused<16>(fp, smem, grid, s)
-                      : launch_fused<32>(fp, smem, grid, s);
-  }
+  tm.mark(1);
+  ce = launch_fused(fp, pl.t, s);
   if (ce != cudaSuccess)
     return fail(GGM_ERR_CUDA, "fused_recon_topk launch: %s", cudaGetErrorString(ce));
-  count_launches(1);
   tm.mark(2);
+  g_stats[0] = 0;
+  g_stats[1] = (double)pl.RB * kRowsPerBlock * pl.NT * kTileN;
 
   DevScalars hs;
   if (pl.mode == 0) {
     if (pl.C > 1) {
       const int threads = 128;
       const int blocks = (int)((pl.rows + threads - 1) / threads);
-      if (pl.t <= 16)
+      if (pl.t <= 5)
+        merge_partials<5><<<blocks, threads, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t,
+                                                     row_ptr, col, val);
+      else if (pl.t <= 10)
+        merge_partials<10><<<blocks, threads, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t,
+                                                      row_ptr, col, val);
+      else if (pl.t <= 16)
         merge_partials<16><<<blocks, threads, 0, s>>>(w.pcol, w.pval, pl.rows, (int)pl.C, pl.t,
                                                       row_ptr, col, val);
       else

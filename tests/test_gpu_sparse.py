@@ -29,8 +29,9 @@ def _run(G, V, lam, row_begin=0, row_end=None, **kw):
 @pytest.mark.parametrize("n,k,t", [(1000, 64, 10), (777, 37, 5), (2053, 100, 10),
                                    (300, 16, 32), (257, 1, 3), (2, 1, 10), (129, 128, 16)])
 def test_topk_full_rows(G, n, k, t):
+    """Plain scheme (symmetric=2) over the full axis."""
     V, lam = gen.small_factor(n + k + t, n, k)
-    rp, c, v = _run(G, V, lam, 0, n, mode=0, topk=t)
+    rp, c, v = _run(G, V, lam, 0, n, mode=0, topk=t, symmetric=2)
     st = check_topk(rp, c, v, V, lam, np.arange(n), t)
     assert st["exact"] + st["excused"] == n
 
@@ -137,3 +138,26 @@ def test_permutation_equivariance_and_scaling(G):
         assert a == b
         assert list(c3[rp3[i]:rp3[i + 1]]) == list(c[rp[i]:rp[i + 1]])
         np.testing.assert_allclose(v3[rp3[i]:rp3[i + 1]], 4.0 * v[rp[i]:rp[i + 1]], rtol=1e-6)
+
+
+@pytest.mark.parametrize("n,k,t", [(100, 8, 5), (256, 16, 10), (300, 32, 10), (1000, 48, 10),
+                                   (2053, 100, 10), (9000, 64, 10), (20000, 100, 16),
+                                   (3000, 64, 3), (1500, 20, 32)])
+def test_symmetric_scheme_vs_oracle_and_plain(G, n, k, t):
+    """Symmetric half-evaluation (each unordered block pair once + seed-bounded transposed
+    candidates) gives the oracle's per-row top-t, and the plain scheme's sets."""
+    V, lam = gen.small_factor(n + 3 * k + t, n, k)
+    rp, c, v = _run(G, V, lam, 0, n, mode=0, topk=t, symmetric=1)
+    st = G.last_stats()
+    assert st["scheme"] == "symmetric"
+    rows = np.arange(n) if n <= 3000 else np.unique(
+        np.concatenate([np.arange(0, n, 7), [n - 1, n // 2]]))
+    prp = np.concatenate([[0], np.cumsum(rp[rows + 1] - rp[rows])])
+    pc = np.concatenate([c[rp[i]:rp[i + 1]] for i in rows])
+    pv = np.concatenate([v[rp[i]:rp[i + 1]] for i in rows])
+    res = check_topk(prp, pc, pv, V, lam, rows, t)
+    assert res["exact"] + res["excused"] == len(rows)
+    rp2, c2, v2 = _run(G, V, lam, 0, n, mode=0, topk=t, symmetric=2)
+    assert G.last_stats()["scheme"] == "plain"
+    same = np.mean([np.array_equal(c[rp[i]:rp[i + 1]], c2[rp2[i]:rp2[i + 1]]) for i in range(n)])
+    assert same > 0.999
