@@ -39,17 +39,19 @@ constexpr int kTileN = 256;               // N (columns of Ψ per tile; 2 operan
 constexpr int kAtomElems = 64;            // fp16 elements per 128-byte swizzle row
 constexpr int kAtomBytes = kRowsPerBlock * 128;  // one (128-row block, K atom) = 16 KB
 constexpr int kStages = 2;
-#ifndef GGM_THREADS
-#define GGM_THREADS 320
-#endif
-constexpr int kThreads = GGM_THREADS;     // producer(+TMEM alloc), MMA, [idle], 8 epilogue warps
-constexpr int kFirstEpiWarp = kThreads / 32 - 8;
+// 12 warps = 3 warpgroups: WG0 = producer (+TMEM alloc), MMA issuer, 2 idle warps, shrunk
+// to kRegsCtl registers; WG1-2 = 8 epilogue warps grown to kRegsEpi (setmaxnreg).  With 10
+// warps one SM sub-partition holds 3 warps and caps every thread at 168 registers.
+constexpr int kThreads = 384;
+constexpr int kFirstEpiWarp = 4;
+constexpr int kRegsCtl = 56;
+constexpr int kRegsEpi = 224;
 constexpr int kTmemCols = 512;            // 2 accumulator buffers x 256 columns
 constexpr int kMaxResidentAtoms = 2;
 // A (128 rows x KA atoms x hi/lo) stays resident in shared memory when KA <= 2 (k <= 128)
 constexpr int kEpiWarps = 8;              // epilogue warps (2 per TMEM lane quadrant)
 constexpr int kScratchFloats = 32 * 32;   // per epilogue warp: [32 values][32 lanes]
-constexpr int kSeedStride = 16;           // seed pass samples every 16th column tile
+constexpr int kSeedStride = 16;           // seed pass samples every 16th column tile (at most)
 
 __host__ __device__ inline size_t block_bytes(int KA) { return (size_t)2 * KA * kAtomBytes; }
 
@@ -117,7 +119,8 @@ __global__ void scale_finalize(DevScalars* sc) {
 // (the SWIZZLE_128B K-major canonical layout; SBO = 1024 B between 8-row groups).
 __global__ void split_tile(const float* __restrict__ V, const double* __restrict__ lam,
                            int64_t n, int k, int KA, int64_t row0, int64_t nrows_pad,
-                           const DevScalars* __restrict__ sc, uint8_t* __restrict__ dst) {
+                           const DevScalars* __restrict__ sc, uint8_t* __restrict__ dst,
+                           const int32_t* __restrict__ perm = nullptr) {
   const int chunks_per_row = KA * 8;
   const int64_t total = nrows_pad * chunks_per_row;
   const double s = ldexp(1.0, sc->exp2);
@@ -125,7 +128,8 @@ __global__ void split_tile(const float* __restrict__ V, const double* __restrict
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = idx / chunks_per_row;
     const int ch = (int)(idx % chunks_per_row);
-    const int64_t g = row0 + row;
+    int64_t g = row0 + row;
+    if (perm && g < n) g = perm[g];  // symmetric scheme: rows in threshold order
     __align__(16) __half hi[8];
     __align__(16) __half lo[8];
 #pragma unroll
@@ -162,6 +166,7 @@ struct FusedParams {
   int kind;          // Kind
   int RB, NT, C, TPC;
   int NB;            // kSym: 128-row blocks of the axis (row_begin == 0, rows == n)
+  int SS;            // kSeed: column-tile stride of the sample
   int mode, t;
   float tau;
   const DevScalars* sc;
@@ -175,7 +180,10 @@ struct FusedParams {
   unsigned long long* coo_count;
   int64_t capacity;
   float* thr_out;          // kSeed: per-row t-th largest sampled |ψ| (accumulator units)
-  const float* thr;        // kSym: per-column lower bound (accumulator units, +inf = none)
+  const float* thr;        // kSym: per-(permuted) column lower bound of that row's t-th
+                           //       magnitude (accumulator units, +inf = padding)
+  const float* thr_min;    // kSym: min of thr over each 32-column chunk
+  const int32_t* perm;     // kSym: permuted index -> original row/column id
   uint32_t* cand_key;      // kSym: candidate pool: target row j (UINT32_MAX = unused slot)
   uint2* cand_val;         //       (source row i, ψ bits)
   int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
@@ -211,8 +219,8 @@ __device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& rb) 
   }
   rb = u;
   if (KIND == kSeed) {
-    const int off = rb % kSeedStride;
-    return off < p.NT ? (p.NT - 1 - off) / kSeedStride + 1 : 0;
+    const int off = rb % p.SS;
+    return off < p.NT ? (p.NT - 1 - off) / p.SS + 1 : 0;
   }
   return (sym_window(rb, p.NB) + 1) / 2;
 }
@@ -232,12 +240,60 @@ __device__ __forceinline__ TileRef tile_ref(const FusedParams& p, int u, int rb,
     tr.K1 = tr.h1 ? (rb + (delta + 2 * s + 1) % W) % p.NB : tr.K0;
     return tr;
   }
-  const int j = KIND == kPlain ? (u % p.C) * p.TPC + s : rb % kSeedStride + s * kSeedStride;
+  const int j = KIND == kPlain ? (u % p.C) * p.TPC + s : rb % p.SS + s * p.SS;
   tr.K0 = 2 * j;
   tr.K1 = 2 * j + 1;
   tr.h1 = true;
   return tr;
 }
+
+// Incremental form of tile_ref (no integer division per tile): the producer, MMA and
+// epilogue roles walk the same sequence.
+template <int KIND>
+struct TileIter {
+  int K0, K1;
+  bool h1;
+  int s, rb, W, o;  // kSym: o = (delta + 2s) mod W
+  __device__ __forceinline__ void start(const FusedParams& p, int u, int rb_) {
+    rb = rb_;
+    s = 0;
+    if (KIND == kSym) {
+      const TileRef t0 = tile_ref<KIND>(p, u, rb, 0);
+      W = sym_window(rb, p.NB);
+      const int X = min(p.NB - 1, u - (int)blockIdx.x + (int)gridDim.x - 1);
+      int delta = (X - rb + p.NB) % p.NB;
+      if (delta >= W) delta = 0;
+      o = delta;
+      K0 = t0.K0;
+      K1 = t0.K1;
+      h1 = t0.h1;
+    } else {
+      const TileRef t0 = tile_ref<KIND>(p, u, rb, 0);
+      K0 = t0.K0;
+      K1 = t0.K1;
+      h1 = true;
+    }
+  }
+  __device__ __forceinline__ void next(const FusedParams& p) {
+    ++s;
+    if (KIND == kSym) {
+      o += 2;
+      if (o >= W) o -= W;
+      int o1 = o + 1;
+      if (o1 >= W) o1 -= W;
+      K0 = rb + o;
+      if (K0 >= p.NB) K0 -= p.NB;
+      h1 = 2 * s + 1 < W;
+      K1 = rb + o1;
+      if (K1 >= p.NB) K1 -= p.NB;
+      if (!h1) K1 = K0;
+    } else {
+      const int step = KIND == kPlain ? 2 : 2 * p.SS;
+      K0 += step;
+      K1 += step;
+    }
+  }
+};
 
 // Per-thread (= per-row) top-t list kept entirely in registers.  Slots are sorted
 // ASCENDING by magnitude; slots p >= t hold +inf and never move, so the eviction threshold
@@ -253,6 +309,17 @@ struct TopList {
 #pragma unroll
     for (int p = 0; p < MAXT; ++p) {
       mag[p] = (p < t) ? -1.f : __int_as_float(0x7f800000);
+      sval[p] = 0.f;
+      idx[p] = -1;
+    }
+  }
+  // kSym: start from a known lower bound b of the row's t-th magnitude (phantom entries,
+  // idx -1, just below b: any |ψ| >= b displaces them; never emitted)
+  __device__ __forceinline__ void init_bound(int t, float b) {
+    const float lb = b > 0.f ? __int_as_float(__float_as_int(b) - 1) : -1.f;
+#pragma unroll
+    for (int p = 0; p < MAXT; ++p) {
+      mag[p] = (p < t) ? lb : __int_as_float(0x7f800000);
       sval[p] = 0.f;
       idx[p] = -1;
     }
@@ -334,15 +401,84 @@ __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
   return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
 }
 
-// Epilogue role (warps 2-9): TMEM -> registers, fused per-row top-t / threshold.
-// Warp w handles TMEM lane quadrant q = w & 3 (thread = row) and column half h = (w-2) >> 2
-// of every 256-column tile, i.e. one 128-column operand block (4 x tcgen05.ld.32x32b.x32,
-// the next chunk's load in flight while the current chunk is reduced).  Two warps share
-// each row; their partial lists are merged through shared memory at the end of a unit.
-// Fast path per 32 values: 4 independent FMNMX chains of |v| against the row's current t-th
-// magnitude; the rare path stages the chunk in the warp's shared scratch and inserts
-// candidates in column order.  kSym additionally tests each value against its COLUMN's
-// lower bound (the transposed entry ψ_ji = ψ_ij) and appends survivors to row j's bucket.
+// One 32-row x 32-column chunk of the accumulator (thread = row, 32 columns in registers).
+// Fast path: one FMNMX3 chain of |v| against the row's current t-th magnitude (and, kSym, the
+// exact per-column test |ψ_ij| >= bound_j for the transposed direction).  Rare paths walk
+// the warp-union of the hit columns in ascending order and re-read each such column from
+// TMEM (tcgen05.ld 32x32b.x1: every lane gets its own row's value), so no register array is
+// ever indexed dynamically and no shared-memory staging is needed.
+struct CandCursor {
+  int64_t base, used;  // current reservation [base, base + kCandChunk) of the pool
+};
+template <int MAXT, int KIND>
+__device__ __forceinline__ void epi_chunk(const FusedParams& p, const uint32_t (&vr)[32],
+                                          uint32_t tchunk, int64_t col0, int64_t gi, int64_t lr,
+                                          bool valid, bool need_mask, float tau_s, float sd2,
+                                          TopList<MAXT>& top, int lane) {
+  // the loaded registers are only read (never rewritten), so the compiler keeps them in the
+  // tcgen05.ld destination block without copies
+  float m = max32_abs(reinterpret_cast<const float(&)[32]>(vr));
+  uint32_t excl = 0;  // diagonal (j == i: not an edge, Q8) and padding columns (j >= n)
+  if (need_mask) {
+    const int64_t dd = gi - col0;
+    if ((uint64_t)dd < 32ull) excl |= 1u << dd;
+    const int64_t nn = p.n - col0;
+    if (nn < 32) excl |= nn <= 0 ? 0xffffffffu : (0xffffffffu << nn);
+    m = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      m = fmaxf(m, ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(vr[e])));
+  }
+  const float thr = p.mode == 0 ? top.thr() : tau_s;
+  if (__any_sync(0xffffffffu, m > thr)) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) mask |= (fabsf(__uint_as_float(vr[e])) > thr ? 1u : 0u) << e;
+    mask &= ~excl;
+    if (p.mode == 0) {
+      // visit this row's candidates in column order (ties -> smaller j, Q9)
+      uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+      while (um) {
+        const int e = __ffs(um) - 1;
+        um &= um - 1;
+        const float x = __uint_as_float(tmem_ld1(tchunk + e));
+        if ((mask >> e) & 1u) {
+          const float a = fabsf(x);
+          if (a > top.thr()) top.insert(a, x, (int)(col0 + e));
+        }
+      }
+    } else {
+      if (!valid) mask = 0;
+      const int cnt = __popc(mask);
+      const int total = __reduce_add_sync(0xffffffffu, cnt);
+      unsigned long long b0 = 0;
+      if (lane == 0 && total) b0 = atomicAdd(p.coo_count, (unsigned long long)total);
+      int64_t at = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+      uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+      const uint32_t lt = (1u << lane) - 1u;
+      while (um) {
+        const int e = __ffs(um) - 1;
+        um &= um - 1;
+        const float x = __uint_as_float(tmem_ld1(tchunk + e));
+        const bool mine = (mask >> e) & 1u;
+        const uint32_t bm = __ballot_sync(0xffffffffu, mine);
+        const int64_t pos = at + __popc(bm & lt);
+        if (mine && pos < p.capacity) {
+          p.coo_key[pos] = lr * p.n + col0 + e;
+          p.coo_val[pos] = x * sd2;
+        }
+        at += __popc(bm);
+      }
+    }
+  }
+}
+
+// Epilogue role (8 warps), list form (kPlain, kSeed): TMEM -> registers, fused per-row
+// top-t / threshold.  Warp w handles TMEM lane quadrant q = w & 3 (thread = row) and column
+// half h of every 256-column tile, i.e. one 128-column operand block = 4 chunks of 32
+// columns, loaded with tcgen05.ld.32x32b.x32 into two alternating register buffers (the next
+// chunk's load is in flight while the current one is reduced).  Two warps share each row;
+// their lists are merged through shared memory at the end of a unit.
 template <int MAXT, int KIND>
 __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tmem_base,
                                               uint64_t* tfull, uint64_t* tempty, int warp,
@@ -351,20 +487,14 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
   const int q = warp & 3;   // TMEM lane quadrant accessible to this warp
   const int h = ew >> 2;    // column half of each tile
   const int r = q * 32 + lane;
-  float* scratch = scratch_all + ew * kScratchFloats;
   const float sd = ldexpf(1.f, -p.sc->exp2);  // ψ = acc · 2^-e · 2^-e
   const float sd2 = sd * sd;
   const float tau_s = ldexpf(ldexpf(p.tau, p.sc->exp2), p.sc->exp2);
-  const float qnan = __int_as_float(0x7fc00000);
   const int t = p.t;
   const int units = KIND == kPlain ? p.RB * p.C : p.RB;
   int buf = 0;
   uint32_t tphase = 0;
   TopList<MAXT> top;
-  // kSym candidates: appended into chunks reserved from a global pool (one atomic per
-  // kCandChunk entries); slots are claimed within the warp by ballot + popc (no atomics)
-  int64_t cbase = 0, cused = kCandChunk;  // current chunk [cbase, cbase + kCandChunk)
-  DevScalars* scw = const_cast<DevScalars*>(p.sc);
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     int rb;
     const int ntiles = unit_tiles<KIND>(p, u, rb);
@@ -372,149 +502,40 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     const int64_t lr = (int64_t)rb * kRowsPerBlock + r;
     const bool valid = lr < p.rows;
     const int64_t gi = p.row_begin + lr;
+    // global rows of this unit [rlo, rhi): tiles whose columns meet them hold the diagonal
+    const int64_t rlo = p.row_begin + (int64_t)rb * kRowsPerBlock;
+    const int64_t rhi = rlo + kRowsPerBlock;
     top.init(t);
-    for (int s = 0; s < ntiles; ++s) {
-      const TileRef tr = tile_ref<KIND>(p, u, rb, s);
-      const int Kh = h ? tr.K1 : tr.K0;
-      const bool live = (h == 0 || tr.h1) && p.dbg != 2;
-      const bool emit_cols = KIND == kSym && Kh != rb && p.dbg != 3 && p.dbg != 4;
+    TileIter<KIND> ti;
+    ti.start(p, u, rb);
+    for (int s = 0; s < ntiles; ++s, ti.next(p)) {
+      const int Kh = h ? ti.K1 : ti.K0;
+      const bool live = (h == 0 || ti.h1) && p.dbg != 2;
+      const int64_t cb = (int64_t)Kh * kRowsPerBlock;  // first column of this warp's block
+      const bool need_mask = (cb < rhi && cb + kRowsPerBlock > rlo) || (cb + kRowsPerBlock > p.n);
       mbar_wait(&tfull[buf], tphase);
       tc_fence_after();
       const uint32_t taddr =
           tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTileN + h * (kTileN / 2));
-      const int nchunks = live ? (kTileN / 2) / 32 : 0;
-      uint32_t vn[32];
-      if (nchunks) tmem_ld32_nowait(taddr, vn);
+      if (live) {
+        uint32_t va[32], vb[32];
+        tmem_ld32_nowait(taddr, va);
 #pragma unroll 1
-      for (int c = 0; c < nchunks; ++c) {
-        float v[32];
-        // kSym: this chunk's column bounds (warp-uniform 16-byte loads), issued before the
-        // TMEM wait and the row-direction work so their latency is hidden
-        float4 thc[8];
-        if (emit_cols) {
-          const float4* tp =
-              reinterpret_cast<const float4*>(p.thr + (int64_t)Kh * kRowsPerBlock + c * 32);
-#pragma unroll
-          for (int g = 0; g < 8; ++g) thc[g] = __ldg(tp + g);
-        }
-        tmem_wait_ld(vn);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(vn[e]);
-        if (c + 1 < nchunks) tmem_ld32_nowait(taddr + (c + 1) * 32, vn);
-
-        if (p.dbg == 1) {
-          if (v[0] == 12345.f && v[31] == 54321.f) p.row_ptr[0] = (int64_t)v[7];
-          continue;
-        }
-        const int64_t col0 = (int64_t)Kh * kRowsPerBlock + c * 32;
-        if (((uint64_t)(gi - col0) < 32ull) || (col0 + 32 > p.n)) {
-          // diagonal (j == i: not an edge, Q8) and padding columns (j >= n): NaN, ignored
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int64_t jj = col0 + e;
-            if (jj == gi || jj >= p.n) v[e] = qnan;
-          }
-        }
-        const float m = max32_abs(v);
-        if (emit_cols) {
-          // transposed direction: ψ_ij is also entry (j, i) of row j, kept if |ψ| >= the
-          // seed lower bound of row j (the true t-th magnitude of row j is >= that bound).
-          // Exact per-column test: max_e(|v_e| - thr_{col0+e}) >= 0, bounds read with
-          // warp-uniform (broadcast) 16-byte loads.
-          float d0 = -INFINITY, d1 = -INFINITY;
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            const float4 th = thc[g];
-            d0 = fmaxf(d0, fmaxf(fabsf(v[4 * g + 0]) - th.x, fabsf(v[4 * g + 1]) - th.y));
-            d1 = fmaxf(d1, fmaxf(fabsf(v[4 * g + 2]) - th.z, fabsf(v[4 * g + 3]) - th.w));
-          }
-          if (__any_sync(0xffffffffu, valid && fmaxf(d0, d1) >= 0.f)) {
-            if (cused + 32 * 32 > kCandChunk) {  // reserve a fresh chunk for this chunk's hits
-              unsigned long long b0 = 0;
-              if (lane == 0) b0 = atomicAdd(&scw->cand_alloc, (unsigned long long)kCandChunk);
-              cbase = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
-              cused = 0;
-              if (cbase + kCandChunk > p.cand_total) {
-                if (lane == 0) atomicOr(&scw->cand_overflow, 1);  // exact fallback by the host
-                cused = kCandChunk;
-              }
-            }
-            if (cused + 32 * 32 <= kCandChunk) {
-              // per-thread hit mask, warp prefix sum of hit counts, then each thread writes
-              // its own hits (values staged in the warp's scratch for dynamic indexing)
-              uint32_t mask = 0;
-#pragma unroll
-              for (int g = 0; g < 8; ++g) {
-                const float4 th = thc[g];
-                mask |= (fabsf(v[4 * g + 0]) >= th.x ? 1u : 0u) << (4 * g + 0);
-                mask |= (fabsf(v[4 * g + 1]) >= th.y ? 1u : 0u) << (4 * g + 1);
-                mask |= (fabsf(v[4 * g + 2]) >= th.z ? 1u : 0u) << (4 * g + 2);
-                mask |= (fabsf(v[4 * g + 3]) >= th.w ? 1u : 0u) << (4 * g + 3);
-              }
-              if (!valid) mask = 0;
-              const int cnt = __popc(mask);
-              int incl = cnt;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-              }
-              const int total = __shfl_sync(0xffffffffu, incl, 31);
-              if (mask) {
-#pragma unroll
-                for (int e = 0; e < 32; ++e) scratch[e * 32 + lane] = v[e];
-              }
-              __syncwarp();
-              int64_t at = cbase + cused + (incl - cnt);
-              while (mask) {
-                const int e = __ffs(mask) - 1;
-                mask &= mask - 1;
-                p.cand_key[at] = (uint32_t)(col0 + e);
-                p.cand_val[at] = make_uint2((unsigned)gi,
-                                            __float_as_uint(scratch[e * 32 + lane] * sd2));
-                ++at;
-              }
-              cused += total;
-              __syncwarp();
-            }
-          }
-        }
-        const float thr = p.mode == 0 ? top.thr() : tau_s;
-        if (p.dbg == 4) {
-          if (m == 12345.f) p.row_ptr[0] = 7;
-          continue;
-        }
-        if (__any_sync(0xffffffffu, m > thr)) {
-          // rare path: stage the chunk, then visit this thread's candidates in column order
-          uint32_t mask = 0;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            scratch[e * 32 + lane] = v[e];
-            mask |= (fabsf(v[e]) > thr ? 1u : 0u) << e;
-          }
-          __syncwarp();
-          if (p.mode == 0) {
-            while (mask) {
-              const int e = __ffs(mask) - 1;
-              mask &= mask - 1;
-              const float x = scratch[e * 32 + lane];
-              const float a = fabsf(x);
-              if (a > top.thr()) top.insert(a, x, (int)(col0 + e));
-            }
-          } else if (valid && mask) {
-            unsigned long long base =
-                atomicAdd(p.coo_count, (unsigned long long)__popc(mask));
-            while (mask) {
-              const int e = __ffs(mask) - 1;
-              mask &= mask - 1;
-              if ((int64_t)base < p.capacity) {
-                p.coo_key[base] = lr * p.n + col0 + e;
-                p.coo_val[base] = scratch[e * 32 + lane] * sd2;
-              }
-              ++base;
-            }
-          }
-          __syncwarp();
+        for (int c = 0; c < (kTileN / 2) / 32; c += 2) {
+          tmem_wait_ld(va);
+          tmem_ld32_nowait(taddr + (c + 1) * 32, vb);
+          if (p.dbg != 1)
+            epi_chunk<MAXT, KIND>(p, va, taddr + c * 32, cb + c * 32, gi, lr, valid, need_mask,
+                                  tau_s, sd2, top, lane);
+          else if (va[0] == 12345u && va[31] == 54321u)
+            p.row_ptr[0] = (int64_t)va[7];
+          tmem_wait_ld(vb);
+          if (c + 2 < (kTileN / 2) / 32) tmem_ld32_nowait(taddr + (c + 2) * 32, va);
+          if (p.dbg != 1)
+            epi_chunk<MAXT, KIND>(p, vb, taddr + (c + 1) * 32, cb + (c + 1) * 32, gi, lr, valid,
+                                  need_mask, tau_s, sd2, top, lane);
+          else if (vb[0] == 12345u && vb[31] == 54321u)
+            p.row_ptr[0] = (int64_t)vb[7];
         }
       }
       tc_fence_before();
@@ -555,8 +576,8 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
           p.row_ptr[lr] = lr * t;
           if (lr == p.rows - 1) p.row_ptr[p.rows] = p.rows * t;
         } else {
-          const int cc = KIND == kPlain ? u % p.C : 0;
-          const int64_t base = ((int64_t)cc * p.rows + lr) * t;
+          const int cc2 = KIND == kPlain ? u % p.C : 0;
+          const int64_t base = ((int64_t)cc2 * p.rows + lr) * t;
 #pragma unroll
           for (int a = 0; a < MAXT; ++a) {
             if (a < t) {
@@ -571,11 +592,188 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
   }
 }
 
+// Per-lane register select v[e] for a lane-varying e (binary tree of 31 selects; a dynamic
+// index into a register array would go through local memory).
+__device__ __forceinline__ float sel32(const uint32_t* v, uint32_t e) {
+  uint32_t a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = (e & 16u) ? v[i + 16] : v[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (e & 8u) ? a[i + 8] : a[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = (e & 4u) ? a[i + 4] : a[i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) a[i] = (e & 2u) ? a[i + 2] : a[i];
+  return __uint_as_float((e & 1u) ? a[1] : a[0]);
+}
+
+// Epilogue role, candidate form (kSym): every row i carries a lower bound b_i of its t-th
+// magnitude (the seed pass); rows and columns are in bound order.  Entry ψ_ij of a tile is
+// emitted as a candidate of row i if |ψ| >= b_i (row direction) and, for off-diagonal
+// blocks, of row j if |ψ| >= b_j (transposed direction, each unordered block pair being
+// evaluated once).  No per-row list is kept: the whole 128-column block of the warp is
+// loaded into registers and the TMEM buffer released before the filter runs; a final merge
+// selects each row's top t among its candidates.  Fast path per 32 columns: one FMNMX3
+// chain + two compares (row bound; chunk minimum of the column bounds).
+template <int KIND>
+__device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tmem_base,
+                                              uint64_t* tfull, uint64_t* tempty, int warp,
+                                              int lane, float* scratch_all) {
+  const int ew = warp - kFirstEpiWarp;
+  const int q = warp & 3;
+  const int h = ew >> 2;
+  const int r = q * 32 + lane;
+  float* thr_w = scratch_all + ew * kScratchFloats;  // this warp's 128 column bounds
+  const float sd = ldexpf(1.f, -p.sc->exp2);
+  const float sd2 = sd * sd;
+  const int units = p.RB;
+  const uint32_t lt = (1u << lane) - 1u;
+  DevScalars* scw = const_cast<DevScalars*>(p.sc);
+  int buf = 0;
+  uint32_t tphase = 0;
+  CandCursor cc{0, kCandChunk};
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    int rb;
+    const int ntiles = unit_tiles<KIND>(p, u, rb);
+    const int64_t gi = (int64_t)rb * kRowsPerBlock + r;  // permuted row index
+    const bool valid = gi < p.n;
+    const float bi = valid ? __ldg(p.thr + gi) : INFINITY;  // row bound (accumulator units)
+    TileIter<KIND> ti;
+    ti.start(p, u, rb);
+    float4 thr_next = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ntiles > 0)
+      thr_next = __ldg(reinterpret_cast<const float4*>(p.thr + (int64_t)(h ? ti.K1 : ti.K0) *
+                                                               kRowsPerBlock) + lane);
+    for (int s = 0; s < ntiles; ++s) {
+      const int Kh = h ? ti.K1 : ti.K0;
+      const bool live = (h == 0 || ti.h1) && p.dbg != 2;
+      const bool emit_cols = Kh != rb;
+      const int64_t cb = (int64_t)Kh * kRowsPerBlock;
+      const bool need_mask = Kh == rb || cb + kRowsPerBlock > p.n;
+      ti.next(p);
+      // stage the block's 128 column bounds; chunk minima by shuffles
+      float cm = fminf(fminf(thr_next.x, thr_next.y), fminf(thr_next.z, thr_next.w));
+      cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+      cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+      cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, 4));
+      float cmin[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cmin[c] = emit_cols ? __shfl_sync(0xffffffffu, cm, 8 * c) : INFINITY;
+      __syncwarp();
+      reinterpret_cast<float4*>(thr_w)[lane] = thr_next;
+      __syncwarp();
+      if (s + 1 < ntiles)
+        thr_next = __ldg(reinterpret_cast<const float4*>(p.thr + (int64_t)(h ? ti.K1 : ti.K0) *
+                                                                 kRowsPerBlock) + lane);
+      mbar_wait(&tfull[buf], tphase);
+      tc_fence_after();
+      const uint32_t taddr =
+          tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTileN + h * (kTileN / 2));
+      uint32_t v[4][32];
+      if (live) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_wait_ld(v[c]);
+      }
+      // the accumulator buffer is free as soon as the block is in registers
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (++buf == 2) {
+        buf = 0;
+        tphase ^= 1;
+      }
+      if (!live || p.dbg == 1) {
+        if (live && v[0][0] == 12345u && v[3][31] == 54321u) p.row_ptr[0] = (int64_t)v[1][7];
+        continue;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int64_t col0 = cb + c * 32;
+        float m = max32_abs(reinterpret_cast<const float(&)[32]>(v[c]));
+        uint32_t excl = 0;  // diagonal (Q8) and padding columns
+        if (need_mask) {
+          const int64_t dd = gi - col0;
+          if ((uint64_t)dd < 32ull) excl |= 1u << dd;
+          const int64_t nn = p.n - col0;
+          if (nn < 32) excl |= nn <= 0 ? 0xffffffffu : (0xffffffffu << nn);
+          m = 0.f;
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            m = fmaxf(m, ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(v[c][e])));
+        }
+        const bool rh = valid && m >= bi;
+        const bool ch = valid && m >= cmin[c];
+        if (!__any_sync(0xffffffffu, rh || ch)) continue;
+        // rare path: exact per-entry masks, then each lane walks its own hits
+        uint32_t mr = 0, mc = 0;
+        if (rh) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) mr |= (fabsf(__uint_as_float(v[c][e])) >= bi ? 1u : 0u) << e;
+          mr &= ~excl;
+        }
+        if (ch) {
+          const float4* t4 = reinterpret_cast<const float4*>(thr_w + c * 32);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const float4 th = t4[g];
+            mc |= (fabsf(__uint_as_float(v[c][4 * g + 0])) >= th.x ? 1u : 0u) << (4 * g + 0);
+            mc |= (fabsf(__uint_as_float(v[c][4 * g + 1])) >= th.y ? 1u : 0u) << (4 * g + 1);
+            mc |= (fabsf(__uint_as_float(v[c][4 * g + 2])) >= th.z ? 1u : 0u) << (4 * g + 2);
+            mc |= (fabsf(__uint_as_float(v[c][4 * g + 3])) >= th.w ? 1u : 0u) << (4 * g + 3);
+          }
+          mc &= ~excl;
+        }
+        const int total = __reduce_add_sync(0xffffffffu, __popc(mr) + __popc(mc));
+        if (total == 0) continue;
+        if (cc.used + total > kCandChunk) {  // reserve a fresh chunk of the pool
+          unsigned long long b0 = 0;
+          if (lane == 0) b0 = atomicAdd(&scw->cand_alloc, (unsigned long long)kCandChunk);
+          cc.base = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+          cc.used = 0;
+          if (cc.base + kCandChunk > p.cand_total) {
+            if (lane == 0) atomicOr(&scw->cand_overflow, 1);
+            cc.used = kCandChunk;  // pool exhausted: the host recomputes exactly
+          }
+        }
+        if (cc.used + total > kCandChunk) continue;
+        int64_t at = cc.base + cc.used;
+        cc.used += total;
+        uint32_t mh = mr | mc;
+        while (__any_sync(0xffffffffu, mh != 0)) {
+          const uint32_t e = mh ? (uint32_t)(__ffs(mh) - 1) : 0u;
+          const bool hr = mh && ((mr >> e) & 1u);
+          const bool hc = mh && ((mc >> e) & 1u);
+          const uint32_t br = __ballot_sync(0xffffffffu, hr);
+          const uint32_t bc = __ballot_sync(0xffffffffu, hc);
+          if (mh) {
+            const uint32_t xb = __float_as_uint(sel32(v[c], e) * sd2);
+            if (hr) {  // candidate (i -> j): target row i
+              const int64_t pos = at + __popc(br & lt);
+              p.cand_key[pos] = (uint32_t)gi;
+              p.cand_val[pos] = make_uint2((uint32_t)(col0 + e), xb);
+            }
+            if (hc) {  // candidate (j -> i): target row j
+              const int64_t pos = at + __popc(br) + __popc(bc & lt);
+              p.cand_key[pos] = (uint32_t)(col0 + e);
+              p.cand_val[pos] = make_uint2((uint32_t)gi, xb);
+            }
+            mh &= mh - 1;
+          }
+          at += __popc(br) + __popc(bc);
+        }
+      }
+    }
+  }
+}
+
 template <int MAXT, int KIND>
 __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-B aligned base (pointer arithmetic keeps the shared address space visible to the
+  // compiler, so epilogue accesses through derived pointers compile to LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int KA = p.KA;
   const int resident = p.resident;
   const size_t a_bytes = resident ? block_bytes(KA) : 0;
@@ -617,7 +815,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
 
   if (p.sc->flags != 0) {
     // invalid input: skip all work (status reported by the host after synchronising)
-  } else if (warp == 0) {
+  } else if (warp >= kFirstEpiWarp) {
+    setmaxnreg_inc<kRegsEpi>();
+    if (KIND == kSym)
+      epilogue_emit<KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
+    else
+      epilogue_role<MAXT, KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
+  } else {
+    setmaxnreg_dec<kRegsCtl>();
+    if (warp == 0) {
     // ===================== producer: bulk async copies global -> shared ==============
     if (lane == 0) {
       const uint64_t pol_b = policy_evict_last();
@@ -636,10 +842,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
           bulk_g2s(sA, Ablk, (uint32_t)bb, afull, pol_a);
           ++a_iter;
         }
-        for (int s = 0; s < ntiles; ++s) {
-          const TileRef tr = tile_ref<KIND>(p, u, rb, s);
-          const uint8_t* B0 = p.B + (size_t)tr.K0 * bb;
-          const uint8_t* B1 = p.B + (size_t)tr.K1 * bb;
+        TileIter<KIND> ti;
+        ti.start(p, u, rb);
+        for (int s = 0; s < ntiles; ++s, ti.next(p)) {
+          const uint8_t* B0 = p.B + (size_t)ti.K0 * bb;
+          const uint8_t* B1 = p.B + (size_t)ti.K1 * bb;
           for (int a = 0; a < KA; ++a) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* st = sStage + stage * st_bytes;
@@ -725,8 +932,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
         }
       }
     }
-  } else if (warp >= kFirstEpiWarp) {
-    epilogue_role<MAXT, KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
+    }
   }
   __syncthreads();
   if (warp == 0) {
@@ -775,31 +981,32 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n,
 }
 
 template <int MAXT>
-__global__ void merge_sym(const int32_t* __restrict__ pcol, const float* __restrict__ pval,
-                          const uint32_t* __restrict__ key, const uint2* __restrict__ cv,
-                          int64_t ncand, int64_t n, int t, int64_t* row_ptr, int32_t* col,
-                          float* val) {
+__global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restrict__ cv,
+                          int64_t ncand, int64_t n, int t, const int32_t* __restrict__ perm,
+                          int64_t* row_ptr, int32_t* col, float* val) {
+  // row j (permuted index): top t of its candidates (source in permuted index, value) by
+  // (|ψ| desc, original column id asc); emitted at the original row id in ascending columns
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   TopList<MAXT> top;
   top.init(t);
-  for (int e = 0; e < t; ++e) {
-    const int c = pcol[j * t + e];
-    if (c >= 0) {
-      const float v = pval[j * t + e];
-      top.merge_insert(fabsf(v), v, c);
-    }
-  }
   const int64_t b0 = lower_bound_u32(key, ncand, (uint32_t)j);
   const int64_t b1 = lower_bound_u32(key, ncand, (uint32_t)j + 1u);
   for (int64_t e = b0; e < b1; ++e) {
     const uint2 x = cv[e];
     const float v = __uint_as_float(x.y);
-    top.merge_insert(fabsf(v), v, (int)x.x);
+    top.merge_insert(fabsf(v), v, __ldg(perm + x.x));
   }
-  top.emit_sorted(t, col + j * t, val + j * t, 1.f);
-  row_ptr[j] = j * t;
-  if (j == n - 1) row_ptr[n] = n * t;
+  const int64_t o = perm[j];  // original row id
+  top.emit_sorted(t, col + o * t, val + o * t, 1.f);
+  row_ptr[o] = o * t;
+  if (o == n - 1) row_ptr[n] = n * t;
+}
+
+__global__ void iota_i32(int32_t* p, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)i;
 }
 
 __global__ void fill_f32(float* p, int64_t count, float v) {
@@ -840,6 +1047,7 @@ struct Plan {
   int64_t capacity;
   size_t coo_temp_bytes;
   int sym;       // symmetric scheme (kSeed + kSym + merge_sym)
+  int SS;        // seed column-tile stride
   int64_t NB;    // 128-row blocks of the axis
   int64_t cand_total;  // kSym: candidate pool capacity (entries)
   size_t sort_temp_bytes;
@@ -905,13 +1113,20 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // candidates: ~ t x 16 / 2 per row expected (seed samples 1/16 of the columns, half of
   // each row's columns come from the transposed direction); regions hold 2x that on average
   // pool: 2x the expected candidates + one chunk per epilogue warp of partially used space
-  pl->cand_total = pl->sym ? n * 16 * pl->t + (int64_t)sms * kEpiWarps * kCandChunk * 2 : 0;
+  // candidates: each row's entries >= its bound b_i (the t-th largest over a 1/SS column
+  // sample, i.e. about the (SS t)-th largest overall): ~SS t per row, from both directions;
+  // the pool holds 2x that plus the partially used reservation of every epilogue warp
+  pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(kSeedStride, pl->NT));
+  pl->cand_total = pl->sym ? n * 2 * pl->SS * pl->t + (int64_t)sms * kEpiWarps * kCandChunk * 2 : 0;
   pl->sort_temp_bytes = 0;
   if (pl->sym) {
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const uint2*)nullptr, (uint2*)nullptr, pl->cand_total);
-    pl->sort_temp_bytes = tb;
+    size_t tb2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb2, (const float*)nullptr, (float*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, n);
+    pl->sort_temp_bytes = std::max(tb, tb2);
   }
   int64_t C = o->col_chunks > 0 ? o->col_chunks
                                 : (pl->mode == 0 ? choose_chunks(pl->RB, pl->NT, sms) : 1);
@@ -940,7 +1155,10 @@ struct Work {
   float* cv_in;
   float* cv_out;
   void* cub_tmp;
-  float* thr;          // kSym: [NB*128]
+  float* thr;          // kSym: seed bounds by original row [NB*128]
+  float* thr_p;        // kSym: bounds in permuted (sorted) order [NB*128]
+  int32_t* ids;        // kSym: 0..n-1
+  int32_t* perm;       // kSym: permuted index -> original id [n]
   uint32_t* ckey;      // kSym: candidate pool
   uint2* cval;
   uint32_t* skey;      // kSym: sorted by target row
@@ -954,7 +1172,6 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->Bop = cv.take<uint8_t>((size_t)pl.nBblocks * block_bytes(pl.KA));
   w->Aop = cv.take<uint8_t>((size_t)pl.nAblocks * block_bytes(pl.KA));
   size_t npart = (pl.mode == 0 && pl.C > 1) ? (size_t)pl.C * pl.rows * pl.t : 0;
-  if (pl.sym) npart = std::max(npart, (size_t)pl.n * pl.t);
   w->pcol = cv.take<int32_t>(npart);
   w->pval = cv.take<float>(npart);
   const size_t ncoo = pl.mode == 1 ? (size_t)std::max<int64_t>(pl.capacity, 0) : 0;
@@ -966,6 +1183,9 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   const size_t nb = pl.sym ? (size_t)pl.NB : 0;
   const size_t ct = pl.sym ? (size_t)pl.cand_total : 0;
   w->thr = cv.take<float>(nb * kRowsPerBlock);
+  w->thr_p = cv.take<float>(nb * kRowsPerBlock);
+  w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
+  w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->ckey = cv.take<uint32_t>(ct);
   w->cval = cv.take<uint2>(ct);
   w->skey = cv.take<uint32_t>(ct);
@@ -1028,8 +1248,8 @@ static void launch_merge_sym_t(const Work& w, const Plan& pl, int64_t ncand, int
                                int32_t* col, float* val, cudaStream_t s) {
   const int threads = 128;
   const int blocks = (int)((pl.n + threads - 1) / threads);
-  merge_sym<MAXT><<<blocks, threads, 0, s>>>(w.pcol, w.pval, w.skey, w.sval, ncand, pl.n, pl.t,
-                                             row_ptr, col, val);
+  merge_sym<MAXT><<<blocks, threads, 0, s>>>(w.skey, w.sval, ncand, pl.n, pl.t, w.perm, row_ptr,
+                                             col, val);
 }
 
 static thread_local double g_stats[4] = {0, 0, 0, 0};
@@ -1145,13 +1365,33 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     FusedParams sp = fp;
     sp.kind = kSeed;
     sp.RB = (int)pl.NB;
+    sp.SS = pl.SS;
     sp.thr_out = w.thr;
     ce = launch_fused(sp, pl.t, s);
     if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "seed launch: %s", cudaGetErrorString(ce));
+    // order rows (= columns) by their bound: a CUB radix sort of the n seed bounds gives
+    // the permutation and the permuted bounds; the column operand is re-split in that order,
+    // so the 32 columns of every epilogue chunk carry nearly equal bounds
+    iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
+    {
+      size_t tb = pl.sort_temp_bytes;
+      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.thr, w.thr_p, w.ids, w.perm,
+                                                   (int)n, 0, 32, s));
+    }
+    fill_f32<<<(int)std::min<int64_t>((nthr - n + 255) / 256 + 1, sms * 8), 256, 0, s>>>(
+        w.thr_p + n, nthr - n, INFINITY);
+    {
+      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 8;
+      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+          V, lambda, n, k, pl.KA, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop, w.perm);
+    }
+    count_launches(3);
+    GGM_CUDA_TRY(cudaGetLastError());
     tm.mark(1);
     fp.kind = kSym;
     fp.RB = (int)pl.NB;
-    fp.thr = w.thr;
+    fp.thr = w.thr_p;
+    fp.perm = w.perm;
     fp.cand_key = w.ckey;
     fp.cand_val = w.cval;
     fp.cand_total = pl.cand_total;
@@ -1166,7 +1406,14 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
     const int hovf = hs.cand_overflow;
     if (hovf) {
-      // a candidate region filled up: recompute the whole axis with the plain scheme (exact)
+      // the candidate pool filled up: recompute the whole axis with the plain scheme (exact)
+      // from an un-permuted split
+      {
+        const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 8;
+        split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+            V, lambda, n, k, pl.KA, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
+        count_launches(1);
+      }
       Plan bp = pl;
       bp.sym = 0;
       FusedParams op = base_params(bp, w, n, 0);
@@ -1201,8 +1448,12 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
     if (ncand > 0) {
       size_t tb = pl.sort_temp_bytes;
+      // keys are permuted row ids < n; unused slots (UINT32_MAX) keep all low bits set, so
+      // sorting on the low ebits bits (2^ebits > n) still places them last
+      int ebits = 1;
+      while ((int64_t(1) << ebits) <= n) ++ebits;
       GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
-                                                   ncand, 0, 32, s));
+                                                   ncand, 0, ebits, s));
     }
     if (pl.t <= 5)
       launch_merge_sym_t<5>(w, pl, ncand, row_ptr, col, val, s);
