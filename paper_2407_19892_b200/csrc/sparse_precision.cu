@@ -51,7 +51,7 @@ constexpr int kMaxResidentAtoms = 2;
 // A (128 rows x KA atoms x hi/lo) stays resident in shared memory when KA <= 2 (k <= 128)
 constexpr int kEpiWarps = 8;              // epilogue warps (2 per TMEM lane quadrant)
 constexpr int kScratchFloats = 32 * 32;   // per epilogue warp: [32 values][32 lanes]
-constexpr int kSeedStride = 16;           // seed pass samples every 16th column tile (at most)
+constexpr int kSeedStride = 8;            // seed pass samples every 8th column tile (at most)
 
 __host__ __device__ inline size_t block_bytes(int KA) { return (size_t)2 * KA * kAtomBytes; }
 
@@ -62,6 +62,7 @@ struct DevScalars {
   int cand_overflow;         // kSym: candidate pool exhausted -> exact fallback
   unsigned long long coo_count;
   unsigned long long cand_alloc;  // kSym: entries reserved from the candidate pool
+  unsigned int rn_max_bits;       // kSym: float bits of max_i ||U_i||
 };
 constexpr int kCandChunk = 4096;  // candidate-pool reservation granularity (entries)
 
@@ -97,6 +98,44 @@ __global__ void absmax_check(const float* __restrict__ V, const double* __restri
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (threadIdx.x == 0) atomicMax(&sc->absmax_bits, __float_as_uint(m));
+  }
+}
+
+// kSym: per-row norm ||U_i|| = sqrt(Σ_r λ_r V_ir²) (fp64, one warp per row) and its maximum
+__global__ void row_norms(const float* __restrict__ V, const double* __restrict__ lam, int64_t n,
+                          int k, float* __restrict__ rn, unsigned int* __restrict__ rn_max_bits) {
+  const int lane = threadIdx.x & 31;
+  float wmax = 0.f;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double acc = 0.0;
+    for (int c = lane; c < k; c += 32) {
+      const double x = (double)V[i * k + c];
+      acc += lam[c] * x * x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const float f = (float)sqrt(acc);
+    if (lane == 0) rn[i] = f;
+    wmax = fmaxf(wmax, f);
+  }
+  if (lane == 0) atomicMax(rn_max_bits, __float_as_uint(wmax));
+}
+
+// kSym: seed value b1_i (t-th largest |hi·hi| chunk maximum, accumulator units) -> a lower
+// bound of the row's t-th 3-term magnitude.  With x = hi + lo, |lo| <= 2^-11 |hi|:
+// |ψ3 - ψ1| = |Σ_r hi_ir lo_jr + lo_ir hi_jr| <= 2^-10 (1 + 2^-11) ||x_i|| ||x_j||, plus fp32
+// accumulation differences (k 2^-24 ||x_i|| ||x_j||); margin 1.1 · 2^-10 ||x_i|| max_j ||x_j||.
+__global__ void seed_bounds(float* __restrict__ thr, const float* __restrict__ rn,
+                            const unsigned int* __restrict__ rn_max_bits, int64_t n,
+                            const DevScalars* __restrict__ sc) {
+  const float s = ldexpf(1.f, sc->exp2);
+  const float umax = __uint_as_float(*rn_max_bits) * s;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float b1 = thr[i];
+    const float margin = 1.1f * ldexpf(rn[i] * s * umax, -10);
+    thr[i] = b1 > 0.f ? fmaxf(b1 - margin, -1.f) : -1.f;
   }
 }
 
@@ -390,14 +429,19 @@ struct TopList {
 };
 
 __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
+  // four independent chains over columns j, j+4, ..., j+28 (pairs fuse into FMNMX3)
   float m0 = fabsf(v[0]), m1 = fabsf(v[1]), m2 = fabsf(v[2]), m3 = fabsf(v[3]);
 #pragma unroll
-  for (int e = 4; e < 32; e += 8) {
+  for (int e = 4; e < 28; e += 8) {
     m0 = fmaxf(m0, fmaxf(fabsf(v[e + 0]), fabsf(v[e + 4])));
     m1 = fmaxf(m1, fmaxf(fabsf(v[e + 1]), fabsf(v[e + 5])));
     m2 = fmaxf(m2, fmaxf(fabsf(v[e + 2]), fabsf(v[e + 6])));
     m3 = fmaxf(m3, fmaxf(fabsf(v[e + 3]), fabsf(v[e + 7])));
   }
+  m0 = fmaxf(m0, fabsf(v[28]));
+  m1 = fmaxf(m1, fabsf(v[29]));
+  m2 = fmaxf(m2, fabsf(v[30]));
+  m3 = fmaxf(m3, fabsf(v[31]));
   return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
 }
 
@@ -587,6 +631,100 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
           }
         }
       }
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+  }
+}
+
+// Epilogue role of the seed pass (kSeed): per row, the t-th largest of the 32-column chunk
+// maxima of |hi·hi| over the sampled column tiles.  t chunk maxima are t distinct entries,
+// so this is a lower bound of the row's t-th magnitude in the same arithmetic (converted to
+// a bound on the 3-term values by seed_bounds).  Magnitude-only list, one predicated insert
+// of the chunk maximum per lane: no per-entry work beyond the FMNMX3 chain.
+template <int MAXT>
+struct MagList {
+  float m[MAXT];  // ascending; slots >= t hold +inf
+  __device__ __forceinline__ void init(int t) {
+#pragma unroll
+    for (int p = 0; p < MAXT; ++p) m[p] = (p < t) ? -1.f : __int_as_float(0x7f800000);
+  }
+  __device__ __forceinline__ void insert(float a) {
+#pragma unroll
+    for (int p = 0; p < MAXT - 1; ++p) m[p] = a > m[p + 1] ? m[p + 1] : (a > m[p] ? a : m[p]);
+    if (a > m[MAXT - 1]) m[MAXT - 1] = a;
+  }
+};
+template <int MAXT>
+__device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tmem_base,
+                                              uint64_t* tfull, uint64_t* tempty, int warp,
+                                              int lane, float* scratch_all) {
+  const int ew = warp - kFirstEpiWarp;
+  const int q = warp & 3;
+  const int h = ew >> 2;
+  const int r = q * 32 + lane;
+  const int t = p.t;
+  int buf = 0;
+  uint32_t tphase = 0;
+  MagList<MAXT> top;
+  for (int u = blockIdx.x; u < p.RB; u += gridDim.x) {
+    int rb;
+    const int ntiles = unit_tiles<kSeed>(p, u, rb);
+    const int64_t gi = (int64_t)rb * kRowsPerBlock + r;
+    top.init(t);
+    TileIter<kSeed> ti;
+    ti.start(p, u, rb);
+    for (int s = 0; s < ntiles; ++s, ti.next(p)) {
+      const int Kh = h ? ti.K1 : ti.K0;
+      const int64_t cb = (int64_t)Kh * kRowsPerBlock;
+      const bool need_mask = Kh == rb || cb + kRowsPerBlock > p.n;
+      mbar_wait(&tfull[buf], tphase);
+      tc_fence_after();
+      const uint32_t taddr =
+          tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTileN + h * (kTileN / 2));
+      uint32_t v[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_wait_ld(v[c]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (++buf == 2) {
+        buf = 0;
+        tphase ^= 1;
+      }
+      if (p.dbg != 0 && p.dbg != 7) {
+        if (v[0][0] == 12345u && v[3][31] == 54321u) p.thr_out[0] = __uint_as_float(v[1][7]);
+        continue;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float m = max32_abs(reinterpret_cast<const float(&)[32]>(v[c]));
+        if (need_mask) {
+          const int64_t col0 = cb + c * 32;
+          m = 0.f;
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (col0 + e != gi && col0 + e < p.n) m = fmaxf(m, fabsf(__uint_as_float(v[c][e])));
+        }
+        if (m > top.m[0]) top.insert(m);
+      }
+    }
+    // merge the two column halves: half 1 publishes its list, half 0 inserts and writes
+    float* pv = scratch_all + (4 + ((q - kFirstEpiWarp) & 3)) * kScratchFloats;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    if (h == 1) {
+#pragma unroll
+      for (int a = 0; a < MAXT; ++a) pv[a * 32 + lane] = top.m[a];
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    if (h == 0) {
+#pragma unroll 1
+      for (int a = 0; a < t; ++a) {
+        const float x = pv[a * 32 + lane];
+        if (x > top.m[0]) top.insert(x);
+      }
+      if (gi < p.n) p.thr_out[gi] = top.m[0];  // -1: fewer than t chunks sampled
     }
     asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
   }
@@ -819,6 +957,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
     setmaxnreg_inc<kRegsEpi>();
     if (KIND == kSym)
       epilogue_emit<KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
+    else if (KIND == kSeed)
+      epilogue_seed<MAXT>(p, tmem_base, tfull, tempty, warp, lane, scratch);
     else
       epilogue_role<MAXT, KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
   } else {
@@ -910,8 +1050,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
                 const uint32_t off = ks * 32;
                 const uint32_t acc = (a | ks) ? 1u : 0u;
                 mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc, acc);
-                mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
-                mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
+                if (KIND != kSeed || p.dbg == 7) {  // the seed pass bounds with hi*hi alone (see seed_bounds)
+                  mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
+                  mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
+                }
               }
             }
             mma_commit(&empty[stage]);
@@ -1117,6 +1259,8 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // sample, i.e. about the (SS t)-th largest overall): ~SS t per row, from both directions;
   // the pool holds 2x that plus the partially used reservation of every epilogue warp
   pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(kSeedStride, pl->NT));
+  if (const char* e = getenv("GGM_SEED_STRIDE"))  // tuning experiments only
+    pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(atoi(e), pl->NT));
   pl->cand_total = pl->sym ? n * 2 * pl->SS * pl->t + (int64_t)sms * kEpiWarps * kCandChunk * 2 : 0;
   pl->sort_temp_bytes = 0;
   if (pl->sym) {
@@ -1159,6 +1303,7 @@ struct Work {
   float* thr_p;        // kSym: bounds in permuted (sorted) order [NB*128]
   int32_t* ids;        // kSym: 0..n-1
   int32_t* perm;       // kSym: permuted index -> original id [n]
+  float* rn;           // kSym: row norms ||U_i|| [n]
   uint32_t* ckey;      // kSym: candidate pool
   uint2* cval;
   uint32_t* skey;      // kSym: sorted by target row
@@ -1186,6 +1331,7 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->thr_p = cv.take<float>(nb * kRowsPerBlock);
   w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
+  w->rn = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
   w->ckey = cv.take<uint32_t>(ct);
   w->cval = cv.take<uint2>(ct);
   w->skey = cv.take<uint32_t>(ct);
@@ -1367,8 +1513,13 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     sp.RB = (int)pl.NB;
     sp.SS = pl.SS;
     sp.thr_out = w.thr;
+    row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+        V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
     ce = launch_fused(sp, pl.t, s);
     if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "seed launch: %s", cudaGetErrorString(ce));
+    seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
+        w.thr, w.rn, &w.sc->rn_max_bits, n, w.sc);
+    count_launches(2);
     // order rows (= columns) by their bound: a CUB radix sort of the n seed bounds gives
     // the permutation and the permuted bounds; the column operand is re-split in that order,
     // so the 32 columns of every epilogue chunk carry nearly equal bounds
