@@ -156,13 +156,18 @@ typedef struct {
   float tau;  /* mode 1 only, >= 0 */
   int col_chunks; /* 0 = automatic; else split each row block's column sweep into this
                      many chunks merged afterwards (balances small row ranges) */
-  int symmetric;  /* mode 0 over the FULL axis only (row_begin = 0, row_end = n), k <= 128:
-                     1 = use the symmetric scheme; 0 (automatic) and 2 = plain scheme.
-                     Ψ is symmetric, so each unordered 128x128 block pair is evaluated once
-                     (cyclic window per row block); the transposed direction keeps entries
-                     >= a per-row lower bound of the t-th |ψ| obtained from a strided seed
-                     pass over 1/16 of the columns; per-row candidate buckets are merged,
-                     and any row block whose bucket overflowed is recomputed exactly. */
+  int symmetric;  /* scheme selection, mode 0 over the FULL axis (row_begin = 0, row_end = n)
+                     with k <= 128 only (otherwise always plain):
+                     0 = automatic (symmetric for n >= 65536), 1 = symmetric, 2 = plain.
+                     Symmetric scheme (Ψ = Ψ^T): a seed pass over every 8th column
+                     tile (hi·hi products) gives each row i a lower bound b_i of its t-th |ψ|
+                     (t-th largest 32-column chunk maximum, minus the hi·hi rounding bound
+                     2^-10·1.1·||U_i||·max_j||U_j||); rows are reordered by b_i; each
+                     unordered 128x128 block pair is then evaluated once (cyclic window per
+                     row block) and entry ψ_ij is kept as a candidate of row i if
+                     |ψ| >= b_i and of row j if |ψ| >= b_j; a CUB sort by row and a merge
+                     select each row's top t by (|ψ| desc, j asc).  If the candidate pool
+                     fills up, the axis is recomputed with the plain scheme (exact). */
 } ggm_sparsify_opts;
 
 ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t row_begin, int64_t row_end,

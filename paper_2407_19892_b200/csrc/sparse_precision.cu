@@ -38,7 +38,7 @@ constexpr int kRowsPerBlock = 128;        // M (rows of Ψ per CTA tile; TMEM la
 constexpr int kTileN = 256;               // N (columns of Ψ per tile; 2 operand blocks)
 constexpr int kAtomElems = 64;            // fp16 elements per 128-byte swizzle row
 constexpr int kAtomBytes = kRowsPerBlock * 128;  // one (128-row block, K atom) = 16 KB
-constexpr int kStages = 2;
+constexpr int kMaxStages = 4;  // operand pipeline: 4 x 32 KB (A resident) or 2 x 96 KB
 // 12 warps = 3 warpgroups: WG0 = producer (+TMEM alloc), MMA issuer, 2 idle warps, shrunk
 // to kRegsCtl registers; WG1-2 = 8 epilogue warps grown to kRegsEpi (setmaxnreg).  With 10
 // warps one SM sub-partition holds 3 warps and caps every thread at 168 registers.
@@ -64,7 +64,8 @@ struct DevScalars {
   unsigned long long cand_alloc;  // kSym: entries reserved from the candidate pool
   unsigned int rn_max_bits;       // kSym: float bits of max_i ||U_i||
 };
-constexpr int kCandChunk = 4096;  // candidate-pool reservation granularity (entries)
+constexpr int kCandChunk = 4096;
+constexpr int64_t kSymAutoN = 65536;  // automatic symmetric scheme from this axis length  // candidate-pool reservation granularity (entries)
 
 // ------------------------------------------------------------------ BK1a
 __global__ void absmax_check(const float* __restrict__ V, const double* __restrict__ lam,
@@ -156,38 +157,67 @@ __global__ void scale_finalize(DevScalars* sc) {
 // dst holds `nblocks` 128-row blocks: [block][hi atoms 0..KA-1][lo atoms 0..KA-1], each
 // atom 128 rows x 128 bytes, 16-byte chunk c of row r stored at chunk (c ^ (r & 7))
 // (the SWIZZLE_128B K-major canonical layout; SBO = 1024 B between 8-row groups).
+// A K slot is 16 fp16 (32 B, one MMA K step); slot s of the hi/lo array holds hi/lo of
+// elements 16s..16s+15 for s < KS.  With a packed tail (TS > 0, r = k - 16 KS), the
+// products of the last r elements go into TS slots that hold 3r values each:
+//   hi array slot KS+u : TB = [hi(x_tail) | lo(x_tail) | hi(x_tail)]   (B side)
+//   lo array slot KS+u : TA = [hi(x_tail) | hi(x_tail) | lo(x_tail)]   (A side)
+// so one MMA TA·TB^T = hi·hi + hi·lo + lo·hi over the tail (positions 16u.. of the packed
+// sequence).  Remaining slots are zero.
+__device__ __forceinline__ void split2(double x, __half& h, __half& l) {
+  h = __double2half(x);
+  l = __double2half(x - (double)__half2float(h));
+}
 __global__ void split_tile(const float* __restrict__ V, const double* __restrict__ lam,
-                           int64_t n, int k, int KA, int64_t row0, int64_t nrows_pad,
-                           const DevScalars* __restrict__ sc, uint8_t* __restrict__ dst,
-                           const int32_t* __restrict__ perm = nullptr) {
-  const int chunks_per_row = KA * 8;
-  const int64_t total = nrows_pad * chunks_per_row;
+                           int64_t n, int k, int KA, int KS, int TS, int64_t row0,
+                           int64_t nrows_pad, const DevScalars* __restrict__ sc,
+                           uint8_t* __restrict__ dst, const int32_t* __restrict__ perm = nullptr) {
+  const int chunks_per_row = KA * 8;  // 16-byte chunks of one array (hi or lo)
+  const int64_t total = nrows_pad * chunks_per_row * 2;
   const double s = ldexp(1.0, sc->exp2);
+  const int r = k - 16 * KS;  // tail elements (packed when TS > 0)
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = idx / chunks_per_row;
-    const int ch = (int)(idx % chunks_per_row);
+    const int arr = (int)(idx % 2);  // 0 = hi array, 1 = lo array
+    const int64_t rc = idx / 2;
+    const int64_t row = rc / chunks_per_row;
+    const int ch = (int)(rc % chunks_per_row);
     int64_t g = row0 + row;
-    if (perm && g < n) g = perm[g];  // symmetric scheme: rows in threshold order
-    __align__(16) __half hi[8];
-    __align__(16) __half lo[8];
+    const bool real = g < n;
+    if (perm && real) g = perm[g];  // symmetric scheme: rows in bound order
+    const int slot = ch >> 1;
+    __align__(16) __half out[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int c = ch * 8 + e;
-      double x = 0.0;
-      if (g < n && c < k) x = (double)V[g * k + c] * sqrt(lam[c]) * s;
-      __half h = __double2half(x);
-      hi[e] = h;
-      lo[e] = __double2half(x - (double)__half2float(h));
+      const int pos = (ch & 1) * 8 + e;  // position within the slot
+      __half h = __float2half(0.f), l = __float2half(0.f);
+      __half v = __float2half(0.f);
+      if (real) {
+        if (slot < KS || TS == 0) {
+          const int c = slot * 16 + pos;
+          if (c < k) {
+            split2((double)V[g * k + c] * sqrt(lam[c]) * s, h, l);
+            v = arr ? l : h;
+          }
+        } else if (slot < KS + TS) {
+          const int q = (slot - KS) * 16 + pos;  // position in the packed tail sequence
+          if (q < 3 * r) {
+            const int seg = q / r;
+            const int c = 16 * KS + q % r;
+            split2((double)V[g * k + c] * sqrt(lam[c]) * s, h, l);
+            // B (hi array): [hi | lo | hi];  A (lo array): [hi | hi | lo]
+            v = arr == 0 ? (seg == 1 ? l : h) : (seg == 2 ? l : h);
+          }
+        }
+      }
+      out[e] = v;
     }
     const int64_t b = row / kRowsPerBlock;
-    const int r = (int)(row % kRowsPerBlock);
+    const int rr = (int)(row % kRowsPerBlock);
     const int a = ch >> 3, c8 = ch & 7;
-    const size_t off = (size_t)b * block_bytes(KA) + (size_t)a * kAtomBytes + (size_t)r * 128 +
-                       (size_t)((c8 ^ (r & 7)) * 16);
-    *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(hi);
-    *reinterpret_cast<uint4*>(dst + off + (size_t)KA * kAtomBytes) =
-        *reinterpret_cast<const uint4*>(lo);
+    const size_t off = (size_t)b * block_bytes(KA) + (size_t)(arr * KA + a) * kAtomBytes +
+                       (size_t)rr * 128 + (size_t)((c8 ^ (rr & 7)) * 16);
+    *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(out);
   }
 }
 
@@ -199,7 +229,8 @@ struct FusedParams {
   const uint8_t* A;  // row-block operand (rows [row_begin,row_end)), tiled layout
   const uint8_t* B;  // column operand (all n rows, padded to 256), tiled layout
   int KA;            // K atoms of 64
-  int KS;            // K steps of 16 actually issued (ceil(k/16))
+  int KS;            // full K slots of 16 (3 MMAs each: hi·hi, hi·lo, lo·hi)
+  int TS;            // packed tail slots (1 MMA each), see split_tile
   int resident;      // 1: A kept in shared memory for a whole row block
   int64_t n, row_begin, rows;
   int kind;          // Kind
@@ -229,13 +260,19 @@ struct FusedParams {
   int dbg;  // timing experiments only (GGM_DEBUG_EPI): 1 = TMEM loads only, 2 = no epilogue work
 };
 
+// A resident (k <= 128): a stage holds B hi and B lo of one K atom for both 128-row operand
+// blocks of the tile = 64 KB, 2 stages (the seed pass fills only the hi half).  A streamed: a
+// stage holds A hi+lo and B hi+lo of one K atom = 96 KB, 2 stages.  (4 x 32 KB stages
+// measured slower: the MMA warp, which shares its SM sub-partition with two epilogue warps,
+// then has to be woken twice as often per tile.)
+__host__ __device__ inline int num_stages(int resident) { return 2; }
 __host__ __device__ inline size_t stage_bytes(int resident) {
-  return (resident ? 0 : (size_t)2 * kAtomBytes) + (size_t)4 * kAtomBytes;
+  return (size_t)(resident ? 4 : 6) * kAtomBytes;
 }
 __host__ inline size_t fused_smem_bytes(int KA, int resident) {
   size_t a = resident ? block_bytes(KA) : 0;
-  return 1024 /*align slack*/ + a + kStages * stage_bytes(resident) + 256 /*barriers*/ +
-         kEpiWarps * kScratchFloats * sizeof(float);
+  return 1024 /*align slack*/ + a + num_stages(resident) * stage_bytes(resident) +
+         256 /*barriers*/ + kEpiWarps * kScratchFloats * sizeof(float);
 }
 
 // Tile enumeration shared by the producer, MMA and epilogue roles.  A unit is one 128-row
@@ -918,10 +955,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
   const size_t st_bytes = stage_bytes(resident);
   uint8_t* sA = smem;
   uint8_t* sStage = smem + a_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + kStages * st_bytes);
+  const int NS = num_stages(resident);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + NS * st_bytes);
   uint64_t* full = bars;
-  uint64_t* empty = bars + kStages;
-  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* tfull = bars + 2 * kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* afull = tempty + 2;
   uint64_t* aempty = afull + 1;
@@ -933,7 +971,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
   const int units = KIND == kPlain ? p.RB * p.C : p.RB;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -987,17 +1025,34 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
         for (int s = 0; s < ntiles; ++s, ti.next(p)) {
           const uint8_t* B0 = p.B + (size_t)ti.K0 * bb;
           const uint8_t* B1 = p.B + (size_t)ti.K1 * bb;
+          if (resident) {
+            // B hi (block K0 | block K1), then B lo, of each K atom: 256 rows per atom,
+            // uniform 1 KB SBO (the seed pass reads only the hi array)
+            const uint32_t sbytes = (uint32_t)(KIND == kSeed ? 2 : 4) * kAtomBytes;
+            for (int a = 0; a < KA; ++a) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              uint8_t* st = sStage + stage * st_bytes;
+              mbar_arrive_expect_tx(&full[stage], sbytes);
+              for (int hl = 0; hl < (KIND == kSeed ? 1 : 2); ++hl) {
+                const size_t ao = (size_t)(hl * KA + a) * kAtomBytes;
+                bulk_g2s(st + 2 * hl * kAtomBytes, B0 + ao, kAtomBytes, &full[stage], pol_b);
+                bulk_g2s(st + (2 * hl + 1) * kAtomBytes, B1 + ao, kAtomBytes, &full[stage], pol_b);
+              }
+              if (++stage == NS) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+            continue;
+          }
           for (int a = 0; a < KA; ++a) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* st = sStage + stage * st_bytes;
             mbar_arrive_expect_tx(&full[stage], (uint32_t)st_bytes);
-            uint8_t* sb = st;
-            if (!resident) {
-              bulk_g2s(st, Ablk + (size_t)a * kAtomBytes, kAtomBytes, &full[stage], pol_a);
-              bulk_g2s(st + kAtomBytes, Ablk + (size_t)(KA + a) * kAtomBytes, kAtomBytes,
-                       &full[stage], pol_a);
-              sb = st + 2 * kAtomBytes;
-            }
+            bulk_g2s(st, Ablk + (size_t)a * kAtomBytes, kAtomBytes, &full[stage], pol_a);
+            bulk_g2s(st + kAtomBytes, Ablk + (size_t)(KA + a) * kAtomBytes, kAtomBytes,
+                     &full[stage], pol_a);
+            uint8_t* sb = st + 2 * kAtomBytes;
             // B hi (block K0 | block K1), then B lo: 256 rows per atom, uniform 1 KB SBO
             bulk_g2s(sb, B0 + (size_t)a * kAtomBytes, kAtomBytes, &full[stage], pol_b);
             bulk_g2s(sb + kAtomBytes, B1 + (size_t)a * kAtomBytes, kAtomBytes, &full[stage],
@@ -1006,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
                      &full[stage], pol_b);
             bulk_g2s(sb + 3 * kAtomBytes, B1 + (size_t)(KA + a) * kAtomBytes, kAtomBytes,
                      &full[stage], pol_b);
-            if (++stage == kStages) {
+            if (++stage == NS) {
               stage = 0;
               phase ^= 1;
             }
@@ -1034,33 +1089,67 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
           mbar_wait(&tempty[buf], tphase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(buf * kTileN);
+          if (resident) {
+            const uint32_t sA_s = smem_u32(sA);
+            for (int a = 0; a < KA; ++a) {
+              const uint32_t aHi_s = sA_s + (uint32_t)(a * kAtomBytes);
+              const uint32_t aLo_s = sA_s + (uint32_t)((KA + a) * kAtomBytes);
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t bHi_s = smem_u32(sStage + stage * st_bytes);
+              const uint32_t bLo_s = bHi_s + 2 * kAtomBytes;
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                const int slot = a * 4 + ks;
+                const uint32_t off = ks * 32;
+                const uint32_t acc = (a | ks) ? 1u : 0u;
+                if (slot < p.KS) {
+                  mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc, acc);
+                  if (KIND != kSeed) {  // the seed pass bounds with hi*hi alone (seed_bounds)
+                    mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
+                    mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
+                  }
+                } else if (slot < p.KS + p.TS) {
+                  // packed tail: A's slot in the lo array [hi|hi|lo], B's in the hi array
+                  // [hi|lo|hi] (3 products of the last k mod 16 elements in one K step)
+                  mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, acc);
+                }
+              }
+              mma_commit(&empty[stage]);
+              if (++stage == NS) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+          } else {
           for (int a = 0; a < KA; ++a) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             uint8_t* st = sStage + stage * st_bytes;
-            const uint8_t* aHi = resident ? sA + (size_t)a * kAtomBytes : st;
-            const uint8_t* aLo = resident ? sA + (size_t)(KA + a) * kAtomBytes : st + kAtomBytes;
-            const uint8_t* bHi = resident ? st : st + 2 * kAtomBytes;
-            const uint8_t* bLo = bHi + 2 * kAtomBytes;
-            const uint32_t aHi_s = smem_u32(aHi), aLo_s = smem_u32(aLo);
-            const uint32_t bHi_s = smem_u32(bHi), bLo_s = smem_u32(bLo);
+            const uint32_t aHi_s = smem_u32(st), aLo_s = smem_u32(st + kAtomBytes);
+            const uint32_t bHi_s = smem_u32(st + 2 * kAtomBytes);
+            const uint32_t bLo_s = smem_u32(st + 4 * kAtomBytes);
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
-              if (a * 4 + ks < p.KS) {
-                const uint32_t off = ks * 32;
-                const uint32_t acc = (a | ks) ? 1u : 0u;
+              const int slot = a * 4 + ks;
+              const uint32_t off = ks * 32;
+              const uint32_t acc = (a | ks) ? 1u : 0u;
+              if (slot < p.KS) {
                 mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc, acc);
-                if (KIND != kSeed || p.dbg == 7) {  // the seed pass bounds with hi*hi alone (see seed_bounds)
+                if (KIND != kSeed) {
                   mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
                   mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
                 }
+              } else if (slot < p.KS + p.TS) {
+                mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, acc);
               }
             }
             mma_commit(&empty[stage]);
-            if (++stage == kStages) {
+            if (++stage == NS) {
               stage = 0;
               phase ^= 1;
             }
+          }
           }
           mma_commit(&tfull[buf]);
           if (++buf == 2) {
@@ -1183,7 +1272,7 @@ __global__ void zero_row_ptr(int64_t* row_ptr, int64_t rows) {
 
 struct Plan {
   int64_t n, rows, row_begin;
-  int k, KA, KS, t, mode, resident, alias;
+  int k, KA, KS, TS, t, mode, resident, alias;
   int64_t RB, NT, C, TPC;
   int64_t nBblocks, nAblocks;
   int64_t capacity;
@@ -1239,7 +1328,15 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   pl->mode = o->mode;
   pl->t = (int)std::max<int64_t>(1, std::min<int64_t>(o->topk, n - 1));
   pl->KA = (k + kAtomElems - 1) / kAtomElems;
-  pl->KS = (k + 15) / 16;
+  // K slots: full 16-element slots x 3 MMAs, plus the packed tail (3 products of the last
+  // k mod 16 elements in ceil(3r/16) slots) when it saves MMAs and fits the free slots of
+  // the last atom: k = 100 -> 6 x 3 + 1 = 19 MMAs per K sweep instead of 7 x 3 = 21
+  {
+    const int m = k / 16, r = k % 16, ts = (3 * r + 15) / 16;
+    const bool pack = r > 0 && ts < 3 && m + ts <= 4 * pl->KA && !getenv("GGM_NO_TAILPACK");
+    pl->KS = pack ? m : (k + 15) / 16;
+    pl->TS = pack ? ts : 0;
+  }
   pl->resident = pl->KA <= kMaxResidentAtoms ? 1 : 0;
   pl->alias = (row_begin % kRowsPerBlock) == 0 ? 1 : 0;
   pl->NT = (n + kTileN - 1) / kTileN;
@@ -1249,9 +1346,11 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   pl->NB = (n + kRowsPerBlock - 1) / kRowsPerBlock;
   const int sms = num_sms();
   const bool full_axis = row_begin == 0 && row_end == n;
-  // automatic selection keeps the plain scheme: on B200 the symmetric scheme halves the MMA
-  // work but its transposed-direction epilogue costs about what it saves
-  pl->sym = (o->mode == 0 && o->symmetric == 1 && full_axis && pl->resident) ? 1 : 0;
+  // symmetric scheme (each unordered block pair evaluated once): full axis, top-t mode, A
+  // resident; automatic (0) above kSymAutoN rows, where the seed pass and the candidate
+  // merge are small against the halved tensor-core work
+  const bool sym_ok = o->mode == 0 && full_axis && pl->resident;
+  pl->sym = sym_ok && (o->symmetric == 1 || (o->symmetric == 0 && n >= kSymAutoN)) ? 1 : 0;
   // candidates: ~ t x 16 / 2 per row expected (seed samples 1/16 of the columns, half of
   // each row's columns come from the transposed direction); regions hold 2x that on average
   // pool: 2x the expected candidates + one chunk per epilogue warp of partially used space
@@ -1429,6 +1528,7 @@ static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t
   fp.A = pl.alias ? w.Bop + (size_t)(row_begin / kRowsPerBlock) * block_bytes(pl.KA) : w.Aop;
   fp.KA = pl.KA;
   fp.KS = pl.KS;
+  fp.TS = pl.TS;
   fp.resident = pl.resident;
   fp.n = n;
   fp.row_begin = row_begin;
@@ -1486,14 +1586,15 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 8));
     absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
     scale_finalize<<<1, 1, 0, s>>>(w.sc);
-    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 8;
+    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-        V, lambda, n, k, pl.KA, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
+        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
     count_launches(3);
     if (!pl.alias) {
-      const int64_t totA = (int64_t)pl.nAblocks * kRowsPerBlock * pl.KA * 8;  // rows padded
+      const int64_t totA = (int64_t)pl.nAblocks * kRowsPerBlock * pl.KA * 16;  // rows padded
       split_tile<<<(int)std::min<int64_t>((totA + 255) / 256, sms * 16), 256, 0, s>>>(
-          V, lambda, n, k, pl.KA, row_begin, (int64_t)pl.nAblocks * kRowsPerBlock, w.sc, w.Aop);
+          V, lambda, n, k, pl.KA, pl.KS, pl.TS, row_begin, (int64_t)pl.nAblocks * kRowsPerBlock,
+          w.sc, w.Aop);
       count_launches(1);
     }
     GGM_CUDA_TRY(cudaGetLastError());
@@ -1532,9 +1633,10 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     fill_f32<<<(int)std::min<int64_t>((nthr - n + 255) / 256 + 1, sms * 8), 256, 0, s>>>(
         w.thr_p + n, nthr - n, INFINITY);
     {
-      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 8;
+      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
       split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-          V, lambda, n, k, pl.KA, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop, w.perm);
+          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop,
+          w.perm);
     }
     count_launches(3);
     GGM_CUDA_TRY(cudaGetLastError());
@@ -1560,9 +1662,9 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       // the candidate pool filled up: recompute the whole axis with the plain scheme (exact)
       // from an un-permuted split
       {
-        const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 8;
+        const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
         split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-            V, lambda, n, k, pl.KA, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
+            V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
         count_launches(1);
       }
       Plan bp = pl;

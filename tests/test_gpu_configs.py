@@ -109,7 +109,12 @@ def test_factor_config_sampled_rows_and_shards(G, name):
         prp, pc, pv = _csr_rows(rp, col, val, rows)
         st = check_topk(prp, pc, pv, V, lam, rows, t)
         assert st["exact"] + st["excused"] == len(rows)
-        # simulated ranks: concatenated shards == one call, bitwise
+        # simulated ranks: concatenated row shards (plain scheme) == one plain full-axis call,
+        # bitwise (the automatic full-axis call above may use the symmetric scheme, whose
+        # transposed-direction entries accumulate the two cross-term MMAs in swapped order)
+        ref = G.SparsePlan(n, k, 0, n, topk=t, symmetric=2)
+        ref.run(Vd, ld)
+        col, val = ref.col.cpu().numpy(), ref.val.cpu().numpy()
         for P in (2, 8):
             cols, vals = [], []
             for r in range(P):
