@@ -233,3 +233,22 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
 }
 
 }  // namespace ggm
+
+namespace ggm {
+// 1-CTA or CTA-pair MMA / commit, selected at compile time.
+template <bool PAIR>
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  if (PAIR)
+    mma_f16_ss_pair(d_tmem, a_desc, b_desc, idesc, accumulate);
+  else
+    mma_f16_ss(d_tmem, a_desc, b_desc, idesc, accumulate);
+}
+template <bool PAIR>
+__device__ __forceinline__ void mma_commit_any(uint64_t* bar) {
+  if (PAIR)
+    mma_commit_pair(bar);
+  else
+    mma_commit(bar);
+}
+}  // namespace ggm

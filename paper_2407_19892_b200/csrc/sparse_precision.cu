@@ -18,6 +18,8 @@
 //                       the transposed direction emits candidates above the seed bound)
 //   BK3  merge_partials / merge_sym / coo_to_csr  CSR assembly
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -257,27 +259,33 @@ struct FusedParams {
   uint32_t* cand_key;      // kSym: candidate pool: target row j (UINT32_MAX = unused slot)
   uint2* cand_val;         //       (source row i, ψ bits)
   int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
+  int pair;          // CTA-pair kernel (host-side selection; the kernel's template PAIR)
   int dbg;  // timing experiments only (GGM_DEBUG_EPI): 1 = TMEM loads only, 2 = no epilogue work
 };
 
-// A resident (k <= 128): a stage holds B hi and B lo of one K atom for both 128-row operand
-// blocks of the tile = 64 KB, 2 stages (the seed pass fills only the hi half).  A streamed: a
-// stage holds A hi+lo and B hi+lo of one K atom = 96 KB, 2 stages.  (4 x 32 KB stages
-// measured slower: the MMA warp, which shares its SM sub-partition with two epilogue warps,
-// then has to be woken twice as often per tile.)
-__host__ __device__ inline int num_stages(int resident) { return 2; }
-__host__ __device__ inline size_t stage_bytes(int resident) {
-  return (size_t)(resident ? 4 : 6) * kAtomBytes;
+// Operand pipeline.  1 CTA, A resident (k <= 128): a stage holds B hi and B lo of one K atom
+// for both 128-row operand blocks of the tile = 64 KB, 2 stages (the seed pass fills only the
+// hi half).  1 CTA, A streamed: A hi+lo and B hi+lo of one K atom = 96 KB, 2 stages.  CTA
+// pair (cta_group::2, A resident): each CTA holds only ITS 128-row half of the B tile, so a
+// stage is 32 KB and the pipeline is 4 deep; per-SM L2->SMEM traffic per 128x256 tile halves
+// (the 1-CTA kernel is bounded by the ~42 B/clk/SM L2 throughput at k = 100).
+__host__ __device__ inline int num_stages(int resident, int pair) {
+  return pair ? 4 : 2;
 }
-__host__ inline size_t fused_smem_bytes(int KA, int resident) {
+__host__ __device__ inline size_t stage_bytes(int resident, int pair) {
+  return (size_t)(pair ? 2 : (resident ? 4 : 6)) * kAtomBytes;
+}
+__host__ inline size_t fused_smem_bytes(int KA, int resident, int pair) {
   size_t a = resident ? block_bytes(KA) : 0;
-  return 1024 /*align slack*/ + a + num_stages(resident) * stage_bytes(resident) +
+  return 1024 /*align slack*/ + a + num_stages(resident, pair) * stage_bytes(resident, pair) +
          256 /*barriers*/ + kEpiWarps * kScratchFloats * sizeof(float);
 }
 
-// Tile enumeration shared by the producer, MMA and epilogue roles.  A unit is one 128-row
-// block rb (plus a column chunk cc for kPlain); tile s of the unit pairs two 128-column
-// operand blocks K0, K1 (the two N-halves of one 128x256 MMA tile); h1 = second half valid.
+// Tile enumeration shared by the producer, MMA and epilogue roles.  A unit is one row block
+// ub (128 rows, or 256 rows = two 128-row blocks for a CTA pair) plus a column chunk for
+// kPlain; tile s of the unit covers two 128-column operand blocks K0, K1 (the two N-halves
+// of one x256 MMA tile; h1 = second half valid).  Units are strided over the CTAs (or CTA
+// pairs): u = u0, u0 + ustep, ...
 struct TileRef {
   int K0, K1;
   bool h1;
@@ -286,83 +294,73 @@ __device__ __forceinline__ int sym_window(int rb, int NB) {
   // blocks K = rb + d (mod NB), d < W: each unordered pair {I, K} exactly once
   return (NB & 1) ? (NB + 1) / 2 : NB / 2 + (rb < NB / 2 ? 1 : 0);
 }
-template <int KIND>
-__device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& rb) {
+template <int KIND, bool PAIR>
+__device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& ub) {
   if (KIND == kPlain) {
-    rb = u / p.C;
+    ub = u / p.C;
     const int j0 = (u % p.C) * p.TPC;
     return min(p.NT, j0 + p.TPC) - j0;
   }
-  rb = u;
+  ub = u;
   if (KIND == kSeed) {
-    const int off = rb % p.SS;
+    const int off = ub % p.SS;
     return off < p.NT ? (p.NT - 1 - off) / p.SS + 1 : 0;
   }
-  return (sym_window(rb, p.NB) + 1) / 2;
+  // kSym: window over p.NB blocks (128-column blocks, or 256-column super blocks for pairs)
+  return PAIR ? sym_window(ub, p.NB) : (sym_window(ub, p.NB) + 1) / 2;
 }
-template <int KIND>
-__device__ __forceinline__ TileRef tile_ref(const FusedParams& p, int u, int rb, int s) {
-  TileRef tr;
-  if (KIND == kSym) {
-    // Visit the window [rb, rb + W) starting at X = the last row block of this wave of
-    // units (all CTAs of a wave contain X in their windows), so concurrently running CTAs
-    // stream the same column blocks in lockstep and share them through L2.
-    const int W = sym_window(rb, p.NB);
-    const int X = min(p.NB - 1, u - (int)blockIdx.x + (int)gridDim.x - 1);
-    int delta = (X - rb + p.NB) % p.NB;
-    if (delta >= W) delta = 0;
-    tr.K0 = (rb + (delta + 2 * s) % W) % p.NB;
-    tr.h1 = 2 * s + 1 < W;
-    tr.K1 = tr.h1 ? (rb + (delta + 2 * s + 1) % W) % p.NB : tr.K0;
-    return tr;
-  }
-  const int j = KIND == kPlain ? (u % p.C) * p.TPC + s : rb % p.SS + s * p.SS;
-  tr.K0 = 2 * j;
-  tr.K1 = 2 * j + 1;
-  tr.h1 = true;
-  return tr;
+// Visit the kSym window [ub, ub + W) starting at X = the last unit of this wave (all CTAs of
+// a wave contain X in their windows), so concurrently running CTAs stream the same column
+// blocks in lockstep and share them through L2.
+__device__ __forceinline__ int sym_start(const FusedParams& p, int u, int ub, int u0, int ustep,
+                                         int W) {
+  const int X = min(p.NB - 1, u - u0 + ustep - 1);
+  const int delta = (X - ub + p.NB) % p.NB;
+  return delta >= W ? 0 : delta;
 }
-
-// Incremental form of tile_ref (no integer division per tile): the producer, MMA and
-// epilogue roles walk the same sequence.
-template <int KIND>
+// Incremental enumeration (no integer division per tile).
+template <int KIND, bool PAIR>
 struct TileIter {
   int K0, K1;
   bool h1;
-  int s, rb, W, o;  // kSym: o = (delta + 2s) mod W
-  __device__ __forceinline__ void start(const FusedParams& p, int u, int rb_) {
-    rb = rb_;
+  int s, ub, W, o;  // kSym: o = window offset of the current tile
+  __device__ __forceinline__ void start(const FusedParams& p, int u, int ub_, int u0, int ustep) {
+    ub = ub_;
     s = 0;
+    h1 = true;
     if (KIND == kSym) {
-      const TileRef t0 = tile_ref<KIND>(p, u, rb, 0);
-      W = sym_window(rb, p.NB);
-      const int X = min(p.NB - 1, u - (int)blockIdx.x + (int)gridDim.x - 1);
-      int delta = (X - rb + p.NB) % p.NB;
-      if (delta >= W) delta = 0;
-      o = delta;
-      K0 = t0.K0;
-      K1 = t0.K1;
-      h1 = t0.h1;
+      W = sym_window(ub, p.NB);
+      o = sym_start(p, u, ub, u0, ustep, W);
+      place(p);
     } else {
-      const TileRef t0 = tile_ref<KIND>(p, u, rb, 0);
-      K0 = t0.K0;
-      K1 = t0.K1;
-      h1 = true;
+      const int j = KIND == kPlain ? (u % p.C) * p.TPC : ub % p.SS;
+      K0 = 2 * j;
+      K1 = 2 * j + 1;
+    }
+  }
+  __device__ __forceinline__ void place(const FusedParams& p) {
+    if (PAIR) {  // one 256-column super block J per tile
+      int J = ub + o;
+      if (J >= p.NB) J -= p.NB;
+      K0 = 2 * J;
+      K1 = 2 * J + 1;
+    } else {  // two 128-column blocks (window offsets o, o+1)
+      int o1 = o + 1;
+      if (o1 >= W) o1 -= W;
+      K0 = ub + o;
+      if (K0 >= p.NB) K0 -= p.NB;
+      h1 = 2 * s + 1 < W;
+      K1 = ub + o1;
+      if (K1 >= p.NB) K1 -= p.NB;
+      if (!h1) K1 = K0;
     }
   }
   __device__ __forceinline__ void next(const FusedParams& p) {
     ++s;
     if (KIND == kSym) {
-      o += 2;
+      o += PAIR ? 1 : 2;
       if (o >= W) o -= W;
-      int o1 = o + 1;
-      if (o1 >= W) o1 -= W;
-      K0 = rb + o;
-      if (K0 >= p.NB) K0 -= p.NB;
-      h1 = 2 * s + 1 < W;
-      K1 = rb + o1;
-      if (K1 >= p.NB) K1 -= p.NB;
-      if (!h1) K1 = K0;
+      place(p);
     } else {
       const int step = KIND == kPlain ? 2 : 2 * p.SS;
       K0 += step;
@@ -482,6 +480,16 @@ __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
   return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
 }
 
+// An epilogue warp is done with a TMEM accumulator buffer: arrive on the (pair leader's)
+// tempty barrier.
+template <bool PAIR>
+__device__ __forceinline__ void release_tmem(uint64_t* bar) {
+  if (PAIR)
+    mbar_arrive_cluster(bar, 0);
+  else
+    mbar_arrive(bar);
+}
+
 // One 32-row x 32-column chunk of the accumulator (thread = row, 32 columns in registers).
 // Fast path: one FMNMX3 chain of |v| against the row's current t-th magnitude (and, kSym, the
 // exact per-column test |ψ_ij| >= bound_j for the transposed direction).  Rare paths walk
@@ -560,10 +568,11 @@ __device__ __forceinline__ void epi_chunk(const FusedParams& p, const uint32_t (
 // columns, loaded with tcgen05.ld.32x32b.x32 into two alternating register buffers (the next
 // chunk's load is in flight while the current one is reduced).  Two warps share each row;
 // their lists are merged through shared memory at the end of a unit.
-template <int MAXT, int KIND>
+template <int MAXT, int KIND, bool PAIR>
 __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tmem_base,
                                               uint64_t* tfull, uint64_t* tempty, int warp,
-                                              int lane, float* scratch_all) {
+                                              int lane, float* scratch_all, int u0, int ustep,
+                                              int rank) {
   const int ew = warp - kFirstEpiWarp;  // 0..7; slot of (quadrant q, half h) = h*4 + ((q-first)&3)
   const int q = warp & 3;   // TMEM lane quadrant accessible to this warp
   const int h = ew >> 2;    // column half of each tile
@@ -576,9 +585,10 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   TopList<MAXT> top;
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    int rb;
-    const int ntiles = unit_tiles<KIND>(p, u, rb);
+  for (int u = u0; u < units; u += ustep) {
+    int ub;
+    const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
+    const int rb = PAIR ? 2 * ub + rank : ub;  // this CTA's 128-row block
 
     const int64_t lr = (int64_t)rb * kRowsPerBlock + r;
     const bool valid = lr < p.rows;
@@ -587,8 +597,8 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     const int64_t rlo = p.row_begin + (int64_t)rb * kRowsPerBlock;
     const int64_t rhi = rlo + kRowsPerBlock;
     top.init(t);
-    TileIter<KIND> ti;
-    ti.start(p, u, rb);
+    TileIter<KIND, PAIR> ti;
+    ti.start(p, u, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s, ti.next(p)) {
       const int Kh = h ? ti.K1 : ti.K0;
       const bool live = (h == 0 || ti.h1) && p.dbg != 2;
@@ -621,7 +631,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) release_tmem<PAIR>(&tempty[buf]);
       if (++buf == 2) {
         buf = 0;
         tphase ^= 1;
@@ -691,10 +701,11 @@ struct MagList {
     if (a > m[MAXT - 1]) m[MAXT - 1] = a;
   }
 };
-template <int MAXT>
+template <int MAXT, bool PAIR>
 __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tmem_base,
                                               uint64_t* tfull, uint64_t* tempty, int warp,
-                                              int lane, float* scratch_all) {
+                                              int lane, float* scratch_all, int u0, int ustep,
+                                              int rank) {
   const int ew = warp - kFirstEpiWarp;
   const int q = warp & 3;
   const int h = ew >> 2;
@@ -703,13 +714,14 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   MagList<MAXT> top;
-  for (int u = blockIdx.x; u < p.RB; u += gridDim.x) {
-    int rb;
-    const int ntiles = unit_tiles<kSeed>(p, u, rb);
+  for (int u = u0; u < p.RB; u += ustep) {
+    int ub;
+    const int ntiles = unit_tiles<kSeed, PAIR>(p, u, ub);
+    const int rb = PAIR ? 2 * ub + rank : ub;
     const int64_t gi = (int64_t)rb * kRowsPerBlock + r;
     top.init(t);
-    TileIter<kSeed> ti;
-    ti.start(p, u, rb);
+    TileIter<kSeed, PAIR> ti;
+    ti.start(p, u, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s, ti.next(p)) {
       const int Kh = h ? ti.K1 : ti.K0;
       const int64_t cb = (int64_t)Kh * kRowsPerBlock;
@@ -725,7 +737,7 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
       for (int c = 0; c < 4; ++c) tmem_wait_ld(v[c]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) release_tmem<PAIR>(&tempty[buf]);
       if (++buf == 2) {
         buf = 0;
         tphase ^= 1;
@@ -790,10 +802,11 @@ __device__ __forceinline__ float sel32(const uint32_t* v, uint32_t e) {
 // loaded into registers and the TMEM buffer released before the filter runs; a final merge
 // selects each row's top t among its candidates.  Fast path per 32 columns: one FMNMX3
 // chain + two compares (row bound; chunk minimum of the column bounds).
-template <int KIND>
+template <int KIND, bool PAIR>
 __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tmem_base,
                                               uint64_t* tfull, uint64_t* tempty, int warp,
-                                              int lane, float* scratch_all) {
+                                              int lane, float* scratch_all, int u0, int ustep,
+                                              int rank) {
   const int ew = warp - kFirstEpiWarp;
   const int q = warp & 3;
   const int h = ew >> 2;
@@ -807,14 +820,15 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   CandCursor cc{0, kCandChunk};
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    int rb;
-    const int ntiles = unit_tiles<KIND>(p, u, rb);
+  for (int u = u0; u < units; u += ustep) {
+    int ub;
+    const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
+    const int rb = PAIR ? 2 * ub + rank : ub;
     const int64_t gi = (int64_t)rb * kRowsPerBlock + r;  // permuted row index
     const bool valid = gi < p.n;
     const float bi = valid ? __ldg(p.thr + gi) : INFINITY;  // row bound (accumulator units)
-    TileIter<KIND> ti;
-    ti.start(p, u, rb);
+    TileIter<KIND, PAIR> ti;
+    ti.start(p, u, ub, u0, ustep);
     float4 thr_next = make_float4(0.f, 0.f, 0.f, 0.f);
     if (ntiles > 0)
       thr_next = __ldg(reinterpret_cast<const float4*>(p.thr + (int64_t)(h ? ti.K1 : ti.K0) *
@@ -822,7 +836,9 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
     for (int s = 0; s < ntiles; ++s) {
       const int Kh = h ? ti.K1 : ti.K0;
       const bool live = (h == 0 || ti.h1) && p.dbg != 2;
-      const bool emit_cols = Kh != rb;
+      // off-diagonal blocks emit the transposed direction; for a CTA pair, the diagonal
+      // 256x256 super tile covers both directions of its blocks in the row direction
+      const bool emit_cols = PAIR ? (ti.K0 >> 1) != ub : Kh != rb;
       const int64_t cb = (int64_t)Kh * kRowsPerBlock;
       const bool need_mask = Kh == rb || cb + kRowsPerBlock > p.n;
       ti.next(p);
@@ -854,7 +870,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       // the accumulator buffer is free as soon as the block is in registers
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) release_tmem<PAIR>(&tempty[buf]);
       if (++buf == 2) {
         buf = 0;
         tphase ^= 1;
@@ -943,19 +959,22 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   }
 }
 
-template <int MAXT, int KIND>
-__global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParams p) {
+template <int MAXT, int KIND, bool PAIR>
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_recon_topk(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const FusedParams p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base (pointer arithmetic keeps the shared address space visible to the
-  // compiler, so epilogue accesses through derived pointers compile to LDS/STS)
+  // compiler, so epilogue accesses through derived pointers compile to LDS/STS); the offset
+  // is the same in both CTAs of a pair (same kernel, same dynamic smem size)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int KA = p.KA;
-  const int resident = p.resident;
+  const int resident = PAIR ? 1 : p.resident;
   const size_t a_bytes = resident ? block_bytes(KA) : 0;
-  const size_t st_bytes = stage_bytes(resident);
+  const size_t st_bytes = stage_bytes(resident, PAIR);
   uint8_t* sA = smem;
   uint8_t* sStage = smem + a_bytes;
-  const int NS = num_stages(resident);
+  const int NS = num_stages(resident, PAIR);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + NS * st_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kMaxStages;
@@ -969,6 +988,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int units = KIND == kPlain ? p.RB * p.C : p.RB;
+  const int rank = PAIR ? (int)cluster_ctarank() : 0;
+  const int u0 = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
+  const int ustep = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
@@ -977,15 +999,23 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiWarps);
+      mbar_init(&tempty[b], PAIR ? 2 * kEpiWarps : kEpiWarps);  // pair: both CTAs' warps
     }
     mbar_init(afull, 1);
     mbar_init(aempty, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 0) {
+    if (PAIR)
+      tmem_alloc_pair(tmem_slot, kTmemCols);
+    else
+      tmem_alloc(tmem_slot, kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -994,35 +1024,68 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
   } else if (warp >= kFirstEpiWarp) {
     setmaxnreg_inc<kRegsEpi>();
     if (KIND == kSym)
-      epilogue_emit<KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
+      epilogue_emit<KIND, PAIR>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep, rank);
     else if (KIND == kSeed)
-      epilogue_seed<MAXT>(p, tmem_base, tfull, tempty, warp, lane, scratch);
+      epilogue_seed<MAXT, PAIR>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep, rank);
     else
-      epilogue_role<MAXT, KIND>(p, tmem_base, tfull, tempty, warp, lane, scratch);
+      epilogue_role<MAXT, KIND, PAIR>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep,
+                                      rank);
   } else {
     setmaxnreg_dec<kRegsCtl>();
-    if (warp == 0) {
-    // ===================== producer: bulk async copies global -> shared ==============
-    if (lane == 0) {
+    if (warp == 0 && lane == 0) {
+      // ===================== producer: async copies global -> shared ===================
       const uint64_t pol_b = policy_evict_last();
       const uint64_t pol_a = policy_evict_first();
       const size_t bb = block_bytes(KA);
+      const int lines_per_block = 2 * KA * kRowsPerBlock;  // 128-byte lines per 128-row block
+      if (PAIR) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      }
       int stage = 0;
       uint32_t phase = 0;
       int a_iter = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int rb;
-        const int ntiles = unit_tiles<KIND>(p, u, rb);
+      for (int u = u0; u < units; u += ustep) {
+        int ub;
+        const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
+        const int rb = PAIR ? 2 * ub + rank : ub;
         const uint8_t* Ablk = p.A + (size_t)rb * bb;
         if (resident) {
           if (a_iter > 0) mbar_wait(aempty, (a_iter - 1) & 1);
-          mbar_arrive_expect_tx(afull, (uint32_t)bb);
-          bulk_g2s(sA, Ablk, (uint32_t)bb, afull, pol_a);
+          if (PAIR) {
+            // both CTAs' A bytes are credited to the leader's barrier
+            if (rank == 0) mbar_arrive_expect_tx(afull, (uint32_t)(2 * bb));
+            for (int a = 0; a < 2 * KA; ++a)
+              tma_load_2d_pair(sA + (size_t)a * kAtomBytes, &tmA, 0,
+                               rb * lines_per_block + a * kRowsPerBlock, afull, pol_a);
+          } else {
+            mbar_arrive_expect_tx(afull, (uint32_t)bb);
+            bulk_g2s(sA, Ablk, (uint32_t)bb, afull, pol_a);
+          }
           ++a_iter;
         }
-        TileIter<KIND> ti;
-        ti.start(p, u, rb);
+        TileIter<KIND, PAIR> ti;
+        ti.start(p, u, ub, u0, ustep);
         for (int s = 0; s < ntiles; ++s, ti.next(p)) {
+          if (PAIR) {
+            // this CTA's half of the B tile: operand block K0 + rank, hi (+ lo) per K atom
+            const int bline = (ti.K0 + rank) * lines_per_block;
+            const uint32_t sbytes = (uint32_t)(KIND == kSeed ? 1 : 2) * kAtomBytes;
+            for (int a = 0; a < KA; ++a) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * sbytes);
+              uint8_t* st = sStage + stage * st_bytes;
+              tma_load_2d_pair(st, &tmB, 0, bline + a * kRowsPerBlock, &full[stage], pol_b);
+              if (KIND != kSeed)
+                tma_load_2d_pair(st + kAtomBytes, &tmB, 0, bline + (KA + a) * kRowsPerBlock,
+                                 &full[stage], pol_b);
+              if (++stage == NS) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+            continue;
+          }
           const uint8_t* B0 = p.B + (size_t)ti.K0 * bb;
           const uint8_t* B1 = p.B + (size_t)ti.K1 * bb;
           if (resident) {
@@ -1053,7 +1116,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
             bulk_g2s(st + kAtomBytes, Ablk + (size_t)(KA + a) * kAtomBytes, kAtomBytes,
                      &full[stage], pol_a);
             uint8_t* sb = st + 2 * kAtomBytes;
-            // B hi (block K0 | block K1), then B lo: 256 rows per atom, uniform 1 KB SBO
             bulk_g2s(sb, B0 + (size_t)a * kAtomBytes, kAtomBytes, &full[stage], pol_b);
             bulk_g2s(sb + kAtomBytes, B1 + (size_t)a * kAtomBytes, kAtomBytes, &full[stage],
                      pol_b);
@@ -1068,19 +1130,17 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
           }
         }
       }
-    }
-  } else if (warp == 1) {
-    // ===================== MMA issuer: one thread drives the tensor cores ==============
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32(kRowsPerBlock, kTileN);
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+      // ===================== MMA issuer: one thread (of the pair leader) ===============
+      constexpr uint32_t idesc = idesc_f16_f32(PAIR ? 2 * kRowsPerBlock : kRowsPerBlock, kTileN);
       int stage = 0;
       uint32_t phase = 0;
       int buf = 0;
       uint32_t tphase = 0;
       int a_iter = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int rb;
-        const int ntiles = unit_tiles<KIND>(p, u, rb);
+      for (int u = u0; u < units; u += ustep) {
+        int ub;
+        const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         if (resident) {
           mbar_wait(afull, a_iter & 1);
           tc_fence_after();
@@ -1089,86 +1149,67 @@ __global__ void __launch_bounds__(kThreads, 1) fused_recon_topk(const FusedParam
           mbar_wait(&tempty[buf], tphase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(buf * kTileN);
-          if (resident) {
-            const uint32_t sA_s = smem_u32(sA);
-            for (int a = 0; a < KA; ++a) {
-              const uint32_t aHi_s = sA_s + (uint32_t)(a * kAtomBytes);
-              const uint32_t aLo_s = sA_s + (uint32_t)((KA + a) * kAtomBytes);
-              mbar_wait(&full[stage], phase);
-              tc_fence_after();
-              const uint32_t bHi_s = smem_u32(sStage + stage * st_bytes);
-              const uint32_t bLo_s = bHi_s + 2 * kAtomBytes;
-#pragma unroll
-              for (int ks = 0; ks < 4; ++ks) {
-                const int slot = a * 4 + ks;
-                const uint32_t off = ks * 32;
-                const uint32_t acc = (a | ks) ? 1u : 0u;
-                if (slot < p.KS) {
-                  mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc, acc);
-                  if (KIND != kSeed) {  // the seed pass bounds with hi*hi alone (seed_bounds)
-                    mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
-                    mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
-                  }
-                } else if (slot < p.KS + p.TS) {
-                  // packed tail: A's slot in the lo array [hi|hi|lo], B's in the hi array
-                  // [hi|lo|hi] (3 products of the last k mod 16 elements in one K step)
-                  mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, acc);
-                }
-              }
-              mma_commit(&empty[stage]);
-              if (++stage == NS) {
-                stage = 0;
-                phase ^= 1;
-              }
-            }
-          } else {
           for (int a = 0; a < KA; ++a) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             uint8_t* st = sStage + stage * st_bytes;
-            const uint32_t aHi_s = smem_u32(st), aLo_s = smem_u32(st + kAtomBytes);
-            const uint32_t bHi_s = smem_u32(st + 2 * kAtomBytes);
-            const uint32_t bLo_s = smem_u32(st + 4 * kAtomBytes);
+            uint32_t aHi_s, aLo_s, bHi_s, bLo_s;
+            if (resident) {
+              aHi_s = smem_u32(sA + (size_t)a * kAtomBytes);
+              aLo_s = smem_u32(sA + (size_t)(KA + a) * kAtomBytes);
+              bHi_s = smem_u32(st);
+              bLo_s = bHi_s + (PAIR ? 1 : 2) * kAtomBytes;
+            } else {
+              aHi_s = smem_u32(st);
+              aLo_s = aHi_s + kAtomBytes;
+              bHi_s = aHi_s + 2 * kAtomBytes;
+              bLo_s = aHi_s + 4 * kAtomBytes;
+            }
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
               const int slot = a * 4 + ks;
               const uint32_t off = ks * 32;
               const uint32_t acc = (a | ks) ? 1u : 0u;
               if (slot < p.KS) {
-                mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc, acc);
-                if (KIND != kSeed) {
-                  mma_f16_ss(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
-                  mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
+                mma_f16<PAIR>(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc, acc);
+                if (KIND != kSeed) {  // the seed pass bounds with hi*hi alone (seed_bounds)
+                  mma_f16<PAIR>(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
+                  mma_f16<PAIR>(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
                 }
               } else if (slot < p.KS + p.TS) {
-                mma_f16_ss(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, acc);
+                // packed tail: A's slot in the lo array [hi|hi|lo], B's in the hi array
+                // [hi|lo|hi] (3 products of the last k mod 16 elements in one K step)
+                mma_f16<PAIR>(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, acc);
               }
             }
-            mma_commit(&empty[stage]);
+            mma_commit_any<PAIR>(&empty[stage]);
             if (++stage == NS) {
               stage = 0;
               phase ^= 1;
             }
           }
-          }
-          mma_commit(&tfull[buf]);
+          mma_commit_any<PAIR>(&tfull[buf]);
           if (++buf == 2) {
             buf = 0;
             tphase ^= 1;
           }
         }
         if (resident) {
-          mma_commit(aempty);
+          mma_commit_any<PAIR>(aempty);
           ++a_iter;
         }
       }
     }
-    }
   }
+  tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    if (PAIR)
+      tmem_dealloc_pair(tmem_base, kTmemCols);
+    else
+      tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 
@@ -1277,6 +1318,9 @@ struct Plan {
   int64_t nBblocks, nAblocks;
   int64_t capacity;
   size_t coo_temp_bytes;
+  int pair;      // CTA-pair kernels (cta_group::2), A resident only
+  int64_t RBu;   // units of row blocks: RB (1 CTA) or ceil(RB/2) 256-row blocks (pair)
+  int64_t NBu;   // kSym/kSeed units over the axis: NB or ceil(NB/2)
   int sym;       // symmetric scheme (kSeed + kSym + merge_sym)
   int SS;        // seed column-tile stride
   int64_t NB;    // 128-row blocks of the axis
@@ -1341,10 +1385,17 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   pl->alias = (row_begin % kRowsPerBlock) == 0 ? 1 : 0;
   pl->NT = (n + kTileN - 1) / kTileN;
   pl->RB = (pl->rows + kRowsPerBlock - 1) / kRowsPerBlock;
-  pl->nBblocks = pl->NT * 2;
-  pl->nAblocks = pl->alias ? 0 : pl->RB;
   pl->NB = (n + kRowsPerBlock - 1) / kRowsPerBlock;
+  // CTA pairs whenever A is resident: per-SM operand traffic halves (see num_stages)
+  pl->pair = pl->resident && !getenv("GGM_NO_PAIR") ? 1 : 0;
+  pl->RBu = pl->pair ? (pl->RB + 1) / 2 : pl->RB;
+  pl->NBu = pl->pair ? (pl->NB + 1) / 2 : pl->NB;
+  // B: all 256-row column tiles, + 2 zero blocks so a pair's second 128-row A block of an
+  // aliased row range always exists; A (unaligned row ranges): whole units
+  pl->nBblocks = pl->NT * 2 + 2;
+  pl->nAblocks = pl->alias ? 0 : (pl->pair ? 2 * pl->RBu : pl->RB);
   const int sms = num_sms();
+  const int ctas = pl->pair ? sms / 2 : sms;  // concurrent units
   const bool full_axis = row_begin == 0 && row_end == n;
   // symmetric scheme (each unordered block pair evaluated once): full axis, top-t mode, A
   // resident; automatic (0) above kSymAutoN rows, where the seed pass and the candidate
@@ -1372,7 +1423,7 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
     pl->sort_temp_bytes = std::max(tb, tb2);
   }
   int64_t C = o->col_chunks > 0 ? o->col_chunks
-                                : (pl->mode == 0 ? choose_chunks(pl->RB, pl->NT, sms) : 1);
+                                : (pl->mode == 0 ? choose_chunks(pl->RBu, pl->NT, ctas) : 1);
   C = std::max<int64_t>(1, std::min<int64_t>(C, pl->NT));
   pl->TPC = (pl->NT + C - 1) / C;
   pl->C = (pl->NT + pl->TPC - 1) / pl->TPC;  // no empty chunks
@@ -1424,7 +1475,7 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->cv_in = cv.take<float>(ncoo);
   w->cv_out = cv.take<float>(ncoo);
   w->cub_tmp = cv.take<char>(pl.coo_temp_bytes);
-  const size_t nb = pl.sym ? (size_t)pl.NB : 0;
+  const size_t nb = pl.sym ? (size_t)(2 * pl.NBu) : 0;  // 128-column blocks incl. pair padding
   const size_t ct = pl.sym ? (size_t)pl.cand_total : 0;
   w->thr = cv.take<float>(nb * kRowsPerBlock);
   w->thr_p = cv.take<float>(nb * kRowsPerBlock);
@@ -1462,30 +1513,100 @@ struct EventTimer {
   }
 };
 
-template <int MAXT, int KIND>
-static cudaError_t launch_fused_k(const FusedParams& fp, size_t smem, int grid, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(fused_recon_topk<MAXT, KIND>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  fused_recon_topk<MAXT, KIND><<<grid, kThreads, smem, st>>>(fp);
-  return cudaGetLastError();
-}
-template <int MAXT>
-static cudaError_t launch_fused_t(const FusedParams& fp, size_t smem, int grid, cudaStream_t st) {
-  return fp.kind == kPlain  ? launch_fused_k<MAXT, kPlain>(fp, smem, grid, st)
-         : fp.kind == kSeed ? launch_fused_k<MAXT, kSeed>(fp, smem, grid, st)
-                            : launch_fused_k<MAXT, kSym>(fp, smem, grid, st);
+// 2-D tensor map over a tiled operand array viewed as lines of 128 bytes (64 x uint16):
+// box = 128 lines = one 16 KB (128-row block, K atom) chunk, no swizzle (the data is already
+// stored in the SWIZZLE_128B canonical layout by split_tile).  Used by the CTA-pair kernels,
+// whose cta_group::2 tensor copies credit the pair leader's mbarrier.
+static ggm_status make_line_tmap(CUtensorMap* tm, const void* base, uint64_t lines) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(GGM_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {64, (cuuint64_t)std::max<uint64_t>(lines, 128)};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides,
+                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(GGM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return GGM_OK;
 }
 
-static cudaError_t launch_fused(const FusedParams& fp, int t, cudaStream_t s) {
-  const size_t smem = fused_smem_bytes(fp.KA, fp.resident);
+struct TMaps {
+  CUtensorMap A, B;
+};
+
+template <int MAXT, int KIND, bool PAIR>
+static cudaError_t launch_fused_k(const TMaps& tm, const FusedParams& fp, size_t smem, int grid,
+                                  cudaStream_t st) {
+  auto kern = fused_recon_topk<MAXT, KIND, PAIR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (PAIR) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  e = cudaLaunchKernelEx(&cfg, kern, tm.A, tm.B, fp);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+template <int MAXT, bool PAIR>
+static cudaError_t launch_fused_t(const TMaps& tm, const FusedParams& fp, size_t smem, int grid,
+                                  cudaStream_t st) {
+  // the candidate epilogue (kSym) keeps no per-row list: one instantiation
+  return fp.kind == kPlain  ? launch_fused_k<MAXT, kPlain, PAIR>(tm, fp, smem, grid, st)
+         : fp.kind == kSeed ? launch_fused_k<MAXT, kSeed, PAIR>(tm, fp, smem, grid, st)
+                            : launch_fused_k<5, kSym, PAIR>(tm, fp, smem, grid, st);
+}
+template <bool PAIR>
+static cudaError_t launch_fused_p(const TMaps& tm, const FusedParams& fp, int t, size_t smem,
+                                  int grid, cudaStream_t s) {
+  return t <= 5    ? launch_fused_t<5, PAIR>(tm, fp, smem, grid, s)
+         : t <= 10 ? launch_fused_t<10, PAIR>(tm, fp, smem, grid, s)
+         : t <= 16 ? launch_fused_t<16, PAIR>(tm, fp, smem, grid, s)
+                   : launch_fused_t<32, PAIR>(tm, fp, smem, grid, s);
+}
+
+// fp.pair selects the CTA-pair kernel; its tensor maps are built over fp.A / fp.B with the
+// given numbers of 128-row blocks
+static ggm_status launch_fused(const FusedParams& fp, int t, int64_t ablocks, int64_t bblocks,
+                               cudaStream_t s) {
+  const size_t smem = fused_smem_bytes(fp.KA, fp.resident, fp.pair);
   const int units = fp.kind == kPlain ? fp.RB * fp.C : fp.RB;
-  const int grid = std::max(1, std::min(num_sms(), units));
+  TMaps tm;
+  memset(&tm, 0, sizeof(tm));
+  cudaError_t ce;
   count_launches(1);
-  return t <= 5    ? launch_fused_t<5>(fp, smem, grid, s)
-         : t <= 10 ? launch_fused_t<10>(fp, smem, grid, s)
-         : t <= 16 ? launch_fused_t<16>(fp, smem, grid, s)
-                   : launch_fused_t<32>(fp, smem, grid, s);
+  if (fp.pair) {
+    const uint64_t lpb = (uint64_t)2 * fp.KA * kRowsPerBlock;
+    ggm_status st = make_line_tmap(&tm.A, fp.A, (uint64_t)ablocks * lpb);
+    if (st == GGM_OK) st = make_line_tmap(&tm.B, fp.B, (uint64_t)bblocks * lpb);
+    if (st != GGM_OK) return st;
+    const int pairs = std::max(1, std::min(num_sms() / 2, units));
+    ce = launch_fused_p<true>(tm, fp, t, smem, 2 * pairs, s);
+  } else {
+    const int grid = std::max(1, std::min(num_sms(), units));
+    ce = launch_fused_p<false>(tm, fp, t, smem, grid, s);
+  }
+  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(ce));
+  return GGM_OK;
 }
 
 template <int MAXT>
@@ -1522,6 +1643,10 @@ extern "C" ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t r
   return GGM_OK;
 }
 
+// 128-row blocks readable from fp.A (aliased into the B operand, or the separate A operand)
+static int64_t a_blocks(const Plan& pl, int64_t row_begin) {
+  return pl.alias ? pl.nBblocks - row_begin / kRowsPerBlock : pl.nAblocks;
+}
 static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t row_begin) {
   FusedParams fp{};
   fp.B = w.Bop;
@@ -1534,11 +1659,12 @@ static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t
   fp.row_begin = row_begin;
   fp.rows = pl.rows;
   fp.kind = kPlain;
-  fp.RB = (int)pl.RB;
+  fp.RB = (int)pl.RBu;
   fp.NT = (int)pl.NT;
+  fp.pair = pl.pair;
   fp.C = (int)pl.C;
   fp.TPC = (int)pl.TPC;
-  fp.NB = (int)pl.NB;
+  fp.NB = (int)pl.NBu;  // kSym window modulus (128- or 256-row blocks)
   fp.mode = pl.mode;
   fp.t = pl.t;
   fp.sc = w.sc;
@@ -1600,24 +1726,23 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     GGM_CUDA_TRY(cudaGetLastError());
   }
   FusedParams fp = base_params(pl, w, n, row_begin);
-  cudaError_t ce;
   if (pl.sym) {
     // seed: per-row t-th largest |ψ| over every 16th column tile (a lower bound of the
     // row's true t-th magnitude), padded rows +inf
-    const int64_t nthr = pl.NB * kRowsPerBlock;
+    const int64_t nthr = 2 * pl.NBu * kRowsPerBlock;
     fill_f32<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, nthr,
                                                                                INFINITY);
     count_launches(1);
     GGM_CUDA_TRY(cudaMemsetAsync(w.ckey, 0xFF, sizeof(uint32_t) * pl.cand_total, s));
     FusedParams sp = fp;
     sp.kind = kSeed;
-    sp.RB = (int)pl.NB;
+    sp.RB = (int)pl.NBu;
     sp.SS = pl.SS;
     sp.thr_out = w.thr;
     row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
         V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
-    ce = launch_fused(sp, pl.t, s);
-    if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "seed launch: %s", cudaGetErrorString(ce));
+    st = launch_fused(sp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+    if (st != GGM_OK) return st;
     seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
         w.thr, w.rn, &w.sc->rn_max_bits, n, w.sc);
     count_launches(2);
@@ -1642,14 +1767,14 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     GGM_CUDA_TRY(cudaGetLastError());
     tm.mark(1);
     fp.kind = kSym;
-    fp.RB = (int)pl.NB;
+    fp.RB = (int)pl.NBu;
     fp.thr = w.thr_p;
     fp.perm = w.perm;
     fp.cand_key = w.ckey;
     fp.cand_val = w.cval;
     fp.cand_total = pl.cand_total;
-    ce = launch_fused(fp, pl.t, s);
-    if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "sym launch: %s", cudaGetErrorString(ce));
+    st = launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+    if (st != GGM_OK) return st;
     tm.mark(2);
     // sort the candidate pool by target row (unused slots carry UINT32_MAX -> sorted last)
     DevScalars hs;
@@ -1675,8 +1800,8 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
         op.col = col;
         op.val = val;
       }
-      ce = launch_fused(op, pl.t, s);
-      if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "fallback launch: %s", cudaGetErrorString(ce));
+      st = launch_fused(op, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+      if (st != GGM_OK) return st;
       if (pl.C > 1) {
         const int blocks = (int)((pl.rows + 127) / 128);
         if (pl.t <= 5)
@@ -1693,7 +1818,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       GGM_CUDA_TRY(cudaStreamSynchronize(s));
       tm.finish();
       g_stats[0] = 0;
-      g_stats[1] = (double)pl.RB * kRowsPerBlock * pl.NT * kTileN;
+      g_stats[1] = (double)(pl.pair ? 2 * pl.RBu : pl.RB) * kRowsPerBlock * pl.NT * kTileN;
       g_stats[3] = 1;
       *nnz_out = pl.rows * pl.t;
       return GGM_OK;
@@ -1722,9 +1847,11 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     GGM_CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
     double evaluated = 0.0;  // entries evaluated by the symmetric pass (incl. masked halves)
-    for (int64_t b = 0; b < pl.NB; ++b) {
-      const int64_t W = (pl.NB & 1) ? (pl.NB + 1) / 2 : pl.NB / 2 + (b < pl.NB / 2 ? 1 : 0);
-      evaluated += (double)((W + 1) / 2) * kRowsPerBlock * kTileN;
+    for (int64_t b = 0; b < pl.NBu; ++b) {
+      const int64_t NBu = pl.NBu;
+      const int64_t W = (NBu & 1) ? (NBu + 1) / 2 : NBu / 2 + (b < NBu / 2 ? 1 : 0);
+      evaluated += pl.pair ? (double)W * 2 * kRowsPerBlock * kTileN
+                           : (double)((W + 1) / 2) * kRowsPerBlock * kTileN;
     }
     g_stats[0] = 2;
     g_stats[1] = evaluated;
@@ -1742,12 +1869,11 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
   fp.coo_count = &w.sc->coo_count;
   fp.capacity = pl.mode == 1 ? capacity : 0;
   tm.mark(1);
-  ce = launch_fused(fp, pl.t, s);
-  if (ce != cudaSuccess)
-    return fail(GGM_ERR_CUDA, "fused_recon_topk launch: %s", cudaGetErrorString(ce));
+  st = launch_fused(fp, pl.t, a_blocks(pl, row_begin), pl.nBblocks, s);
+  if (st != GGM_OK) return st;
   tm.mark(2);
   g_stats[0] = 0;
-  g_stats[1] = (double)pl.RB * kRowsPerBlock * pl.NT * kTileN;
+  g_stats[1] = (double)(pl.pair ? 2 * pl.RBu : pl.RB) * kRowsPerBlock * pl.NT * kTileN;
 
   DevScalars hs;
   if (pl.mode == 0) {
