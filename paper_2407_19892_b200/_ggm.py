@@ -13,7 +13,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libggm.so")
+# GGM_LIB_PATH: alternative build of the same library (same-session A/B experiments, tools/)
+_LIB_PATH = os.environ.get("GGM_LIB_PATH") or os.path.join(_PKG, "libggm.so")
 
 GGM_OK = 0
 STATUS_NAMES = {

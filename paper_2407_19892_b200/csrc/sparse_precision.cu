@@ -41,18 +41,26 @@ constexpr int kTileN = 256;               // N (columns of Ψ per tile; 2 operan
 constexpr int kAtomElems = 64;            // fp16 elements per 128-byte swizzle row
 constexpr int kAtomBytes = kRowsPerBlock * 128;  // one (128-row block, K atom) = 16 KB
 constexpr int kMaxStages = 4;  // operand pipeline: 4 x 32 KB (A resident) or 2 x 96 KB
-// 12 warps = 3 warpgroups: WG0 = producer (+TMEM alloc), MMA issuer, 2 idle warps, shrunk
-// to kRegsCtl registers; WG1-2 = 8 epilogue warps grown to kRegsEpi (setmaxnreg).  With 10
-// warps one SM sub-partition holds 3 warps and caps every thread at 168 registers.
-constexpr int kThreads = 384;
+// Warp layout: warpgroup 0 = producer (+TMEM alloc), MMA issuer and 2 idle warps, shrunk to
+// kRegsCtl registers (setmaxnreg); then EPW epilogue warps (EPW/4 per TMEM lane quadrant)
+// grown to regs_epi(EPW).  The list epilogue (kPlain, and the seed for t > 10) runs 8 warps
+// with 224 registers; the candidate / seed epilogues run 16 warps with 104 registers, which
+// halves each warp's TMEM read-out and processing per tile and doubles the warps available
+// to hide their latency.  (With 10 warps one SM sub-partition would hold 3 warps and cap
+// every thread at 168 registers.)
 constexpr int kFirstEpiWarp = 4;
 constexpr int kRegsCtl = 56;
-constexpr int kRegsEpi = 224;
+__host__ __device__ constexpr int threads_of(int EPW) { return (kFirstEpiWarp + EPW) * 32; }
+// setmaxnreg.inc draws only on what warpgroup 0 released: 8 warps: 384 threads launch at 168,
+// 128 x (168 - 56) = 256 x (224 - 168); 16 warps: 640 threads launch at 96,
+// 128 x (96 - 56) >= 512 x (104 - 96).
+__host__ __device__ constexpr int regs_epi(int EPW) { return EPW == 16 ? 104 : 224; }
 constexpr int kTmemCols = 512;            // 2 accumulator buffers x 256 columns
 constexpr int kMaxResidentAtoms = 2;
 // A (128 rows x KA atoms x hi/lo) stays resident in shared memory when KA <= 2 (k <= 128)
-constexpr int kEpiWarps = 8;              // epilogue warps (2 per TMEM lane quadrant)
-constexpr int kScratchFloats = 32 * 32;   // per epilogue warp: [32 values][32 lanes]
+constexpr int kEpiWarps = 8;              // list epilogue: 2 warps per TMEM lane quadrant
+constexpr int kScratchBytes = 32 * 1024;  // epilogue shared scratch (per CTA)
+constexpr int kScratchFloats = 32 * 32;   // per warp at 8 epilogue warps (half at 16)
 constexpr int kSeedStride = 8;            // seed pass samples every 8th column tile (at most)
 
 __host__ __device__ inline size_t block_bytes(int KA) { return (size_t)2 * KA * kAtomBytes; }
@@ -278,7 +286,7 @@ __host__ __device__ inline size_t stage_bytes(int resident, int pair) {
 __host__ inline size_t fused_smem_bytes(int KA, int resident, int pair) {
   size_t a = resident ? block_bytes(KA) : 0;
   return 1024 /*align slack*/ + a + num_stages(resident, pair) * stage_bytes(resident, pair) +
-         256 /*barriers*/ + kEpiWarps * kScratchFloats * sizeof(float);
+         256 /*barriers*/ + kScratchBytes;
 }
 
 // Tile enumeration shared by the producer, MMA and epilogue roles.  A unit is one row block
@@ -701,15 +709,33 @@ struct MagList {
     if (a > m[MAXT - 1]) m[MAXT - 1] = a;
   }
 };
-template <int MAXT, bool PAIR>
+// Epilogue geometry for EPW warps: warp (quadrant q = warp & 3, part) reads TMEM lanes
+// 32q..32q+31 and columns [part*W, part*W + W) of each 256-column tile, W = 256 / (EPW/4),
+// i.e. NC = W/32 chunks; those columns are operand block (part*W)/128 (K0 or K1) from column
+// offset (part*W) % 128.
+template <int EPW>
+struct EpiGeom {
+  static constexpr int P = EPW / 4;        // warps per quadrant
+  static constexpr int W = kTileN / P;     // columns per warp per tile
+  static constexpr int NC = W / 32;        // 32-column chunks per warp per tile
+  int q, part, r;
+  __device__ __forceinline__ EpiGeom(int warp, int lane) {
+    const int ew = warp - kFirstEpiWarp;
+    q = warp & 3;
+    part = ew >> 2;
+    r = q * 32 + lane;
+  }
+  __device__ __forceinline__ bool second() const { return part * W >= 128; }
+  __device__ __forceinline__ int col_off() const { return (part * W) & 127; }
+};
+
+template <int MAXT, bool PAIR, int EPW>
 __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tmem_base,
                                               uint64_t* tfull, uint64_t* tempty, int warp,
                                               int lane, float* scratch_all, int u0, int ustep,
                                               int rank) {
-  const int ew = warp - kFirstEpiWarp;
-  const int q = warp & 3;
-  const int h = ew >> 2;
-  const int r = q * 32 + lane;
+  using G = EpiGeom<EPW>;
+  const G g(warp, lane);
   const int t = p.t;
   int buf = 0;
   uint32_t tphase = 0;
@@ -718,23 +744,23 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
     int ub;
     const int ntiles = unit_tiles<kSeed, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
-    const int64_t gi = (int64_t)rb * kRowsPerBlock + r;
+    const int64_t gi = (int64_t)rb * kRowsPerBlock + g.r;
     top.init(t);
     TileIter<kSeed, PAIR> ti;
     ti.start(p, u, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s, ti.next(p)) {
-      const int Kh = h ? ti.K1 : ti.K0;
-      const int64_t cb = (int64_t)Kh * kRowsPerBlock;
-      const bool need_mask = Kh == rb || cb + kRowsPerBlock > p.n;
+      const int Kh = g.second() ? ti.K1 : ti.K0;
+      const int64_t cb = (int64_t)Kh * kRowsPerBlock + g.col_off();
+      const bool need_mask = Kh == rb || cb + G::W > p.n;
       mbar_wait(&tfull[buf], tphase);
       tc_fence_after();
-      const uint32_t taddr =
-          tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTileN + h * (kTileN / 2));
-      uint32_t v[4][32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(g.q * 32) << 16) +
+                             (uint32_t)(buf * kTileN + g.part * G::W);
+      uint32_t v[G::NC][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+      for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_wait_ld(v[c]);
+      for (int c = 0; c < G::NC; ++c) tmem_wait_ld(v[c]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) release_tmem<PAIR>(&tempty[buf]);
@@ -742,12 +768,12 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
         buf = 0;
         tphase ^= 1;
       }
-      if (p.dbg != 0 && p.dbg != 7) {
-        if (v[0][0] == 12345u && v[3][31] == 54321u) p.thr_out[0] = __uint_as_float(v[1][7]);
+      if (p.dbg != 0) {
+        if (v[0][0] == 12345u && v[G::NC - 1][31] == 54321u) p.thr_out[0] = __uint_as_float(v[0][7]);
         continue;
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < G::NC; ++c) {
         float m = max32_abs(reinterpret_cast<const float(&)[32]>(v[c]));
         if (need_mask) {
           const int64_t col0 = cb + c * 32;
@@ -759,23 +785,26 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
         if (m > top.m[0]) top.insert(m);
       }
     }
-    // merge the two column halves: half 1 publishes its list, half 0 inserts and writes
-    float* pv = scratch_all + (4 + ((q - kFirstEpiWarp) & 3)) * kScratchFloats;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-    if (h == 1) {
+    // merge the quadrant's P lists: parts 1..P-1 publish, part 0 inserts and writes
+    float* slot = scratch_all + (size_t)(warp - kFirstEpiWarp) * (kScratchBytes / 4 / EPW);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g.q), "r"(32 * G::P) : "memory");
+    if (g.part != 0) {
 #pragma unroll
-      for (int a = 0; a < MAXT; ++a) pv[a * 32 + lane] = top.m[a];
+      for (int a = 0; a < MAXT; ++a) slot[a * 32 + lane] = top.m[a];
     }
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-    if (h == 0) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g.q), "r"(32 * G::P) : "memory");
+    if (g.part == 0) {
+      for (int pp = 1; pp < G::P; ++pp) {
+        const float* o = scratch_all + (size_t)(warp - kFirstEpiWarp + 4 * pp) * (kScratchBytes / 4 / EPW);
 #pragma unroll 1
-      for (int a = 0; a < t; ++a) {
-        const float x = pv[a * 32 + lane];
-        if (x > top.m[0]) top.insert(x);
+        for (int a = 0; a < t; ++a) {
+          const float x = o[a * 32 + lane];
+          if (x > top.m[0]) top.insert(x);
+        }
       }
       if (gi < p.n) p.thr_out[gi] = top.m[0];  // -1: fewer than t chunks sampled
     }
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g.q), "r"(32 * G::P) : "memory");
   }
 }
 
@@ -802,16 +831,16 @@ __device__ __forceinline__ float sel32(const uint32_t* v, uint32_t e) {
 // loaded into registers and the TMEM buffer released before the filter runs; a final merge
 // selects each row's top t among its candidates.  Fast path per 32 columns: one FMNMX3
 // chain + two compares (row bound; chunk minimum of the column bounds).
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, int EPW>
 __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tmem_base,
                                               uint64_t* tfull, uint64_t* tempty, int warp,
                                               int lane, float* scratch_all, int u0, int ustep,
                                               int rank) {
-  const int ew = warp - kFirstEpiWarp;
-  const int q = warp & 3;
-  const int h = ew >> 2;
-  const int r = q * 32 + lane;
-  float* thr_w = scratch_all + ew * kScratchFloats;  // this warp's 128 column bounds
+  using G = EpiGeom<EPW>;
+  constexpr int VPL = G::W / 32;  // column bounds per lane (4 or 2)
+  const G g(warp, lane);
+  // this warp's W column bounds
+  float* thr_w = scratch_all + (size_t)(warp - kFirstEpiWarp) * (kScratchBytes / 4 / EPW);
   const float sd = ldexpf(1.f, -p.sc->exp2);
   const float sd2 = sd * sd;
   const int units = p.RB;
@@ -824,48 +853,58 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
-    const int64_t gi = (int64_t)rb * kRowsPerBlock + r;  // permuted row index
+    const int64_t gi = (int64_t)rb * kRowsPerBlock + g.r;  // permuted row index
     const bool valid = gi < p.n;
     const float bi = valid ? __ldg(p.thr + gi) : INFINITY;  // row bound (accumulator units)
     TileIter<KIND, PAIR> ti;
     ti.start(p, u, ub, u0, ustep);
-    float4 thr_next = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (ntiles > 0)
-      thr_next = __ldg(reinterpret_cast<const float4*>(p.thr + (int64_t)(h ? ti.K1 : ti.K0) *
-                                                               kRowsPerBlock) + lane);
+    float tn[VPL];
+    auto load_bounds = [&](const TileIter<KIND, PAIR>& it) {
+      const float* src = p.thr + (int64_t)(g.second() ? it.K1 : it.K0) * kRowsPerBlock +
+                         g.col_off() + lane * VPL;
+      if (VPL == 4) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+        tn[0] = x.x; tn[1] = x.y; tn[VPL > 2 ? 2 : 0] = x.z; tn[VPL > 3 ? 3 : 0] = x.w;
+      } else {
+        const float2 x = __ldg(reinterpret_cast<const float2*>(src));
+        tn[0] = x.x; tn[1] = x.y;
+      }
+    };
+    if (ntiles > 0) load_bounds(ti);
     for (int s = 0; s < ntiles; ++s) {
-      const int Kh = h ? ti.K1 : ti.K0;
-      const bool live = (h == 0 || ti.h1) && p.dbg != 2;
+      const int Kh = g.second() ? ti.K1 : ti.K0;
+      const bool live = (!g.second() || ti.h1) && p.dbg != 2;
       // off-diagonal blocks emit the transposed direction; for a CTA pair, the diagonal
       // 256x256 super tile covers both directions of its blocks in the row direction
       const bool emit_cols = PAIR ? (ti.K0 >> 1) != ub : Kh != rb;
-      const int64_t cb = (int64_t)Kh * kRowsPerBlock;
-      const bool need_mask = Kh == rb || cb + kRowsPerBlock > p.n;
+      const int64_t cb = (int64_t)Kh * kRowsPerBlock + g.col_off();
+      const bool need_mask = Kh == rb || cb + G::W > p.n;
       ti.next(p);
-      // stage the block's 128 column bounds; chunk minima by shuffles
-      float cm = fminf(fminf(thr_next.x, thr_next.y), fminf(thr_next.z, thr_next.w));
-      cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
-      cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
-      cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, 4));
-      float cmin[4];
+      // stage the W column bounds; chunk minima by shuffles within each chunk's lanes
+      float cm = tn[0];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) cmin[c] = emit_cols ? __shfl_sync(0xffffffffu, cm, 8 * c) : INFINITY;
+      for (int e = 1; e < VPL; ++e) cm = fminf(cm, tn[e]);
+#pragma unroll
+      for (int o = 1; o < 32 / VPL; o <<= 1) cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+      float cmin[G::NC];
+#pragma unroll
+      for (int c = 0; c < G::NC; ++c)
+        cmin[c] = emit_cols ? __shfl_sync(0xffffffffu, cm, c * (32 / VPL)) : INFINITY;
       __syncwarp();
-      reinterpret_cast<float4*>(thr_w)[lane] = thr_next;
+#pragma unroll
+      for (int e = 0; e < VPL; ++e) thr_w[lane * VPL + e] = tn[e];
       __syncwarp();
-      if (s + 1 < ntiles)
-        thr_next = __ldg(reinterpret_cast<const float4*>(p.thr + (int64_t)(h ? ti.K1 : ti.K0) *
-                                                                 kRowsPerBlock) + lane);
+      if (s + 1 < ntiles) load_bounds(ti);
       mbar_wait(&tfull[buf], tphase);
       tc_fence_after();
-      const uint32_t taddr =
-          tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTileN + h * (kTileN / 2));
-      uint32_t v[4][32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(g.q * 32) << 16) +
+                             (uint32_t)(buf * kTileN + g.part * G::W);
+      uint32_t v[G::NC][32];
       if (live) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+        for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_wait_ld(v[c]);
+        for (int c = 0; c < G::NC; ++c) tmem_wait_ld(v[c]);
       }
       // the accumulator buffer is free as soon as the block is in registers
       tc_fence_before();
@@ -876,11 +915,11 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         tphase ^= 1;
       }
       if (!live || p.dbg == 1) {
-        if (live && v[0][0] == 12345u && v[3][31] == 54321u) p.row_ptr[0] = (int64_t)v[1][7];
+        if (live && v[0][0] == 12345u && v[G::NC - 1][31] == 54321u) p.row_ptr[0] = (int64_t)v[0][7];
         continue;
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < G::NC; ++c) {
         const int64_t col0 = cb + c * 32;
         float m = max32_abs(reinterpret_cast<const float(&)[32]>(v[c]));
         uint32_t excl = 0;  // diagonal (Q8) and padding columns
@@ -907,12 +946,12 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         if (ch) {
           const float4* t4 = reinterpret_cast<const float4*>(thr_w + c * 32);
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            const float4 th = t4[g];
-            mc |= (fabsf(__uint_as_float(v[c][4 * g + 0])) >= th.x ? 1u : 0u) << (4 * g + 0);
-            mc |= (fabsf(__uint_as_float(v[c][4 * g + 1])) >= th.y ? 1u : 0u) << (4 * g + 1);
-            mc |= (fabsf(__uint_as_float(v[c][4 * g + 2])) >= th.z ? 1u : 0u) << (4 * g + 2);
-            mc |= (fabsf(__uint_as_float(v[c][4 * g + 3])) >= th.w ? 1u : 0u) << (4 * g + 3);
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 th = t4[q4];
+            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 0])) >= th.x ? 1u : 0u) << (4 * q4 + 0);
+            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 1])) >= th.y ? 1u : 0u) << (4 * q4 + 1);
+            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 2])) >= th.z ? 1u : 0u) << (4 * q4 + 2);
+            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 3])) >= th.w ? 1u : 0u) << (4 * q4 + 3);
           }
           mc &= ~excl;
         }
@@ -959,8 +998,19 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   }
 }
 
-template <int MAXT, int KIND, bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1)
+// Epilogue warps per kind: 16 for the candidate and seed epilogues (t <= 10), else 8.
+#ifndef GGM_SEED_EPW
+#define GGM_SEED_EPW 16
+#endif
+#ifndef GGM_SYM_EPW
+#define GGM_SYM_EPW 16
+#endif
+__host__ __device__ constexpr int epw_of(int KIND, int MAXT) {
+  return KIND == kSym ? GGM_SYM_EPW : (KIND == kSeed && MAXT <= 10) ? GGM_SEED_EPW : 8;
+}
+
+template <int MAXT, int KIND, bool PAIR, int EPW = epw_of(KIND, MAXT)>
+__global__ void __launch_bounds__(threads_of(EPW), 1)
     fused_recon_topk(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, const FusedParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -999,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], PAIR ? 2 * kEpiWarps : kEpiWarps);  // pair: both CTAs' warps
+      mbar_init(&tempty[b], PAIR ? 2 * EPW : EPW);  // pair: both CTAs' epilogue warps
     }
     mbar_init(afull, 1);
     mbar_init(aempty, 1);
@@ -1022,11 +1072,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.sc->flags != 0) {
     // invalid input: skip all work (status reported by the host after synchronising)
   } else if (warp >= kFirstEpiWarp) {
-    setmaxnreg_inc<kRegsEpi>();
+    setmaxnreg_inc<regs_epi(EPW)>();
     if (KIND == kSym)
-      epilogue_emit<KIND, PAIR>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep, rank);
+      epilogue_emit<KIND, PAIR, EPW>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep,
+                                     rank);
     else if (KIND == kSeed)
-      epilogue_seed<MAXT, PAIR>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep, rank);
+      epilogue_seed<MAXT, PAIR, EPW>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep,
+                                     rank);
     else
       epilogue_role<MAXT, KIND, PAIR>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep,
                                       rank);
@@ -1411,7 +1463,7 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(kSeedStride, pl->NT));
   if (const char* e = getenv("GGM_SEED_STRIDE"))  // tuning experiments only
     pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(atoi(e), pl->NT));
-  pl->cand_total = pl->sym ? n * 2 * pl->SS * pl->t + (int64_t)sms * kEpiWarps * kCandChunk * 2 : 0;
+  pl->cand_total = pl->sym ? n * 2 * pl->SS * pl->t + (int64_t)sms * 16 * kCandChunk * 2 : 0;
   pl->sort_temp_bytes = 0;
   if (pl->sym) {
     size_t tb = 0;
@@ -1551,7 +1603,7 @@ static cudaError_t launch_fused_k(const TMaps& tm, const FusedParams& fp, size_t
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.blockDim = dim3(threads_of(epw_of(KIND, MAXT)), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
