@@ -270,13 +270,18 @@ def main():
     stream = torch.cuda.current_stream()
 
     fused_ms = [[] for _ in plans]
+    stage_ms = [[] for _ in plans]   # (prep incl. seed pass, main kernel, merge) per call
+    stats = [None for _ in plans]
     launches = [0]
 
     def step(record=False):
         for a, (plan, (V, lam)) in enumerate(zip(plans, dev_axes)):
             plan.run(V, lam)
             if record:
-                fused_ms[a].append(G.last_timing()[1])
+                tm = G.last_timing()
+                fused_ms[a].append(tm[1])
+                stage_ms[a].append(tuple(tm))
+                stats[a] = G.last_stats()
                 launches[0] += G.last_launches()
             if world > 1:
                 gather_topk_csr(plan.col, plan.val, plan.t_eff, V.shape[0])
@@ -312,7 +317,13 @@ def main():
     n0, k0 = V0.shape
     rows0 = plans[a0].row_end - plans[a0].row_begin
     avg_fused = float(np.mean(fused_ms[a0]))
-    alg_flops = 2.0 * k0 * rows0 * n0                     # 2k flops / entry
+    st0 = stats[a0]
+    sym0 = st0["scheme"] == "symmetric"
+    # algorithmic work of the dominant kernel: 2k flops per entry it must
+    # evaluate -- all rows x n entries (plain), or each unordered pair once, n(n+1)/2 entries
+    # (symmetric scheme: ψ_ij = ψ_ji)
+    alg_entries = n0 * (n0 + 1) / 2.0 if sym0 else float(rows0) * n0
+    alg_flops = 2.0 * k0 * alg_entries
     achieved = alg_flops / (avg_fused * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
     traffic = None
@@ -380,13 +391,20 @@ def main():
                        "parallelism": f"row-shard x{world}", "l2": "inputs > L2 (no flush needed)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "fused_recon_topk (BK2)",
-                         "achieved_basis": "2k flops per entry (SURVEY 8(d)) x rows x n / mean CUDA-event "
-                                           "duration of BK2 on the largest axis",
+                         "kernel": "fused_recon_topk (BK2, %s scheme%s)" % (
+                             st0["scheme"], ", CTA pairs" if st0["cta_pair"] else ""),
+                         "achieved_basis": "2k flops per entry (SURVEY 8(d)) x %s / mean CUDA-event "
+                                           "duration of BK2 on the largest axis" % (
+                                               "n(n+1)/2 unordered entries" if sym0 else "rows x n"),
                          "peak_basis": f"{peak_src} bf16_tflops_sustained / 3 (3-term fp16 split = 3 MMAs "
                                        "per fp32-accurate product; fp16 rate = bf16 rate)",
                          "kernel_ms": avg_fused, "step_share": step_ms_fused_share,
-                         "tensor_pipe_tflops": achieved * 3.0 * (16 * ((k0 + 15) // 16)) / k0},
+                         "tensor_pipe_tflops": st0["entries_main"] * 2.0 * st0["mma_k_per_entry"]
+                         / (avg_fused * 1e-3) / 1e12,
+                         "stages_ms_axis": {"prep_incl_seed": float(np.mean([x[0] for x in stage_ms[a0]])),
+                                            "main": avg_fused,
+                                            "merge": float(np.mean([x[2] for x in stage_ms[a0]]))},
+                         "candidates_per_row": st0["candidates"] / n0 if sym0 else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,

@@ -190,9 +190,11 @@ void ggm_last_timing(float ms[3]);
 int ggm_last_launches(void);
 /* Statistics of the last ggm_sparse_precision call on this thread: out[0] = scheme (0 plain,
  * 2 symmetric), out[1] = entries evaluated by the main fused kernel (incl. padding),
- * out[2] = transposed-direction candidates emitted, out[3] = row blocks recomputed after a
- * candidate-bucket overflow. */
-void ggm_last_stats(double out[4]);
+ * out[2] = candidates emitted (symmetric scheme), out[3] = 1 if the symmetric scheme's
+ * candidate pool overflowed and the axis was recomputed with the plain scheme, out[4] = MMA
+ * K elements issued per evaluated entry (16 x (3 full slots + packed tail slots)), out[5] =
+ * 1 if the CTA-pair (cta_group::2) kernels ran. */
+void ggm_last_stats(double out[6]);
 
 #ifdef __cplusplus
 }

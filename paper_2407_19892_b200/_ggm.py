@@ -256,10 +256,11 @@ def set_timing(enabled: bool):
 
 
 def last_stats() -> dict:
-    arr = (C.c_double * 4)()
+    arr = (C.c_double * 6)()
     lib().ggm_last_stats(arr)
     return {"scheme": "symmetric" if arr[0] == 2 else "plain", "entries_main": arr[1],
-            "candidates": int(arr[2]), "recomputed_blocks": int(arr[3])}
+            "candidates": int(arr[2]), "recomputed": int(arr[3]),
+            "mma_k_per_entry": int(arr[4]), "cta_pair": bool(arr[5])}
 
 
 def last_launches() -> int:

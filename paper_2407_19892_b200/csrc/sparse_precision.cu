@@ -1670,7 +1670,7 @@ static void launch_merge_sym_t(const Work& w, const Plan& pl, int64_t ncand, int
                                              col, val);
 }
 
-static thread_local double g_stats[4] = {0, 0, 0, 0};
+static thread_local double g_stats[6] = {0, 0, 0, 0, 0, 0};
 
 }  // namespace sp
 }  // namespace ggm
@@ -1678,8 +1678,8 @@ static thread_local double g_stats[4] = {0, 0, 0, 0};
 using namespace ggm;
 using namespace ggm::sp;
 
-extern "C" void ggm_last_stats(double out[4]) {
-  for (int i = 0; i < 4; ++i) out[i] = g_stats[i];
+extern "C" void ggm_last_stats(double out[6]) {
+  for (int i = 0; i < 6; ++i) out[i] = g_stats[i];
 }
 
 extern "C" ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t row_begin,
@@ -1755,6 +1755,8 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   reset_launches();
   for (double& x : g_stats) x = 0.0;
+  g_stats[4] = 16.0 * (3 * pl.KS + pl.TS);  // MMA K elements issued per evaluated entry
+  g_stats[5] = pl.pair;
   EventTimer tm(timing_enabled(), s);
   tm.mark(0);
   GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
