@@ -490,9 +490,11 @@ __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
 
 // An epilogue warp is done with a TMEM accumulator buffer: arrive on the (pair leader's)
 // tempty barrier.
+// The data was already waited into registers (tcgen05.wait::ld), so the arrive needs no
+// cluster-scope release fence: the leader's own warps arrive locally, the peer's remotely.
 template <bool PAIR>
 __device__ __forceinline__ void release_tmem(uint64_t* bar) {
-  if (PAIR)
+  if (PAIR && cluster_ctarank() != 0)
     mbar_arrive_cluster(bar, 0);
   else
     mbar_arrive(bar);
