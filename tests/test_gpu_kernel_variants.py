@@ -1,0 +1,98 @@
+"""GPU parity of the BK2 kernel variants added for speed, each against the fp64 oracle and
+against the reference variant it replaces (through the C ABI):
+
+  * CTA pairs (tcgen05 cta_group::2, M = 256 over two SMs) vs the 1-CTA kernel
+    (GGM_NO_PAIR=1): the same fp16 products accumulated in the same K order, so bitwise equal;
+  * the packed K tail (3 products of the last k mod 16 elements in one MMA slot) vs the
+    padded tail (GGM_NO_TAILPACK=1): same products, different accumulation order;
+  * the symmetric scheme's seed bounds at small t (t = 1, 2, 3 make any overestimated bound
+    visible as a missing entry) and with the seed stride forced to 1 and 16.
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import gen
+from parity_util import check_topk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2407_19892_b200 as G
+    assert torch.cuda.is_available()
+    assert G.device_supported(), "needs an sm_100a (B200) device"
+    return G
+
+
+def _run(G, V, lam, row_begin=0, row_end=None, **kw):
+    Vd = torch.from_numpy(V).cuda()
+    ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
+    rp, c, v = G.ggm_sparse_precision(Vd, ld, row_begin, row_end, **kw)
+    torch.cuda.synchronize()
+    return rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy(), G.last_stats()
+
+
+@pytest.mark.parametrize("n,k,t,rb,re,sym", [(1500, 100, 10, 0, 1500, 2), (1500, 64, 5, 0, 1500, 2),
+                                             (1000, 37, 10, 130, 901, 2), (3000, 100, 10, 0, 3000, 1),
+                                             (777, 128, 16, 0, 777, 2)])
+def test_cta_pair_matches_single_cta(G, monkeypatch, n, k, t, rb, re, sym):
+    V, lam = gen.small_factor(1000 + n + k, n, k)
+    rp, c, v, st = _run(G, V, lam, rb, re, topk=t, symmetric=sym)
+    assert st["cta_pair"]
+    monkeypatch.setenv("GGM_NO_PAIR", "1")
+    rp1, c1, v1, st1 = _run(G, V, lam, rb, re, topk=t, symmetric=sym)
+    assert not st1["cta_pair"]
+    assert np.array_equal(rp, rp1) and np.array_equal(c, c1)
+    if sym == 2:
+        np.testing.assert_array_equal(v, v1)
+    else:
+        # symmetric scheme: the 256x256 super tiles of the pair evaluate some entries as
+        # (j, i) where the 1-CTA 128-block windows evaluate (i, j): the two cross-term MMAs
+        # accumulate in swapped order (a few ulp)
+        np.testing.assert_allclose(v, v1, rtol=1e-6, atol=0)
+    check_topk(rp, c, v, V, lam, np.arange(rb, re), t)
+
+
+@pytest.mark.parametrize("k", [1, 5, 16, 17, 37, 50, 100, 116, 120, 128])
+def test_packed_tail_vs_padded(G, monkeypatch, k):
+    n, t = 1200, 10
+    V, lam = gen.small_factor(2000 + k, n, k)
+    rp, c, v, st = _run(G, V, lam, 0, n, topk=t, symmetric=2)
+    r = k % 16
+    packed = r > 0 and (3 * r + 15) // 16 < 3 and k // 16 + (3 * r + 15) // 16 <= 4 * ((k + 63) // 64)
+    want_k = 16 * (3 * (k // 16) + (3 * r + 15) // 16) if packed else 48 * ((k + 15) // 16)
+    assert st["mma_k_per_entry"] == want_k
+    check_topk(rp, c, v, V, lam, np.arange(n), t)
+    monkeypatch.setenv("GGM_NO_TAILPACK", "1")
+    rp2, c2, v2, st2 = _run(G, V, lam, 0, n, topk=t, symmetric=2)
+    assert st2["mma_k_per_entry"] == 48 * ((k + 15) // 16)
+    same = np.mean([np.array_equal(c[rp[i]:rp[i + 1]], c2[rp2[i]:rp2[i + 1]]) for i in range(n)])
+    assert same > 0.995
+    np.testing.assert_allclose(v[np.isin(c, c2)][:50], v2[np.isin(c2, c)][:50], rtol=1e-5, atol=1e-9)
+
+
+@pytest.mark.parametrize("n,k,t,ss", [(4000, 64, 1, None), (4000, 64, 2, None), (5000, 100, 3, None),
+                                      (3000, 48, 3, "1"), (6000, 32, 10, "16"), (2600, 100, 32, None)])
+def test_symmetric_seed_bounds_small_t(G, monkeypatch, n, k, t, ss):
+    """An overestimated seed bound drops entries from a row's candidates; t <= 3 makes that
+    visible (the t-th magnitude is close to the largest)."""
+    if ss is not None:
+        monkeypatch.setenv("GGM_SEED_STRIDE", ss)
+    V, lam = gen.small_factor(3000 + n + t, n, k)
+    rp, c, v, st = _run(G, V, lam, 0, n, topk=t, symmetric=1)
+    assert st["scheme"] == "symmetric" and st["recomputed"] == 0
+    res = check_topk(rp, c, v, V, lam, np.arange(n), t)
+    assert res["exact"] + res["excused"] == n
+
+
+def test_symmetric_single_cta_matches_pair(G, monkeypatch):
+    n, k, t = 5000, 100, 10
+    V, lam = gen.small_factor(77, n, k)
+    rp, c, v, st = _run(G, V, lam, 0, n, topk=t, symmetric=1)
+    monkeypatch.setenv("GGM_NO_PAIR", "1")
+    rp1, c1, v1, st1 = _run(G, V, lam, 0, n, topk=t, symmetric=1)
+    assert st["cta_pair"] and not st1["cta_pair"]
+    assert np.mean([np.array_equal(c[rp[i]:rp[i + 1]], c1[rp1[i]:rp1[i + 1]]) for i in range(n)]) > 0.999
+    check_topk(rp1, c1, v1, V, lam, np.arange(n), t)
