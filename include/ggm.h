@@ -159,10 +159,10 @@ typedef struct {
   int symmetric;  /* scheme selection, mode 0 over the FULL axis (row_begin = 0, row_end = n)
                      with k <= 128 only (otherwise always plain):
                      0 = automatic (symmetric for n >= 65536), 1 = symmetric, 2 = plain.
-                     Symmetric scheme (Ψ = Ψ^T): a seed pass over every 8th column
-                     tile (hi·hi products) gives each row i a lower bound b_i of its t-th |ψ|
-                     (t-th largest 32-column chunk maximum, minus the hi·hi rounding bound
-                     2^-10·1.1·||U_i||·max_j||U_j||); rows are reordered by b_i; each
+                     Symmetric scheme (Ψ = Ψ^T): a seed pass over the n/64 columns of
+                     largest ||U_j|| (hi·hi products) gives each row i a lower bound b_i of
+                     its t-th |ψ| (t-th largest 32-column chunk maximum, minus the hi·hi
+                     rounding bound 2^-10·1.1·||U_i||·max_j||U_j||); rows are reordered by b_i; each
                      unordered 128x128 block pair is then evaluated once (cyclic window per
                      row block) and entry ψ_ij is kept as a candidate of row i if
                      |ψ| >= b_i and of row j if |ψ| >= b_j; a CUB sort by row and a merge

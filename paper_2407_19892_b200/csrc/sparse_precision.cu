@@ -61,7 +61,7 @@ constexpr int kMaxResidentAtoms = 2;
 constexpr int kEpiWarps = 8;              // list epilogue: 2 warps per TMEM lane quadrant
 constexpr int kScratchBytes = 32 * 1024;  // epilogue shared scratch (per CTA)
 constexpr int kScratchFloats = 32 * 32;   // per warp at 8 epilogue warps (half at 16)
-constexpr int kSeedStride = 8;            // seed pass samples every 8th column tile (at most)
+constexpr int kSeedFrac = 64;  // seed pass: the n/64 largest-norm columns (see make_plan)
 
 __host__ __device__ inline size_t block_bytes(int KA) { return (size_t)2 * KA * kAtomBytes; }
 
@@ -246,7 +246,7 @@ struct FusedParams {
   int kind;          // Kind
   int RB, NT, C, TPC;
   int NB;            // kSym: 128-row blocks of the axis (row_begin == 0, rows == n)
-  int SS;            // kSeed: column-tile stride of the sample
+  int SS;            // kSeed: number of 256-column tiles in the sample (the first ones)
   int mode, t;
   float tau;
   const DevScalars* sc;
@@ -310,10 +310,7 @@ __device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& ub) 
     return min(p.NT, j0 + p.TPC) - j0;
   }
   ub = u;
-  if (KIND == kSeed) {
-    const int off = ub % p.SS;
-    return off < p.NT ? (p.NT - 1 - off) / p.SS + 1 : 0;
-  }
+  if (KIND == kSeed) return p.SS;  // the sample: the first SS column tiles
   // kSym: window over p.NB blocks (128-column blocks, or 256-column super blocks for pairs)
   return PAIR ? sym_window(ub, p.NB) : (sym_window(ub, p.NB) + 1) / 2;
 }
@@ -341,7 +338,7 @@ struct TileIter {
       o = sym_start(p, u, ub, u0, ustep, W);
       place(p);
     } else {
-      const int j = KIND == kPlain ? (u % p.C) * p.TPC : ub % p.SS;
+      const int j = KIND == kPlain ? (u % p.C) * p.TPC : 0;
       K0 = 2 * j;
       K1 = 2 * j + 1;
     }
@@ -370,9 +367,8 @@ struct TileIter {
       if (o >= W) o -= W;
       place(p);
     } else {
-      const int step = KIND == kPlain ? 2 : 2 * p.SS;
-      K0 += step;
-      K1 += step;
+      K0 += 2;
+      K1 += 2;
     }
   }
 };
@@ -1462,10 +1458,24 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // candidates: each row's entries >= its bound b_i (the t-th largest over a 1/SS column
   // sample, i.e. about the (SS t)-th largest overall): ~SS t per row, from both directions;
   // the pool holds 2x that plus the partially used reservation of every epilogue warp
-  pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(kSeedStride, pl->NT));
-  if (const char* e = getenv("GGM_SEED_STRIDE"))  // tuning experiments only
-    pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(atoi(e), pl->NT));
-  pl->cand_total = pl->sym ? n * 2 * pl->SS * pl->t + (int64_t)sms * 16 * kCandChunk * 2 : 0;
+  // seed sample: the n/kSeedFrac columns of largest ||U_j|| (whole 256-column tiles, at
+  // least one).  |ψ_ij| <= ||U_i|| ||U_j||, so large-norm columns hold most rows' largest
+  // entries: on C5 factors the t-th largest over this 1/64 sample leaves ~21 candidates per
+  // row where a strided 1/8 sample left ~89 (any sample gives a valid bound).
+  {
+    int64_t frac = kSeedFrac;
+    if (const char* e = getenv("GGM_SEED_FRAC")) frac = std::max(1, atoi(e));  // tuning only
+    // at least 8 tiles (2048 columns): small axes get a proportionally larger sample
+    const int64_t tiles = std::max<int64_t>(8, (n / frac + kTileN - 1) / kTileN);
+    pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(pl->NT, tiles));
+  }
+  // pool: an uninformative sample leaves ~ t x (n / sample size) candidates per row; hold
+  // twice that, capped at 32 t per row (overflow -> exact plain recomputation)
+  {
+    const int64_t ratio = (n + pl->SS * kTileN - 1) / (pl->SS * kTileN);
+    const int64_t per_row = pl->t * std::max<int64_t>(4, std::min<int64_t>(2 * ratio, 32));
+    pl->cand_total = pl->sym ? n * per_row + (int64_t)sms * 16 * kCandChunk * 2 : 0;
+  }
   pl->sort_temp_bytes = 0;
   if (pl->sym) {
     size_t tb = 0;
@@ -1508,6 +1518,8 @@ struct Work {
   int32_t* ids;        // kSym: 0..n-1
   int32_t* perm;       // kSym: permuted index -> original id [n]
   float* rn;           // kSym: row norms ||U_i|| [n]
+  float* rn_s;         // kSym: row norms in descending order [n]
+  int32_t* perm_n;     // kSym: norm order -> original id [n]
   uint32_t* ckey;      // kSym: candidate pool
   uint2* cval;
   uint32_t* skey;      // kSym: sorted by target row
@@ -1536,6 +1548,8 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->rn = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
+  w->rn_s = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
+  w->perm_n = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->ckey = cv.take<uint32_t>(ct);
   w->cval = cv.take<uint2>(ct);
   w->skey = cv.take<uint32_t>(ct);
@@ -1769,9 +1783,13 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
     scale_finalize<<<1, 1, 0, s>>>(w.sc);
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-    split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
-    count_launches(3);
+    if (!pl.sym) {  // (the symmetric scheme splits in norm order below)
+      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
+          w.Bop);
+      count_launches(1);
+    }
+    count_launches(2);
     if (!pl.alias) {
       const int64_t totA = (int64_t)pl.nAblocks * kRowsPerBlock * pl.KA * 16;  // rows padded
       split_tile<<<(int)std::min<int64_t>((totA + 255) / 256, sms * 16), 256, 0, s>>>(
@@ -1783,32 +1801,42 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
   }
   FusedParams fp = base_params(pl, w, n, row_begin);
   if (pl.sym) {
-    // seed: per-row t-th largest |ψ| over every 16th column tile (a lower bound of the
-    // row's true t-th magnitude), padded rows +inf
+    // (1) rows in descending ||U_i|| order (CUB sort of the row norms), split in that order
     const int64_t nthr = 2 * pl.NBu * kRowsPerBlock;
     fill_f32<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, nthr,
                                                                                INFINITY);
-    count_launches(1);
     GGM_CUDA_TRY(cudaMemsetAsync(w.ckey, 0xFF, sizeof(uint32_t) * pl.cand_total, s));
+    row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+        V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
+    iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
+    {
+      size_t tb = pl.sort_temp_bytes;
+      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.sort_tmp, tb, w.rn, w.rn_s, w.ids,
+                                                             w.perm_n, (int)n, 0, 32, s));
+      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
+      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
+          w.Bop, w.perm_n);
+    }
+    count_launches(5);
+    // (2) seed: per row, the t-th largest hi·hi chunk maximum over the first SS column tiles
+    // (the largest-norm columns), minus the hi·hi rounding bound -> lower bound b_i
     FusedParams sp = fp;
     sp.kind = kSeed;
     sp.RB = (int)pl.NBu;
     sp.SS = pl.SS;
     sp.thr_out = w.thr;
-    row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-        V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
     st = launch_fused(sp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
     if (st != GGM_OK) return st;
     seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
-        w.thr, w.rn, &w.sc->rn_max_bits, n, w.sc);
-    count_launches(2);
-    // order rows (= columns) by their bound: a CUB radix sort of the n seed bounds gives
-    // the permutation and the permuted bounds; the column operand is re-split in that order,
-    // so the 32 columns of every epilogue chunk carry nearly equal bounds
-    iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
+        w.thr, w.rn_s, &w.sc->rn_max_bits, n, w.sc);
+    count_launches(1);
+    // (3) order rows (= columns) by their bound: sort (bound, original id) -> the final
+    // permutation and the permuted bounds; re-split in that order, so the 32 columns of
+    // every epilogue chunk carry nearly equal bounds
     {
       size_t tb = pl.sort_temp_bytes;
-      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.thr, w.thr_p, w.ids, w.perm,
+      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.thr, w.thr_p, w.perm_n, w.perm,
                                                    (int)n, 0, 32, s));
     }
     fill_f32<<<(int)std::min<int64_t>((nthr - n + 255) / 256 + 1, sms * 8), 256, 0, s>>>(

@@ -6,7 +6,7 @@ against the reference variant it replaces (through the C ABI):
   * the packed K tail (3 products of the last k mod 16 elements in one MMA slot) vs the
     padded tail (GGM_NO_TAILPACK=1): same products, different accumulation order;
   * the symmetric scheme's seed bounds at small t (t = 1, 2, 3 make any overestimated bound
-    visible as a missing entry) and with the seed stride forced to 1 and 16.
+    visible as a missing entry) and with the seed sample forced to all columns / 1/256.
 """
 import numpy as np
 import pytest
@@ -74,15 +74,18 @@ def test_packed_tail_vs_padded(G, monkeypatch, k):
 
 
 @pytest.mark.parametrize("n,k,t,ss", [(4000, 64, 1, None), (4000, 64, 2, None), (5000, 100, 3, None),
-                                      (3000, 48, 3, "1"), (6000, 32, 10, "16"), (2600, 100, 32, None)])
+                                      (3000, 48, 3, "1"), (6000, 32, 10, "256"), (2600, 100, 32, None)])
 def test_symmetric_seed_bounds_small_t(G, monkeypatch, n, k, t, ss):
     """An overestimated seed bound drops entries from a row's candidates; t <= 3 makes that
     visible (the t-th magnitude is close to the largest)."""
     if ss is not None:
-        monkeypatch.setenv("GGM_SEED_STRIDE", ss)
+        monkeypatch.setenv("GGM_SEED_FRAC", ss)
     V, lam = gen.small_factor(3000 + n + t, n, k)
     rp, c, v, st = _run(G, V, lam, 0, n, topk=t, symmetric=1)
-    assert st["scheme"] == "symmetric" and st["recomputed"] == 0
+    # a tiny sample may overflow the candidate pool: the axis is then recomputed exactly
+    assert (st["scheme"] == "symmetric") != bool(st["recomputed"])
+    if ss is None:
+        assert st["scheme"] == "symmetric"
     res = check_topk(rp, c, v, V, lam, np.arange(n), t)
     assert res["exact"] + res["excused"] == n
 
