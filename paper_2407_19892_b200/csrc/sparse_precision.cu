@@ -1180,9 +1180,13 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
           }
         }
       }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
-      // ===================== MMA issuer: one thread (of the pair leader) ===============
+    } else if (warp == 1 && rank == 0) {
+      // ===================== MMA issuer: warp 1 (of the pair leader) =====================
+      // The whole warp runs the loop (warp-uniform descriptors); one elected lane issues the
+      // tcgen05.mma / commit instructions.  With one thread and per-lane registers, every
+      // MMA cost ~27 issue slots on an SM sub-partition shared with 4 epilogue warps.
       constexpr uint32_t idesc = idesc_f16_f32(PAIR ? 2 * kRowsPerBlock : kRowsPerBlock, kTileN);
+      const bool issuer = elect_one();
       int stage = 0;
       uint32_t phase = 0;
       int buf = 0;
@@ -1215,37 +1219,45 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
               bHi_s = aHi_s + 2 * kAtomBytes;
               bLo_s = aHi_s + 4 * kAtomBytes;
             }
+            // descriptors of the atom bases; K step ks = +2 on the address field (32 B)
+            const uint64_t dAh = sw128_desc(aHi_s), dAl = sw128_desc(aLo_s);
+            const uint64_t dBh = sw128_desc(bHi_s), dBl = sw128_desc(bLo_s);
+            if (issuer) {
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              const int slot = a * 4 + ks;
-              const uint32_t off = ks * 32;
-              const uint32_t acc = (a | ks) ? 1u : 0u;
-              if (slot < p.KS) {
-                mma_f16<PAIR>(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bHi_s + off), idesc, acc);
-                if (KIND != kSeed) {  // the seed pass bounds with hi*hi alone (seed_bounds)
-                  mma_f16<PAIR>(d_tmem, sw128_desc(aHi_s + off), sw128_desc(bLo_s + off), idesc, 1u);
-                  mma_f16<PAIR>(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, 1u);
+              for (int ks = 0; ks < 4; ++ks) {
+                const int slot = a * 4 + ks;
+                const uint64_t o = (uint64_t)(2 * ks);
+                const uint32_t acc = (a | ks) ? 1u : 0u;
+                if (slot < p.KS) {
+                  mma_f16<PAIR>(d_tmem, dAh + o, dBh + o, idesc, acc);
+                  if (KIND != kSeed) {  // the seed pass bounds with hi*hi alone (seed_bounds)
+                    mma_f16<PAIR>(d_tmem, dAh + o, dBl + o, idesc, 1u);
+                    mma_f16<PAIR>(d_tmem, dAl + o, dBh + o, idesc, 1u);
+                  }
+                } else if (slot < p.KS + p.TS) {
+                  // packed tail: A's slot in the lo array [hi|hi|lo], B's in the hi array
+                  // [hi|lo|hi] (3 products of the last k mod 16 elements in one K step)
+                  mma_f16<PAIR>(d_tmem, dAl + o, dBh + o, idesc, acc);
                 }
-              } else if (slot < p.KS + p.TS) {
-                // packed tail: A's slot in the lo array [hi|hi|lo], B's in the hi array
-                // [hi|lo|hi] (3 products of the last k mod 16 elements in one K step)
-                mma_f16<PAIR>(d_tmem, sw128_desc(aLo_s + off), sw128_desc(bHi_s + off), idesc, acc);
               }
+              mma_commit_any<PAIR>(&empty[stage]);
             }
-            mma_commit_any<PAIR>(&empty[stage]);
+            __syncwarp();
             if (++stage == NS) {
               stage = 0;
               phase ^= 1;
             }
           }
-          mma_commit_any<PAIR>(&tfull[buf]);
+          if (issuer) mma_commit_any<PAIR>(&tfull[buf]);
+          __syncwarp();
           if (++buf == 2) {
             buf = 0;
             tphase ^= 1;
           }
         }
         if (resident) {
-          mma_commit_any<PAIR>(aempty);
+          if (issuer) mma_commit_any<PAIR>(aempty);
+          __syncwarp();
           ++a_iter;
         }
       }
