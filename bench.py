@@ -325,7 +325,13 @@ def main():
     alg_entries = n0 * (n0 + 1) / 2.0 if sym0 else float(rows0) * n0
     alg_flops = 2.0 * k0 * alg_entries
     achieved = alg_flops / (avg_fused * 1e-3) / 1e12
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
+    # fp32-accurate tensor peak = fp16 (= bf16) dense rate / 3 (3-term split).  The sustained
+    # cuBLAS figure is the default; when BK2 runs above it (its clock under the power cap
+    # stays higher than cuBLAS's), the burst figure is the honest denominator.
+    peak_sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
+    peak_burst = peaks.get("bf16_tflops", peak_sus * 3.0) / 3.0
+    peak_is_burst = achieved > peak_sus
+    peak = peak_burst if peak_is_burst else peak_sus
     traffic = None
     tp = os.path.join(ROOT, "profiles", "fused_traffic.json")
     if os.path.exists(tp):
@@ -390,14 +396,17 @@ def main():
                        "k": [int(V.shape[1]) for V, _ in dev_axes], "topk": int(t),
                        "parallelism": f"row-shard x{world}", "l2": "inputs > L2 (no flush needed)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "frac_vs_sustained": achieved / peak_sus,
+                         "traffic": traffic,
                          "kernel": "fused_recon_topk (BK2, %s scheme%s)" % (
                              st0["scheme"], ", CTA pairs" if st0["cta_pair"] else ""),
                          "achieved_basis": "2k flops per entry (SURVEY 8(d)) x %s / mean CUDA-event "
                                            "duration of BK2 on the largest axis" % (
                                                "n(n+1)/2 unordered entries" if sym0 else "rows x n"),
-                         "peak_basis": f"{peak_src} bf16_tflops_sustained / 3 (3-term fp16 split = 3 MMAs "
-                                       "per fp32-accurate product; fp16 rate = bf16 rate)",
+                         "peak_basis": f"{peak_src} bf16_tflops{'' if peak_is_burst else '_sustained'} / 3 "
+                                       "(3-term fp16 split = 3 MMAs per fp32-accurate product; fp16 rate = "
+                                       "bf16 rate)" + ("; burst figure because BK2 runs above the cuBLAS "
+                                                       "sustained rate" if peak_is_burst else ""),
                          "kernel_ms": avg_fused, "step_share": step_ms_fused_share,
                          "tensor_pipe_tflops": st0["entries_main"] * 2.0 * st0["mma_k_per_entry"]
                          / (avg_fused * 1e-3) / 1e12,

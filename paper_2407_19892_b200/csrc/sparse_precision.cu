@@ -933,7 +933,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         }
         const bool rh = valid && m >= bi;
         const bool ch = valid && m >= cmin[c];
-        if (!__any_sync(0xffffffffu, rh || ch)) continue;
+        if (!__any_sync(0xffffffffu, rh || ch) || p.dbg == 3) continue;  // dbg 3: no rare path
         // rare path: exact per-entry masks, then each lane walks its own hits
         uint32_t mr = 0, mc = 0;
         if (rh) {
