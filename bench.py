@@ -226,7 +226,8 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2407_19892_b200 as G
-    from paper_2407_19892_b200.parallel import gather_topk_csr, shard_rows
+    from paper_2407_19892_b200.parallel import (assemble_rows, exchange_candidates, gather_topk_csr,
+                                                shard_rows)
 
     world, rank, local = _dist_env()
     torch.cuda.set_device(local)
@@ -260,11 +261,20 @@ def main():
     if host_axes is None:   # host copies for the e2e arm on the other ranks
         host_axes = [(V.cpu().numpy(), lam.cpu().numpy()) for V, lam in dev_axes]
 
-    plans = []
+    # per axis: at N > 1, large axes (n >= 65,536, k <= 128) run the distributed symmetric
+    # scheme (this rank's share of the block pairs + all-to-all of candidate buckets + merge of
+    # its rows); the others run row shards of the plain scheme.  At N = 1 every axis is one
+    # ggm_sparse_precision call (symmetric scheme chosen automatically for large axes).
+    plans, kinds = [], []
     for (V, lam) in dev_axes:
         n, k = V.shape
-        b, e = shard_rows(n, world, rank)
-        plans.append(G.SparsePlan(n, k, b, e, mode=0, topk=t))
+        if (world > 1 or os.environ.get("BENCH_FORCE_SYMSHARD")) and n >= 65536 and k <= 128:
+            plans.append(G.SymShardPlan(n, k, t, rank, world))
+            kinds.append("symshard")
+        else:
+            b, e = shard_rows(n, world, rank)
+            plans.append(G.SparsePlan(n, k, b, e, mode=0, topk=t))
+            kinds.append("rows")
     entries_step = float(sum(V.shape[0] ** 2 for V, _ in dev_axes))
     G.set_timing(True)
     stream = torch.cuda.current_stream()
@@ -274,17 +284,37 @@ def main():
     stats = [None for _ in plans]
     launches = [0]
 
-    def step(record=False):
-        for a, (plan, (V, lam)) in enumerate(zip(plans, dev_axes)):
-            plan.run(V, lam)
+    def run_axis(a, V, lam, record=False):
+        """One axis of the hot path; returns its CSR (row_ptr, col, val) (full at N > 1)."""
+        plan = plans[a]
+        n = V.shape[0]
+        if kinds[a] == "symshard":
+            key, val, counts, perm = plan.run(V, lam)
             if record:
                 tm = G.last_timing()
                 fused_ms[a].append(tm[1])
                 stage_ms[a].append(tuple(tm))
                 stats[a] = G.last_stats()
                 launches[0] += G.last_launches()
-            if world > 1:
-                gather_topk_csr(plan.col, plan.val, plan.t_eff, V.shape[0])
+            rkey, rval = exchange_candidates(key, val, counts)
+            b, e = G.sym_rows_begin(n, plan.k, t, rank, world), G.sym_rows_begin(n, plan.k, t, rank + 1, world)
+            row_id, col, vals = G.sym_merge(n, t, rkey, rval, perm, b, e)
+            if record:
+                launches[0] += G.last_launches()
+            return assemble_rows(row_id, col, vals, n, min(t, n - 1))
+        plan.run(V, lam)
+        if record:
+            tm = G.last_timing()
+            fused_ms[a].append(tm[1])
+            stage_ms[a].append(tuple(tm))
+            stats[a] = G.last_stats()
+            launches[0] += G.last_launches()
+        if world > 1:
+            return gather_topk_csr(plan.col, plan.val, plan.t_eff, n)
+        return plan.row_ptr, plan.col, plan.val
+
+    def step(record=False):
+        return [run_axis(a, V, lam, record) for a, (V, lam) in enumerate(dev_axes)]
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -315,7 +345,7 @@ def main():
     a0 = int(np.argmax([V.shape[0] for V, _ in dev_axes]))
     V0 = dev_axes[a0][0]
     n0, k0 = V0.shape
-    rows0 = plans[a0].row_end - plans[a0].row_begin
+    rows0 = n0 if kinds[a0] == "symshard" else plans[a0].row_end - plans[a0].row_begin
     avg_fused = float(np.mean(fused_ms[a0]))
     st0 = stats[a0]
     sym0 = st0["scheme"] == "symmetric"
@@ -323,6 +353,8 @@ def main():
     # evaluate -- all rows x n entries (plain), or each unordered pair once, n(n+1)/2 entries
     # (symmetric scheme: ψ_ij = ψ_ji)
     alg_entries = n0 * (n0 + 1) / 2.0 if sym0 else float(rows0) * n0
+    if kinds[a0] == "symshard":   # this rank's share of the unordered pairs
+        alg_entries /= world
     alg_flops = 2.0 * k0 * alg_entries
     achieved = alg_flops / (avg_fused * 1e-3) / 1e12
     # fp32-accurate tensor peak = fp16 (= bf16) dense rate / 3 (3-term split).  The sustained
@@ -349,21 +381,22 @@ def main():
     if not args.no_e2e:
         hV = [torch.from_numpy(np.ascontiguousarray(h[0])).pin_memory() for h in host_axes]
         hL = [torch.from_numpy(np.ascontiguousarray(h[1])).pin_memory() for h in host_axes]
-        hout = [(torch.empty(p.row_ptr.numel(), dtype=torch.int64).pin_memory(),
-                 torch.empty(p.col.numel(), dtype=torch.int32).pin_memory(),
-                 torch.empty(p.val.numel(), dtype=torch.float32).pin_memory()) for p in plans]
+        outs = step()
+        hout = [(torch.empty(o[0].numel(), dtype=torch.int64).pin_memory(),
+                 torch.empty(o[1].numel(), dtype=torch.int32).pin_memory(),
+                 torch.empty(o[2].numel(), dtype=torch.float32).pin_memory()) for o in outs]
         h2d = sum(v.numel() * 4 + l.numel() * 8 for v, l in zip(hV, hL))
         d2h = sum(o[0].numel() * 8 + o[1].numel() * 4 + o[2].numel() * 4 for o in hout)
 
         def e2e_step():
-            for a, plan in enumerate(plans):
+            for a in range(len(plans)):
                 V, lam = dev_axes[a]
                 V.copy_(hV[a], non_blocking=True)
                 lam.copy_(hL[a], non_blocking=True)
-                plan.run(V, lam)
-                hout[a][0].copy_(plan.row_ptr, non_blocking=True)
-                hout[a][1].copy_(plan.col, non_blocking=True)
-                hout[a][2].copy_(plan.val, non_blocking=True)
+                rp, col, val = run_axis(a, V, lam)
+                hout[a][0].copy_(rp, non_blocking=True)
+                hout[a][1].copy_(col, non_blocking=True)
+                hout[a][2].copy_(val, non_blocking=True)
             torch.cuda.synchronize()
         e2e_step()
         if world > 1:
@@ -394,7 +427,8 @@ def main():
             "dtype": DTYPE, "data": "synthetic (synth.gen seeded recipes of BASELINE.json configs)",
             "config": {"workload": WORKLOADS[args.config], "axes_n": [int(V.shape[0]) for V, _ in dev_axes],
                        "k": [int(V.shape[1]) for V, _ in dev_axes], "topk": int(t),
-                       "parallelism": f"row-shard x{world}", "l2": "inputs > L2 (no flush needed)"},
+                       "parallelism": (f"symmetric block-pair shards + all-to-all x{world} (axes n >= 65536), "
+                                       f"row shards (others)" if world > 1 else "single GPU"), "l2": "inputs > L2 (no flush needed)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "frac_vs_sustained": achieved / peak_sus,
                          "traffic": traffic,

@@ -44,6 +44,7 @@ typedef enum {
 } ggm_status;
 
 #define GGM_MAX_TOPK 32
+#define GGM_MAX_RANKS 1024
 
 const char *ggm_last_error(void);
 int ggm_version(void);
@@ -178,6 +179,46 @@ ggm_status ggm_sparse_precision(int64_t n, int k, const float *V, const double *
                                 const ggm_sparsify_opts *opts, int64_t *row_ptr, int32_t *col,
                                 float *val, int64_t capacity, int64_t *nnz_out,
                                 void *workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------
+ * (3b) Distributed symmetric scheme (multi-GPU form of symmetric = 1; SURVEY §8(e)/(f),
+ * DESIGN.md §5).  One process per GPU; every rank calls with the same (n, k, V, λ, opts).
+ *
+ * ggm_sparse_precision_sym_shard: runs the replicated phases (row norms, seed pass, the two
+ * orderings and splits — deterministic, so every rank derives the same permutation) and
+ * this rank's contiguous share of the symmetric units (units = 256-row blocks of the
+ * bound-ordered axis, [NBu·rank/nranks, NBu·(rank+1)/nranks)).  Outputs this rank's
+ * candidates sorted by target row, as two device arrays: cand_key[e] = target row (bound
+ * order index), cand_val[2e..2e+1] = (source row, bound order index; ψ as float bits);
+ * counts[r] (host) = number of candidates whose target row rank r owns (contiguous in the
+ * sorted arrays, in rank order); perm (device, n int32) = bound order index -> original row
+ * id.  Rank r owns bound-order rows [ggm_sym_rows_begin(.., r, ..), ggm_sym_rows_begin(..,
+ * r+1, ..)).  Errors: GGM_ERR_CAPACITY if the candidates exceed cand_capacity or the
+ * internal pool (callers fall back to the row-sharded plain scheme); GGM_ERR_UNSUPPORTED for
+ * mode 1 or k > 128.  Synchronizes `stream`.
+ *
+ * ggm_sym_merge: after the caller's all-to-all exchange of the buckets, merges the
+ * candidates of this rank's rows [row_begin, row_end) (bound order; ncand candidates in any
+ * order): row j's top t_eff by (|ψ| desc, original column asc), written at local row
+ * j - row_begin: row_id[j - row_begin] = perm[j] (original row id), col/val[(j - row_begin)
+ * * t_eff + 0..t_eff-1] in ascending original column order.  Workspace from
+ * ggm_sym_merge_workspace(ncand).  Asynchronous. */
+int64_t ggm_sym_rows_begin(int64_t n, int k, const ggm_sparsify_opts *opts, int rank,
+                           int nranks);
+ggm_status ggm_sparse_precision_sym_shard_workspace(int64_t n, int k,
+                                                    const ggm_sparsify_opts *opts,
+                                                    size_t *bytes);
+ggm_status ggm_sparse_precision_sym_shard(int64_t n, int k, const float *V,
+                                          const double *lambda, const ggm_sparsify_opts *opts,
+                                          int rank, int nranks, uint32_t *cand_key,
+                                          uint32_t *cand_val, int64_t cand_capacity,
+                                          int64_t *counts, int32_t *perm, void *workspace,
+                                          size_t workspace_bytes, void *stream);
+ggm_status ggm_sym_merge_workspace(int64_t ncand, size_t *bytes);
+ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t *cand_key, const uint32_t *cand_val,
+                         int64_t ncand, const int32_t *perm, int64_t row_begin, int64_t row_end,
+                         int64_t *row_id, int32_t *col, float *val, void *workspace,
+                         size_t workspace_bytes, void *stream);
 
 /* Per-kernel timing of the last ggm_sparse_precision call on this thread, measured with
  * CUDA events on `stream` when enabled (for bench.py's roofline).  ms[0] = prep (absmax +

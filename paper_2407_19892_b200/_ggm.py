@@ -31,6 +31,8 @@ EXPORTED = [
     "ggm_solve_opts_default", "ggm_solve_eigvals", "ggm_grid_marginals",
     "ggm_sparse_precision_workspace", "ggm_sparse_precision",
     "ggm_set_timing", "ggm_last_timing", "ggm_last_launches", "ggm_last_stats",
+    "ggm_sym_rows_begin", "ggm_sparse_precision_sym_shard_workspace",
+    "ggm_sparse_precision_sym_shard", "ggm_sym_merge_workspace", "ggm_sym_merge",
 ]
 
 
@@ -92,8 +94,19 @@ def lib() -> C.CDLL:
     L.ggm_last_launches.restype = i32
     L.ggm_last_stats.argtypes = [C.POINTER(C.c_double)]
     L.ggm_last_stats.restype = None
+    L.ggm_sym_rows_begin.argtypes = [i64, i32, C.POINTER(SparsifyOpts), i32, i32]
+    L.ggm_sym_rows_begin.restype = i64
+    L.ggm_sparse_precision_sym_shard_workspace.argtypes = [i64, i32, C.POINTER(SparsifyOpts),
+                                                           C.POINTER(C.c_size_t)]
+    L.ggm_sparse_precision_sym_shard.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts), i32,
+                                                 i32, vp, vp, i64, C.POINTER(i64), vp, vp,
+                                                 C.c_size_t, vp]
+    L.ggm_sym_merge_workspace.argtypes = [i64, C.POINTER(C.c_size_t)]
+    L.ggm_sym_merge.argtypes = [i64, i32, vp, vp, i64, vp, i64, i64, vp, vp, vp, vp, C.c_size_t, vp]
     for name in ("ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
-                 "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision"):
+                 "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision",
+                 "ggm_sparse_precision_sym_shard_workspace", "ggm_sparse_precision_sym_shard",
+                 "ggm_sym_merge_workspace", "ggm_sym_merge"):
         getattr(L, name).restype = i32
     _lib = L
     return L
@@ -249,6 +262,71 @@ def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
                           max(e.required, 1), device=V.device, symmetric=symmetric)
         nnz = plan.run(V, lam, stream)
     return plan.row_ptr, plan.col[:nnz], plan.val[:nnz]
+
+
+def sym_rows_begin(n: int, k: int, topk: int, rank: int, nranks: int) -> int:
+    """First bound-order row owned by `rank` in the distributed symmetric scheme."""
+    o = SparsifyOpts(0, int(topk), 0.0, 0, 1)
+    r = lib().ggm_sym_rows_begin(int(n), int(k), C.byref(o), int(rank), int(nranks))
+    if r < 0:
+        raise GGMError(1, "ggm_sym_rows_begin: invalid arguments")
+    return int(r)
+
+
+class SymShardPlan:
+    """Workspace for repeated ggm_sparse_precision_sym_shard calls (one rank's share of the
+    distributed symmetric scheme, include/ggm.h (3b))."""
+
+    def __init__(self, n, k, topk, rank, nranks, cand_capacity=None, device="cuda"):
+        self.n, self.k, self.t = int(n), int(k), int(topk)
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.opts = SparsifyOpts(0, self.t, 0.0, 0, 1)
+        nb = C.c_size_t(0)
+        _check(lib().ggm_sparse_precision_sym_shard_workspace(self.n, self.k, C.byref(self.opts),
+                                                              C.byref(nb)))
+        self.ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=device)
+        cap = cand_capacity if cand_capacity is not None else self.n * max(8 * self.t, 64)
+        self.cap = int(cap)
+        self.key = torch.empty(self.cap, dtype=torch.int32, device=device)
+        self.val = torch.empty((self.cap, 2), dtype=torch.int32, device=device)
+        self.perm = torch.empty(self.n, dtype=torch.int32, device=device)
+        self.counts = (C.c_int64 * self.nranks)()
+
+    def run(self, V: torch.Tensor, lam: torch.Tensor, stream=None):
+        """Returns (key, val, counts, perm): this rank's candidates sorted by target row,
+        counts per destination rank (list), bound order -> original id."""
+        _require_cuda(V, torch.float32, "V")
+        _require_cuda(lam, torch.float64, "lam")
+        st = lib().ggm_sparse_precision_sym_shard(
+            self.n, self.k, _ptr(V), _ptr(lam), C.byref(self.opts), self.rank, self.nranks,
+            _ptr(self.key), _ptr(self.val), self.cap, self.counts, _ptr(self.perm), _ptr(self.ws),
+            self.ws.numel(), _stream(stream))
+        _check(st)
+        counts = [int(c) for c in self.counts]
+        tot = sum(counts)
+        return self.key[:tot], self.val[:tot], counts, self.perm
+
+
+def sym_merge(n: int, t: int, key: torch.Tensor, val: torch.Tensor, perm: torch.Tensor,
+              row_begin: int, row_end: int, stream=None):
+    """Merge received candidates of bound-order rows [row_begin, row_end): returns
+    (row_id int64 [rows], col int32 [rows*t_eff], val float32 [rows*t_eff])."""
+    ncand = int(key.numel())
+    dev = perm.device
+    te = min(int(t), int(n) - 1)
+    rows = int(row_end) - int(row_begin)
+    nb = C.c_size_t(0)
+    _check(lib().ggm_sym_merge_workspace(ncand, C.byref(nb)))
+    ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=dev)
+    row_id = torch.empty(max(rows, 1), dtype=torch.int64, device=dev)
+    col = torch.empty(max(rows * te, 1), dtype=torch.int32, device=dev)
+    out = torch.empty(max(rows * te, 1), dtype=torch.float32, device=dev)
+    kp = _ptr(key) if ncand else C.c_void_p(0)
+    vp_ = _ptr(val) if ncand else C.c_void_p(0)
+    _check(lib().ggm_sym_merge(int(n), int(t), kp, vp_, ncand, _ptr(perm), int(row_begin),
+                               int(row_end), _ptr(row_id), _ptr(col), _ptr(out), _ptr(ws),
+                               ws.numel(), _stream(stream)))
+    return row_id[:rows], col[:rows * te], out[:rows * te]
 
 
 def set_timing(enabled: bool):

@@ -268,6 +268,8 @@ struct FusedParams {
   uint2* cand_val;         //       (source row i, ψ bits)
   int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
   int pair;          // CTA-pair kernel (host-side selection; the kernel's template PAIR)
+  int unit_lo, unit_hi;  // units processed by this launch (a rank's share in the sharded
+                         // symmetric scheme; [0, all units) otherwise)
   int dbg;  // timing experiments only (GGM_DEBUG_EPI): 1 = TMEM loads only, 2 = no epilogue work
 };
 
@@ -319,7 +321,7 @@ __device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& ub) 
 // blocks in lockstep and share them through L2.
 __device__ __forceinline__ int sym_start(const FusedParams& p, int u, int ub, int u0, int ustep,
                                          int W) {
-  const int X = min(p.NB - 1, u - u0 + ustep - 1);
+  const int X = min(p.unit_hi - 1, u - u0 + ustep - 1);
   const int delta = (X - ub + p.NB) % p.NB;
   return delta >= W ? 0 : delta;
 }
@@ -587,11 +589,10 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
   const float sd2 = sd * sd;
   const float tau_s = ldexpf(ldexpf(p.tau, p.sc->exp2), p.sc->exp2);
   const int t = p.t;
-  const int units = KIND == kPlain ? p.RB * p.C : p.RB;
   int buf = 0;
   uint32_t tphase = 0;
   TopList<MAXT> top;
-  for (int u = u0; u < units; u += ustep) {
+  for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;  // this CTA's 128-row block
@@ -738,7 +739,7 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   MagList<MAXT> top;
-  for (int u = u0; u < p.RB; u += ustep) {
+  for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
     int ub;
     const int ntiles = unit_tiles<kSeed, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
@@ -841,13 +842,12 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   float* thr_w = scratch_all + (size_t)(warp - kFirstEpiWarp) * (kScratchBytes / 4 / EPW);
   const float sd = ldexpf(1.f, -p.sc->exp2);
   const float sd2 = sd * sd;
-  const int units = p.RB;
   const uint32_t lt = (1u << lane) - 1u;
   DevScalars* scw = const_cast<DevScalars*>(p.sc);
   int buf = 0;
   uint32_t tphase = 0;
   CandCursor cc{0, kCandChunk};
-  for (int u = u0; u < units; u += ustep) {
+  for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int units = KIND == kPlain ? p.RB * p.C : p.RB;
+  const int units = p.unit_hi;
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
   const int u0 = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
   const int ustep = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
@@ -1095,7 +1095,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
       int stage = 0;
       uint32_t phase = 0;
       int a_iter = 0;
-      for (int u = u0; u < units; u += ustep) {
+      for (int u = p.unit_lo + u0; u < units; u += ustep) {
         int ub;
         const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1192,7 +1192,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
       int buf = 0;
       uint32_t tphase = 0;
       int a_iter = 0;
-      for (int u = u0; u < units; u += ustep) {
+      for (int u = p.unit_lo + u0; u < units; u += ustep) {
         int ub;
         const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         if (resident) {
@@ -1317,11 +1317,14 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n,
 template <int MAXT>
 __global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restrict__ cv,
                           int64_t ncand, int64_t n, int t, const int32_t* __restrict__ perm,
+                          int64_t row_begin, int64_t row_end, int64_t* row_id,
                           int64_t* row_ptr, int32_t* col, float* val) {
-  // row j (permuted index): top t of its candidates (source in permuted index, value) by
-  // (|ψ| desc, original column id asc); emitted at the original row id in ascending columns
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+  // row j (bound-order index): top t of its candidates (source in bound order, value) by
+  // (|ψ| desc, original column id asc), ascending columns.  row_id == nullptr: written at
+  // the original row id (single GPU, full axis); else at j - row_begin, with its original id
+  // in row_id (a rank's share of the distributed symmetric scheme)
+  const int64_t j = row_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= row_end) return;
   TopList<MAXT> top;
   top.init(t);
   const int64_t b0 = lower_bound_u32(key, ncand, (uint32_t)j);
@@ -1331,10 +1334,20 @@ __global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restr
     const float v = __uint_as_float(x.y);
     top.merge_insert(fabsf(v), v, __ldg(perm + x.x));
   }
-  const int64_t o = perm[j];  // original row id
+  const int64_t o = row_id ? j - row_begin : (int64_t)perm[j];
+  if (row_id) row_id[o] = perm[j];
   top.emit_sorted(t, col + o * t, val + o * t, 1.f);
-  row_ptr[o] = o * t;
-  if (o == n - 1) row_ptr[n] = n * t;
+  if (row_ptr) {
+    row_ptr[o] = o * t;
+    if (o == n - 1) row_ptr[n] = n * t;
+  }
+}
+
+// per-destination counts of a key-sorted candidate list: bnd[r] = first index with key >= lo[r]
+__global__ void bucket_bounds(const uint32_t* __restrict__ key, int64_t ncand,
+                              const int64_t* __restrict__ lo, int nb, int64_t* __restrict__ bnd) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r <= nb) bnd[r] = lower_bound_u32(key, ncand, (uint32_t)lo[r]);
 }
 
 __global__ void iota_i32(int32_t* p, int64_t count) {
@@ -1666,10 +1679,16 @@ static cudaError_t launch_fused_p(const TMaps& tm, const FusedParams& fp, int t,
 
 // fp.pair selects the CTA-pair kernel; its tensor maps are built over fp.A / fp.B with the
 // given numbers of 128-row blocks
-static ggm_status launch_fused(const FusedParams& fp, int t, int64_t ablocks, int64_t bblocks,
+static ggm_status launch_fused(const FusedParams& fp_in, int t, int64_t ablocks, int64_t bblocks,
                                cudaStream_t s) {
+  FusedParams fp = fp_in;
+  if (fp.unit_hi <= 0) {  // default: all units of this kind
+    fp.unit_lo = 0;
+    fp.unit_hi = fp.kind == kPlain ? fp.RB * fp.C : fp.RB;
+  }
+  if (fp.unit_hi <= fp.unit_lo) return GGM_OK;  // empty shard
   const size_t smem = fused_smem_bytes(fp.KA, fp.resident, fp.pair);
-  const int units = fp.kind == kPlain ? fp.RB * fp.C : fp.RB;
+  const int units = fp.unit_hi - fp.unit_lo;
   TMaps tm;
   memset(&tm, 0, sizeof(tm));
   cudaError_t ce;
@@ -1694,8 +1713,8 @@ static void launch_merge_sym_t(const Work& w, const Plan& pl, int64_t ncand, int
                                int32_t* col, float* val, cudaStream_t s) {
   const int threads = 128;
   const int blocks = (int)((pl.n + threads - 1) / threads);
-  merge_sym<MAXT><<<blocks, threads, 0, s>>>(w.skey, w.sval, ncand, pl.n, pl.t, w.perm, row_ptr,
-                                             col, val);
+  merge_sym<MAXT><<<blocks, threads, 0, s>>>(w.skey, w.sval, ncand, pl.n, pl.t, w.perm, 0, pl.n,
+                                             nullptr, row_ptr, col, val);
 }
 
 static thread_local double g_stats[6] = {0, 0, 0, 0, 0, 0};
@@ -1753,6 +1772,82 @@ static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t
   const char* d = getenv("GGM_DEBUG_EPI");
   fp.dbg = d ? atoi(d) : 0;
   return fp;
+}
+
+// Symmetric scheme, phases 1-3 (replicated on every rank of the distributed form): rows in
+// descending ||U_i|| order, seed pass over the largest-norm columns -> per-row lower bounds,
+// rows re-ordered by bound (w.perm: bound order -> original id, w.thr_p: bounds), operand
+// re-split in bound order.
+static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, const double* lambda,
+                              int64_t n, int k, const FusedParams& fp, cudaStream_t s) {
+  const int sms = num_sms();
+  ggm_status st;
+    // (1) rows in descending ||U_i|| order (CUB sort of the row norms), split in that order
+  const int64_t nthr = 2 * pl.NBu * kRowsPerBlock;
+  fill_f32<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, nthr,
+                                                                             INFINITY);
+  GGM_CUDA_TRY(cudaMemsetAsync(w.ckey, 0xFF, sizeof(uint32_t) * pl.cand_total, s));
+  row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+      V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
+  iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
+  {
+    size_t tb = pl.sort_temp_bytes;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.sort_tmp, tb, w.rn, w.rn_s, w.ids,
+                                                           w.perm_n, (int)n, 0, 32, s));
+    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
+    split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
+        w.Bop, w.perm_n);
+  }
+  count_launches(5);
+  // (2) seed: per row, the t-th largest hi·hi chunk maximum over the first SS column tiles
+  // (the largest-norm columns), minus the hi·hi rounding bound -> lower bound b_i
+  FusedParams sp = fp;
+  sp.kind = kSeed;
+  sp.RB = (int)pl.NBu;
+  sp.SS = pl.SS;
+  sp.thr_out = w.thr;
+  st = launch_fused(sp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+  if (st != GGM_OK) return st;
+  seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
+      w.thr, w.rn_s, &w.sc->rn_max_bits, n, w.sc);
+  count_launches(1);
+  // (3) order rows (= columns) by their bound: sort (bound, original id) -> the final
+  // permutation and the permuted bounds; re-split in that order, so the 32 columns of
+  // every epilogue chunk carry nearly equal bounds
+  {
+    size_t tb = pl.sort_temp_bytes;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.thr, w.thr_p, w.perm_n, w.perm,
+                                                 (int)n, 0, 32, s));
+  }
+  fill_f32<<<(int)std::min<int64_t>((nthr - n + 255) / 256 + 1, sms * 8), 256, 0, s>>>(
+      w.thr_p + n, nthr - n, INFINITY);
+  {
+    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
+    split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop,
+        w.perm);
+  }
+  count_launches(3);
+  GGM_CUDA_TRY(cudaGetLastError());
+  return GGM_OK;
+}
+
+// Phase 4: the symmetric main kernel over units [unit_lo, unit_hi) (all units on one GPU, a
+// contiguous share per rank in the distributed form); candidates -> w.ckey / w.cval.
+static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int unit_lo,
+                           int unit_hi, cudaStream_t s) {
+  fp.kind = kSym;
+  fp.RB = (int)pl.NBu;
+  fp.thr = w.thr_p;
+  fp.perm = w.perm;
+  fp.cand_key = w.ckey;
+  fp.cand_val = w.cval;
+  fp.cand_total = pl.cand_total;
+  fp.unit_lo = unit_lo;
+  fp.unit_hi = unit_hi;
+  if (unit_hi <= unit_lo) return GGM_OK;
+  return launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
 }
 
 extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, const double* lambda,
@@ -1813,63 +1908,10 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
   }
   FusedParams fp = base_params(pl, w, n, row_begin);
   if (pl.sym) {
-    // (1) rows in descending ||U_i|| order (CUB sort of the row norms), split in that order
-    const int64_t nthr = 2 * pl.NBu * kRowsPerBlock;
-    fill_f32<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, nthr,
-                                                                               INFINITY);
-    GGM_CUDA_TRY(cudaMemsetAsync(w.ckey, 0xFF, sizeof(uint32_t) * pl.cand_total, s));
-    row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-        V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
-    iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
-    {
-      size_t tb = pl.sort_temp_bytes;
-      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.sort_tmp, tb, w.rn, w.rn_s, w.ids,
-                                                             w.perm_n, (int)n, 0, 32, s));
-      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
-          w.Bop, w.perm_n);
-    }
-    count_launches(5);
-    // (2) seed: per row, the t-th largest hi·hi chunk maximum over the first SS column tiles
-    // (the largest-norm columns), minus the hi·hi rounding bound -> lower bound b_i
-    FusedParams sp = fp;
-    sp.kind = kSeed;
-    sp.RB = (int)pl.NBu;
-    sp.SS = pl.SS;
-    sp.thr_out = w.thr;
-    st = launch_fused(sp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+    st = sym_prepare(pl, w, V, lambda, n, k, fp, s);
     if (st != GGM_OK) return st;
-    seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
-        w.thr, w.rn_s, &w.sc->rn_max_bits, n, w.sc);
-    count_launches(1);
-    // (3) order rows (= columns) by their bound: sort (bound, original id) -> the final
-    // permutation and the permuted bounds; re-split in that order, so the 32 columns of
-    // every epilogue chunk carry nearly equal bounds
-    {
-      size_t tb = pl.sort_temp_bytes;
-      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.thr, w.thr_p, w.perm_n, w.perm,
-                                                   (int)n, 0, 32, s));
-    }
-    fill_f32<<<(int)std::min<int64_t>((nthr - n + 255) / 256 + 1, sms * 8), 256, 0, s>>>(
-        w.thr_p + n, nthr - n, INFINITY);
-    {
-      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop,
-          w.perm);
-    }
-    count_launches(3);
-    GGM_CUDA_TRY(cudaGetLastError());
     tm.mark(1);
-    fp.kind = kSym;
-    fp.RB = (int)pl.NBu;
-    fp.thr = w.thr_p;
-    fp.perm = w.perm;
-    fp.cand_key = w.ckey;
-    fp.cand_val = w.cval;
-    fp.cand_total = pl.cand_total;
-    st = launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+    st = sym_main(pl, w, fp, 0, (int)pl.NBu, s);
     if (st != GGM_OK) return st;
     tm.mark(2);
     // sort the candidate pool by target row (unused slots carry UINT32_MAX -> sorted last)
@@ -2029,5 +2071,209 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
   tm.mark(3);
   GGM_CUDA_TRY(cudaStreamSynchronize(s));
   tm.finish();
+  return GGM_OK;
+}
+
+// ------------------------------------------------------------------ distributed symmetric scheme
+// (DESIGN.md §5): every rank runs the replicated phases 1-3 and its contiguous share of the
+// symmetric units, buckets its candidates by the rank that owns their target row, the caller
+// exchanges the buckets (all-to-all), and each rank merges the candidates of its own rows.
+
+static ggm_status sym_shard_plan(int64_t n, int k, const ggm_sparsify_opts* opts, Plan* pl) {
+  if (!opts) return fail(GGM_ERR_INVALID_ARGUMENT, "opts is NULL");
+  ggm_sparsify_opts o = *opts;
+  o.symmetric = 1;
+  ggm_status st = make_plan(n, k, 0, n, &o, n * (int64_t)std::max(1, std::min<int>(o.topk, (int)(n - 1))), pl);
+  if (st != GGM_OK) return st;
+  if (!pl->sym)
+    return fail(GGM_ERR_UNSUPPORTED, "distributed symmetric scheme needs mode 0 and k <= 128");
+  return GGM_OK;
+}
+
+static int64_t sym_unit_rows(const Plan& pl) { return pl.pair ? 2 * kRowsPerBlock : kRowsPerBlock; }
+static int64_t sym_unit_lo(const Plan& pl, int rank, int nranks) {
+  return pl.NBu * (int64_t)rank / nranks;
+}
+
+extern "C" int64_t ggm_sym_rows_begin(int64_t n, int k, const ggm_sparsify_opts* opts, int rank,
+                                      int nranks) {
+  Plan pl;
+  if (nranks < 1 || rank < 0 || rank > nranks) return -1;
+  if (sym_shard_plan(n, k, opts, &pl) != GGM_OK) return -1;
+  return std::min<int64_t>(n, sym_unit_lo(pl, rank, nranks) * sym_unit_rows(pl));
+}
+
+extern "C" ggm_status ggm_sparse_precision_sym_shard_workspace(int64_t n, int k,
+                                                                const ggm_sparsify_opts* opts,
+                                                                size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  Plan pl;
+  ggm_status st = sym_shard_plan(n, k, opts, &pl);
+  if (st != GGM_OK) return st;
+  Work w;
+  *bytes = carve(pl, nullptr, &w) + 256 + sizeof(int64_t) * 2 * (GGM_MAX_RANKS + 1);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_sparse_precision_sym_shard(
+    int64_t n, int k, const float* V, const double* lambda, const ggm_sparsify_opts* opts,
+    int rank, int nranks, uint32_t* cand_key, uint32_t* cand_val, int64_t cand_capacity,
+    int64_t* counts, int32_t* perm, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!V || !lambda || !cand_key || !cand_val || !counts || !perm || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (nranks < 1 || nranks > GGM_MAX_RANKS || rank < 0 || rank >= nranks)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "rank %d / nranks %d invalid", rank, nranks);
+  Plan pl;
+  ggm_status st = sym_shard_plan(n, k, opts, &pl);
+  if (st != GGM_OK) return st;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  Work w;
+  const size_t need = carve(pl, workspace, &w);
+  const size_t extra = 256 + sizeof(int64_t) * 2 * (GGM_MAX_RANKS + 1);
+  if (workspace_bytes < need + extra)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes,
+                need + extra);
+  if (!ggm_device_supported())
+    return fail(GGM_ERR_CUDA, "current device is not compute capability 10.0 (sm_100a)");
+  int64_t* d_lo = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + ((need + 255) & ~size_t(255)));
+  int64_t* d_bnd = d_lo + (GGM_MAX_RANKS + 1);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  reset_launches();
+  for (double& x : g_stats) x = 0.0;
+  EventTimer tm(timing_enabled(), s);
+  tm.mark(0);
+  const int sms = num_sms();
+  GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
+  {
+    const int64_t total = n * (int64_t)k;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 8));
+    absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
+    scale_finalize<<<1, 1, 0, s>>>(w.sc);
+    count_launches(2);
+  }
+  FusedParams fp = base_params(pl, w, n, 0);
+  st = sym_prepare(pl, w, V, lambda, n, k, fp, s);
+  if (st != GGM_OK) return st;
+  tm.mark(1);
+  const int ulo = (int)sym_unit_lo(pl, rank, nranks), uhi = (int)sym_unit_lo(pl, rank + 1, nranks);
+  st = sym_main(pl, w, fp, ulo, uhi, s);
+  if (st != GGM_OK) return st;
+  tm.mark(2);
+  DevScalars hs;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
+  if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
+  if (hs.cand_overflow)
+    return fail(GGM_ERR_CAPACITY, "symmetric candidate pool overflow (use the row-sharded plain scheme)");
+  const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
+  int ebits = 1;
+  while ((int64_t(1) << ebits) <= n) ++ebits;
+  if (ncand > 0) {
+    size_t tb = pl.sort_temp_bytes;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
+                                                 ncand, 0, ebits, s));
+  }
+  // destination buckets: rank r owns bound-order rows [lo_r, lo_{r+1}); unused pool slots
+  // (key UINT32_MAX) sort after every real key
+  std::vector<int64_t> lo(nranks + 1);
+  for (int r = 0; r <= nranks; ++r)
+    lo[r] = std::min<int64_t>(n, sym_unit_lo(pl, r, nranks) * sym_unit_rows(pl));
+  GGM_CUDA_TRY(cudaMemcpyAsync(d_lo, lo.data(), sizeof(int64_t) * (nranks + 1),
+                               cudaMemcpyHostToDevice, s));
+  bucket_bounds<<<1, 64, 0, s>>>(w.skey, ncand, d_lo, nranks, d_bnd);
+  count_launches(1);
+  std::vector<int64_t> bnd(nranks + 1);
+  GGM_CUDA_TRY(cudaMemcpyAsync(bnd.data(), d_bnd, sizeof(int64_t) * (nranks + 1),
+                               cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t total = bnd[nranks] - bnd[0];
+  for (int r = 0; r < nranks; ++r) counts[r] = bnd[r + 1] - bnd[r];
+  if (total > cand_capacity)
+    return fail(GGM_ERR_CAPACITY, "%lld candidates > capacity %lld", (long long)total,
+                (long long)cand_capacity);
+  if (total > 0) {
+    GGM_CUDA_TRY(cudaMemcpyAsync(cand_key, w.skey + bnd[0], sizeof(uint32_t) * total,
+                                 cudaMemcpyDeviceToDevice, s));
+    GGM_CUDA_TRY(cudaMemcpyAsync(cand_val, w.sval + bnd[0], sizeof(uint2) * total,
+                                 cudaMemcpyDeviceToDevice, s));
+  }
+  GGM_CUDA_TRY(cudaMemcpyAsync(perm, w.perm, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  tm.mark(3);
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  tm.finish();
+  double evaluated = 0.0;  // entries evaluated by this rank's units
+  for (int64_t b = ulo; b < uhi; ++b) {
+    const int64_t NBu = pl.NBu;
+    const int64_t W = (NBu & 1) ? (NBu + 1) / 2 : NBu / 2 + (b < NBu / 2 ? 1 : 0);
+    evaluated += pl.pair ? (double)W * 2 * kRowsPerBlock * kTileN
+                         : (double)((W + 1) / 2) * kRowsPerBlock * kTileN;
+  }
+  g_stats[0] = 2;
+  g_stats[1] = evaluated;
+  g_stats[2] = (double)total;
+  g_stats[4] = 16.0 * (3 * pl.KS + pl.TS);
+  g_stats[5] = pl.pair;
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_sym_merge_workspace(int64_t ncand, size_t* bytes) {
+  if (!bytes || ncand < 0) return fail(GGM_ERR_INVALID_ARGUMENT, "bad argument");
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint2*)nullptr, (uint2*)nullptr, std::max<int64_t>(ncand, 1));
+  const size_t a = ((size_t)std::max<int64_t>(ncand, 1) * sizeof(uint32_t) + 255) & ~size_t(255);
+  const size_t b = ((size_t)std::max<int64_t>(ncand, 1) * sizeof(uint2) + 255) & ~size_t(255);
+  *bytes = a + b + tb + 256;
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t* cand_key,
+                                    const uint32_t* cand_val, int64_t ncand, const int32_t* perm,
+                                    int64_t row_begin, int64_t row_end, int64_t* row_id,
+                                    int32_t* col, float* val, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  if (!perm || !row_id || !col || !val || (ncand > 0 && (!cand_key || !cand_val)) || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (n < 2 || row_begin < 0 || row_end > n || row_begin > row_end || ncand < 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "row range / n / ncand invalid");
+  if (t < 1 || t > GGM_MAX_TOPK) return fail(GGM_ERR_INVALID_ARGUMENT, "t=%d invalid", t);
+  const int te = (int)std::min<int64_t>(t, n - 1);
+  size_t need = 0;
+  ggm_sym_merge_workspace(ncand, &need);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  reset_launches();
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const size_t a = ((size_t)std::max<int64_t>(ncand, 1) * sizeof(uint32_t) + 255) & ~size_t(255);
+  const size_t b = ((size_t)std::max<int64_t>(ncand, 1) * sizeof(uint2) + 255) & ~size_t(255);
+  uint32_t* skey = reinterpret_cast<uint32_t*>(ws);
+  uint2* sval = reinterpret_cast<uint2*>(ws + a);
+  void* tmp = ws + a + b;
+  if (ncand > 0) {
+    int ebits = 1;
+    while ((int64_t(1) << ebits) <= n) ++ebits;
+    size_t tb = need - a - b - 256;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, cand_key, skey,
+                                                 reinterpret_cast<const uint2*>(cand_val), sval,
+                                                 ncand, 0, ebits, s));
+  }
+  const int64_t rows = row_end - row_begin;
+  if (rows > 0) {
+    const int threads = 128;
+    const int blocks = (int)((rows + threads - 1) / threads);
+    if (te <= 5)
+      merge_sym<5><<<blocks, threads, 0, s>>>(skey, sval, ncand, n, te, perm, row_begin, row_end, row_id, nullptr, col, val);
+    else if (te <= 10)
+      merge_sym<10><<<blocks, threads, 0, s>>>(skey, sval, ncand, n, te, perm, row_begin, row_end, row_id, nullptr, col, val);
+    else if (te <= 16)
+      merge_sym<16><<<blocks, threads, 0, s>>>(skey, sval, ncand, n, te, perm, row_begin, row_end, row_id, nullptr, col, val);
+    else
+      merge_sym<32><<<blocks, threads, 0, s>>>(skey, sval, ncand, n, te, perm, row_begin, row_end, row_id, nullptr, col, val);
+    count_launches(1);
+    GGM_CUDA_TRY(cudaGetLastError());
+  }
   return GGM_OK;
 }

@@ -1,11 +1,18 @@
-"""Row-sharded multi-GPU driver for ggm_sparse_precision.
+"""Multi-GPU drivers for ggm_sparse_precision.
 
-Rows of Ψ_l = V_l diag(λ_l) V_l^T are independent units (each row's top-t needs all n
-columns but no other row), so rank r owns rows [begin_r, end_r) of every axis and sweeps all
-n columns locally.  V_l and λ_l are replicated (one NCCL broadcast from rank 0); the only
-data-path collective is the gather of the per-rank CSR shards.  One process per GPU,
-torch.distributed over NCCL (NVLink/NVSwitch) on the GPU box; the same code runs on gloo for
-the CPU tests (tests/test_parallel.py) with an injected compute function.
+Plain scheme (row shards): rows of Ψ_l = V_l diag(λ_l) V_l^T are independent units (each
+row's top-t needs all n columns but no other row), so rank r owns rows [begin_r, end_r) of
+every axis and sweeps all n columns locally.  V_l and λ_l are replicated (one NCCL broadcast
+from rank 0); the only data-path collective is the gather of the per-rank CSR shards.
+
+Symmetric scheme (Ψ = Ψᵀ, each unordered block pair once): every rank runs the replicated
+seed/ordering phases and its share of the symmetric units, which emit candidates for rows
+owned by any rank; one all-to-all moves each candidate bucket to the owner of its target
+row, which merges its rows; the CSR rows (in bound order, with their original ids) are then
+all-gathered and scattered.
+
+One process per GPU, torch.distributed over NCCL (NVLink/NVSwitch) on the GPU box; the same
+code runs on gloo for the CPU tests (tests/test_parallel.py) with injected compute functions.
 """
 from __future__ import annotations
 
@@ -90,3 +97,93 @@ def sharded_sparse_precision(axes, t: int, compute: Callable | None = None, grou
         else:
             out.append((rp, col, val))
     return out
+
+
+def exchange_candidates(key: torch.Tensor, val: torch.Tensor, counts, group=None):
+    """All-to-all of key-sorted candidate buckets (bucket r -> rank r).  key: [m], val: [m, 2]
+    (int32 views of (source, ψ bits)); counts: per-destination sizes, in rank order.
+    Returns the (key, val) this rank received."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return key, val
+    send = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=key.device)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    rc = [int(x) for x in recv.tolist()]
+    sc = [int(c) for c in counts]
+    rkey = torch.empty(sum(rc), dtype=key.dtype, device=key.device)
+    rval = torch.empty((sum(rc), 2), dtype=val.dtype, device=val.device)
+    dist.all_to_all_single(rkey, key.contiguous(), output_split_sizes=rc, input_split_sizes=sc,
+                           group=group)
+    dist.all_to_all_single(rval, val.contiguous(), output_split_sizes=rc, input_split_sizes=sc,
+                           group=group)
+    return rkey, rval
+
+
+def assemble_rows(row_id: torch.Tensor, col: torch.Tensor, val: torch.Tensor, n: int,
+                  t_eff: int, group=None):
+    """All-gather the (original row id, t_eff columns, t_eff values) rows every rank merged
+    and scatter them into one full CSR (row_ptr = i * t_eff) on every rank."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    dev = col.device
+    if world > 1:
+        m = torch.tensor([row_id.numel()], dtype=torch.int64, device=dev)
+        ms = [torch.empty_like(m) for _ in range(world)]
+        dist.all_gather(ms, m, group=group)
+        sizes = [int(x.item()) for x in ms]
+        mx = max(sizes)
+        rid = torch.full((mx,), -1, dtype=torch.int64, device=dev)
+        c = torch.zeros((mx * t_eff,), dtype=col.dtype, device=dev)
+        v = torch.zeros((mx * t_eff,), dtype=val.dtype, device=dev)
+        rid[:row_id.numel()] = row_id
+        c[:col.numel()] = col
+        v[:val.numel()] = val
+        rid_all = [torch.empty_like(rid) for _ in range(world)]
+        c_all = [torch.empty_like(c) for _ in range(world)]
+        v_all = [torch.empty_like(v) for _ in range(world)]
+        dist.all_gather(rid_all, rid, group=group)
+        dist.all_gather(c_all, c, group=group)
+        dist.all_gather(v_all, v, group=group)
+        row_id = torch.cat([r[:sz] for r, sz in zip(rid_all, sizes)])
+        col = torch.cat([x[:sz * t_eff] for x, sz in zip(c_all, sizes)])
+        val = torch.cat([x[:sz * t_eff] for x, sz in zip(v_all, sizes)])
+    if row_id.numel() != n:
+        raise RuntimeError(f"assembled {row_id.numel()} rows, expected {n}")
+    full_c = torch.empty((n, t_eff), dtype=col.dtype, device=dev)
+    full_v = torch.empty((n, t_eff), dtype=val.dtype, device=dev)
+    full_c[row_id] = col.view(-1, t_eff)
+    full_v[row_id] = val.view(-1, t_eff)
+    rp = torch.arange(0, (n + 1) * t_eff, t_eff, dtype=torch.int64, device=dev)
+    return rp, full_c.view(-1), full_v.view(-1)
+
+
+def sharded_symmetric_precision(V, lam, t: int, group=None, shard=None, merge=None,
+                                rows_begin=None, gather: bool = True):
+    """Distributed symmetric scheme for one axis (include/ggm.h (3b)).
+
+    shard      : (V, λ, t, rank, world) -> (key, val, counts, perm); default libggm
+                 ggm_sparse_precision_sym_shard.
+    merge      : (n, t, key, val, perm, row_begin, row_end) -> (row_id, col, val); default
+                 libggm ggm_sym_merge.
+    rows_begin : (rank) -> first bound-order row owned by rank (default ggm_sym_rows_begin).
+    Returns the full CSR (gather) or this rank's (row_id, col, val)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n, k = V.shape
+    if shard is None or merge is None or rows_begin is None:
+        from . import _ggm as G
+        if shard is None:
+            def shard(V_, lam_, tt, r, w):
+                return G.SymShardPlan(n, k, tt, r, w, device=V_.device).run(V_, lam_)
+        if merge is None:
+            merge = G.sym_merge
+        if rows_begin is None:
+            def rows_begin(r):
+                return G.sym_rows_begin(n, k, t, r, world)
+    key, val, counts, perm = shard(V, lam, t, rank, world)
+    rkey, rval = exchange_candidates(key, val, counts, group=group)
+    b, e = rows_begin(rank), rows_begin(rank + 1)
+    row_id, col, vals = merge(n, t, rkey, rval, perm, b, e)
+    if not gather:
+        return row_id, col, vals
+    return assemble_rows(row_id, col, vals, n, min(t, n - 1), group=group)

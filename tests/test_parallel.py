@@ -90,3 +90,97 @@ def test_gather_single_process_passthrough():
     rp, c, v = gather_topk_csr(col, val, 3, 4)
     assert rp.tolist() == [0, 3, 6, 9, 12]
     assert torch.equal(c, col)
+
+
+# ---------------------------------------------------------------- distributed symmetric scheme
+# Host logic of parallel.sharded_symmetric_precision (all-to-all of candidate buckets, merge
+# of the received rows, all-gather + scatter by original row id) with oracle-backed injected
+# shard / merge functions standing in for libggm's ggm_sparse_precision_sym_shard / ggm_sym_merge.
+
+def _sym_fns(n, world, t):
+    import oracle as O
+    rng = np.random.default_rng(12)
+    perm = rng.permutation(n).astype(np.int32)          # bound order -> original id
+    bounds = [shard_rows(n, world, r)[0] for r in range(world)] + [n]
+
+    def rows_begin(r):
+        return bounds[r]
+
+    def shard(V, lam, tt, rank, w):
+        Vp = V.numpy()[perm]                            # rows in bound order
+        P = O.psi_rows(Vp, lam.numpy(), np.arange(n))
+        A = np.abs(P)
+        np.fill_diagonal(A, -1.0)
+        thr = -np.partition(-A, min(tt + 3, n - 2), axis=1)[:, min(tt + 3, n - 2)]
+        keys, src, vals = [], [], []
+        for i in range(bounds[rank], bounds[rank + 1]):  # this rank's pairs (i, j), j >= i
+            for j in range(i, n):
+                if j == i:
+                    continue
+                if A[i, j] >= thr[i]:
+                    keys.append(i); src.append(j); vals.append(P[i, j])
+                if A[j, i] >= thr[j]:               # the transposed direction
+                    keys.append(j); src.append(i); vals.append(P[j, i])
+        order = np.argsort(np.asarray(keys, np.int64), kind="stable")
+        keys = np.asarray(keys, np.int32)[order]
+        v2 = np.stack([np.asarray(src, np.int32)[order],
+                       np.asarray(vals, np.float32)[order].view(np.int32)], 1)
+        counts = [int(np.sum((keys >= bounds[d]) & (keys < bounds[d + 1]))) for d in range(w)]
+        return torch.from_numpy(keys), torch.from_numpy(v2), counts, torch.from_numpy(perm)
+
+    def merge(nn, tt, key, val, pm, b, e):
+        key, val, pm = key.numpy(), val.numpy(), pm.numpy()
+        te = min(tt, nn - 1)
+        rid, cols, vs = [], [], []
+        for j in range(b, e):
+            sel = key == j
+            src = pm[val[sel, 0]]
+            v = val[sel, 1].copy().view(np.float32)
+            order = np.lexsort((src, -np.abs(v)))[:te]
+            keep = np.argsort(src[order], kind="stable")
+            rid.append(pm[j]); cols.append(src[order][keep]); vs.append(v[order][keep])
+        return (torch.tensor(rid, dtype=torch.int64),
+                torch.from_numpy(np.concatenate(cols).astype(np.int32)) if cols else torch.empty(0, dtype=torch.int32),
+                torch.from_numpy(np.concatenate(vs).astype(np.float32)) if vs else torch.empty(0))
+
+    return shard, merge, rows_begin
+
+
+def _sym_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from synth import gen
+        from paper_2407_19892_b200.parallel import sharded_symmetric_precision
+        n, k, t = 150, 6, 5
+        V, lam = gen.small_factor(31, n, k)
+        shard, merge, rows_begin = _sym_fns(n, world, t)
+        rp, c, v = sharded_symmetric_precision(torch.from_numpy(V), torch.from_numpy(lam), t,
+                                               shard=shard, merge=merge, rows_begin=rows_begin)
+        q.put((rank, rp.numpy(), c.numpy(), v.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_symmetric_equals_oracle(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sym_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import oracle as O
+    from synth import gen
+    n, k, t = 150, 6, 5
+    V, lam = gen.small_factor(31, n, k)
+    rp1, c1, v1 = O.sparse_precision(V, lam, 0, n, mode=0, t=t)
+    for _, rp, c, v in got:                      # every rank holds the full CSR
+        np.testing.assert_array_equal(rp, rp1)
+        np.testing.assert_array_equal(c, c1)
+        np.testing.assert_allclose(v, v1, rtol=1e-6)
