@@ -203,6 +203,25 @@ def stage_timings(G, torch):
                      "stationarity": info["stationarity"],
                      "grid_points_per_s": pts * max(info["iterations"], 1) / (solve_ms * 1e-3),
                      "grid_points": pts}
+    # at-scale spectrum: a 40,000 x 40,000 unfolding (beyond the dense
+    # Gram path) of known spectrum, X = U diag(s) W^T, k = 50, randomized subspace iteration
+    d = m = 40_000
+    g = torch.Generator(device="cuda").manual_seed(11)
+    U = torch.linalg.qr(torch.randn(d, 64, device="cuda", dtype=torch.float64, generator=g))[0]
+    W = torch.linalg.qr(torch.randn(m, 64, device="cuda", dtype=torch.float64, generator=g))[0]
+    sv = torch.logspace(3, 1, 64, device="cuda", dtype=torch.float64)
+    X = ((U * sv) @ W.T).float()
+    del U, W
+    G.ggm_gram_eig_rsi(X, 0, 50)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, E, _, it, ch = G.ggm_gram_eig_rsi(X, 0, 50)
+    rsi_ms = (time.perf_counter() - t0) * 1e3
+    err = float(torch.max(torch.abs(E - sv[:50] ** 2) / sv[:50] ** 2))
+    out["rsi_40000x40000_k50"] = {"ms": rsi_ms, "iterations": it, "ritz_change": ch,
+                                  "max_rel_err_vs_closed_form": err}
+    del X
+    torch.cuda.empty_cache()
     return out
 
 

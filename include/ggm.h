@@ -79,6 +79,25 @@ ggm_status ggm_gram_eig(const float *X, int ndim, const int64_t *shape, int axis
                         float *V, double *E, double *trace_S, void *workspace,
                         size_t workspace_bytes, void *stream);
 
+/* (1b) At-scale Gram spectrum: the top-k eigenpairs of S_axis by
+ * randomized subspace iteration in fp64 (Halko–Martinsson–Tropp range finder with power
+ * steps and Rayleigh–Ritz), never forming the d x d Gram: M = mat_axis(X) (fp64 copy,
+ * d x m), Y = M Ω (Ω: m x r seeded standard normals, r = k + oversample), Q = qr(Y), then
+ * repeated { Z = Mᵀ Q; T = Zᵀ Z = Qᵀ S Q; eig(T); Q = qr(M Z) } until the top-k Ritz
+ * values change by <= tol relative to the largest (or max_iter).  V = Q W_k, E = Ritz
+ * values.  ggm_gram_eig uses it automatically (oversample = max(16, k), tol 1e-13,
+ * max_iter 200) when both sides of the unfolding exceed 32768.  Memory: 8·d·m bytes for
+ * the fp64 unfolding + O((d + m)·r).  oversample <= 0 selects max(16, k).
+ *  iters_out / change_out (host, optional): iterations run and the last relative change
+ *  (> tol when max_iter was reached: the subspace did not converge to tol).
+ * Synchronizes `stream` once per iteration. */
+ggm_status ggm_gram_eig_rsi_workspace(int ndim, const int64_t *shape, int axis, int k,
+                                      int oversample, size_t *bytes);
+ggm_status ggm_gram_eig_rsi(const float *X, int ndim, const int64_t *shape, int axis, int k,
+                            int oversample, int max_iter, double tol, uint64_t seed, float *V,
+                            double *E, double *trace_S, int *iters_out, double *change_out,
+                            void *workspace, size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------------------------
  * (2) Eigenvalue MLE — Theorem 2, Algorithm 1 lines 5-17.
  *

@@ -27,7 +27,7 @@ MAX_TOPK = 32
 # symbols declared in include/ggm.h (checked by tests/test_abi.py)
 EXPORTED = [
     "ggm_last_error", "ggm_version", "ggm_device_supported",
-    "ggm_gram_eig_workspace", "ggm_gram_eig",
+    "ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_gram_eig_rsi_workspace", "ggm_gram_eig_rsi",
     "ggm_solve_opts_default", "ggm_solve_eigvals", "ggm_grid_marginals",
     "ggm_sparse_precision_workspace", "ggm_sparse_precision",
     "ggm_set_timing", "ggm_last_timing", "ggm_last_launches", "ggm_last_stats",
@@ -78,6 +78,11 @@ def lib() -> C.CDLL:
     L.ggm_gram_eig_workspace.argtypes = [i32, C.POINTER(i64), i32, i32, C.POINTER(C.c_size_t)]
     L.ggm_gram_eig.argtypes = [vp, i32, C.POINTER(i64), i32, i32, vp, vp, C.POINTER(C.c_double),
                                vp, C.c_size_t, vp]
+    L.ggm_gram_eig_rsi_workspace.argtypes = [i32, C.POINTER(i64), i32, i32, i32,
+                                             C.POINTER(C.c_size_t)]
+    L.ggm_gram_eig_rsi.argtypes = [vp, i32, C.POINTER(i64), i32, i32, i32, i32, C.c_double,
+                                   C.c_uint64, vp, vp, C.POINTER(C.c_double), C.POINTER(i32),
+                                   C.POINTER(C.c_double), vp, C.c_size_t, vp]
     L.ggm_solve_opts_default.argtypes = [C.POINTER(SolveOpts)]
     L.ggm_solve_opts_default.restype = None
     L.ggm_solve_eigvals.argtypes = [i32, C.POINTER(i32), vp, C.POINTER(SolveOpts), vp,
@@ -104,6 +109,7 @@ def lib() -> C.CDLL:
     L.ggm_sym_merge_workspace.argtypes = [i64, C.POINTER(C.c_size_t)]
     L.ggm_sym_merge.argtypes = [i64, i32, vp, vp, i64, vp, i64, i64, vp, vp, vp, vp, C.c_size_t, vp]
     for name in ("ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
+                 "ggm_gram_eig_rsi_workspace", "ggm_gram_eig_rsi",
                  "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision",
                  "ggm_sparse_precision_sym_shard_workspace", "ggm_sparse_precision_sym_shard",
                  "ggm_sym_merge_workspace", "ggm_sym_merge"):
@@ -161,6 +167,26 @@ def ggm_gram_eig(X: torch.Tensor, axis: int, k: int, stream=None):
     _check(lib().ggm_gram_eig(_ptr(X), X.dim(), shape, axis, k, _ptr(V), _ptr(E), C.byref(tr),
                               _ptr(ws), nbytes.value, _stream(stream)))
     return V, E, tr.value
+
+
+def ggm_gram_eig_rsi(X: torch.Tensor, axis: int, k: int, oversample: int = 0,
+                     max_iter: int = 200, tol: float = 1e-13, seed: int = 0x2407198920240728,
+                     stream=None):
+    """At-scale top-k eigenpairs of S_axis by randomized subspace iteration (include/ggm.h
+    (1b)).  Returns (V, E, trace_S, iterations, last relative change of the Ritz values)."""
+    _require_cuda(X, torch.float32, "X")
+    shape = (C.c_int64 * X.dim())(*X.shape)
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_gram_eig_rsi_workspace(X.dim(), shape, axis, k, oversample, C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=X.device)
+    d = X.shape[axis]
+    V = torch.empty((d, k), dtype=torch.float32, device=X.device)
+    E = torch.empty((k,), dtype=torch.float64, device=X.device)
+    tr, it, ch = C.c_double(0.0), C.c_int(0), C.c_double(0.0)
+    _check(lib().ggm_gram_eig_rsi(_ptr(X), X.dim(), shape, axis, k, oversample, max_iter, tol,
+                                  C.c_uint64(seed), _ptr(V), _ptr(E), C.byref(tr), C.byref(it),
+                                  C.byref(ch), _ptr(ws), nbytes.value, _stream(stream)))
+    return V, E, tr.value, it.value, ch.value
 
 
 # --------------------------------------------------------------------------- (2) solve

@@ -179,9 +179,14 @@ static ggm_status make_gplan(int ndim, const int64_t* shape, int axis, int k, GP
     g->Md_rows = g->d;
     g->Md_cols = g->m;
   }
-  if (g->dim > 32768) return fail(GGM_ERR_UNSUPPORTED, "Gram dimension %lld too large", (long long)g->dim);
   return GGM_OK;
 }
+// Gram dimensions above this use randomized subspace iteration (ggm_gram_eig_rsi): a dense
+// fp64 eigensolve of a 32768^2 Gram (8.6 GB) is already minutes of DSYEVD.
+constexpr int64_t kMaxDenseGram = 32768;
+constexpr int kRsiMaxIter = 200;       // ggm_gram_eig's automatic at-scale path
+constexpr double kRsiTol = 1e-13;      // max relative change of the top-k Ritz values
+constexpr uint64_t kRsiSeed = 0x2407198920240728ull;
 
 static size_t gcarve(const GPlan& g, int lwork, void* ws, double** Md, double** S, double** w,
                      double** work, int** info, double** V64, double** fro, double** Ek,
@@ -212,11 +217,206 @@ static ggm_status query_lwork(const GPlan& g, int* lwork) {
   return GGM_OK;
 }
 
+
+// ------------------------------------------------------------------ randomized subspace iteration
+// Seeded standard normals (counter-based splitmix64 + Box-Muller): Omega[idx], idx < count.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void fill_normal(double* __restrict__ out, int64_t count, uint64_t seed) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < count;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = splitmix64(seed ^ (2 * (uint64_t)idx));
+    const uint64_t b = splitmix64(seed ^ (2 * (uint64_t)idx + 1));
+    const double u1 = ((double)(a >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double u2 = ((double)(b >> 11)) * (1.0 / 9007199254740992.0);
+    out[idx] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+  }
+}
+
+struct RPlan {
+  int64_t d, m, pre_n, post_n;
+  int k, r;  // wanted pairs, subspace width (k + oversampling)
+  int lw_syevd, lw_geqrf, lw_orgqr;
+};
+
+static ggm_status make_rplan(int ndim, const int64_t* shape, int axis, int k, int oversample,
+                             RPlan* rp) {
+  GPlan g;
+  ggm_status st = make_gplan(ndim, shape, axis, k, &g);
+  if (st != GGM_OK) return st;
+  rp->d = g.d;
+  rp->m = g.m;
+  rp->pre_n = g.pre_n;
+  rp->post_n = g.post_n;
+  rp->k = k;
+  const int64_t mn = std::min(g.d, g.m);
+  const int64_t p = oversample > 0 ? oversample : std::max<int64_t>(16, k);
+  rp->r = (int)std::min<int64_t>(mn, k + p);
+  cusolverDnHandle_t h = g_handles.solver;
+  if (!h && cusolverDnCreate(&g_handles.solver) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnCreate failed");
+  h = g_handles.solver;
+  if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, rp->r,
+                                  nullptr, rp->r, nullptr, &rp->lw_syevd) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDgeqrf_bufferSize(h, (int)rp->d, rp->r, nullptr, (int)rp->d, &rp->lw_geqrf) !=
+          CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDorgqr_bufferSize(h, (int)rp->d, rp->r, rp->r, nullptr, (int)rp->d, nullptr,
+                                  &rp->lw_orgqr) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cuSOLVER buffer size query failed");
+  if (rp->d > INT32_MAX || rp->m > INT32_MAX)
+    return fail(GGM_ERR_UNSUPPORTED, "axis extents above 2^31 are not supported");
+  return GGM_OK;
+}
+
+struct RWork {
+  double *M, *Om, *Y, *T, *w, *work, *tau, *V64, *fro, *Ek, *Wk;
+  int* info;
+};
+static size_t rcarve(const RPlan& rp, void* ws, RWork* w) {
+  Carve c(ws);
+  w->M = c.take<double>((size_t)rp.d * rp.m);
+  w->Om = c.take<double>((size_t)rp.m * rp.r);  // Omega, then Z = M^T Q
+  w->Y = c.take<double>((size_t)rp.d * rp.r);   // Y = M Z, then Q
+  w->T = c.take<double>((size_t)rp.r * rp.r);
+  w->w = c.take<double>((size_t)rp.r);
+  w->work = c.take<double>((size_t)std::max({rp.lw_syevd, rp.lw_geqrf, rp.lw_orgqr, 1}));
+  w->tau = c.take<double>((size_t)rp.r);
+  w->V64 = c.take<double>((size_t)rp.d * rp.k);
+  w->fro = c.take<double>(4);
+  w->Ek = c.take<double>((size_t)rp.k);
+  w->Wk = c.take<double>((size_t)rp.r * rp.k);
+  w->info = c.take<int>(4);
+  return c.used();
+}
+
+// top-k of T's eigen-decomposition (ascending w, vectors in T): Ek descending, Wk (r x k)
+__global__ void take_topk_small(const double* __restrict__ w, const double* __restrict__ T, int r,
+                                int k, double* __restrict__ Ek, double* __restrict__ Wk) {
+  const int c = blockIdx.x;
+  if (c >= k) return;
+  const int src = r - 1 - c;
+  if (threadIdx.x == 0) Ek[c] = w[src];
+  for (int i = threadIdx.x; i < r; i += blockDim.x) Wk[(size_t)c * r + i] = T[(size_t)src * r + i];
+}
+
 }  // namespace ge
 }  // namespace ggm
 
 using namespace ggm;
 using namespace ggm::ge;
+
+extern "C" ggm_status ggm_gram_eig_rsi_workspace(int ndim, const int64_t* shape, int axis, int k,
+                                                 int oversample, size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  RPlan rp;
+  ggm_status st = make_rplan(ndim, shape, axis, k, oversample, &rp);
+  if (st != GGM_OK) return st;
+  RWork w;
+  *bytes = rcarve(rp, nullptr, &w);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_gram_eig_rsi(const float* X, int ndim, const int64_t* shape, int axis,
+                                       int k, int oversample, int max_iter, double tol,
+                                       uint64_t seed, float* V, double* E, double* trace_S,
+                                       int* iters_out, double* change_out, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+  if (!X || !V || !E || !workspace) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  if (max_iter < 1 || !(tol >= 0.0)) return fail(GGM_ERR_INVALID_ARGUMENT, "max_iter/tol invalid");
+  RPlan rp;
+  ggm_status st = make_rplan(ndim, shape, axis, k, oversample, &rp);
+  if (st != GGM_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  RWork w;
+  const size_t need = rcarve(rp, workspace, &w);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  const int sms = num_sms();
+  const int d = (int)rp.d, m = (int)rp.m, r = rp.r, kk = rp.k;
+  GGM_CUDA_TRY(cudaMemsetAsync(w.fro, 0, sizeof(double), s));
+  {
+    const int64_t total = rp.pre_n * rp.d * rp.post_n;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 16));
+    unfold_f64<<<grid, 256, 0, s>>>(X, rp.pre_n, rp.d, rp.post_n, w.M, w.fro);  // M: d x m
+    fill_normal<<<(int)std::min<int64_t>(((int64_t)m * r + 255) / 256, sms * 8), 256, 0, s>>>(
+        w.Om, (int64_t)m * r, seed);
+    GGM_CUDA_TRY(cudaGetLastError());
+  }
+  const double one = 1.0, zero = 0.0;
+  auto orth = [&](double* A) -> ggm_status {  // A (d x r) := Q of its Householder QR
+    if (cusolverDnDgeqrf(hs, d, r, A, d, w.tau, w.work, rp.lw_geqrf, w.info) != CUSOLVER_STATUS_SUCCESS ||
+        cusolverDnDorgqr(hs, d, r, r, A, d, w.tau, w.work, rp.lw_orgqr, w.info) != CUSOLVER_STATUS_SUCCESS)
+      return fail(GGM_ERR_CUDA, "cuSOLVER QR failed");
+    return GGM_OK;
+  };
+  // range finder: Y = M Omega, Q = orth(Y)
+  if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, d, r, m, &one, w.M, d, w.Om, m, &zero, w.Y, d) !=
+      CUBLAS_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+  st = orth(w.Y);
+  if (st != GGM_OK) return st;
+  std::vector<double> prev(kk, 0.0), cur(kk);
+  int it = 0;
+  double change = INFINITY;
+  for (it = 1; it <= max_iter; ++it) {
+    // Rayleigh-Ritz on span(Q): Z = M^T Q (m x r), T = Z^T Z = Q^T S Q (r x r)
+    if (cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, r, d, &one, w.M, d, w.Y, d, &zero, w.Om, m) !=
+            CUBLAS_STATUS_SUCCESS ||
+        cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, r, m, &one, w.Om, m, &zero, w.T, r) !=
+            CUBLAS_STATUS_SUCCESS)
+      return fail(GGM_ERR_CUDA, "cuBLAS Rayleigh-Ritz failed");
+    if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, r, w.T, r, w.w,
+                         w.work, rp.lw_syevd, w.info) != CUSOLVER_STATUS_SUCCESS)
+      return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed");
+    take_topk_small<<<kk, 128, 0, s>>>(w.w, w.T, r, kk, w.Ek, w.Wk);
+    GGM_CUDA_TRY(cudaMemcpyAsync(cur.data(), w.Ek, sizeof(double) * kk, cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    change = 0.0;
+    for (int c = 0; c < kk; ++c)
+      change = std::max(change, std::fabs(cur[c] - prev[c]) / std::max(std::fabs(cur[0]), 1e-300));
+    prev = cur;
+    if (change <= tol || r >= std::min(d, m) || it == max_iter) break;
+    // power step: Y = M Z = S Q, Q = orth(Y)
+    if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, d, r, m, &one, w.M, d, w.Om, m, &zero, w.Y, d) !=
+        CUBLAS_STATUS_SUCCESS)
+      return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+    st = orth(w.Y);
+    if (st != GGM_OK) return st;
+  }
+  // Ritz vectors V = Q W_k (d x k)
+  if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, d, kk, r, &one, w.Y, d, w.Wk, r, &zero, w.V64, d) !=
+      CUBLAS_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+  sign_and_store<<<kk, 256, 0, s>>>(w.V64, rp.d, kk, V);
+  GGM_CUDA_TRY(cudaGetLastError());
+  GGM_CUDA_TRY(cudaMemcpyAsync(E, w.Ek, sizeof(double) * kk, cudaMemcpyDeviceToDevice, s));
+  double hfro = 0.0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hfro, w.fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (trace_S) *trace_S = hfro;
+  if (iters_out) *iters_out = it > max_iter ? max_iter : it;
+  if (change_out) *change_out = change;
+  if (!(cur[0] > 0.0) || !std::isfinite(cur[0]) || !(cur[kk - 1] > 1e-12 * cur[0]))
+    return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)",
+                cur[kk - 1], cur[0]);
+  return GGM_OK;
+}
+
+namespace ggm {
+namespace ge {
+}  // namespace ge
+}  // namespace ggm
+
 
 extern "C" ggm_status ggm_gram_eig_workspace(int ndim, const int64_t* shape, int axis, int k,
                                              size_t* bytes) {
@@ -224,6 +424,8 @@ extern "C" ggm_status ggm_gram_eig_workspace(int ndim, const int64_t* shape, int
   GPlan g;
   ggm_status st = make_gplan(ndim, shape, axis, k, &g);
   if (st != GGM_OK) return st;
+  if (g.dim > kMaxDenseGram)  // at-scale path (randomized subspace iteration)
+    return ggm_gram_eig_rsi_workspace(ndim, shape, axis, k, 0, bytes);
   int lwork = 0;
   st = query_lwork(g, &lwork);
   if (st != GGM_OK) return st;
@@ -240,6 +442,9 @@ extern "C" ggm_status ggm_gram_eig(const float* X, int ndim, const int64_t* shap
   GPlan g;
   ggm_status st = make_gplan(ndim, shape, axis, k, &g);
   if (st != GGM_OK) return st;
+  if (g.dim > kMaxDenseGram)  // at-scale path: both sides of the unfolding exceed 32768
+    return ggm_gram_eig_rsi(X, ndim, shape, axis, k, 0, kRsiMaxIter, kRsiTol, kRsiSeed, V, E,
+                            trace_S, nullptr, nullptr, workspace, workspace_bytes, stream);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cublasHandle_t hb;
   cusolverDnHandle_t hs;
