@@ -239,6 +239,21 @@ ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t *cand_key, const uint3
                          int64_t *row_id, int32_t *col, float *val, void *workspace,
                          size_t workspace_bytes, void *stream);
 
+/* ------------------------------------------------------------------------------------
+ * (4) Edge significance (Theorem 5, P:768-; Corollary 10) — host-side scalars.
+ * Single modality: z = sqrt(d_rest)·sigma²·psi/2 ~ N(0,1) under the empty-graph null, with
+ * d_rest = d_\l (product of the other axes) and sigma² the null variance (1 after whole-data
+ * standardisation, 1/L after per-axis standardisation).  p_raw = 2(1 - Phi(|z|)),
+ * p_bonferroni = min(1, n_tests·p_raw) (n_tests: all off-diagonal pairs of the tested axes,
+ * "after applying the Bonferroni correction").
+ * ggm_wald_threshold: the critical magnitude tau = 2·Phi^-1(1 - alpha/(2 n_tests)) /
+ * (sqrt(d_rest)·sigma²): |psi| > tau <=> p_bonferroni < alpha (p = 0.05 after
+ * Bonferroni), for ggm_sparse_precision mode 1. */
+ggm_status ggm_wald_edge(double psi, int64_t d_rest, double sigma2, int64_t n_tests, double *z,
+                         double *p_raw, double *p_bonferroni);
+ggm_status ggm_wald_threshold(int64_t d_rest, double sigma2, double alpha, int64_t n_tests,
+                              double *tau);
+
 /* Per-kernel timing of the last ggm_sparse_precision call on this thread, measured with
  * CUDA events on `stream` when enabled (for bench.py's roofline).  ms[0] = prep (absmax +
  * split, + the seed pass in the symmetric scheme), ms[1] = main fused tcgen05 kernel,

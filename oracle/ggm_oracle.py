@@ -33,6 +33,7 @@ __all__ = [
     "trace_inconsistency",
     "kron_sum", "sb_trace", "dense_nll",
     "psi_rows", "top_t_row", "threshold_row", "sparse_precision",
+    "wald_edge", "wald_threshold",
 ]
 
 
@@ -388,3 +389,22 @@ def sparse_precision(V, lam, row_begin: int, row_end: int, mode: int = 0, t: int
     col = np.concatenate(cols) if cols else np.zeros(0, np.int64)
     val = np.concatenate(vals) if vals else np.zeros(0)
     return np.asarray(ptr, np.int64), col, val
+
+
+# ---------------------------------------------------------------------------
+# Edge significance — Theorem 5 (P:768-), Corollary 10, Bonferroni (P:1033,
+# P:1097).  Single modality: sqrt(d_\l) sigma^2 psi / 2 ~ N(0, 1) under the empty-graph null.
+# ---------------------------------------------------------------------------
+
+def wald_edge(psi: float, d_rest: int, sigma2: float, n_tests: int):
+    """(z, p_raw, p_bonferroni) for one edge (Cor. 10; two-sided; Bonferroni over n_tests)."""
+    from scipy.stats import norm
+    z = np.sqrt(float(d_rest)) * sigma2 * psi / 2.0
+    p_raw = min(1.0, 2.0 * norm.sf(abs(z)))
+    return z, p_raw, min(1.0, n_tests * p_raw)
+
+
+def wald_threshold(d_rest: int, sigma2: float, alpha: float, n_tests: int) -> float:
+    """|psi| above which p_bonferroni < alpha: 2 z_{1 - alpha/(2 n_tests)} / (sqrt(d_\\l) sigma^2)."""
+    from scipy.stats import norm
+    return 2.0 * norm.isf(alpha / (2.0 * n_tests)) / (np.sqrt(float(d_rest)) * sigma2)

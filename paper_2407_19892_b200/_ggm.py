@@ -33,6 +33,7 @@ EXPORTED = [
     "ggm_set_timing", "ggm_last_timing", "ggm_last_launches", "ggm_last_stats",
     "ggm_sym_rows_begin", "ggm_sparse_precision_sym_shard_workspace",
     "ggm_sparse_precision_sym_shard", "ggm_sym_merge_workspace", "ggm_sym_merge",
+    "ggm_wald_edge", "ggm_wald_threshold",
 ]
 
 
@@ -99,6 +100,11 @@ def lib() -> C.CDLL:
     L.ggm_last_launches.restype = i32
     L.ggm_last_stats.argtypes = [C.POINTER(C.c_double)]
     L.ggm_last_stats.restype = None
+    L.ggm_wald_edge.argtypes = [C.c_double, i64, C.c_double, i64, C.POINTER(C.c_double),
+                                C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.ggm_wald_edge.restype = i32
+    L.ggm_wald_threshold.argtypes = [i64, C.c_double, C.c_double, i64, C.POINTER(C.c_double)]
+    L.ggm_wald_threshold.restype = i32
     L.ggm_sym_rows_begin.argtypes = [i64, i32, C.POINTER(SparsifyOpts), i32, i32]
     L.ggm_sym_rows_begin.restype = i64
     L.ggm_sparse_precision_sym_shard_workspace.argtypes = [i64, i32, C.POINTER(SparsifyOpts),
@@ -288,6 +294,22 @@ def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
                           max(e.required, 1), device=V.device, symmetric=symmetric)
         nnz = plan.run(V, lam, stream)
     return plan.row_ptr, plan.col[:nnz], plan.val[:nnz]
+
+
+def wald_edge(psi: float, d_rest: int, sigma2: float, n_tests: int):
+    """(z, p_raw, p_bonferroni) of one edge under the empty-graph null (Thm 5 / Cor. 10)."""
+    z, pr, pb = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().ggm_wald_edge(float(psi), int(d_rest), float(sigma2), int(n_tests), C.byref(z),
+                               C.byref(pr), C.byref(pb)))
+    return z.value, pr.value, pb.value
+
+
+def wald_threshold(d_rest: int, sigma2: float = 1.0, alpha: float = 0.05, n_tests: int = 1) -> float:
+    """Critical magnitude: |psi| > tau <=> Bonferroni-corrected p < alpha."""
+    tau = C.c_double()
+    _check(lib().ggm_wald_threshold(int(d_rest), float(sigma2), float(alpha), int(n_tests),
+                                    C.byref(tau)))
+    return tau.value
 
 
 def sym_rows_begin(n: int, k: int, topk: int, rank: int, nranks: int) -> int:

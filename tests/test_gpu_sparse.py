@@ -161,3 +161,28 @@ def test_symmetric_scheme_vs_oracle_and_plain(G, n, k, t):
     assert G.last_stats()["scheme"] == "plain"
     same = np.mean([np.array_equal(c[rp[i]:rp[i + 1]], c2[rp2[i]:rp2[i + 1]]) for i in range(n)])
     assert same > 0.999
+
+
+def test_wald_significance_threshold_end_to_end(G):
+    """P:1033 recommended rule: keep edges significant at p = 0.05 after Bonferroni.  C1 data
+    standardised to unit variance (sigma^2 = 1 null); spectrum -> MLE -> mode 1 with
+    the Wald critical magnitude (Cor. 10), against the oracle pipeline's threshold sets."""
+    import oracle as O
+    cfg = gen.config("C1")
+    X = cfg["X"].astype(np.float64)
+    X = ((X - X.mean()) / X.std()).astype(np.float32)
+    ks = cfg["k"]
+    Xd = torch.from_numpy(X).cuda()
+    Es = [G.ggm_gram_eig(Xd, a, k)[1] for a, k in enumerate(ks)]
+    lam, _ = G.ggm_solve_eigvals(torch.cat(Es), ks)
+    lams = torch.split(lam, list(ks))
+    n_tests = sum(d * (d - 1) // 2 for d in X.shape)
+    Vo, Eo = zip(*[O.gram_eig(X, a, k) for a, k in enumerate(ks)])
+    lo, _ = O.solve_eigvals(list(Eo), tol=1e-12)
+    for a, k in enumerate(ks):
+        d_rest = int(np.prod(X.shape)) // X.shape[a]
+        tau = G.wald_threshold(d_rest, 1.0, 0.05, n_tests)
+        assert abs(tau - O.wald_threshold(d_rest, 1.0, 0.05, n_tests)) < 1e-12 * tau
+        V, _, _ = G.ggm_gram_eig(Xd, a, k)
+        rp, c, v = _run(G, V.cpu().numpy(), lams[a].cpu().numpy(), 0, X.shape[a], mode=1, tau=tau)
+        check_threshold(rp, c, v, Vo[a].astype(np.float32), lo[a], np.arange(X.shape[a]), tau)
