@@ -33,7 +33,7 @@ __all__ = [
     "trace_inconsistency",
     "kron_sum", "sb_trace", "dense_nll",
     "psi_rows", "top_t_row", "threshold_row", "sparse_precision",
-    "wald_edge", "wald_threshold",
+    "wald_edge", "wald_threshold", "overall_edges", "edges_to_symmetric_csr",
 ]
 
 
@@ -408,3 +408,53 @@ def wald_threshold(d_rest: int, sigma2: float, alpha: float, n_tests: int) -> fl
     """|psi| above which p_bonferroni < alpha: 2 z_{1 - alpha/(2 n_tests)} / (sqrt(d_\\l) sigma^2)."""
     from scipy.stats import norm
     return 2.0 * norm.isf(alpha / (2.0 * n_tests)) / (np.sqrt(float(d_rest)) * sigma2)
+
+
+# ---------------------------------------------------------------------------
+# Whole-graph edge rules (P:1018-1022, P:1033-1036; SPEC S:312 readings, DESIGN.md Q16):
+# overall thresholding ("the n_l largest edges overall"), optionally down-weighting edges of
+# high-degree vertices ("dividing by the total outgoing edge weight of the vertex": score
+# |psi_ij| / sqrt(w_i w_j), w_i = sum_{k != i} |psi_ik|) and keeping a minimum number of
+# edges per vertex (each vertex's m best edges by the same score).
+# ---------------------------------------------------------------------------
+
+def overall_edges(V, lam, n_edges: int, downweight: bool = False, min_edges: int = 0):
+    """Undirected edges (i < j) kept by the overall rule, sorted by (i, j); returns
+    (i, j, psi_ij) arrays.  Dense n x n fp64 (small n only).  Ranking: score descending,
+    ties -> smaller (i, j) lexicographically; min-edges ties -> smaller j."""
+    V = np.asarray(V, np.float64)
+    n = V.shape[0]
+    P = (V * np.asarray(lam, np.float64)) @ V.T
+    A = np.abs(P)
+    np.fill_diagonal(A, 0.0)
+    if downweight:
+        w = A.sum(axis=1)
+        inv = np.where(w > 0, 1.0 / np.sqrt(np.where(w > 0, w, 1.0)), 0.0)
+        S = A * inv[:, None] * inv[None, :]
+    else:
+        S = A
+    iu, ju = np.triu_indices(n, 1)
+    sc = S[iu, ju]
+    order = np.lexsort((ju, iu, -sc))          # score desc, then i, then j
+    keep = set(zip(iu[order[:n_edges]].tolist(), ju[order[:n_edges]].tolist()))
+    if min_edges > 0:
+        for i in range(n):
+            row = S[i].copy()
+            row[i] = -np.inf
+            js = np.lexsort((np.arange(n), -row))[:min(min_edges, n - 1)]
+            for j in js.tolist():
+                keep.add((min(i, j), max(i, j)))
+    e = np.array(sorted(keep), dtype=np.int64).reshape(-1, 2)
+    return e[:, 0], e[:, 1], P[e[:, 0], e[:, 1]]
+
+
+def edges_to_symmetric_csr(n: int, i, j, v):
+    """Both directions of every undirected edge, rows ascending, columns ascending."""
+    r = np.concatenate([i, j])
+    c = np.concatenate([j, i])
+    vv = np.concatenate([v, v])
+    o = np.lexsort((c, r))
+    r, c, vv = r[o], c[o], vv[o]
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, r + 1, 1)
+    return np.cumsum(rp), c, vv

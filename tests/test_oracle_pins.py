@@ -300,3 +300,54 @@ def test_rank1_large_n_topt_is_top_of_v():
         a[i] = -1
         want = sorted(np.argsort(-a, kind="stable")[:10])
         assert list(col[ptr[r]:ptr[r + 1]]) == want
+
+
+# ------------------------------------------------------------------ whole-graph edge rules
+def test_overall_edges_brute_force_and_closed_forms():
+    """overall_edges against brute force over all pairs, and closed forms:
+    rank 1 (psi_ij = lam v_i v_j): the overall top-N pairs are the pairs of the largest |v|;
+    with down-weighting w_i = |v_i| (sum_k|v_k| - |v_i|) ... checked by brute force."""
+    import itertools
+    rng = np.random.default_rng(4)
+    n, k = 23, 4
+    V = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    lam = rng.lognormal(0, 1, k)
+    P = (V * lam) @ V.T
+    for dw in (False, True):
+        A = np.abs(P)
+        np.fill_diagonal(A, 0)
+        w = A.sum(1)
+        pairs = []
+        for i, j in itertools.combinations(range(n), 2):
+            s = A[i, j] / np.sqrt(w[i] * w[j]) if dw else A[i, j]
+            pairs.append((-s, i, j))
+        pairs.sort()
+        for N in (1, 7, 40):
+            want = sorted((i, j) for _, i, j in pairs[:N])
+            ii, jj, vv = O.overall_edges(V, lam, N, downweight=dw)
+            assert list(zip(ii.tolist(), jj.tolist())) == want
+            np.testing.assert_allclose(vv, P[ii, jj])
+    # rank 1 closed form (psi_ij = lam v_i v_j): with a1, a2, a3 the indices of the three
+    # largest |v|, the two largest pairs are {a1, a2} and {a1, a3}
+    v = rng.standard_normal(30)
+    v /= np.linalg.norm(v)
+    ii, jj, _ = O.overall_edges(v.reshape(-1, 1), [2.0], 2)
+    a1, a2, a3 = np.argsort(-np.abs(v))[:3].tolist()
+    assert set(zip(ii.tolist(), jj.tolist())) == {tuple(sorted((a1, a2))), tuple(sorted((a1, a3)))}
+
+
+def test_overall_min_edges_and_symmetric_csr():
+    rng = np.random.default_rng(5)
+    n, k = 40, 5
+    V = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    lam = rng.lognormal(0, 1, k)
+    ii, jj, vv = O.overall_edges(V, lam, 5, downweight=True, min_edges=2)
+    deg = np.bincount(np.concatenate([ii, jj]), minlength=n)
+    assert deg.min() >= 2                         # every vertex keeps >= 2 edges
+    rp, c, v = O.edges_to_symmetric_csr(n, ii, jj, vv)
+    assert rp[-1] == 2 * len(ii)
+    P = (V * lam) @ V.T
+    for r in range(n):
+        cc = c[rp[r]:rp[r + 1]]
+        assert np.all(np.diff(cc) > 0) and r not in cc
+        np.testing.assert_allclose(v[rp[r]:rp[r + 1]], P[r, cc])
