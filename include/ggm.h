@@ -240,6 +240,29 @@ ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t *cand_key, const uint3
                          size_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------
+ * (3c) Whole-graph edge rules (readings in
+ * DESIGN.md Q16): keep the n_edges largest undirected edges overall by score |ψ_ij|, or by
+ * |ψ_ij| / sqrt(w_i·w_j) with w_i = Σ_{k≠i} |ψ_ik| when downweight = 1 ("down-weighting edges
+ * of vertices with high degree"), then add each vertex's min_edges best edges by the
+ * same score — ties -> smaller (i, j).  Output: symmetric CSR (each kept edge in
+ * rows i and j), columns ascending, values ψ_ij; nnz_out = 2·|edges|.
+ * Errors: GGM_ERR_CAPACITY if nnz > capacity (*nnz_out = required), or if the candidate
+ * pass needs more than cand_capacity entries (*nnz_out = -required); both retry-able.
+ * Synchronizes `stream`. */
+typedef struct {
+  int64_t n_edges;  /* N >= 1 (the paper keeps ~10 edges per vertex on scRNA-seq) */
+  int downweight;   /* 0: score |ψ_ij|; 1: |ψ_ij| / sqrt(w_i w_j) */
+  int min_edges;    /* 0..GGM_MAX_TOPK edges per vertex always kept */
+} ggm_overall_opts;
+ggm_status ggm_sparse_precision_overall_workspace(int64_t n, int k, const ggm_overall_opts *opts,
+                                                  int64_t cand_capacity, size_t *bytes);
+ggm_status ggm_sparse_precision_overall(int64_t n, int k, const float *V, const double *lambda,
+                                        const ggm_overall_opts *opts, int64_t cand_capacity,
+                                        int64_t *row_ptr, int32_t *col, float *val,
+                                        int64_t capacity, int64_t *nnz_out, void *workspace,
+                                        size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------
  * (4) Edge significance (Theorem 5, P:768-; Corollary 10) — host-side scalars.
  * Single modality: z = sqrt(d_rest)·sigma²·psi/2 ~ N(0,1) under the empty-graph null, with
  * d_rest = d_\l (product of the other axes) and sigma² the null variance (1 after whole-data

@@ -436,14 +436,16 @@ def overall_edges(V, lam, n_edges: int, downweight: bool = False, min_edges: int
     iu, ju = np.triu_indices(n, 1)
     sc = S[iu, ju]
     order = np.lexsort((ju, iu, -sc))          # score desc, then i, then j
-    keep = set(zip(iu[order[:n_edges]].tolist(), ju[order[:n_edges]].tolist()))
+    order = order[sc[order] > 0][:n_edges]     # an exactly-zero psi_ij is no edge (Q17)
+    keep = set(zip(iu[order].tolist(), ju[order].tolist()))
     if min_edges > 0:
         for i in range(n):
             row = S[i].copy()
             row[i] = -np.inf
             js = np.lexsort((np.arange(n), -row))[:min(min_edges, n - 1)]
             for j in js.tolist():
-                keep.add((min(i, j), max(i, j)))
+                if row[j] > 0:
+                    keep.add((min(i, j), max(i, j)))
     e = np.array(sorted(keep), dtype=np.int64).reshape(-1, 2)
     return e[:, 0], e[:, 1], P[e[:, 0], e[:, 1]]
 

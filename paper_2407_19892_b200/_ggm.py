@@ -34,6 +34,7 @@ EXPORTED = [
     "ggm_sym_rows_begin", "ggm_sparse_precision_sym_shard_workspace",
     "ggm_sparse_precision_sym_shard", "ggm_sym_merge_workspace", "ggm_sym_merge",
     "ggm_wald_edge", "ggm_wald_threshold",
+    "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
 ]
 
 
@@ -58,6 +59,10 @@ class SolveInfo(C.Structure):
 class SparsifyOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("topk", C.c_int), ("tau", C.c_float),
                 ("col_chunks", C.c_int), ("symmetric", C.c_int)]
+
+
+class OverallOpts(C.Structure):
+    _fields_ = [("n_edges", C.c_int64), ("downweight", C.c_int), ("min_edges", C.c_int)]
 
 
 _lib = None
@@ -114,7 +119,12 @@ def lib() -> C.CDLL:
                                                  C.c_size_t, vp]
     L.ggm_sym_merge_workspace.argtypes = [i64, C.POINTER(C.c_size_t)]
     L.ggm_sym_merge.argtypes = [i64, i32, vp, vp, i64, vp, i64, i64, vp, vp, vp, vp, C.c_size_t, vp]
-    for name in ("ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
+    L.ggm_sparse_precision_overall_workspace.argtypes = [i64, i32, C.POINTER(OverallOpts), i64,
+                                                         C.POINTER(C.c_size_t)]
+    L.ggm_sparse_precision_overall.argtypes = [i64, i32, vp, vp, C.POINTER(OverallOpts), i64, vp,
+                                               vp, vp, i64, C.POINTER(i64), vp, C.c_size_t, vp]
+    for name in ("ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
+                 "ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
                  "ggm_gram_eig_rsi_workspace", "ggm_gram_eig_rsi",
                  "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision",
                  "ggm_sparse_precision_sym_shard_workspace", "ggm_sparse_precision_sym_shard",
@@ -294,6 +304,45 @@ def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
                           max(e.required, 1), device=V.device, symmetric=symmetric)
         nnz = plan.run(V, lam, stream)
     return plan.row_ptr, plan.col[:nnz], plan.val[:nnz]
+
+
+def ggm_sparse_precision_overall(V: torch.Tensor, lam: torch.Tensor, n_edges: int,
+                                 downweight: bool = False, min_edges: int = 0,
+                                 cand_capacity: int | None = None, capacity: int | None = None,
+                                 stream=None):
+    """Whole-graph edge rules (include/ggm.h (3c)): the n_edges best undirected
+    edges by |psi| (or |psi|/sqrt(w_i w_j), downweight) plus each vertex's min_edges best.
+    Returns the symmetric CSR (row_ptr, col, val).  Retries on either capacity error."""
+    _require_cuda(V, torch.float32, "V")
+    _require_cuda(lam, torch.float64, "lam")
+    n, k = V.shape
+    o = OverallOpts(int(n_edges), int(bool(downweight)), int(min_edges))
+    if cand_capacity is None:
+        cand_capacity = 4 * int(n_edges) + 2 * n * int(min_edges) + 1024
+    if capacity is None:
+        capacity = 2 * int(n_edges) + 2 * n * int(min_edges)
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device=V.device)
+    for _ in range(4):
+        nbytes = C.c_size_t(0)
+        _check(lib().ggm_sparse_precision_overall_workspace(n, k, C.byref(o), int(cand_capacity),
+                                                            C.byref(nbytes)))
+        ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=V.device)
+        col = torch.empty(max(capacity, 1), dtype=torch.int32, device=V.device)
+        val = torch.empty(max(capacity, 1), dtype=torch.float32, device=V.device)
+        nnz = C.c_int64(0)
+        st = lib().ggm_sparse_precision_overall(n, k, _ptr(V), _ptr(lam), C.byref(o),
+                                                int(cand_capacity), _ptr(row_ptr), _ptr(col),
+                                                _ptr(val), int(capacity), C.byref(nnz), _ptr(ws),
+                                                nbytes.value, _stream(stream))
+        if st == 5 and nnz.value < 0:
+            cand_capacity = -int(nnz.value)
+            continue
+        if st == 5:
+            capacity = int(nnz.value)
+            continue
+        _check(st)
+        return row_ptr, col[:nnz.value], val[:nnz.value]
+    raise GGMError(5, "capacity retries exhausted")
 
 
 def wald_edge(psi: float, d_rest: int, sigma2: float, n_tests: int):

@@ -18,6 +18,7 @@
 //                       the transposed direction emits candidates above the seed bound)
 //   BK3  merge_partials / merge_sym / coo_to_csr  CSR assembly
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -25,6 +26,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstring>
 #include <cstdlib>
 #include <cmath>
 #include <cstdint>
@@ -260,6 +262,7 @@ struct FusedParams {
   unsigned long long* coo_count;
   int64_t capacity;
   float* thr_out;          // kSeed: per-row t-th largest sampled |ψ| (accumulator units)
+  double* mass_out;        // mode 2 (plain): row masses Σ_{j≠i} |ψ_ij| (atomic partials)
   const float* thr;        // kSym: per-(permuted) column lower bound of that row's t-th
                            //       magnitude (accumulator units, +inf = padding)
   const float* thr_min;    // kSym: min of thr over each 32-column chunk
@@ -511,7 +514,7 @@ template <int MAXT, int KIND>
 __device__ __forceinline__ void epi_chunk(const FusedParams& p, const uint32_t (&vr)[32],
                                           uint32_t tchunk, int64_t col0, int64_t gi, int64_t lr,
                                           bool valid, bool need_mask, float tau_s, float sd2,
-                                          TopList<MAXT>& top, int lane) {
+                                          TopList<MAXT>& top, double& macc, int lane) {
   // the loaded registers are only read (never rewritten), so the compiler keeps them in the
   // tcgen05.ld destination block without copies
   float m = max32_abs(reinterpret_cast<const float(&)[32]>(vr));
@@ -525,6 +528,13 @@ __device__ __forceinline__ void epi_chunk(const FusedParams& p, const uint32_t (
 #pragma unroll
     for (int e = 0; e < 32; ++e)
       m = fmaxf(m, ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(vr[e])));
+  }
+  if (p.mode == 2) {  // row mass (degree down-weighting): Σ |ψ_ij| over j != i, j < n
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) sum += ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(vr[e]));
+    macc += (double)sum;
+    return;
   }
   const float thr = p.mode == 0 ? top.thr() : tau_s;
   if (__any_sync(0xffffffffu, m > thr)) {
@@ -604,6 +614,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     const int64_t rlo = p.row_begin + (int64_t)rb * kRowsPerBlock;
     const int64_t rhi = rlo + kRowsPerBlock;
     top.init(t);
+    double macc = 0.0;
     TileIter<KIND, PAIR> ti;
     ti.start(p, u, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s, ti.next(p)) {
@@ -624,14 +635,14 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
           tmem_ld32_nowait(taddr + (c + 1) * 32, vb);
           if (p.dbg != 1)
             epi_chunk<MAXT, KIND>(p, va, taddr + c * 32, cb + c * 32, gi, lr, valid, need_mask,
-                                  tau_s, sd2, top, lane);
+                                  tau_s, sd2, top, macc, lane);
           else if (va[0] == 12345u && va[31] == 54321u)
             p.row_ptr[0] = (int64_t)va[7];
           tmem_wait_ld(vb);
           if (c + 2 < (kTileN / 2) / 32) tmem_ld32_nowait(taddr + (c + 2) * 32, va);
           if (p.dbg != 1)
             epi_chunk<MAXT, KIND>(p, vb, taddr + (c + 1) * 32, cb + (c + 1) * 32, gi, lr, valid,
-                                  need_mask, tau_s, sd2, top, lane);
+                                  need_mask, tau_s, sd2, top, macc, lane);
           else if (vb[0] == 12345u && vb[31] == 54321u)
             p.row_ptr[0] = (int64_t)vb[7];
         }
@@ -643,6 +654,10 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
         buf = 0;
         tphase ^= 1;
       }
+    }
+    if (p.mode == 2) {  // both column halves add their partial row mass (unscaled ψ units)
+      if (valid) atomicAdd(p.mass_out + lr, macc * (double)sd2);
+      continue;
     }
     if (p.mode != 0) continue;
     // merge the two column halves of each row: half 1 publishes (values into its own
@@ -1430,7 +1445,8 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   if (row_begin < 0 || row_end > n || row_begin >= row_end)
     return fail(GGM_ERR_INVALID_ARGUMENT, "row range [%lld,%lld) invalid for n=%lld",
                 (long long)row_begin, (long long)row_end, (long long)n);
-  if (o->mode != 0 && o->mode != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "mode=%d", o->mode);
+  if (o->mode != 0 && o->mode != 1 && o->mode != 2)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "mode=%d", o->mode);
   if (o->mode == 0 && (o->topk < 1))
     return fail(GGM_ERR_INVALID_ARGUMENT, "topk=%d < 1", o->topk);
   if (o->mode == 0 && o->topk > GGM_MAX_TOPK)
@@ -2275,5 +2291,455 @@ extern "C" ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t* cand_key,
     count_launches(1);
     GGM_CUDA_TRY(cudaGetLastError());
   }
+  return GGM_OK;
+}
+
+// ------------------------------------------------------------------ whole-graph edge rules
+// (DESIGN.md §4 "overall"): keep the N largest edges overall by
+// score |ψ_ij| (or |ψ_ij| / sqrt(w_i w_j) with w_i = Σ_{k≠i}|ψ_ik|, down-weighting high-degree
+// vertices), plus each vertex's m best edges.  Down-weighting is a diagonal similarity:
+// score_ij = |ψ'_ij| for Ψ' = D^-1/2 Ψ D^-1/2 = U' U'^T with U' = D^-1/2 U, so every pass runs
+// on the row-scaled factors V' = V ⊙ w^-1/2.  Steps: (1) row masses (plain tiles, mode 2);
+// (2) per-row top-t1 of Ψ' (t1 >= max(m, ceil(2N/n))) -> a lower bound L of the N-th largest
+// score (the smallest row t1-th value, and the 2N-th largest listed value: both are scores of
+// >= N distinct pairs); (3) every directed entry with score >= L (threshold mode); (4) keep
+// i < j, rank (score desc, i, j) with two stable radix sorts, take N, add the min-edges from
+// (2), de-duplicate; (5) symmetric CSR with ψ_ij = ψ'_ij · sqrt(w_i w_j).
+
+namespace ggm {
+namespace sp {
+
+__global__ void scale_rows(const float* __restrict__ V, const double* __restrict__ w, int64_t n,
+                           int k, float* __restrict__ Vs, double* __restrict__ sq) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * (int64_t)k;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / k;
+    const double wr = w ? w[r] : 1.0;
+    const double rs = wr > 0.0 ? 1.0 / sqrt(wr) : 0.0;
+    Vs[i] = (float)((double)V[i] * rs);
+    if (i % k == 0) sq[r] = wr > 0.0 ? sqrt(wr) : 0.0;
+  }
+}
+
+// abs values of the pass-1 list entries; per-row t1-th largest |value| (lists hold exactly t1
+// entries per row) -> atomic min
+__global__ void list_stats(const float* __restrict__ val, int64_t n, int t1,
+                           float* __restrict__ absv, unsigned int* __restrict__ min_tth_bits) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float mn = INFINITY;
+    for (int e = 0; e < t1; ++e) {
+      const float a = fabsf(val[i * t1 + e]);
+      absv[i * t1 + e] = a;
+      mn = fminf(mn, a);
+    }
+    atomicMin(min_tth_bits, __float_as_uint(mn));  // non-negative floats order as uints
+  }
+}
+
+// pass-3 COO (row, col, value') -> upper-triangle candidate arrays (pair key i*n+j, score)
+__global__ void upper_pairs(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const float* __restrict__ val, int64_t n,
+                            unsigned long long* __restrict__ cnt, uint64_t* __restrict__ pkey,
+                            float* __restrict__ score) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      const int64_t j = col[e];
+      if (j <= i) continue;
+      const unsigned long long at = atomicAdd(cnt, 1ull);
+      pkey[at] = (uint64_t)i * (uint64_t)n + (uint64_t)j;
+      score[at] = val[e];  // signed ψ'; ranked by |.|
+    }
+  }
+}
+
+// min-edges: each row's m best list entries (score desc, column asc) -> pair keys (i<j order)
+__global__ void min_edge_pairs(const int32_t* __restrict__ col, const float* __restrict__ val,
+                               int64_t n, int t1, int m, uint64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int a = 0; a < m; ++a) {  // a-th best: rank among the row's t1 entries
+      int best = -1;
+      for (int e = 0; e < t1; ++e) {
+        int rank = 0;
+        const float ae = fabsf(val[i * t1 + e]);
+        const int ce = col[i * t1 + e];
+        for (int f = 0; f < t1; ++f) {
+          const float af = fabsf(val[i * t1 + f]);
+          if (af > ae || (af == ae && col[i * t1 + f] < ce)) ++rank;
+        }
+        if (rank == a) best = e;
+      }
+      const int64_t j = best >= 0 ? col[i * t1 + best] : i;
+      const int64_t lo = j < i ? j : i, hi = j < i ? i : j;
+      // an exactly-zero ψ'_ij is no edge (Q17)
+      const bool ok = best >= 0 && fabsf(val[i * t1 + best]) > 0.f;
+      out[i * m + a] = ok ? (uint64_t)lo * (uint64_t)n + (uint64_t)hi : ~0ull;
+    }
+  }
+}
+
+// final edges (sorted unique pair keys) -> both directions (row key = r*n + c) with ψ values
+__global__ void expand_edges(const uint64_t* __restrict__ pk, int64_t ne, int64_t n,
+                             const float* __restrict__ sval, const double* __restrict__ sq,
+                             uint64_t* __restrict__ dkey, float* __restrict__ dval) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = pk[e] / (uint64_t)n, j = pk[e] % (uint64_t)n;
+    const float v = (float)((double)sval[e] * sq[i] * sq[j]);
+    dkey[2 * e] = i * (uint64_t)n + j;
+    dkey[2 * e + 1] = j * (uint64_t)n + i;
+    dval[2 * e] = v;
+    dval[2 * e + 1] = v;
+  }
+}
+
+__global__ void dir_to_csr(const uint64_t* __restrict__ key, const float* __restrict__ v,
+                           int64_t count, int64_t n, int64_t* row_ptr, int32_t* col, float* val) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < count) {
+      col[e] = (int32_t)(key[e] % (uint64_t)n);
+      val[e] = v[e];
+    }
+    const int64_t r = (e < count) ? (int64_t)(key[e] / (uint64_t)n) : n;
+    const int64_t rp = (e == 0) ? -1 : (int64_t)(key[e - 1] / (uint64_t)n);
+    for (int64_t rr = rp + 1; rr <= r && rr <= n; ++rr) row_ptr[rr] = e;
+  }
+}
+
+}  // namespace sp
+}  // namespace ggm
+
+using namespace ggm;
+using namespace ggm::sp;
+
+namespace {
+
+struct OverallPlan {
+  int64_t n, N, cand_cap, E_max;
+  int k, t1, m, downweight;
+  size_t ws_sub;   // max sub-call workspace (mass / top-t1 / threshold)
+  size_t cub_tmp;  // max CUB temp
+};
+
+ggm_status overall_plan(int64_t n, int k, const ggm_overall_opts* o, int64_t cand_capacity,
+                        OverallPlan* op) {
+  if (!o) return fail(GGM_ERR_INVALID_ARGUMENT, "opts is NULL");
+  if (n < 3 || k < 1 || k > n) return fail(GGM_ERR_INVALID_ARGUMENT, "n >= 3, 1 <= k <= n");
+  const int64_t pairs = n * (n - 1) / 2;
+  if (o->n_edges < 1 || o->n_edges > pairs)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "n_edges=%lld not in [1, n(n-1)/2]", (long long)o->n_edges);
+  if (o->min_edges < 0 || o->min_edges > GGM_MAX_TOPK)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "min_edges not in [0, %d]", GGM_MAX_TOPK);
+  if (cand_capacity < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "cand_capacity < 1");
+  op->n = n;
+  op->k = k;
+  op->N = o->n_edges;
+  op->m = (int)std::min<int64_t>(o->min_edges, n - 1);
+  op->downweight = o->downweight ? 1 : 0;
+  // n·t1 >= 4N listed entries when possible: the 2N-th largest listed value is then a tight
+  // lower bound (exact unless a row holds more than t1 of the top 2N directed entries)
+  const int64_t need_t = 2 * ((2 * op->N + n - 1) / n);
+  op->t1 = (int)std::min<int64_t>(n - 1, std::min<int64_t>(GGM_MAX_TOPK, std::max<int64_t>(
+                                                                std::max<int64_t>(op->m, need_t), 1)));
+  op->cand_cap = cand_capacity;
+  op->E_max = op->N + n * op->m;
+  size_t b = 0, mx = 0;
+  ggm_sparsify_opts so{};
+  so.mode = 2;
+  so.topk = 1;
+  ggm_status st = ggm_sparse_precision_workspace(n, k, 0, n, &so, 0, &b);
+  if (st != GGM_OK) return st;
+  mx = std::max(mx, b);
+  so.mode = 0;
+  so.topk = op->t1;
+  st = ggm_sparse_precision_workspace(n, k, 0, n, &so, n * op->t1, &b);
+  if (st != GGM_OK) return st;
+  mx = std::max(mx, b);
+  so.mode = 1;
+  so.topk = 1;
+  so.tau = 0.f;
+  st = ggm_sparse_precision_workspace(n, k, 0, n, &so, cand_capacity, &b);
+  if (st != GGM_OK) return st;
+  op->ws_sub = std::max(mx, b);
+  size_t c = 0, t = 0;
+  const int64_t L = std::max<int64_t>(op->n * op->t1, std::max<int64_t>(cand_capacity, 2 * op->E_max));
+  cub::DeviceRadixSort::SortKeysDescending(nullptr, t, (const float*)nullptr, (float*)nullptr, L);
+  c = std::max(c, t);
+  cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int64_t*)nullptr, (int64_t*)nullptr, L);
+  c = std::max(c, t);
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, t, (const float*)nullptr, (float*)nullptr,
+                                            (const int64_t*)nullptr, (int64_t*)nullptr, L);
+  c = std::max(c, t);
+  cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const float*)nullptr, (float*)nullptr, L);
+  c = std::max(c, t);
+  cub::DeviceSelect::UniqueByKey(nullptr, t, (const uint64_t*)nullptr, (const float*)nullptr,
+                                 (uint64_t*)nullptr, (float*)nullptr, (int64_t*)nullptr, L);
+  c = std::max(c, t);
+  op->cub_tmp = c;
+  return GGM_OK;
+}
+
+struct OverallWork {
+  float* Vs;
+  double *w, *sq;
+  void* sub;
+  int64_t *rp1, *rp3;
+  int32_t *col1, *col3;
+  float *val1, *val3, *absv, *absv_s;
+  unsigned int* min_bits;
+  unsigned long long* cnt;
+  uint64_t *pk, *pk_s, *uk, *uk_s;
+  float *sc, *ak, *ak_s, *uv, *uv_s;
+  int64_t *idx, *idx1, *idx2, *nsel;
+  void* cub;
+};
+
+size_t overall_carve(const OverallPlan& op, void* ws, OverallWork* w) {
+  Carve c(ws);
+  const int64_t n = op.n, C = op.cand_cap, E = op.E_max, L = n * op.t1;
+  w->Vs = c.take<float>((size_t)n * op.k);
+  w->w = c.take<double>(n);
+  w->sq = c.take<double>(n);
+  w->sub = c.take<char>(op.ws_sub);
+  w->rp1 = c.take<int64_t>(n + 1);
+  w->col1 = c.take<int32_t>(L);
+  w->val1 = c.take<float>(L);
+  w->absv = c.take<float>(L);
+  w->absv_s = c.take<float>(L);
+  w->min_bits = c.take<unsigned int>(1);
+  w->cnt = c.take<unsigned long long>(1);
+  w->rp3 = c.take<int64_t>(n + 1);
+  w->col3 = c.take<int32_t>(C);
+  w->val3 = c.take<float>(C);
+  w->pk = c.take<uint64_t>(C);
+  w->pk_s = c.take<uint64_t>(C);
+  w->sc = c.take<float>(C);
+  w->ak = c.take<float>(C);
+  w->ak_s = c.take<float>(C);
+  w->idx = c.take<int64_t>(C);
+  w->idx1 = c.take<int64_t>(C);
+  w->idx2 = c.take<int64_t>(C);
+  w->uk = c.take<uint64_t>(2 * E);    // union keys, then directed keys
+  w->uk_s = c.take<uint64_t>(2 * E);
+  w->uv = c.take<float>(2 * E);
+  w->uv_s = c.take<float>(2 * E);
+  w->nsel = c.take<int64_t>(1);
+  w->cub = c.take<char>(op.cub_tmp);
+  return c.used();
+}
+
+__global__ void iota_i64(int64_t* p, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = i;
+}
+__global__ void gather_abs(const float* __restrict__ sc, const int64_t* __restrict__ idx,
+                           int64_t count, float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = fabsf(sc[idx[i]]);
+}
+// top N (by idx2 order) -> union arrays [0, N): pair key, signed value'
+__global__ void take_top(const int64_t* __restrict__ idx2, int64_t N,
+                         const uint64_t* __restrict__ pk, const float* __restrict__ sc,
+                         uint64_t* __restrict__ uk, float* __restrict__ uv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uk[i] = pk[idx2[i]];
+    uv[i] = sc[idx2[i]];
+  }
+}
+// min-edge values from the pass-1 lists (signed ψ'), keyed like min_edge_pairs
+__global__ void min_edge_vals(const int32_t* __restrict__ col, const float* __restrict__ val,
+                              const uint64_t* __restrict__ keys, int64_t n, int t1, int m,
+                              float* __restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * m;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / m;
+    const uint64_t key = keys[q];
+    float v = 0.f;
+    if (key != ~0ull) {
+      const uint64_t lo = key / (uint64_t)n, hi = key % (uint64_t)n;
+      const int64_t j = (int64_t)(lo == (uint64_t)i ? hi : lo);
+      for (int e = 0; e < t1; ++e)
+        if (col[i * t1 + e] == j) v = val[i * t1 + e];
+    }
+    out[q] = v;
+  }
+}
+
+}  // namespace
+
+extern "C" ggm_status ggm_sparse_precision_overall_workspace(int64_t n, int k,
+                                                            const ggm_overall_opts* opts,
+                                                            int64_t cand_capacity, size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  OverallPlan op;
+  ggm_status st = overall_plan(n, k, opts, cand_capacity, &op);
+  if (st != GGM_OK) return st;
+  OverallWork w;
+  *bytes = overall_carve(op, nullptr, &w);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_sparse_precision_overall(
+    int64_t n, int k, const float* V, const double* lambda, const ggm_overall_opts* opts,
+    int64_t cand_capacity, int64_t* row_ptr, int32_t* col, float* val, int64_t capacity,
+    int64_t* nnz_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!V || !lambda || !row_ptr || !nnz_out || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
+  OverallPlan op;
+  ggm_status st = overall_plan(n, k, opts, cand_capacity, &op);
+  if (st != GGM_OK) return st;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  OverallWork w;
+  const size_t need = overall_carve(op, workspace, &w);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  if (!ggm_device_supported())
+    return fail(GGM_ERR_CUDA, "current device is not compute capability 10.0 (sm_100a)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int sms = num_sms();
+  const int g = sms * 8;
+  auto blocks = [&](int64_t cnt) { return (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 255) / 256, g)); };
+  int launches = 0;
+  // (1) row masses of Ψ (plain tiles, mode 2), then V' = V ⊙ w^-1/2
+  if (op.downweight) {
+    Plan pl;
+    ggm_sparsify_opts so{};
+    so.mode = 2;
+    so.topk = 1;
+    st = make_plan(n, k, 0, n, &so, 0, &pl);
+    if (st != GGM_OK) return st;
+    Work sw;
+    carve(pl, w.sub, &sw);
+    GGM_CUDA_TRY(cudaMemsetAsync(sw.sc, 0, sizeof(DevScalars), s));
+    GGM_CUDA_TRY(cudaMemsetAsync(w.w, 0, sizeof(double) * n, s));
+    absmax_check<<<blocks(n * (int64_t)k), 256, 0, s>>>(V, lambda, n, k, sw.sc);
+    scale_finalize<<<1, 1, 0, s>>>(sw.sc);
+    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
+    split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
+    FusedParams fp = base_params(pl, sw, n, 0);
+    fp.mass_out = w.w;
+    st = launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+    if (st != GGM_OK) return st;
+    launches += 4;
+  }
+  scale_rows<<<blocks(n * (int64_t)k), 256, 0, s>>>(V, op.downweight ? w.w : nullptr, n, k, w.Vs, w.sq);
+  GGM_CUDA_TRY(cudaGetLastError());
+  ++launches;
+  // (2) per-row top-t1 of Ψ'
+  {
+    ggm_sparsify_opts so{};
+    so.mode = 0;
+    so.topk = op.t1;
+    int64_t nnz = 0;
+    st = ggm_sparse_precision(n, k, w.Vs, lambda, 0, n, &so, w.rp1, w.col1, w.val1, n * op.t1,
+                              &nnz, w.sub, op.ws_sub, stream);
+    if (st != GGM_OK) return st;
+    launches += ggm_last_launches();
+  }
+  // lower bound L of the N-th largest score
+  GGM_CUDA_TRY(cudaMemsetAsync(w.min_bits, 0x7f, sizeof(unsigned int), s));
+  list_stats<<<blocks(n), 256, 0, s>>>(w.val1, n, op.t1, w.absv, w.min_bits);
+  {
+    size_t tb = op.cub_tmp;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortKeysDescending(w.cub, tb, w.absv, w.absv_s, n * op.t1, 0, 32, s));
+  }
+  launches += 1;
+  float L1 = 0.f, L2 = 0.f;
+  unsigned int mb = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&mb, w.min_bits, sizeof(mb), cudaMemcpyDeviceToHost, s));
+  const int64_t q2 = std::min<int64_t>(2 * op.N, n * op.t1) - 1;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&L2, w.absv_s + q2, sizeof(float), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  std::memcpy(&L1, &mb, sizeof(float));
+  if (n * (int64_t)op.t1 < 2 * op.N) L1 = 0.f;
+  if (q2 + 1 < 2 * op.N) L2 = 0.f;  // fewer than 2N listed entries: no bound from the list
+  const float Lb = std::max(L1, L2);
+  // (3) every directed entry of Ψ' with score >= L: threshold mode at the float below L
+  int64_t ncoo = 0;
+  {
+    ggm_sparsify_opts so{};
+    so.mode = 1;
+    so.topk = 1;
+    // margin: pass-1 values may differ from pass-3 values by accumulation order (ulps)
+    so.tau = Lb > 0.f ? Lb * (1.f - 1e-5f) : 0.f;
+    st = ggm_sparse_precision(n, k, w.Vs, lambda, 0, n, &so, w.rp3, w.col3, w.val3, op.cand_cap,
+                              &ncoo, w.sub, op.ws_sub, stream);
+    if (st == GGM_ERR_CAPACITY) {
+      *nnz_out = -ncoo;  // negative: candidate capacity required (two-call protocol)
+      return fail(GGM_ERR_CAPACITY, "overall: %lld candidates > cand_capacity %lld",
+                  (long long)ncoo, (long long)op.cand_cap);
+    }
+    if (st != GGM_OK) return st;
+    launches += ggm_last_launches();
+  }
+  // (4) upper-triangle candidates ranked by (score desc, i, j); top N; + min-edges; unique
+  GGM_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned long long), s));
+  upper_pairs<<<blocks(n), 256, 0, s>>>(w.rp3, w.col3, w.val3, n, w.cnt, w.pk, w.sc);
+  unsigned long long hc = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hc, w.cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t nc = (int64_t)hc;
+  const int64_t Ntop = std::min<int64_t>(op.N, nc);
+  iota_i64<<<blocks(nc), 256, 0, s>>>(w.idx, nc);
+  {
+    size_t tb = op.cub_tmp;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub, tb, w.pk, w.pk_s, w.idx, w.idx1, nc, 0, 64, s));
+  }
+  gather_abs<<<blocks(nc), 256, 0, s>>>(w.sc, w.idx1, nc, w.ak);
+  {
+    // stable descending sort by |score| keeps (i, j) order among ties
+    size_t tb = op.cub_tmp;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.cub, tb, w.ak, w.ak_s, w.idx1, w.idx2,
+                                                           nc, 0, 32, s));
+  }
+  take_top<<<blocks(Ntop), 256, 0, s>>>(w.idx2, Ntop, w.pk, w.sc, w.uk, w.uv);
+  int64_t nu = Ntop;
+  if (op.m > 0) {
+    min_edge_pairs<<<blocks(n), 256, 0, s>>>(w.col1, w.val1, n, op.t1, op.m, w.uk + Ntop);
+    min_edge_vals<<<blocks(n * op.m), 256, 0, s>>>(w.col1, w.val1, w.uk + Ntop, n, op.t1, op.m, w.uv + Ntop);
+    nu += n * op.m;
+  }
+  launches += 5 + (op.m > 0 ? 2 : 0);
+  {
+    size_t tb = op.cub_tmp;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub, tb, w.uk, w.uk_s, w.uv, w.uv_s, nu, 0, 64, s));
+    tb = op.cub_tmp;
+    GGM_CUDA_TRY(cub::DeviceSelect::UniqueByKey(w.cub, tb, w.uk_s, w.uv_s, w.uk, w.uv, w.nsel, nu, s));
+  }
+  int64_t ne = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&ne, w.nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  uint64_t last = 0;
+  if (ne > 0) {  // drop the ~0 sentinel (min-edge slots of rows with fewer entries)
+    GGM_CUDA_TRY(cudaMemcpyAsync(&last, w.uk + ne - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (last == ~0ull) --ne;
+  }
+  // (5) both directions, ψ = ψ'·sqrt(w_i w_j), sorted by (row, col) -> CSR
+  *nnz_out = 2 * ne;
+  if (2 * ne > capacity)
+    return fail(GGM_ERR_CAPACITY, "overall: %lld entries > capacity %lld", (long long)(2 * ne),
+                (long long)capacity);
+  if (ne > 0 && (!col || !val)) return fail(GGM_ERR_INVALID_ARGUMENT, "col/val NULL");
+  expand_edges<<<blocks(ne), 256, 0, s>>>(w.uk, ne, n, w.uv, w.sq, w.uk_s, w.uv_s);
+  {
+    size_t tb = op.cub_tmp;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub, tb, w.uk_s, w.uk, w.uv_s, w.uv, 2 * ne, 0, 64, s));
+  }
+  dir_to_csr<<<blocks(2 * ne + 1), 256, 0, s>>>(w.uk, w.uv, 2 * ne, n, row_ptr, col, val);
+  GGM_CUDA_TRY(cudaGetLastError());
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  reset_launches();
+  count_launches(launches + 3);
   return GGM_OK;
 }

@@ -69,3 +69,52 @@ def check_threshold(row_ptr, col, val, V, lam, rows, tau):
         vv = np.asarray(val[row_ptr[r]:row_ptr[r + 1]], dtype=np.float64)
         assert np.all(np.diff(cc) > 0)
         assert np.all(np.abs(vv - P[r, cc]) <= tol(P[r, cc]))
+
+
+def check_overall(row_ptr, col, val, V, lam, n_edges, downweight=False, min_edges=0):
+    """Whole-graph rules: the GPU edge set equals oracle.overall_edges except
+    near ties (score within tolerance of the global N-th score or of a vertex's m-th score);
+    the CSR is symmetric with ascending columns and values within tolerance of psi_ij."""
+    V = np.asarray(V, np.float64)
+    n = V.shape[0]
+    P = (V * np.asarray(lam, np.float64)) @ V.T
+    A = np.abs(P)
+    np.fill_diagonal(A, 0.0)
+    if downweight:
+        w = A.sum(axis=1)
+        inv = np.where(w > 0, 1.0 / np.sqrt(np.where(w > 0, w, 1.0)), 0.0)
+        S = A * inv[:, None] * inv[None, :]
+    else:
+        S = A
+    row_ptr, col, val = (np.asarray(x) for x in (row_ptr, col, val))
+    assert row_ptr[0] == 0 and np.all(np.diff(row_ptr) >= 0) and row_ptr[-1] == len(col)
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    for r in range(n):
+        c = col[row_ptr[r]:row_ptr[r + 1]]
+        assert np.all(np.diff(c) > 0), f"row {r}: columns not strictly ascending"
+    assert np.all((col >= 0) & (col < n) & (col != rows))
+    d = {(int(a), int(b)): float(v) for a, b, v in zip(rows, col, val)}
+    for (a, b), v in d.items():
+        assert (b, a) in d and d[(b, a)] == v, f"asymmetric entry ({a},{b})"
+    want = P[rows, col]
+    assert np.all(np.abs(val - want) <= tol(want)), "value mismatch"
+    G = {(a, b) for (a, b) in d if a < b}
+    oi, oj, _ = O.overall_edges(V, lam, n_edges, downweight=downweight, min_edges=min_edges)
+    Oset = set(zip(oi.tolist(), oj.tolist()))
+    iu, ju = np.triu_indices(n, 1)
+    sc = np.sort(S[iu, ju])[::-1]
+    sN = sc[min(n_edges, len(sc)) - 1]
+    m = min(min_edges, n - 1)
+    rowthr = np.full(n, np.inf)
+    if m > 0:
+        Sr = S.copy()
+        np.fill_diagonal(Sr, -np.inf)
+        rowthr = -np.sort(-Sr, axis=1)[:, m - 1]
+    diff = G ^ Oset
+    for (a, b) in diff:
+        s = S[a, b]
+        near = [abs(s - sN) <= tol(sN)]
+        if m > 0:
+            near += [abs(s - rowthr[a]) <= tol(rowthr[a]), abs(s - rowthr[b]) <= tol(rowthr[b])]
+        assert any(near), f"edge ({a},{b}) score {s:.6e} differs with a clear gap (sN {sN:.6e})"
+    return dict(edges=len(G), oracle_edges=len(Oset), excused=len(diff))

@@ -351,3 +351,15 @@ def test_overall_min_edges_and_symmetric_csr():
         cc = c[rp[r]:rp[r + 1]]
         assert np.all(np.diff(cc) > 0) and r not in cc
         np.testing.assert_allclose(v[rp[r]:rp[r + 1]], P[r, cc])
+
+
+def test_overall_zero_psi_is_no_edge():
+    """Q17: exactly-zero psi_ij (block-diagonal Psi) never becomes an edge, even when fewer
+    than N nonzero pairs exist; min-edges skip zero entries too."""
+    V = np.zeros((6, 2))
+    V[:3, 0] = [1.0, 2.0, 3.0]     # block {0,1,2}
+    V[3:, 1] = [1.0, -1.0, 0.0]    # block {3,4,5}; vertex 5 isolated
+    ii, jj, vv = O.overall_edges(V, [1.0, 1.0], 15, min_edges=3)
+    got = set(zip(ii.tolist(), jj.tolist()))
+    assert got == {(0, 1), (0, 2), (1, 2), (3, 4)}
+    assert np.allclose(vv, [2.0, 3.0, 6.0, -1.0])
