@@ -225,6 +225,26 @@ def stage_timings(G, torch):
     return out
 
 
+def overall_timing(G, torch, V, lam):
+    """§8(f) NEXT 2 on the largest axis: whole-graph rules as the paper recommends for
+    scRNA-seq: N = 10 n edges overall, degree down-weighting, 1 min edge."""
+    n = V.shape[0]
+    kw = dict(downweight=True, min_edges=1)
+    _, _, _, (ccap, cap) = G.ggm_sparse_precision_overall(V, lam, 10 * n, return_caps=True, **kw)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rp, c, v = G.ggm_sparse_precision_overall(V, lam, 10 * n, cand_capacity=ccap, capacity=cap, **kw)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    path, sat = G.overall_last_path()
+    return {"path": {0: "lists", 1: "histogram+threshold", 2: "lists+saturated block"}.get(path, path),
+            "saturated_rows": sat, "phases_ms": G.overall_last_timing(), "n": int(n), "n_edges": 10 * int(n), "downweight": True, "min_edges": 1,
+            "edges_kept": int(c.numel()) // 2, "ms": ms, "entries_per_s": float(n) * n / (ms * 1e-3),
+            "launches": G.last_launches()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -439,6 +459,8 @@ def main():
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(host_axes, t, args.cpu_rows)
         stages = None if args.no_stages else stage_timings(G, torch)
+        if stages is not None:
+            stages["overall_rules_axisA"] = overall_timing(G, torch, *dev_axes[a0])
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

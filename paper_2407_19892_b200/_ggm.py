@@ -35,6 +35,7 @@ EXPORTED = [
     "ggm_sparse_precision_sym_shard", "ggm_sym_merge_workspace", "ggm_sym_merge",
     "ggm_wald_edge", "ggm_wald_threshold",
     "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
+    "ggm_overall_last_path",
 ]
 
 
@@ -123,6 +124,8 @@ def lib() -> C.CDLL:
                                                          C.POINTER(C.c_size_t)]
     L.ggm_sparse_precision_overall.argtypes = [i64, i32, vp, vp, C.POINTER(OverallOpts), i64, vp,
                                                vp, vp, i64, C.POINTER(i64), vp, C.c_size_t, vp]
+    L.ggm_overall_last_path.argtypes = [C.POINTER(i64), C.POINTER(C.c_float)]
+    L.ggm_overall_last_path.restype = i32
     for name in ("ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
                  "ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
                  "ggm_gram_eig_rsi_workspace", "ggm_gram_eig_rsi",
@@ -309,10 +312,11 @@ def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
 def ggm_sparse_precision_overall(V: torch.Tensor, lam: torch.Tensor, n_edges: int,
                                  downweight: bool = False, min_edges: int = 0,
                                  cand_capacity: int | None = None, capacity: int | None = None,
-                                 stream=None):
+                                 stream=None, return_caps: bool = False):
     """Whole-graph edge rules (include/ggm.h (3c)): the n_edges best undirected
     edges by |psi| (or |psi|/sqrt(w_i w_j), downweight) plus each vertex's min_edges best.
-    Returns the symmetric CSR (row_ptr, col, val).  Retries on either capacity error."""
+    Returns the symmetric CSR (row_ptr, col, val) (+ the (cand_capacity, capacity) that
+    succeeded when return_caps).  Retries on either capacity error."""
     _require_cuda(V, torch.float32, "V")
     _require_cuda(lam, torch.float64, "lam")
     n, k = V.shape
@@ -341,8 +345,27 @@ def ggm_sparse_precision_overall(V: torch.Tensor, lam: torch.Tensor, n_edges: in
             capacity = int(nnz.value)
             continue
         _check(st)
-        return row_ptr, col[:nnz.value], val[:nnz.value]
+        out = (row_ptr, col[:nnz.value], val[:nnz.value])
+        return out + ((int(cand_capacity), int(capacity)),) if return_caps else out
     raise GGMError(5, "capacity retries exhausted")
+
+
+def overall_last_path():
+    """(path, saturated rows) of the last ggm_sparse_precision_overall call on this thread:
+    0 lists only, 2 lists + saturated block, 1 histogram + threshold pass."""
+    sat = C.c_int64(0)
+    ms = (C.c_float * 5)()
+    p = lib().ggm_overall_last_path(C.byref(sat), ms)
+    return int(p), int(sat.value)
+
+
+def overall_last_timing():
+    """Phase times (ms) of the last overall call when set_timing(True): row masses,
+    top-t1 lists, bound + saturation, candidate pass, ranking + CSR."""
+    sat = C.c_int64(0)
+    ms = (C.c_float * 5)()
+    lib().ggm_overall_last_path(C.byref(sat), ms)
+    return dict(zip(("mass", "lists", "bound", "candidates", "rank_csr"), [float(x) for x in ms]))
 
 
 def wald_edge(psi: float, d_rest: int, sigma2: float, n_tests: int):

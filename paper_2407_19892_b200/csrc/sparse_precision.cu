@@ -235,7 +235,10 @@ __global__ void split_tile(const float* __restrict__ V, const double* __restrict
 
 // ------------------------------------------------------------------ BK2
 // ------------------------------------------------------------------ BK2
-enum Kind : int { kPlain = 0, kSeed = 1, kSym = 2 };
+// kSymList: the kSym block-pair enumeration (each unordered 128-row block pair once) with the
+// list-form epilogue; used for the row masses of the overall rules (mode 2: row sums into
+// the rows, column sums into the columns of every off-diagonal tile)
+enum Kind : int { kPlain = 0, kSeed = 1, kSym = 2, kSymList = 3 };
 
 struct FusedParams {
   const uint8_t* A;  // row-block operand (rows [row_begin,row_end)), tiled layout
@@ -263,6 +266,9 @@ struct FusedParams {
   int64_t capacity;
   float* thr_out;          // kSeed: per-row t-th largest sampled |ψ| (accumulator units)
   double* mass_out;        // mode 2 (plain): row masses Σ_{j≠i} |ψ_ij| (atomic partials)
+  unsigned long long* hist_out;  // mode 3 (plain): counts of upper entries (j > i) with
+                                 // |ψ| > τ in 256 log buckets b = min(255, (bits|ψ| - bits τ) >> hshift)
+  int hshift;
   const float* thr;        // kSym: per-(permuted) column lower bound of that row's t-th
                            //       magnitude (accumulator units, +inf = padding)
   const float* thr_min;    // kSym: min of thr over each 32-column chunk
@@ -338,7 +344,7 @@ struct TileIter {
     ub = ub_;
     s = 0;
     h1 = true;
-    if (KIND == kSym) {
+    if (KIND >= kSym) {
       W = sym_window(ub, p.NB);
       o = sym_start(p, u, ub, u0, ustep, W);
       place(p);
@@ -367,7 +373,7 @@ struct TileIter {
   }
   __device__ __forceinline__ void next(const FusedParams& p) {
     ++s;
-    if (KIND == kSym) {
+    if (KIND >= kSym) {
       o += PAIR ? 1 : 2;
       if (o >= W) o -= W;
       place(p);
@@ -489,6 +495,25 @@ __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
   return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
 }
 
+// Column sums of |v| over the warp's 32 rows for its 32 columns (reduce-scatter transpose:
+// 31 shuffles); lane L returns the sum of column L.  Masked entries (bit e of ex) count 0.
+__device__ __forceinline__ float col_abs_sums32(const uint32_t (&vr)[32], uint32_t ex, int lane) {
+  float a[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) a[e] = ((ex >> e) & 1u) ? 0.f : fabsf(__uint_as_float(vr[e]));
+#pragma unroll
+  for (int st = 16; st >= 1; st >>= 1) {
+    const bool up = (lane & st) != 0;
+#pragma unroll
+    for (int e = 0; e < st; ++e) {
+      const float keep = up ? a[e + st] : a[e];
+      const float send = up ? a[e] : a[e + st];
+      a[e] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+    }
+  }
+  return a[0];
+}
+
 // An epilogue warp is done with a TMEM accumulator buffer: arrive on the (pair leader's)
 // tempty barrier.
 // The data was already waited into registers (tcgen05.wait::ld), so the arrive needs no
@@ -514,7 +539,8 @@ template <int MAXT, int KIND>
 __device__ __forceinline__ void epi_chunk(const FusedParams& p, const uint32_t (&vr)[32],
                                           uint32_t tchunk, int64_t col0, int64_t gi, int64_t lr,
                                           bool valid, bool need_mask, float tau_s, float sd2,
-                                          TopList<MAXT>& top, double& macc, int lane) {
+                                          TopList<MAXT>& top, double& macc, int lane,
+                                          float* hist_smem, float* colacc = nullptr) {
   // the loaded registers are only read (never rewritten), so the compiler keeps them in the
   // tcgen05.ld destination block without copies
   float m = max32_abs(reinterpret_cast<const float(&)[32]>(vr));
@@ -534,6 +560,26 @@ __device__ __forceinline__ void epi_chunk(const FusedParams& p, const uint32_t (
 #pragma unroll
     for (int e = 0; e < 32; ++e) sum += ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(vr[e]));
     macc += (double)sum;
+    if (KIND == kSymList && colacc != nullptr) {  // off-diagonal tile: also the columns' mass
+      const float cs = col_abs_sums32(vr, valid ? excl : 0xffffffffu, lane);
+      atomicAdd(colacc + lane, cs);
+    }
+    return;
+  }
+  if (p.mode == 3) {  // log-bucket histogram of upper-triangle |ψ| > τ (overall rules)
+    if (__any_sync(0xffffffffu, m > tau_s) && valid) {
+      const int64_t dd = gi - col0;  // columns e <= dd are j <= i
+      const uint32_t low = dd < 0 ? 0u : (dd >= 31 ? 0xffffffffu : ((2u << dd) - 1u));
+      const uint32_t ex = excl | low;
+      unsigned int* hist = reinterpret_cast<unsigned int*>(hist_smem);
+      const uint32_t tb = __float_as_uint(tau_s);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float x = fabsf(__uint_as_float(vr[e]));
+        if (!((ex >> e) & 1u) && x > tau_s)
+          atomicAdd(hist + min(255u, (__float_as_uint(x) - tb) >> p.hshift), 1u);
+      }
+    }
     return;
   }
   const float thr = p.mode == 0 ? top.thr() : tau_s;
@@ -602,6 +648,17 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   TopList<MAXT> top;
+  if (p.mode == 3) {  // CTA histogram in the (otherwise unused) merge scratch
+    for (int b = ew * 32 + lane; b < 256; b += 256) reinterpret_cast<unsigned int*>(scratch_all)[b] = 0u;
+    asm volatile("bar.sync 5, 256;" ::: "memory");
+  }
+  // kSymList mass: column-sum accumulators [tile parity][half][128] in the merge scratch
+  constexpr bool kColMass = KIND == kSymList;
+  if (kColMass) {
+    for (int b = ew * 32 + lane; b < 512; b += 256) scratch_all[b] = 0.f;
+    asm volatile("bar.sync 5, 256;" ::: "memory");
+  }
+  int tpar = 0;
   for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
@@ -626,6 +683,10 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
       tc_fence_after();
       const uint32_t taddr =
           tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTileN + h * (kTileN / 2));
+      // kSymList: column sums only off the diagonal (super) block, whose tile holds both
+      // (i, j) and (j, i)
+      const bool diag_blk = PAIR ? (Kh >> 1) == ub : Kh == ub;
+      float* cacc = (kColMass && p.mode == 2 && !diag_blk) ? scratch_all + (tpar * 2 + h) * 128 : nullptr;
       if (live) {
         uint32_t va[32], vb[32];
         tmem_ld32_nowait(taddr, va);
@@ -635,14 +696,16 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
           tmem_ld32_nowait(taddr + (c + 1) * 32, vb);
           if (p.dbg != 1)
             epi_chunk<MAXT, KIND>(p, va, taddr + c * 32, cb + c * 32, gi, lr, valid, need_mask,
-                                  tau_s, sd2, top, macc, lane);
+                                  tau_s, sd2, top, macc, lane, scratch_all,
+                                  cacc ? cacc + c * 32 : nullptr);
           else if (va[0] == 12345u && va[31] == 54321u)
             p.row_ptr[0] = (int64_t)va[7];
           tmem_wait_ld(vb);
           if (c + 2 < (kTileN / 2) / 32) tmem_ld32_nowait(taddr + (c + 2) * 32, va);
           if (p.dbg != 1)
             epi_chunk<MAXT, KIND>(p, vb, taddr + (c + 1) * 32, cb + (c + 1) * 32, gi, lr, valid,
-                                  need_mask, tau_s, sd2, top, macc, lane);
+                                  need_mask, tau_s, sd2, top, macc, lane, scratch_all,
+                                  cacc ? cacc + (c + 1) * 32 : nullptr);
           else if (vb[0] == 12345u && vb[31] == 54321u)
             p.row_ptr[0] = (int64_t)vb[7];
         }
@@ -654,12 +717,28 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
         buf = 0;
         tphase ^= 1;
       }
+      if (kColMass && p.mode == 2) {
+        // the 4 quadrant warps of this half have added their column sums: one warp flushes
+        // (and clears) them; the other parity buffer takes the next tile meanwhile
+        asm volatile("bar.sync %0, 128;" ::"r"(6 + h) : "memory");
+        if (q == 0 && live && !diag_blk) {
+          float* acc = scratch_all + (tpar * 2 + h) * 128;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int64_t j = cb + c * 32 + lane;
+            const float v = acc[c * 32 + lane];
+            acc[c * 32 + lane] = 0.f;
+            if (j < p.n && v != 0.f) atomicAdd(p.mass_out + j, (double)v * (double)sd2);
+          }
+        }
+        tpar ^= 1;
+      }
     }
     if (p.mode == 2) {  // both column halves add their partial row mass (unscaled ψ units)
       if (valid) atomicAdd(p.mass_out + lr, macc * (double)sd2);
       continue;
     }
-    if (p.mode != 0) continue;
+    if (p.mode != 0) continue;  // modes 1, 3: nothing per row
     // merge the two column halves of each row: half 1 publishes (values into its own
     // scratch, columns into the half-0 warp's), half 0 merges and emits.
     float* pv = scratch_all + (4 + ((q - kFirstEpiWarp) & 3)) * kScratchFloats;
@@ -702,6 +781,12 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
       }
     }
     asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+  }
+  if (p.mode == 3) {
+    asm volatile("bar.sync 5, 256;" ::: "memory");
+    const unsigned int* hist = reinterpret_cast<const unsigned int*>(scratch_all);
+    for (int b = ew * 32 + lane; b < 256; b += 256)
+      if (hist[b]) atomicAdd(p.hist_out + b, (unsigned long long)hist[b]);
   }
 }
 
@@ -1436,6 +1521,16 @@ static int choose_chunks(int64_t RB, int64_t NT, int sms) {
   return best;
 }
 
+// seed sample fraction for the next plans on this thread (0: kSeedFrac).  The overall rules'
+// top-32 lists pass on down-weighted scores sets 8: the flattened score distribution leaves
+// ~t x (n / sample) candidates per row, which a 1/64 sample would overflow.
+static thread_local int g_seed_frac_override = 0;
+struct SeedFracScope {
+  int saved;
+  explicit SeedFracScope(int f) : saved(g_seed_frac_override) { g_seed_frac_override = f; }
+  ~SeedFracScope() { g_seed_frac_override = saved; }
+};
+
 static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end,
                             const ggm_sparsify_opts* o, int64_t capacity, Plan* pl) {
   if (!o) return fail(GGM_ERR_INVALID_ARGUMENT, "opts is NULL");
@@ -1445,7 +1540,7 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   if (row_begin < 0 || row_end > n || row_begin >= row_end)
     return fail(GGM_ERR_INVALID_ARGUMENT, "row range [%lld,%lld) invalid for n=%lld",
                 (long long)row_begin, (long long)row_end, (long long)n);
-  if (o->mode != 0 && o->mode != 1 && o->mode != 2)
+  if (o->mode < 0 || o->mode > 3)  // 2 (row mass), 3 (histogram): internal (overall rules)
     return fail(GGM_ERR_INVALID_ARGUMENT, "mode=%d", o->mode);
   if (o->mode == 0 && (o->topk < 1))
     return fail(GGM_ERR_INVALID_ARGUMENT, "topk=%d < 1", o->topk);
@@ -1504,7 +1599,7 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // entries: on C5 factors the t-th largest over this 1/64 sample leaves ~21 candidates per
   // row where a strided 1/8 sample left ~89 (any sample gives a valid bound).
   {
-    int64_t frac = kSeedFrac;
+    int64_t frac = g_seed_frac_override > 0 ? g_seed_frac_override : kSeedFrac;
     if (const char* e = getenv("GGM_SEED_FRAC")) frac = std::max(1, atoi(e));  // tuning only
     // at least 8 tiles (2048 columns): small axes get a proportionally larger sample
     const int64_t tiles = std::max<int64_t>(8, (n / frac + kTileN - 1) / kTileN);
@@ -1680,9 +1775,10 @@ template <int MAXT, bool PAIR>
 static cudaError_t launch_fused_t(const TMaps& tm, const FusedParams& fp, size_t smem, int grid,
                                   cudaStream_t st) {
   // the candidate epilogue (kSym) keeps no per-row list: one instantiation
-  return fp.kind == kPlain  ? launch_fused_k<MAXT, kPlain, PAIR>(tm, fp, smem, grid, st)
-         : fp.kind == kSeed ? launch_fused_k<MAXT, kSeed, PAIR>(tm, fp, smem, grid, st)
-                            : launch_fused_k<5, kSym, PAIR>(tm, fp, smem, grid, st);
+  return fp.kind == kPlain      ? launch_fused_k<MAXT, kPlain, PAIR>(tm, fp, smem, grid, st)
+         : fp.kind == kSeed     ? launch_fused_k<MAXT, kSeed, PAIR>(tm, fp, smem, grid, st)
+         : fp.kind == kSymList  ? launch_fused_k<5, kSymList, PAIR>(tm, fp, smem, grid, st)
+                                : launch_fused_k<5, kSym, PAIR>(tm, fp, smem, grid, st);
 }
 template <bool PAIR>
 static cudaError_t launch_fused_p(const TMaps& tm, const FusedParams& fp, int t, size_t smem,
@@ -1750,6 +1846,8 @@ extern "C" ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t r
                                                      const ggm_sparsify_opts* opts,
                                                      int64_t capacity, size_t* bytes) {
   if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  if (opts && opts->mode != 0 && opts->mode != 1)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "mode=%d not in {0,1}", opts->mode);
   Plan pl;
   ggm_status st = make_plan(n, k, row_begin, row_end, opts, capacity, &pl);
   if (st != GGM_OK) return st;
@@ -1874,6 +1972,8 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
                                            size_t workspace_bytes, void* stream) {
   if (!V || !lambda || !row_ptr || !nnz_out || !workspace)
     return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (opts && opts->mode != 0 && opts->mode != 1)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "mode=%d not in {0,1}", opts->mode);
   Plan pl;
   ggm_status st = make_plan(n, k, row_begin, row_end, opts, capacity, &pl);
   if (st != GGM_OK) return st;
@@ -2324,16 +2424,41 @@ __global__ void scale_rows(const float* __restrict__ V, const double* __restrict
 // abs values of the pass-1 list entries; per-row t1-th largest |value| (lists hold exactly t1
 // entries per row) -> atomic min
 __global__ void list_stats(const float* __restrict__ val, int64_t n, int t1,
-                           float* __restrict__ absv, unsigned int* __restrict__ min_tth_bits) {
+                           float* __restrict__ rowmin, unsigned int* __restrict__ max_bits) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float mn = INFINITY;
+    float mn = INFINITY, mx = 0.f;
     for (int e = 0; e < t1; ++e) {
       const float a = fabsf(val[i * t1 + e]);
-      absv[i * t1 + e] = a;
       mn = fminf(mn, a);
+      mx = fmaxf(mx, a);
     }
-    atomicMin(min_tth_bits, __float_as_uint(mn));  // non-negative floats order as uints
+    rowmin[i] = mn;
+    atomicMax(max_bits, __float_as_uint(mx));  // non-negative floats order as uints
+  }
+}
+
+// rows whose t1-th listed score is >= x (saturated)
+__global__ void count_ge(const float* __restrict__ rowmin, int64_t n, float x,
+                         unsigned int* __restrict__ cnt) {
+  unsigned int c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += rowmin[i] >= x ? 1u : 0u;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+// listed entries -> (pair key min*n+max, signed ψ') in slot i*t1 + e; zero entries -> ~0
+__global__ void list_pairs(const int32_t* __restrict__ col, const float* __restrict__ val,
+                           int64_t n, int t1, uint64_t* __restrict__ pkey,
+                           float* __restrict__ score) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * t1;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)(q / t1), j = (uint64_t)col[q];
+    const float v = val[q];
+    pkey[q] = fabsf(v) > 0.f ? (i < j ? i * (uint64_t)n + j : j * (uint64_t)n + i) : ~0ull;
+    score[q] = v;
   }
 }
 
@@ -2350,6 +2475,63 @@ __global__ void upper_pairs(const int64_t* __restrict__ rp, const int32_t* __res
       const unsigned long long at = atomicAdd(cnt, 1ull);
       pkey[at] = (uint64_t)i * (uint64_t)n + (uint64_t)j;
       score[at] = val[e];  // signed ψ'; ranked by |.|
+    }
+  }
+}
+
+__global__ void abs_copy(const float* __restrict__ x, int64_t cnt, float* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fabsf(x[i]);
+}
+__global__ void gather_rows(const float* __restrict__ V, const int32_t* __restrict__ ids,
+                            int64_t rows, int k, float* __restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < rows * k;
+       q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = V[(int64_t)ids[q / k] * k + q % k];
+}
+__global__ void mark_rows(const int32_t* __restrict__ ids, int64_t rows, uint8_t* __restrict__ in) {
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < rows;
+       a += (int64_t)gridDim.x * blockDim.x)
+    in[ids[a]] = 1;
+}
+// listed pairs with an endpoint outside S -> the overall histogram (same buckets as mode 3)
+__global__ void list_hist(const uint64_t* __restrict__ pk, const float* __restrict__ sc,
+                          int64_t cnt, int64_t n, const uint8_t* __restrict__ inS, float x0,
+                          int hs, unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0u;
+  __syncthreads();
+  const uint32_t bx0 = __float_as_uint(x0);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = pk[q];
+    const int64_t i = (int64_t)(key / (uint64_t)n), j = (int64_t)(key % (uint64_t)n);
+    const float a = fabsf(sc[q]);
+    if (a > x0 && !(inS[i] && inS[j]))
+      atomicAdd(&h[min(255u, (__float_as_uint(a) - bx0) >> hs)], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    if (h[b]) atomicAdd(hist + b, (unsigned long long)h[b]);
+}
+
+// block threshold output (local rows a < b of S) -> global pair keys appended at *cnt
+__global__ void block_pairs(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const float* __restrict__ val, int64_t rows,
+                            const int32_t* __restrict__ ids, int64_t n,
+                            unsigned long long* __restrict__ cnt, uint64_t* __restrict__ pkey,
+                            float* __restrict__ score) {
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < rows;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t gi = (uint64_t)ids[a];
+    for (int64_t e = rp[a]; e < rp[a + 1]; ++e) {
+      const int64_t b = col[e];
+      if (b <= a) continue;
+      const uint64_t gj = (uint64_t)ids[b];
+      const unsigned long long at = atomicAdd(cnt, 1ull);
+      pkey[at] = gi < gj ? gi * (uint64_t)n + gj : gj * (uint64_t)n + gi;
+      score[at] = val[e];
     }
   }
 }
@@ -2417,6 +2599,37 @@ using namespace ggm::sp;
 
 namespace {
 
+constexpr int kOverallSeedFrac = 8;  // seed sample of the top-t1 lists pass (see make_plan)
+thread_local int g_overall_path = -1;  // 0: lists only, 1: histogram + threshold, 2: block
+thread_local int64_t g_overall_sat = 0;  // saturated rows at L3
+thread_local float g_overall_ms[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+
+// phase marks of the overall driver (CUDA events on its stream, when ggm_set_timing(1))
+struct PhaseTimer {
+  cudaEvent_t ev[6] = {};
+  bool on;
+  cudaStream_t s;
+  int last = -1;
+  PhaseTimer(bool enabled, cudaStream_t st) : on(enabled), s(st) {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark(int i) {
+    if (on) {
+      cudaEventRecord(ev[i], s);
+      last = i;
+    }
+  }
+  ~PhaseTimer() {
+    if (!on) return;
+    if (last == 5) {
+      cudaEventSynchronize(ev[5]);
+      for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&g_overall_ms[i], ev[i], ev[i + 1]);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
 struct OverallPlan {
   int64_t n, N, cand_cap, E_max;
   int k, t1, m, downweight;
@@ -2450,12 +2663,20 @@ ggm_status overall_plan(int64_t n, int k, const ggm_overall_opts* o, int64_t can
   ggm_sparsify_opts so{};
   so.mode = 2;
   so.topk = 1;
-  ggm_status st = ggm_sparse_precision_workspace(n, k, 0, n, &so, 0, &b);
-  if (st != GGM_OK) return st;
-  mx = std::max(mx, b);
+  {  // internal passes (row mass, histogram): plain plan, no output capacity
+    Plan pl;
+    Work wk;
+    ggm_status st2 = make_plan(n, k, 0, n, &so, 0, &pl);
+    if (st2 != GGM_OK) return st2;
+    mx = std::max(mx, carve(pl, nullptr, &wk));
+  }
+  ggm_status st = GGM_OK;
   so.mode = 0;
   so.topk = op->t1;
-  st = ggm_sparse_precision_workspace(n, k, 0, n, &so, n * op->t1, &b);
+  {
+    SeedFracScope sf(kOverallSeedFrac);
+    st = ggm_sparse_precision_workspace(n, k, 0, n, &so, n * op->t1, &b);
+  }
   if (st != GGM_OK) return st;
   mx = std::max(mx, b);
   so.mode = 1;
@@ -2465,7 +2686,10 @@ ggm_status overall_plan(int64_t n, int k, const ggm_overall_opts* o, int64_t can
   if (st != GGM_OK) return st;
   op->ws_sub = std::max(mx, b);
   size_t c = 0, t = 0;
-  const int64_t L = std::max<int64_t>(op->n * op->t1, std::max<int64_t>(cand_capacity, 2 * op->E_max));
+  const int64_t L = op->n * op->t1 + cand_capacity + 2 * op->E_max;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, t, (const float*)nullptr, (float*)nullptr,
+                                            (const int32_t*)nullptr, (int32_t*)nullptr, L);
+  c = std::max(c, t);
   cub::DeviceRadixSort::SortKeysDescending(nullptr, t, (const float*)nullptr, (float*)nullptr, L);
   c = std::max(c, t);
   cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint64_t*)nullptr, (uint64_t*)nullptr,
@@ -2490,8 +2714,11 @@ struct OverallWork {
   void* sub;
   int64_t *rp1, *rp3;
   int32_t *col1, *col3;
-  float *val1, *val3, *absv, *absv_s;
-  unsigned int* min_bits;
+  float *val1, *val3, *rowmin, *Vsub;
+  int32_t *rid, *rid_s;
+  uint8_t* inS;
+  unsigned int* min_bits;  // [0] saturated-row count, [1] max listed score bits
+  unsigned long long* hist;
   unsigned long long* cnt;
   uint64_t *pk, *pk_s, *uk, *uk_s;
   float *sc, *ak, *ak_s, *uv, *uv_s;
@@ -2501,7 +2728,7 @@ struct OverallWork {
 
 size_t overall_carve(const OverallPlan& op, void* ws, OverallWork* w) {
   Carve c(ws);
-  const int64_t n = op.n, C = op.cand_cap, E = op.E_max, L = n * op.t1;
+  const int64_t n = op.n, E = op.E_max, L = n * op.t1, C = op.cand_cap + L;
   w->Vs = c.take<float>((size_t)n * op.k);
   w->w = c.take<double>(n);
   w->sq = c.take<double>(n);
@@ -2509,13 +2736,17 @@ size_t overall_carve(const OverallPlan& op, void* ws, OverallWork* w) {
   w->rp1 = c.take<int64_t>(n + 1);
   w->col1 = c.take<int32_t>(L);
   w->val1 = c.take<float>(L);
-  w->absv = c.take<float>(L);
-  w->absv_s = c.take<float>(L);
-  w->min_bits = c.take<unsigned int>(1);
+  w->rowmin = c.take<float>(n);
+  w->Vsub = c.take<float>((size_t)n * op.k);
+  w->rid = c.take<int32_t>(n);
+  w->rid_s = c.take<int32_t>(n);
+  w->inS = c.take<uint8_t>(n);
+  w->min_bits = c.take<unsigned int>(2);
+  w->hist = c.take<unsigned long long>(256);
   w->cnt = c.take<unsigned long long>(1);
   w->rp3 = c.take<int64_t>(n + 1);
-  w->col3 = c.take<int32_t>(C);
-  w->val3 = c.take<float>(C);
+  w->col3 = c.take<int32_t>(op.cand_cap);
+  w->val3 = c.take<float>(op.cand_cap);
   w->pk = c.take<uint64_t>(C);
   w->pk_s = c.take<uint64_t>(C);
   w->sc = c.take<float>(C);
@@ -2609,6 +2840,8 @@ extern "C" ggm_status ggm_sparse_precision_overall(
   const int g = sms * 8;
   auto blocks = [&](int64_t cnt) { return (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 255) / 256, g)); };
   int launches = 0;
+  PhaseTimer ph(timing_enabled(), s);
+  ph.mark(0);
   // (1) row masses of Ψ (plain tiles, mode 2), then V' = V ⊙ w^-1/2
   if (op.downweight) {
     Plan pl;
@@ -2628,6 +2861,11 @@ extern "C" ggm_status ggm_sparse_precision_overall(
         V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
     FusedParams fp = base_params(pl, sw, n, 0);
     fp.mass_out = w.w;
+    if (pl.resident && !std::getenv("GGM_OVERALL_PLAIN_MASS")) {
+      // each unordered block pair once: row sums + column sums (half the plain MMA work)
+      fp.kind = kSymList;
+      fp.RB = (int)pl.NBu;
+    }
     st = launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
     if (st != GGM_OK) return st;
     launches += 4;
@@ -2636,59 +2874,198 @@ extern "C" ggm_status ggm_sparse_precision_overall(
   GGM_CUDA_TRY(cudaGetLastError());
   ++launches;
   // (2) per-row top-t1 of Ψ'
+  ph.mark(1);
   {
     ggm_sparsify_opts so{};
     so.mode = 0;
     so.topk = op.t1;
     int64_t nnz = 0;
+    SeedFracScope sf(kOverallSeedFrac);
     st = ggm_sparse_precision(n, k, w.Vs, lambda, 0, n, &so, w.rp1, w.col1, w.val1, n * op.t1,
                               &nnz, w.sub, op.ws_sub, stream);
     if (st != GGM_OK) return st;
+    if (std::getenv("GGM_DEBUG_OVERALL"))
+      fprintf(stderr, "overall lists t1=%d: scheme %.0f entries %.3g cand %.3g recomputed %.0f\n",
+              op.t1, g_stats[0], g_stats[1], g_stats[2], g_stats[3]);
     launches += ggm_last_launches();
   }
-  // lower bound L of the N-th largest score
-  GGM_CUDA_TRY(cudaMemsetAsync(w.min_bits, 0x7f, sizeof(unsigned int), s));
-  list_stats<<<blocks(n), 256, 0, s>>>(w.val1, n, op.t1, w.absv, w.min_bits);
-  {
+  // (3) candidates.  The listed pairs (either direction, de-duplicated) give L3 = the N-th
+  // largest listed pair score, a lower bound of the N-th largest pair score (N real pairs
+  // reach it).  Row i is saturated when its t1-th listed score is >= L3 (it may hold
+  // unlisted entries >= L3).  A pair (i, j) with score >= L3 is missing from the lists only
+  // if both i and j are saturated, so: no saturated row -> the lists hold the top N pairs
+  // (path 0); a few -> add the saturated rows' block S x S by a threshold pass on their
+  // gathered factor rows (path 2); many -> histogram + full threshold pass (path 1).
+  auto dedupe = [&](int64_t cnt, int64_t* out) -> ggm_status {
     size_t tb = op.cub_tmp;
-    GGM_CUDA_TRY(cub::DeviceRadixSort::SortKeysDescending(w.cub, tb, w.absv, w.absv_s, n * op.t1, 0, 32, s));
-  }
-  launches += 1;
-  float L1 = 0.f, L2 = 0.f;
-  unsigned int mb = 0;
-  GGM_CUDA_TRY(cudaMemcpyAsync(&mb, w.min_bits, sizeof(mb), cudaMemcpyDeviceToHost, s));
-  const int64_t q2 = std::min<int64_t>(2 * op.N, n * op.t1) - 1;
-  GGM_CUDA_TRY(cudaMemcpyAsync(&L2, w.absv_s + q2, sizeof(float), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  std::memcpy(&L1, &mb, sizeof(float));
-  if (n * (int64_t)op.t1 < 2 * op.N) L1 = 0.f;
-  if (q2 + 1 < 2 * op.N) L2 = 0.f;  // fewer than 2N listed entries: no bound from the list
-  const float Lb = std::max(L1, L2);
-  // (3) every directed entry of Ψ' with score >= L: threshold mode at the float below L
-  int64_t ncoo = 0;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub, tb, w.pk, w.pk_s, w.sc, w.ak_s, cnt, 0, 64, s));
+    tb = op.cub_tmp;
+    GGM_CUDA_TRY(cub::DeviceSelect::UniqueByKey(w.cub, tb, w.pk_s, w.ak_s, w.pk, w.sc, w.nsel, cnt, s));
+    int64_t u = 0;
+    GGM_CUDA_TRY(cudaMemcpyAsync(&u, w.nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (u > 0) {  // drop the ~0 sentinel (zero entries)
+      uint64_t lastk = 0;
+      GGM_CUDA_TRY(cudaMemcpyAsync(&lastk, w.pk + u - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      GGM_CUDA_TRY(cudaStreamSynchronize(s));
+      if (lastk == ~0ull) --u;
+    }
+    *out = u;
+    return GGM_OK;
+  };
+  ph.mark(2);
+  GGM_CUDA_TRY(cudaMemsetAsync(w.min_bits, 0, 2 * sizeof(unsigned int), s));
+  list_stats<<<blocks(n), 256, 0, s>>>(w.val1, n, op.t1, w.rowmin, w.min_bits + 1);
+  // deterministic slots i*t1 + e: duplicates keep the entry of the smaller row (stable sort)
+  list_pairs<<<blocks(n * op.t1), 256, 0, s>>>(w.col1, w.val1, n, op.t1, w.pk, w.sc);
+  int64_t nu1 = 0;
+  st = dedupe(n * op.t1, &nu1);
+  if (st != GGM_OK) return st;
+  float L3 = 0.f, gmax = 0.f;
   {
-    ggm_sparsify_opts so{};
-    so.mode = 1;
-    so.topk = 1;
-    // margin: pass-1 values may differ from pass-3 values by accumulation order (ulps)
-    so.tau = Lb > 0.f ? Lb * (1.f - 1e-5f) : 0.f;
-    st = ggm_sparse_precision(n, k, w.Vs, lambda, 0, n, &so, w.rp3, w.col3, w.val3, op.cand_cap,
-                              &ncoo, w.sub, op.ws_sub, stream);
+    unsigned int mb = 0;
+    GGM_CUDA_TRY(cudaMemcpyAsync(&mb, w.min_bits + 1, sizeof(mb), cudaMemcpyDeviceToHost, s));
+    if (nu1 >= op.N) {
+      abs_copy<<<blocks(nu1), 256, 0, s>>>(w.sc, nu1, w.ak);
+      size_t tb = op.cub_tmp;
+      GGM_CUDA_TRY(cub::DeviceRadixSort::SortKeysDescending(w.cub, tb, w.ak, w.ak_s, nu1, 0, 32, s));
+      GGM_CUDA_TRY(cudaMemcpyAsync(&L3, w.ak_s + op.N - 1, sizeof(float), cudaMemcpyDeviceToHost, s));
+      launches += 1;
+    }
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    std::memcpy(&gmax, &mb, 4);
+  }
+  count_ge<<<blocks(n), 256, 0, s>>>(w.rowmin, n, L3, w.min_bits);
+  launches += 3;
+  unsigned int nsat = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&nsat, w.min_bits, sizeof(nsat), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  int64_t nc = nu1;
+  const char* force = std::getenv("GGM_OVERALL_PATH");  // test hook: "1" hist, "2" block
+  g_overall_path = L3 <= 0.f ? 1 : (nsat == 0 ? 0 : (2 * (int64_t)nsat <= n ? 2 : 1));
+  if (force && L3 > 0.f && (force[0] == '1' || force[0] == '2')) g_overall_path = force[0] - '0';
+  g_overall_sat = nsat;
+  ph.mark(3);
+  if (g_overall_path != 0) {
+    // Path 2: S = the s_eff rows with the largest t1-th listed score (all saturated rows,
+    // at least k rows so the block is a valid factor), gathered into V_S; path 1: S = all
+    // rows.  (a) histogram, in 256 log buckets above x0 ~ L3, of the pair scores: the
+    // block's upper triangle (plain tiles, mode 3) plus, on path 2, the listed pairs with
+    // an endpoint outside S (complete above L3: such a row is not saturated) -> the exact
+    // count of pairs above each bucket edge >= L3; (b) the bucket edge where that count
+    // reaches N (<= the N-th largest score) is the threshold of one pass over the block
+    // (threshold mode; the histogram used the same kernel arithmetic, so the candidate
+    // count is known before the pass).
+    const float* F = w.Vs;
+    int64_t rows = n;
+    if (g_overall_path == 2) {
+      rows = std::min<int64_t>(n, std::max<int64_t>({(int64_t)nsat, (int64_t)k, 2}));
+      iota_i32<<<blocks(n), 256, 0, s>>>(w.rid, n);
+      {
+        size_t tb = op.cub_tmp;
+        GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.cub, tb, w.rowmin, w.ak_s, w.rid, w.rid_s, n, 0, 32, s));
+      }
+      gather_rows<<<blocks(rows * k), 256, 0, s>>>(w.Vs, w.rid_s, rows, k, w.Vsub);
+      GGM_CUDA_TRY(cudaMemsetAsync(w.inS, 0, n, s));
+      mark_rows<<<blocks(rows), 256, 0, s>>>(w.rid_s, rows, w.inS);
+      F = w.Vsub;
+      launches += 3;
+    }
+    // x0 > 0 keeps bucket offsets invariant under the kernel's power-of-two operand scale
+    // (bits(x·2^s) - bits(x0·2^s) = bits(x) - bits(x0) for normal floats); with no bound
+    // from the lists, x0 = 2^-60 max|ψ'| (smaller entries are below the fp32 accuracy of
+    // the products and count as zero, Q17)
+    const float x0 = L3 > 0.f ? L3 * (1.f - 1e-5f) : std::ldexp(gmax, -60);
+    uint32_t bx0, bmax;
+    std::memcpy(&bx0, &x0, 4);
+    std::memcpy(&bmax, &gmax, 4);
+    const uint64_t range = (uint64_t)(bmax > bx0 ? bmax - bx0 : 0) + 64;  // ulp slack
+    int hs = 0;
+    while ((range >> hs) > 255) ++hs;
+    {
+      Plan pl;
+      ggm_sparsify_opts so{};
+      so.mode = 3;
+      so.topk = 1;
+      st = make_plan(rows, k, 0, rows, &so, 0, &pl);
+      if (st != GGM_OK) return st;
+      Work sw;
+      carve(pl, w.sub, &sw);
+      GGM_CUDA_TRY(cudaMemsetAsync(sw.sc, 0, sizeof(DevScalars), s));
+      GGM_CUDA_TRY(cudaMemsetAsync(w.hist, 0, 256 * sizeof(unsigned long long), s));
+      absmax_check<<<blocks(rows * (int64_t)k), 256, 0, s>>>(F, lambda, rows, k, sw.sc);
+      scale_finalize<<<1, 1, 0, s>>>(sw.sc);
+      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
+      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+          F, lambda, rows, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
+      FusedParams fp = base_params(pl, sw, rows, 0);
+      fp.tau = x0;
+      fp.hist_out = w.hist;
+      fp.hshift = hs;
+      st = launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+      if (st != GGM_OK) return st;
+      launches += 3;
+      if (g_overall_path == 2) {
+        list_hist<<<std::max(1, std::min(sms * 4, (int)((nu1 + 1023) / 1024))), 256, 0, s>>>(
+            w.pk, w.sc, nu1, n, w.inS, x0, hs, w.hist);
+        launches += 1;
+      }
+    }
+    unsigned long long hh[256];
+    GGM_CUDA_TRY(cudaMemcpyAsync(hh, w.hist, sizeof(hh), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    unsigned long long cum = 0;
+    int bstar = 0;
+    for (int bb = 255; bb >= 0; --bb) {
+      cum += hh[bb];
+      if (cum >= (unsigned long long)op.N) { bstar = bb; break; }
+    }
+    // threshold just below the bucket's lower edge: |ψ'| > tau <=> bits >= edge
+    const uint32_t edge = bx0 + ((uint32_t)bstar << hs);
+    const uint32_t tb3 = edge > 0 ? edge - 1 : 0;
+    float tau3;
+    std::memcpy(&tau3, &tb3, 4);
+    // directed candidates <= 2 x the pairs counted (+ slack for ulp asymmetry ψ_ij / ψ_ji)
+    const int64_t need = 2 * (int64_t)cum + 2 * (int64_t)(cum / 1000) + 4096;
+    if (need > op.cand_cap) {
+      *nnz_out = -need;
+      return fail(GGM_ERR_CAPACITY, "overall: ~%lld candidates > cand_capacity %lld",
+                  (long long)need, (long long)op.cand_cap);
+    }
+    int64_t ncoo = 0;
+    ggm_sparsify_opts so3{};
+    so3.mode = 1;
+    so3.topk = 1;
+    so3.tau = edge > 0 ? tau3 : 0.f;
+    st = ggm_sparse_precision(rows, k, F, lambda, 0, rows, &so3, w.rp3, w.col3, w.val3,
+                              op.cand_cap, &ncoo, w.sub, op.ws_sub, stream);
     if (st == GGM_ERR_CAPACITY) {
-      *nnz_out = -ncoo;  // negative: candidate capacity required (two-call protocol)
+      *nnz_out = -ncoo;
       return fail(GGM_ERR_CAPACITY, "overall: %lld candidates > cand_capacity %lld",
                   (long long)ncoo, (long long)op.cand_cap);
     }
     if (st != GGM_OK) return st;
-    launches += ggm_last_launches();
+    launches += ggm_last_launches() + 1;
+    if (g_overall_path == 1) {
+      GGM_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned long long), s));
+      upper_pairs<<<blocks(n), 256, 0, s>>>(w.rp3, w.col3, w.val3, n, w.cnt, w.pk, w.sc);
+      unsigned long long hc = 0;
+      GGM_CUDA_TRY(cudaMemcpyAsync(&hc, w.cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      GGM_CUDA_TRY(cudaStreamSynchronize(s));
+      nc = (int64_t)hc;
+    } else {
+      GGM_CUDA_TRY(cudaMemcpyAsync(w.cnt, &nu1, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+      block_pairs<<<blocks(rows), 256, 0, s>>>(w.rp3, w.col3, w.val3, rows, w.rid_s, n, w.cnt, w.pk, w.sc);
+      unsigned long long hc = 0;
+      GGM_CUDA_TRY(cudaMemcpyAsync(&hc, w.cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      GGM_CUDA_TRY(cudaStreamSynchronize(s));
+      st = dedupe((int64_t)hc, &nc);
+      if (st != GGM_OK) return st;
+      launches += 1;
+    }
   }
-  // (4) upper-triangle candidates ranked by (score desc, i, j); top N; + min-edges; unique
-  GGM_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned long long), s));
-  upper_pairs<<<blocks(n), 256, 0, s>>>(w.rp3, w.col3, w.val3, n, w.cnt, w.pk, w.sc);
-  unsigned long long hc = 0;
-  GGM_CUDA_TRY(cudaMemcpyAsync(&hc, w.cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  const int64_t nc = (int64_t)hc;
+  // (4) candidates ranked by (score desc, i, j): stable sorts by pair key, then by |score|
+  ph.mark(4);
   const int64_t Ntop = std::min<int64_t>(op.N, nc);
   iota_i64<<<blocks(nc), 256, 0, s>>>(w.idx, nc);
   {
@@ -2738,8 +3115,16 @@ extern "C" ggm_status ggm_sparse_precision_overall(
   }
   dir_to_csr<<<blocks(2 * ne + 1), 256, 0, s>>>(w.uk, w.uv, 2 * ne, n, row_ptr, col, val);
   GGM_CUDA_TRY(cudaGetLastError());
+  ph.mark(5);
   GGM_CUDA_TRY(cudaStreamSynchronize(s));
   reset_launches();
   count_launches(launches + 3);
   return GGM_OK;
+}
+
+extern "C" int ggm_overall_last_path(int64_t* saturated, float ms[5]) {
+  if (saturated) *saturated = g_overall_sat;
+  if (ms)
+    for (int i = 0; i < 5; ++i) ms[i] = g_overall_ms[i];
+  return g_overall_path;
 }

@@ -29,18 +29,29 @@ def _run(G, V, lam, N, dw=False, m=0, **kw):
     return rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy()
 
 
+@pytest.fixture(params=["auto", "hist", "block"])
+def path(request, monkeypatch):
+    """auto: the driver's choice; hist / block: force the histogram + threshold passes or
+    the saturated-block pass (whenever the lists give a bound)."""
+    if request.param == "auto":
+        monkeypatch.delenv("GGM_OVERALL_PATH", raising=False)
+    else:
+        monkeypatch.setenv("GGM_OVERALL_PATH", "1" if request.param == "hist" else "2")
+    return request.param
+
+
 @pytest.mark.parametrize("n,k,N,dw,m", [
     (1000, 64, 3000, False, 0), (1000, 64, 3000, True, 0), (777, 37, 500, False, 2),
     (2053, 100, 20530, True, 3), (300, 16, 40000, False, 0), (3, 1, 1, False, 0),
     (129, 128, 64, True, 1), (600, 300, 6000, False, 32), (500, 8, 1, True, 0)])
-def test_overall_matches_oracle(G, n, k, N, dw, m):
+def test_overall_matches_oracle(G, path, n, k, N, dw, m):
     V, lam = gen.small_factor(n * 7 + k + N, n, k)
     rp, c, v = _run(G, V, lam, N, dw, m)
     st = check_overall(rp, c, v, V, lam, N, dw, m)
     assert st["excused"] <= max(2, st["edges"] // 500), st
 
 
-def test_overall_small_capacities_retry(G):
+def test_overall_small_capacities_retry(G, path):
     """Both two-call capacity protocols (candidates and output) through the binding."""
     n, k, N = 400, 24, 900
     V, lam = gen.small_factor(5, n, k)
@@ -48,12 +59,29 @@ def test_overall_small_capacities_retry(G):
     check_overall(rp, c, v, V, lam, N, False, 1)
 
 
-def test_overall_all_zero_offdiagonal(G):
+def test_overall_all_zero_offdiagonal(G, path):
     """V = first k columns of I: every off-diagonal psi is exactly 0 -> no edges (Q17)."""
     n, k = 300, 8
     V = np.eye(n, dtype=np.float32)[:, :k].copy()
     rp, c, v = _run(G, V, np.ones(k), 50, True, 2)
     assert len(c) == 0 and np.all(rp == 0)
+
+
+@pytest.mark.parametrize("dw", [False, True])
+def test_overall_hub_vertices(G, dw):
+    """40 hub rows with 8x the norm: without down-weighting the top pairs concentrate on the
+    hubs, their lists saturate and the histogram + threshold path runs; with it, the
+    scores are rebalanced (the over-focus the paper describes)."""
+    n, k, N = 4000, 48, 40000
+    V, lam = gen.small_factor(77, n, k)
+    V = V.copy()
+    V[::100] *= 8.0
+    rp, c, v = _run(G, V, lam, N, dw, 1)
+    st = check_overall(rp, c, v, V, lam, N, dw, 1)
+    assert st["excused"] <= max(2, st["edges"] // 500), st
+    path, sat = G.overall_last_path()
+    if not dw:
+        assert path != 0 and sat > 0, (path, sat)
 
 
 def test_overall_rank1_closed_form(G):
@@ -80,6 +108,7 @@ def test_overall_at_scale_properties(G):
     Vd = torch.from_numpy(V).cuda()
     ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
     rp, c, v = G.ggm_sparse_precision_overall(Vd, ld, N, min_edges=m)
+    print("overall path, saturated rows:", G.overall_last_path())
     rp, c, v = rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy()
     rows = np.repeat(np.arange(n), np.diff(rp))
     up = rows < c
