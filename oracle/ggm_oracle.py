@@ -20,6 +20,11 @@ Pinning (tests/test_oracle_pins.py, ``-m "not gpu"``):
   canonical gauge           grid invariance; PSD; closed form on shifted inputs
   psi_rows / top_t / thr    dense V diag(λ) V^T + brute-force sort on tiny inputs;
                             rank-1 closed form; identity-factor all-tie case
+  *_multi (shared axes)     one modality = the single-modality functions; disjoint
+                            modalities = independent solves; dense multi-modal NLL and
+                            the dense stationarity Σ_γ sb-trace[(⊕_γΨ)^-1] = S_l
+                            at the solution; gauge-class invariance; SVD of the
+                            concatenation vs eigh of Σ_γ S^γ_l
 No function here is "parity unpinned".
 """
 from __future__ import annotations
@@ -34,6 +39,8 @@ __all__ = [
     "kron_sum", "sb_trace", "dense_nll",
     "psi_rows", "top_t_row", "threshold_row", "sparse_precision",
     "wald_edge", "wald_threshold", "overall_edges", "edges_to_symmetric_csr",
+    "gram_eig_multi", "grid_sums_multi", "marginals_multi", "nll_multi", "gradient_multi",
+    "stationarity_multi", "gauge_space_multi", "canonical_gauge_multi", "solve_eigvals_multi",
 ]
 
 
@@ -293,6 +300,163 @@ def paper_gd_solve(E, max_iter: int = 200000, tol: float = 1e-9, eps_scale: floa
         lams, f = cand, fc
         it += 1
     return lams, dict(iterations=it, stationarity=stationarity(E, lams))
+
+
+# ---------------------------------------------------------------------------
+# Multi-modal datasets — shared axes (Thm 2 Σ_γ P:356, Alg. 1 line 2 P:909)
+# ---------------------------------------------------------------------------
+# A modality γ is a tensor D^γ whose axes are a subset of the global axes (no repeated axis
+# within one modality); `modalities` lists, per modality, its global axis ids in the
+# tensor's own axis order.
+
+def gram_eig_multi(tensors, modalities, axis: int, k: int):
+    """Alg. 1 lines 2-4 for global axis `axis`: D_l = [mat_l(D^γ1) ... mat_l(D^γΓ)] over the
+    modalities containing l, top-k left singular vectors and E = σ²."""
+    blocks = [matricize(x, list(mod).index(axis)) for x, mod in zip(tensors, modalities)
+              if axis in mod]
+    if not blocks:
+        raise ValueError(f"axis {axis} occurs in no modality")
+    m = np.concatenate(blocks, axis=1)
+    if not 1 <= k <= min(m.shape):
+        raise RankError(f"k={k} not in [1, {min(m.shape)}] (S:116)")
+    u, sig, _ = np.linalg.svd(m, full_matrices=False)
+    e = sig ** 2
+    _check_rank(e, k)
+    return u[:, :k].copy(), e[:k].copy()
+
+
+def _check_modalities(nax: int, modalities):
+    for mod in modalities:
+        if len(set(mod)) != len(mod):
+            raise ValueError("repeated axis within a modality (P:181)")
+        if any(a < 0 or a >= nax for a in mod):
+            raise ValueError("axis id out of range")
+    if set(a for mod in modalities for a in mod) != set(range(nax)):
+        raise ValueError("every axis must occur in some modality")
+
+
+def grid_sums_multi(lams, modalities):
+    """Per modality γ: s^γ_j = Σ_{l∈γ} λ_l[j_l] on γ's k-grid (diagonal of ⊕_{l∈γ}Λ_l)."""
+    return [grid_sums([lams[a] for a in mod]) for mod in modalities]
+
+
+def marginals_multi(lams, modalities):
+    """Σ_{γ∋l} tr^{k^γ_<l}_{k^γ_>l}[(⊕_{l'∈γ}Λ_l')^†] diagonals (Thm 2): per axis l,
+    the sum over the modalities containing l of the single-modality marginals."""
+    g = [np.zeros(len(l)) for l in lams]
+    for mod in modalities:
+        mg = marginals([lams[a] for a in mod])
+        for pos, a in enumerate(mod):
+            g[a] = g[a] + mg[pos]
+    return g
+
+
+def nll_multi(E, lams, modalities) -> float:
+    """NLL = ½ Σ_l E_l·λ_l − ½ Σ_γ Σ_{j∈grid γ} log s^γ_j: the product of the per-modality
+    densities in the eigenbasis of S_l = Σ_γ S^γ_l (constants dropped, Q11)."""
+    lin = sum(float(np.dot(np.asarray(e, np.float64), np.asarray(l, np.float64)))
+              for e, l in zip(E, lams))
+    tot = 0.0
+    for s in grid_sums_multi(lams, modalities):
+        if s.min() <= 0:
+            return np.inf
+        tot += float(np.log(s).sum())
+    return 0.5 * lin - 0.5 * tot
+
+
+def gradient_multi(E, lams, modalities):
+    """∂NLL/∂Λ_l = ½ (E_l − Σ_{γ∋l} g^γ_l)  (Theorem 2)."""
+    g = marginals_multi(lams, modalities)
+    return [0.5 * (np.asarray(e, np.float64) - gl) for e, gl in zip(E, g)]
+
+
+def stationarity_multi(E, lams, modalities) -> float:
+    g = marginals_multi(lams, modalities)
+    emax = max(float(np.max(e)) for e in E)
+    return max(float(np.max(np.abs(np.asarray(e) - gl))) for e, gl in zip(E, g)) / emax
+
+
+def gauge_space_multi(nax: int, modalities) -> np.ndarray:
+    """Orthonormal basis (nax x r) of G = {c : Σ_{l∈γ} c_l = 0 for every γ}: the per-axis
+    shifts λ_l + c_l that leave every grid sum unchanged (reading G)."""
+    M = np.zeros((len(modalities), nax))
+    for r, mod in enumerate(modalities):
+        M[r, list(mod)] = 1.0
+    _, sv, vt = np.linalg.svd(M)
+    rank = int(np.sum(sv > 1e-12 * max(sv.max(), 1.0)))
+    return vt[rank:].T.copy()
+
+
+def canonical_gauge_multi(lams, modalities):
+    """Gauge 0 for shared axes (reading G2): with μ_l = min λ_l, subtract the G-component
+    of μ: λ_l ← λ_l − (P_G μ)_l.  A function of the gauge class only (P_G c = c on G);
+    for one modality P_G μ = μ − mean(μ), i.e. canonical_gauge."""
+    N = gauge_space_multi(len(lams), modalities)
+    mu = np.array([float(np.min(l)) for l in lams])
+    sh = N @ (N.T @ mu) if N.size else np.zeros(len(lams))
+    return [np.asarray(l, np.float64) - float(sh[a]) for a, l in enumerate(lams)]
+
+
+def solve_eigvals_multi(E, modalities, tol: float = 1e-12, max_iter: int = 200,
+                        gauge: int = 0):
+    """Multi-modal eigenvalue MLE (Thm 2 with Σ_γ): argmin of nll_multi, computed as
+    in solve_eigvals — projected Newton on G⊥ (Hessian: per modality the 1/s² marginals,
+    summed), backtracking on NLL with grid feasibility, start λ = 1/E (Alg. 1 line 5)."""
+    E = [np.asarray(e, np.float64) for e in E]
+    ks = [len(e) for e in E]
+    _check_modalities(len(E), modalities)
+    if any(np.any(~np.isfinite(e)) or np.any(e <= 0) for e in E):
+        raise ValueError("E must be finite and > 0 (Thm 4 hypothesis, P:742)")
+    off = np.cumsum([0] + ks)
+    n = int(off[-1])
+    Nax = gauge_space_multi(len(E), modalities)
+    if Nax.size:
+        B = np.zeros((n, Nax.shape[1]))
+        for a in range(len(E)):
+            B[off[a]:off[a + 1], :] = Nax[a][None, :]
+        Q, _ = np.linalg.qr(B)
+        P = np.eye(n) - Q @ Q.T
+    else:
+        P = np.eye(n)
+    lam = np.concatenate([1.0 / e for e in E])
+    f = nll_multi(E, _split(lam, ks), modalities)
+    it = 0
+    res = stationarity_multi(E, _split(lam, ks), modalities)
+    while res > tol and it < max_iter:
+        lams = _split(lam, ks)
+        grad = np.concatenate(gradient_multi(E, lams, modalities))
+        H = np.zeros((n, n))
+        for mod in modalities:
+            diag, pair = marginals_sq2d([lams[a] for a in mod])
+            for pa, a in enumerate(mod):
+                H[off[a]:off[a + 1], off[a]:off[a + 1]] += np.diag(0.5 * diag[pa])
+            for (pa, pb), m in pair.items():
+                a, b = mod[pa], mod[pb]
+                H[off[a]:off[a + 1], off[b]:off[b + 1]] += 0.5 * m
+                H[off[b]:off[b + 1], off[a]:off[a + 1]] += 0.5 * m.T
+        step = P @ (-np.linalg.lstsq(P @ H @ P, P @ grad, rcond=None)[0])
+        alpha = 1.0
+        while True:
+            cand = lam + alpha * step
+            fc = nll_multi(E, _split(cand, ks), modalities)
+            if np.isfinite(fc) and fc <= f + 1e-4 * alpha * float(grad @ step):
+                break
+            alpha *= 0.5
+            if alpha < 1e-12:
+                cand, fc = lam, f
+                break
+        if np.array_equal(cand, lam):
+            break
+        lam, f = cand, fc
+        it += 1
+        res = stationarity_multi(E, _split(lam, ks), modalities)
+    lams = _split(lam, ks)
+    if gauge == 0:
+        lams = canonical_gauge_multi(lams, modalities)
+    info = dict(iterations=it, stationarity=stationarity_multi(E, lams, modalities),
+                nll=nll_multi(E, lams, modalities),
+                grid_min=min(float(s.min()) for s in grid_sums_multi(lams, modalities)))
+    return lams, info
 
 
 # ---------------------------------------------------------------------------

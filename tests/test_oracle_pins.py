@@ -363,3 +363,100 @@ def test_overall_zero_psi_is_no_edge():
     got = set(zip(ii.tolist(), jj.tolist()))
     assert got == {(0, 1), (0, 2), (1, 2), (3, 4)}
     assert np.allclose(vv, [2.0, 3.0, 6.0, -1.0])
+
+
+# ---------------------------------------------------------------- multi-modal (shared axes)
+
+def _two_matrices(seed=3):
+    """Modality 0 = X1 (axes 0, 1), modality 1 = X2 stored as (axis 2, axis 1): axis 1 is
+    shared.  Full rank on every axis."""
+    rng = np.random.default_rng(seed)
+    X1 = rng.standard_normal((3, 4))
+    X2 = rng.standard_normal((3, 4))
+    return [X1, X2], [[0, 1], [2, 1]]
+
+
+def test_gram_eig_multi_concatenation_vs_summed_grams():
+    """Alg. 1 line 2: SVD of [mat(D^1) mat(D^2)] = eigh of Σ_γ S^γ_l."""
+    T, mods = _two_matrices()
+    V, E = O.gram_eig_multi(T, mods, 1, 4)
+    S = O.gram(T[0], 1) + O.gram(T[1], 1)
+    ev = np.sort(np.linalg.eigvalsh(S))[::-1]
+    assert np.allclose(E, ev, rtol=1e-12)
+    assert np.allclose(V @ np.diag(E) @ V.T, S, atol=1e-10)
+    with pytest.raises(ValueError):
+        O.gram_eig_multi(T, mods, 5, 1)
+
+
+def test_multi_single_modality_reduces_to_single():
+    rng = np.random.default_rng(5)
+    E = [np.sort(rng.uniform(1, 4, k))[::-1] for k in (4, 3, 5)]
+    E = [e * 12.0 / e.sum() for e in E]          # equal traces: interior MLE (reading T)
+    a, ia = O.solve_eigvals(E)
+    b, ib = O.solve_eigvals_multi(E, [[0, 1, 2]])
+    assert ib["stationarity"] < 1e-10
+    for x, y in zip(a, b):
+        assert np.allclose(x, y, rtol=1e-9, atol=1e-12)
+    assert np.allclose(O.grid_sums(a), O.grid_sums_multi(b, [[0, 1, 2]])[0], rtol=1e-10)
+
+
+def test_multi_disjoint_modalities_are_independent():
+    rng = np.random.default_rng(6)
+    E = [np.sort(rng.uniform(1, 3, k))[::-1] for k in (3, 4, 2, 5)]
+    E[0] *= E[1].sum() / E[0].sum()
+    E[2] *= E[3].sum() / E[2].sum()
+    m, _ = O.solve_eigvals_multi(E, [[0, 1], [2, 3]])
+    a, _ = O.solve_eigvals(E[:2])
+    b, _ = O.solve_eigvals(E[2:])
+    assert np.allclose(O.grid_sums(m[:2]), O.grid_sums(a), rtol=1e-10)
+    assert np.allclose(O.grid_sums(m[2:]), O.grid_sums(b), rtol=1e-10)
+
+
+def test_multi_dense_nll_and_stationarity():
+    """Shared axis: nll_multi = Σ_γ of the dense matrix-form NLL of each modality,
+    and at the solution the dense full-rank stationarity Σ_{γ∋l} sb-trace[(⊕_γ Ψ)^-1] = S_l
+    (Thm 2 with Σ_γ) holds."""
+    T, mods = _two_matrices()
+    d = {0: 3, 1: 4, 2: 3}
+    Sg = [[O.gram(T[g], p) for p in range(2)] for g in range(2)]
+    S = {0: Sg[0][0], 1: Sg[0][1] + Sg[1][1], 2: Sg[1][0]}
+    VE = {a: np.linalg.eigh(S[a]) for a in range(3)}
+    V = {a: VE[a][1][:, ::-1] for a in range(3)}
+    E = [VE[a][0][::-1].copy() for a in range(3)]
+    rng = np.random.default_rng(9)
+    lam = [rng.uniform(0.5, 2.0, d[a]) for a in range(3)]
+    psi = {a: V[a] @ np.diag(lam[a]) @ V[a].T for a in range(3)}
+    dense = sum(O.dense_nll([Sg[g][p] for p in range(2)], [psi[a] for a in mods[g]])
+                for g in range(2))
+    assert abs(O.nll_multi(E, lam, mods) - dense) < 1e-9 * max(1.0, abs(dense))
+    sol, info = O.solve_eigvals_multi(E, mods, tol=1e-13)
+    assert info["stationarity"] < 1e-11
+    psi = {a: V[a] @ np.diag(sol[a]) @ V[a].T for a in range(3)}
+    acc = {a: np.zeros((d[a], d[a])) for a in range(3)}
+    for g, mod in enumerate(mods):
+        inv = np.linalg.inv(O.kron_sum([psi[a] for a in mod]))
+        dims = [d[a] for a in mod]
+        for p, a in enumerate(mod):
+            pre = int(np.prod(dims[:p])) if p else 1
+            post = int(np.prod(dims[p + 1:])) if p + 1 < len(dims) else 1
+            acc[a] += O.sb_trace(inv, pre, post, d[a])
+    for a in range(3):
+        assert np.allclose(acc[a], S[a], atol=1e-8 * np.abs(S[a]).max())
+
+
+def test_multi_gauge_space_and_canonical_invariance():
+    mods = [[0, 1], [2, 1]]
+    N = O.gauge_space_multi(3, mods)
+    assert N.shape == (3, 1)
+    assert np.allclose(N[:, 0] / N[0, 0], [1.0, -1.0, 1.0])
+    rng = np.random.default_rng(2)
+    lam = [rng.uniform(1, 2, k) for k in (3, 4, 3)]
+    c = 0.37 * N[:, 0]
+    sh = [l + c[a] for a, l in enumerate(lam)]
+    for s1, s2 in zip(O.grid_sums_multi(lam, mods), O.grid_sums_multi(sh, mods)):
+        assert np.allclose(s1, s2, rtol=1e-13)
+    for x, y in zip(O.canonical_gauge_multi(lam, mods), O.canonical_gauge_multi(sh, mods)):
+        assert np.allclose(x, y, rtol=1e-12)
+    single = O.canonical_gauge_multi(lam, [[0, 1, 2]])
+    for x, y in zip(single, O.canonical_gauge(lam)):
+        assert np.allclose(x, y, rtol=1e-12)
