@@ -98,6 +98,21 @@ ggm_status ggm_gram_eig_rsi(const float *X, int ndim, const int64_t *shape, int 
                             double *E, double *trace_S, int *iters_out, double *change_out,
                             void *workspace, size_t workspace_bytes, void *stream);
 
+/* (1c) Multi-modal spectrum of one shared axis l (Alg. 1 line 2): the top-k left
+ * singular vectors of D_l = [mat_l(D^γ1) ... mat_l(D^γΓ)] — the eigenpairs of
+ * S_l = Σ_γ mat_l(D^γ) mat_l(D^γ)^T.  M modalities; X[g] (host array of DEVICE pointers)
+ * is modality g's row-major fp32 tensor with ndim[g] axes, shapes[] concatenates all M
+ * shapes (host), axis_pos[g] = position of axis l in modality g or -1 if absent (its X[g]
+ * may then be NULL).  The shared axis must have the same length in every modality that has
+ * it.  Output as ggm_gram_eig (V: d_l x k fp32, E: k fp64 descending, trace_S = ||D_l||_F^2);
+ * dense path up to a 32768^2 Gram of either side, randomized subspace iteration above. */
+ggm_status ggm_gram_eig_multi_workspace(int M, const int *ndim, const int64_t *shapes,
+                                        const int *axis_pos, int k, size_t *bytes);
+ggm_status ggm_gram_eig_multi(int M, const float *const *X, const int *ndim,
+                              const int64_t *shapes, const int *axis_pos, int k, float *V,
+                              double *E, double *trace_S, void *workspace,
+                              size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------------------------
  * (2) Eigenvalue MLE — Theorem 2, Algorithm 1 lines 5-17.
  *
@@ -140,6 +155,20 @@ typedef struct {
 void ggm_solve_opts_default(ggm_solve_opts *opts);
 ggm_status ggm_solve_eigvals(int L, const int *k, const double *E, const ggm_solve_opts *opts,
                              double *lambda, ggm_solve_info *info, void *stream);
+
+/* (2b) Multi-modal eigenvalue MLE (Thm 2 with Σ_γ; shared axes P:170-181):
+ * A global axes with ranks k[A] and axis-concatenated E (from ggm_gram_eig_multi of each
+ * axis); M <= 8 modalities, modality g = global axes mod_axes[mod_ptr[g] .. mod_ptr[g+1])
+ * (host; no repeated axis within a modality, every axis in some modality).  Minimises
+ * ½ Σ_l E_l·λ_l − ½ Σ_γ Σ_{j in grid γ} log s^γ_j by the majorise-minimise step
+ * λ ← λ ⊙ (Σ_{γ∋l} g^γ_l) / E_l.  Gauge 0 (reading G2): λ_l − (P_G μ)_l with μ_l = min λ_l
+ * and P_G the projector onto the shifts that keep every modality's grid sums (one modality:
+ * identical to ggm_solve_eigvals' gauge 0).  info as ggm_solve_eigvals (grid_min = the
+ * smallest modality grid minimum).  Synchronizes `stream`. */
+ggm_status ggm_solve_eigvals_multi(int A, const int *k, const double *E, int M,
+                                   const int *mod_ptr, const int *mod_axes,
+                                   const ggm_solve_opts *opts, double *lambda,
+                                   ggm_solve_info *info, void *stream);
 
 /* Grid marginals alone (the Thm 2 trace term), for parity tests and the bench:
  * g (out, float64 sum(k)) and, if logsum_out != NULL, F = Σ_j log s_j (host).  Synchronizes

@@ -36,6 +36,7 @@ EXPORTED = [
     "ggm_wald_edge", "ggm_wald_threshold",
     "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
     "ggm_overall_last_path",
+    "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
 ]
 
 
@@ -125,8 +126,17 @@ def lib() -> C.CDLL:
     L.ggm_sparse_precision_overall.argtypes = [i64, i32, vp, vp, C.POINTER(OverallOpts), i64, vp,
                                                vp, vp, i64, C.POINTER(i64), vp, C.c_size_t, vp]
     L.ggm_overall_last_path.argtypes = [C.POINTER(i64), C.POINTER(C.c_float)]
+    L.ggm_gram_eig_multi_workspace.argtypes = [i32, C.POINTER(i32), C.POINTER(i64), C.POINTER(i32),
+                                               i32, C.POINTER(C.c_size_t)]
+    L.ggm_gram_eig_multi.argtypes = [i32, C.POINTER(vp), C.POINTER(i32), C.POINTER(i64),
+                                     C.POINTER(i32), i32, vp, vp, C.POINTER(C.c_double), vp,
+                                     C.c_size_t, vp]
+    L.ggm_solve_eigvals_multi.argtypes = [i32, C.POINTER(i32), vp, i32, C.POINTER(i32),
+                                          C.POINTER(i32), C.POINTER(SolveOpts), vp,
+                                          C.POINTER(SolveInfo), vp]
     L.ggm_overall_last_path.restype = i32
-    for name in ("ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
+    for name in ("ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
+                 "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
                  "ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
                  "ggm_gram_eig_rsi_workspace", "ggm_gram_eig_rsi",
                  "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision",
@@ -208,6 +218,40 @@ def ggm_gram_eig_rsi(X: torch.Tensor, axis: int, k: int, oversample: int = 0,
     return V, E, tr.value, it.value, ch.value
 
 
+def ggm_gram_eig_multi(tensors, axis_pos, k: int, stream=None):
+    """Shared-axis spectrum (Alg. 1 line 2): tensors = per-modality fp32 CUDA tensors
+    (None where the axis is absent), axis_pos[g] = the axis' position in modality g or -1.
+    Returns (V float32 d x k, E float64 k descending, ||D_l||_F^2)."""
+    M = len(tensors)
+    if len(axis_pos) != M:
+        raise ValueError("axis_pos length != number of modalities")
+    dev = None
+    for X, p in zip(tensors, axis_pos):
+        if p >= 0:
+            _require_cuda(X, torch.float32, "X")
+            dev = X.device
+    if dev is None:
+        raise ValueError("the axis occurs in no modality")
+    nd = [X.dim() if X is not None else 1 for X in tensors]
+    flat = []
+    for X in tensors:
+        flat.extend(list(X.shape) if X is not None else [1])
+    ndim = (C.c_int * M)(*nd)
+    shapes = (C.c_int64 * len(flat))(*flat)
+    pos = (C.c_int * M)(*[int(p) for p in axis_pos])
+    ptrs = (C.c_void_p * M)(*[X.data_ptr() if X is not None else None for X in tensors])
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_gram_eig_multi_workspace(M, ndim, shapes, pos, int(k), C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=dev)
+    d = next(X.shape[p] for X, p in zip(tensors, axis_pos) if p >= 0)
+    V = torch.empty((d, k), dtype=torch.float32, device=dev)
+    E = torch.empty((k,), dtype=torch.float64, device=dev)
+    tr = C.c_double(0.0)
+    _check(lib().ggm_gram_eig_multi(M, ptrs, ndim, shapes, pos, int(k), _ptr(V), _ptr(E),
+                                    C.byref(tr), _ptr(ws), nbytes.value, _stream(stream)))
+    return V, E, tr.value
+
+
 # --------------------------------------------------------------------------- (2) solve
 
 def ggm_solve_eigvals(E: torch.Tensor, ks, tol: float = 1e-7, max_iter: int = 20000,
@@ -226,6 +270,31 @@ def ggm_solve_eigvals(E: torch.Tensor, ks, tol: float = 1e-7, max_iter: int = 20
     info = SolveInfo()
     _check(lib().ggm_solve_eigvals(len(ks), karr, _ptr(E), C.byref(o), _ptr(lam), C.byref(info),
                                    _stream(stream)))
+    return lam, {f: getattr(info, f) for f, _ in SolveInfo._fields_}
+
+
+def ggm_solve_eigvals_multi(E: torch.Tensor, ks, modalities, tol: float = 1e-7,
+                            max_iter: int = 20000, gauge: int = 0, stream=None):
+    """Multi-modal eigenvalue MLE (Thm 2 with Σ_γ): E axis-concatenated over the global
+    axes (ranks ks), modalities = lists of global axis ids.  Returns (lambda, info)."""
+    _require_cuda(E, torch.float64, "E")
+    ks = [int(k) for k in ks]
+    if E.numel() != sum(ks):
+        raise ValueError("E length != sum(ks)")
+    ptr = [0]
+    axes = []
+    for mod in modalities:
+        axes.extend(int(a) for a in mod)
+        ptr.append(len(axes))
+    o = SolveOpts()
+    lib().ggm_solve_opts_default(C.byref(o))
+    o.tol, o.max_iter, o.gauge = tol, max_iter, gauge
+    lam = torch.empty_like(E)
+    info = SolveInfo()
+    _check(lib().ggm_solve_eigvals_multi(len(ks), (C.c_int * len(ks))(*ks), _ptr(E),
+                                         len(modalities), (C.c_int * len(ptr))(*ptr),
+                                         (C.c_int * max(len(axes), 1))(*axes), C.byref(o),
+                                         _ptr(lam), C.byref(info), _stream(stream)))
     return lam, {f: getattr(info, f) for f, _ in SolveInfo._fields_}
 
 

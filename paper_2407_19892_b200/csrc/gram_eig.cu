@@ -309,6 +309,11 @@ __global__ void take_topk_small(const double* __restrict__ w, const double* __re
 using namespace ggm;
 using namespace ggm::ge;
 
+static ggm_status rsi_core(const RPlan& rp, const RWork& w, int max_iter, double tol,
+                           uint64_t seed, float* V, double* E, double* trace_S, int* iters_out,
+                           double* change_out, cublasHandle_t hb, cusolverDnHandle_t hs,
+                           cudaStream_t s);
+
 extern "C" ggm_status ggm_gram_eig_rsi_workspace(int ndim, const int64_t* shape, int axis, int k,
                                                  int oversample, size_t* bytes) {
   if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
@@ -342,16 +347,28 @@ extern "C" ggm_status ggm_gram_eig_rsi(const float* X, int ndim, const int64_t* 
   if (workspace_bytes < need)
     return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
   const int sms = num_sms();
-  const int d = (int)rp.d, m = (int)rp.m, r = rp.r, kk = rp.k;
   GGM_CUDA_TRY(cudaMemsetAsync(w.fro, 0, sizeof(double), s));
   {
     const int64_t total = rp.pre_n * rp.d * rp.post_n;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 16));
     unfold_f64<<<grid, 256, 0, s>>>(X, rp.pre_n, rp.d, rp.post_n, w.M, w.fro);  // M: d x m
-    fill_normal<<<(int)std::min<int64_t>(((int64_t)m * r + 255) / 256, sms * 8), 256, 0, s>>>(
-        w.Om, (int64_t)m * r, seed);
     GGM_CUDA_TRY(cudaGetLastError());
   }
+  return rsi_core(rp, w, max_iter, tol, seed, V, E, trace_S, iters_out, change_out, hb, hs, s);
+}
+
+// Randomized subspace iteration on the unfolding already in w.M (d x m column-major) and its
+// squared Frobenius norm in w.fro.
+static ggm_status rsi_core(const RPlan& rp, const RWork& w, int max_iter, double tol,
+                           uint64_t seed, float* V, double* E, double* trace_S, int* iters_out,
+                           double* change_out, cublasHandle_t hb, cusolverDnHandle_t hs,
+                           cudaStream_t s) {
+  const int sms = num_sms();
+  const int d = (int)rp.d, m = (int)rp.m, r = rp.r, kk = rp.k;
+  ggm_status st = GGM_OK;
+  fill_normal<<<(int)std::min<int64_t>(((int64_t)m * r + 255) / 256, sms * 8), 256, 0, s>>>(
+      w.Om, (int64_t)m * r, seed);
+  GGM_CUDA_TRY(cudaGetLastError());
   const double one = 1.0, zero = 0.0;
   auto orth = [&](double* A) -> ggm_status {  // A (d x r) := Q of its Householder QR
     if (cusolverDnDgeqrf(hs, d, r, A, d, w.tau, w.work, rp.lw_geqrf, w.info) != CUSOLVER_STATUS_SUCCESS ||
@@ -418,6 +435,11 @@ namespace ge {
 }  // namespace ggm
 
 
+static ggm_status dense_core(const GPlan& g, int lwork, double* Md, double* S, double* w,
+                             double* work, int* dinfo, double* V64, double* fro, double* Ek,
+                             double* Vasc, float* V, double* E, double* trace_S,
+                             cublasHandle_t hb, cusolverDnHandle_t hs, cudaStream_t s);
+
 extern "C" ggm_status ggm_gram_eig_workspace(int ndim, const int64_t* shape, int axis, int k,
                                              size_t* bytes) {
   if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
@@ -483,6 +505,14 @@ extern "C" ggm_status ggm_gram_eig(const float* X, int ndim, const int64_t* shap
     unfold_f64<<<grid, 256, 0, s>>>(X, pre_n, d, post_n, Md, fro);
     GGM_CUDA_TRY(cudaGetLastError());
   }
+  return dense_core(g, lwork, Md, S, w, work, dinfo, V64, fro, Ek, Vasc, V, E, trace_S, hb, hs, s);
+}
+
+// Gram + eigensolve + top-k mapping on the unfolding already in Md (GPlan g decides the side).
+static ggm_status dense_core(const GPlan& g, int lwork, double* Md, double* S, double* w,
+                             double* work, int* dinfo, double* V64, double* fro, double* Ek,
+                             double* Vasc, float* V, double* E, double* trace_S,
+                             cublasHandle_t hb, cusolverDnHandle_t hs, cudaStream_t s) {
   const double one = 1.0, zero = 0.0;
   cublasStatus_t bs;
   if (g.mode == 2)  // S = M^T M  (m x m), M is d x m column-major
@@ -529,4 +559,139 @@ extern "C" ggm_status ggm_gram_eig(const float* X, int ndim, const int64_t* shap
     return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)",
                 hE[g.k - 1], hE[0]);
   return GGM_OK;
+}
+
+// ------------------------------------------------------------------ multi-modal spectrum
+// Alg. 1 line 2: D_l = [mat_l(D^γ1) ... mat_l(D^γΓ)] over the modalities that
+// contain axis l; V, E = top-k left singular vectors / squared singular values of D_l, i.e.
+// the eigenpairs of S_l = Σ_γ mat_l(D^γ) mat_l(D^γ)^T.  Each modality is unfolded into its
+// own column block of one fp64 d x Σm matrix; the dense (primal or dual Gram) or at-scale
+// (randomized subspace iteration) path then runs on the concatenation.
+namespace {
+struct MultiShape {
+  int64_t d, m_tot;
+  std::vector<int64_t> pre, post, coloff;
+  std::vector<int> used;  // modalities that contain the axis
+};
+ggm_status multi_shape(int M, const int* ndim, const int64_t* shapes, const int* axis_pos,
+                       MultiShape* ms) {
+  if (M < 1 || !ndim || !shapes || !axis_pos)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "M < 1 or null descriptor");
+  ms->d = -1;
+  ms->m_tot = 0;
+  const int64_t* sh = shapes;
+  for (int g = 0; g < M; ++g) {
+    if (ndim[g] < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "ndim[%d] < 1", g);
+    const int ax = axis_pos[g];
+    if (ax >= ndim[g]) return fail(GGM_ERR_INVALID_ARGUMENT, "axis_pos[%d] out of range", g);
+    if (ax >= 0) {
+      int64_t pre = 1, post = 1;
+      for (int a = 0; a < ndim[g]; ++a) {
+        if (sh[a] < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "shape < 1");
+        if (a < ax) pre *= sh[a];
+        if (a > ax) post *= sh[a];
+      }
+      if (ms->d >= 0 && sh[ax] != ms->d)
+        return fail(GGM_ERR_INVALID_ARGUMENT, "shared axis length differs between modalities");
+      ms->d = sh[ax];
+      ms->pre.push_back(pre);
+      ms->post.push_back(post);
+      ms->coloff.push_back(ms->m_tot);
+      ms->used.push_back(g);
+      ms->m_tot += pre * post;
+    }
+    sh += ndim[g];
+  }
+  if (ms->used.empty()) return fail(GGM_ERR_INVALID_ARGUMENT, "the axis occurs in no modality");
+  return GGM_OK;
+}
+}  // namespace
+
+extern "C" ggm_status ggm_gram_eig_multi_workspace(int M, const int* ndim, const int64_t* shapes,
+                                                   const int* axis_pos, int k, size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  MultiShape ms;
+  ggm_status st = multi_shape(M, ndim, shapes, axis_pos, &ms);
+  if (st != GGM_OK) return st;
+  const int64_t shape2[2] = {ms.d, ms.m_tot};
+  GPlan g;
+  st = make_gplan(2, shape2, 0, k, &g);
+  if (st != GGM_OK) return st;
+  if (g.dim > kMaxDenseGram) return ggm_gram_eig_rsi_workspace(2, shape2, 0, k, 0, bytes);
+  if (g.mode == 1) {  // the concatenation is a plain d x m matrix: use the M^T M form
+    g.mode = 2;
+    g.Md_rows = g.d;
+    g.Md_cols = g.m;
+  }
+  int lwork = 0;
+  st = query_lwork(g, &lwork);
+  if (st != GGM_OK) return st;
+  double *a, *b, *c, *d, *f, *h, *e, *v;
+  int* i;
+  *bytes = gcarve(g, lwork, nullptr, &a, &b, &c, &d, &i, &f, &h, &e, &v);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_gram_eig_multi(int M, const float* const* X, const int* ndim,
+                                         const int64_t* shapes, const int* axis_pos, int k,
+                                         float* V, double* E, double* trace_S, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+  if (!X || !V || !E || !workspace) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  MultiShape ms;
+  ggm_status st = multi_shape(M, ndim, shapes, axis_pos, &ms);
+  if (st != GGM_OK) return st;
+  for (int g = 0; g < M; ++g)
+    if (axis_pos[g] >= 0 && !X[g]) return fail(GGM_ERR_INVALID_ARGUMENT, "X[%d] is NULL", g);
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  const int64_t shape2[2] = {ms.d, ms.m_tot};
+  const int sms = num_sms();
+  auto unfold_all = [&](double* Mbase, double* fro) -> ggm_status {
+    GGM_CUDA_TRY(cudaMemsetAsync(fro, 0, sizeof(double), s));
+    for (size_t u = 0; u < ms.used.size(); ++u) {
+      const int64_t total = ms.pre[u] * ms.d * ms.post[u];
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 16));
+      unfold_f64<<<grid, 256, 0, s>>>(X[ms.used[u]], ms.pre[u], ms.d, ms.post[u],
+                                      Mbase + (size_t)ms.coloff[u] * ms.d, fro);
+      GGM_CUDA_TRY(cudaGetLastError());
+    }
+    return GGM_OK;
+  };
+  GPlan g;
+  st = make_gplan(2, shape2, 0, k, &g);
+  if (st != GGM_OK) return st;
+  if (g.dim > kMaxDenseGram) {
+    RPlan rp;
+    st = make_rplan(2, shape2, 0, k, 0, &rp);
+    if (st != GGM_OK) return st;
+    RWork w;
+    const size_t need = rcarve(rp, workspace, &w);
+    if (workspace_bytes < need)
+      return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+    st = unfold_all(w.M, w.fro);
+    if (st != GGM_OK) return st;
+    return rsi_core(rp, w, kRsiMaxIter, kRsiTol, kRsiSeed, V, E, trace_S, nullptr, nullptr, hb,
+                    hs, s);
+  }
+  if (g.mode == 1) {
+    g.mode = 2;
+    g.Md_rows = g.d;
+    g.Md_cols = g.m;
+  }
+  int lwork = 0;
+  st = query_lwork(g, &lwork);
+  if (st != GGM_OK) return st;
+  double *Md, *S, *w, *work, *V64, *fro, *Ek, *Vasc;
+  int* dinfo;
+  const size_t need = gcarve(g, lwork, workspace, &Md, &S, &w, &work, &dinfo, &V64, &fro, &Ek, &Vasc);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  st = unfold_all(Md, fro);
+  if (st != GGM_OK) return st;
+  return dense_core(g, lwork, Md, S, w, work, dinfo, V64, fro, Ek, Vasc, V, E, trace_S, hb, hs, s);
 }

@@ -161,8 +161,12 @@ __device__ __forceinline__ void load_lambda(const double* lam, int total, double
     slam[i] = bypass_l1 ? __ldcg(&lam[i]) : lam[i];
 }
 
+constexpr int kMaxMods = 8;  // modalities of a multi-modal solve
+
 struct SolveParams {
-  GridDesc gd;
+  GridDesc gd[kMaxMods];  // one per modality; offsets index the global concatenation
+  int M;                  // modalities
+  int T;                  // Σk over all axes
   const double* E;
   double* lam_out;    // converged λ (gauge 1: as iterated), Σk
   double* g;          // marginals at lam_out, Σk
@@ -183,8 +187,7 @@ template <int J>
 __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
-  const GridDesc& gd = p.gd;
-  const int T = gd.total;
+  const int T = p.T;
   double* sg = dsm;        // Σk block partials, then the reduced marginals
   double* slam = sg + T;   // Σk this block's λ
   __shared__ double s_red[kWarps];
@@ -207,7 +210,8 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p)
     if (blockIdx.x == 0 && !single)
       for (int i = threadIdx.x; i < T; i += blockDim.x) p.gacc[(size_t)((it + 1) % 3) * T + i] = 0.0;
     __syncthreads();
-    grid_pass<J>(gd, slam, sg, gw, nw);
+    // Σ_γ of the modalities' marginals (Thm 2): each pass adds into the same sg
+    for (int m = 0; m < p.M; ++m) grid_pass<J>(p.gd[m], slam, sg, gw, nw);
     __syncthreads();
     double mr = 0.0;
     if (single) {  // one block: the block partials are the marginals, no grid barrier
@@ -365,6 +369,21 @@ static ggm_status make_desc(int L, const int* k, GridDesc* gd) {
   return GGM_OK;
 }
 
+// Modality descriptor: axes `ax[0..L)` of the global axes (ranks kg, offsets offg), so the
+// pass indexes λ and accumulates the marginals directly in the global concatenation.
+static ggm_status make_desc_mod(int L, const int* ax, const int* kg, const int* offg, int T,
+                                GridDesc* gd) {
+  if (L < 1 || L > kMaxAxes) return fail(GGM_ERR_INVALID_ARGUMENT, "modality with %d axes", L);
+  int kl[kMaxAxes];
+  for (int a = 0; a < L; ++a) kl[a] = kg[ax[a]];
+  ggm_status st = make_desc(L, kl, gd);
+  if (st != GGM_OK) return st;
+  for (int a = 0; a < L; ++a) gd->off[a] = offg[ax[a]];
+  gd->off[L] = T;
+  gd->total = T;
+  return GGM_OK;
+}
+
 static int pick_J(int kin) { return kin <= 128 ? 4 : kin <= 256 ? 8 : kin <= 512 ? 16 : 32; }
 
 static size_t pass_smem(const GridDesc& gd) {
@@ -388,8 +407,8 @@ static int grid_blocks(const GridDesc& gd) {
 
 // Blocks for the cooperative solve: enough warps that each owns >= ~8 outer rows (a grid
 // barrier costs microseconds; small grids run in one block).
-static int solve_blocks(const GridDesc& gd) {
-  const double pts = (double)gd.rows * gd.k[gd.inner];
+static int solve_blocks(const GridDesc& gd, double extra_pts = 0.0) {
+  const double pts = (double)gd.rows * gd.k[gd.inner] + extra_pts;
   const int64_t want = (int64_t)std::ceil(pts / (kWarps * 8.0 * 32.0 * 16.0));
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, num_sms()));
 }
@@ -506,7 +525,9 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   if (hbad) return fail(GGM_ERR_DOMAIN, "E must be finite and > 0 (Thm 4, P:742)");
 
   SolveParams sp;
-  sp.gd = gd;
+  sp.gd[0] = gd;
+  sp.M = 1;
+  sp.T = gd.total;
   sp.E = E;
   sp.lam_out = lam_res;
   sp.g = g;
@@ -565,5 +586,174 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   if (!hstat[1])
     return fail(GGM_ERR_NO_CONVERGENCE, "no convergence in %d iterations (residual %.3e)",
                 o.max_iter, hres);
+  return GGM_OK;
+}
+
+// ------------------------------------------------------------------ multi-modal solve
+// Thm 2 with Σ_γ: NLL = ½ Σ_l E_l·λ_l − ½ Σ_γ Σ_{j∈grid γ} log s^γ_j, gradient
+// ½(E_l − Σ_{γ∋l} g^γ_l).  The majorise-minimise step is unchanged (one Jensen majoriser
+// per modality, summed): λ ← λ ⊙ (Σ_γ g^γ) / E, so the same persistent kernel runs with one
+// grid pass per modality per iteration.  Gauge (reading G2): shifts c with Σ_{l∈γ} c_l = 0
+// for every γ leave all grid sums unchanged; gauge 0 subtracts the G-component of the axis
+// minima (for one modality: the min-balanced gauge of ggm_solve_eigvals).
+extern "C" ggm_status ggm_solve_eigvals_multi(int A, const int* k, const double* E, int M,
+                                              const int* mod_ptr, const int* mod_axes,
+                                              const ggm_solve_opts* opts, double* lambda,
+                                              ggm_solve_info* info, void* stream) {
+  if (A < 1 || A > 64 || !k || !E || !lambda || !mod_ptr || !mod_axes)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "invalid axes / null pointer");
+  if (M < 1 || M > kMaxMods) return fail(GGM_ERR_INVALID_ARGUMENT, "M=%d not in [1,%d]", M, kMaxMods);
+  std::vector<int> offg(A + 1, 0), seen(A, 0);
+  for (int a = 0; a < A; ++a) {
+    if (k[a] < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "k[%d] < 1", a);
+    offg[a + 1] = offg[a] + k[a];
+  }
+  const int T = offg[A];
+  SolveParams sp;
+  memset(&sp, 0, sizeof(sp));
+  double pts = 0.0;
+  int J = 4;
+  for (int g = 0; g < M; ++g) {
+    const int L = mod_ptr[g + 1] - mod_ptr[g];
+    const int* ax = mod_axes + mod_ptr[g];
+    std::vector<int> here(A, 0);
+    for (int a = 0; a < L; ++a) {
+      if (ax[a] < 0 || ax[a] >= A) return fail(GGM_ERR_INVALID_ARGUMENT, "axis id out of range");
+      if (here[ax[a]]++) return fail(GGM_ERR_INVALID_ARGUMENT, "repeated axis in a modality (P:181)");
+      seen[ax[a]] = 1;
+    }
+    ggm_status st = make_desc_mod(L, ax, k, offg.data(), T, &sp.gd[g]);
+    if (st != GGM_OK) return st;
+    pts += (double)sp.gd[g].rows * sp.gd[g].k[sp.gd[g].inner];
+    J = std::max(J, pick_J(sp.gd[g].k[sp.gd[g].inner]));
+  }
+  for (int a = 0; a < A; ++a)
+    if (!seen[a]) return fail(GGM_ERR_INVALID_ARGUMENT, "axis %d occurs in no modality", a);
+  ggm_solve_opts o;
+  ggm_solve_opts_default(&o);
+  if (opts) o = *opts;
+  if (!(o.tol > 0.0) || o.max_iter < 0 || !(o.eps_scale >= 0.0))
+    return fail(GGM_ERR_INVALID_ARGUMENT, "invalid solve options");
+  if (o.method != 0)
+    return fail(GGM_ERR_UNSUPPORTED, "method %d not implemented on the GPU (use 0)", o.method);
+  if (o.gauge != 0 && o.gauge != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "gauge=%d", o.gauge);
+  sp.M = M;
+  sp.T = T;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = sizeof(double) * (5 * (size_t)T + 8) + 64;
+  DevBuf buf;
+  GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
+  double* lam_res = static_cast<double*>(buf.p);
+  double* g = lam_res + T;
+  double* gacc = g + T;
+  double* scal = gacc + 3 * (size_t)T;  // [1] logsum, [2] residual
+  int* istat = reinterpret_cast<int*>(scal + 4);
+  GGM_CUDA_TRY(cudaMemsetAsync(gacc, 0, sizeof(double) * (3 * (size_t)T + 8) + 64, s));
+  check_E<<<4, 256, 0, s>>>(E, T, istat + 3);
+  GGM_CUDA_TRY(cudaGetLastError());
+  int hbad = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hbad, istat + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hbad) return fail(GGM_ERR_DOMAIN, "E must be finite and > 0 (Thm 4, P:742)");
+  sp.E = E;
+  sp.lam_out = lam_res;
+  sp.g = g;
+  sp.gacc = gacc;
+  sp.status = istat;
+  sp.res_out = scal + 2;
+  sp.tol = o.tol;
+  sp.max_iter = o.max_iter;
+  const int nblk = solve_blocks(sp.gd[0], pts - (double)sp.gd[0].rows * sp.gd[0].k[sp.gd[0].inner]);
+  const size_t smem = (size_t)T * 2 * sizeof(double) + 16;
+  cudaError_t ce;
+  switch (J) {
+    case 4: ce = launch_solve<4>(sp, nblk, smem, s); break;
+    case 8: ce = launch_solve<8>(sp, nblk, smem, s); break;
+    case 16: ce = launch_solve<16>(sp, nblk, smem, s); break;
+    default: ce = launch_solve<32>(sp, nblk, smem, s); break;
+  }
+  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+  for (int m = 0; m < M; ++m) logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(sp.gd[m], lam_res, scal + 1);
+  GGM_CUDA_TRY(cudaGetLastError());
+  int hstat[2] = {0, 0};
+  double hscal[3] = {0, 0, 0};
+  std::vector<double> hL(T), hE(T);
+  GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(hL.data(), lam_res, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(hE.data(), E, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  // gauge space G = null(incidence): orthonormal basis R of the row space by Gram-Schmidt;
+  // P_G x = x - Σ_r (r·x) r
+  std::vector<std::vector<double>> R;
+  for (int gm = 0; gm < M; ++gm) {
+    std::vector<double> v(A, 0.0);
+    for (int q = mod_ptr[gm]; q < mod_ptr[gm + 1]; ++q) v[mod_axes[q]] = 1.0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (const auto& r : R) {
+        double dt = 0.0;
+        for (int a = 0; a < A; ++a) dt += r[a] * v[a];
+        for (int a = 0; a < A; ++a) v[a] -= dt * r[a];
+      }
+    double nv = 0.0;
+    for (double x : v) nv += x * x;
+    if (nv > 1e-20) {
+      nv = std::sqrt(nv);
+      for (double& x : v) x /= nv;
+      R.push_back(v);
+    }
+  }
+  auto proj_G = [&](const std::vector<double>& x) {
+    std::vector<double> y = x;
+    for (const auto& r : R) {
+      double dt = 0.0;
+      for (int a = 0; a < A; ++a) dt += r[a] * x[a];
+      for (int a = 0; a < A; ++a) y[a] -= dt * r[a];
+    }
+    return y;
+  };
+  std::vector<double> mins(A), tr(A, 0.0);
+  for (int a = 0; a < A; ++a) {
+    double mn = hL[offg[a]];
+    for (int i = offg[a]; i < offg[a + 1]; ++i) {
+      mn = std::min(mn, hL[i]);
+      tr[a] += hE[i];
+    }
+    mins[a] = mn;
+  }
+  const std::vector<double> shift = o.gauge == 0 ? proj_G(mins) : std::vector<double>(A, 0.0);
+  std::vector<double> out(T);
+  for (int a = 0; a < A; ++a)
+    for (int i = offg[a]; i < offg[a + 1]; ++i) out[i] = hL[i] - shift[a];
+  GGM_CUDA_TRY(cudaMemcpyAsync(lambda, out.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (info) {
+    double lin = 0.0, emax = 0.0;
+    for (int i = 0; i < T; ++i) {
+      lin += hE[i] * hL[i];
+      emax = std::max(emax, 1.0 / hE[i]);
+    }
+    double gmin = INFINITY;
+    for (int gm = 0; gm < M; ++gm) {
+      double sm = 0.0;
+      for (int q = mod_ptr[gm]; q < mod_ptr[gm + 1]; ++q) sm += mins[mod_axes[q]];
+      gmin = std::min(gmin, sm);
+    }
+    const std::vector<double> ptr = proj_G(tr);
+    double trmean = 0.0, ti = 0.0;
+    for (int a = 0; a < A; ++a) trmean += tr[a] / A;
+    for (int a = 0; a < A; ++a) ti = std::max(ti, std::fabs(ptr[a]));
+    info->iterations = hstat[0];
+    info->stationarity = hscal[2];
+    info->nll = 0.5 * lin - 0.5 * hscal[1];
+    info->grid_min = gmin;
+    info->floor_active = gmin <= o.eps_scale * emax ? 1 : 0;
+    info->trace_inconsistency = trmean > 0 ? ti / trmean : 0.0;
+  }
+  GGM_CUDA_TRY(cudaFreeAsync(buf.p, s));
+  buf.p = nullptr;
+  if (!hstat[1])
+    return fail(GGM_ERR_NO_CONVERGENCE, "no convergence in %d iterations (residual %.3e)",
+                o.max_iter, hscal[2]);
   return GGM_OK;
 }
