@@ -20,6 +20,10 @@ Pinning (tests/test_oracle_pins.py, ``-m "not gpu"``):
   canonical gauge           grid invariance; PSD; closed form on shifted inputs
   psi_rows / top_t / thr    dense V diag(λ) V^T + brute-force sort on tiny inputs;
                             rank-1 closed form; identity-factor all-tie case
+  nonparanormal (COCA)      the paper's worked example (ranks, Φ^-1 values, sparse part
+                            and z, P:983-1000; tests/golden/nonparanormal.json);
+                            invariance under strictly increasing maps; row values are
+                            the Φ^-1(r/(n+1)) of a rank multiset
   *_multi (shared axes)     one modality = the single-modality functions; disjoint
                             modalities = independent solves; dense multi-modal NLL and
                             the dense stationarity Σ_γ sb-trace[(⊕_γΨ)^-1] = S_l
@@ -41,6 +45,7 @@ __all__ = [
     "wald_edge", "wald_threshold", "overall_edges", "edges_to_symmetric_csr",
     "gram_eig_multi", "grid_sums_multi", "marginals_multi", "nll_multi", "gradient_multi",
     "stationarity_multi", "gauge_space_multi", "canonical_gauge_multi", "solve_eigvals_multi",
+    "nonparanormal", "nonparanormal_sparse_split", "gram_eig_nonparanormal",
 ]
 
 
@@ -300,6 +305,46 @@ def paper_gd_solve(E, max_iter: int = 200000, tol: float = 1e-9, eps_scale: floa
         lams, f = cand, fc
         it += 1
     return lams, dict(iterations=it, stationarity=stationarity(E, lams))
+
+
+# ---------------------------------------------------------------------------
+# Nonparanormal skeptic via COCA and the sparse rank-one form
+# ---------------------------------------------------------------------------
+
+def nonparanormal(x: np.ndarray, axis: int) -> np.ndarray:
+    """COCA transform of mat_l[D] ("replacing D_l with its ranks, mapping them to a
+    normal distribution"): each row i (all entries with l-index i) is ranked, ties sharing
+    the smallest rank (reading Q19, as in the worked example P:983-996), and r -> Φ^-1(r /
+    (n + 1)) with n = d_\l.  Returns the transformed d_l x d_\l matrix (fp64)."""
+    from scipy.special import ndtri
+    from scipy.stats import rankdata
+    m = matricize(x, axis)
+    r = rankdata(m, method="min", axis=1)
+    return ndtri(r / (m.shape[1] + 1.0))
+
+
+def nonparanormal_sparse_split(x: np.ndarray, axis: int):
+    """The sparse rank-one form: nonparanormal(x) = S + z 1^T, where z_i is the
+    value the zeros of row i map to and S is zero wherever mat_l[D] is ("the same
+    sparsity structure as our original data").  Returns (S, z); rows without zeros get
+    z_i = 0."""
+    m = matricize(x, axis)
+    t = nonparanormal(x, axis)
+    zero = m == 0
+    z = np.array([t[i, zero[i]][0] if zero[i].any() else 0.0 for i in range(m.shape[0])])
+    S = np.where(zero, 0.0, t - z[:, None])
+    return S, z
+
+
+def gram_eig_nonparanormal(x: np.ndarray, axis: int, k: int):
+    """Top-k left singular vectors / σ² of the COCA-transformed mat_l."""
+    t = nonparanormal(x, axis)
+    if not 1 <= k <= min(t.shape):
+        raise RankError(f"k={k} not in [1, {min(t.shape)}] (S:116)")
+    u, sig, _ = np.linalg.svd(t, full_matrices=False)
+    e = sig ** 2
+    _check_rank(e, k)
+    return u[:, :k].copy(), e[:k].copy()
 
 
 # ---------------------------------------------------------------------------

@@ -460,3 +460,40 @@ def test_multi_gauge_space_and_canonical_invariance():
     single = O.canonical_gauge_multi(lam, [[0, 1, 2]])
     for x, y in zip(single, O.canonical_gauge(lam)):
         assert np.allclose(x, y, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- nonparanormal (COCA)
+
+def test_nonparanormal_paper_example():
+    """ranks, Φ^-1(r/6) values and the sparse part + z 1^T, to the paper's
+    printed 2 decimals."""
+    with open(os.path.join(GOLD, "nonparanormal.json")) as f:
+        g = json.load(f)
+    X = np.array(g["data"], dtype=np.float64)
+    from scipy.stats import rankdata
+    assert np.array_equal(rankdata(X, method="min", axis=1), np.array(g["ranks"]))
+    T = O.nonparanormal(X, 0)
+    assert np.allclose(np.round(T, 2), g["normal"], atol=1e-12)
+    S, z = O.nonparanormal_sparse_split(X, 0)
+    assert np.allclose(np.round(S, 2), g["sparse_part"], atol=0.011)
+    assert np.allclose(np.round(z, 2), g["z"], atol=1e-12)
+    assert np.array_equal(S == 0, X == 0)
+    assert np.allclose(S + z[:, None], T, atol=1e-15)
+
+
+def test_nonparanormal_invariances():
+    """Copula invariance: strictly increasing maps of the data leave the transform unchanged;
+    with no ties every row holds exactly the values Φ^-1(r/(n+1)), r = 1..n."""
+    from scipy.special import ndtri
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((7, 5, 6))
+    for ax in range(3):
+        a = O.nonparanormal(X, ax)
+        b = O.nonparanormal(np.exp(3.0 * X) + 2.0, ax)
+        assert np.allclose(a, b, atol=1e-14)
+        n = a.shape[1]
+        want = ndtri(np.arange(1, n + 1) / (n + 1.0))
+        assert np.allclose(np.sort(a, axis=1), np.broadcast_to(want, a.shape), atol=1e-14)
+    V, E = O.gram_eig_nonparanormal(X, 1, 5)
+    T = O.nonparanormal(X, 1)
+    assert np.allclose(np.sort(np.linalg.eigvalsh(T @ T.T))[::-1][:5], E, rtol=1e-12)
