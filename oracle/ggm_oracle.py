@@ -315,7 +315,8 @@ def nonparanormal(x: np.ndarray, axis: int) -> np.ndarray:
     """COCA transform of mat_l[D] ("replacing D_l with its ranks, mapping them to a
     normal distribution"): each row i (all entries with l-index i) is ranked, ties sharing
     the smallest rank (reading Q19, as in the worked example P:983-996), and r -> Φ^-1(r /
-    (n + 1)) with n = d_\l.  Returns the transformed d_l x d_\l matrix (fp64)."""
+    (n + 1)) with n = d_rest (the product of the other axes).  Returns the transformed
+    d_l x d_rest matrix (fp64)."""
     from scipy.special import ndtri
     from scipy.stats import rankdata
     m = matricize(x, axis)
