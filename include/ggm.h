@@ -113,6 +113,29 @@ ggm_status ggm_gram_eig_multi(int M, const float *const *X, const int *ndim,
                               double *E, double *trace_S, void *workspace,
                               size_t workspace_bytes, void *stream);
 
+/* (1d) Sparse unfolding (§8(f) rows 1 and 4).  D_l given as CSR: d rows (the
+ * axis), m columns, nnz stored entries (row_ptr int64 d+1, col int32, val fp32; DEVICE).
+ * Randomized subspace iteration (as (1b)) with cuSPARSE SpMM products, never densified.
+ * nonparanormal = 1 applies the COCA transform first (row ranks among all m
+ * entries incl. the implicit zeros, ties -> smallest rank, Φ^-1(r/(m+1))) in its sparse
+ * rank-one form S + z 1^T (S keeps D's pattern): the operator products add the
+ * rank-one terms z (1^T X) and 1 (z^T Y) instead of a rank-one SVD update.  Output as
+ * ggm_gram_eig; trace_S = ||A||_F^2 of the (transformed) matrix.  Synchronizes `stream`. */
+ggm_status ggm_gram_eig_csr_workspace(int64_t d, int64_t m, int64_t nnz, int k, int oversample,
+                                      size_t *bytes);
+ggm_status ggm_gram_eig_csr(int64_t d, int64_t m, int64_t nnz, const int64_t *row_ptr,
+                            const int32_t *col, const float *val, int k, int nonparanormal,
+                            int oversample, int max_iter, double tol, uint64_t seed, float *V,
+                            double *E, double *trace_S, int *iters_out, double *change_out,
+                            void *workspace, size_t workspace_bytes, void *stream);
+
+/* (1e) Dense nonparanormal skeptic / COCA: out (same shape and layout as X) =
+ * Φ^-1(r/(m+1)), r = rank of the entry (ties -> smallest rank, reading Q19) among the
+ * m = d_rest entries with the same index on `axis`.  Feed `out` to ggm_gram_eig(axis). */
+ggm_status ggm_nonparanormal_workspace(int ndim, const int64_t *shape, int axis, size_t *bytes);
+ggm_status ggm_nonparanormal(const float *X, int ndim, const int64_t *shape, int axis, float *out,
+                             void *workspace, size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------------------------
  * (2) Eigenvalue MLE — Theorem 2, Algorithm 1 lines 5-17.
  *

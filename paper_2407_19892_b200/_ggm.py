@@ -37,6 +37,8 @@ EXPORTED = [
     "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
     "ggm_overall_last_path",
     "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
+    "ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
+    "ggm_nonparanormal",
 ]
 
 
@@ -135,7 +137,14 @@ def lib() -> C.CDLL:
                                           C.POINTER(i32), C.POINTER(SolveOpts), vp,
                                           C.POINTER(SolveInfo), vp]
     L.ggm_overall_last_path.restype = i32
-    for name in ("ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
+    L.ggm_gram_eig_csr_workspace.argtypes = [i64, i64, i64, i32, i32, C.POINTER(C.c_size_t)]
+    L.ggm_gram_eig_csr.argtypes = [i64, i64, i64, vp, vp, vp, i32, i32, i32, i32, C.c_double,
+                                   C.c_uint64, vp, vp, C.POINTER(C.c_double), C.POINTER(i32),
+                                   C.POINTER(C.c_double), vp, C.c_size_t, vp]
+    L.ggm_nonparanormal_workspace.argtypes = [i32, C.POINTER(i64), i32, C.POINTER(C.c_size_t)]
+    L.ggm_nonparanormal.argtypes = [vp, i32, C.POINTER(i64), i32, vp, vp, C.c_size_t, vp]
+    for name in ("ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
+                 "ggm_nonparanormal", "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
                  "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
                  "ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
                  "ggm_gram_eig_rsi_workspace", "ggm_gram_eig_rsi",
@@ -250,6 +259,45 @@ def ggm_gram_eig_multi(tensors, axis_pos, k: int, stream=None):
     _check(lib().ggm_gram_eig_multi(M, ptrs, ndim, shapes, pos, int(k), _ptr(V), _ptr(E),
                                     C.byref(tr), _ptr(ws), nbytes.value, _stream(stream)))
     return V, E, tr.value
+
+
+def ggm_gram_eig_csr(row_ptr: torch.Tensor, col: torch.Tensor, val: torch.Tensor, m: int, k: int,
+                     nonparanormal: bool = False, oversample: int = 0, max_iter: int = 200,
+                     tol: float = 1e-13, seed: int = 0x2407198920240728, stream=None):
+    """Spectrum of a sparse unfolding given as CSR (d = len(row_ptr) - 1 rows, m columns),
+    optionally COCA-transformed in its sparse + rank-one form (include/ggm.h (1d)).
+    Returns (V, E, trace, iterations, last Ritz change)."""
+    _require_cuda(row_ptr, torch.int64, "row_ptr")
+    _require_cuda(col, torch.int32, "col")
+    _require_cuda(val, torch.float32, "val")
+    d = row_ptr.numel() - 1
+    nnz = val.numel()
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_gram_eig_csr_workspace(d, int(m), nnz, int(k), int(oversample),
+                                            C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=val.device)
+    V = torch.empty((d, k), dtype=torch.float32, device=val.device)
+    E = torch.empty((k,), dtype=torch.float64, device=val.device)
+    tr, it, ch = C.c_double(0.0), C.c_int(0), C.c_double(0.0)
+    _check(lib().ggm_gram_eig_csr(d, int(m), nnz, _ptr(row_ptr), _ptr(col), _ptr(val), int(k),
+                                  int(bool(nonparanormal)), int(oversample), int(max_iter),
+                                  float(tol), C.c_uint64(seed), _ptr(V), _ptr(E), C.byref(tr),
+                                  C.byref(it), C.byref(ch), _ptr(ws), nbytes.value,
+                                  _stream(stream)))
+    return V, E, tr.value, it.value, ch.value
+
+
+def ggm_nonparanormal(X: torch.Tensor, axis: int, stream=None) -> torch.Tensor:
+    """COCA transform of X for `axis` (include/ggm.h (1e)); same shape as X."""
+    _require_cuda(X, torch.float32, "X")
+    shape = (C.c_int64 * X.dim())(*X.shape)
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_nonparanormal_workspace(X.dim(), shape, int(axis), C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=X.device)
+    out = torch.empty_like(X)
+    _check(lib().ggm_nonparanormal(_ptr(X), X.dim(), shape, int(axis), _ptr(out), _ptr(ws),
+                                   nbytes.value, _stream(stream)))
+    return out
 
 
 # --------------------------------------------------------------------------- (2) solve

@@ -14,6 +14,9 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <cusparse.h>
+
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -276,9 +279,9 @@ struct RWork {
   double *M, *Om, *Y, *T, *w, *work, *tau, *V64, *fro, *Ek, *Wk;
   int* info;
 };
-static size_t rcarve(const RPlan& rp, void* ws, RWork* w) {
+static size_t rcarve(const RPlan& rp, void* ws, RWork* w, bool dense_M = true) {
   Carve c(ws);
-  w->M = c.take<double>((size_t)rp.d * rp.m);
+  w->M = c.take<double>(dense_M ? (size_t)rp.d * rp.m : 0);
   w->Om = c.take<double>((size_t)rp.m * rp.r);  // Omega, then Z = M^T Q
   w->Y = c.take<double>((size_t)rp.d * rp.r);   // Y = M Z, then Q
   w->T = c.take<double>((size_t)rp.r * rp.r);
@@ -357,12 +360,41 @@ extern "C" ggm_status ggm_gram_eig_rsi(const float* X, int ndim, const int64_t* 
   return rsi_core(rp, w, max_iter, tol, seed, V, E, trace_S, iters_out, change_out, hb, hs, s);
 }
 
+template <class FA, class FAt>
+static ggm_status rsi_generic(const RPlan& rp, const RWork& w, FA applyA, FAt applyAt,
+                              int max_iter, double tol, uint64_t seed, float* V, double* E,
+                              double* trace_S, int* iters_out, double* change_out,
+                              cublasHandle_t hb, cusolverDnHandle_t hs, cudaStream_t s);
+
 // Randomized subspace iteration on the unfolding already in w.M (d x m column-major) and its
 // squared Frobenius norm in w.fro.
 static ggm_status rsi_core(const RPlan& rp, const RWork& w, int max_iter, double tol,
                            uint64_t seed, float* V, double* E, double* trace_S, int* iters_out,
                            double* change_out, cublasHandle_t hb, cusolverDnHandle_t hs,
                            cudaStream_t s) {
+  const int d = (int)rp.d, m = (int)rp.m, r = rp.r;
+  const double one = 1.0, zero = 0.0;
+  auto applyA = [&](const double* in, double* out) -> bool {  // out (d x r) = M in (m x r)
+    return cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, d, r, m, &one, w.M, d, in, m, &zero, out,
+                       d) == CUBLAS_STATUS_SUCCESS;
+  };
+  auto applyAt = [&](const double* in, double* out) -> bool {  // out (m x r) = M^T in (d x r)
+    return cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, r, d, &one, w.M, d, in, d, &zero, out,
+                       m) == CUBLAS_STATUS_SUCCESS;
+  };
+  return rsi_generic(rp, w, applyA, applyAt, max_iter, tol, seed, V, E, trace_S, iters_out,
+                     change_out, hb, hs, s);
+}
+
+// Randomized subspace iteration for an implicit operator A (d x m): applyA(in, out) computes
+// out = A in (in m x r, out d x r), applyAt(in, out) out = A^T in; all column-major fp64.
+// ||A||_F^2 is expected in w.fro.  Range finder Y = A Ω, then per iteration Rayleigh-Ritz
+// (Z = A^T Q, T = Z^T Z = Q^T A A^T Q, DSYEVD) and a power step Q = orth(A Z).
+template <class FA, class FAt>
+static ggm_status rsi_generic(const RPlan& rp, const RWork& w, FA applyA, FAt applyAt,
+                              int max_iter, double tol, uint64_t seed, float* V, double* E,
+                              double* trace_S, int* iters_out, double* change_out,
+                              cublasHandle_t hb, cusolverDnHandle_t hs, cudaStream_t s) {
   const int sms = num_sms();
   const int d = (int)rp.d, m = (int)rp.m, r = rp.r, kk = rp.k;
   ggm_status st = GGM_OK;
@@ -376,22 +408,19 @@ static ggm_status rsi_core(const RPlan& rp, const RWork& w, int max_iter, double
       return fail(GGM_ERR_CUDA, "cuSOLVER QR failed");
     return GGM_OK;
   };
-  // range finder: Y = M Omega, Q = orth(Y)
-  if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, d, r, m, &one, w.M, d, w.Om, m, &zero, w.Y, d) !=
-      CUBLAS_STATUS_SUCCESS)
-    return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+  // range finder: Y = A Omega, Q = orth(Y)
+  if (!applyA(w.Om, w.Y)) return fail(GGM_ERR_CUDA, "operator product A Omega failed");
   st = orth(w.Y);
   if (st != GGM_OK) return st;
   std::vector<double> prev(kk, 0.0), cur(kk);
   int it = 0;
   double change = INFINITY;
   for (it = 1; it <= max_iter; ++it) {
-    // Rayleigh-Ritz on span(Q): Z = M^T Q (m x r), T = Z^T Z = Q^T S Q (r x r)
-    if (cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, r, d, &one, w.M, d, w.Y, d, &zero, w.Om, m) !=
-            CUBLAS_STATUS_SUCCESS ||
+    // Rayleigh-Ritz on span(Q): Z = A^T Q (m x r), T = Z^T Z = Q^T S Q (r x r)
+    if (!applyAt(w.Y, w.Om) ||
         cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, r, m, &one, w.Om, m, &zero, w.T, r) !=
             CUBLAS_STATUS_SUCCESS)
-      return fail(GGM_ERR_CUDA, "cuBLAS Rayleigh-Ritz failed");
+      return fail(GGM_ERR_CUDA, "Rayleigh-Ritz products failed");
     if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, r, w.T, r, w.w,
                          w.work, rp.lw_syevd, w.info) != CUSOLVER_STATUS_SUCCESS)
       return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed");
@@ -403,10 +432,8 @@ static ggm_status rsi_core(const RPlan& rp, const RWork& w, int max_iter, double
       change = std::max(change, std::fabs(cur[c] - prev[c]) / std::max(std::fabs(cur[0]), 1e-300));
     prev = cur;
     if (change <= tol || r >= std::min(d, m) || it == max_iter) break;
-    // power step: Y = M Z = S Q, Q = orth(Y)
-    if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, d, r, m, &one, w.M, d, w.Om, m, &zero, w.Y, d) !=
-        CUBLAS_STATUS_SUCCESS)
-      return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+    // power step: Y = A Z = S Q, Q = orth(Y)
+    if (!applyA(w.Om, w.Y)) return fail(GGM_ERR_CUDA, "operator product A Z failed");
     st = orth(w.Y);
     if (st != GGM_OK) return st;
   }
@@ -694,4 +721,373 @@ extern "C" ggm_status ggm_gram_eig_multi(int M, const float* const* X, const int
   st = unfold_all(Md, fro);
   if (st != GGM_OK) return st;
   return dense_core(g, lwork, Md, S, w, work, dinfo, V64, fro, Ek, Vasc, V, E, trace_S, hb, hs, s);
+}
+
+// ------------------------------------------------------------------ sparse unfoldings (CSR)
+// §8(f) row 1 (sparse inputs) and row 4 (nonparanormal skeptic, sparse rank-one trick,
+// P:965-1016).  The unfolding D_l is given as CSR (d rows = the axis, m columns).  With the
+// COCA transform the data become S + z 1^T (S with D's sparsity pattern, z_i the value the
+// zeros of row i map to); instead of a rank-one SVD update the randomized
+// subspace iteration applies the operator implicitly: A X = S X + z (1^T X),
+// A^T Y = S^T Y + 1 (z^T Y) — the matrix is never densified.
+namespace {
+
+struct SparseHandle {
+  cusparseHandle_t h = nullptr;
+  ~SparseHandle() {
+    if (h) cusparseDestroy(h);
+  }
+};
+thread_local SparseHandle g_sparse;
+
+__device__ __forceinline__ float canon_zero(float x) { return x == 0.f ? 0.f : x; }
+
+__global__ void copy_canon(const float* __restrict__ v, int64_t n, float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = canon_zero(v[i]);
+}
+
+// first position in sorted[lo, hi) with sorted[p] >= x
+__device__ __forceinline__ int64_t lower_bound_f(const float* sorted, int64_t lo, int64_t hi,
+                                                 float x) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sorted[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// One warp per row: COCA values of the stored entries (rank = 1 + #entries < x, the row's
+// implicit zeros counted when x > 0; Φ^-1(r/(m+1))), z_i for the zeros, S = value - z_i,
+// and ||S + z 1^T||_F^2.  np = 0: S = val, z = 0.
+__global__ void csr_values(const int64_t* __restrict__ rp, const float* __restrict__ val,
+                           const float* __restrict__ sorted, int64_t d, int64_t m, int np,
+                           double* __restrict__ sval, double* __restrict__ z,
+                           double* __restrict__ fro) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < d;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = rp[i], e = rp[i + 1];
+    const int64_t implicit0 = m - (e - b);
+    double zi = 0.0;
+    if (np) {
+      const int64_t neg = lower_bound_f(sorted, b, e, 0.f) - b;  // stored entries < 0
+      const bool has_zero = implicit0 > 0 || (neg < e - b && sorted[b + neg] == 0.f);
+      zi = has_zero ? normcdfinv((double)(neg + 1) / (double)(m + 1)) : 0.0;
+    }
+    for (int64_t q = b + lane; q < e; q += 32) {
+      const float x = canon_zero(val[q]);
+      double v;
+      if (np) {
+        const int64_t less = lower_bound_f(sorted, b, e, x) - b + (x > 0.f ? implicit0 : 0);
+        v = normcdfinv((double)(less + 1) / (double)(m + 1)) - zi;
+        if (x == 0.f) v = 0.0;  // explicit zeros keep the pattern
+      } else {
+        v = (double)x;
+      }
+      sval[q] = v;
+      acc += (v + zi) * (v + zi);
+    }
+    if (lane == 0) {
+      z[i] = zi;
+      acc += (double)implicit0 * zi * zi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) atomicAdd(fro, acc);
+}
+
+__global__ void fill_f64(double* p, int64_t n, double v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void rp_to_i32(const int64_t* rp, int64_t n, int32_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)rp[i];
+}
+__global__ void col_to_i64(const int32_t* c, int64_t n, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = c[i];
+}
+
+struct CsrWork {
+  double *sval, *z, *ones, *cs, *zq;
+  float *canon, *sorted;
+  int32_t* rp32;
+  int64_t* col64;
+  void* cub;
+  size_t cub_bytes;
+};
+size_t csr_carve(int64_t d, int64_t m, int64_t nnz, int r, bool idx32, size_t cub_bytes,
+                 void* ws, CsrWork* w) {
+  Carve c(ws);
+  w->sval = c.take<double>(nnz);
+  w->z = c.take<double>(d);
+  w->ones = c.take<double>(m);
+  w->cs = c.take<double>(r);
+  w->zq = c.take<double>(r);
+  w->canon = c.take<float>(nnz);
+  w->sorted = c.take<float>(nnz);
+  w->rp32 = c.take<int32_t>(idx32 ? d + 1 : 0);
+  w->col64 = c.take<int64_t>(idx32 ? 0 : nnz);
+  w->cub = c.take<char>(cub_bytes);
+  w->cub_bytes = cub_bytes;
+  return c.used();
+}
+size_t csr_sort_bytes(int64_t d, int64_t nnz) {
+  size_t b = 0;
+  cub::DeviceSegmentedSort::SortKeys(nullptr, b, (const float*)nullptr, (float*)nullptr, nnz,
+                                     d, (const int64_t*)nullptr, (const int64_t*)nullptr);
+  return b;
+}
+
+ggm_status csr_plan(int64_t d, int64_t m, int64_t nnz, int k, int oversample, RPlan* rp) {
+  if (d < 1 || m < 1 || nnz < 0) return fail(GGM_ERR_INVALID_ARGUMENT, "d, m >= 1, nnz >= 0");
+  const int64_t shape2[2] = {d, m};
+  return make_rplan(2, shape2, 0, k, oversample, rp);
+}
+
+}  // namespace
+
+extern "C" ggm_status ggm_gram_eig_csr_workspace(int64_t d, int64_t m, int64_t nnz, int k,
+                                                 int oversample, size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  RPlan rp;
+  ggm_status st = csr_plan(d, m, nnz, k, oversample, &rp);
+  if (st != GGM_OK) return st;
+  RWork w;
+  size_t b = rcarve(rp, nullptr, &w, false);
+  b = (b + 255) / 256 * 256;
+  const bool idx32 = nnz < INT32_MAX && d < INT32_MAX;
+  CsrWork cw;
+  *bytes = b + csr_carve(d, m, nnz, rp.r, idx32, csr_sort_bytes(d, nnz), nullptr, &cw);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_gram_eig_csr(int64_t d, int64_t m, int64_t nnz, const int64_t* row_ptr,
+                                       const int32_t* col, const float* val, int k,
+                                       int nonparanormal, int oversample, int max_iter,
+                                       double tol, uint64_t seed, float* V, double* E,
+                                       double* trace_S, int* iters_out, double* change_out,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (!row_ptr || (nnz > 0 && (!col || !val)) || !V || !E || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  if (max_iter < 1 || !(tol >= 0.0)) return fail(GGM_ERR_INVALID_ARGUMENT, "max_iter/tol invalid");
+  RPlan rp;
+  ggm_status st = csr_plan(d, m, nnz, k, oversample, &rp);
+  if (st != GGM_OK) return st;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  RWork w;
+  size_t b0 = rcarve(rp, workspace, &w, false);
+  b0 = (b0 + 255) / 256 * 256;
+  const bool idx32 = nnz < INT32_MAX && d < INT32_MAX;
+  CsrWork cw;
+  const size_t need = b0 + csr_carve(d, m, nnz, rp.r, idx32, csr_sort_bytes(d, nnz),
+                                     static_cast<char*>(workspace) + b0, &cw);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  if (!g_sparse.h && cusparseCreate(&g_sparse.h) != CUSPARSE_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusparseCreate failed");
+  cusparseSetStream(g_sparse.h, s);
+  const int sms = num_sms();
+  auto grid_of = [&](int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, sms * 8));
+  };
+  // (1) values of S (COCA-transformed or raw), z, ||A||_F^2
+  GGM_CUDA_TRY(cudaMemsetAsync(w.fro, 0, sizeof(double), s));
+  if (nnz > 0) {
+    copy_canon<<<grid_of(nnz), 256, 0, s>>>(val, nnz, cw.canon);
+    if (nonparanormal) {
+      size_t tb = cw.cub_bytes;
+      GGM_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(cw.cub, tb, cw.canon, cw.sorted, nnz, d,
+                                                      row_ptr, row_ptr + 1, s));
+    }
+  }
+  csr_values<<<grid_of(32 * d), 256, 0, s>>>(row_ptr, cw.canon, cw.sorted, d, m,
+                                              nonparanormal ? 1 : 0, cw.sval, cw.z, w.fro);
+  fill_f64<<<grid_of(m), 256, 0, s>>>(cw.ones, m, 1.0);
+  GGM_CUDA_TRY(cudaGetLastError());
+  // (2) cuSPARSE descriptors
+  const void* rpp = row_ptr;
+  const void* colp = col;
+  if (idx32) {
+    rp_to_i32<<<grid_of(d + 1), 256, 0, s>>>(row_ptr, d + 1, cw.rp32);
+    rpp = cw.rp32;
+  } else {
+    col_to_i64<<<grid_of(nnz), 256, 0, s>>>(col, nnz, cw.col64);
+    colp = cw.col64;
+  }
+  GGM_CUDA_TRY(cudaGetLastError());
+  const cusparseIndexType_t it = idx32 ? CUSPARSE_INDEX_32I : CUSPARSE_INDEX_64I;
+  cusparseSpMatDescr_t A = nullptr;
+  if (cusparseCreateCsr(&A, d, m, nnz, const_cast<void*>(rpp), const_cast<void*>(colp), cw.sval,
+                        it, it, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F) != CUSPARSE_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusparseCreateCsr failed");
+  const int r = rp.r;
+  cusparseDnMatDescr_t Xm = nullptr, Yd = nullptr, Xd = nullptr, Ym = nullptr;
+  cusparseCreateDnMat(&Xm, m, r, m, w.Om, CUDA_R_64F, CUSPARSE_ORDER_COL);  // m x r operand
+  cusparseCreateDnMat(&Yd, d, r, d, w.Y, CUDA_R_64F, CUSPARSE_ORDER_COL);   // d x r
+  const double one = 1.0, zero = 0.0;
+  size_t bN = 0, bT = 0;
+  cusparseSpMM_bufferSize(g_sparse.h, CUSPARSE_OPERATION_NON_TRANSPOSE,
+                          CUSPARSE_OPERATION_NON_TRANSPOSE, &one, A, Xm, &zero, Yd, CUDA_R_64F,
+                          CUSPARSE_SPMM_ALG_DEFAULT, &bN);
+  cusparseSpMM_bufferSize(g_sparse.h, CUSPARSE_OPERATION_TRANSPOSE,
+                          CUSPARSE_OPERATION_NON_TRANSPOSE, &one, A, Yd, &zero, Xm, CUDA_R_64F,
+                          CUSPARSE_SPMM_ALG_DEFAULT, &bT);
+  void* spbuf = nullptr;
+  GGM_CUDA_TRY(cudaMallocAsync(&spbuf, std::max<size_t>(std::max(bN, bT), 256), s));
+  auto cleanup = [&]() {
+    cusparseDestroySpMat(A);
+    cusparseDestroyDnMat(Xm);
+    cusparseDestroyDnMat(Yd);
+    cudaFreeAsync(spbuf, s);
+  };
+  (void)Xd;
+  (void)Ym;
+  // operator products: the RSI buffers are fixed (Om: m x r, Y: d x r), so the descriptors
+  // are bound to them; applyA reads Om and writes Y, applyAt reads Y and writes Om
+  auto applyA = [&](const double* in, double* out) -> bool {  // Y = S Om + z (1^T Om)
+    if (in != w.Om || out != w.Y) return false;
+    if (cusparseSpMM(g_sparse.h, CUSPARSE_OPERATION_NON_TRANSPOSE,
+                     CUSPARSE_OPERATION_NON_TRANSPOSE, &one, A, Xm, &zero, Yd, CUDA_R_64F,
+                     CUSPARSE_SPMM_ALG_DEFAULT, spbuf) != CUSPARSE_STATUS_SUCCESS)
+      return false;
+    if (!nonparanormal) return true;
+    return cublasDgemv(hb, CUBLAS_OP_T, (int)m, r, &one, w.Om, (int)m, cw.ones, 1, &zero, cw.cs,
+                       1) == CUBLAS_STATUS_SUCCESS &&
+           cublasDger(hb, (int)d, r, &one, cw.z, 1, cw.cs, 1, w.Y, (int)d) == CUBLAS_STATUS_SUCCESS;
+  };
+  auto applyAt = [&](const double* in, double* out) -> bool {  // Om = S^T Y + 1 (z^T Y)
+    if (in != w.Y || out != w.Om) return false;
+    if (cusparseSpMM(g_sparse.h, CUSPARSE_OPERATION_TRANSPOSE, CUSPARSE_OPERATION_NON_TRANSPOSE,
+                     &one, A, Yd, &zero, Xm, CUDA_R_64F, CUSPARSE_SPMM_ALG_DEFAULT,
+                     spbuf) != CUSPARSE_STATUS_SUCCESS)
+      return false;
+    if (!nonparanormal) return true;
+    return cublasDgemv(hb, CUBLAS_OP_T, (int)d, r, &one, w.Y, (int)d, cw.z, 1, &zero, cw.zq,
+                       1) == CUBLAS_STATUS_SUCCESS &&
+           cublasDger(hb, (int)m, r, &one, cw.ones, 1, cw.zq, 1, w.Om, (int)m) ==
+               CUBLAS_STATUS_SUCCESS;
+  };
+  st = rsi_generic(rp, w, applyA, applyAt, max_iter, tol, seed, V, E, trace_S, iters_out,
+                   change_out, hb, hs, s);
+  cleanup();
+  return st;
+}
+
+// ------------------------------------------------------------------ dense COCA transform
+// ggm_nonparanormal: every entry of the tensor is replaced by Φ^-1(r / (m + 1)), r = its
+// rank (ties -> smallest rank, reading Q19) among the m = d_rest entries sharing its index
+// on `axis` (the row of mat_axis); output in the input's own layout, so the
+// transformed tensor feeds ggm_gram_eig for that axis unchanged.
+namespace {
+__global__ void unfold_rows_f32(const float* __restrict__ X, int64_t pre_n, int64_t d,
+                                int64_t post_n, float* __restrict__ rows) {
+  const int64_t total = pre_n * d * post_n;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t post = idx % post_n, i = (idx / post_n) % d, pre = idx / (post_n * d);
+    rows[i * (pre_n * post_n) + pre * post_n + post] = canon_zero(X[idx]);
+  }
+}
+__global__ void row_offsets(int64_t d, int64_t m, int64_t* off) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= d;
+       i += (int64_t)gridDim.x * blockDim.x)
+    off[i] = i * m;
+}
+__global__ void coca_dense(const float* __restrict__ X, const float* __restrict__ sorted,
+                           int64_t pre_n, int64_t d, int64_t post_n, float* __restrict__ out) {
+  const int64_t total = pre_n * d * post_n, m = pre_n * post_n;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = (idx / post_n) % d;
+    const int64_t less = lower_bound_f(sorted, i * m, (i + 1) * m, canon_zero(X[idx])) - i * m;
+    out[idx] = (float)normcdfinv((double)(less + 1) / (double)(m + 1));
+  }
+}
+ggm_status np_shape(int ndim, const int64_t* shape, int axis, int64_t* pre, int64_t* d,
+                    int64_t* post) {
+  if (ndim < 1 || !shape || axis < 0 || axis >= ndim)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "ndim/shape/axis invalid");
+  *pre = 1;
+  *post = 1;
+  for (int a = 0; a < ndim; ++a) {
+    if (shape[a] < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "shape[%d] < 1", a);
+    if (a < axis) *pre *= shape[a];
+    if (a > axis) *post *= shape[a];
+  }
+  *d = shape[axis];
+  return GGM_OK;
+}
+size_t np_carve(int64_t d, int64_t n, void* ws, float** rows, float** sorted, int64_t** off,
+                void** cub, size_t* cub_bytes) {
+  size_t b = 0;
+  cub::DeviceSegmentedSort::SortKeys(nullptr, b, (const float*)nullptr, (float*)nullptr, n, d,
+                                     (const int64_t*)nullptr, (const int64_t*)nullptr);
+  Carve c(ws);
+  *rows = c.take<float>(n);
+  *sorted = c.take<float>(n);
+  *off = c.take<int64_t>(d + 1);
+  *cub = c.take<char>(b);
+  *cub_bytes = b;
+  return c.used();
+}
+}  // namespace
+
+extern "C" ggm_status ggm_nonparanormal_workspace(int ndim, const int64_t* shape, int axis,
+                                                  size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  int64_t pre, d, post;
+  ggm_status st = np_shape(ndim, shape, axis, &pre, &d, &post);
+  if (st != GGM_OK) return st;
+  float *a, *b;
+  int64_t* o;
+  void* c;
+  size_t cb;
+  *bytes = np_carve(d, pre * d * post, nullptr, &a, &b, &o, &c, &cb);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_nonparanormal(const float* X, int ndim, const int64_t* shape, int axis,
+                                        float* out, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
+  if (!X || !out || !workspace) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  int64_t pre, d, post;
+  ggm_status st = np_shape(ndim, shape, axis, &pre, &d, &post);
+  if (st != GGM_OK) return st;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  const int64_t n = pre * d * post;
+  float *rows, *sorted;
+  int64_t* off;
+  void* cub;
+  size_t cb;
+  const size_t need = np_carve(d, n, workspace, &rows, &sorted, &off, &cub, &cb);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 16));
+  unfold_rows_f32<<<grid, 256, 0, s>>>(X, pre, d, post, rows);
+  row_offsets<<<(int)std::min<int64_t>((d + 256) / 256, 1024), 256, 0, s>>>(d, pre * post, off);
+  GGM_CUDA_TRY(cudaGetLastError());
+  GGM_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(cub, cb, rows, sorted, n, d, off, off + 1, s));
+  coca_dense<<<grid, 256, 0, s>>>(X, sorted, pre, d, post, out);
+  GGM_CUDA_TRY(cudaGetLastError());
+  return GGM_OK;
 }

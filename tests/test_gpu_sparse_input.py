@@ -1,0 +1,109 @@
+"""GPU parity of the sparse-input spectrum and the nonparanormal skeptic (§8(f) rows 1 and 4;
+P:965-1016): ggm_nonparanormal (dense COCA) and ggm_gram_eig_csr (CSR unfolding, optional
+COCA in its sparse + rank-one form), against oracle.nonparanormal / gram_eig /
+gram_eig_nonparanormal."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2407_19892_b200 as G
+    assert torch.cuda.is_available()
+    assert G.device_supported(), "needs an sm_100a (B200) device"
+    return G
+
+
+def _sparse_counts(seed, d, m, keep=0.15):
+    """C2-like: negative-binomial counts, zero-inflated, log1p (DESIGN.md §3 recipe)."""
+    rng = np.random.default_rng(seed)
+    mu = rng.lognormal(0.0, 1.0, size=m)
+    counts = rng.negative_binomial(2, 2.0 / (2.0 + mu), size=(d, m))
+    counts = counts * (rng.random((d, m)) < keep)
+    return np.log1p(counts).astype(np.float32)
+
+
+def _csr(M):
+    rows, cols = np.nonzero(M)
+    rp = np.zeros(M.shape[0] + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    rp = np.cumsum(rp)
+    return (torch.from_numpy(rp).cuda(), torch.from_numpy(cols.astype(np.int32)).cuda(),
+            torch.from_numpy(M[rows, cols].astype(np.float32)).cuda())
+
+
+def test_nonparanormal_paper_example(G):
+    with open(os.path.join(GOLD, "nonparanormal.json")) as f:
+        g = json.load(f)
+    X = np.array(g["data"], np.float32)
+    out = G.ggm_nonparanormal(torch.from_numpy(X).cuda(), 0).cpu().numpy()
+    assert np.allclose(np.round(out, 2), g["normal"], atol=1e-6)
+    assert np.allclose(out, O.nonparanormal(X, 0), atol=1e-6)
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_nonparanormal_dense_matches_oracle(G, axis):
+    rng = np.random.default_rng(axis)
+    X = np.round(rng.standard_normal((9, 13, 7)) * 2.0) / 2.0   # many ties and zeros
+    X[X == 0] = np.where(rng.random(np.sum(X == 0)) < 0.5, -0.0, 0.0)
+    X = X.astype(np.float32)
+    out = G.ggm_nonparanormal(torch.from_numpy(X).cuda(), axis).cpu().numpy()
+    want = np.moveaxis(O.nonparanormal(X, axis).reshape(
+        (X.shape[axis],) + tuple(s for a, s in enumerate(X.shape) if a != axis)), 0, axis)
+    assert np.max(np.abs(out - want)) < 2e-6
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_gram_eig_csr_matches_dense_oracle(G, axis):
+    X = _sparse_counts(1, 1500, 400)
+    M = X if axis == 0 else np.ascontiguousarray(X.T)
+    rp, c, v = _csr(M)
+    k = 10
+    V, E, tr, it, ch = G.ggm_gram_eig_csr(rp, c, v, M.shape[1], k)
+    Vo, Eo = O.gram_eig(X, axis, k)
+    assert np.allclose(E.cpu().numpy(), Eo, rtol=1e-8)
+    assert abs(tr - float(np.sum(X.astype(np.float64) ** 2))) < 1e-9 * tr
+    d = np.abs(np.sum(V.cpu().numpy().astype(np.float64)[:, :5] * Vo[:, :5], axis=0))
+    assert np.all(1.0 - d < 1e-5)
+
+
+def test_gram_eig_csr_nonparanormal_rank_one(G):
+    """COCA on the sparse matrix through S + z 1^T equals the dense transform's spectrum."""
+    X = _sparse_counts(2, 600, 300, keep=0.2)
+    rp, c, v = _csr(X)
+    k = 8
+    V, E, tr, it, ch = G.ggm_gram_eig_csr(rp, c, v, X.shape[1], k, nonparanormal=True)
+    Vo, Eo = O.gram_eig_nonparanormal(X, 0, k)
+    assert np.allclose(E.cpu().numpy(), Eo, rtol=1e-8)
+    T = O.nonparanormal(X, 0)
+    assert abs(tr - float(np.sum(T ** 2))) < 1e-9 * tr
+    d = np.abs(np.sum(V.cpu().numpy().astype(np.float64)[:, :4] * Vo[:, :4], axis=0))
+    assert np.all(1.0 - d < 1e-5)
+
+
+def test_gram_eig_csr_edge_rows(G):
+    """Empty rows, explicit stored zeros, rows without zeros (z_i = 0)."""
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((80, 60)).astype(np.float32)
+    X[3] = 0.0                      # empty row
+    X[7, ::2] = 0.0
+    rows, cols = np.nonzero(np.ones_like(X))        # store every entry, zeros included
+    rp = torch.from_numpy(np.arange(0, 80 * 60 + 1, 60, dtype=np.int64)).cuda()
+    c = torch.from_numpy(cols.astype(np.int32)).cuda()
+    v = torch.from_numpy(X[rows, cols]).cuda()
+    for npn in (False, True):
+        V, E, tr, it, ch = G.ggm_gram_eig_csr(rp, c, v, 60, 6, nonparanormal=npn)
+        Eo = (O.gram_eig_nonparanormal(X, 0, 6) if npn else O.gram_eig(X, 0, 6))[1]
+        assert np.allclose(E.cpu().numpy(), Eo, rtol=1e-8)
+        # the same matrix with only its nonzeros stored (row 3 empty)
+        V, E, tr, it, ch = G.ggm_gram_eig_csr(*_csr(X), 60, 6, nonparanormal=npn)
+        assert np.allclose(E.cpu().numpy(), Eo, rtol=1e-8)
