@@ -225,6 +225,56 @@ def stage_timings(G, torch):
     return out
 
 
+def sparse_spectrum_timing(G, torch):
+    """§8(f) rows 1 + 4 at the paper's largest real-data scale (PBMC, 1,248,980 cells x 2,200
+    genes): a synthetic CSR count matrix (10 % nonzero, log1p of uniform counts,
+    generated on the device) -> COCA in its sparse + rank-one form + randomized subspace
+    iteration for the cell axis, k = 50, bounded at 20 iterations (time per iteration
+    reported)."""
+    d, m, dens = 1_248_980, 2_200, 0.10
+    g = torch.Generator(device="cuda").manual_seed(13)
+    rps, cols, vals = [torch.zeros(1, dtype=torch.int64, device="cuda")], [], []
+    base = 0
+    for r0 in range(0, d, 65536):
+        mask = torch.rand((min(65536, d - r0), m), device="cuda", generator=g) < dens
+        idx = mask.nonzero()
+        cnt = mask.sum(1)
+        rps.append(base + torch.cumsum(cnt, 0))
+        base += int(idx.shape[0])
+        cols.append(idx[:, 1].to(torch.int32))
+        vals.append(torch.log1p(torch.randint(1, 30, (idx.shape[0],), device="cuda",
+                                              generator=g).float()))
+        del mask, idx
+    rp, col, val = torch.cat(rps), torch.cat(cols), torch.cat(vals)
+    del rps, cols, vals
+    out = {"shape": [d, m], "nnz": int(val.numel()), "k": 50,
+           "method": "exact Gram of the 2,200 side over 1 GiB dense chunks (fp64 DSYRK) + "
+                     "DSYEVD; COCA as S + z 1^T (P:1003-1012)"}
+
+    def run(tag, rp_, col_, val_, mm):
+        for npn in (False, True):
+            G.ggm_gram_eig_csr(rp_, col_, val_, mm, 50, nonparanormal=npn)  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            G.ggm_gram_eig_csr(rp_, col_, val_, mm, 50, nonparanormal=npn)
+            torch.cuda.synchronize()
+            out[f"{tag}_{'coca' if npn else 'raw'}_ms"] = (time.perf_counter() - t0) * 1e3
+
+    run("cell_axis", rp, col, val, m)
+    # gene axis: the same matrix as gene-major CSR (2,200 rows of 1,248,980 cells)
+    rows = torch.repeat_interleave(torch.arange(d, device="cuda"), rp[1:] - rp[:-1])
+    order = torch.argsort(col.to(torch.int64) * d + rows)
+    tcol = rows[order].to(torch.int32)
+    tval = val[order]
+    trp = torch.zeros(m + 1, dtype=torch.int64, device="cuda")
+    trp[1:] = torch.cumsum(torch.bincount(col.to(torch.int64), minlength=m), 0)
+    del rows, order, rp, col, val
+    run("gene_axis", trp, tcol, tval, d)
+    del trp, tcol, tval
+    torch.cuda.empty_cache()
+    return out
+
+
 def overall_timing(G, torch, V, lam):
     """§8(f) NEXT 2 on the largest axis: whole-graph rules as the paper recommends for
     scRNA-seq: N = 10 n edges overall, degree down-weighting, 1 min edge."""
@@ -461,6 +511,7 @@ def main():
         stages = None if args.no_stages else stage_timings(G, torch)
         if stages is not None:
             stages["overall_rules_axisA"] = overall_timing(G, torch, *dev_axes[a0])
+            stages["sparse_coca_spectrum_pbmc_scale"] = sparse_spectrum_timing(G, torch)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

@@ -115,7 +115,10 @@ ggm_status ggm_gram_eig_multi(int M, const float *const *X, const int *ndim,
 
 /* (1d) Sparse unfolding (§8(f) rows 1 and 4).  D_l given as CSR: d rows (the
  * axis), m columns, nnz stored entries (row_ptr int64 d+1, col int32, val fp32; DEVICE).
- * Randomized subspace iteration (as (1b)) with cuSPARSE SpMM products, never densified.
+ * Columns ascending within each row.  When min(d, m) <= 32768 the Gram of the shorter
+ * side is accumulated exactly over bounded dense chunks (1 GiB) of the matrix by fp64 DSYRK
+ * and eigensolved densely (iters_out = 0); otherwise randomized subspace iteration (as
+ * (1b)) with cuSPARSE SpMM products.  The whole matrix is never densified.
  * nonparanormal = 1 applies the COCA transform first (row ranks among all m
  * entries incl. the implicit zeros, ties -> smallest rank, Φ^-1(r/(m+1))) in its sparse
  * rank-one form S + z 1^T (S keeps D's pattern): the operator products add the

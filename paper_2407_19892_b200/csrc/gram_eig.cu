@@ -856,11 +856,205 @@ ggm_status csr_plan(int64_t d, int64_t m, int64_t nnz, int k, int oversample, RP
   return make_rplan(2, shape2, 0, k, oversample, rp);
 }
 
+// ---- exact path when the shorter side fits a dense Gram (min(d, m) <= kMaxDenseGram):
+// the Gram of the shorter side accumulated over bounded dense chunks of A = S + z 1^T
+// (fp64 DSYRK), dense eigensolve, and (long rows side) V = A W diag(1/σ) chunk by chunk.
+// Memory stays O(chunk + dim^2): the matrix is never densified as a whole.
+constexpr int64_t kChunkElems = int64_t(1) << 27;  // 1 GiB of fp64 per dense chunk
+
+// rows [r0, r1) of A, dense column-major (r1 - r0) x m
+__global__ void csr_rows_dense(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                               const double* __restrict__ sval, const double* __restrict__ z,
+                               int64_t r0, int64_t r1, int64_t m, double* __restrict__ out) {
+  const int64_t ld = r1 - r0;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < r1;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double zi = z[i];
+    for (int64_t c = lane; c < m; c += 32) out[(i - r0) + c * ld] = zi;
+    __syncwarp();
+    for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) out[(i - r0) + (int64_t)col[q] * ld] = sval[q] + zi;
+  }
+}
+// columns [c0, c1) of A, dense column-major d x (c1 - c0) (columns ascending within rows)
+__global__ void csr_cols_dense(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                               const double* __restrict__ sval, const double* __restrict__ z,
+                               int64_t d, int64_t c0, int64_t c1, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < d;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double zi = z[i];
+    for (int64_t c = c0 + lane; c < c1; c += 32) out[i + (c - c0) * d] = zi;
+    __syncwarp();
+    int64_t lo = rp[i], hi = rp[i + 1];
+    {  // first stored entry with col >= c0
+      int64_t a = lo, b = hi;
+      while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (col[mid] < c0) a = mid + 1; else b = mid;
+      }
+      lo = a;
+    }
+    for (int64_t q = lo + lane; q < hi; q += 32) {
+      const int64_t c = col[q];
+      if (c >= c1) break;
+      out[i + (c - c0) * d] = sval[q] + zi;
+    }
+  }
+}
+
+struct CsrDense {
+  int64_t dim, chunk;
+  bool rows_side;  // Gram = A^T A (m x m) accumulated over row chunks (m <= d)
+  int lwork;
+};
+ggm_status csr_dense_plan(int64_t d, int64_t m, int k, CsrDense* cd) {
+  cd->rows_side = m <= d;
+  cd->dim = cd->rows_side ? m : d;
+  cd->chunk = std::max<int64_t>(1, kChunkElems / (cd->rows_side ? m : d));
+  cusolverDnHandle_t h = g_handles.solver;
+  if (!h && cusolverDnCreate(&g_handles.solver) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnCreate failed");
+  if (cusolverDnDsyevd_bufferSize(g_handles.solver, CUSOLVER_EIG_MODE_VECTOR,
+                                  CUBLAS_FILL_MODE_LOWER, (int)cd->dim, nullptr, (int)cd->dim,
+                                  nullptr, &cd->lwork) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
+  if (k < 1 || k > std::min(d, m)) return fail(GGM_ERR_RANK, "k=%d not in [1, min(d, m)]", k);
+  return GGM_OK;
+}
+struct CsrDenseWork {
+  double *G, *w, *work, *chunk, *V64, *Vasc, *Ek, *fro;
+  int* info;
+};
+size_t csr_dense_carve(int64_t d, int64_t m, int k, const CsrDense& cd, void* ws, CsrDenseWork* w) {
+  Carve c(ws);
+  w->G = c.take<double>((size_t)cd.dim * cd.dim);
+  w->w = c.take<double>(cd.dim);
+  w->work = c.take<double>(std::max(cd.lwork, 1));
+  w->chunk = c.take<double>((size_t)cd.chunk * (cd.rows_side ? m : d));
+  w->V64 = c.take<double>((size_t)d * k);
+  w->Vasc = c.take<double>(cd.rows_side ? (size_t)d * k : 0);
+  w->Ek = c.take<double>(k);
+  w->fro = c.take<double>(4);
+  w->info = c.take<int>(4);
+  return c.used();
+}
+
+bool csr_dense_path(int64_t d, int64_t m) {
+  return std::min(d, m) <= kMaxDenseGram && !getenv("GGM_CSR_RSI");
+}
+
 }  // namespace
+
+static ggm_status csr_gram_dense(int64_t d, int64_t m, int64_t nnz, const int64_t* row_ptr,
+                                 const int32_t* col, const float* val, int k, int nonparanormal,
+                                 float* V, double* E, double* trace_S, int* iters_out,
+                                 double* change_out, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  CsrDense cd;
+  ggm_status st = csr_dense_plan(d, m, k, &cd);
+  if (st != GGM_OK) return st;
+  CsrDenseWork dw;
+  const size_t b0 = csr_dense_carve(d, m, k, cd, workspace, &dw);
+  CsrWork cw;
+  const size_t need = b0 + csr_carve(d, m, nnz, 1, true, csr_sort_bytes(d, nnz),
+                                     static_cast<char*>(workspace) + b0, &cw);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  const int sms = num_sms();
+  auto grid_of = [&](int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, sms * 8));
+  };
+  GGM_CUDA_TRY(cudaMemsetAsync(dw.fro, 0, sizeof(double), s));
+  if (nnz > 0) {
+    copy_canon<<<grid_of(nnz), 256, 0, s>>>(val, nnz, cw.canon);
+    if (nonparanormal) {
+      size_t tb = cw.cub_bytes;
+      GGM_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(cw.cub, tb, cw.canon, cw.sorted, nnz, d,
+                                                      row_ptr, row_ptr + 1, s));
+    }
+  }
+  csr_values<<<grid_of(32 * d), 256, 0, s>>>(row_ptr, cw.canon, cw.sorted, d, m,
+                                              nonparanormal ? 1 : 0, cw.sval, cw.z, dw.fro);
+  GGM_CUDA_TRY(cudaGetLastError());
+  const double one = 1.0, zero = 0.0;
+  const int dim = (int)cd.dim;
+  // Gram of the shorter side over dense chunks
+  const int64_t total = cd.rows_side ? d : m;
+  for (int64_t c0 = 0; c0 < total; c0 += cd.chunk) {
+    const int64_t c1 = std::min(total, c0 + cd.chunk);
+    const double beta = c0 == 0 ? 0.0 : 1.0;
+    cublasStatus_t bs;
+    if (cd.rows_side) {  // chunk: (c1-c0) x m; G += chunk^T chunk
+      csr_rows_dense<<<grid_of(32 * (c1 - c0)), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, c0, c1, m, dw.chunk);
+      bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, dim, (int)(c1 - c0), &one,
+                       dw.chunk, (int)(c1 - c0), &beta, dw.G, dim);
+    } else {             // chunk: d x (c1-c0); G += chunk chunk^T
+      csr_cols_dense<<<grid_of(32 * d), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, d, c0, c1, dw.chunk);
+      bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, dim, (int)(c1 - c0), &one,
+                       dw.chunk, (int)d, &beta, dw.G, dim);
+    }
+    GGM_CUDA_TRY(cudaGetLastError());
+    if (bs != CUBLAS_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cublasDsyrk failed (%d)", (int)bs);
+  }
+  if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, dim, dw.G, dim, dw.w,
+                       dw.work, cd.lwork, dw.info) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed");
+  if (!cd.rows_side) {
+    take_topk<<<k, 256, 0, s>>>(dw.w, dw.G, dim, k, dw.Ek, dw.V64);
+  } else {
+    // V = A W_k diag(1/σ): rows chunk by chunk into Vasc (d x k, ascending order), then
+    // reverse + scale
+    const double* Zk = dw.G + (size_t)(dim - k) * dim;
+    for (int64_t r0 = 0; r0 < d; r0 += cd.chunk) {
+      const int64_t r1 = std::min(d, r0 + cd.chunk);
+      csr_rows_dense<<<grid_of(32 * (r1 - r0)), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, r0, r1, m, dw.chunk);
+      if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)(r1 - r0), k, dim, &one, dw.chunk,
+                      (int)(r1 - r0), Zk, dim, &zero, dw.Vasc + r0, (int)d) != CUBLAS_STATUS_SUCCESS)
+        return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+    }
+    reverse_scale<<<dim3(std::max<int64_t>(1, std::min<int64_t>((d + 255) / 256, 64)), k), 256, 0, s>>>(
+        dw.w, dim, dw.Vasc, d, k, dw.Ek, dw.V64);
+  }
+  GGM_CUDA_TRY(cudaGetLastError());
+  sign_and_store<<<k, 256, 0, s>>>(dw.V64, d, k, V);
+  GGM_CUDA_TRY(cudaGetLastError());
+  GGM_CUDA_TRY(cudaMemcpyAsync(E, dw.Ek, sizeof(double) * k, cudaMemcpyDeviceToDevice, s));
+  std::vector<double> hE(k);
+  int hinfo = 0;
+  double hfro = 0.0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(hE.data(), dw.Ek, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hinfo, dw.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hfro, dw.fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hinfo != 0) return fail(GGM_ERR_CUDA, "cusolverDnDsyevd info=%d", hinfo);
+  if (trace_S) *trace_S = hfro;
+  if (iters_out) *iters_out = 0;
+  if (change_out) *change_out = 0.0;
+  if (!(hE[0] > 0.0) || !std::isfinite(hE[0]) || !(hE[k - 1] > 1e-12 * hE[0]))
+    return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)",
+                hE[k - 1], hE[0]);
+  return GGM_OK;
+}
 
 extern "C" ggm_status ggm_gram_eig_csr_workspace(int64_t d, int64_t m, int64_t nnz, int k,
                                                  int oversample, size_t* bytes) {
   if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  if (d >= 1 && m >= 1 && csr_dense_path(d, m)) {
+    CsrDense cd;
+    ggm_status st = csr_dense_plan(d, m, k, &cd);
+    if (st != GGM_OK) return st;
+    CsrDenseWork dw;
+    CsrWork cw;
+    *bytes = csr_dense_carve(d, m, k, cd, nullptr, &dw) +
+             csr_carve(d, m, nnz, 1, true, csr_sort_bytes(d, nnz), nullptr, &cw);
+    return GGM_OK;
+  }
   RPlan rp;
   ggm_status st = csr_plan(d, m, nnz, k, oversample, &rp);
   if (st != GGM_OK) return st;
@@ -882,11 +1076,14 @@ extern "C" ggm_status ggm_gram_eig_csr(int64_t d, int64_t m, int64_t nnz, const 
   if (!row_ptr || (nnz > 0 && (!col || !val)) || !V || !E || !workspace)
     return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
   if (max_iter < 1 || !(tol >= 0.0)) return fail(GGM_ERR_INVALID_ARGUMENT, "max_iter/tol invalid");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  if (d >= 1 && m >= 1 && csr_dense_path(d, m))
+    return csr_gram_dense(d, m, nnz, row_ptr, col, val, k, nonparanormal, V, E, trace_S,
+                          iters_out, change_out, workspace, workspace_bytes, stream);
   RPlan rp;
   ggm_status st = csr_plan(d, m, nnz, k, oversample, &rp);
   if (st != GGM_OK) return st;
-  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
-    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
   RWork w;
   size_t b0 = rcarve(rp, workspace, &w, false);
   b0 = (b0 + 255) / 256 * 256;

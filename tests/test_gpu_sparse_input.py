@@ -15,6 +15,17 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
+@pytest.fixture(params=["dense_gram", "rsi"])
+def csr_path(request, monkeypatch):
+    """dense_gram: exact chunked Gram of the shorter side (default below 32768);
+    rsi: force the randomized subspace iteration with cuSPARSE products."""
+    if request.param == "rsi":
+        monkeypatch.setenv("GGM_CSR_RSI", "1")
+    else:
+        monkeypatch.delenv("GGM_CSR_RSI", raising=False)
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def G():
     import paper_2407_19892_b200 as G
@@ -63,7 +74,7 @@ def test_nonparanormal_dense_matches_oracle(G, axis):
 
 
 @pytest.mark.parametrize("axis", [0, 1])
-def test_gram_eig_csr_matches_dense_oracle(G, axis):
+def test_gram_eig_csr_matches_dense_oracle(G, csr_path, axis):
     X = _sparse_counts(1, 1500, 400)
     M = X if axis == 0 else np.ascontiguousarray(X.T)
     rp, c, v = _csr(M)
@@ -76,7 +87,7 @@ def test_gram_eig_csr_matches_dense_oracle(G, axis):
     assert np.all(1.0 - d < 1e-5)
 
 
-def test_gram_eig_csr_nonparanormal_rank_one(G):
+def test_gram_eig_csr_nonparanormal_rank_one(G, csr_path):
     """COCA on the sparse matrix through S + z 1^T equals the dense transform's spectrum."""
     X = _sparse_counts(2, 600, 300, keep=0.2)
     rp, c, v = _csr(X)
@@ -90,7 +101,7 @@ def test_gram_eig_csr_nonparanormal_rank_one(G):
     assert np.all(1.0 - d < 1e-5)
 
 
-def test_gram_eig_csr_edge_rows(G):
+def test_gram_eig_csr_edge_rows(G, csr_path):
     """Empty rows, explicit stored zeros, rows without zeros (z_i = 0)."""
     rng = np.random.default_rng(5)
     X = rng.standard_normal((80, 60)).astype(np.float32)
