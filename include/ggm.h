@@ -139,6 +139,30 @@ ggm_status ggm_nonparanormal_workspace(int ndim, const int64_t *shape, int axis,
 ggm_status ggm_nonparanormal(const float *X, int ndim, const int64_t *shape, int axis, float *out,
                              void *workspace, size_t workspace_bytes, void *stream);
 
+/* (1f) Sharded spectrum (§8(f) row 1: "sharded Gram with one all-reduce").  A matrix whose
+ * rows (the long axis, e.g. cells) are split over ranks, m <= 32768 columns (e.g. genes):
+ *   ggm_gram_accumulate_csr: G (m x m, fp64 column-major, LOWER triangle) = (accumulate ?
+ *     G : 0) + A_r^T A_r over this rank's CSR rows (COCA of each row when nonparanormal = 1,
+ *     as (1d)); optional *fro_out (host) = ||A_r||_F^2.  The caller all-reduces G.
+ *   ggm_eig_gram: top-k eigenpairs of G (G overwritten): V (m x k fp32 row-major, the
+ *     short-axis factor), E (k, descending), W (m x k fp64 column-major, same signs as V).
+ *   ggm_project_csr: this rank's rows of the long-axis factor V_r = A_r W diag(E^-1/2)
+ *     (d x k fp32 row-major; signs follow W, consistent across ranks).
+ * With nonparanormal = 1 both factors belong to the row-wise (long-axis) COCA transform. */
+ggm_status ggm_gram_accumulate_csr_workspace(int64_t d, int64_t m, int64_t nnz, size_t *bytes);
+ggm_status ggm_gram_accumulate_csr(int64_t d, int64_t m, int64_t nnz, const int64_t *row_ptr,
+                                   const int32_t *col, const float *val, int nonparanormal,
+                                   double *G, int accumulate, double *fro_out, void *workspace,
+                                   size_t workspace_bytes, void *stream);
+ggm_status ggm_eig_gram_workspace(int64_t dim, int k, size_t *bytes);
+ggm_status ggm_eig_gram(int64_t dim, double *G, int k, float *V, double *E, double *W,
+                        void *workspace, size_t workspace_bytes, void *stream);
+ggm_status ggm_project_csr_workspace(int64_t d, int64_t m, int64_t nnz, int k, size_t *bytes);
+ggm_status ggm_project_csr(int64_t d, int64_t m, int64_t nnz, const int64_t *row_ptr,
+                           const int32_t *col, const float *val, int nonparanormal, int k,
+                           const double *W, const double *E, float *V, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------------------------
  * (2) Eigenvalue MLE — Theorem 2, Algorithm 1 lines 5-17.
  *

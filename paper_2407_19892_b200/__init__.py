@@ -13,6 +13,7 @@ Public API (thin bindings of libggm.so, include/ggm.h):
 """
 from ._ggm import (GGMError, SparsePlan, device_supported, ggm_gram_eig, ggm_gram_eig_rsi,
                    ggm_gram_eig_multi, ggm_solve_eigvals_multi, ggm_gram_eig_csr, ggm_nonparanormal,
+                   gram_accumulate_csr, eig_gram, project_csr,
                    ggm_grid_marginals,
                    ggm_solve_eigvals, ggm_sparse_precision, ggm_sparse_precision_overall, overall_last_path, overall_last_timing, last_launches, last_stats, last_timing, lib,
                    set_timing, SymShardPlan, sym_merge, sym_rows_begin, wald_edge, wald_threshold,
@@ -20,6 +21,7 @@ from ._ggm import (GGMError, SparsePlan, device_supported, ggm_gram_eig, ggm_gra
 
 __all__ = ["GGMError", "SparsePlan", "device_supported", "ggm_gram_eig", "ggm_gram_eig_rsi",
            "ggm_gram_eig_multi", "ggm_solve_eigvals_multi", "ggm_gram_eig_csr", "ggm_nonparanormal",
+           "gram_accumulate_csr", "eig_gram", "project_csr",
            "ggm_grid_marginals",
            "ggm_solve_eigvals", "ggm_sparse_precision", "ggm_sparse_precision_overall", "overall_last_path", "overall_last_timing", "last_launches", "last_stats", "last_timing", "lib", "set_timing",
            "SymShardPlan", "sym_merge", "sym_rows_begin", "wald_edge", "wald_threshold", "version",

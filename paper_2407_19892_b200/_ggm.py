@@ -38,7 +38,8 @@ EXPORTED = [
     "ggm_overall_last_path",
     "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
     "ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
-    "ggm_nonparanormal",
+    "ggm_nonparanormal", "ggm_gram_accumulate_csr_workspace", "ggm_gram_accumulate_csr",
+    "ggm_eig_gram_workspace", "ggm_eig_gram", "ggm_project_csr_workspace", "ggm_project_csr",
 ]
 
 
@@ -143,7 +144,17 @@ def lib() -> C.CDLL:
                                    C.POINTER(C.c_double), vp, C.c_size_t, vp]
     L.ggm_nonparanormal_workspace.argtypes = [i32, C.POINTER(i64), i32, C.POINTER(C.c_size_t)]
     L.ggm_nonparanormal.argtypes = [vp, i32, C.POINTER(i64), i32, vp, vp, C.c_size_t, vp]
-    for name in ("ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
+    L.ggm_gram_accumulate_csr_workspace.argtypes = [i64, i64, i64, C.POINTER(C.c_size_t)]
+    L.ggm_gram_accumulate_csr.argtypes = [i64, i64, i64, vp, vp, vp, i32, vp, i32,
+                                          C.POINTER(C.c_double), vp, C.c_size_t, vp]
+    L.ggm_eig_gram_workspace.argtypes = [i64, i32, C.POINTER(C.c_size_t)]
+    L.ggm_eig_gram.argtypes = [i64, vp, i32, vp, vp, vp, vp, C.c_size_t, vp]
+    L.ggm_project_csr_workspace.argtypes = [i64, i64, i64, i32, C.POINTER(C.c_size_t)]
+    L.ggm_project_csr.argtypes = [i64, i64, i64, vp, vp, vp, i32, i32, vp, vp, vp, vp,
+                                  C.c_size_t, vp]
+    for name in ("ggm_gram_accumulate_csr_workspace", "ggm_gram_accumulate_csr",
+                 "ggm_eig_gram_workspace", "ggm_eig_gram", "ggm_project_csr_workspace",
+                 "ggm_project_csr", "ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
                  "ggm_nonparanormal", "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
                  "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
                  "ggm_gram_eig_workspace", "ggm_gram_eig", "ggm_solve_eigvals",
@@ -285,6 +296,57 @@ def ggm_gram_eig_csr(row_ptr: torch.Tensor, col: torch.Tensor, val: torch.Tensor
                                   C.byref(it), C.byref(ch), _ptr(ws), nbytes.value,
                                   _stream(stream)))
     return V, E, tr.value, it.value, ch.value
+
+
+def gram_accumulate_csr(row_ptr, col, val, m: int, nonparanormal: bool = False, G=None,
+                        stream=None):
+    """G (+)= A_r^T A_r for this rank's CSR rows (include/ggm.h (1f)); returns (G, ||A_r||^2).
+    G is fp64 m x m column-major with the LOWER triangle filled."""
+    _require_cuda(row_ptr, torch.int64, "row_ptr")
+    _require_cuda(col, torch.int32, "col")
+    _require_cuda(val, torch.float32, "val")
+    d, nnz = row_ptr.numel() - 1, val.numel()
+    acc = G is not None
+    if G is None:
+        G = torch.zeros((m, m), dtype=torch.float64, device=val.device)
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_gram_accumulate_csr_workspace(d, int(m), nnz, C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=val.device)
+    fro = C.c_double(0.0)
+    _check(lib().ggm_gram_accumulate_csr(d, int(m), nnz, _ptr(row_ptr), _ptr(col), _ptr(val),
+                                         int(bool(nonparanormal)), _ptr(G), int(acc),
+                                         C.byref(fro), _ptr(ws), nbytes.value, _stream(stream)))
+    return G, fro.value
+
+
+def eig_gram(G: torch.Tensor, k: int, stream=None):
+    """Top-k eigenpairs of an (all-reduced) Gram; G is overwritten.  Returns (V fp32 m x k,
+    E fp64 k descending, W fp64 for ggm_project_csr)."""
+    _require_cuda(G, torch.float64, "G")
+    m = G.shape[0]
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_eig_gram_workspace(m, int(k), C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=G.device)
+    V = torch.empty((m, k), dtype=torch.float32, device=G.device)
+    E = torch.empty((k,), dtype=torch.float64, device=G.device)
+    W = torch.empty((k, m), dtype=torch.float64, device=G.device)   # column-major m x k
+    _check(lib().ggm_eig_gram(m, _ptr(G), int(k), _ptr(V), _ptr(E), _ptr(W), _ptr(ws),
+                              nbytes.value, _stream(stream)))
+    return V, E, W
+
+
+def project_csr(row_ptr, col, val, m: int, W: torch.Tensor, E: torch.Tensor,
+                nonparanormal: bool = False, stream=None) -> torch.Tensor:
+    """This rank's rows of the long-axis factor A_r W diag(E^-1/2) (fp32 d x k)."""
+    d, nnz, k = row_ptr.numel() - 1, val.numel(), E.numel()
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_project_csr_workspace(d, int(m), nnz, int(k), C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=val.device)
+    V = torch.empty((d, k), dtype=torch.float32, device=val.device)
+    _check(lib().ggm_project_csr(d, int(m), nnz, _ptr(row_ptr), _ptr(col), _ptr(val),
+                                 int(bool(nonparanormal)), int(k), _ptr(W), _ptr(E), _ptr(V),
+                                 _ptr(ws), nbytes.value, _stream(stream)))
+    return V
 
 
 def ggm_nonparanormal(X: torch.Tensor, axis: int, stream=None) -> torch.Tensor:

@@ -1288,3 +1288,238 @@ extern "C" ggm_status ggm_nonparanormal(const float* X, int ndim, const int64_t*
   GGM_CUDA_TRY(cudaGetLastError());
   return GGM_OK;
 }
+
+// ------------------------------------------------------------------ sharded spectrum pieces
+// §8(f) row 1 "sharded Gram with one all-reduce": a matrix whose rows (the long axis, e.g.
+// cells) are split over ranks.  Each rank accumulates G_r = A_r^T A_r (m x m, the short side)
+// over its rows (ggm_gram_accumulate_csr), the caller all-reduces G (one NCCL all-reduce of
+// m^2 doubles), every rank eigensolves it (ggm_eig_gram: short-axis V and E, plus W for the
+// projection) and maps its own rows V_r = A_r W diag(E^-1/2) (ggm_project_csr).
+namespace {
+struct ShardWork {
+  CsrWork cw;
+  double *chunk, *fro;
+};
+size_t shard_carve(int64_t d, int64_t m, int64_t nnz, void* ws, ShardWork* w) {
+  Carve c(ws);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(d, kChunkElems / m));
+  w->chunk = c.take<double>((size_t)chunk * m);
+  w->fro = c.take<double>(4);
+  const size_t b0 = c.used();
+  return b0 + csr_carve(d, m, nnz, 1, true, csr_sort_bytes(d, nnz),
+                        ws ? static_cast<char*>(ws) + b0 : nullptr, &w->cw);
+}
+ggm_status shard_values(int64_t d, int64_t m, int64_t nnz, const int64_t* rp, const float* val,
+                        int np, ShardWork& w, cudaStream_t s) {
+  const int sms = num_sms();
+  auto grid_of = [&](int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, sms * 8));
+  };
+  GGM_CUDA_TRY(cudaMemsetAsync(w.fro, 0, sizeof(double), s));
+  if (nnz > 0) {
+    copy_canon<<<grid_of(nnz), 256, 0, s>>>(val, nnz, w.cw.canon);
+    if (np) {
+      size_t tb = w.cw.cub_bytes;
+      GGM_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(w.cw.cub, tb, w.cw.canon, w.cw.sorted, nnz,
+                                                      d, rp, rp + 1, s));
+    }
+  }
+  csr_values<<<grid_of(32 * d), 256, 0, s>>>(rp, w.cw.canon, w.cw.sorted, d, m, np ? 1 : 0,
+                                              w.cw.sval, w.cw.z, w.fro);
+  GGM_CUDA_TRY(cudaGetLastError());
+  return GGM_OK;
+}
+}  // namespace
+
+extern "C" ggm_status ggm_gram_accumulate_csr_workspace(int64_t d, int64_t m, int64_t nnz,
+                                                        size_t* bytes) {
+  if (!bytes || d < 1 || m < 1 || nnz < 0) return fail(GGM_ERR_INVALID_ARGUMENT, "bad sizes");
+  ShardWork w;
+  *bytes = shard_carve(d, m, nnz, nullptr, &w);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_gram_accumulate_csr(int64_t d, int64_t m, int64_t nnz,
+                                              const int64_t* row_ptr, const int32_t* col,
+                                              const float* val, int nonparanormal, double* G,
+                                              int accumulate, double* fro_out, void* workspace,
+                                              size_t workspace_bytes, void* stream) {
+  if (d < 1 || m < 1 || nnz < 0 || !row_ptr || (nnz > 0 && (!col || !val)) || !G || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "bad sizes / null pointer");
+  if (m > kMaxDenseGram) return fail(GGM_ERR_UNSUPPORTED, "short side m=%lld > 32768", (long long)m);
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  ShardWork w;
+  const size_t need = shard_carve(d, m, nnz, workspace, &w);
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  ggm_status st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  st = shard_values(d, m, nnz, row_ptr, val, nonparanormal, w, s);
+  if (st != GGM_OK) return st;
+  const int sms = num_sms();
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(d, kChunkElems / m));
+  const double one = 1.0;
+  for (int64_t r0 = 0; r0 < d; r0 += chunk) {
+    const int64_t r1 = std::min(d, r0 + chunk);
+    const double beta = (r0 == 0 && !accumulate) ? 0.0 : 1.0;
+    csr_rows_dense<<<(int)std::max<int64_t>(1, std::min<int64_t>((32 * (r1 - r0) + 255) / 256, sms * 8)),
+                     256, 0, s>>>(row_ptr, col, w.cw.sval, w.cw.z, r0, r1, m, w.chunk);
+    GGM_CUDA_TRY(cudaGetLastError());
+    if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)m, (int)(r1 - r0), &one, w.chunk,
+                    (int)(r1 - r0), &beta, G, (int)m) != CUBLAS_STATUS_SUCCESS)
+      return fail(GGM_ERR_CUDA, "cublasDsyrk failed");
+  }
+  if (fro_out) {
+    GGM_CUDA_TRY(cudaMemcpyAsync(fro_out, w.fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  return GGM_OK;
+}
+
+namespace {
+__global__ void fix_sign_cols(double* W, int64_t rows, int k) {
+  // largest-|.| entry of each column positive (first index on ties), in place
+  const int r = blockIdx.x;
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  double best = -1.0;
+  long long bi = 0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double a = fabs(W[(size_t)r * rows + i]);
+    if (a > best) { best = a; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (sv[q] > sv[0] || (sv[q] == sv[0] && si[q] < si[0])) { sv[0] = sv[q]; si[0] = si[q]; }
+  __syncthreads();
+  const double sgn = W[(size_t)r * rows + si[0]] < 0 ? -1.0 : 1.0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) W[(size_t)r * rows + i] *= sgn;
+}
+__global__ void scale_cols_store(const double* __restrict__ X, int64_t rows, int k,
+                                 const double* __restrict__ E, float* __restrict__ V) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < rows * k;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / k;
+    const int c = (int)(q % k);
+    V[q] = (float)(X[(size_t)c * rows + i] / sqrt(E[c]));
+  }
+}
+}  // namespace
+
+extern "C" ggm_status ggm_eig_gram_workspace(int64_t dim, int k, size_t* bytes) {
+  if (!bytes || dim < 1 || dim > kMaxDenseGram || k < 1 || k > dim)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "bad sizes");
+  cusolverDnHandle_t h = g_handles.solver;
+  if (!h && cusolverDnCreate(&g_handles.solver) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnCreate failed");
+  int lw = 0;
+  if (cusolverDnDsyevd_bufferSize(g_handles.solver, CUSOLVER_EIG_MODE_VECTOR,
+                                  CUBLAS_FILL_MODE_LOWER, (int)dim, nullptr, (int)dim, nullptr,
+                                  &lw) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
+  Carve c(nullptr);
+  c.take<double>((size_t)dim);
+  c.take<double>((size_t)std::max(lw, 1));
+  c.take<int>(4);
+  *bytes = c.used();
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_eig_gram(int64_t dim, double* G, int k, float* V, double* E, double* W,
+                                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (!G || !V || !E || !W || !workspace) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  size_t need = 0;
+  ggm_status st = ggm_eig_gram_workspace(dim, k, &need);
+  if (st != GGM_OK) return st;
+  if (workspace_bytes < need) return fail(GGM_ERR_INVALID_ARGUMENT, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  int lw = 0;
+  cusolverDnDsyevd_bufferSize(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)dim,
+                              G, (int)dim, nullptr, &lw);
+  Carve c(workspace);
+  double* w = c.take<double>((size_t)dim);
+  double* work = c.take<double>((size_t)std::max(lw, 1));
+  int* info = c.take<int>(4);
+  if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)dim, G,
+                       (int)dim, w, work, lw, info) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed");
+  take_topk<<<k, 256, 0, s>>>(w, G, (int)dim, k, E, W);  // W: dim x k, descending
+  fix_sign_cols<<<k, 256, 0, s>>>(W, dim, k);
+  sign_and_store<<<k, 256, 0, s>>>(W, dim, k, V);         // signs already fixed: plain store
+  GGM_CUDA_TRY(cudaGetLastError());
+  std::vector<double> hE(k);
+  int hinfo = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(hE.data(), E, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hinfo != 0) return fail(GGM_ERR_CUDA, "cusolverDnDsyevd info=%d", hinfo);
+  if (!(hE[0] > 0.0) || !std::isfinite(hE[0]) || !(hE[k - 1] > 1e-12 * hE[0]))
+    return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)",
+                hE[k - 1], hE[0]);
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_project_csr_workspace(int64_t d, int64_t m, int64_t nnz, int k,
+                                                size_t* bytes) {
+  ggm_status st = ggm_gram_accumulate_csr_workspace(d, m, nnz, bytes);
+  if (st != GGM_OK) return st;
+  if (k < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "k < 1");
+  *bytes += (size_t)d * k * sizeof(double) + 256;
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_project_csr(int64_t d, int64_t m, int64_t nnz, const int64_t* row_ptr,
+                                      const int32_t* col, const float* val, int nonparanormal,
+                                      int k, const double* W, const double* E, float* V,
+                                      void* workspace, size_t workspace_bytes, void* stream) {
+  if (d < 1 || m < 1 || k < 1 || !row_ptr || !W || !E || !V || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "bad sizes / null pointer");
+  size_t need = 0;
+  ggm_status st = ggm_gram_accumulate_csr_workspace(d, m, nnz, &need);
+  if (st != GGM_OK) return st;
+  need += (size_t)d * k * sizeof(double) + 256;
+  if (workspace_bytes < need) return fail(GGM_ERR_INVALID_ARGUMENT, "workspace too small");
+  ShardWork w;
+  const size_t b0 = shard_carve(d, m, nnz, workspace, &w);
+  double* X = reinterpret_cast<double*>(static_cast<char*>(workspace) + b0);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  st = shard_values(d, m, nnz, row_ptr, val, nonparanormal, w, s);
+  if (st != GGM_OK) return st;
+  const int sms = num_sms();
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(d, kChunkElems / m));
+  const double one = 1.0, zero = 0.0;
+  for (int64_t r0 = 0; r0 < d; r0 += chunk) {
+    const int64_t r1 = std::min(d, r0 + chunk);
+    csr_rows_dense<<<(int)std::max<int64_t>(1, std::min<int64_t>((32 * (r1 - r0) + 255) / 256, sms * 8)),
+                     256, 0, s>>>(row_ptr, col, w.cw.sval, w.cw.z, r0, r1, m, w.chunk);
+    GGM_CUDA_TRY(cudaGetLastError());
+    if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)(r1 - r0), k, (int)m, &one, w.chunk,
+                    (int)(r1 - r0), W, (int)m, &zero, X + r0, (int)d) != CUBLAS_STATUS_SUCCESS)
+      return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+  }
+  scale_cols_store<<<(int)std::max<int64_t>(1, std::min<int64_t>((d * k + 255) / 256, sms * 8)), 256, 0, s>>>(
+      X, d, k, E, V);
+  GGM_CUDA_TRY(cudaGetLastError());
+  return GGM_OK;
+}

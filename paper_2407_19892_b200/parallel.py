@@ -187,3 +187,32 @@ def sharded_symmetric_precision(V, lam, t: int, group=None, shard=None, merge=No
     if not gather:
         return row_id, col, vals
     return assemble_rows(row_id, col, vals, n, min(t, n - 1), group=group)
+
+
+def sharded_csr_spectrum(row_ptr, col, val, m: int, k: int, nonparanormal: bool = False,
+                         group=None, accumulate: Callable | None = None,
+                         eig: Callable | None = None, project: Callable | None = None):
+    """Spectrum of a matrix whose rows (the long axis, e.g. 1.25M cells) are sharded over the
+    process group, m <= 32768 columns (e.g. genes) — §8(f) row 1, "sharded Gram with one
+    all-reduce" (include/ggm.h (1f)).  Every rank passes its own CSR rows.
+
+    G_r = A_r^T A_r (m x m) -> ONE all_reduce(SUM) -> every rank eigensolves G (short-axis V,
+    E, W) -> local long-axis rows V_r = A_r W diag(E^-1/2).  For a matrix both axes share E
+    (Thm 1).  Returns (V_short replicated, E, V_long local rows).
+
+    accumulate(rp, col, val, m, nonparanormal) -> G, eig(G, k) -> (V, E, W),
+    project(rp, col, val, m, W, E, nonparanormal) -> V_r default to the CUDA path; the CPU
+    tests inject NumPy versions."""
+    if accumulate is None or eig is None or project is None:
+        from . import _ggm as G_
+        accumulate = accumulate or (lambda rp, c, v, mm, npn: G_.gram_accumulate_csr(
+            rp, c, v, mm, npn)[0])
+        eig = eig or (lambda Gm, kk: G_.eig_gram(Gm, kk))
+        project = project or (lambda rp, c, v, mm, W, E, npn: G_.project_csr(
+            rp, c, v, mm, W, E, npn))
+    Gm = accumulate(row_ptr, col, val, m, nonparanormal)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(Gm, op=dist.ReduceOp.SUM, group=group)
+    V_short, E, W = eig(Gm, k)
+    V_long = project(row_ptr, col, val, m, W, E, nonparanormal)
+    return V_short, E, V_long

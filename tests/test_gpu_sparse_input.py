@@ -118,3 +118,29 @@ def test_gram_eig_csr_edge_rows(G, csr_path):
         # the same matrix with only its nonzeros stored (row 3 empty)
         V, E, tr, it, ch = G.ggm_gram_eig_csr(*_csr(X), 60, 6, nonparanormal=npn)
         assert np.allclose(E.cpu().numpy(), Eo, rtol=1e-8)
+
+
+@pytest.mark.parametrize("npn", [False, True])
+def test_sharded_spectrum_pieces(G, npn):
+    """§8(f) row 1 sharded Gram: two row shards accumulated into one G (the all-reduce is a
+    sum; here the second shard accumulates in place), eigensolved, each shard projected —
+    equals the oracle spectrum of the whole (row-transformed) matrix on both axes."""
+    X = _sparse_counts(3, 900, 120, keep=0.25)
+    T = O.nonparanormal(X, 0) if npn else X.astype(np.float64)
+    k = 7
+    Gm = None
+    shards = [(0, 400), (400, 900)]
+    for b, e in shards:
+        rp, c, v = _csr(X[b:e])
+        Gm, fro = G.gram_accumulate_csr(rp, c, v, X.shape[1], nonparanormal=npn, G=Gm)
+    Vs, E, W = G.eig_gram(Gm, k)
+    Vl = torch.cat([G.project_csr(*_csr(X[b:e]), X.shape[1], W, E, nonparanormal=npn)
+                    for b, e in shards]).cpu().numpy().astype(np.float64)
+    u, sig, vt = np.linalg.svd(T, full_matrices=False)
+    assert np.allclose(E.cpu().numpy(), sig[:k] ** 2, rtol=1e-9)
+    d_short = np.abs(np.sum(Vs.cpu().numpy().astype(np.float64) * vt[:k].T, axis=0))
+    d_long = np.abs(np.sum(Vl * u[:, :k], axis=0))
+    assert np.all(1.0 - d_short < 1e-5) and np.all(1.0 - d_long < 1e-5)
+    # long-axis factor signs follow W: V_l = T W diag(E^-1/2) exactly
+    Wn = W.cpu().numpy().reshape(k, -1).T
+    assert np.allclose(Vl, (T @ Wn) / np.sqrt(E.cpu().numpy()), atol=1e-5)

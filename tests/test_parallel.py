@@ -184,3 +184,82 @@ def test_sharded_symmetric_equals_oracle(world):
         np.testing.assert_array_equal(rp, rp1)
         np.testing.assert_array_equal(c, c1)
         np.testing.assert_allclose(v, v1, rtol=1e-6)
+
+
+# ------------------------------------------------------------ sharded spectrum (one all-reduce)
+
+def _np_csr_fns():
+    """NumPy stand-ins of the three CUDA steps (dense from CSR; host logic under test)."""
+    def dense(rp, c, v, m):
+        rp, c, v = rp.numpy(), c.numpy(), v.numpy().astype(np.float64)
+        A = np.zeros((len(rp) - 1, m))
+        for i in range(len(rp) - 1):
+            A[i, c[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+        return A
+
+    def acc(rp, c, v, m, npn):
+        A = dense(rp, c, v, m)
+        return torch.from_numpy(A.T @ A)
+
+    def eig(Gm, k):
+        w, Z = np.linalg.eigh(Gm.numpy())
+        W = Z[:, ::-1][:, :k].copy()
+        E = w[::-1][:k].copy()
+        return torch.from_numpy(W.astype(np.float32)), torch.from_numpy(E), torch.from_numpy(W)
+
+    def proj(rp, c, v, m, W, E, npn):
+        A = dense(rp, c, v, m)
+        return torch.from_numpy((A @ W.numpy()) / np.sqrt(E.numpy()))
+    return acc, eig, proj
+
+
+def _spectrum_matrix():
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((157, 23)) * (rng.random((157, 23)) < 0.3)
+    return X.astype(np.float32)
+
+
+def _spec_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2407_19892_b200.parallel import sharded_csr_spectrum
+        X = _spectrum_matrix()
+        b, e = shard_rows(X.shape[0], world, rank)
+        Xr = X[b:e]
+        rows, cols = np.nonzero(Xr)
+        rp = np.zeros(e - b + 1, np.int64)
+        np.add.at(rp, rows + 1, 1)
+        rp = np.cumsum(rp)
+        acc, eig, proj = _np_csr_fns()
+        Vs, E, Vl = sharded_csr_spectrum(torch.from_numpy(rp), torch.from_numpy(cols.astype(np.int32)),
+                                         torch.from_numpy(Xr[rows, cols]), X.shape[1], 6,
+                                         accumulate=acc, eig=eig, project=proj)
+        q.put((rank, Vs.numpy(), E.numpy(), Vl.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_spectrum_equals_oracle(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_spec_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=240) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import oracle as O
+    X = _spectrum_matrix()
+    Vg, Eg = O.gram_eig(X, 1, 6)      # short axis (columns)
+    Vc, Ec = O.gram_eig(X, 0, 6)      # long axis (rows), same spectrum for a matrix
+    for _, Vs, E, _ in got:
+        np.testing.assert_allclose(E, Eg, rtol=1e-10)
+        np.testing.assert_allclose(np.abs(np.sum(Vs * Vg, axis=0)), 1.0, atol=1e-6)
+    Vl = np.concatenate([g[3] for g in got], axis=0)
+    np.testing.assert_allclose(np.abs(np.sum(Vl * Vc, axis=0)), 1.0, atol=1e-9)
+    np.testing.assert_allclose(Ec, Eg, rtol=1e-10)
