@@ -89,17 +89,35 @@ __global__ void absmax_check(const float* __restrict__ V, const double* __restri
       if (!(l > 0.0) || !isfinite(l)) atomicOr(&sc->flags, 2);
     }
   }
+  __shared__ double sl[1024];
+  const bool staged = k <= 1024;
+  if (staged)
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+      const double l = lam[c];
+      sl[c] = sqrt(l > 0.0 ? l : 0.0);
+    }
+  __syncthreads();
   float m = 0.f;
   int bad = 0;
   const int64_t total = n * (int64_t)k;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  const int cstep = (int)(step % k);
+  int c = (int)(i0 % k);  // column of idx, advanced incrementally (no division per element)
+  for (int64_t idx = i0; idx < total; idx += step) {
     float v = V[idx];
-    int c = (int)(idx % k);
     if (!isfinite(v)) bad = 1;
-    double l = lam[c];
-    float u = (float)(fabs((double)v) * sqrt(l > 0.0 ? l : 0.0));
+    double sq;
+    if (staged) {
+      sq = sl[c];
+    } else {
+      const double l = lam[c];
+      sq = sqrt(l > 0.0 ? l : 0.0);
+    }
+    float u = (float)(fabs((double)v) * sq);
     m = fmaxf(m, u);
+    c += cstep;
+    if (c >= k) c -= k;
   }
   if (bad) atomicOr(&sc->flags, 1);
 #pragma unroll
@@ -180,56 +198,76 @@ __device__ __forceinline__ void split2(double x, __half& h, __half& l) {
   h = __double2half(x);
   l = __double2half(x - (double)__half2float(h));
 }
+// One thread per (row, 16-byte chunk): the 8 elements are split once and both the hi-array
+// and the lo-array chunk are written (sqrt(λ) staged in shared memory; 32-bit index math).
+constexpr int kSplitMaxK = 1024;
 __global__ void split_tile(const float* __restrict__ V, const double* __restrict__ lam,
                            int64_t n, int k, int KA, int KS, int TS, int64_t row0,
                            int64_t nrows_pad, const DevScalars* __restrict__ sc,
                            uint8_t* __restrict__ dst, const int32_t* __restrict__ perm = nullptr) {
-  const int chunks_per_row = KA * 8;  // 16-byte chunks of one array (hi or lo)
-  const int64_t total = nrows_pad * chunks_per_row * 2;
+  __shared__ double sl[kSplitMaxK];
+  const bool staged = k <= kSplitMaxK;
+  if (staged)
+    for (int c = threadIdx.x; c < k; c += blockDim.x) sl[c] = sqrt(lam[c]);
+  __syncthreads();
+  const int cpr = KA * 8;  // 16-byte chunks of one array per row
+  const int64_t total = nrows_pad * cpr;
   const double s = ldexp(1.0, sc->exp2);
   const int r = k - 16 * KS;  // tail elements (packed when TS > 0)
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int arr = (int)(idx % 2);  // 0 = hi array, 1 = lo array
-    const int64_t rc = idx / 2;
-    const int64_t row = rc / chunks_per_row;
-    const int ch = (int)(rc % chunks_per_row);
+    int64_t row;
+    int ch;
+    if (total < (int64_t(1) << 31)) {
+      const uint32_t i32 = (uint32_t)idx;
+      row = i32 / (uint32_t)cpr;
+      ch = (int)(i32 - (uint32_t)row * (uint32_t)cpr);
+    } else {
+      row = idx / cpr;
+      ch = (int)(idx % cpr);
+    }
     int64_t g = row0 + row;
     const bool real = g < n;
     if (perm && real) g = perm[g];  // symmetric scheme: rows in bound order
     const int slot = ch >> 1;
-    __align__(16) __half out[8];
+    __align__(16) __half oh[8];
+    __align__(16) __half ol[8];
+    const float* vrow = V + g * k;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int pos = (ch & 1) * 8 + e;  // position within the slot
       __half h = __float2half(0.f), l = __float2half(0.f);
-      __half v = __float2half(0.f);
+      __half v0 = h, v1 = h;
       if (real) {
         if (slot < KS || TS == 0) {
           const int c = slot * 16 + pos;
           if (c < k) {
-            split2((double)V[g * k + c] * sqrt(lam[c]) * s, h, l);
-            v = arr ? l : h;
+            split2((double)vrow[c] * (staged ? sl[c] : sqrt(lam[c])) * s, h, l);
+            v0 = h;
+            v1 = l;
           }
         } else if (slot < KS + TS) {
           const int q = (slot - KS) * 16 + pos;  // position in the packed tail sequence
           if (q < 3 * r) {
             const int seg = q / r;
             const int c = 16 * KS + q % r;
-            split2((double)V[g * k + c] * sqrt(lam[c]) * s, h, l);
+            split2((double)vrow[c] * (staged ? sl[c] : sqrt(lam[c])) * s, h, l);
             // B (hi array): [hi | lo | hi];  A (lo array): [hi | hi | lo]
-            v = arr == 0 ? (seg == 1 ? l : h) : (seg == 2 ? l : h);
+            v0 = seg == 1 ? l : h;
+            v1 = seg == 2 ? l : h;
           }
         }
       }
-      out[e] = v;
+      oh[e] = v0;
+      ol[e] = v1;
     }
     const int64_t b = row / kRowsPerBlock;
     const int rr = (int)(row % kRowsPerBlock);
     const int a = ch >> 3, c8 = ch & 7;
-    const size_t off = (size_t)b * block_bytes(KA) + (size_t)(arr * KA + a) * kAtomBytes +
-                       (size_t)rr * 128 + (size_t)((c8 ^ (rr & 7)) * 16);
-    *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(out);
+    const size_t base = (size_t)b * block_bytes(KA) + (size_t)rr * 128 + (size_t)((c8 ^ (rr & 7)) * 16);
+    *reinterpret_cast<uint4*>(dst + base + (size_t)a * kAtomBytes) = *reinterpret_cast<const uint4*>(oh);
+    *reinterpret_cast<uint4*>(dst + base + (size_t)(KA + a) * kAtomBytes) =
+        *reinterpret_cast<const uint4*>(ol);
   }
 }
 
