@@ -449,8 +449,13 @@ def main():
     # fp32-accurate tensor peak = fp16 (= bf16) dense rate / 3 (3-term split).  The sustained
     # cuBLAS figure is the default; when BK2 runs above it (its clock under the power cap
     # stays higher than cuBLAS's), the burst figure is the honest denominator.
-    peak_sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
-    peak_burst = peaks.get("bf16_tflops", peak_sus * 3.0) / 3.0
+    # With hi*hi screening (symmetric scheme default) the main kernel issues ONE fp16 product
+    # per entry (+ the packed 3-term tail) and the candidates are re-evaluated exactly
+    # afterwards: its peak is the plain fp16 (= bf16) dense rate.
+    screening = st0["mma_k_per_entry"] < 2.0 * k0
+    div = 1.0 if screening else 3.0
+    peak_sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / div
+    peak_burst = peaks.get("bf16_tflops", peak_sus * div) / div
     peak_is_burst = achieved > peak_sus
     peak = peak_burst if peak_is_burst else peak_sus
     traffic = None
@@ -529,10 +534,15 @@ def main():
                          "achieved_basis": "2k flops per entry (SURVEY 8(d)) x %s / mean CUDA-event "
                                            "duration of BK2 on the largest axis" % (
                                                "n(n+1)/2 unordered entries" if sym0 else "rows x n"),
-                         "peak_basis": f"{peak_src} bf16_tflops{'' if peak_is_burst else '_sustained'} / 3 "
-                                       "(3-term fp16 split = 3 MMAs per fp32-accurate product; fp16 rate = "
-                                       "bf16 rate)" + ("; burst figure because BK2 runs above the cuBLAS "
-                                                       "sustained rate" if peak_is_burst else ""),
+                         "peak_basis": (f"{peak_src} bf16_tflops{'' if peak_is_burst else '_sustained'} "
+                                        "(hi*hi screening: one fp16 MMA product per entry, fp16 rate = "
+                                        "bf16 rate; candidates re-evaluated exactly in fp64 afterwards)"
+                                        if screening else
+                                        f"{peak_src} bf16_tflops{'' if peak_is_burst else '_sustained'} / 3 "
+                                        "(3-term fp16 split = 3 MMAs per fp32-accurate product; fp16 rate = "
+                                        "bf16 rate)") + ("; burst figure because BK2 runs above the cuBLAS "
+                                                         "sustained rate" if peak_is_burst else ""),
+                         "screening": bool(screening),
                          "kernel_ms": avg_fused, "step_share": step_ms_fused_share,
                          "tensor_pipe_tflops": st0["entries_main"] * 2.0 * st0["mma_k_per_entry"]
                          / (avg_fused * 1e-3) / 1e12,

@@ -170,6 +170,55 @@ __global__ void seed_bounds(float* __restrict__ thr, const float* __restrict__ r
   }
 }
 
+// kSym screening thresholds: the main pass computes hi·hi only (|ψ1 - ψ| <= 2^-10 (1+2^-11)
+// ||x_i|| ||x_j|| + fp32 terms, see seed_bounds), so entry (i, j) is kept for row i if
+// |ψ1| >= b_i - 1.1·2^-10 ||x_i|| max||x|| (and symmetrically for row j): every entry with
+// |ψ| >= b_i survives.  Bound order p (perm[p] = original id); padding stays +inf.
+__global__ void screen_bounds(const float* __restrict__ thr_p, const float* __restrict__ rn,
+                              const int32_t* __restrict__ perm,
+                              const unsigned int* __restrict__ rn_max_bits, int64_t n,
+                              int64_t nthr, const DevScalars* __restrict__ sc,
+                              float* __restrict__ thr_s) {
+  const float s = ldexpf(1.f, sc->exp2);
+  const float umax = __uint_as_float(*rn_max_bits) * s;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nthr;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const float b = thr_p[p];
+    if (p < n && b < INFINITY) {
+      const float margin = 1.1f * ldexpf(rn[perm[p]] * s * umax, -10);
+      thr_s[p] = b > -1.f ? b - margin : b;
+    } else {
+      thr_s[p] = b;
+    }
+  }
+}
+
+// Exact re-evaluation of the screened candidates: ψ_ij = Σ_r λ_r V_ir V_jr in fp64 from the
+// fp32 inputs (one warp per candidate; the pair is visited in (min id, max id) order so
+// both directions of a pair get bit-identical values).  Unused pool slots (key UINT32_MAX)
+// are skipped.
+__global__ void recompute_cands(const uint32_t* __restrict__ key, uint2* __restrict__ cv,
+                                int64_t ncand, const int32_t* __restrict__ perm,
+                                const float* __restrict__ V, const double* __restrict__ lam,
+                                int k) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ncand;
+       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t j = key[q];
+    if (j == 0xFFFFFFFFu) continue;
+    const uint2 x = cv[q];
+    const int64_t a = perm[j], b = perm[x.x];
+    const int64_t lo = a < b ? a : b, hi = a < b ? b : a;
+    const float* vl = V + lo * k;
+    const float* vh = V + hi * k;
+    double acc = 0.0;
+    for (int c = lane; c < k; c += 32) acc += lam[c] * ((double)vl[c] * (double)vh[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) cv[q].y = __float_as_uint((float)acc);
+  }
+}
+
 // ------------------------------------------------------------------ BK1b
 __global__ void scale_finalize(DevScalars* sc) {
   float m = __uint_as_float(sc->absmax_bits);
@@ -314,6 +363,7 @@ struct FusedParams {
   uint32_t* cand_key;      // kSym: candidate pool: target row j (UINT32_MAX = unused slot)
   uint2* cand_val;         //       (source row i, ψ bits)
   int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
+  int screen;        // kSym: hi*hi screening MMAs only (candidates re-evaluated exactly)
   int pair;          // CTA-pair kernel (host-side selection; the kernel's template PAIR)
   int unit_lo, unit_hi;  // units processed by this launch (a rank's share in the sharded
                          // symmetric scheme; [0, all units) otherwise)
@@ -1258,13 +1308,14 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
           if (PAIR) {
             // this CTA's half of the B tile: operand block K0 + rank, hi (+ lo) per K atom
             const int bline = (ti.K0 + rank) * lines_per_block;
-            const uint32_t sbytes = (uint32_t)(KIND == kSeed ? 1 : 2) * kAtomBytes;
+            const bool hi_only = KIND == kSeed || p.screen;
+            const uint32_t sbytes = (uint32_t)(hi_only ? 1 : 2) * kAtomBytes;
             for (int a = 0; a < KA; ++a) {
               mbar_wait(&empty[stage], phase ^ 1);
               if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * sbytes);
               uint8_t* st = sStage + stage * st_bytes;
               tma_load_2d_pair(st, &tmB, 0, bline + a * kRowsPerBlock, &full[stage], pol_b);
-              if (KIND != kSeed)
+              if (!hi_only)
                 tma_load_2d_pair(st + kAtomBytes, &tmB, 0, bline + (KA + a) * kRowsPerBlock,
                                  &full[stage], pol_b);
               if (++stage == NS) {
@@ -1279,12 +1330,13 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
           if (resident) {
             // B hi (block K0 | block K1), then B lo, of each K atom: 256 rows per atom,
             // uniform 1 KB SBO (the seed pass reads only the hi array)
-            const uint32_t sbytes = (uint32_t)(KIND == kSeed ? 2 : 4) * kAtomBytes;
+            const bool hi_only = KIND == kSeed || p.screen;
+            const uint32_t sbytes = (uint32_t)(hi_only ? 2 : 4) * kAtomBytes;
             for (int a = 0; a < KA; ++a) {
               mbar_wait(&empty[stage], phase ^ 1);
               uint8_t* st = sStage + stage * st_bytes;
               mbar_arrive_expect_tx(&full[stage], sbytes);
-              for (int hl = 0; hl < (KIND == kSeed ? 1 : 2); ++hl) {
+              for (int hl = 0; hl < (hi_only ? 1 : 2); ++hl) {
                 const size_t ao = (size_t)(hl * KA + a) * kAtomBytes;
                 bulk_g2s(st + 2 * hl * kAtomBytes, B0 + ao, kAtomBytes, &full[stage], pol_b);
                 bulk_g2s(st + (2 * hl + 1) * kAtomBytes, B1 + ao, kAtomBytes, &full[stage], pol_b);
@@ -1325,6 +1377,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
       // MMA cost ~27 issue slots on an SM sub-partition shared with 4 epilogue warps.
       constexpr uint32_t idesc = idesc_f16_f32(PAIR ? 2 * kRowsPerBlock : kRowsPerBlock, kTileN);
       const bool issuer = elect_one();
+      const bool three = KIND != kSeed && !p.screen;  // hi*lo and lo*hi products too
       int stage = 0;
       uint32_t phase = 0;
       int buf = 0;
@@ -1368,7 +1421,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
                 const uint32_t acc = (a | ks) ? 1u : 0u;
                 if (slot < p.KS) {
                   mma_f16<PAIR>(d_tmem, dAh + o, dBh + o, idesc, acc);
-                  if (KIND != kSeed) {  // the seed pass bounds with hi*hi alone (seed_bounds)
+                  if (three) {  // the seed and screening passes use hi*hi alone
                     mma_f16<PAIR>(d_tmem, dAh + o, dBl + o, idesc, 1u);
                     mma_f16<PAIR>(d_tmem, dAl + o, dBh + o, idesc, 1u);
                   }
@@ -1535,6 +1588,7 @@ struct Plan {
   int64_t RBu;   // units of row blocks: RB (1 CTA) or ceil(RB/2) 256-row blocks (pair)
   int64_t NBu;   // kSym/kSeed units over the axis: NB or ceil(NB/2)
   int sym;       // symmetric scheme (kSeed + kSym + merge_sym)
+  int screen;    // symmetric scheme: hi*hi screening + exact re-evaluation of candidates
   int SS;        // seed column-tile stride
   int64_t NB;    // 128-row blocks of the axis
   int64_t cand_total;  // kSym: candidate pool capacity (entries)
@@ -1626,6 +1680,7 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // merge are small against the halved tensor-core work
   const bool sym_ok = o->mode == 0 && full_axis && pl->resident;
   pl->sym = sym_ok && (o->symmetric == 1 || (o->symmetric == 0 && n >= kSymAutoN)) ? 1 : 0;
+  pl->screen = pl->sym && !getenv("GGM_NO_SCREEN") ? 1 : 0;
   // candidates: ~ t x 16 / 2 per row expected (seed samples 1/16 of the columns, half of
   // each row's columns come from the transposed direction); regions hold 2x that on average
   // pool: 2x the expected candidates + one chunk per epilogue warp of partially used space
@@ -1689,6 +1744,7 @@ struct Work {
   void* cub_tmp;
   float* thr;          // kSym: seed bounds by original row [NB*128]
   float* thr_p;        // kSym: bounds in permuted (sorted) order [NB*128]
+  float* thr_s;        // kSym screening: thr_p lowered by the hi*hi error bound [NB*128]
   int32_t* ids;        // kSym: 0..n-1
   int32_t* perm;       // kSym: permuted index -> original id [n]
   float* rn;           // kSym: row norms ||U_i|| [n]
@@ -1719,6 +1775,7 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   const size_t ct = pl.sym ? (size_t)pl.cand_total : 0;
   w->thr = cv.take<float>(nb * kRowsPerBlock);
   w->thr_p = cv.take<float>(nb * kRowsPerBlock);
+  w->thr_s = cv.take<float>(pl.screen ? nb * kRowsPerBlock : 0);
   w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->rn = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
@@ -1974,6 +2031,11 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   }
   fill_f32<<<(int)std::min<int64_t>((nthr - n + 255) / 256 + 1, sms * 8), 256, 0, s>>>(
       w.thr_p + n, nthr - n, INFINITY);
+  if (pl.screen) {
+    screen_bounds<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(
+        w.thr_p, w.rn, w.perm, &w.sc->rn_max_bits, n, nthr, w.sc, w.thr_s);
+    count_launches(1);
+  }
   {
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
@@ -1991,7 +2053,8 @@ static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int un
                            int unit_hi, cudaStream_t s) {
   fp.kind = kSym;
   fp.RB = (int)pl.NBu;
-  fp.thr = w.thr_p;
+  fp.thr = pl.screen ? w.thr_s : w.thr_p;
+  fp.screen = pl.screen;
   fp.perm = w.perm;
   fp.cand_key = w.ckey;
   fp.cand_val = w.cval;
@@ -2032,7 +2095,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   reset_launches();
   for (double& x : g_stats) x = 0.0;
-  g_stats[4] = 16.0 * (3 * pl.KS + pl.TS);  // MMA K elements issued per evaluated entry
+  g_stats[4] = 16.0 * ((pl.screen ? 1 : 3) * pl.KS + pl.TS);  // MMA K elements issued per evaluated entry
   g_stats[5] = pl.pair;
   EventTimer tm(timing_enabled(), s);
   tm.mark(0);
@@ -2116,6 +2179,11 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       return GGM_OK;
     }
     const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
+    if (pl.screen && ncand > 0) {
+      recompute_cands<<<(int)std::min<int64_t>((ncand * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+          w.ckey, w.cval, ncand, w.perm, V, lambda, k);
+      count_launches(1);
+    }
     if (ncand > 0) {
       size_t tb = pl.sort_temp_bytes;
       // keys are permuted row ids < n; unused slots (UINT32_MAX) keep all low bits set, so
@@ -2322,6 +2390,11 @@ extern "C" ggm_status ggm_sparse_precision_sym_shard(
   if (hs.cand_overflow)
     return fail(GGM_ERR_CAPACITY, "symmetric candidate pool overflow (use the row-sharded plain scheme)");
   const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
+  if (pl.screen && ncand > 0) {
+    recompute_cands<<<(int)std::min<int64_t>((ncand * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+        w.ckey, w.cval, ncand, w.perm, V, lambda, k);
+    count_launches(1);
+  }
   int ebits = 1;
   while ((int64_t(1) << ebits) <= n) ++ebits;
   if (ncand > 0) {
@@ -2367,7 +2440,7 @@ extern "C" ggm_status ggm_sparse_precision_sym_shard(
   g_stats[0] = 2;
   g_stats[1] = evaluated;
   g_stats[2] = (double)total;
-  g_stats[4] = 16.0 * (3 * pl.KS + pl.TS);
+  g_stats[4] = 16.0 * ((pl.screen ? 1 : 3) * pl.KS + pl.TS);
   g_stats[5] = pl.pair;
   return GGM_OK;
 }
