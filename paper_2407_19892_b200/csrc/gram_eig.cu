@@ -1136,7 +1136,7 @@ extern "C" ggm_status ggm_gram_eig_csr(int64_t d, int64_t m, int64_t nnz, const 
                         it, it, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F) != CUSPARSE_STATUS_SUCCESS)
     return fail(GGM_ERR_CUDA, "cusparseCreateCsr failed");
   const int r = rp.r;
-  cusparseDnMatDescr_t Xm = nullptr, Yd = nullptr, Xd = nullptr, Ym = nullptr;
+  cusparseDnMatDescr_t Xm = nullptr, Yd = nullptr;
   cusparseCreateDnMat(&Xm, m, r, m, w.Om, CUDA_R_64F, CUSPARSE_ORDER_COL);  // m x r operand
   cusparseCreateDnMat(&Yd, d, r, d, w.Y, CUDA_R_64F, CUSPARSE_ORDER_COL);   // d x r
   const double one = 1.0, zero = 0.0;
@@ -1155,8 +1155,6 @@ extern "C" ggm_status ggm_gram_eig_csr(int64_t d, int64_t m, int64_t nnz, const 
     cusparseDestroyDnMat(Yd);
     cudaFreeAsync(spbuf, s);
   };
-  (void)Xd;
-  (void)Ym;
   // operator products: the RSI buffers are fixed (Om: m x r, Y: d x r), so the descriptors
   // are bound to them; applyA reads Om and writes Y, applyAt reads Y and writes Om
   auto applyA = [&](const double* in, double* out) -> bool {  // Y = S Om + z (1^T Om)

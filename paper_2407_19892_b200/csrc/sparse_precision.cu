@@ -193,29 +193,13 @@ __global__ void screen_bounds(const float* __restrict__ thr_p, const float* __re
   }
 }
 
-// Exact re-evaluation of the screened candidates: ψ_ij = Σ_r λ_r V_ir V_jr in fp64 from the
-// fp32 inputs (one warp per candidate; the pair is visited in (min id, max id) order so
-// both directions of a pair get bit-identical values).  Unused pool slots (key UINT32_MAX)
-// are skipped.
-__global__ void recompute_cands(const uint32_t* __restrict__ key, uint2* __restrict__ cv,
-                                int64_t ncand, const int32_t* __restrict__ perm,
-                                const float* __restrict__ V, const double* __restrict__ lam,
-                                int k) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ncand;
-       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const uint32_t j = key[q];
-    if (j == 0xFFFFFFFFu) continue;
-    const uint2 x = cv[q];
-    const int64_t a = perm[j], b = perm[x.x];
-    const int64_t lo = a < b ? a : b, hi = a < b ? b : a;
-    const float* vl = V + lo * k;
-    const float* vh = V + hi * k;
-    double acc = 0.0;
-    for (int c = lane; c < k; c += 32) acc += lam[c] * ((double)vl[c] * (double)vh[c]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) cv[q].y = __float_as_uint((float)acc);
+__global__ void chunk_min32(const float* __restrict__ thr, int64_t nchunks,
+                            float* __restrict__ out) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float m = INFINITY;
+    for (int e = 0; e < 32; ++e) m = fminf(m, thr[c * 32 + e]);
+    out[c] = m;
   }
 }
 
@@ -358,7 +342,7 @@ struct FusedParams {
   int hshift;
   const float* thr;        // kSym: per-(permuted) column lower bound of that row's t-th
                            //       magnitude (accumulator units, +inf = padding)
-  const float* thr_min;    // kSym: min of thr over each 32-column chunk
+  const float* thr_min;    // kSym: min of thr over each 32-column chunk (bound order)
   const int32_t* perm;     // kSym: permuted index -> original row/column id
   uint32_t* cand_key;      // kSym: candidate pool: target row j (UINT32_MAX = unused slot)
   uint2* cand_val;         //       (source row i, ψ bits)
@@ -1023,15 +1007,24 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
                                               uint64_t* tfull, uint64_t* tempty, int warp,
                                               int lane, float* scratch_all, int u0, int ustep,
                                               int rank) {
+  // Per tile and warp the work is: wait for the accumulator, load the warp's W columns,
+  // release the buffer, one FMNMX3 chain per 32 columns against min(row bound, the
+  // precomputed minimum of the chunk's column bounds).  Everything else is hoisted: column
+  // bounds are read from global memory only on the rare path, indices are 32-bit
+  // (n < 2^31), and the per-chunk minima come from p.thr_min (one broadcast load).
   using G = EpiGeom<EPW>;
-  constexpr int VPL = G::W / 32;  // column bounds per lane (4 or 2)
   const G g(warp, lane);
-  // this warp's W column bounds
-  float* thr_w = scratch_all + (size_t)(warp - kFirstEpiWarp) * (kScratchBytes / 4 / EPW);
+  (void)scratch_all;
   const float sd = ldexpf(1.f, -p.sc->exp2);
   const float sd2 = sd * sd;
   const uint32_t lt = (1u << lane) - 1u;
   DevScalars* scw = const_cast<DevScalars*>(p.sc);
+  const int n = (int)p.n;
+  const float* __restrict__ thr = p.thr;
+  const float* __restrict__ thr_min = p.thr_min;
+  const uint32_t trow = tmem_base + ((uint32_t)(g.q * 32) << 16) + (uint32_t)(g.part * G::W);
+  const int coff = g.col_off();
+  const bool second = g.second();
   int buf = 0;
   uint32_t tphase = 0;
   CandCursor cc{0, kCandChunk};
@@ -1039,52 +1032,27 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
-    const int64_t gi = (int64_t)rb * kRowsPerBlock + g.r;  // permuted row index
-    const bool valid = gi < p.n;
-    const float bi = valid ? __ldg(p.thr + gi) : INFINITY;  // row bound (accumulator units)
+    const int gi = rb * kRowsPerBlock + g.r;  // permuted row index
+    const bool valid = gi < n;
+    const float bi = valid ? __ldg(thr + gi) : INFINITY;  // row bound (accumulator units)
     TileIter<KIND, PAIR> ti;
     ti.start(p, u, ub, u0, ustep);
-    float tn[VPL];
-    auto load_bounds = [&](const TileIter<KIND, PAIR>& it) {
-      const float* src = p.thr + (int64_t)(g.second() ? it.K1 : it.K0) * kRowsPerBlock +
-                         g.col_off() + lane * VPL;
-      if (VPL == 4) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(src));
-        tn[0] = x.x; tn[1] = x.y; tn[VPL > 2 ? 2 : 0] = x.z; tn[VPL > 3 ? 3 : 0] = x.w;
-      } else {
-        const float2 x = __ldg(reinterpret_cast<const float2*>(src));
-        tn[0] = x.x; tn[1] = x.y;
-      }
-    };
-    if (ntiles > 0) load_bounds(ti);
     for (int s = 0; s < ntiles; ++s) {
-      const int Kh = g.second() ? ti.K1 : ti.K0;
-      const bool live = (!g.second() || ti.h1) && p.dbg != 2;
+      const int Kh = second ? ti.K1 : ti.K0;
+      const bool live = (!second || ti.h1) && p.dbg != 2;
       // off-diagonal blocks emit the transposed direction; for a CTA pair, the diagonal
       // 256x256 super tile covers both directions of its blocks in the row direction
       const bool emit_cols = PAIR ? (ti.K0 >> 1) != ub : Kh != rb;
-      const int64_t cb = (int64_t)Kh * kRowsPerBlock + g.col_off();
-      const bool need_mask = Kh == rb || cb + G::W > p.n;
+      const int cb = Kh * kRowsPerBlock + coff;
+      const bool need_mask = Kh == rb || cb + G::W > n;
       ti.next(p);
-      // stage the W column bounds; chunk minima by shuffles within each chunk's lanes
-      float cm = tn[0];
-#pragma unroll
-      for (int e = 1; e < VPL; ++e) cm = fminf(cm, tn[e]);
-#pragma unroll
-      for (int o = 1; o < 32 / VPL; o <<= 1) cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
       float cmin[G::NC];
 #pragma unroll
       for (int c = 0; c < G::NC; ++c)
-        cmin[c] = emit_cols ? __shfl_sync(0xffffffffu, cm, c * (32 / VPL)) : INFINITY;
-      __syncwarp();
-#pragma unroll
-      for (int e = 0; e < VPL; ++e) thr_w[lane * VPL + e] = tn[e];
-      __syncwarp();
-      if (s + 1 < ntiles) load_bounds(ti);
+        cmin[c] = emit_cols ? __ldg(thr_min + (cb >> 5) + c) : INFINITY;
       mbar_wait(&tfull[buf], tphase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(g.q * 32) << 16) +
-                             (uint32_t)(buf * kTileN + g.part * G::W);
+      const uint32_t taddr = trow + (uint32_t)(buf * kTileN);
       uint32_t v[G::NC][32];
       if (live) {
 #pragma unroll
@@ -1096,23 +1064,21 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       tc_fence_before();
       __syncwarp();
       if (lane == 0) release_tmem<PAIR>(&tempty[buf]);
-      if (++buf == 2) {
-        buf = 0;
-        tphase ^= 1;
-      }
+      buf ^= 1;
+      tphase ^= (uint32_t)(buf == 0);
       if (!live || p.dbg == 1) {
         if (live && v[0][0] == 12345u && v[G::NC - 1][31] == 54321u) p.row_ptr[0] = (int64_t)v[0][7];
         continue;
       }
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) {
-        const int64_t col0 = cb + c * 32;
+        const int col0 = cb + c * 32;
         float m = max32_abs(reinterpret_cast<const float(&)[32]>(v[c]));
         uint32_t excl = 0;  // diagonal (Q8) and padding columns
         if (need_mask) {
-          const int64_t dd = gi - col0;
-          if ((uint64_t)dd < 32ull) excl |= 1u << dd;
-          const int64_t nn = p.n - col0;
+          const int dd = gi - col0;
+          if ((unsigned)dd < 32u) excl |= 1u << dd;
+          const int nn = n - col0;
           if (nn < 32) excl |= nn <= 0 ? 0xffffffffu : (0xffffffffu << nn);
           m = 0.f;
 #pragma unroll
@@ -1130,10 +1096,10 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
           mr &= ~excl;
         }
         if (ch) {
-          const float4* t4 = reinterpret_cast<const float4*>(thr_w + c * 32);
+          const float4* t4 = reinterpret_cast<const float4*>(thr + col0);
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
-            const float4 th = t4[q4];
+            const float4 th = __ldg(t4 + q4);
             mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 0])) >= th.x ? 1u : 0u) << (4 * q4 + 0);
             mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 1])) >= th.y ? 1u : 0u) << (4 * q4 + 1);
             mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 2])) >= th.z ? 1u : 0u) << (4 * q4 + 2);
@@ -1168,11 +1134,11 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
             if (hr) {  // candidate (i -> j): target row i
               const int64_t pos = at + __popc(br & lt);
               p.cand_key[pos] = (uint32_t)gi;
-              p.cand_val[pos] = make_uint2((uint32_t)(col0 + e), xb);
+              p.cand_val[pos] = make_uint2((uint32_t)(col0 + (int)e), xb);
             }
             if (hc) {  // candidate (j -> i): target row j
               const int64_t pos = at + __popc(br) + __popc(bc & lt);
-              p.cand_key[pos] = (uint32_t)(col0 + e);
+              p.cand_key[pos] = (uint32_t)(col0 + (int)e);
               p.cand_val[pos] = make_uint2((uint32_t)gi, xb);
             }
             mh &= mh - 1;
@@ -1505,6 +1471,56 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n,
   return lo;
 }
 
+// Same re-evaluation on the pool sorted by target row: one warp per target row j keeps row
+// perm[j] of V in registers and streams its candidates' source rows (coalesced 128-B loads);
+// fp32 x fp32 products are exact in fp64 and λ multiplies the exact product, so ψ_ij and
+// ψ_ji come out bit-identical.
+constexpr int kRecMaxK = 128;
+__global__ void recompute_sorted(const uint32_t* __restrict__ skey, uint2* __restrict__ sval,
+                                 int64_t ncand, int64_t n, const int32_t* __restrict__ perm,
+                                 const float* __restrict__ V, const double* __restrict__ lam,
+                                 int k) {
+  const int lane = threadIdx.x & 31;
+  constexpr int R = kRecMaxK / 32;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b0 = lower_bound_u32(skey, ncand, (uint32_t)j);
+    const int64_t b1 = lower_bound_u32(skey, ncand, (uint32_t)j + 1u);
+    if (b0 >= b1) continue;
+    const float* va = V + (int64_t)perm[j] * k;
+    double xa[R], lr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int c = lane + 32 * r;
+      xa[r] = c < k ? (double)va[c] : 0.0;
+      lr[r] = c < k ? lam[c] : 0.0;
+    }
+    // four candidates per step: their source-row loads are in flight together
+    for (int64_t e0 = b0; e0 < b1; e0 += 4) {
+      float xb[4][R];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u < b1 ? e0 + u : b1 - 1;
+        const float* vb = V + (int64_t)perm[sval[e].x] * k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int c = lane + 32 * r;
+          xb[u][r] = c < k ? __ldg(vb + c) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double acc = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc += lr[r] * (xa[r] * (double)xb[u][r]);  // exact product, then λ
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0 && e0 + u < b1) sval[e0 + u].y = __float_as_uint((float)acc);
+      }
+    }
+  }
+}
+
 template <int MAXT>
 __global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restrict__ cv,
                           int64_t ncand, int64_t n, int t, const int32_t* __restrict__ perm,
@@ -1680,7 +1696,7 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // merge are small against the halved tensor-core work
   const bool sym_ok = o->mode == 0 && full_axis && pl->resident;
   pl->sym = sym_ok && (o->symmetric == 1 || (o->symmetric == 0 && n >= kSymAutoN)) ? 1 : 0;
-  pl->screen = pl->sym && !getenv("GGM_NO_SCREEN") ? 1 : 0;
+  pl->screen = pl->sym && k <= 128 && !getenv("GGM_NO_SCREEN") ? 1 : 0;
   // candidates: ~ t x 16 / 2 per row expected (seed samples 1/16 of the columns, half of
   // each row's columns come from the transposed direction); regions hold 2x that on average
   // pool: 2x the expected candidates + one chunk per epilogue warp of partially used space
@@ -1745,6 +1761,7 @@ struct Work {
   float* thr;          // kSym: seed bounds by original row [NB*128]
   float* thr_p;        // kSym: bounds in permuted (sorted) order [NB*128]
   float* thr_s;        // kSym screening: thr_p lowered by the hi*hi error bound [NB*128]
+  float* thr_cmin;     // kSym: minimum of the effective bounds over each 32-column chunk
   int32_t* ids;        // kSym: 0..n-1
   int32_t* perm;       // kSym: permuted index -> original id [n]
   float* rn;           // kSym: row norms ||U_i|| [n]
@@ -1776,6 +1793,7 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->thr = cv.take<float>(nb * kRowsPerBlock);
   w->thr_p = cv.take<float>(nb * kRowsPerBlock);
   w->thr_s = cv.take<float>(pl.screen ? nb * kRowsPerBlock : 0);
+  w->thr_cmin = cv.take<float>(nb * kRowsPerBlock / 32);
   w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->rn = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
@@ -2036,6 +2054,9 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
         w.thr_p, w.rn, w.perm, &w.sc->rn_max_bits, n, nthr, w.sc, w.thr_s);
     count_launches(1);
   }
+  chunk_min32<<<(int)std::min<int64_t>((nthr / 32 + 255) / 256, sms * 8), 256, 0, s>>>(
+      pl.screen ? w.thr_s : w.thr_p, nthr / 32, w.thr_cmin);
+  count_launches(1);
   {
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
@@ -2054,6 +2075,7 @@ static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int un
   fp.kind = kSym;
   fp.RB = (int)pl.NBu;
   fp.thr = pl.screen ? w.thr_s : w.thr_p;
+  fp.thr_min = w.thr_cmin;
   fp.screen = pl.screen;
   fp.perm = w.perm;
   fp.cand_key = w.ckey;
@@ -2179,11 +2201,6 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       return GGM_OK;
     }
     const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
-    if (pl.screen && ncand > 0) {
-      recompute_cands<<<(int)std::min<int64_t>((ncand * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-          w.ckey, w.cval, ncand, w.perm, V, lambda, k);
-      count_launches(1);
-    }
     if (ncand > 0) {
       size_t tb = pl.sort_temp_bytes;
       // keys are permuted row ids < n; unused slots (UINT32_MAX) keep all low bits set, so
@@ -2192,6 +2209,11 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       while ((int64_t(1) << ebits) <= n) ++ebits;
       GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                    ncand, 0, ebits, s));
+      if (pl.screen) {  // exact values of the screened candidates
+        recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+            w.skey, w.sval, ncand, n, w.perm, V, lambda, k);
+        count_launches(1);
+      }
     }
     if (pl.t <= 5)
       launch_merge_sym_t<5>(w, pl, ncand, row_ptr, col, val, s);
@@ -2390,17 +2412,17 @@ extern "C" ggm_status ggm_sparse_precision_sym_shard(
   if (hs.cand_overflow)
     return fail(GGM_ERR_CAPACITY, "symmetric candidate pool overflow (use the row-sharded plain scheme)");
   const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
-  if (pl.screen && ncand > 0) {
-    recompute_cands<<<(int)std::min<int64_t>((ncand * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-        w.ckey, w.cval, ncand, w.perm, V, lambda, k);
-    count_launches(1);
-  }
   int ebits = 1;
   while ((int64_t(1) << ebits) <= n) ++ebits;
   if (ncand > 0) {
     size_t tb = pl.sort_temp_bytes;
     GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                  ncand, 0, ebits, s));
+    if (pl.screen) {  // exact values before the buckets leave this rank
+      recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+          w.skey, w.sval, ncand, n, w.perm, V, lambda, k);
+      count_launches(1);
+    }
   }
   // destination buckets: rank r owns bound-order rows [lo_r, lo_{r+1}); unused pool slots
   // (key UINT32_MAX) sort after every real key
