@@ -1053,6 +1053,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       mbar_wait(&tfull[buf], tphase);
       tc_fence_after();
       const uint32_t taddr = trow + (uint32_t)(buf * kTileN);
+#ifdef GGM_EPI_BLOCK
       uint32_t v[G::NC][32];
       if (live) {
 #pragma unroll
@@ -1070,10 +1071,35 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         if (live && v[0][0] == 12345u && v[G::NC - 1][31] == 54321u) p.row_ptr[0] = (int64_t)v[0][7];
         continue;
       }
+#define VC v[c]
+#else
+      // one 32-column chunk in registers at a time (32 value registers instead of W: no
+      // rematerialisation at 96 registers/thread); the buffer is released as soon as the
+      // last chunk is in registers, before its filter runs
+      const uint32_t cur_buf = buf;
+      buf ^= 1;
+      tphase ^= (uint32_t)(buf == 0);
+      auto release_cur = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) release_tmem<PAIR>(&tempty[cur_buf]);
+      };
+      if (!live || p.dbg == 1) {
+        release_cur();
+        continue;
+      }
+#define VC vc
+#endif
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) {
         const int col0 = cb + c * 32;
-        float m = max32_abs(reinterpret_cast<const float(&)[32]>(v[c]));
+#ifndef GGM_EPI_BLOCK
+        uint32_t vc[32];
+        tmem_ld32_nowait(taddr + c * 32, vc);
+        tmem_wait_ld(vc);
+        if (c == G::NC - 1) release_cur();  // the last chunk is in registers
+#endif
+        float m = max32_abs(reinterpret_cast<const float(&)[32]>(VC));
         uint32_t excl = 0;  // diagonal (Q8) and padding columns
         if (need_mask) {
           const int dd = gi - col0;
@@ -1083,7 +1109,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
           m = 0.f;
 #pragma unroll
           for (int e = 0; e < 32; ++e)
-            m = fmaxf(m, ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(v[c][e])));
+            m = fmaxf(m, ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(VC[e])));
         }
         const bool rh = valid && m >= bi;
         const bool ch = valid && m >= cmin[c];
@@ -1092,7 +1118,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         uint32_t mr = 0, mc = 0;
         if (rh) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) mr |= (fabsf(__uint_as_float(v[c][e])) >= bi ? 1u : 0u) << e;
+          for (int e = 0; e < 32; ++e) mr |= (fabsf(__uint_as_float(VC[e])) >= bi ? 1u : 0u) << e;
           mr &= ~excl;
         }
         if (ch) {
@@ -1100,10 +1126,10 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
             const float4 th = __ldg(t4 + q4);
-            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 0])) >= th.x ? 1u : 0u) << (4 * q4 + 0);
-            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 1])) >= th.y ? 1u : 0u) << (4 * q4 + 1);
-            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 2])) >= th.z ? 1u : 0u) << (4 * q4 + 2);
-            mc |= (fabsf(__uint_as_float(v[c][4 * q4 + 3])) >= th.w ? 1u : 0u) << (4 * q4 + 3);
+            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 0])) >= th.x ? 1u : 0u) << (4 * q4 + 0);
+            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 1])) >= th.y ? 1u : 0u) << (4 * q4 + 1);
+            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 2])) >= th.z ? 1u : 0u) << (4 * q4 + 2);
+            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 3])) >= th.w ? 1u : 0u) << (4 * q4 + 3);
           }
           mc &= ~excl;
         }
@@ -1130,7 +1156,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
           const uint32_t br = __ballot_sync(0xffffffffu, hr);
           const uint32_t bc = __ballot_sync(0xffffffffu, hc);
           if (mh) {
-            const uint32_t xb = __float_as_uint(sel32(v[c], e) * sd2);
+            const uint32_t xb = __float_as_uint(sel32(VC, e) * sd2);
             if (hr) {  // candidate (i -> j): target row i
               const int64_t pos = at + __popc(br & lt);
               p.cand_key[pos] = (uint32_t)gi;
@@ -1149,6 +1175,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
     }
   }
 }
+#undef VC
 
 // Epilogue warps per kind: 16 for the candidate and seed epilogues (t <= 10), else 8.
 #ifndef GGM_SEED_EPW
