@@ -1498,51 +1498,106 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n,
   return lo;
 }
 
-// Same re-evaluation on the pool sorted by target row: one warp per target row j keeps row
-// perm[j] of V in registers and streams its candidates' source rows (coalesced 128-B loads);
-// fp32 x fp32 products are exact in fp64 and λ multiplies the exact product, so ψ_ij and
-// ψ_ji come out bit-identical.
+// Re-evaluation on the pool sorted by target row: one warp per target row j keeps row j of
+// U (bound order) in registers and streams its candidates' source rows (coalesced 128-B
+// loads, no permutation lookups); fp32 x fp32 products are exact in fp64 and summed in a
+// fixed order, so ψ_ij and ψ_ji come out bit-identical.
 constexpr int kRecMaxK = 128;
-__global__ void recompute_sorted(const uint32_t* __restrict__ skey, uint2* __restrict__ sval,
-                                 int64_t ncand, int64_t n, const int32_t* __restrict__ perm,
-                                 const float* __restrict__ V, const double* __restrict__ lam,
-                                 int k) {
+// Only candidates that can still reach the row's exact top t are re-evaluated: with M_j =
+// 1.1·2^-10 ||x_j|| max||x|| (the screening error bound of every pair of row j) and s_t the
+// t-th largest screened magnitude of the row's candidates, an exact top-t entry c has
+// |ψ1(c)| >= T - M_j >= s_t - 2 M_j (T the exact t-th magnitude, s_t <= T + M_j).  The
+// others get value 0 and cannot displace the re-evaluated ones in merge_sym.  On a rank's
+// partial list (distributed scheme) s_t is smaller than on the full row: still conservative.
+// rows' candidate ranges of the key-sorted pool: off[j] = first index with key >= j
+__global__ void cand_row_offsets(const uint32_t* __restrict__ skey, int64_t ncand, int64_t n,
+                                 int64_t* __restrict__ off) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    off[j] = lower_bound_u32(skey, ncand, (uint32_t)j);
+}
+// U = V diag(sqrt(λ)) in bound order (fp32), the re-evaluation operand: ψ_ij = Σ_r U_ir U_jr
+__global__ void gather_u_bound(const float* __restrict__ V, const double* __restrict__ lam,
+                               const int32_t* __restrict__ perm, int64_t n, int k,
+                               float* __restrict__ Ub) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * k;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = q / k;
+    const int c = (int)(q - p * k);
+    Ub[q] = (float)((double)V[(int64_t)perm[p] * k + c] * sqrt(lam[c]));
+  }
+}
+__global__ void recompute_sorted(const int64_t* __restrict__ off, uint2* __restrict__ sval,
+                                 int64_t n, const float* __restrict__ Ub, int k, int t,
+                                 const float* __restrict__ rn, const int32_t* __restrict__ perm,
+                                 const unsigned int* __restrict__ rn_max_bits) {
   const int lane = threadIdx.x & 31;
   constexpr int R = kRecMaxK / 32;
+  const float umax = __uint_as_float(*rn_max_bits);
   for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
        j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t b0 = lower_bound_u32(skey, ncand, (uint32_t)j);
-    const int64_t b1 = lower_bound_u32(skey, ncand, (uint32_t)j + 1u);
+    const int64_t b0 = off[j];
+    const int64_t b1 = off[j + 1];
     if (b0 >= b1) continue;
-    const float* va = V + (int64_t)perm[j] * k;
-    double xa[R], lr[R];
+    // x = s_t - 2 M_j (no filter when the row has at most t candidates)
+    float xcut = -1.f;
+    constexpr int NV = 8;  // screened magnitudes held per lane (rows with <= 256 candidates)
+    if (b1 - b0 > t && b1 - b0 <= 32 * NV) {
+      float av[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const int64_t e = b0 + lane + 32 * q;
+        av[q] = e < b1 ? fabsf(__uint_as_float(sval[e].y)) : -1.f;
+      }
+      float cur = INFINITY;
+      int have = 0;
+      while (have < t) {  // t-th largest with multiplicity, by rounds of warp maxima
+        float mx = -1.f;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) mx = fmaxf(mx, av[q] < cur ? av[q] : -1.f);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int cnt = 0;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) cnt += av[q] == mx;
+        have += __reduce_add_sync(0xffffffffu, cnt);
+        cur = mx;
+        if (mx < 0.f) break;
+      }
+      const float mj = 1.1f * ldexpf(rn[perm[j]] * umax, -10);
+      xcut = cur - 2.f * mj;
+    }
+    const float* ua = Ub + j * k;
+    double xa[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int c = lane + 32 * r;
-      xa[r] = c < k ? (double)va[c] : 0.0;
-      lr[r] = c < k ? lam[c] : 0.0;
+      xa[r] = c < k ? (double)ua[c] : 0.0;
     }
     // four candidates per step: their source-row loads are in flight together
     for (int64_t e0 = b0; e0 < b1; e0 += 4) {
       float xb[4][R];
+      bool keep[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t e = e0 + u < b1 ? e0 + u : b1 - 1;
-        const float* vb = V + (int64_t)perm[sval[e].x] * k;
+        const uint2 cvv = sval[e];
+        keep[u] = e0 + u < b1 && fabsf(__uint_as_float(cvv.y)) >= xcut;
+        const float* vb = Ub + (int64_t)cvv.x * k;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int c = lane + 32 * r;
-          xb[u][r] = c < k ? __ldg(vb + c) : 0.f;
+          xb[u][r] = (keep[u] && c < k) ? __ldg(vb + c) : 0.f;
         }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         double acc = 0.0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) acc += lr[r] * (xa[r] * (double)xb[u][r]);  // exact product, then λ
+        for (int r = 0; r < R; ++r) acc += xa[r] * (double)xb[u][r];  // exact fp32 x fp32 products
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0 && e0 + u < b1) sval[e0 + u].y = __float_as_uint((float)acc);
+        if (lane == 0 && e0 + u < b1) sval[e0 + u].y = __float_as_uint(keep[u] ? (float)acc : 0.f);
       }
     }
   }
@@ -1789,6 +1844,8 @@ struct Work {
   float* thr_p;        // kSym: bounds in permuted (sorted) order [NB*128]
   float* thr_s;        // kSym screening: thr_p lowered by the hi*hi error bound [NB*128]
   float* thr_cmin;     // kSym: minimum of the effective bounds over each 32-column chunk
+  float* Ub;           // kSym screening: U = V diag(sqrt λ) in bound order (re-evaluation)
+  int64_t* roff;       // kSym screening: candidate row offsets of the sorted pool [n+1]
   int32_t* ids;        // kSym: 0..n-1
   int32_t* perm;       // kSym: permuted index -> original id [n]
   float* rn;           // kSym: row norms ||U_i|| [n]
@@ -1821,6 +1878,8 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->thr_p = cv.take<float>(nb * kRowsPerBlock);
   w->thr_s = cv.take<float>(pl.screen ? nb * kRowsPerBlock : 0);
   w->thr_cmin = cv.take<float>(nb * kRowsPerBlock / 32);
+  w->Ub = cv.take<float>(pl.screen ? (size_t)pl.n * pl.k : 0);
+  w->roff = cv.take<int64_t>(pl.screen ? (size_t)pl.n + 1 : 0);
   w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->rn = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
@@ -2084,6 +2143,11 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   chunk_min32<<<(int)std::min<int64_t>((nthr / 32 + 255) / 256, sms * 8), 256, 0, s>>>(
       pl.screen ? w.thr_s : w.thr_p, nthr / 32, w.thr_cmin);
   count_launches(1);
+  if (pl.screen) {
+    gather_u_bound<<<(int)std::min<int64_t>((n * k + 255) / 256, sms * 16), 256, 0, s>>>(
+        V, lambda, w.perm, n, k, w.Ub);
+    count_launches(1);
+  }
   {
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
@@ -2237,9 +2301,11 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                    ncand, 0, ebits, s));
       if (pl.screen) {  // exact values of the screened candidates
+        cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
+            w.skey, ncand, n, w.roff);
         recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-            w.skey, w.sval, ncand, n, w.perm, V, lambda, k);
-        count_launches(1);
+            w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits);
+        count_launches(2);
       }
     }
     if (pl.t <= 5)
@@ -2446,9 +2512,11 @@ extern "C" ggm_status ggm_sparse_precision_sym_shard(
     GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                  ncand, 0, ebits, s));
     if (pl.screen) {  // exact values before the buckets leave this rank
+      cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
+          w.skey, ncand, n, w.roff);
       recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-          w.skey, w.sval, ncand, n, w.perm, V, lambda, k);
-      count_launches(1);
+          w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits);
+      count_launches(2);
     }
   }
   // destination buckets: rank r owns bound-order rows [lo_r, lo_{r+1}); unused pool slots
