@@ -1015,6 +1015,11 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   using G = EpiGeom<EPW>;
   const G g(warp, lane);
   (void)scratch_all;
+#ifdef GGM_EPI_DEBUG
+  const int dbg = dbg;  // 1: skip the filter, 2: skip TMEM loads, 3: no rare path
+#else
+  constexpr int dbg = 0;
+#endif
   const float sd = ldexpf(1.f, -p.sc->exp2);
   const float sd2 = sd * sd;
   const uint32_t lt = (1u << lane) - 1u;
@@ -1039,7 +1044,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
     ti.start(p, u, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s) {
       const int Kh = second ? ti.K1 : ti.K0;
-      const bool live = (!second || ti.h1) && p.dbg != 2;
+      const bool live = (!second || ti.h1) && dbg != 2;
       // off-diagonal blocks emit the transposed direction; for a CTA pair, the diagonal
       // 256x256 super tile covers both directions of its blocks in the row direction
       const bool emit_cols = PAIR ? (ti.K0 >> 1) != ub : Kh != rb;
@@ -1067,7 +1072,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       if (lane == 0) release_tmem<PAIR>(&tempty[buf]);
       buf ^= 1;
       tphase ^= (uint32_t)(buf == 0);
-      if (!live || p.dbg == 1) {
+      if (!live || dbg == 1) {
         if (live && v[0][0] == 12345u && v[G::NC - 1][31] == 54321u) p.row_ptr[0] = (int64_t)v[0][7];
         continue;
       }
@@ -1084,7 +1089,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         __syncwarp();
         if (lane == 0) release_tmem<PAIR>(&tempty[cur_buf]);
       };
-      if (!live || p.dbg == 1) {
+      if (!live || dbg == 1) {
         release_cur();
         continue;
       }
@@ -1113,7 +1118,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         }
         const bool rh = valid && m >= bi;
         const bool ch = valid && m >= cmin[c];
-        if (!__any_sync(0xffffffffu, rh || ch) || p.dbg == 3) continue;  // dbg 3: no rare path
+        if (!__any_sync(0xffffffffu, rh || ch) || dbg == 3) continue;  // dbg 3: no rare path
         // rare path: exact per-entry masks, then each lane walks its own hits
         uint32_t mr = 0, mc = 0;
         if (rh) {
