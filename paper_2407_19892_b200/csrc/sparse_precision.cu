@@ -1030,6 +1030,12 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   const uint32_t trow = tmem_base + ((uint32_t)(g.q * 32) << 16) + (uint32_t)(g.part * G::W);
   const int coff = g.col_off();
   const bool second = g.second();
+  // barrier addresses of both accumulator buffers, computed once: tfull is waited on
+  // locally; tempty lives in the pair leader (remote arrive from the peer CTA)
+  const uint32_t tfull_a0 = smem_u32(&tfull[0]), tfull_a1 = smem_u32(&tfull[1]);
+  const bool remote_rel = PAIR && rank != 0;
+  const uint32_t tempty_a0 = remote_rel ? mbar_map_cluster(&tempty[0], 0) : smem_u32(&tempty[0]);
+  const uint32_t tempty_a1 = remote_rel ? mbar_map_cluster(&tempty[1], 0) : smem_u32(&tempty[1]);
   int buf = 0;
   uint32_t tphase = 0;
   CandCursor cc{0, kCandChunk};
@@ -1055,7 +1061,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #pragma unroll
       for (int c = 0; c < G::NC; ++c)
         cmin[c] = emit_cols ? __ldg(thr_min + (cb >> 5) + c) : INFINITY;
-      mbar_wait(&tfull[buf], tphase);
+      mbar_wait_a(buf ? tfull_a1 : tfull_a0, tphase);
       tc_fence_after();
       const uint32_t taddr = trow + (uint32_t)(buf * kTileN);
 #ifdef GGM_EPI_BLOCK
@@ -1087,7 +1093,13 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       auto release_cur = [&]() {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) release_tmem<PAIR>(&tempty[cur_buf]);
+        if (lane == 0) {
+          const uint32_t ta = cur_buf ? tempty_a1 : tempty_a0;
+          if (remote_rel)
+            mbar_arrive_cluster_a(ta);
+          else
+            mbar_arrive_a(ta);
+        }
       };
       if (!live || dbg == 1) {
         release_cur();
