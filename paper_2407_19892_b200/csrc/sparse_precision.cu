@@ -1016,7 +1016,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   const G g(warp, lane);
   (void)scratch_all;
 #ifdef GGM_EPI_DEBUG
-  const int dbg = dbg;  // 1: skip the filter, 2: skip TMEM loads, 3: no rare path
+  const int dbg = p.dbg;  // 1: skip the filter, 2: skip TMEM loads, 3: no rare path
 #else
   constexpr int dbg = 0;
 #endif
