@@ -257,7 +257,7 @@ typedef struct {
                      many chunks merged afterwards (balances small row ranges) */
   int symmetric;  /* scheme selection, mode 0 over the FULL axis (row_begin = 0, row_end = n)
                      with k <= 128 only (otherwise always plain):
-                     0 = automatic (symmetric for n >= 65536), 1 = symmetric, 2 = plain.
+                     0 = automatic (symmetric for full axes with n >= 16384), 1 = symmetric, 2 = plain.
                      Symmetric scheme (Ψ = Ψ^T): a seed pass over the n/64 columns of
                      largest ||U_j|| (hi·hi products) gives each row i a lower bound b_i of
                      its t-th |ψ| (t-th largest 32-column chunk maximum, minus the hi·hi

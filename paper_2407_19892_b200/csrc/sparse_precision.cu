@@ -77,7 +77,7 @@ struct DevScalars {
   unsigned int rn_max_bits;       // kSym: float bits of max_i ||U_i||
 };
 constexpr int kCandChunk = 4096;
-constexpr int64_t kSymAutoN = 65536;  // automatic symmetric scheme from this axis length  // candidate-pool reservation granularity (entries)
+constexpr int64_t kSymAutoN = 16384;  // automatic symmetric scheme from this axis length (measured crossover 8192-16384)  // candidate-pool reservation granularity (entries)
 
 // ------------------------------------------------------------------ BK1a
 __global__ void absmax_check(const float* __restrict__ V, const double* __restrict__ lam,
