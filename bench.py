@@ -378,7 +378,11 @@ def main():
         plan = plans[a]
         n = V.shape[0]
         if kinds[a] == "symshard":
-            key, val, counts, perm = plan.run(V, lam)
+            thr_all = None
+            if world > 1:  # sharded seed pass: one all-reduce(MIN) of n floats
+                thr_all = plan.seed(V, lam)
+                dist.all_reduce(thr_all, op=dist.ReduceOp.MIN)
+            key, val, counts, perm = plan.run(V, lam, thr_all=thr_all)
             if record:
                 tm = G.last_timing()
                 fused_ms[a].append(tm[1])

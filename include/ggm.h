@@ -312,6 +312,25 @@ ggm_status ggm_sparse_precision_sym_shard(int64_t n, int k, const float *V,
                                           uint32_t *cand_val, int64_t cand_capacity,
                                           int64_t *counts, int32_t *perm, void *workspace,
                                           size_t workspace_bytes, void *stream);
+/* Sharded seed pass (optional; saves each rank the whole seed pass): ggm_sym_seed_shard
+ * writes, into thr_out (DEVICE, n floats), the raw seed values of this rank's equal share of
+ * the row blocks (rows in descending-norm order) and +inf for all other rows; the caller
+ * combines the ranks' arrays by an element-wise minimum (one all-reduce MIN) and passes the
+ * result to ggm_sparse_precision_sym_shard_seeded, which skips the seed pass and is
+ * otherwise identical to ggm_sparse_precision_sym_shard.  Same workspace size.
+ * ggm_sym_seed_shard synchronizes `stream`. */
+ggm_status ggm_sym_seed_shard(int64_t n, int k, const float *V, const double *lambda,
+                              const ggm_sparsify_opts *opts, int rank, int nranks,
+                              float *thr_out, void *workspace, size_t workspace_bytes,
+                              void *stream);
+ggm_status ggm_sparse_precision_sym_shard_seeded(int64_t n, int k, const float *V,
+                                                 const double *lambda,
+                                                 const ggm_sparsify_opts *opts, int rank,
+                                                 int nranks, const float *thr_all,
+                                                 uint32_t *cand_key, uint32_t *cand_val,
+                                                 int64_t cand_capacity, int64_t *counts,
+                                                 int32_t *perm, void *workspace,
+                                                 size_t workspace_bytes, void *stream);
 ggm_status ggm_sym_merge_workspace(int64_t ncand, size_t *bytes);
 ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t *cand_key, const uint32_t *cand_val,
                          int64_t ncand, const int32_t *perm, int64_t row_begin, int64_t row_end,

@@ -37,6 +37,7 @@ EXPORTED = [
     "ggm_sparse_precision_overall_workspace", "ggm_sparse_precision_overall",
     "ggm_overall_last_path",
     "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
+    "ggm_sym_seed_shard", "ggm_sparse_precision_sym_shard_seeded",
     "ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
     "ggm_nonparanormal", "ggm_gram_accumulate_csr_workspace", "ggm_gram_accumulate_csr",
     "ggm_eig_gram_workspace", "ggm_eig_gram", "ggm_project_csr_workspace", "ggm_project_csr",
@@ -122,6 +123,11 @@ def lib() -> C.CDLL:
     L.ggm_sparse_precision_sym_shard.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts), i32,
                                                  i32, vp, vp, i64, C.POINTER(i64), vp, vp,
                                                  C.c_size_t, vp]
+    L.ggm_sym_seed_shard.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts), i32, i32, vp, vp,
+                                     C.c_size_t, vp]
+    L.ggm_sparse_precision_sym_shard_seeded.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts),
+                                                        i32, i32, vp, vp, vp, i64, C.POINTER(i64),
+                                                        vp, vp, C.c_size_t, vp]
     L.ggm_sym_merge_workspace.argtypes = [i64, C.POINTER(C.c_size_t)]
     L.ggm_sym_merge.argtypes = [i64, i32, vp, vp, i64, vp, i64, i64, vp, vp, vp, vp, C.c_size_t, vp]
     L.ggm_sparse_precision_overall_workspace.argtypes = [i64, i32, C.POINTER(OverallOpts), i64,
@@ -161,7 +167,8 @@ def lib() -> C.CDLL:
                  "ggm_gram_eig_rsi_workspace", "ggm_gram_eig_rsi",
                  "ggm_grid_marginals", "ggm_sparse_precision_workspace", "ggm_sparse_precision",
                  "ggm_sparse_precision_sym_shard_workspace", "ggm_sparse_precision_sym_shard",
-                 "ggm_sym_merge_workspace", "ggm_sym_merge"):
+                 "ggm_sym_merge_workspace", "ggm_sym_merge", "ggm_sym_seed_shard",
+                 "ggm_sparse_precision_sym_shard_seeded"):
         getattr(L, name).restype = i32
     _lib = L
     return L
@@ -591,15 +598,34 @@ class SymShardPlan:
         self.perm = torch.empty(self.n, dtype=torch.int32, device=device)
         self.counts = (C.c_int64 * self.nranks)()
 
-    def run(self, V: torch.Tensor, lam: torch.Tensor, stream=None):
-        """Returns (key, val, counts, perm): this rank's candidates sorted by target row,
-        counts per destination rank (list), bound order -> original id."""
+    def seed(self, V: torch.Tensor, lam: torch.Tensor, stream=None) -> torch.Tensor:
+        """This rank's share of the sharded seed pass: raw seed values of its row blocks,
+        +inf elsewhere (combine the ranks' arrays with an element-wise minimum)."""
         _require_cuda(V, torch.float32, "V")
         _require_cuda(lam, torch.float64, "lam")
-        st = lib().ggm_sparse_precision_sym_shard(
-            self.n, self.k, _ptr(V), _ptr(lam), C.byref(self.opts), self.rank, self.nranks,
-            _ptr(self.key), _ptr(self.val), self.cap, self.counts, _ptr(self.perm), _ptr(self.ws),
-            self.ws.numel(), _stream(stream))
+        thr = torch.empty(self.n, dtype=torch.float32, device=V.device)
+        _check(lib().ggm_sym_seed_shard(self.n, self.k, _ptr(V), _ptr(lam), C.byref(self.opts),
+                                        self.rank, self.nranks, _ptr(thr), _ptr(self.ws),
+                                        self.ws.numel(), _stream(stream)))
+        return thr
+
+    def run(self, V: torch.Tensor, lam: torch.Tensor, stream=None, thr_all=None):
+        """Returns (key, val, counts, perm): this rank's candidates sorted by target row,
+        counts per destination rank (list), bound order -> original id.  thr_all: the
+        combined sharded seed (skips this rank's own full seed pass)."""
+        _require_cuda(V, torch.float32, "V")
+        _require_cuda(lam, torch.float64, "lam")
+        if thr_all is None:
+            st = lib().ggm_sparse_precision_sym_shard(
+                self.n, self.k, _ptr(V), _ptr(lam), C.byref(self.opts), self.rank, self.nranks,
+                _ptr(self.key), _ptr(self.val), self.cap, self.counts, _ptr(self.perm),
+                _ptr(self.ws), self.ws.numel(), _stream(stream))
+        else:
+            _require_cuda(thr_all, torch.float32, "thr_all")
+            st = lib().ggm_sparse_precision_sym_shard_seeded(
+                self.n, self.k, _ptr(V), _ptr(lam), C.byref(self.opts), self.rank, self.nranks,
+                _ptr(thr_all), _ptr(self.key), _ptr(self.val), self.cap, self.counts,
+                _ptr(self.perm), _ptr(self.ws), self.ws.numel(), _stream(stream))
         _check(st)
         counts = [int(c) for c in self.counts]
         tot = sum(counts)

@@ -2108,8 +2108,13 @@ static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t
 // descending ||U_i|| order, seed pass over the largest-norm columns -> per-row lower bounds,
 // rows re-ordered by bound (w.perm: bound order -> original id, w.thr_p: bounds), operand
 // re-split in bound order.
+// seed_ulo/seed_uhi >= 0: run only the seed pass over those units, leave the raw per-row seed
+// values (norm order) in w.thr and return (a rank's share of a sharded seed).
+// thr_all != nullptr: skip the seed pass and take the raw seed values of all rows from it.
 static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, const double* lambda,
-                              int64_t n, int k, const FusedParams& fp, cudaStream_t s) {
+                              int64_t n, int k, const FusedParams& fp, cudaStream_t s,
+                              int seed_ulo = -1, int seed_uhi = -1,
+                              const float* thr_all = nullptr) {
   const int sms = num_sms();
   ggm_status st;
     // (1) rows in descending ||U_i|| order (CUB sort of the row norms), split in that order
@@ -2124,21 +2129,33 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
     size_t tb = pl.sort_temp_bytes;
     GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.sort_tmp, tb, w.rn, w.rn_s, w.ids,
                                                            w.perm_n, (int)n, 0, 32, s));
-    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-    split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
-        w.Bop, w.perm_n);
   }
-  count_launches(5);
-  // (2) seed: per row, the t-th largest hi·hi chunk maximum over the first SS column tiles
-  // (the largest-norm columns), minus the hi·hi rounding bound -> lower bound b_i
-  FusedParams sp = fp;
-  sp.kind = kSeed;
-  sp.RB = (int)pl.NBu;
-  sp.SS = pl.SS;
-  sp.thr_out = w.thr;
-  st = launch_fused(sp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
-  if (st != GGM_OK) return st;
+  count_launches(4);
+  if (thr_all) {
+    GGM_CUDA_TRY(cudaMemcpyAsync(w.thr, thr_all, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    {
+      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
+      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
+          w.Bop, w.perm_n);
+      count_launches(1);
+    }
+    // (2) seed: per row, the t-th largest hi·hi chunk maximum over the first SS column
+    // tiles (the largest-norm columns), minus the hi·hi rounding bound -> lower bound b_i
+    FusedParams sp = fp;
+    sp.kind = kSeed;
+    sp.RB = (int)pl.NBu;
+    sp.SS = pl.SS;
+    sp.thr_out = w.thr;
+    if (seed_ulo >= 0) {
+      sp.unit_lo = seed_ulo;
+      sp.unit_hi = seed_uhi;
+    }
+    st = launch_fused(sp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+    if (st != GGM_OK) return st;
+    if (seed_ulo >= 0) return GGM_OK;
+  }
   seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
       w.thr, w.rn_s, &w.sc->rn_max_bits, n, w.sc);
   count_launches(1);
@@ -2469,10 +2486,78 @@ extern "C" ggm_status ggm_sparse_precision_sym_shard_workspace(int64_t n, int k,
   return GGM_OK;
 }
 
+static ggm_status sym_shard_impl(
+    int64_t n, int k, const float* V, const double* lambda, const ggm_sparsify_opts* opts,
+    int rank, int nranks, uint32_t* cand_key, uint32_t* cand_val, int64_t cand_capacity,
+    int64_t* counts, int32_t* perm, void* workspace, size_t workspace_bytes, void* stream,
+    const float* thr_all);
+
 extern "C" ggm_status ggm_sparse_precision_sym_shard(
     int64_t n, int k, const float* V, const double* lambda, const ggm_sparsify_opts* opts,
     int rank, int nranks, uint32_t* cand_key, uint32_t* cand_val, int64_t cand_capacity,
     int64_t* counts, int32_t* perm, void* workspace, size_t workspace_bytes, void* stream) {
+  return sym_shard_impl(n, k, V, lambda, opts, rank, nranks, cand_key, cand_val, cand_capacity,
+                        counts, perm, workspace, workspace_bytes, stream, nullptr);
+}
+
+extern "C" ggm_status ggm_sparse_precision_sym_shard_seeded(
+    int64_t n, int k, const float* V, const double* lambda, const ggm_sparsify_opts* opts,
+    int rank, int nranks, const float* thr_all, uint32_t* cand_key, uint32_t* cand_val,
+    int64_t cand_capacity, int64_t* counts, int32_t* perm, void* workspace,
+    size_t workspace_bytes, void* stream) {
+  if (!thr_all) return fail(GGM_ERR_INVALID_ARGUMENT, "thr_all is NULL");
+  return sym_shard_impl(n, k, V, lambda, opts, rank, nranks, cand_key, cand_val, cand_capacity,
+                        counts, perm, workspace, workspace_bytes, stream, thr_all);
+}
+
+extern "C" ggm_status ggm_sym_seed_shard(int64_t n, int k, const float* V, const double* lambda,
+                                         const ggm_sparsify_opts* opts, int rank, int nranks,
+                                         float* thr_out, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+  if (!V || !lambda || !thr_out || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (nranks < 1 || nranks > GGM_MAX_RANKS || rank < 0 || rank >= nranks)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "rank %d / nranks %d invalid", rank, nranks);
+  Plan pl;
+  ggm_status st = sym_shard_plan(n, k, opts, &pl);
+  if (st != GGM_OK) return st;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  Work w;
+  const size_t need = carve(pl, workspace, &w);
+  if (workspace_bytes < need) return fail(GGM_ERR_INVALID_ARGUMENT, "workspace too small");
+  if (!ggm_device_supported())
+    return fail(GGM_ERR_CUDA, "current device is not compute capability 10.0 (sm_100a)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  reset_launches();
+  const int sms = num_sms();
+  GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
+  {
+    const int64_t total = n * (int64_t)k;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 8));
+    absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
+    scale_finalize<<<1, 1, 0, s>>>(w.sc);
+    count_launches(2);
+  }
+  FusedParams fp = base_params(pl, w, n, 0);
+  // seed units (row blocks, equal work each): an even split
+  const int ulo = (int)(pl.NBu * rank / nranks), uhi = (int)(pl.NBu * (rank + 1) / nranks);
+  st = sym_prepare(pl, w, V, lambda, n, k, fp, s, ulo, uhi);
+  if (st != GGM_OK) return st;
+  GGM_CUDA_TRY(cudaMemcpyAsync(thr_out, w.thr, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  DevScalars hs;
+  GGM_CUDA_TRY(cudaMemcpy(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost));
+  if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
+  if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
+  return GGM_OK;
+}
+
+static ggm_status sym_shard_impl(
+    int64_t n, int k, const float* V, const double* lambda, const ggm_sparsify_opts* opts,
+    int rank, int nranks, uint32_t* cand_key, uint32_t* cand_val, int64_t cand_capacity,
+    int64_t* counts, int32_t* perm, void* workspace, size_t workspace_bytes, void* stream,
+    const float* thr_all) {
   if (!V || !lambda || !cand_key || !cand_val || !counts || !perm || !workspace)
     return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
   if (nranks < 1 || nranks > GGM_MAX_RANKS || rank < 0 || rank >= nranks)
@@ -2507,7 +2592,7 @@ extern "C" ggm_status ggm_sparse_precision_sym_shard(
     count_launches(2);
   }
   FusedParams fp = base_params(pl, w, n, 0);
-  st = sym_prepare(pl, w, V, lambda, n, k, fp, s);
+  st = sym_prepare(pl, w, V, lambda, n, k, fp, s, -1, -1, thr_all);
   if (st != GGM_OK) return st;
   tm.mark(1);
   const int ulo = (int)sym_unit_lo(pl, rank, nranks), uhi = (int)sym_unit_lo(pl, rank + 1, nranks);

@@ -161,8 +161,9 @@ def sharded_symmetric_precision(V, lam, t: int, group=None, shard=None, merge=No
                                 rows_begin=None, gather: bool = True):
     """Distributed symmetric scheme for one axis (include/ggm.h (3b)).
 
-    shard      : (V, λ, t, rank, world) -> (key, val, counts, perm); default libggm
-                 ggm_sparse_precision_sym_shard.
+    shard      : (V, λ, t, rank, world) -> (key, val, counts, perm); default libggm:
+                 this rank's share of the seed pass (ggm_sym_seed_shard), one all-reduce(MIN)
+                 of the n seed values, then ggm_sparse_precision_sym_shard_seeded.
     merge      : (n, t, key, val, perm, row_begin, row_end) -> (row_id, col, val); default
                  libggm ggm_sym_merge.
     rows_begin : (rank) -> first bound-order row owned by rank (default ggm_sym_rows_begin).
@@ -174,7 +175,12 @@ def sharded_symmetric_precision(V, lam, t: int, group=None, shard=None, merge=No
         from . import _ggm as G
         if shard is None:
             def shard(V_, lam_, tt, r, w):
-                return G.SymShardPlan(n, k, tt, r, w, device=V_.device).run(V_, lam_)
+                plan = G.SymShardPlan(n, k, tt, r, w, device=V_.device)
+                thr_all = None
+                if w > 1:  # sharded seed pass, combined by one all-reduce(MIN) of n floats
+                    thr_all = plan.seed(V_, lam_)
+                    dist.all_reduce(thr_all, op=dist.ReduceOp.MIN, group=group)
+                return plan.run(V_, lam_, thr_all=thr_all)
         if merge is None:
             merge = G.sym_merge
         if rows_begin is None:

@@ -22,12 +22,18 @@ def G():
     return G
 
 
-def _simulate(G, V, lam, t, P):
+def _simulate(G, V, lam, t, P, seeded=False):
     n, k = V.shape
+    thr_all = None
+    if seeded:  # sharded seed pass: every rank's share, combined by an element-wise minimum
+        parts = [G.SymShardPlan(n, k, t, r, P).seed(V, lam) for r in range(P)]
+        thr_all = torch.stack(parts).min(dim=0).values
+        for r, part in enumerate(parts):
+            assert torch.isinf(part).any() or P == 1
     shards = []
     for r in range(P):
         plan = G.SymShardPlan(n, k, t, r, P)
-        key, val, counts, perm = plan.run(V, lam)
+        key, val, counts, perm = plan.run(V, lam, thr_all=thr_all)
         torch.cuda.synchronize()
         shards.append((key.clone(), val.clone(), counts, perm.clone()))
     perm = shards[0][3]
@@ -58,7 +64,8 @@ def _simulate(G, V, lam, t, P):
 
 @pytest.mark.parametrize("n,k,t,P", [(3000, 64, 10, 2), (5000, 100, 10, 3), (2600, 48, 5, 5),
                                      (20000, 100, 16, 8), (700, 32, 10, 1)])
-def test_simulated_ranks_equal_single_call(G, n, k, t, P):
+@pytest.mark.parametrize("seeded", [False, True])
+def test_simulated_ranks_equal_single_call(G, n, k, t, P, seeded):
     V, lam = gen.small_factor(4000 + n + P, n, k)
     Vd = torch.from_numpy(V).cuda()
     ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
@@ -66,7 +73,7 @@ def test_simulated_ranks_equal_single_call(G, n, k, t, P):
     torch.cuda.synchronize()
     assert G.last_stats()["scheme"] == "symmetric"
     c, v = c.cpu().numpy(), v.cpu().numpy()
-    c2, v2 = _simulate(G, Vd, ld, t, P)
+    c2, v2 = _simulate(G, Vd, ld, t, P, seeded)
     assert np.array_equal(c, c2)
     np.testing.assert_array_equal(v, v2)
     te = min(t, n - 1)
