@@ -255,8 +255,8 @@ typedef struct {
   float tau;  /* mode 1 only, >= 0 */
   int col_chunks; /* 0 = automatic; else split each row block's column sweep into this
                      many chunks merged afterwards (balances small row ranges) */
-  int symmetric;  /* scheme selection, mode 0 over the FULL axis (row_begin = 0, row_end = n)
-                     with k <= 128 only (otherwise always plain):
+  int symmetric;  /* scheme selection, over the FULL axis (row_begin = 0, row_end = n) with
+                     A resident (otherwise always plain):
                      0 = automatic (symmetric for full axes with n >= 16384), 1 = symmetric, 2 = plain.
                      Symmetric scheme (Ψ = Ψ^T): a seed pass over the n/64 columns of
                      largest ||U_j|| (hi·hi products) gives each row i a lower bound b_i of
@@ -265,7 +265,11 @@ typedef struct {
                      unordered 128x128 block pair is then evaluated once (cyclic window per
                      row block) and entry ψ_ij is kept as a candidate of row i if
                      |ψ| >= b_i and of row j if |ψ| >= b_j; a CUB sort by row and a merge
-                     select each row's top t by (|ψ| desc, j asc).  If the candidate pool
+                     select each row's top t by (|ψ| desc, j asc).  For k <= 128 the main
+                     pass computes hi·hi only, with every threshold lowered by its error
+                     bound, and the candidates are re-evaluated exactly (fp64 sums of the
+                     fp32 inputs) before the selection.  Mode 1 uses τ as every row's bound
+                     (no seed pass; the pool holds 1.25 x capacity).  If the candidate pool
                      fills up, the axis is recomputed with the plain scheme (exact). */
 } ggm_sparsify_opts;
 

@@ -193,6 +193,45 @@ __global__ void screen_bounds(const float* __restrict__ thr_p, const float* __re
   }
 }
 
+__global__ void fill_tau(float* __restrict__ thr, int64_t n, float tau,
+                         const DevScalars* __restrict__ sc) {
+  const float ts = ldexpf(tau, 2 * sc->exp2);  // ψ units -> accumulator units
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    thr[i] = ts;
+}
+// symmetric threshold mode: candidates with |ψ| > τ (exact values) -> COO (original row * n +
+// original column, ψ); count in *count (entries beyond capacity are counted, not written)
+__global__ void sym_threshold_coo(const uint32_t* __restrict__ skey, const uint2* __restrict__ sval,
+                                  int64_t ncand, int64_t n, const int32_t* __restrict__ perm,
+                                  float tau, int64_t capacity, unsigned long long* count,
+                                  int64_t* __restrict__ key_out, float* __restrict__ val_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ncand; base += stride) {
+    const int64_t e = base + threadIdx.x;
+    bool keep = false;
+    uint32_t j = 0;
+    uint2 x = make_uint2(0, 0);
+    if (e < ncand) {
+      j = skey[e];
+      x = sval[e];
+      keep = j != 0xFFFFFFFFu && fabsf(__uint_as_float(x.y)) > tau;
+    }
+    const uint32_t bm = __ballot_sync(0xffffffffu, keep);
+    unsigned long long b0 = 0;
+    if (lane == 0 && bm) b0 = atomicAdd(count, (unsigned long long)__popc(bm));
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (keep) {
+      const int64_t pos = (int64_t)b0 + __popc(bm & ((1u << lane) - 1u));
+      if (pos < capacity) {
+        key_out[pos] = (int64_t)perm[j] * n + perm[x.x];
+        val_out[pos] = __uint_as_float(x.y);
+      }
+    }
+  }
+}
+
 __global__ void chunk_min32(const float* __restrict__ thr, int64_t nchunks,
                             float* __restrict__ out) {
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
@@ -1793,7 +1832,8 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // symmetric scheme (each unordered block pair evaluated once): full axis, top-t mode, A
   // resident; automatic (0) above kSymAutoN rows, where the seed pass and the candidate
   // merge are small against the halved tensor-core work
-  const bool sym_ok = o->mode == 0 && full_axis && pl->resident;
+  // symmetric scheme: per-row top-t (mode 0) or threshold (mode 1, thresholds = τ)
+  const bool sym_ok = (o->mode == 0 || o->mode == 1) && full_axis && pl->resident;
   pl->sym = sym_ok && (o->symmetric == 1 || (o->symmetric == 0 && n >= kSymAutoN)) ? 1 : 0;
   pl->screen = pl->sym && k <= 128 && !getenv("GGM_NO_SCREEN") ? 1 : 0;
   // candidates: ~ t x 16 / 2 per row expected (seed samples 1/16 of the columns, half of
@@ -1818,7 +1858,11 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   {
     const int64_t ratio = (n + pl->SS * kTileN - 1) / (pl->SS * kTileN);
     const int64_t per_row = pl->t * std::max<int64_t>(4, std::min<int64_t>(2 * ratio, 32));
-    pl->cand_total = pl->sym ? n * per_row + (int64_t)sms * 16 * kCandChunk * 2 : 0;
+    // mode 1: every directed entry above τ (minus the screening bound) is a candidate;
+    // room for the output capacity + 25 % (overflow -> exact plain recomputation)
+    const int64_t want = pl->mode == 1 ? std::max<int64_t>(capacity + capacity / 4, int64_t(1) << 20)
+                                       : n * per_row;
+    pl->cand_total = pl->sym ? want + (int64_t)sms * 16 * kCandChunk * 2 : 0;
   }
   pl->sort_temp_bytes = 0;
   if (pl->sym) {
@@ -2131,7 +2175,11 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
                                                            w.perm_n, (int)n, 0, 32, s));
   }
   count_launches(4);
-  if (thr_all) {
+  if (pl.mode == 1) {
+    // threshold mode: every row's bound is τ itself (accumulator units); no seed pass
+    fill_tau<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, n, fp.tau, w.sc);
+    count_launches(1);
+  } else if (thr_all) {
     GGM_CUDA_TRY(cudaMemcpyAsync(w.thr, thr_all, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
   } else {
     {
@@ -2156,9 +2204,11 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
     if (st != GGM_OK) return st;
     if (seed_ulo >= 0) return GGM_OK;
   }
-  seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
-      w.thr, w.rn_s, &w.sc->rn_max_bits, n, w.sc);
-  count_launches(1);
+  if (pl.mode != 1) {
+    seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
+        w.thr, w.rn_s, &w.sc->rn_max_bits, n, w.sc);
+    count_launches(1);
+  }
   // (3) order rows (= columns) by their bound: sort (bound, original id) -> the final
   // permutation and the permuted bounds; re-split in that order, so the 32 columns of
   // every epilogue chunk carry nearly equal bounds
@@ -2270,8 +2320,43 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     }
     GGM_CUDA_TRY(cudaGetLastError());
   }
+  // mode 1 tail (plain scheme, and the symmetric scheme after its candidates became COO):
+  // count, capacity check, sort COO by (row, col), assemble CSR
+  auto mode1_tail = [&]() -> ggm_status {
+    DevScalars hs;
+    GGM_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
+    if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
+    const int64_t count = (int64_t)hs.coo_count;
+    *nnz_out = count;
+    if (count > capacity) {
+      tm.mark(3);
+      tm.finish();
+      return fail(GGM_ERR_CAPACITY, "threshold mode: %lld entries > capacity %lld",
+                  (long long)count, (long long)capacity);
+    }
+    if (count > 0) {
+      size_t tb = pl.coo_temp_bytes;
+      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.key_in, w.key_out, w.cv_in,
+                                                   w.cv_out, count, 0, 64, s));
+      const int blocks = (int)std::min<int64_t>((count + 256) / 256 + 1, sms * 8);
+      coo_to_csr<<<blocks, 256, 0, s>>>(w.key_out, w.cv_out, count, n, pl.rows, row_ptr, col, val);
+      count_launches(1);
+    } else {
+      zero_row_ptr<<<(int)std::min<int64_t>((pl.rows + 256) / 256 + 1, sms * 8), 256, 0, s>>>(
+          row_ptr, pl.rows);
+      count_launches(1);
+    }
+    GGM_CUDA_TRY(cudaGetLastError());
+    tm.mark(3);
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    tm.finish();
+    return GGM_OK;
+  };
   FusedParams fp = base_params(pl, w, n, row_begin);
   if (pl.sym) {
+    fp.tau = pl.mode == 1 ? opts->tau : 0.f;
     st = sym_prepare(pl, w, V, lambda, n, k, fp, s);
     if (st != GGM_OK) return st;
     tm.mark(1);
@@ -2285,6 +2370,51 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
     if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
     const int hovf = hs.cand_overflow;
+    if (pl.mode == 1) {
+      if (hovf) {
+        // pool exhausted: the plain threshold pass (exact) from an un-permuted split
+        const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
+        split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
+            V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
+        count_launches(1);
+        Plan bp = pl;
+        bp.sym = 0;
+        FusedParams op = base_params(bp, w, n, 0);
+        op.row_ptr = row_ptr;
+        op.tau = opts->tau;
+        op.coo_key = w.key_in;
+        op.coo_val = w.cv_in;
+        op.coo_count = &w.sc->coo_count;
+        op.capacity = capacity;
+        st = launch_fused(op, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
+        if (st != GGM_OK) return st;
+        g_stats[0] = 0;
+        g_stats[3] = 1;
+        return mode1_tail();
+      }
+      const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
+      if (ncand > 0) {
+        size_t tb = pl.sort_temp_bytes;
+        int ebits = 1;
+        while ((int64_t(1) << ebits) <= n) ++ebits;
+        GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval,
+                                                     w.sval, ncand, 0, ebits, s));
+        if (pl.screen) {  // exact values of every screened candidate (no top-t filter)
+          cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
+              w.skey, ncand, n, w.roff);
+          recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+              w.roff, w.sval, n, w.Ub, k, INT_MAX, w.rn, w.perm, &w.sc->rn_max_bits);
+          count_launches(2);
+        }
+        sym_threshold_coo<<<(int)std::min<int64_t>((ncand + 255) / 256, sms * 16), 256, 0, s>>>(
+            w.skey, w.sval, ncand, n, w.perm, opts->tau, capacity, &w.sc->coo_count, w.key_in,
+            w.cv_in);
+        count_launches(1);
+      }
+      g_stats[0] = 2;
+      g_stats[2] = (double)ncand;
+      return mode1_tail();
+    }
     if (hovf) {
       // the candidate pool filled up: recompute the whole axis with the plain scheme (exact)
       // from an un-permuted split
@@ -2414,35 +2544,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     return GGM_OK;
   }
   // mode 1: count, capacity check, sort COO by (row, col), assemble CSR
-  GGM_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
-  if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
-  const int64_t count = (int64_t)hs.coo_count;
-  *nnz_out = count;
-  if (count > capacity) {
-    tm.mark(3);
-    tm.finish();
-    return fail(GGM_ERR_CAPACITY, "threshold mode: %lld entries > capacity %lld",
-                (long long)count, (long long)capacity);
-  }
-  if (count > 0) {
-    size_t tb = pl.coo_temp_bytes;
-    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.key_in, w.key_out, w.cv_in,
-                                                 w.cv_out, count, 0, 64, s));
-    const int blocks = (int)std::min<int64_t>((count + 256) / 256 + 1, sms * 8);
-    coo_to_csr<<<blocks, 256, 0, s>>>(w.key_out, w.cv_out, count, n, pl.rows, row_ptr, col, val);
-    count_launches(1);
-  } else {
-    zero_row_ptr<<<(int)std::min<int64_t>((pl.rows + 256) / 256 + 1, sms * 8), 256, 0, s>>>(
-        row_ptr, pl.rows);
-    count_launches(1);
-  }
-  GGM_CUDA_TRY(cudaGetLastError());
-  tm.mark(3);
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  tm.finish();
-  return GGM_OK;
+  return mode1_tail();
 }
 
 // ------------------------------------------------------------------ distributed symmetric scheme

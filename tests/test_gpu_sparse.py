@@ -104,6 +104,27 @@ def test_threshold_mode(G):
     assert e.value.status == 5 and e.value.required == len(c)
 
 
+@pytest.mark.parametrize("n,k,sym,q", [(3000, 64, 1, 0.999), (2500, 150, 1, 0.998),
+                                       (20000, 100, 0, 0.9999), (4000, 32, 1, 0.0)])
+def test_threshold_mode_symmetric(G, n, k, sym, q):
+    """Threshold mode on the symmetric block-pair scheme (τ as every row's bound; hi·hi
+    screening + exact re-evaluation for k <= 128, 3-term for k > 128): the oracle's entries
+    up to ties within tolerance of τ, and the same count as the plain scheme."""
+    import oracle as O
+    V, lam = gen.small_factor(31 + n + k, n, k)
+    rows = np.arange(n) if n <= 4000 else np.arange(0, n, 97)
+    tau = float(np.quantile(np.abs(O.psi_rows(V, lam, rows[:300])).ravel(), q)) if q > 0 else 0.0
+    cap = max(4 * int((1 - q) * n * n) + 4096, 1024) if q > 0 else n * n
+    rp, c, v = _run(G, V, lam, 0, n, mode=1, tau=tau, symmetric=sym, capacity=cap)
+    sub_rp = np.concatenate([[0], np.cumsum([rp[i + 1] - rp[i] for i in rows])])
+    sub_c = np.concatenate([c[rp[i]:rp[i + 1]] for i in rows])
+    sub_v = np.concatenate([v[rp[i]:rp[i + 1]] for i in rows])
+    check_threshold(sub_rp, sub_c, sub_v, V, lam, rows, tau)
+    if n <= 4000:
+        rp2, c2, v2 = _run(G, V, lam, 0, n, mode=1, tau=tau, symmetric=2, capacity=len(c) + 1024)
+        assert abs(len(c2) - len(c)) <= max(2, len(c) // 10000)
+
+
 def test_domain_errors(G):
     n, k = 300, 8
     V, lam = gen.small_factor(1, n, k)
