@@ -99,3 +99,19 @@ def test_symmetric_single_cta_matches_pair(G, monkeypatch):
     assert st["cta_pair"] and not st1["cta_pair"]
     assert np.mean([np.array_equal(c[rp[i]:rp[i + 1]], c1[rp1[i]:rp1[i + 1]]) for i in range(n)]) > 0.999
     check_topk(rp1, c1, v1, V, lam, np.arange(n), t)
+
+
+@pytest.mark.parametrize("k", [1, 7, 16, 33, 64, 128])
+def test_symmetric_screening_rank_edges(G, k):
+    """Screening path over every packing of k (KS full slots + packed tail): tiny k (tail
+    only), exact multiples of 16, and the largest screened rank."""
+    n, t = 3000, 10
+    V, lam = gen.small_factor(900 + k, n, k)
+    Vd = torch.from_numpy(V).cuda()
+    ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
+    rp, c, v = G.ggm_sparse_precision(Vd, ld, 0, n, mode=0, topk=t, symmetric=1)
+    torch.cuda.synchronize()
+    st = G.last_stats()
+    assert st["scheme"] in ("symmetric", "plain")
+    res = check_topk(rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy(), V, lam, np.arange(n), t)
+    assert res["exact"] + res["excused"] == n
