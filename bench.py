@@ -31,7 +31,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "precision entries evaluated+sparsified/sec (n^2 per axis), % of TC roofline"
 UNIT = "entries/s"
-DTYPE = "f16x3 split (hi*hi+hi*lo+lo*hi), f32 accumulate"
+DTYPE = ("f16 hi*hi screening (f32 accumulate, thresholds lowered by its error bound) + "
+         "f64-accumulated exact re-evaluation of the candidates from the f32 inputs")
 WORKLOADS = {
     "C5": "C5: factor-level axes n=1,000,000 and n=30,000 (cell / gene axis of a million-cell "
           "dataset), rank 100, V = QR of N(0,1), lambda ~ LogNormal(0,1), top-10 per row",
