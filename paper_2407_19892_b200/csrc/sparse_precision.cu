@@ -17,6 +17,9 @@
 //                       symmetric (each unordered 128x128 block pair once, cyclic window;
 //                       the transposed direction emits candidates above the seed bound)
 //   BK3  merge_partials / merge_sym / coo_to_csr  CSR assembly
+// The CTA-pair instantiations always keep A resident, so the streamed-A producer loop is
+// statically unreachable there (diagnostic 128).
+#pragma nv_diag_suppress 128
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cuda.h>
@@ -60,7 +63,6 @@ __host__ __device__ constexpr int regs_epi(int EPW) { return EPW == 16 ? 104 : 2
 constexpr int kTmemCols = 512;            // 2 accumulator buffers x 256 columns
 constexpr int kMaxResidentAtoms = 2;
 // A (128 rows x KA atoms x hi/lo) stays resident in shared memory when KA <= 2 (k <= 128)
-constexpr int kEpiWarps = 8;              // list epilogue: 2 warps per TMEM lane quadrant
 constexpr int kScratchBytes = 32 * 1024;  // epilogue shared scratch (per CTA)
 constexpr int kScratchFloats = 32 * 32;   // per warp at 8 epilogue warps (half at 16)
 constexpr int kSeedFrac = 64;  // seed pass: the n/64 largest-norm columns (see make_plan)
