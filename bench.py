@@ -489,8 +489,8 @@ def main():
 
         # Every step uploads its inputs from pinned host memory and reads its CSR back.  The
         # upload of step i+1 runs on a copy stream while step i computes (double-buffered
-        # device inputs), as a streaming service would; the first upload and every
-        # download are on the timed path.
+        # device inputs) and step i's download overlaps step i+1, as a streaming service
+        # would; the first upload and the last download are on the timed path.
         copy_s = torch.cuda.Stream()
         bufs = [[(torch.empty_like(V), torch.empty_like(lam)) for V, lam in dev_axes]
                 for _ in range(2)]
@@ -505,20 +505,37 @@ def main():
                     bufs[slot][a][1].copy_(hL[a], non_blocking=True)
                 ev_in[slot].record(copy_s)
 
+        # downloads: the step's CSR is copied (device to device) into one of two output
+        # slots and read back to pinned host memory on a third stream while the next step
+        # computes
+        dl_s = torch.cuda.Stream()
+        dslots = [[tuple(torch.empty_like(x) for x in o) for o in outs] for _ in range(2)]
+        hslots = [hout, [tuple(torch.empty_like(x).pin_memory() for x in h) for h in hout]]
+        ev_out = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_dl = [torch.cuda.Event(), torch.cuda.Event()]
+
         def e2e_run(nsteps):
             copy_s.wait_stream(stream)   # uploads start after the timing event
+            dl_s.wait_stream(stream)
             upload(0)
             for i in range(nsteps):
                 slot = i % 2
                 if i + 1 < nsteps:
                     upload(1 - slot)
                 stream.wait_event(ev_in[slot])
+                stream.wait_event(ev_dl[slot])   # this output slot's previous download is done
                 for a in range(len(plans)):
-                    rp, col, val = run_axis(a, *bufs[slot][a])
-                    hout[a][0].copy_(rp, non_blocking=True)
-                    hout[a][1].copy_(col, non_blocking=True)
-                    hout[a][2].copy_(val, non_blocking=True)
+                    res = run_axis(a, *bufs[slot][a])
+                    for d, x in zip(dslots[slot][a], res):
+                        d.copy_(x, non_blocking=True)
                 ev_used[slot].record(stream)
+                ev_out[slot].record(stream)
+                with torch.cuda.stream(dl_s):
+                    dl_s.wait_event(ev_out[slot])
+                    for a in range(len(plans)):
+                        for h, d in zip(hslots[slot][a], dslots[slot][a]):
+                            h.copy_(d, non_blocking=True)
+                    ev_dl[slot].record(dl_s)
             torch.cuda.synchronize()
         e2e_run(2)
         if world > 1:
