@@ -131,3 +131,11 @@ def test_overall_at_scale_properties(G):
         cc = c[rp[i]:rp[i + 1]]
         want = O.psi_rows(V, lam, np.array([i]))[0, cc]
         assert np.all(np.abs(v[rp[i]:rp[i + 1]] - want) <= tol(want))
+
+
+def test_overall_spec_rank1_example(G):
+    """v = (1, 1, 0)/√2, λ = 2, d = 3, top_overall(1) -> edge (1, 2, 1.0)."""
+    v = (np.array([[1.0], [1.0], [0.0]]) / np.sqrt(2.0)).astype(np.float32)
+    rp, c, val = _run(G, v, [2.0], 1)
+    assert rp.tolist() == [0, 1, 2, 2] and c.tolist() == [1, 0]
+    assert np.allclose(val, [1.0, 1.0], rtol=1e-6)

@@ -497,3 +497,15 @@ def test_nonparanormal_invariances():
     V, E = O.gram_eig_nonparanormal(X, 1, 5)
     T = O.nonparanormal(X, 1)
     assert np.allclose(np.sort(np.linalg.eigvalsh(T @ T.T))[::-1][:5], E, rtol=1e-12)
+
+
+def test_overall_spec_worked_examples():
+    """SPEC S:316-318 (recompose_threshold examples): Λ = 0 gives the empty graph; the rank-1
+    spectrum v = (1, 1, 0)/√2, λ = 2 on d = 3 has the single off-diagonal ψ_12 = 1 and
+    top_overall(1) yields the edge (1, 2, 1.0) (0-based (0, 1))."""
+    v = np.array([[1.0], [1.0], [0.0]]) / np.sqrt(2.0)
+    ii, jj, vv = O.overall_edges(v, [2.0], 1)
+    assert (ii.tolist(), jj.tolist()) == ([0], [1]) and np.allclose(vv, [1.0], atol=1e-15)
+    V = np.random.default_rng(1).standard_normal((6, 3))
+    ii, jj, vv = O.overall_edges(V, [0.0, 0.0, 0.0], 5, min_edges=2)
+    assert len(ii) == 0
