@@ -105,7 +105,10 @@ ggm_status ggm_gram_eig_rsi(const float *X, int ndim, const int64_t *shape, int 
  * shapes (host), axis_pos[g] = position of axis l in modality g or -1 if absent (its X[g]
  * may then be NULL).  The shared axis must have the same length in every modality that has
  * it.  Output as ggm_gram_eig (V: d_l x k fp32, E: k fp64 descending, trace_S = ||D_l||_F^2);
- * dense path up to a 32768^2 Gram of either side, randomized subspace iteration above. */
+ * dense path up to a 32768^2 Gram of either side, randomized subspace iteration above.
+ * Nonparanormal (COCA) on a shared axis ranks each row of the concatenation D_l: build
+ * D_l as one d_l x Σm matrix and use ggm_nonparanormal(axis 0) + ggm_gram_eig (or the CSR
+ * path with nonparanormal = 1). */
 ggm_status ggm_gram_eig_multi_workspace(int M, const int *ndim, const int64_t *shapes,
                                         const int *axis_pos, int k, size_t *bytes);
 ggm_status ggm_gram_eig_multi(int M, const float *const *X, const int *ndim,
