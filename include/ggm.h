@@ -98,6 +98,16 @@ ggm_status ggm_gram_eig_rsi(const float *X, int ndim, const int64_t *shape, int 
                             double *E, double *trace_S, int *iters_out, double *change_out,
                             void *workspace, size_t workspace_bytes, void *stream);
 
+/* (1g) Both axes of a matrix X (d0 x d1, row-major fp32) from ONE Gram of the shorter side
+ * and one eigensolve (Thm 1 / P:125: the nonzero spectra of X X^T and X^T X coincide, and
+ * the longer side's eigenvectors are X^T W diag(1/σ) or X W diag(1/σ)).  Outputs as
+ * ggm_gram_eig per axis (V0: d0 x k0, E0; V1: d1 x k1, E1; E0[i] = E1[i]); shorter side
+ * <= 32768. */
+ggm_status ggm_gram_eig_matrix_workspace(int64_t d0, int64_t d1, int k0, int k1, size_t *bytes);
+ggm_status ggm_gram_eig_matrix(const float *X, int64_t d0, int64_t d1, int k0, int k1, float *V0,
+                               double *E0, float *V1, double *E1, double *trace_S,
+                               void *workspace, size_t workspace_bytes, void *stream);
+
 /* (1c) Multi-modal spectrum of one shared axis l (Alg. 1 line 2): the top-k left
  * singular vectors of D_l = [mat_l(D^γ1) ... mat_l(D^γΓ)] — the eigenpairs of
  * S_l = Σ_γ mat_l(D^γ) mat_l(D^γ)^T.  M modalities; X[g] (host array of DEVICE pointers)

@@ -38,6 +38,7 @@ EXPORTED = [
     "ggm_overall_last_path",
     "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
     "ggm_sym_seed_shard", "ggm_sparse_precision_sym_shard_seeded",
+    "ggm_gram_eig_matrix_workspace", "ggm_gram_eig_matrix",
     "ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
     "ggm_nonparanormal", "ggm_gram_accumulate_csr_workspace", "ggm_gram_accumulate_csr",
     "ggm_eig_gram_workspace", "ggm_eig_gram", "ggm_project_csr_workspace", "ggm_project_csr",
@@ -123,6 +124,11 @@ def lib() -> C.CDLL:
     L.ggm_sparse_precision_sym_shard.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts), i32,
                                                  i32, vp, vp, i64, C.POINTER(i64), vp, vp,
                                                  C.c_size_t, vp]
+    L.ggm_gram_eig_matrix_workspace.argtypes = [i64, i64, i32, i32, C.POINTER(C.c_size_t)]
+    L.ggm_gram_eig_matrix.argtypes = [vp, i64, i64, i32, i32, vp, vp, vp, vp,
+                                      C.POINTER(C.c_double), vp, C.c_size_t, vp]
+    L.ggm_gram_eig_matrix_workspace.restype = i32
+    L.ggm_gram_eig_matrix.restype = i32
     L.ggm_sym_seed_shard.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts), i32, i32, vp, vp,
                                      C.c_size_t, vp]
     L.ggm_sparse_precision_sym_shard_seeded.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts),
@@ -223,6 +229,27 @@ def ggm_gram_eig(X: torch.Tensor, axis: int, k: int, stream=None):
     _check(lib().ggm_gram_eig(_ptr(X), X.dim(), shape, axis, k, _ptr(V), _ptr(E), C.byref(tr),
                               _ptr(ws), nbytes.value, _stream(stream)))
     return V, E, tr.value
+
+
+def ggm_gram_eig_matrix(X: torch.Tensor, k0: int, k1: int, stream=None):
+    """Both axes of a matrix from one Gram + one eigensolve (include/ggm.h (1g)).
+    Returns (V0, E0, V1, E1, trace)."""
+    _require_cuda(X, torch.float32, "X")
+    if X.dim() != 2:
+        raise ValueError("X must be a matrix")
+    d0, d1 = X.shape
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_gram_eig_matrix_workspace(d0, d1, int(k0), int(k1), C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=X.device)
+    V0 = torch.empty((d0, k0), dtype=torch.float32, device=X.device)
+    V1 = torch.empty((d1, k1), dtype=torch.float32, device=X.device)
+    E0 = torch.empty((k0,), dtype=torch.float64, device=X.device)
+    E1 = torch.empty((k1,), dtype=torch.float64, device=X.device)
+    tr = C.c_double(0.0)
+    _check(lib().ggm_gram_eig_matrix(_ptr(X), d0, d1, int(k0), int(k1), _ptr(V0), _ptr(E0),
+                                     _ptr(V1), _ptr(E1), C.byref(tr), _ptr(ws), nbytes.value,
+                                     _stream(stream)))
+    return V0, E0, V1, E1, tr.value
 
 
 def ggm_gram_eig_rsi(X: torch.Tensor, axis: int, k: int, oversample: int = 0,

@@ -1521,3 +1521,122 @@ extern "C" ggm_status ggm_project_csr(int64_t d, int64_t m, int64_t nnz, const i
   GGM_CUDA_TRY(cudaGetLastError());
   return GGM_OK;
 }
+
+// ------------------------------------------------------------------ both axes of a matrix
+// Thm 1 / P:125: for a matrix X (d0 x d1) the nonzero spectra of S_0 = X X^T and S_1 = X^T X
+// coincide, and the top eigenvectors of the larger Gram are X^T W diag(1/σ) (or X W ...) of
+// the smaller one's.  One Gram of the shorter side + one eigensolve give both axes' factors
+// (the per-axis calls would form and solve the same Gram twice).
+extern "C" ggm_status ggm_gram_eig_matrix_workspace(int64_t d0, int64_t d1, int k0, int k1,
+                                                    size_t* bytes) {
+  if (!bytes) return fail(GGM_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  const int64_t dim = std::min(d0, d1), big = std::max(d0, d1);
+  const int kmax = std::max(k0, k1);
+  if (d0 < 1 || d1 < 1 || k0 < 1 || k1 < 1 || kmax > dim)
+    return fail(GGM_ERR_RANK, "k0=%d, k1=%d not in [1, min(d0, d1)=%lld]", k0, k1, (long long)dim);
+  if (dim > kMaxDenseGram) return fail(GGM_ERR_UNSUPPORTED, "both sides exceed 32768: use ggm_gram_eig (RSI)");
+  cusolverDnHandle_t h = g_handles.solver;
+  if (!h && cusolverDnCreate(&g_handles.solver) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnCreate failed");
+  int lw = 0;
+  if (cusolverDnDsyevd_bufferSize(g_handles.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                  (int)dim, nullptr, (int)dim, nullptr, &lw) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
+  Carve c(nullptr);
+  c.take<double>((size_t)d0 * d1);   // unfolding of the Gram side
+  c.take<double>((size_t)dim * dim); // Gram / eigenvectors
+  c.take<double>(dim);               // eigenvalues
+  c.take<double>(std::max(lw, 1));
+  c.take<int>(4);
+  c.take<double>((size_t)big * kmax);  // V64 (either side)
+  c.take<double>((size_t)big * kmax);  // Vasc
+  c.take<double>(kmax);                // Ek
+  c.take<double>(4);                   // fro
+  *bytes = c.used();
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_gram_eig_matrix(const float* X, int64_t d0, int64_t d1, int k0, int k1,
+                                          float* V0, double* E0, float* V1, double* E1,
+                                          double* trace_S, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
+  if (!X || !V0 || !E0 || !V1 || !E1 || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  size_t need = 0;
+  ggm_status st = ggm_gram_eig_matrix_workspace(d0, d1, k0, k1, &need);
+  if (st != GGM_OK) return st;
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cublasHandle_t hb;
+  cusolverDnHandle_t hs;
+  st = get_handles(s, &hb, &hs);
+  if (st != GGM_OK) return st;
+  const bool g0 = d0 <= d1;  // the Gram is formed on axis 0 (else on axis 1)
+  const int64_t dim = g0 ? d0 : d1, other = g0 ? d1 : d0;
+  const int kmax = std::max(k0, k1);
+  int lw = 0;
+  cusolverDnDsyevd_bufferSize(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)dim,
+                              nullptr, (int)dim, nullptr, &lw);
+  Carve c(workspace);
+  double* Md = c.take<double>((size_t)d0 * d1);
+  double* S = c.take<double>((size_t)dim * dim);
+  double* w = c.take<double>(dim);
+  double* work = c.take<double>(std::max(lw, 1));
+  int* dinfo = c.take<int>(4);
+  double* V64 = c.take<double>((size_t)std::max(d0, d1) * kmax);
+  double* Vasc = c.take<double>((size_t)std::max(d0, d1) * kmax);
+  double* Ek = c.take<double>(kmax);
+  double* fro = c.take<double>(4);
+  const int sms = num_sms();
+  GGM_CUDA_TRY(cudaMemsetAsync(fro, 0, sizeof(double), s));
+  {
+    // Md: dim x other, column-major (rows = the Gram side)
+    const int64_t total = d0 * d1;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 16));
+    if (g0)
+      unfold_f64<<<grid, 256, 0, s>>>(X, 1, d0, d1, Md, fro);
+    else
+      unfold_f64<<<grid, 256, 0, s>>>(X, d0, d1, 1, Md, fro);
+    GGM_CUDA_TRY(cudaGetLastError());
+  }
+  const double one = 1.0, zero = 0.0;
+  if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)dim, (int)other, &one, Md, (int)dim,
+                  &zero, S, (int)dim) != CUBLAS_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cublasDsyrk failed");
+  if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)dim, S, (int)dim, w,
+                       work, lw, dinfo) != CUSOLVER_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed");
+  // the Gram side: its own eigenvectors
+  const int kg = g0 ? k0 : k1;
+  take_topk<<<kg, 256, 0, s>>>(w, S, (int)dim, kg, Ek, V64);
+  sign_and_store<<<kg, 256, 0, s>>>(V64, dim, kg, g0 ? V0 : V1);
+  GGM_CUDA_TRY(cudaMemcpyAsync(g0 ? E0 : E1, Ek, sizeof(double) * kg, cudaMemcpyDeviceToDevice, s));
+  // the other side: Md^T W_k diag(1/σ)
+  const int ko = g0 ? k1 : k0;
+  const double* Zk = S + (size_t)(dim - ko) * dim;
+  if (cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)other, ko, (int)dim, &one, Md, (int)dim, Zk,
+                  (int)dim, &zero, Vasc, (int)other) != CUBLAS_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+  reverse_scale<<<dim3(std::max<int64_t>(1, std::min<int64_t>((other + 255) / 256, 64)), ko), 256, 0, s>>>(
+      w, (int)dim, Vasc, other, ko, Ek, V64);
+  sign_and_store<<<ko, 256, 0, s>>>(V64, other, ko, g0 ? V1 : V0);
+  GGM_CUDA_TRY(cudaMemcpyAsync(g0 ? E1 : E0, Ek, sizeof(double) * ko, cudaMemcpyDeviceToDevice, s));
+  GGM_CUDA_TRY(cudaGetLastError());
+  std::vector<double> hE(kmax);
+  int hinfo = 0;
+  double hfro = 0.0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(hE.data(), w + (dim - kmax), sizeof(double) * kmax, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hfro, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hinfo != 0) return fail(GGM_ERR_CUDA, "cusolverDnDsyevd info=%d", hinfo);
+  if (trace_S) *trace_S = hfro;
+  // ascending: hE[0] is the kmax-th largest, hE[kmax-1] the largest
+  if (!(hE[kmax - 1] > 0.0) || !std::isfinite(hE[kmax - 1]) || !(hE[0] > 1e-12 * hE[kmax - 1]))
+    return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)", hE[0],
+                hE[kmax - 1]);
+  return GGM_OK;
+}

@@ -120,3 +120,23 @@ def test_gram_eig_rank_error(G):
     with pytest.raises(G.GGMError) as e:
         G.ggm_gram_eig(torch.from_numpy(x).cuda(), 0, 4)
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("shape,k0,k1", [((200, 100), 100, 100), ((10000, 2000), 50, 50),
+                                         ((300, 700), 40, 25), ((64, 64), 64, 64)])
+def test_gram_eig_matrix_both_axes(G, shape, k0, k1):
+    """One Gram + one eigensolve for both axes of a matrix equals the per-axis calls and the
+    oracle (Thm 1 / P:125)."""
+    import oracle as O
+    rng = np.random.default_rng(sum(shape))
+    X = rng.standard_normal(shape).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    V0, E0, V1, E1, tr = G.ggm_gram_eig_matrix(Xd, k0, k1)
+    for V, E, axis, k in ((V0, E0, 0, k0), (V1, E1, 1, k1)):
+        Vo, Eo = O.gram_eig(X, axis, k)
+        np.testing.assert_allclose(E.cpu().numpy(), Eo, rtol=1e-9)
+        d = np.abs(np.sum(V.cpu().numpy().astype(np.float64) * Vo, axis=0))
+        assert np.all(1.0 - d[:min(k, 20)] < 1e-5)
+        Vs, Es, _ = G.ggm_gram_eig(Xd, axis, k)
+        np.testing.assert_allclose(E.cpu().numpy(), Es.cpu().numpy(), rtol=1e-10)
+    assert abs(tr - float(np.sum(X.astype(np.float64) ** 2))) < 1e-9 * tr
