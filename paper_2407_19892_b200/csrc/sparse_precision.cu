@@ -1080,6 +1080,9 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   CandCursor cc{0, kCandChunk};
+#ifdef GGM_MMA_PROF
+  long long pe_t0 = clock64(), pe_w = 0, pe_n = 0;
+#endif
   for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
@@ -1102,7 +1105,14 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #pragma unroll
       for (int c = 0; c < G::NC; ++c)
         cmin[c] = emit_cols ? __ldg(thr_min + (cb >> 5) + c) : INFINITY;
+#ifdef GGM_MMA_PROF
+      const long long pe_c = clock64();
+#endif
       mbar_wait_a(buf ? tfull_a1 : tfull_a0, tphase);
+#ifdef GGM_MMA_PROF
+      pe_w += clock64() - pe_c;
+      ++pe_n;
+#endif
       tc_fence_after();
       const uint32_t taddr = trow + (uint32_t)(buf * kTileN);
 #ifdef GGM_EPI_BLOCK
@@ -1146,6 +1156,18 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         release_cur();
         continue;
       }
+#ifdef GGM_EPI_DEBUG
+      if (dbg == 4) {  // loads only: every chunk in registers, release, no filter
+        uint32_t vv[G::NC][32];
+#pragma unroll
+        for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, vv[c]);
+#pragma unroll
+        for (int c = 0; c < G::NC; ++c) tmem_wait_ld(vv[c]);
+        release_cur();
+        if (vv[0][0] == 12345u && vv[G::NC - 1][31] == 54321u) p.row_ptr[0] = (int64_t)vv[0][7];
+        continue;
+      }
+#endif
 #define VC vc
 #endif
 #pragma unroll
@@ -1232,6 +1254,11 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       }
     }
   }
+#ifdef GGM_MMA_PROF
+  if (lane == 0 && (blockIdx.x & 15) == 0 && (warp == kFirstEpiWarp || warp == kFirstEpiWarp + EPW - 1))
+    printf("EPIPROF cta %d warp %d tiles %lld total %lld wait_tfull %lld\n", (int)blockIdx.x, warp,
+           pe_n, clock64() - pe_t0, pe_w);
+#endif
 }
 #undef VC
 
@@ -1434,19 +1461,34 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
       int buf = 0;
       uint32_t tphase = 0;
       int a_iter = 0;
+#ifdef GGM_MMA_PROF
+      long long pr_t0 = clock64(), pr_te = 0, pr_tf = 0, pr_ta = 0, pr_n = 0, pr_c, pr_is = 0;
+#define PROF_W(acc, stmt) do { pr_c = clock64(); stmt; acc += clock64() - pr_c; } while (0)
+#else
+#define PROF_W(acc, stmt) stmt
+#endif
       for (int u = p.unit_lo + u0; u < units; u += ustep) {
         int ub;
         const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         if (resident) {
-          mbar_wait(afull, a_iter & 1);
+          PROF_W(pr_ta, mbar_wait(afull, a_iter & 1));
           tc_fence_after();
         }
         for (int s = 0; s < ntiles; ++s) {
-          mbar_wait(&tempty[buf], tphase ^ 1);
+#ifdef GGM_MMA_PROF
+          ++pr_n;
+#endif
+#if defined(GGM_MMA_NOWAIT)
+          if (0)
+#endif
+          PROF_W(pr_te, mbar_wait(&tempty[buf], tphase ^ 1));
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(buf * kTileN);
           for (int a = 0; a < KA; ++a) {
-            mbar_wait(&full[stage], phase);
+#if defined(GGM_MMA_NOWAIT) && GGM_MMA_NOWAIT > 1
+            if (0)
+#endif
+            PROF_W(pr_tf, mbar_wait(&full[stage], phase));
             tc_fence_after();
             uint8_t* st = sStage + stage * st_bytes;
             uint32_t aHi_s, aLo_s, bHi_s, bLo_s;
@@ -1464,6 +1506,9 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
             // descriptors of the atom bases; K step ks = +2 on the address field (32 B)
             const uint64_t dAh = sw128_desc(aHi_s), dAl = sw128_desc(aLo_s);
             const uint64_t dBh = sw128_desc(bHi_s), dBl = sw128_desc(bLo_s);
+#ifdef GGM_MMA_PROF
+            const long long pr_i0 = clock64();
+#endif
             if (issuer) {
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
@@ -1485,6 +1530,9 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
               mma_commit_any<PAIR>(&empty[stage]);
             }
             __syncwarp();
+#ifdef GGM_MMA_PROF
+            pr_is += clock64() - pr_i0;
+#endif
             if (++stage == NS) {
               stage = 0;
               phase ^= 1;
@@ -1503,6 +1551,12 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
           ++a_iter;
         }
       }
+#ifdef GGM_MMA_PROF
+      if (issuer && (blockIdx.x & 15) == 0)
+        printf("MMAPROF cta %d tiles %lld total %lld tempty %lld full %lld afull %lld issue %lld\n",
+               (int)blockIdx.x, pr_n, clock64() - pr_t0, pr_te, pr_tf, pr_ta, pr_is);
+#endif
+#undef PROF_W
     }
   }
   tc_fence_before();
