@@ -192,6 +192,12 @@ def stage_timings(G, torch):
             _, E, _ = G.ggm_gram_eig(X, a, k)
             gram_ms.append((time.perf_counter() - t0) * 1e3)
             Es.append(E)
+        if X.dim() > 2:                           # all axes, concurrent eigensolves ((1h))
+            G.ggm_gram_eig_axes(X, ks)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            G.ggm_gram_eig_axes(X, ks)
+            out.setdefault("gram_eig_axes_ms", {})[name] = (time.perf_counter() - t0) * 1e3
         if X.dim() == 2:                          # both axes from one Gram (include/ggm.h (1g))
             G.ggm_gram_eig_matrix(X, ks[0], ks[1])
             torch.cuda.synchronize()

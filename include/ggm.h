@@ -98,6 +98,17 @@ ggm_status ggm_gram_eig_rsi(const float *X, int ndim, const int64_t *shape, int 
                             double *E, double *trace_S, int *iters_out, double *change_out,
                             void *workspace, size_t workspace_bytes, void *stream);
 
+/* (1h) Every axis of one tensor (Alg. 1 lines 1-4 for l = 0 .. ndim-1): the same results as
+ * ndim ggm_gram_eig calls (V[a]: shape[a] x k[a], E[a]: k[a]), but the per-axis Gram
+ * eigensolves run concurrently on library-owned side streams forked from and joined back onto
+ * `stream` (cuSOLVER's reduction of a few-hundred-square Gram is latency-bound).  Workspace:
+ * the per-axis workspaces, each 256-byte aligned, back to back.  Synchronises `stream`.
+ * Errors as ggm_gram_eig (the first failing axis). */
+ggm_status ggm_gram_eig_axes_workspace(int ndim, const int64_t *shape, const int *k, size_t *bytes);
+ggm_status ggm_gram_eig_axes(const float *X, int ndim, const int64_t *shape, const int *k,
+                             float *const *V, double *const *E, double *trace_S, void *workspace,
+                             size_t workspace_bytes, void *stream);
+
 /* (1g) Both axes of a matrix X (d0 x d1, row-major fp32) from ONE Gram of the shorter side
  * and one eigensolve (Thm 1 / P:125: the nonzero spectra of X X^T and X^T X coincide, and
  * the longer side's eigenvectors are X^T W diag(1/σ) or X W diag(1/σ)).  Outputs as

@@ -12,7 +12,7 @@ Public API (thin bindings of libggm.so, include/ggm.h):
                        (plain scheme) or the distributed symmetric scheme with an all-to-all
 """
 from ._ggm import (GGMError, SparsePlan, device_supported, ggm_gram_eig, ggm_gram_eig_rsi,
-                   ggm_gram_eig_multi, ggm_gram_eig_matrix, ggm_solve_eigvals_multi, ggm_gram_eig_csr, ggm_nonparanormal,
+                   ggm_gram_eig_multi, ggm_gram_eig_matrix, ggm_gram_eig_axes, ggm_solve_eigvals_multi, ggm_gram_eig_csr, ggm_nonparanormal,
                    gram_accumulate_csr, eig_gram, project_csr,
                    ggm_grid_marginals,
                    ggm_solve_eigvals, ggm_sparse_precision, ggm_sparse_precision_overall, overall_last_path, overall_last_timing, last_launches, last_stats, last_timing, lib,
@@ -20,7 +20,7 @@ from ._ggm import (GGMError, SparsePlan, device_supported, ggm_gram_eig, ggm_gra
                    version, EXPORTED, MAX_TOPK)
 
 __all__ = ["GGMError", "SparsePlan", "device_supported", "ggm_gram_eig", "ggm_gram_eig_rsi",
-           "ggm_gram_eig_multi", "ggm_gram_eig_matrix", "ggm_solve_eigvals_multi", "ggm_gram_eig_csr", "ggm_nonparanormal",
+           "ggm_gram_eig_multi", "ggm_gram_eig_matrix", "ggm_gram_eig_axes", "ggm_solve_eigvals_multi", "ggm_gram_eig_csr", "ggm_nonparanormal",
            "gram_accumulate_csr", "eig_gram", "project_csr",
            "ggm_grid_marginals",
            "ggm_solve_eigvals", "ggm_sparse_precision", "ggm_sparse_precision_overall", "overall_last_path", "overall_last_timing", "last_launches", "last_stats", "last_timing", "lib", "set_timing",

@@ -39,6 +39,7 @@ EXPORTED = [
     "ggm_gram_eig_multi_workspace", "ggm_gram_eig_multi", "ggm_solve_eigvals_multi",
     "ggm_sym_seed_shard", "ggm_sparse_precision_sym_shard_seeded",
     "ggm_gram_eig_matrix_workspace", "ggm_gram_eig_matrix",
+    "ggm_gram_eig_axes_workspace", "ggm_gram_eig_axes",
     "ggm_gram_eig_csr_workspace", "ggm_gram_eig_csr", "ggm_nonparanormal_workspace",
     "ggm_nonparanormal", "ggm_gram_accumulate_csr_workspace", "ggm_gram_accumulate_csr",
     "ggm_eig_gram_workspace", "ggm_eig_gram", "ggm_project_csr_workspace", "ggm_project_csr",
@@ -127,6 +128,12 @@ def lib() -> C.CDLL:
     L.ggm_gram_eig_matrix_workspace.argtypes = [i64, i64, i32, i32, C.POINTER(C.c_size_t)]
     L.ggm_gram_eig_matrix.argtypes = [vp, i64, i64, i32, i32, vp, vp, vp, vp,
                                       C.POINTER(C.c_double), vp, C.c_size_t, vp]
+    L.ggm_gram_eig_axes_workspace.argtypes = [i32, C.POINTER(i64), C.POINTER(i32),
+                                              C.POINTER(C.c_size_t)]
+    L.ggm_gram_eig_axes.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(i32), C.POINTER(vp),
+                                    C.POINTER(vp), C.POINTER(C.c_double), vp, C.c_size_t, vp]
+    L.ggm_gram_eig_axes_workspace.restype = i32
+    L.ggm_gram_eig_axes.restype = i32
     L.ggm_gram_eig_matrix_workspace.restype = i32
     L.ggm_gram_eig_matrix.restype = i32
     L.ggm_sym_seed_shard.argtypes = [i64, i32, vp, vp, C.POINTER(SparsifyOpts), i32, i32, vp, vp,
@@ -229,6 +236,28 @@ def ggm_gram_eig(X: torch.Tensor, axis: int, k: int, stream=None):
     _check(lib().ggm_gram_eig(_ptr(X), X.dim(), shape, axis, k, _ptr(V), _ptr(E), C.byref(tr),
                               _ptr(ws), nbytes.value, _stream(stream)))
     return V, E, tr.value
+
+
+def ggm_gram_eig_axes(X: torch.Tensor, ks, stream=None):
+    """Every axis of X at once (include/ggm.h (1h)): [(V_a, E_a)], trace."""
+    _require_cuda(X, torch.float32, "X")
+    nd = X.dim()
+    if len(ks) != nd:
+        raise ValueError("one k per axis")
+    shp = (C.c_int64 * nd)(*X.shape)
+    kk = (C.c_int32 * nd)(*[int(k) for k in ks])
+    nbytes = C.c_size_t(0)
+    _check(lib().ggm_gram_eig_axes_workspace(nd, shp, kk, C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=X.device)
+    Vs = [torch.empty((X.shape[a], int(ks[a])), dtype=torch.float32, device=X.device)
+          for a in range(nd)]
+    Es = [torch.empty((int(ks[a]),), dtype=torch.float64, device=X.device) for a in range(nd)]
+    vp_arr = (C.c_void_p * nd)(*[_ptr(v) for v in Vs])
+    ep_arr = (C.c_void_p * nd)(*[_ptr(e) for e in Es])
+    tr = C.c_double(0.0)
+    _check(lib().ggm_gram_eig_axes(_ptr(X), nd, shp, kk, vp_arr, ep_arr, C.byref(tr), _ptr(ws),
+                                   nbytes.value, _stream(stream)))
+    return list(zip(Vs, Es)), tr.value
 
 
 def ggm_gram_eig_matrix(X: torch.Tensor, k0: int, k1: int, stream=None):

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "ggm_internal.h"
@@ -466,6 +467,8 @@ static ggm_status dense_core(const GPlan& g, int lwork, double* Md, double* S, d
                              double* work, int* dinfo, double* V64, double* fro, double* Ek,
                              double* Vasc, float* V, double* E, double* trace_S,
                              cublasHandle_t hb, cusolverDnHandle_t hs, cudaStream_t s);
+static ggm_status enqueue_unfold(const GPlan& g, const float* X, const int64_t* shape, int axis,
+                                 double* Md, double* fro, cudaStream_t s);
 
 extern "C" ggm_status ggm_gram_eig_workspace(int ndim, const int64_t* shape, int axis, int k,
                                              size_t* bytes) {
@@ -511,6 +514,14 @@ extern "C" ggm_status ggm_gram_eig(const float* X, int ndim, const int64_t* shap
   if (workspace_bytes < need)
     return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
 
+  st = enqueue_unfold(g, X, shape, axis, Md, fro, s);
+  if (st != GGM_OK) return st;
+  return dense_core(g, lwork, Md, S, w, work, dinfo, V64, fro, Ek, Vasc, V, E, trace_S, hb, hs, s);
+}
+
+// fro = 0, then the unfolding GPlan g asks for (matrix other side: the transposed view).
+static ggm_status enqueue_unfold(const GPlan& g, const float* X, const int64_t* shape, int axis,
+                                 double* Md, double* fro, cudaStream_t s) {
   GGM_CUDA_TRY(cudaMemsetAsync(fro, 0, sizeof(double), s));
   const int sms = num_sms();
   {
@@ -532,23 +543,40 @@ extern "C" ggm_status ggm_gram_eig(const float* X, int ndim, const int64_t* shap
     unfold_f64<<<grid, 256, 0, s>>>(X, pre_n, d, post_n, Md, fro);
     GGM_CUDA_TRY(cudaGetLastError());
   }
-  return dense_core(g, lwork, Md, S, w, work, dinfo, V64, fro, Ek, Vasc, V, E, trace_S, hb, hs, s);
+  return GGM_OK;
 }
 
-// Gram + eigensolve + top-k mapping on the unfolding already in Md (GPlan g decides the side).
-static ggm_status dense_core(const GPlan& g, int lwork, double* Md, double* S, double* w,
-                             double* work, int* dinfo, double* V64, double* fro, double* Ek,
-                             double* Vasc, float* V, double* E, double* trace_S,
-                             cublasHandle_t hb, cusolverDnHandle_t hs, cudaStream_t s) {
+// Lower triangle of the fp64 Gram S = M M^T (trans = N, M dim x inner, leading dim ld) or
+// S = M^T M (trans = T, M inner x dim).  A long inner dimension leaves DSYRK's dim^2/2 output
+// tiles too few for the SMs (C3: 78 tiles of 32 x 32 over K = 60,000); the full DGEMM, whose
+// heuristics split K, is faster there despite computing both triangles.
+static cublasStatus_t gram_lower(cublasHandle_t hb, cublasOperation_t trans, int dim,
+                                 int64_t inner, const double* M, int ld, double* S) {
+  const double one = 1.0, zero = 0.0;
+  static const bool syrk_only = std::getenv("GGM_GRAM_SYRK") != nullptr;  // A/B hook
+  if (!syrk_only && inner >= 32 * (int64_t)dim)
+    return trans == CUBLAS_OP_N
+               ? cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, dim, dim, (int)inner, &one, M, ld, M,
+                             ld, &zero, S, dim)
+               : cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, dim, dim, (int)inner, &one, M, ld, M,
+                             ld, &zero, S, dim);
+  return cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, trans, dim, (int)inner, &one, M, ld, &zero, S,
+                     dim);
+}
+
+// Gram + eigensolve + top-k mapping on the unfolding already in Md (GPlan g decides the side);
+// device work only (dense_check reads the status back).
+static ggm_status dense_enqueue(const GPlan& g, int lwork, double* Md, double* S, double* w,
+                                double* work, int* dinfo, double* V64, double* Ek, double* Vasc,
+                                float* V, double* E, cublasHandle_t hb, cusolverDnHandle_t hs,
+                                cudaStream_t s) {
   const double one = 1.0, zero = 0.0;
   cublasStatus_t bs;
   if (g.mode == 2)  // S = M^T M  (m x m), M is d x m column-major
-    bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)g.dim, (int)g.Md_rows, &one, Md,
-                     (int)g.Md_rows, &zero, S, (int)g.dim);
+    bs = gram_lower(hb, CUBLAS_OP_T, (int)g.dim, g.Md_rows, Md, (int)g.Md_rows, S);
   else              // S = M M^T  (Md_rows x Md_rows)
-    bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)g.dim, (int)g.Md_cols, &one, Md,
-                     (int)g.Md_rows, &zero, S, (int)g.dim);
-  if (bs != CUBLAS_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cublasDsyrk failed (%d)", (int)bs);
+    bs = gram_lower(hb, CUBLAS_OP_N, (int)g.dim, g.Md_cols, Md, (int)g.Md_rows, S);
+  if (bs != CUBLAS_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "Gram product failed (%d)", (int)bs);
   cusolverStatus_t ss = cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                          (int)g.dim, S, (int)g.dim, w, work, lwork, dinfo);
   if (ss != CUSOLVER_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed (%d)", (int)ss);
@@ -573,6 +601,12 @@ static ggm_status dense_core(const GPlan& g, int lwork, double* Md, double* S, d
   sign_and_store<<<g.k, 256, 0, s>>>(V64, g.d, g.k, V);
   GGM_CUDA_TRY(cudaGetLastError());
   GGM_CUDA_TRY(cudaMemcpyAsync(E, Ek, sizeof(double) * g.k, cudaMemcpyDeviceToDevice, s));
+  return GGM_OK;
+}
+
+// Synchronises s; solver status, trace, rank check.
+static ggm_status dense_check(const GPlan& g, const int* dinfo, const double* fro, const double* Ek,
+                              double* trace_S, cudaStream_t s) {
   std::vector<double> hE(g.k);
   int hinfo = 0;
   double hfro = 0.0;
@@ -586,6 +620,15 @@ static ggm_status dense_core(const GPlan& g, int lwork, double* Md, double* S, d
     return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)",
                 hE[g.k - 1], hE[0]);
   return GGM_OK;
+}
+
+static ggm_status dense_core(const GPlan& g, int lwork, double* Md, double* S, double* w,
+                             double* work, int* dinfo, double* V64, double* fro, double* Ek,
+                             double* Vasc, float* V, double* E, double* trace_S,
+                             cublasHandle_t hb, cusolverDnHandle_t hs, cudaStream_t s) {
+  ggm_status st = dense_enqueue(g, lwork, Md, S, w, work, dinfo, V64, Ek, Vasc, V, E, hb, hs, s);
+  if (st != GGM_OK) return st;
+  return dense_check(g, dinfo, fro, Ek, trace_S, s);
 }
 
 // ------------------------------------------------------------------ multi-modal spectrum
@@ -1603,9 +1646,8 @@ extern "C" ggm_status ggm_gram_eig_matrix(const float* X, int64_t d0, int64_t d1
     GGM_CUDA_TRY(cudaGetLastError());
   }
   const double one = 1.0, zero = 0.0;
-  if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)dim, (int)other, &one, Md, (int)dim,
-                  &zero, S, (int)dim) != CUBLAS_STATUS_SUCCESS)
-    return fail(GGM_ERR_CUDA, "cublasDsyrk failed");
+  if (gram_lower(hb, CUBLAS_OP_N, (int)dim, other, Md, (int)dim, S) != CUBLAS_STATUS_SUCCESS)
+    return fail(GGM_ERR_CUDA, "Gram product failed");
   if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)dim, S, (int)dim, w,
                        work, lw, dinfo) != CUSOLVER_STATUS_SUCCESS)
     return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed");
@@ -1638,5 +1680,145 @@ extern "C" ggm_status ggm_gram_eig_matrix(const float* X, int64_t d0, int64_t d1
   if (!(hE[kmax - 1] > 0.0) || !std::isfinite(hE[kmax - 1]) || !(hE[0] > 1e-12 * hE[kmax - 1]))
     return fail(GGM_ERR_RANK, "E_k=%.3e <= 1e-12 E_1=%.3e: k exceeds the rank (S:140)", hE[0],
                 hE[kmax - 1]);
+  return GGM_OK;
+}
+
+// ------------------------------------------------------------------ every axis at once
+// Alg. 1 lines 1-4 for all axes of one tensor.  The per-axis eigensolves (cuSOLVER's
+// tridiagonal reduction of a few-hundred-square Gram is latency-bound: ~10 sequential
+// kernels of a few CTAs) run concurrently on side streams forked from `stream`; every
+// axis has its own workspace segment and handles, results are joined back onto `stream`.
+namespace {
+constexpr int kAxisStreams = 4;
+struct AxisPool {
+  cudaStream_t s[kAxisStreams] = {};
+  cudaEvent_t ev[kAxisStreams + 1] = {};
+  cublasHandle_t b[kAxisStreams] = {};
+  cusolverDnHandle_t so[kAxisStreams] = {};
+  bool ready = false;
+  ~AxisPool() {
+    for (int i = 0; i < kAxisStreams; ++i) {
+      if (b[i]) cublasDestroy(b[i]);
+      if (so[i]) cusolverDnDestroy(so[i]);
+    }
+    // streams and events are reclaimed with the context
+  }
+};
+thread_local AxisPool g_axis_pool;
+
+ggm_status axis_pool(AxisPool** out) {
+  AxisPool& P = g_axis_pool;
+  if (!P.ready) {
+    for (int i = 0; i < kAxisStreams; ++i) {
+      GGM_CUDA_TRY(cudaStreamCreateWithFlags(&P.s[i], cudaStreamNonBlocking));
+      if (cublasCreate(&P.b[i]) != CUBLAS_STATUS_SUCCESS ||
+          cusolverDnCreate(&P.so[i]) != CUSOLVER_STATUS_SUCCESS ||
+          cublasSetStream(P.b[i], P.s[i]) != CUBLAS_STATUS_SUCCESS ||
+          cusolverDnSetStream(P.so[i], P.s[i]) != CUSOLVER_STATUS_SUCCESS)
+        return fail(GGM_ERR_CUDA, "axis stream handles");
+    }
+    for (int i = 0; i <= kAxisStreams; ++i)
+      GGM_CUDA_TRY(cudaEventCreateWithFlags(&P.ev[i], cudaEventDisableTiming));
+    P.ready = true;
+  }
+  *out = &P;
+  return GGM_OK;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+}  // namespace
+
+extern "C" ggm_status ggm_gram_eig_axes_workspace(int ndim, const int64_t* shape, const int* k,
+                                                  size_t* bytes) {
+  if (!bytes || !shape || !k) return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  size_t tot = 0;
+  for (int a = 0; a < ndim; ++a) {
+    size_t b = 0;
+    ggm_status st = ggm_gram_eig_workspace(ndim, shape, a, k[a], &b);
+    if (st != GGM_OK) return st;
+    tot += align256(b);
+  }
+  *bytes = tot;
+  return GGM_OK;
+}
+
+extern "C" ggm_status ggm_gram_eig_axes(const float* X, int ndim, const int64_t* shape,
+                                        const int* k, float* const* V, double* const* E,
+                                        double* trace_S, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
+  if (!X || !shape || !k || !V || !E || !workspace)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  size_t need = 0;
+  ggm_status st = ggm_gram_eig_axes_workspace(ndim, shape, k, &need);
+  if (st != GGM_OK) return st;
+  if (workspace_bytes < need)
+    return fail(GGM_ERR_INVALID_ARGUMENT, "workspace %zu < required %zu", workspace_bytes, need);
+  for (int a = 0; a < ndim; ++a)
+    if (!V[a] || !E[a]) return fail(GGM_ERR_INVALID_ARGUMENT, "null V/E for axis %d", a);
+  cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+  AxisPool* P = nullptr;
+  st = axis_pool(&P);
+  if (st != GGM_OK) return st;
+  std::vector<GPlan> g(ndim);
+  std::vector<int> lwork(ndim, 0);
+  std::vector<size_t> off(ndim, 0);
+  std::vector<char> dense(ndim, 0);
+  size_t at = 0;
+  for (int a = 0; a < ndim; ++a) {
+    st = make_gplan(ndim, shape, a, k[a], &g[a]);
+    if (st != GGM_OK) return st;
+    size_t b = 0;
+    ggm_gram_eig_workspace(ndim, shape, a, k[a], &b);
+    off[a] = at;
+    at += align256(b);
+    dense[a] = g[a].dim <= kMaxDenseGram;
+    if (dense[a]) {
+      st = query_lwork(g[a], &lwork[a]);
+      if (st != GGM_OK) return st;
+    }
+  }
+  // fork: every side stream starts after the work already queued on `stream`
+  GGM_CUDA_TRY(cudaEventRecord(P->ev[kAxisStreams], s0));
+  const int nside = std::min(ndim, kAxisStreams);
+  for (int i = 0; i < nside; ++i) GGM_CUDA_TRY(cudaStreamWaitEvent(P->s[i], P->ev[kAxisStreams], 0));
+  struct Ptrs { double *Md, *S, *w, *work, *V64, *fro, *Ek, *Vasc; int* dinfo; };
+  std::vector<Ptrs> pp(ndim);
+  ggm_status first = GGM_OK;
+  for (int a = 0; a < ndim && first == GGM_OK; ++a) {
+    if (!dense[a]) continue;
+    const int i = a % kAxisStreams;
+    Ptrs& q = pp[a];
+    gcarve(g[a], lwork[a], static_cast<char*>(workspace) + off[a], &q.Md, &q.S, &q.w, &q.work,
+           &q.dinfo, &q.V64, &q.fro, &q.Ek, &q.Vasc);
+    st = enqueue_unfold(g[a], X, shape, a, q.Md, q.fro, P->s[i]);
+    if (st == GGM_OK)
+      st = dense_enqueue(g[a], lwork[a], q.Md, q.S, q.w, q.work, q.dinfo, q.V64, q.Ek, q.Vasc,
+                         V[a], E[a], P->b[i], P->so[i], P->s[i]);
+    if (st != GGM_OK) first = st;
+  }
+  // status checks (each synchronises its own side stream while the others keep running)
+  double tr = 0.0;
+  for (int a = 0; a < ndim && first == GGM_OK; ++a) {
+    if (!dense[a]) continue;
+    st = dense_check(g[a], pp[a].dinfo, pp[a].fro, pp[a].Ek, &tr, P->s[a % kAxisStreams]);
+    if (st != GGM_OK) first = st;
+  }
+  // join back onto `stream`
+  for (int i = 0; i < nside; ++i) {
+    GGM_CUDA_TRY(cudaEventRecord(P->ev[i], P->s[i]));
+    GGM_CUDA_TRY(cudaStreamWaitEvent(s0, P->ev[i], 0));
+  }
+  if (first != GGM_OK) return first;
+  // axes beyond the dense Gram: randomized subspace iteration on `stream`
+  for (int a = 0; a < ndim; ++a) {
+    if (dense[a]) continue;
+    st = ggm_gram_eig(X, ndim, shape, a, k[a], V[a], E[a], &tr,
+                      static_cast<char*>(workspace) + off[a],
+                      (a + 1 < ndim ? off[a + 1] : need) - off[a], stream);
+    if (st != GGM_OK) return st;
+  }
+  if (trace_S) *trace_S = tr;
   return GGM_OK;
 }

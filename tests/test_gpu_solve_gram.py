@@ -140,3 +140,28 @@ def test_gram_eig_matrix_both_axes(G, shape, k0, k1):
         Vs, Es, _ = G.ggm_gram_eig(Xd, axis, k)
         np.testing.assert_allclose(E.cpu().numpy(), Es.cpu().numpy(), rtol=1e-10)
     assert abs(tr - float(np.sum(X.astype(np.float64) ** 2))) < 1e-9 * tr
+
+
+@pytest.mark.parametrize("cfg_name", ["C1", "C3"])
+def test_gram_eig_axes_concurrent(G, cfg_name):
+    """Every axis at once on side streams (include/ggm.h (1h)) equals the per-axis calls
+    (same kernels; the trace and library reductions may sum in another order) and the
+    oracle's spectra."""
+    cfg = gen.config(cfg_name)
+    X = cfg["X"]
+    Xd = torch.from_numpy(X).cuda()
+    res, tr = G.ggm_gram_eig_axes(Xd, cfg["k"])
+    for a, (V, E) in enumerate(res):
+        Vs, Es, trs = G.ggm_gram_eig(Xd, a, cfg["k"][a])
+        np.testing.assert_allclose(E.cpu().numpy(), Es.cpu().numpy(), rtol=1e-11)
+        assert float((V - Vs).abs().max()) <= 1e-5
+        assert abs(tr - trs) <= 1e-12 * trs
+        _, Eo = O.gram_eig(X, a, min(cfg["k"][a], 20))
+        np.testing.assert_allclose(E.cpu().numpy()[:len(Eo)], Eo, rtol=1e-9)
+
+
+def test_gram_eig_axes_rank_error(G):
+    x = np.random.default_rng(3).standard_normal((6, 5, 4)).astype(np.float32)
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_gram_eig_axes(torch.from_numpy(x).cuda(), [6, 5, 5])  # k_2 = 5 > d_2 = 4
+    assert e.value.status_name == "GGM_ERR_RANK"
