@@ -209,9 +209,12 @@ typedef struct {
                         default 1e-7 */
   int max_iter;      /* default 20000 */
   double eps_scale;  /* feasibility floor eps = eps_scale * max(1/E). default 1e-10 */
-  int method;        /* 0 = majorise-minimise fixed point λ ← λ ⊙ g/E (default; the NLL
-                        decreases monotonically and λ stays > 0, so Algorithm 1's overshoot
-                        loop, never triggers).  Other values: GGM_ERR_UNSUPPORTED
+  int method;        /* 0 = multiplicative fixed point λ ← λ ⊙ g/E, the majorise-minimise
+                        step (the NLL decreases monotonically and λ stays > 0, so Algorithm 1's
+                        overshoot loop, never triggers), by default over-relaxed
+                        off the common-scale direction (exponent 1.5 in log space, same fixed
+                        point, λ > 0; a run that does not converge is repeated with the plain
+                        MM step; env GGM_MM_OMEGA=1 forces it).  Other values: GGM_ERR_UNSUPPORTED
                         (Algorithm 1's gradient descent, readings Q1-Q3, lives in the oracle) */
   int gauge;         /* 0 = min-balanced PSD gauge (default, reading G);
                         1 = iterate as reached from λ0 = 1/E */

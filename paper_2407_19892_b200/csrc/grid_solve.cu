@@ -10,6 +10,9 @@
 // majorise-minimise step for the NLL (Jensen on -log s with weights λ_l[j_l]/s_j gives a
 // separable majoriser whose minimiser is exactly λ g / E), so the NLL decreases
 // monotonically and λ stays > 0: Algorithm 1's feasibility loop never triggers.
+// By default the step is over-relaxed, λ ← λ ⊙ (g / E)^1.5 off the common-scale direction
+// (same fixed point, λ still > 0, 20-37 % fewer iterations), with a plain-MM rerun if that
+// does not converge (mm_omega).
 // The whole loop runs in ONE cooperative persistent kernel: per iteration a grid pass
 // (per-block partial marginals), grid.sync, a per-entry reduction + update + stationarity
 // max, grid.sync.
@@ -24,6 +27,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -163,6 +167,18 @@ __device__ __forceinline__ void load_lambda(const double* lam, int total, double
 
 constexpr int kMaxMods = 8;  // modalities of a multi-modal solve
 
+// Exponent ω of the multiplicative update λ <- λ ⊙ (g/E)^ω.  ω = 1 is the MM step (monotone
+// NLL); near the fixed point its error contracts by the MM Jacobian's eigenvalues μ ∈ [0, 1),
+// over-relaxation maps them to 1 − ω(1 − μ) (still contracting for ω < 2 / (1 − μ_min)), which
+// speeds the slow modes that set the iteration count; the common-scale direction (μ = 0) is
+// left at the MM step (see solve_kernel).  Default 1.5 with a plain-MM rerun if it does not
+// converge (solve_with_fallback); GGM_MM_OMEGA overrides (BK4 has the sweep).
+static double mm_omega() {
+  const char* e = std::getenv("GGM_MM_OMEGA");
+  const double w = e ? std::atof(e) : 1.5;
+  return (w > 0.0 && w < 2.0) ? w : 1.0;
+}
+
 struct SolveParams {
   GridDesc gd[kMaxMods];  // one per modality; offsets index the global concatenation
   int M;                  // modalities
@@ -175,6 +191,7 @@ struct SolveParams {
   double* res_out;    // stationarity of lam_out
   double tol;
   int max_iter;
+  double omega;       // update exponent: λ <- λ ⊙ (g / E)^omega (1 = the MM step)
 };
 
 // Whole MM iteration in one cooperative kernel with ONE grid-wide barrier per iteration:
@@ -241,7 +258,31 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p)
     }
     if (it == p.max_iter) break;
     // majorise-minimise update λ <- λ ⊙ g / E
-    for (int i = threadIdx.x; i < T; i += blockDim.x) slam[i] = slam[i] * sg[i] / p.E[i];
+    if (p.omega == 1.0) {
+      for (int i = threadIdx.x; i < T; i += blockDim.x) slam[i] = slam[i] * sg[i] / p.E[i];
+    } else {
+      // log-space step δ_i = log(g_i / E_i); its mean m is the common-scale direction, which
+      // the MM step already solves exactly (the map is invariant to λ -> cλ), so only
+      // δ − m is over-relaxed: λ_i <- λ_i exp(m + ω (δ_i − m)).  The block reduction runs in
+      // the same order in every block (bitwise-identical λ copies).
+      double part = 0.0;
+      for (int i = threadIdx.x; i < T; i += blockDim.x) {
+        const double d = log(sg[i] / p.E[i]);
+        sg[i] = d;
+        part += d;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      __syncthreads();  // every warp has read s_red (the stationarity max)
+      if (lane == 0) s_red[wid] = part;
+      __syncthreads();
+      double m = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) m += s_red[w];
+      m /= T;
+      for (int i = threadIdx.x; i < T; i += blockDim.x)
+        slam[i] = slam[i] * exp(m + p.omega * (sg[i] - m));
+    }
     __syncthreads();
   }
   if (blockIdx.x == 0) {
@@ -489,6 +530,37 @@ extern "C" ggm_status ggm_grid_marginals(int L, const int* k, const double* lamb
   return GGM_OK;
 }
 
+// The solve kernel with update exponent sp.omega; an over-relaxed run (omega > 1) that does
+// not converge is repeated with the plain MM step (omega = 1, monotone NLL), and its
+// iterations are returned in *extra.
+static ggm_status solve_with_fallback(SolveParams sp, int J, int nblk, size_t smem,
+                                      cudaStream_t s, const int* istat, int* extra) {
+  auto launch = [&]() -> cudaError_t {
+    switch (J) {
+      case 4: return launch_solve<4>(sp, nblk, smem, s);
+      case 8: return launch_solve<8>(sp, nblk, smem, s);
+      case 16: return launch_solve<16>(sp, nblk, smem, s);
+      default: return launch_solve<32>(sp, nblk, smem, s);
+    }
+  };
+  *extra = 0;
+  cudaError_t ce = launch();
+  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+  if (sp.omega != 1.0) {
+    int h[2] = {0, 0};
+    GGM_CUDA_TRY(cudaMemcpyAsync(h, istat, sizeof(h), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (!h[1]) {
+      *extra = h[0];
+      sp.omega = 1.0;
+      ce = launch();
+      if (ce != cudaSuccess)
+        return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+    }
+  }
+  return GGM_OK;
+}
+
 extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
                                         const ggm_solve_opts* opts, double* lambda,
                                         ggm_solve_info* info, void* stream) {
@@ -536,15 +608,11 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   sp.res_out = scal + 2;
   sp.tol = o.tol;
   sp.max_iter = o.max_iter;
+  sp.omega = mm_omega();
   const size_t smem = pass_smem(gd);
-  cudaError_t ce;
-  switch (pick_J(gd.k[gd.inner])) {
-    case 4: ce = launch_solve<4>(sp, nblk, smem, s); break;
-    case 8: ce = launch_solve<8>(sp, nblk, smem, s); break;
-    case 16: ce = launch_solve<16>(sp, nblk, smem, s); break;
-    default: ce = launch_solve<32>(sp, nblk, smem, s); break;
-  }
-  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+  int extra_it = 0;
+  ggm_status sst = solve_with_fallback(sp, pick_J(gd.k[gd.inner]), nblk, smem, s, istat, &extra_it);
+  if (sst != GGM_OK) return sst;
   int hstat[2] = {0, 0};
   GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
   finalize_kernel<<<1, 32, 0, s>>>(gd, lam_res, o.gauge, lambda, scal);
@@ -571,7 +639,7 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
       }
       double ti = 0.0;
       for (int a = 0; a < L; ++a) ti = std::max(ti, std::fabs(tr[a] - mean));
-      info->iterations = hstat[0];
+      info->iterations = hstat[0] + extra_it;
       info->stationarity = hres;
       info->nll = 0.5 * lin - 0.5 * hscal[1];
       info->grid_min = hscal[0];
@@ -663,16 +731,12 @@ extern "C" ggm_status ggm_solve_eigvals_multi(int A, const int* k, const double*
   sp.res_out = scal + 2;
   sp.tol = o.tol;
   sp.max_iter = o.max_iter;
+  sp.omega = mm_omega();
   const int nblk = solve_blocks(sp.gd[0], pts - (double)sp.gd[0].rows * sp.gd[0].k[sp.gd[0].inner]);
   const size_t smem = (size_t)T * 2 * sizeof(double) + 16;
-  cudaError_t ce;
-  switch (J) {
-    case 4: ce = launch_solve<4>(sp, nblk, smem, s); break;
-    case 8: ce = launch_solve<8>(sp, nblk, smem, s); break;
-    case 16: ce = launch_solve<16>(sp, nblk, smem, s); break;
-    default: ce = launch_solve<32>(sp, nblk, smem, s); break;
-  }
-  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+  int extra_it = 0;
+  ggm_status sst = solve_with_fallback(sp, J, nblk, smem, s, istat, &extra_it);
+  if (sst != GGM_OK) return sst;
   for (int m = 0; m < M; ++m) logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(sp.gd[m], lam_res, scal + 1);
   GGM_CUDA_TRY(cudaGetLastError());
   int hstat[2] = {0, 0};
@@ -743,7 +807,7 @@ extern "C" ggm_status ggm_solve_eigvals_multi(int A, const int* k, const double*
     double trmean = 0.0, ti = 0.0;
     for (int a = 0; a < A; ++a) trmean += tr[a] / A;
     for (int a = 0; a < A; ++a) ti = std::max(ti, std::fabs(ptr[a]));
-    info->iterations = hstat[0];
+    info->iterations = hstat[0] + extra_it;
     info->stationarity = hscal[2];
     info->nll = 0.5 * lin - 0.5 * hscal[1];
     info->grid_min = gmin;
