@@ -1696,6 +1696,7 @@ struct AxisPool {
   cublasHandle_t b[kAxisStreams] = {};
   cusolverDnHandle_t so[kAxisStreams] = {};
   bool ready = false;
+  int device = -1;
   ~AxisPool() {
     for (int i = 0; i < kAxisStreams; ++i) {
       if (b[i]) cublasDestroy(b[i]);
@@ -1708,7 +1709,19 @@ thread_local AxisPool g_axis_pool;
 
 ggm_status axis_pool(AxisPool** out) {
   AxisPool& P = g_axis_pool;
+  int dev = 0;
+  GGM_CUDA_TRY(cudaGetDevice(&dev));
+  if (P.ready && P.device != dev) {  // the thread moved to another device: new streams there
+    for (int i = 0; i < kAxisStreams; ++i) {
+      cublasDestroy(P.b[i]);
+      cusolverDnDestroy(P.so[i]);
+      P.b[i] = nullptr;
+      P.so[i] = nullptr;
+    }
+    P.ready = false;
+  }
   if (!P.ready) {
+    P.device = dev;
     for (int i = 0; i < kAxisStreams; ++i) {
       GGM_CUDA_TRY(cudaStreamCreateWithFlags(&P.s[i], cudaStreamNonBlocking));
       if (cublasCreate(&P.b[i]) != CUBLAS_STATUS_SUCCESS ||
