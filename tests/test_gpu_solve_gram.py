@@ -165,3 +165,22 @@ def test_gram_eig_axes_rank_error(G):
     with pytest.raises(G.GGMError) as e:
         G.ggm_gram_eig_axes(torch.from_numpy(x).cuda(), [6, 5, 5])  # k_2 = 5 > d_2 = 4
     assert e.value.status_name == "GGM_ERR_RANK"
+
+
+def test_solve_overrelaxation_fallback(G, monkeypatch):
+    """An over-relaxed run that does not converge within max_iter is repeated with the plain
+    MM step (BK4): same fixed point, iterations = both runs."""
+    cfg = gen.config("C2")
+    X = torch.from_numpy(cfg["X"]).cuda()
+    Ec = torch.cat([G.ggm_gram_eig(X, a, k)[1] for a, k in enumerate(cfg["k"])])
+    monkeypatch.setenv("GGM_MM_OMEGA", "1")
+    lam1, info1 = G.ggm_solve_eigvals(Ec, cfg["k"], max_iter=200)
+    monkeypatch.setenv("GGM_MM_OMEGA", "1.99")   # oscillates: no convergence in 30 iterations
+    lam2, info2 = G.ggm_solve_eigvals(Ec, cfg["k"], max_iter=30)
+    assert info2["iterations"] == 30 + info1["iterations"]
+    # the rerun is the plain MM run (cross-block fp64 atomics: summation order varies)
+    np.testing.assert_allclose(lam2.cpu().numpy(), lam1.cpu().numpy(), rtol=1e-10)
+    monkeypatch.delenv("GGM_MM_OMEGA")
+    lam3, info3 = G.ggm_solve_eigvals(Ec, cfg["k"])
+    s = [O.grid_sums(_split(l.cpu().numpy(), cfg["k"])) for l in (lam1, lam3)]
+    np.testing.assert_allclose(s[1], s[0], rtol=1e-5)
