@@ -184,3 +184,24 @@ def test_solve_overrelaxation_fallback(G, monkeypatch):
     lam3, info3 = G.ggm_solve_eigvals(Ec, cfg["k"])
     s = [O.grid_sums(_split(l.cpu().numpy(), cfg["k"])) for l in (lam1, lam3)]
     np.testing.assert_allclose(s[1], s[0], rtol=1e-5)
+
+
+def test_gram_eig_axes_with_rsi_axis(G):
+    """(1h) with one axis beyond the dense Gram (33,000 rows, complement 40,000: randomized
+    subspace iteration on `stream` after the concurrent dense axes): every axis equals its
+    per-axis call.  Rank-4 CP tensor + small noise, k = 4 on every axis."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    shape = (33000, 200, 200)
+    fs = [torch.randn(d, 4, device="cuda", generator=g) for d in shape]
+    w = torch.tensor([8.0, 4.0, 2.0, 1.0], device="cuda")
+    X = torch.einsum("ir,jr,lr,r->ijl", fs[0], fs[1], fs[2], w)
+    X += 1e-3 * torch.randn(shape, device="cuda", generator=g)
+    X = X.contiguous()
+    res, tr = G.ggm_gram_eig_axes(X, [4, 4, 4])
+    for a, (V, E) in enumerate(res):
+        Vs, Es, _ = G.ggm_gram_eig(X, a, 4)
+        np.testing.assert_allclose(E.cpu().numpy(), Es.cpu().numpy(), rtol=1e-9)
+        d = (V.double() * Vs.double()).sum(0).abs()
+        assert float((1 - d).max()) < 1e-5
+    del X
+    torch.cuda.empty_cache()
