@@ -27,11 +27,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#if defined(GGM_WAIT_HINT_ALL) && GGM_WAIT_HINT_ALL
+#define GGM_TRY_WAIT_HINT ", 0x989680"
+#else
+#define GGM_TRY_WAIT_HINT ""
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1" GGM_TRY_WAIT_HINT ";\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -195,11 +200,23 @@ __device__ __forceinline__ void cluster_sync() {
 // Arrive on the mbarrier at the same shared offset in CTA `cta` of the cluster.
 // Variants on precomputed shared-memory addresses (hot loops: no generic->shared conversion
 // or mapa per use).  mbar_map_cluster: the address of `bar` in CTA `cta` of the cluster.
+// try_wait with a suspend-time hint: the waiting warp is parked by the hardware until the
+// phase completes (or the hint elapses) instead of re-issuing the test, leaving the issue
+// slots of its SM sub-partition to the epilogue warps that share it.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1" GGM_TRY_WAIT_HINT ";\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");

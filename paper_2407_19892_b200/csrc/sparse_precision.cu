@@ -54,6 +54,17 @@ constexpr int kMaxStages = 4;  // operand pipeline: 4 x 32 KB (A resident) or 2 
 // to hide their latency.  (With 10 warps one SM sub-partition would hold 3 warps and cap
 // every thread at 168 registers.)
 constexpr int kFirstEpiWarp = 4;
+#ifndef GGM_LEAN_ISSUE
+#define GGM_LEAN_ISSUE 1
+#endif
+#ifndef GGM_WAIT_HINT
+#define GGM_WAIT_HINT 1
+#endif
+#if GGM_WAIT_HINT
+#define LEAN_WAIT mbar_wait_sleep
+#else
+#define LEAN_WAIT mbar_wait
+#endif
 constexpr int kRegsCtl = 56;
 __host__ __device__ constexpr int threads_of(int EPW) { return (kFirstEpiWarp + EPW) * 32; }
 // setmaxnreg.inc draws only on what warpgroup 0 released: 8 warps: 384 threads launch at 168,
@@ -1157,7 +1168,9 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         continue;
       }
 #ifdef GGM_EPI_DEBUG
-      if (dbg == 4) {  // loads only: every chunk in registers, release, no filter
+      // 5: dbg 3 except that the warps on the MMA issuer's sub-partition (warp % 4 == 1)
+      //    only load and release (is the slowdown issue contention on that SMSP?)
+      if (dbg == 4 || (dbg == 5 && (warp & 3) == 1)) {  // loads only, release, no filter
         uint32_t vv[G::NC][32];
 #pragma unroll
         for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, vv[c]);
@@ -1193,7 +1206,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         }
         const bool rh = valid && m >= bi;
         const bool ch = valid && m >= cmin[c];
-        if (!__any_sync(0xffffffffu, rh || ch) || dbg == 3) continue;  // dbg 3: no rare path
+        if (!__any_sync(0xffffffffu, rh || ch) || dbg >= 3) continue;  // dbg 3, 5: no rare path
         // rare path: exact per-entry masks, then each lane walks its own hits
         uint32_t mr = 0, mc = 0;
         if (rh) {
@@ -1466,6 +1479,77 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
 #define PROF_W(acc, stmt) do { pr_c = clock64(); stmt; acc += clock64() - pr_c; } while (0)
 #else
 #define PROF_W(acc, stmt) stmt
+#endif
+#if GGM_LEAN_ISSUE
+      if (PAIR && !three) {
+        // Lean hi-only issue loop (screening main pass, seed pass): the MMA warp shares its
+        // SM sub-partition with 4 busy epilogue warps, so every instruction on its path
+        // costs issue slots (profiles/r01i_mma_prof.md).  All descriptors are loop
+        // invariant: A resident (atoms 0/1, hi and lo arrays), B stage s = stage 0 + s·st_bytes
+        // (the 14-bit address field, addr >> 4, does not overflow below 256 KB); per atom
+        // the hi slots and the packed-tail slots are 4-bit masks.
+        const uint64_t dAh0 = sw128_desc(smem_u32(sA)), dAh1 = dAh0 + (kAtomBytes >> 4);
+        const uint64_t dAl0 = dAh0 + (uint64_t)((KA * kAtomBytes) >> 4);
+        const uint64_t dAl1 = dAl0 + (kAtomBytes >> 4);
+        const uint64_t dB0 = sw128_desc(smem_u32(sStage));
+        const uint32_t st16 = (uint32_t)(st_bytes >> 4);
+        uint32_t hm[2], tm[2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          hm[a] = tm[a] = 0;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const int slot = 4 * a + ks;
+            if (slot < p.KS) hm[a] |= 1u << ks;
+            else if (slot < p.KS + p.TS) tm[a] |= 1u << ks;
+          }
+        }
+        for (int u = p.unit_lo + u0; u < units; u += ustep) {
+          int ub;
+          const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
+          PROF_W(pr_ta, mbar_wait(afull, a_iter & 1));
+          tc_fence_after();
+          for (int s = 0; s < ntiles; ++s) {
+#ifdef GGM_MMA_PROF
+            ++pr_n;
+#endif
+            PROF_W(pr_te, LEAN_WAIT(&tempty[buf], tphase ^ 1));
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + (uint32_t)(buf * kTileN);
+            for (int a = 0; a < KA; ++a) {
+              PROF_W(pr_tf, LEAN_WAIT(&full[stage], phase));
+              tc_fence_after();
+              const uint64_t dB = dB0 + (uint64_t)(stage * st16);
+              const uint64_t dAh = a ? dAh1 : dAh0, dAl = a ? dAl1 : dAl0;
+              const uint32_t h = a ? hm[1] : hm[0], tl = a ? tm[1] : tm[0];
+              if (issuer) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                  const uint64_t o = (uint64_t)(2 * ks);
+                  if ((h | tl) >> ks & 1u)
+                    mma_f16<PAIR>(d_tmem, ((h >> ks) & 1u ? dAh : dAl) + o, dB + o, idesc,
+                                  (a | ks) ? 1u : 0u);
+                }
+                mma_commit_any<PAIR>(&empty[stage]);
+              }
+              __syncwarp();
+              if (++stage == NS) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+            if (issuer) mma_commit_any<PAIR>(&tfull[buf]);
+            __syncwarp();
+            if (++buf == 2) {
+              buf = 0;
+              tphase ^= 1;
+            }
+          }
+          if (issuer) mma_commit_any<PAIR>(aempty);
+          __syncwarp();
+          ++a_iter;
+        }
+      } else
 #endif
       for (int u = p.unit_lo + u0; u < units; u += ustep) {
         int ub;
