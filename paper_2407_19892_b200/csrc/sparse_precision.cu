@@ -1170,7 +1170,9 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #ifdef GGM_EPI_DEBUG
       // 5: dbg 3 except that the warps on the MMA issuer's sub-partition (warp % 4 == 1)
       //    only load and release (is the slowdown issue contention on that SMSP?)
-      if (dbg == 4 || (dbg == 5 && (warp & 3) == 1)) {  // loads only, release, no filter
+      //    6: the same for quadrant 2 (control); 7: quadrant 1 of the leader CTA only
+      if (dbg == 4 || (dbg == 5 && (warp & 3) == 1) || (dbg == 6 && (warp & 3) == 2) ||
+          (dbg == 7 && (warp & 3) == 1 && rank == 0)) {  // loads only, release, no filter
         uint32_t vv[G::NC][32];
 #pragma unroll
         for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, vv[c]);
