@@ -57,6 +57,9 @@ constexpr int kFirstEpiWarp = 4;
 #ifndef GGM_LEAN_ISSUE
 #define GGM_LEAN_ISSUE 1
 #endif
+#ifndef GGM_MMA_WARP
+#define GGM_MMA_WARP 1  // control warp (1..3) that issues the MMAs; its SM sub-partition is
+#endif                  // the one of TMEM lane quadrant GGM_MMA_WARP
 #ifndef GGM_WAIT_HINT
 #define GGM_WAIT_HINT 1
 #endif
@@ -1170,9 +1173,10 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #ifdef GGM_EPI_DEBUG
       // 5: dbg 3 except that the warps on the MMA issuer's sub-partition (warp % 4 == 1)
       //    only load and release (is the slowdown issue contention on that SMSP?)
-      //    6: the same for quadrant 2 (control); 7: quadrant 1 of the leader CTA only
+      //    6: the same for quadrant 2 (control); 7: quadrant 1 of the leader CTA only;
+      //    8: quadrant 3 of both CTAs
       if (dbg == 4 || (dbg == 5 && (warp & 3) == 1) || (dbg == 6 && (warp & 3) == 2) ||
-          (dbg == 7 && (warp & 3) == 1 && rank == 0)) {  // loads only, release, no filter
+          (dbg == 7 && (warp & 3) == 1 && rank == 0) || (dbg == 8 && (warp & 3) == 3)) {
         uint32_t vv[G::NC][32];
 #pragma unroll
         for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, vv[c]);
@@ -1463,7 +1467,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
           }
         }
       }
-    } else if (warp == 1 && rank == 0) {
+    } else if (warp == GGM_MMA_WARP && rank == 0) {
       // ===================== MMA issuer: warp 1 (of the pair leader) =====================
       // The whole warp runs the loop (warp-uniform descriptors); one elected lane issues the
       // tcgen05.mma / commit instructions.  With one thread and per-lane registers, every
