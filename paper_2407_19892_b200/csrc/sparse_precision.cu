@@ -57,6 +57,12 @@ constexpr int kFirstEpiWarp = 4;
 #ifndef GGM_LEAN_ISSUE
 #define GGM_LEAN_ISSUE 1
 #endif
+#ifndef GGM_LEAN_ISSUERS
+#define GGM_LEAN_ISSUERS 1  // 2: the lean hi-only loop alternates tiles between warps 1 and 2
+#endif
+#ifndef GGM_MMA_THROTTLE
+#define GGM_MMA_THROTTLE 0
+#endif
 #ifndef GGM_MMA_WARP
 #define GGM_MMA_WARP 1  // control warp (1..3) that issues the MMAs; its SM sub-partition is
 #endif                  // the one of TMEM lane quadrant GGM_MMA_WARP
@@ -1335,7 +1341,9 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
       mbar_init(&tempty[b], PAIR ? 2 * EPW : EPW);  // pair: both CTAs' epilogue warps
     }
     mbar_init(afull, 1);
-    mbar_init(aempty, 1);
+    // two issuer warps (lean hi-only pair loop) each commit once per unit
+    mbar_init(aempty, (GGM_LEAN_ISSUE && GGM_LEAN_ISSUERS == 2 && PAIR &&
+                       (KIND == kSeed || p.screen)) ? 2 : 1);
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -1467,7 +1475,10 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
           }
         }
       }
-    } else if (warp == GGM_MMA_WARP && rank == 0) {
+    } else if (rank == 0 &&
+               (warp == GGM_MMA_WARP ||
+                (GGM_LEAN_ISSUE && GGM_LEAN_ISSUERS == 2 && PAIR && (KIND == kSeed || p.screen) &&
+                 warp == 2))) {
       // ===================== MMA issuer: warp 1 (of the pair leader) =====================
       // The whole warp runs the loop (warp-uniform descriptors); one elected lane issues the
       // tcgen05.mma / commit instructions.  With one thread and per-lane registers, every
@@ -1499,6 +1510,10 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
         const uint64_t dAl1 = dAl0 + (kAtomBytes >> 4);
         const uint64_t dB0 = sw128_desc(smem_u32(sStage));
         const uint32_t st16 = (uint32_t)(st_bytes >> 4);
+#if GGM_MMA_THROTTLE
+        int fs1 = -1, fs2 = -1;  // stages (and phases) of the last two issued atoms
+        uint32_t fp1 = 0, fp2 = 0;
+#endif
         uint32_t hm[2], tm[2];
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
@@ -1519,11 +1534,29 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
 #ifdef GGM_MMA_PROF
             ++pr_n;
 #endif
+            if (GGM_LEAN_ISSUERS == 2 && buf != warp - 1) {  // the other issuer's tile
+              stage += KA;
+              while (stage >= NS) {
+                stage -= NS;
+                phase ^= 1;
+              }
+              if (++buf == 2) {
+                buf = 0;
+                tphase ^= 1;
+              }
+              continue;
+            }
             PROF_W(pr_te, LEAN_WAIT(&tempty[buf], tphase ^ 1));
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(buf * kTileN);
             for (int a = 0; a < KA; ++a) {
               PROF_W(pr_tf, LEAN_WAIT(&full[stage], phase));
+#if GGM_MMA_THROTTLE
+              // at most two atoms of MMAs outstanding: wait for the one before the last
+              // (its commit on empty[] completes phase fp2) so the tcgen05.mma issue does not
+              // block this sub-partition's dispatch on a full MMA queue
+              if (fs2 >= 0) PROF_W(pr_is, LEAN_WAIT(&empty[fs2], fp2));
+#endif
               tc_fence_after();
               const uint64_t dB = dB0 + (uint64_t)(stage * st16);
               const uint64_t dAh = a ? dAh1 : dAh0, dAl = a ? dAl1 : dAl0;
@@ -1539,6 +1572,12 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
                 mma_commit_any<PAIR>(&empty[stage]);
               }
               __syncwarp();
+#if GGM_MMA_THROTTLE
+              fs2 = fs1;
+              fp2 = fp1;
+              fs1 = stage;
+              fp1 = phase;
+#endif
               if (++stage == NS) {
                 stage = 0;
                 phase ^= 1;
