@@ -401,7 +401,16 @@ def eig_gram(G: torch.Tensor, k: int, stream=None):
 def project_csr(row_ptr, col, val, m: int, W: torch.Tensor, E: torch.Tensor,
                 nonparanormal: bool = False, stream=None) -> torch.Tensor:
     """This rank's rows of the long-axis factor A_r W diag(E^-1/2) (fp32 d x k)."""
+    _require_cuda(row_ptr, torch.int64, "row_ptr")
+    _require_cuda(col, torch.int32, "col")
+    _require_cuda(val, torch.float32, "val")
+    _require_cuda(W, torch.float64, "W")
+    _require_cuda(E, torch.float64, "E")
     d, nnz, k = row_ptr.numel() - 1, val.numel(), E.numel()
+    if col.numel() != nnz:
+        raise ValueError("col and val must have the same length")
+    if W.numel() != k * int(m):
+        raise ValueError(f"W must hold k x m = {k} x {m} values (as returned by eig_gram)")
     nbytes = C.c_size_t(0)
     _check(lib().ggm_project_csr_workspace(d, int(m), nnz, int(k), C.byref(nbytes)))
     ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=val.device)

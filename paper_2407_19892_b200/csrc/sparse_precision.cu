@@ -175,30 +175,41 @@ __global__ void row_norms(const float* __restrict__ V, const double* __restrict_
   if (lane == 0) atomicMax(rn_max_bits, __float_as_uint(wmax));
 }
 
+// Screening error bound of entry (i, j) in accumulator units (x = U·2^e, hi = fp16(x),
+// lo = fp16(x - hi)).  For a normal fp16 hi, |x - hi| <= 2^-11 |hi|; below the fp16 normal range
+// (|x| < 2^-14, i.e. |U| < 2^-28 max|U|) the rounding error is absolute, <= 2^-25, and |lo - (x -
+// hi)| <= 2^-25 likewise.  Hence for both the seed relation |ψ3 - ψ1| = |Σ hi lo + lo hi| and the
+// screening relation |ψ - ψ1| (ψ the exact product of the fp32 inputs):
+//   |ψ - ψ1| <= 2^-10 (1 + 2^-11) ||x_i|| ||x_j|| + 2^-24 sqrt(k) (||x_i|| + ||x_j||) + fp32 terms,
+// bounded by 1.1 · 2^-10 ||x_i|| M + 2^-23 sqrt(k) (||x_i|| + M), M = max_j ||x_j|| (the relative
+// term alone is not a bound for rows with near-zero norms).
+__device__ __forceinline__ float screen_margin(float rn_s, float umax_s, int k) {
+  return 1.1f * ldexpf(rn_s * umax_s, -10) + ldexpf(sqrtf((float)k) * (rn_s + umax_s), -23);
+}
+
 // kSym: seed value b1_i (t-th largest |hi·hi| chunk maximum, accumulator units) -> a lower
-// bound of the row's t-th 3-term magnitude.  With x = hi + lo, |lo| <= 2^-11 |hi|:
-// |ψ3 - ψ1| = |Σ_r hi_ir lo_jr + lo_ir hi_jr| <= 2^-10 (1 + 2^-11) ||x_i|| ||x_j||, plus fp32
-// accumulation differences (k 2^-24 ||x_i|| ||x_j||); margin 1.1 · 2^-10 ||x_i|| max_j ||x_j||.
+// bound of the row's t-th 3-term magnitude (b1 minus screen_margin; fp32 accumulation
+// differences, k 2^-24 ||x_i|| ||x_j||, are covered by the factor 1.1).
 __global__ void seed_bounds(float* __restrict__ thr, const float* __restrict__ rn,
-                            const unsigned int* __restrict__ rn_max_bits, int64_t n,
+                            const unsigned int* __restrict__ rn_max_bits, int64_t n, int k,
                             const DevScalars* __restrict__ sc) {
   const float s = ldexpf(1.f, sc->exp2);
   const float umax = __uint_as_float(*rn_max_bits) * s;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float b1 = thr[i];
-    const float margin = 1.1f * ldexpf(rn[i] * s * umax, -10);
+    const float margin = screen_margin(rn[i] * s, umax, k);
     thr[i] = b1 > 0.f ? fmaxf(b1 - margin, -1.f) : -1.f;
   }
 }
 
-// kSym screening thresholds: the main pass computes hi·hi only (|ψ1 - ψ| <= 2^-10 (1+2^-11)
-// ||x_i|| ||x_j|| + fp32 terms, see seed_bounds), so entry (i, j) is kept for row i if
-// |ψ1| >= b_i - 1.1·2^-10 ||x_i|| max||x|| (and symmetrically for row j): every entry with
-// |ψ| >= b_i survives.  Bound order p (perm[p] = original id); padding stays +inf.
+// kSym screening thresholds: the main pass computes hi·hi only (|ψ1 - ψ| <= screen_margin),
+// so entry (i, j) is kept for row i if |ψ1| >= b_i - screen_margin(i) (and symmetrically for
+// row j): every entry with |ψ| >= b_i survives.  Bound order p (perm[p] = original id);
+// padding stays +inf.
 __global__ void screen_bounds(const float* __restrict__ thr_p, const float* __restrict__ rn,
                               const int32_t* __restrict__ perm,
-                              const unsigned int* __restrict__ rn_max_bits, int64_t n,
+                              const unsigned int* __restrict__ rn_max_bits, int64_t n, int k,
                               int64_t nthr, const DevScalars* __restrict__ sc,
                               float* __restrict__ thr_s) {
   const float s = ldexpf(1.f, sc->exp2);
@@ -207,7 +218,7 @@ __global__ void screen_bounds(const float* __restrict__ thr_p, const float* __re
        p += (int64_t)gridDim.x * blockDim.x) {
     const float b = thr_p[p];
     if (p < n && b < INFINITY) {
-      const float margin = 1.1f * ldexpf(rn[perm[p]] * s * umax, -10);
+      const float margin = screen_margin(rn[perm[p]] * s, umax, k);
       thr_s[p] = b > -1.f ? b - margin : b;
     } else {
       thr_s[p] = b;
@@ -412,8 +423,17 @@ struct FusedParams {
   int pair;          // CTA-pair kernel (host-side selection; the kernel's template PAIR)
   int unit_lo, unit_hi;  // units processed by this launch (a rank's share in the sharded
                          // symmetric scheme; [0, all units) otherwise)
+#ifdef GGM_EPI_DEBUG
   int dbg;  // timing experiments only (GGM_DEBUG_EPI): 1 = TMEM loads only, 2 = no epilogue work
+#endif
 };
+// Epilogue timing experiments exist only in -DGGM_EPI_DEBUG builds (tools/build_variant.sh);
+// in the release library the switch is the constant 0 and no environment variable is read.
+#ifdef GGM_EPI_DEBUG
+#define GGM_DBG(p) ((p).dbg)
+#else
+#define GGM_DBG(p) 0
+#endif
 
 // Operand pipeline.  1 CTA, A resident (k <= 128): a stage holds B hi and B lo of one K atom
 // for both 128-row operand blocks of the tile = 64 KB, 2 stages (the seed pass fills only the
@@ -809,7 +829,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     ti.start(p, u, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s, ti.next(p)) {
       const int Kh = h ? ti.K1 : ti.K0;
-      const bool live = (h == 0 || ti.h1) && p.dbg != 2;
+      const bool live = (h == 0 || ti.h1) && GGM_DBG(p) != 2;
       const int64_t cb = (int64_t)Kh * kRowsPerBlock;  // first column of this warp's block
       const bool need_mask = (cb < rhi && cb + kRowsPerBlock > rlo) || (cb + kRowsPerBlock > p.n);
       mbar_wait(&tfull[buf], tphase);
@@ -827,7 +847,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
         for (int c = 0; c < (kTileN / 2) / 32; c += 2) {
           tmem_wait_ld(va);
           tmem_ld32_nowait(taddr + (c + 1) * 32, vb);
-          if (p.dbg != 1)
+          if (GGM_DBG(p) != 1)
             epi_chunk<MAXT, KIND>(p, va, taddr + c * 32, cb + c * 32, gi, lr, valid, need_mask,
                                   tau_s, sd2, top, macc, lane, scratch_all,
                                   cacc ? cacc + c * 32 : nullptr);
@@ -835,7 +855,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
             p.row_ptr[0] = (int64_t)va[7];
           tmem_wait_ld(vb);
           if (c + 2 < (kTileN / 2) / 32) tmem_ld32_nowait(taddr + (c + 2) * 32, va);
-          if (p.dbg != 1)
+          if (GGM_DBG(p) != 1)
             epi_chunk<MAXT, KIND>(p, vb, taddr + (c + 1) * 32, cb + (c + 1) * 32, gi, lr, valid,
                                   need_mask, tau_s, sd2, top, macc, lane, scratch_all,
                                   cacc ? cacc + (c + 1) * 32 : nullptr);
@@ -1000,7 +1020,7 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
         buf = 0;
         tphase ^= 1;
       }
-      if (p.dbg != 0) {
+      if (GGM_DBG(p) != 0) {
         if (v[0][0] == 12345u && v[G::NC - 1][31] == 54321u) p.thr_out[0] = __uint_as_float(v[0][7]);
         continue;
       }
@@ -1745,7 +1765,7 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n,
 // fixed order, so ψ_ij and ψ_ji come out bit-identical.
 constexpr int kRecMaxK = 128;
 // Only candidates that can still reach the row's exact top t are re-evaluated: with M_j =
-// 1.1·2^-10 ||x_j|| max||x|| (the screening error bound of every pair of row j) and s_t the
+// screen_margin(j) in ψ units (the screening error bound of every pair of row j) and s_t the
 // t-th largest screened magnitude of the row's candidates, an exact top-t entry c has
 // |ψ1(c)| >= T - M_j >= s_t - 2 M_j (T the exact t-th magnitude, s_t <= T + M_j).  The
 // others get value 0 and cannot displace the re-evaluated ones in merge_sym.  On a rank's
@@ -1771,7 +1791,8 @@ __global__ void gather_u_bound(const float* __restrict__ V, const double* __rest
 __global__ void recompute_sorted(const int64_t* __restrict__ off, uint2* __restrict__ sval,
                                  int64_t n, const float* __restrict__ Ub, int k, int t,
                                  const float* __restrict__ rn, const int32_t* __restrict__ perm,
-                                 const unsigned int* __restrict__ rn_max_bits) {
+                                 const unsigned int* __restrict__ rn_max_bits,
+                                 const DevScalars* __restrict__ sc) {
   const int lane = threadIdx.x & 31;
   constexpr int R = kRecMaxK / 32;
   const float umax = __uint_as_float(*rn_max_bits);
@@ -1805,7 +1826,8 @@ __global__ void recompute_sorted(const int64_t* __restrict__ off, uint2* __restr
         cur = mx;
         if (mx < 0.f) break;
       }
-      const float mj = 1.1f * ldexpf(rn[perm[j]] * umax, -10);
+      const float sf = ldexpf(1.f, sc->exp2);  // ψ units = accumulator units / s^2
+      const float mj = ldexpf(screen_margin(rn[perm[j]] * sf, umax * sf, k), -2 * sc->exp2);
       xcut = cur - 2.f * mj;
     }
     const float* ua = Ub + j * k;
@@ -2328,8 +2350,10 @@ static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t
   fp.sc = w.sc;
   fp.pcol = w.pcol;
   fp.pval = w.pval;
+#ifdef GGM_EPI_DEBUG
   const char* d = getenv("GGM_DEBUG_EPI");
   fp.dbg = d ? atoi(d) : 0;
+#endif
   return fp;
 }
 
@@ -2391,7 +2415,7 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   }
   if (pl.mode != 1) {
     seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
-        w.thr, w.rn_s, &w.sc->rn_max_bits, n, w.sc);
+        w.thr, w.rn_s, &w.sc->rn_max_bits, n, k, w.sc);
     count_launches(1);
   }
   // (3) order rows (= columns) by their bound: sort (bound, original id) -> the final
@@ -2406,7 +2430,7 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
       w.thr_p + n, nthr - n, INFINITY);
   if (pl.screen) {
     screen_bounds<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(
-        w.thr_p, w.rn, w.perm, &w.sc->rn_max_bits, n, nthr, w.sc, w.thr_s);
+        w.thr_p, w.rn, w.perm, &w.sc->rn_max_bits, n, k, nthr, w.sc, w.thr_s);
     count_launches(1);
   }
   chunk_min32<<<(int)std::min<int64_t>((nthr / 32 + 255) / 256, sms * 8), 256, 0, s>>>(
@@ -2588,7 +2612,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
           cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
               w.skey, ncand, n, w.roff);
           recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-              w.roff, w.sval, n, w.Ub, k, INT_MAX, w.rn, w.perm, &w.sc->rn_max_bits);
+              w.roff, w.sval, n, w.Ub, k, INT_MAX, w.rn, w.perm, &w.sc->rn_max_bits, w.sc);
           count_launches(2);
         }
         sym_threshold_coo<<<(int)std::min<int64_t>((ncand + 255) / 256, sms * 16), 256, 0, s>>>(
@@ -2653,7 +2677,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
         cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
             w.skey, ncand, n, w.roff);
         recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-            w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits);
+            w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits, w.sc);
         count_launches(2);
       }
     }
@@ -2904,7 +2928,7 @@ static ggm_status sym_shard_impl(
       cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
           w.skey, ncand, n, w.roff);
       recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-          w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits);
+          w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits, w.sc);
       count_launches(2);
     }
   }
