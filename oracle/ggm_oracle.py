@@ -17,6 +17,11 @@ Pinning (tests/test_oracle_pins.py, ``-m "not gpu"``):
   gradient                  finite differences of nll; single axis closed form
   solve_eigvals             Lemma 3 (P:272-306) on dense ⊕Ψ; isotropic closed form;
                             Alg. 1 gradient descent (paper_gd_solve) reaches the same grid
+                            and, in gauge 1, the same λ
+  barrier regime (reading T) hand-derived closed forms for k = (2, 1) (all three active
+                            sets); KKT conditions on truncated tensors; SciPy L-BFGS-B on
+                            the box and the clamped majorise-minimise iteration reach the
+                            same grid / λ (tests/test_oracle_barrier.py)
   canonical gauge           grid invariance; PSD; closed form on shifted inputs
   psi_rows / top_t / thr    dense V diag(λ) V^T + brute-force sort on tiny inputs;
                             rank-1 closed form; identity-factor all-tie case
@@ -45,6 +50,8 @@ __all__ = [
     "wald_edge", "wald_threshold", "overall_edges", "edges_to_symmetric_csr",
     "gram_eig_multi", "grid_sums_multi", "marginals_multi", "nll_multi", "gradient_multi",
     "stationarity_multi", "gauge_space_multi", "canonical_gauge_multi", "solve_eigvals_multi",
+    "project_spectrum", "kkt_residual", "trace_inconsistency_multi", "gauge_space_free",
+    "gauge_lift",
     "nonparanormal", "nonparanormal_sparse_split", "gram_eig_nonparanormal",
 ]
 
@@ -215,63 +222,269 @@ def identifiable(lams):
     return t, [np.asarray(l, np.float64) - float(np.mean(l)) for l in lams]
 
 
-def solve_eigvals(E, tol: float = 1e-12, max_iter: int = 200, gauge: int = 0):
-    """Eigenvalue MLE: the minimizer of the convex NLL (Lemma 4, existence
-    Lemma 6, uniqueness up to gauge Thm 4).
+def solve_eigvals(E, tol: float = 1e-12, max_iter: int = 200, gauge: int = 0,
+                  eps_scale: float = 1e-10, trace_tol: float = 1e-8):
+    """Eigenvalue MLE: the minimizer of the convex NLL (Lemma 4) over the paper's
+    domain Λ_l >= ε (Lemma 6), uniqueness of the grid (Thm 4).
+    Reading T:
+      * traces consistent (trace_inconsistency(E) <= trace_tol): the interior stationary
+        point of the NLL with E replaced by its G⊥ projection (the gauge component of the
+        linear term, non-zero only through rounding, is dropped) — projected Newton on G⊥
+        (Hessian from the 1/s^2 marginals, a library least-squares solve as the primitive),
+        backtracking on NLL with grid feasibility, start λ = 1/E (Alg. 1 line 5, P:913-915);
+      * otherwise the NLL is linear and decreasing along a gauge direction and the minimum
+        lies on the barrier λ >= ε = eps_scale·max(1/E): active-set Newton on the box
+        (_box_mle), floor_active = True ("consistently running into this barrier ... pick a
+        smaller k_l").
+    gauge 0 → canonical_gauge (min-balanced), gauge 1 → (λ − 1/E) ⊥ G, the gauge Algorithm 1's
+    gradient steps preserve; in the barrier regime both act only among the axes with no
+    coordinate on the floor (the others have no gauge freedom left).
+    Returns (lams, info dict)."""
+    return _solve_mle(E, None, tol, max_iter, gauge, eps_scale, trace_tol)
 
-    The MLE has a plain definition (argmin of NLL), so the oracle computes that
-    definition: projected Newton on G⊥ (Hessian from the 1/s^2 marginals, a library
-    least-squares solve as the primitive), backtracking on NLL with grid feasibility.
-    Start at λ = 1/E (Alg. 1 line 5).  Returns (lams, info dict).
-    gauge 0 → canonical_gauge; gauge 1 → the iterate as reached from 1/E.
-    """
+
+def gauge_lift(ks, N: np.ndarray) -> np.ndarray:
+    """Orthonormal basis, in the Σk coordinate space, of the per-axis constant shifts
+    {(c_l 1_{k_l})_l : c ∈ span N} (N: axis-space basis, nax x r)."""
+    off = np.cumsum([0] + list(ks))
+    n = int(off[-1])
+    if N.size == 0:
+        return np.zeros((n, 0))
+    B = np.zeros((n, N.shape[1]))
+    for a in range(len(ks)):
+        B[off[a]:off[a + 1], :] = N[a][None, :]
+    Q, _ = np.linalg.qr(B)
+    return Q
+
+
+def gauge_space_free(nax: int, modalities, free_axes) -> np.ndarray:
+    """Axis-space basis of G_F = {c ∈ G : c_l = 0 for l not in free_axes} (the gauge freedom
+    left when the axes outside free_axes have a coordinate pinned at the floor)."""
+    rows = []
+    for mod in modalities:
+        r = np.zeros(nax)
+        r[list(mod)] = 1.0
+        rows.append(r)
+    for a in range(nax):
+        if a not in free_axes:
+            r = np.zeros(nax)
+            r[a] = 1.0
+            rows.append(r)
+    M = np.array(rows)
+    _, sv, vt = np.linalg.svd(M)
+    rank = int(np.sum(sv > 1e-12 * max(sv.max(), 1.0)))
+    return vt[rank:].T.copy()
+
+
+def project_spectrum(E, modalities=None):
+    """E_eff = P_{G⊥}(E) (reading T): the grid marginals g are always ⊥ G (every modality's
+    marginals have the same sum on each of its axes), so E_eff is the part of E that an
+    interior stationary point g = E_eff can match.  Equal to E when the traces agree."""
     E = [np.asarray(e, np.float64) for e in E]
     ks = [len(e) for e in E]
-    if any(np.any(~np.isfinite(e)) or np.any(e <= 0) for e in E):
-        raise ValueError("E must be finite and > 0 (Thm 4 hypothesis, P:742)")
+    if modalities is None:
+        modalities = [list(range(len(E)))]
+    Q = gauge_lift(ks, gauge_space_multi(len(E), modalities))
+    v = np.concatenate(E)
+    return _split(v - Q @ (Q.T @ v), ks)
+
+
+def _hessian_multi(lams, modalities, ks):
+    """∂²NLL/∂λ∂λ = ½ Σ_γ (1D marginals of 1/s² on the diagonal blocks, 2D marginals off it)."""
+    off = np.cumsum([0] + list(ks))
+    n = int(off[-1])
+    H = np.zeros((n, n))
+    for mod in modalities:
+        diag, pair = marginals_sq2d([lams[a] for a in mod])
+        for pa, a in enumerate(mod):
+            H[off[a]:off[a + 1], off[a]:off[a + 1]] += np.diag(0.5 * diag[pa])
+        for (pa, pb), m in pair.items():
+            a, b = mod[pa], mod[pb]
+            H[off[a]:off[a + 1], off[b]:off[b + 1]] += 0.5 * m
+            H[off[b]:off[b + 1], off[a]:off[a + 1]] += 0.5 * m.T
+    return H
+
+
+def _interior_newton(E, modalities, tol, max_iter):
+    """Projected Newton on G⊥ from λ = 1/E (every step ⊥ G, so λ − 1/E stays ⊥ G)."""
+    ks = [len(e) for e in E]
+    n = int(sum(ks))
+    Q = gauge_lift(ks, gauge_space_multi(len(E), modalities))
+    P = np.eye(n) - Q @ Q.T
     lam = np.concatenate([1.0 / e for e in E])
-    P = _gauge_projector(ks)
-    off = np.cumsum([0] + ks)
-    evec = np.concatenate(E)
-    f = nll(E, _split(lam, ks))
+    f = nll_multi(E, _split(lam, ks), modalities)
     it = 0
-    res = stationarity(E, _split(lam, ks))
+    res = stationarity_multi(E, _split(lam, ks), modalities)
     while res > tol and it < max_iter:
         lams = _split(lam, ks)
-        grad = np.concatenate(gradient(E, lams))
-        diag, pair = marginals_sq2d(lams)
-        n = len(lam)
-        H = np.zeros((n, n))
-        for a in range(len(ks)):
-            H[off[a]:off[a + 1], off[a]:off[a + 1]] = np.diag(0.5 * diag[a])
-        for (a, b), m in pair.items():
-            H[off[a]:off[a + 1], off[b]:off[b + 1]] = 0.5 * m
-            H[off[b]:off[b + 1], off[a]:off[a + 1]] = 0.5 * m.T
-        Hp = P @ H @ P
-        step = -np.linalg.lstsq(Hp, P @ grad, rcond=None)[0]
-        step = P @ step
+        grad = np.concatenate(gradient_multi(E, lams, modalities))
+        H = _hessian_multi(lams, modalities, ks)
+        step = P @ (-np.linalg.lstsq(P @ H @ P, P @ grad, rcond=None)[0])
         alpha = 1.0
         while True:
             cand = lam + alpha * step
-            fc = nll(E, _split(cand, ks))
+            fc = nll_multi(E, _split(cand, ks), modalities)
             if np.isfinite(fc) and fc <= f + 1e-4 * alpha * float(grad @ step):
                 break
             alpha *= 0.5
             if alpha < 1e-12:
-                cand = lam
-                fc = f
+                cand, fc = lam, f
                 break
         if np.array_equal(cand, lam):
             break
         lam, f = cand, fc
         it += 1
-        res = stationarity(E, _split(lam, ks))
-    lams = _split(lam, ks)
+        res = stationarity_multi(E, _split(lam, ks), modalities)
+    return _split(lam, ks), it
+
+
+def kkt_residual(E, lams, eps: float, modalities=None) -> float:
+    """Stationarity on the box λ >= ε: max over coordinates of |E − g| off the floor and of
+    max(0, g − E) on it (a floor coordinate needs ∂NLL/∂λ = ½(E − g) >= 0), / max E."""
+    if modalities is None:
+        modalities = [list(range(len(E)))]
+    g = marginals_multi(lams, modalities)
+    emax = max(float(np.max(e)) for e in E)
+    r = 0.0
+    for e, gl, l in zip(E, g, lams):
+        e = np.asarray(e, np.float64)
+        on = np.asarray(l) <= eps
+        r = max(r, float(np.max(np.abs(e - gl)[~on], initial=0.0)),
+                float(np.max(np.maximum(0.0, gl - e)[on], initial=0.0)))
+    return r / emax
+
+
+def _box_mle(E, modalities, eps, tol, max_iter):
+    """argmin NLL over the box λ >= ε (Lemma 6's domain) by a primal active-set method:
+      * gauge directions left free (axes with no floor coordinate) along which the NLL is
+        linear and decreasing are followed to the first coordinate that reaches ε, which
+        joins the active set (the NLL is unbounded below along them otherwise);
+      * else a Newton step on the free coordinates (projected off the remaining gauge
+        directions), cut at the first bound reached, Armijo backtracking on the NLL;
+      * when the free coordinates are stationary, an active coordinate whose multiplier
+        ½(E − g) is negative is released (the most negative first); none left → KKT point.
+    Returns (lams, iterations, active mask)."""
+    ks = [len(e) for e in E]
+    nax = len(E)
+    off = np.cumsum([0] + ks)
+    ev = np.concatenate(E)
+    emax = float(ev.max())
+    lam = np.maximum(eps, np.concatenate([1.0 / e for e in E]))
+    active = lam <= eps
+    f = nll_multi(E, _split(lam, ks), modalities)
+    gtol = 1e-12 * float(np.abs(ev).sum())
+    it = 0
+    for it in range(max_iter):
+        lams = _split(lam, ks)
+        g = np.concatenate(marginals_multi(lams, modalities))
+        grad = 0.5 * (ev - g)
+        free_axes = [a for a in range(nax) if not active[off[a]:off[a + 1]].any()]
+        Q = gauge_lift(ks, gauge_space_free(nax, modalities, free_axes))
+        q = Q @ (Q.T @ grad)
+        if np.linalg.norm(q) > gtol:
+            d = -q
+            d[active] = 0.0          # q lives on the free axes (rounding elsewhere)
+            ratio = np.where(d < 0, (lam - eps) / np.where(d < 0, -d, 1.0), np.inf)
+            i = int(np.argmin(ratio))
+            lam = np.maximum(eps, lam + ratio[i] * d)
+            lam[i] = eps
+            active[i] = True
+            f = nll_multi(E, _split(lam, ks), modalities)
+            continue
+        F = ~active
+        r_free = float(np.max(np.abs(ev - g)[F], initial=0.0)) / emax
+        if r_free <= tol:
+            mult = (ev - g) / emax
+            if active.any() and float(mult[active].min()) < -tol:
+                idx = np.nonzero(active)[0]
+                active[idx[int(np.argmin(mult[active]))]] = False
+                continue
+            break
+        idx = np.nonzero(F)[0]
+        H = _hessian_multi(lams, modalities, ks)
+        QF = Q[idx, :]
+        P = np.eye(len(idx)) - QF @ QF.T
+        dF = -P @ np.linalg.lstsq(P @ H[np.ix_(idx, idx)] @ P, P @ grad[idx], rcond=None)[0]
+        d = np.zeros_like(lam)
+        d[idx] = dF
+        ratio = np.where(d < 0, (lam - eps) / np.where(d < 0, -d, 1.0), np.inf)
+        amax = float(ratio.min())
+        alpha = min(1.0, amax)
+        hit = alpha == amax
+        while True:
+            cand = np.maximum(eps, lam + alpha * d)
+            fc = nll_multi(E, _split(cand, ks), modalities)
+            if fc <= f + 1e-4 * alpha * float(grad @ d):
+                break
+            alpha *= 0.5
+            hit = False
+            if alpha < 1e-14:
+                cand, fc = lam, f
+                break
+        if hit:
+            i = int(np.argmin(ratio))
+            cand[i] = eps
+            active[i] = True
+        lam, f = cand, fc
+    return _split(lam, ks), it, active
+
+
+def _apply_gauge(lams, E, modalities, gauge, free_axes):
+    """Gauge 0 (reading G / G2): λ_l ← λ_l − (P_{G_F} μ)_l, μ_l = min λ_l; gauge 1: remove the
+    G_F component of λ − 1/E in the Σk coordinates (Algorithm 1's gradient steps keep
+    λ − λ⁰ ⊥ G).  G_F: the gauge directions over free_axes (all axes in the interior)."""
+    nax = len(lams)
+    N = gauge_space_free(nax, modalities, free_axes)
+    if N.size == 0:
+        return [np.asarray(l, np.float64).copy() for l in lams]
     if gauge == 0:
-        lams = canonical_gauge(lams)
-    info = dict(iterations=it, stationarity=stationarity(E, lams), nll=nll(E, lams),
-                grid_min=float(grid_sums(lams).min()),
-                trace_inconsistency=trace_inconsistency(E))
+        mu = np.array([float(np.min(l)) for l in lams])
+        sh = N @ (N.T @ mu)
+        return [np.asarray(l, np.float64) - float(sh[a]) for a, l in enumerate(lams)]
+    ks = [len(l) for l in lams]
+    Q = gauge_lift(ks, N)
+    v = np.concatenate([np.asarray(l, np.float64) - 1.0 / np.asarray(e, np.float64)
+                        for l, e in zip(lams, E)])
+    return _split(np.concatenate(lams) - Q @ (Q.T @ v), ks)
+
+
+def trace_inconsistency_multi(E, modalities) -> float:
+    """|P_G(tr E)|_max / mean tr E: the gauge component of the per-axis traces (reading T)."""
+    tr = np.array([float(np.sum(e)) for e in E])
+    N = gauge_space_multi(len(E), modalities)
+    ptr = N @ (N.T @ tr) if N.size else np.zeros_like(tr)
+    return float(np.max(np.abs(ptr)) / max(abs(tr.mean()), 1e-300))
+
+
+def _solve_mle(E, modalities, tol, max_iter, gauge, eps_scale, trace_tol):
+    E = [np.asarray(e, np.float64) for e in E]
+    if any(np.any(~np.isfinite(e)) or np.any(e <= 0) for e in E):
+        raise ValueError("E must be finite and > 0 (Thm 4 hypothesis, P:742)")
+    single = modalities is None
+    if single:
+        modalities = [list(range(len(E)))]
+    _check_modalities(len(E), modalities)
+    eps = eps_scale * max(float(np.max(1.0 / e)) for e in E)
+    ti = trace_inconsistency(E) if single else trace_inconsistency_multi(E, modalities)
+    if ti <= trace_tol:
+        Ee = project_spectrum(E, modalities)
+        lams, it = _interior_newton(Ee, modalities, tol, max_iter)
+        lams = _apply_gauge(lams, E, modalities, gauge, list(range(len(E))))
+        active = np.zeros(sum(len(e) for e in E), bool)
+        stat = stationarity_multi(Ee, lams, modalities)
+        regime = "interior"
+    else:
+        lams, it, active = _box_mle(E, modalities, eps, tol, max_iter)
+        ks = [len(e) for e in E]
+        off = np.cumsum([0] + ks)
+        free_axes = [a for a in range(len(E)) if not active[off[a]:off[a + 1]].any()]
+        lams = _apply_gauge(lams, E, modalities, gauge, free_axes)
+        stat = kkt_residual(E, lams, eps * (1 + 1e-9), modalities)
+        regime = "barrier"
+    info = dict(iterations=it, stationarity=stat, nll=nll_multi(E, lams, modalities),
+                grid_min=min(float(s.min()) for s in grid_sums_multi(lams, modalities)),
+                trace_inconsistency=ti, floor_active=bool(active.any()), eps=eps,
+                regime=regime, active=active)
     return lams, info
 
 
@@ -444,65 +657,13 @@ def canonical_gauge_multi(lams, modalities):
 
 
 def solve_eigvals_multi(E, modalities, tol: float = 1e-12, max_iter: int = 200,
-                        gauge: int = 0):
-    """Multi-modal eigenvalue MLE (Thm 2 with Σ_γ): argmin of nll_multi, computed as
-    in solve_eigvals — projected Newton on G⊥ (Hessian: per modality the 1/s² marginals,
-    summed), backtracking on NLL with grid feasibility, start λ = 1/E (Alg. 1 line 5)."""
-    E = [np.asarray(e, np.float64) for e in E]
-    ks = [len(e) for e in E]
-    _check_modalities(len(E), modalities)
-    if any(np.any(~np.isfinite(e)) or np.any(e <= 0) for e in E):
-        raise ValueError("E must be finite and > 0 (Thm 4 hypothesis, P:742)")
-    off = np.cumsum([0] + ks)
-    n = int(off[-1])
-    Nax = gauge_space_multi(len(E), modalities)
-    if Nax.size:
-        B = np.zeros((n, Nax.shape[1]))
-        for a in range(len(E)):
-            B[off[a]:off[a + 1], :] = Nax[a][None, :]
-        Q, _ = np.linalg.qr(B)
-        P = np.eye(n) - Q @ Q.T
-    else:
-        P = np.eye(n)
-    lam = np.concatenate([1.0 / e for e in E])
-    f = nll_multi(E, _split(lam, ks), modalities)
-    it = 0
-    res = stationarity_multi(E, _split(lam, ks), modalities)
-    while res > tol and it < max_iter:
-        lams = _split(lam, ks)
-        grad = np.concatenate(gradient_multi(E, lams, modalities))
-        H = np.zeros((n, n))
-        for mod in modalities:
-            diag, pair = marginals_sq2d([lams[a] for a in mod])
-            for pa, a in enumerate(mod):
-                H[off[a]:off[a + 1], off[a]:off[a + 1]] += np.diag(0.5 * diag[pa])
-            for (pa, pb), m in pair.items():
-                a, b = mod[pa], mod[pb]
-                H[off[a]:off[a + 1], off[b]:off[b + 1]] += 0.5 * m
-                H[off[b]:off[b + 1], off[a]:off[a + 1]] += 0.5 * m.T
-        step = P @ (-np.linalg.lstsq(P @ H @ P, P @ grad, rcond=None)[0])
-        alpha = 1.0
-        while True:
-            cand = lam + alpha * step
-            fc = nll_multi(E, _split(cand, ks), modalities)
-            if np.isfinite(fc) and fc <= f + 1e-4 * alpha * float(grad @ step):
-                break
-            alpha *= 0.5
-            if alpha < 1e-12:
-                cand, fc = lam, f
-                break
-        if np.array_equal(cand, lam):
-            break
-        lam, f = cand, fc
-        it += 1
-        res = stationarity_multi(E, _split(lam, ks), modalities)
-    lams = _split(lam, ks)
-    if gauge == 0:
-        lams = canonical_gauge_multi(lams, modalities)
-    info = dict(iterations=it, stationarity=stationarity_multi(E, lams, modalities),
-                nll=nll_multi(E, lams, modalities),
-                grid_min=min(float(s.min()) for s in grid_sums_multi(lams, modalities)))
-    return lams, info
+                        gauge: int = 0, eps_scale: float = 1e-10, trace_tol: float = 1e-8):
+    """Multi-modal eigenvalue MLE (Thm 2 with Σ_γ): argmin of nll_multi on the domain
+    Λ_l >= ε, computed as in solve_eigvals (reading T with the multi-modal gauge space G,
+    reading G2): interior projected Newton on G⊥ when |P_G(tr E)| <= trace_tol, else the
+    active-set method on the box."""
+    return _solve_mle(E, [list(m) for m in modalities], tol, max_iter, gauge, eps_scale,
+                      trace_tol)
 
 
 # ---------------------------------------------------------------------------
