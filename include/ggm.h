@@ -191,42 +191,64 @@ ggm_status ggm_project_csr(int64_t d, int64_t m, int64_t nnz, const int64_t *row
  * (2) Eigenvalue MLE — Theorem 2, Algorithm 1 lines 5-17.
  *
  * Minimises NLL(λ) = ½ Σ_l E_l·λ_l − ½ Σ_{j in k-grid} log s_j, s_j = Σ_l λ_l[j_l]
- * for ONE modality with L axes.  The gradient ½(E_l − g_l),
+ * for ONE modality with L axes, over the paper's domain λ_l >= ε (Lemma 6,
+ * P:657-690), ε = eps_scale · max(1/E).  The gradient ½(E_l − g_l),
  * g_l[i] = Σ_{j: j_l = i} 1/s_j, is evaluated by a grid-reduction kernel
  * over all prod(k) grid points, never materialising the grid.
  *
+ * Reading T: the marginals of every axis sum to the same Σ_j 1/s_j, so an interior
+ * stationary point needs equal traces tr E_l.  If the relative trace spread
+ * (trace_inconsistency) is <= opts->trace_tol the spectrum is replaced by its projection on
+ * G⊥ (the rounding-level gauge component dropped) and the interior MLE is returned
+ * (floor_active = 0).  Otherwise the NLL decreases without bound along a gauge direction
+ * and the minimum lies on the barrier: the majorise-minimise step is clamped at ε (a
+ * separable majoriser minimised on the box), every axis but the smallest-trace one ends with
+ * coordinates on the floor, and floor_active = 1 ("pick a smaller k").
+ *
  *  L      : number of axes, 1 <= L <= 8.
- *  k      : (host) L ranks; prod(k) < 2^40.
- *  E      : float64 sum(k), axis-concatenated Gram eigenvalues, each > 0 and finite.
+ *  k      : (host) L ranks; prod(k) < 2^40; max k <= 1024.
+ *  E      : float64 sum(k), axis-concatenated Gram eigenvalues, each > 0 and finite
+ *           (else GGM_ERR_DOMAIN).
  *  opts   : (host, may be NULL = defaults).
- *  lambda : out float64 sum(k), axis-concatenated, in the gauge opts->gauge.
+ *  lambda : out float64 sum(k), axis-concatenated, in the gauge opts->gauge (written also
+ *           when GGM_ERR_NO_CONVERGENCE is returned: the last iterate).
  *  info   : (host, may be NULL) diagnostics.
- * Scratch of O(Σk · #SMs) doubles is taken with stream-ordered cudaMallocAsync and released
+ * Scratch of O(Σk) doubles is taken with stream-ordered cudaMallocAsync and released
  * before returning.  Synchronizes `stream`.
  * ---------------------------------------------------------------------------------- */
 typedef struct {
-  double tol;        /* stop when max_l max_i |E_li − g_li| / max E <= tol (reading Q4).
-                        default 1e-7 */
-  int max_iter;      /* default 20000 */
-  double eps_scale;  /* feasibility floor eps = eps_scale * max(1/E). default 1e-10 */
-  int method;        /* 0 = multiplicative fixed point λ ← λ ⊙ g/E, the majorise-minimise
-                        step (the NLL decreases monotonically and λ stays > 0, so Algorithm 1's
-                        overshoot loop, never triggers), by default over-relaxed
-                        off the common-scale direction (exponent 1.5 in log space, same fixed
-                        point, λ > 0; a run that does not converge is repeated with the plain
-                        MM step; env GGM_MM_OMEGA=1 forces it).  Other values: GGM_ERR_UNSUPPORTED
-                        (Algorithm 1's gradient descent, readings Q1-Q3, lives in the oracle) */
+  double tol;        /* stop when the stationarity residual <= tol (reading Q4): max over
+                        coordinates of |E_li − g_li| (off the floor) or max(0, g_li − E_li) (on
+                        it, a KKT multiplier), / max E.  default 1e-7 */
+  int max_iter;      /* grid passes (methods 0, 1) or accepted steps (method 2); default 20000 */
+  double eps_scale;  /* floor ε = eps_scale * max(1/E). default 1e-10 */
+  int method;        /* 0 = majorise-minimise fixed point λ ← λ ⊙ g/E (the NLL decreases
+                          monotonically, λ stays > 0) accelerated by SQUAREM extrapolation in
+                          log space (3 passes per cycle, residual safeguard); the barrier
+                          regime and a non-converging accelerated run use the plain step;
+                        1 = the plain majorise-minimise step only;
+                        2 = Algorithm 1 as printed: Λ' = Λ − μ·½(E − g) (reading Q1), μ halved
+                          while the grid minimum Σ_l min Λ'_l < ε or the NLL does not decrease
+                          (readings Q2, Q3), never increased; slow (thousands of steps), the
+                          paper's reference method.
+                        Other values: GGM_ERR_INVALID_ARGUMENT.  (Projected Newton is the
+                        oracle's algorithm, not offered here: DESIGN.md BK4.) */
   int gauge;         /* 0 = min-balanced PSD gauge (default, reading G);
-                        1 = iterate as reached from λ0 = 1/E */
+                        1 = Algorithm 1's gauge, (λ − 1/E) ⊥ G (the gauge gradient steps from
+                          λ0 = 1/E keep).  In the barrier regime both act only among the axes
+                          with no coordinate on the floor. */
+  double trace_tol;  /* interior regime when trace_inconsistency <= trace_tol (reading T);
+                        default 1e-8 */
 } ggm_solve_opts;
 
 typedef struct {
-  int iterations;
-  double stationarity;        /* max |E − g| / max E at exit */
-  double nll;                 /* NLL at exit */
+  int iterations;             /* grid passes (methods 0, 1) or accepted steps (method 2) */
+  double stationarity;        /* the tol residual at exit (KKT form, against the projected
+                                 spectrum in the interior regime) */
+  double nll;                 /* NLL of the returned λ with the given E */
   double grid_min;            /* min_j s_j = Σ_l min λ_l */
   double trace_inconsistency; /* max_l |tr E_l − mean| / mean (reading T) */
-  int floor_active;           /* 1 if some grid sum hit the eps floor */
+  int floor_active;           /* 1 if some λ is on the floor ε (barrier regime) */
 } ggm_solve_info;
 
 void ggm_solve_opts_default(ggm_solve_opts *opts);

@@ -55,7 +55,7 @@ class GGMError(RuntimeError):
 
 class SolveOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("eps_scale", C.c_double),
-                ("method", C.c_int), ("gauge", C.c_int)]
+                ("method", C.c_int), ("gauge", C.c_int), ("trace_tol", C.c_double)]
 
 
 class SolveInfo(C.Structure):
@@ -437,9 +437,12 @@ def ggm_nonparanormal(X: torch.Tensor, axis: int, stream=None) -> torch.Tensor:
 # --------------------------------------------------------------------------- (2) solve
 
 def ggm_solve_eigvals(E: torch.Tensor, ks, tol: float = 1e-7, max_iter: int = 20000,
-                      gauge: int = 0, eps_scale: float = 1e-10, method: int = 0, stream=None):
-    """Eigenvalue MLE of Thm 2 on the k-grid (Alg. 1 lines 5-17).  E: float64 CUDA tensor,
-    axis-concatenated (sum(ks)).  Returns (lambda float64 sum(ks), info dict)."""
+                      gauge: int = 0, eps_scale: float = 1e-10, method: int = 0,
+                      trace_tol: float = 1e-8, stream=None, out=None):
+    """Eigenvalue MLE of Thm 2 on the k-grid (Alg. 1 lines 5-17) over Lemma 6's domain
+    λ >= ε (include/ggm.h (2), reading T).  E: float64 CUDA tensor, axis-concatenated
+    (sum(ks)).  Returns (lambda float64 sum(ks), info dict).  With out=(tensor,) the last
+    iterate is written there even when GGM_ERR_NO_CONVERGENCE is raised."""
     _require_cuda(E, torch.float64, "E")
     ks = [int(k) for k in ks]
     if E.numel() != sum(ks):
@@ -448,7 +451,8 @@ def ggm_solve_eigvals(E: torch.Tensor, ks, tol: float = 1e-7, max_iter: int = 20
     o = SolveOpts()
     lib().ggm_solve_opts_default(C.byref(o))
     o.tol, o.max_iter, o.gauge, o.eps_scale, o.method = tol, max_iter, gauge, eps_scale, method
-    lam = torch.empty_like(E)
+    o.trace_tol = trace_tol
+    lam = out[0] if out is not None else torch.empty_like(E)
     info = SolveInfo()
     _check(lib().ggm_solve_eigvals(len(ks), karr, _ptr(E), C.byref(o), _ptr(lam), C.byref(info),
                                    _stream(stream)))
@@ -456,7 +460,8 @@ def ggm_solve_eigvals(E: torch.Tensor, ks, tol: float = 1e-7, max_iter: int = 20
 
 
 def ggm_solve_eigvals_multi(E: torch.Tensor, ks, modalities, tol: float = 1e-7,
-                            max_iter: int = 20000, gauge: int = 0, stream=None):
+                            max_iter: int = 20000, gauge: int = 0, method: int = 0,
+                            eps_scale: float = 1e-10, trace_tol: float = 1e-8, stream=None):
     """Multi-modal eigenvalue MLE (Thm 2 with Σ_γ): E axis-concatenated over the global
     axes (ranks ks), modalities = lists of global axis ids.  Returns (lambda, info)."""
     _require_cuda(E, torch.float64, "E")
@@ -470,7 +475,8 @@ def ggm_solve_eigvals_multi(E: torch.Tensor, ks, modalities, tol: float = 1e-7,
         ptr.append(len(axes))
     o = SolveOpts()
     lib().ggm_solve_opts_default(C.byref(o))
-    o.tol, o.max_iter, o.gauge = tol, max_iter, gauge
+    o.tol, o.max_iter, o.gauge, o.method = tol, max_iter, gauge, method
+    o.eps_scale, o.trace_tol = eps_scale, trace_tol
     lam = torch.empty_like(E)
     info = SolveInfo()
     _check(lib().ggm_solve_eigvals_multi(len(ks), (C.c_int * len(ks))(*ks), _ptr(E),

@@ -1,27 +1,30 @@
 // grid_solve.cu — Kronecker-sum eigenvalue MLE on the k-grid (Theorem 2, P:354-376;
-// Algorithm 1 lines 5-17).
+// Algorithm 1 lines 5-17; the domain Λ_l >= ε of Lemma 6).
 //
 // The Thm 2 trace term for one modality is the vector of grid marginals
 //     g_l[i] = Σ_{grid points j with j_l = i} 1 / s_j,   s_j = Σ_l λ_l[j_l]
 // over all prod(k) grid points.  The grid is never stored: each pass regenerates s_j from
-// the Σk eigenvalues held in shared memory (BK4 is bound by the reciprocal rate, not HBM).
+// the Σk eigenvalues held in shared memory (BK4 is bound by the FP64 + SFU pipes, not HBM).
 //
-// Solver: the multiplicative update λ ← λ ⊙ g / E.  It is the
-// majorise-minimise step for the NLL (Jensen on -log s with weights λ_l[j_l]/s_j gives a
-// separable majoriser whose minimiser is exactly λ g / E), so the NLL decreases
-// monotonically and λ stays > 0: Algorithm 1's feasibility loop never triggers.
-// By default the step is over-relaxed, λ ← λ ⊙ (g / E)^1.5 off the common-scale direction
-// (same fixed point, λ still > 0, 20-37 % fewer iterations), with a plain-MM rerun if that
-// does not converge (mm_omega).
-// The whole loop runs in ONE cooperative persistent kernel: per iteration a grid pass
-// (per-block partial marginals), grid.sync, a per-entry reduction + update + stationarity
-// max, grid.sync.
+// Solver (BK4): the majorise-minimise step λ ← λ ⊙ g / E.  Jensen on -log s with
+// weights λ_l[j_l]/s_j gives a separable majoriser of the NLL whose minimiser is
+// exactly λ g / E (on the box λ >= ε: max(ε, λ g / E)), so the NLL decreases monotonically
+// and λ stays > 0.  Method 0 accelerates the fixed point with SQUAREM (squared extrapolation
+// in log space: two map evaluations, one extrapolated point, one stabilising evaluation per
+// cycle; the extrapolation is kept only if its residual does not exceed the plain iterate's),
+// 3-4x fewer grid passes; method 2 runs Algorithm 1's gradient descent as printed.
+// The whole loop runs in ONE cooperative persistent kernel: per pass, the grid reduction into
+// per-block partials, one grid-wide barrier, and an update computed identically (bitwise) by
+// every block from the same reduced marginals.
 //
 // Layout of the pass: the axis with the largest k is the "inner" axis (contiguous in the
-// lanes of a warp); every other axis is "outer".  One warp owns one outer multi-index row
-// at a time: s = base(row) + λ_inner[m].  fp64 throughout: SFU-seeded fp64 reciprocals
-// (one Newton step), per-lane accumulators, warp-shuffle row sums, shared-memory block
-// partials and cross-block sums.  The pass is bound by the FP64 + SFU pipes, not HBM.
+// lanes of a warp, ⌈k/32⌉ points per lane); the other axes are "outer" and one outer
+// multi-index = one row.  A warp owns a contiguous range of rows.  Per grid point: one fp64
+// add (s), one SFU reciprocal seed + two FP64 FMAs (Newton), two fp64 adds (the inner
+// marginal in a per-lane register, the row sum).  Row sums are reduced four rows at a time
+// by a reduce-scatter across the warp and added into per-warp private shared-memory bins of
+// the fastest outer axis; the slowest outer axis (L = 3) changes once per k_fast rows and is
+// accumulated in a register.  No fp64 shared-memory atomics in the per-row path.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -42,6 +45,7 @@ namespace gs {
 constexpr int kMaxAxes = 8;
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+constexpr int kMaxFastBins = 1024;  // private per-warp bins: kWarps x k_fast doubles
 
 struct GridDesc {
   int L;                   // axes
@@ -55,9 +59,6 @@ struct GridDesc {
   int total;               // Σ k
 };
 
-
-// One grid pass: this block's partial marginals in sg (fp64, Σk entries, zeroed by caller).
-// slam: fp32 λ (Σk), in shared memory.
 // Reciprocal of a positive double: MUFU 64-bit approximation (~2^-20 relative, the SFU
 // pipe) refined by one Newton step on the FP64 pipe (error ~2^-40).
 __device__ __forceinline__ double rcp_f64(double s) {
@@ -67,32 +68,43 @@ __device__ __forceinline__ double rcp_f64(double s) {
   return fma(r, e, r);
 }
 
-// One grid pass over this block's share of the outer rows: per-lane fp64 accumulators for
-// the inner axis, warp-shuffle row sums for the outer axes, fp64 shared-memory partials sg.
-// All of s, 1/s and the sums are fp64 (no fixed fp32 rounding of λ or s that would floor
-// the stationarity residual; e.g. the isotropic case, where every s_j is equal, would
-// otherwise carry one identical rounding error in every term).
-// NOUT = number of outer axes when known at compile time (0, 1, 2 cover L <= 3, i.e. every
-// BASELINE config); -1 = generic.  The per-row bookkeeping (base sum, odometer, outer
-// marginal atomics) is kept out of constant-bank indexing so that it stays small next to the
-// k_inner points of the row.
-template <int J, int NOUT>
-__device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* sg, int64_t gwarp,
-                                int64_t nwarps) {
-  constexpr int NO = NOUT < 0 ? kMaxAxes : (NOUT == 0 ? 1 : NOUT);
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Reduce-scatter of four per-lane row partials: returns, in lanes 0, 8, 16, 24, the warp
+// totals of rows 0, 1, 2, 3 (other lanes: partial garbage).  6 fp64 shuffles for 4 rows.
+__device__ __forceinline__ double reduce4(const double (&p)[4], int lane) {
+  const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
+  const double k0 = b4 ? p[2] : p[0], k1 = b4 ? p[3] : p[1];
+  const double s0 = b4 ? p[0] : p[2], s1 = b4 ? p[1] : p[3];
+  const double a0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+  const double a1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+  double b = (b3 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, b3 ? a0 : a1, 8);
+  b += __shfl_xor_sync(0xffffffffu, b, 4);
+  b += __shfl_xor_sync(0xffffffffu, b, 2);
+  b += __shfl_xor_sync(0xffffffffu, b, 1);
+  return b;
+}
+
+// One grid pass over this block's share of the outer rows, for NOUT outer axes (0, 1, 2:
+// every L <= 3, i.e. every BASELINE config).  slam: λ (Σk, fp64, shared); sg: this block's
+// marginal partials (Σk [+1: Σ log s when LOGS], shared, zeroed by the caller); pw: kWarps x
+// k_fast private bins (shared, zero on entry, zero again on exit).
+template <int J, int NOUT, bool LOGS>
+__device__ void grid_pass_fast(const GridDesc& gd, const double* slam, double* sg, double* pw,
+                               int64_t gwarp, int64_t nwarps) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int kin = gd.k[gd.inner];
   const int oin = gd.off[gd.inner];
-  const int nout = NOUT < 0 ? gd.n_outer : NOUT;
-  int ko[NO], oo[NO], idx[NO];
-  int64_t so[NO];
-#pragma unroll
-  for (int a = 0; a < NO; ++a) {
-    const bool live = a < nout;
-    ko[a] = live ? gd.k[gd.outer_axes[a]] : 1;
-    oo[a] = live ? gd.off[gd.outer_axes[a]] : 0;
-    so[a] = live ? gd.outer_stride[a] : 1;
-  }
+  const int af = NOUT >= 1 ? gd.outer_axes[NOUT - 1] : 0;  // fastest outer axis
+  const int as = NOUT == 2 ? gd.outer_axes[0] : 0;         // slowest outer axis
+  const int kf = NOUT >= 1 ? gd.k[af] : 1, ks = NOUT == 2 ? gd.k[as] : 1;
+  const double* lf = slam + (NOUT >= 1 ? gd.off[af] : 0);
+  const double* ls = slam + (NOUT == 2 ? gd.off[as] : 0);
+  double* bins = pw + wid * kf;
   double lv[J], acc[J];
 #pragma unroll
   for (int jj = 0; jj < J; ++jj) {
@@ -100,44 +112,148 @@ __device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* 
     lv[jj] = (m < kin) ? slam[oin + m] : 1.0;
     acc[jj] = 0.0;
   }
-  // this warp's contiguous range of outer rows; the multi-index advances like an odometer
+  double lsum = 0.0;
   const int64_t per = (gd.rows + nwarps - 1) / nwarps;
   const int64_t r0 = gwarp * per;
   const int64_t r1 = min(gd.rows, r0 + per);
+  int fi = NOUT >= 1 ? (int)(r0 % kf) : 0;
+  int si = NOUT == 2 ? (int)((r0 / kf) % ks) : 0;
+  double slow_acc = 0.0;
+  int slow_idx = si;
+  for (int64_t row = r0; row < r1; row += 4) {
+    double p[4];
+    int fq[4];
 #pragma unroll
-  for (int a = 0; a < NO; ++a) idx[a] = a < nout ? (int)((r0 / so[a]) % ko[a]) : 0;
+    for (int q = 0; q < 4; ++q) {
+      const bool live = row + q < r1;
+      if (NOUT == 2 && live && si != slow_idx) {  // flush the slow axis (once per kf rows)
+        const double t = warp_sum(slow_acc);
+        if (lane == 0) atomicAdd(&sg[gd.off[as] + slow_idx], t);
+        slow_acc = 0.0;
+        slow_idx = si;
+      }
+      double base = 0.0;
+      if (NOUT >= 1) base += lf[fi];
+      if (NOUT == 2) base += ls[si];
+      double pq = 0.0;
+      if (live) {
+        // pairwise row partial (short dependency chain) up to 16 points per lane; a running
+        // sum above that (register pressure)
+        constexpr int JP = J <= 16 ? J : 1;
+        double part[JP];
+#pragma unroll
+        for (int jj = 0; jj < JP; ++jj) part[jj] = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) {
+          const int m = lane + 32 * jj;
+          if (m < kin) {
+            const double s = base + lv[jj];
+            const double r = rcp_f64(s);
+            if (LOGS) lsum += log(s);
+            acc[jj] += r;
+            part[J <= 16 ? jj : 0] += r;
+          }
+        }
+#pragma unroll
+        for (int w = 1; w < JP; w <<= 1)
+#pragma unroll
+          for (int jj = 0; jj + w < JP; jj += 2 * w) part[jj] += part[jj + w];
+        pq = part[0];
+      }
+      p[q] = pq;
+      fq[q] = fi;
+      if (NOUT == 2) slow_acc += pq;
+      if (NOUT >= 1 && live) {  // odometer: fastest outer axis first
+        if (++fi == kf) {
+          fi = 0;
+          if (NOUT == 2 && ++si == ks) si = 0;
+        }
+      }
+    }
+    if (NOUT >= 1) {
+      const double tot = reduce4(p, lane);
+      const int q = lane >> 3;
+      const int f = q == 0 ? fq[0] : q == 1 ? fq[1] : q == 2 ? fq[2] : fq[3];
+      if ((lane & 7) == 0 && row + q < r1) {
+        if (kf >= 4)
+          bins[f] += tot;  // four consecutive rows: four distinct fast indices
+        else
+          atomicAdd(&bins[f], tot);
+      }
+      __syncwarp();  // the next group's lanes may update the same bins
+    }
+  }
+  if (NOUT == 2) {
+    const double t = warp_sum(slow_acc);
+    if (lane == 0 && r0 < r1) atomicAdd(&sg[gd.off[as] + slow_idx], t);
+  }
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const int m = lane + 32 * jj;
+    if (m < kin) atomicAdd(&sg[oin + m], acc[jj]);
+  }
+  if (LOGS) {
+    lsum = warp_sum(lsum);
+    if (lane == 0) atomicAdd(&sg[gd.total], lsum);
+  }
+  if (NOUT >= 1) {  // fold the private bins into the block partials, clear them
+    __syncthreads();
+    for (int f = threadIdx.x; f < kf; f += blockDim.x) {
+      double t = 0.0;
+      for (int w = 0; w < kWarps; ++w) {
+        t += pw[w * kf + f];
+        pw[w * kf + f] = 0.0;
+      }
+      sg[gd.off[af] + f] += t;
+    }
+    __syncthreads();
+  }
+}
+
+// Generic pass (any number of outer axes, or a fastest outer axis above kMaxFastBins): per
+// row a warp-shuffle row sum and one shared-memory atomic per outer axis.
+template <int J, bool LOGS>
+__device__ void grid_pass_generic(const GridDesc& gd, const double* slam, double* sg,
+                                  int64_t gwarp, int64_t nwarps) {
+  const int lane = threadIdx.x & 31;
+  const int kin = gd.k[gd.inner];
+  const int oin = gd.off[gd.inner];
+  const int nout = gd.n_outer;
+  int idx[kMaxAxes];
+  double lv[J], acc[J];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const int m = lane + 32 * jj;
+    lv[jj] = (m < kin) ? slam[oin + m] : 1.0;
+    acc[jj] = 0.0;
+  }
+  double lsum = 0.0;
+  const int64_t per = (gd.rows + nwarps - 1) / nwarps;
+  const int64_t r0 = gwarp * per;
+  const int64_t r1 = min(gd.rows, r0 + per);
+  for (int a = 0; a < nout; ++a) idx[a] = (int)((r0 / gd.outer_stride[a]) % gd.k[gd.outer_axes[a]]);
   for (int64_t row = r0; row < r1; ++row) {
     double base = 0.0;
-#pragma unroll
-    for (int a = 0; a < NO; ++a)
-      if (a < nout) base += slam[oo[a] + idx[a]];
+    for (int a = 0; a < nout; ++a) base += slam[gd.off[gd.outer_axes[a]] + idx[a]];
     double rsum = 0.0;
 #pragma unroll
     for (int jj = 0; jj < J; ++jj) {
       const int m = lane + 32 * jj;
       if (m < kin) {
-        const double r = rcp_f64(base + lv[jj]);
+        const double s = base + lv[jj];
+        const double r = rcp_f64(s);
+        if (LOGS) lsum += log(s);
         rsum += r;
         acc[jj] += r;
       }
     }
     if (nout > 0) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-      // lane a adds the row sum to g_{outer axis a}[idx_a]
-#pragma unroll
-      for (int a = 0; a < NO; ++a)
-        if (a < nout && lane == a) atomicAdd(&sg[oo[a] + idx[a]], rsum);
-      // odometer: last outer axis fastest
-      bool carry = true;
-#pragma unroll
-      for (int a = NO - 1; a >= 0; --a) {
-        if (a < nout && carry) {
-          if (++idx[a] == ko[a])
-            idx[a] = 0;
-          else
-            carry = false;
-        }
+      rsum = warp_sum(rsum);
+      for (int a = 0; a < nout; ++a)
+        if (lane == a) atomicAdd(&sg[gd.off[gd.outer_axes[a]] + idx[a]], rsum);
+      for (int a = nout - 1; a >= 0; --a) {
+        if (++idx[a] < gd.k[gd.outer_axes[a]]) break;
+        idx[a] = 0;
       }
     }
   }
@@ -146,170 +262,284 @@ __device__ void grid_pass_block(const GridDesc& gd, const double* slam, double* 
     const int m = lane + 32 * jj;
     if (m < kin) atomicAdd(&sg[oin + m], acc[jj]);
   }
-}
-
-template <int J>
-__device__ __forceinline__ void grid_pass(const GridDesc& gd, const double* slam, double* sg,
-                                          int64_t gwarp, int64_t nwarps) {
-  switch (gd.n_outer) {
-    case 0: grid_pass_block<J, 0>(gd, slam, sg, gwarp, nwarps); break;
-    case 1: grid_pass_block<J, 1>(gd, slam, sg, gwarp, nwarps); break;
-    case 2: grid_pass_block<J, 2>(gd, slam, sg, gwarp, nwarps); break;
-    default: grid_pass_block<J, -1>(gd, slam, sg, gwarp, nwarps); break;
+  if (LOGS) {
+    lsum = warp_sum(lsum);
+    if (lane == 0) atomicAdd(&sg[gd.total], lsum);
   }
 }
 
-__device__ __forceinline__ void load_lambda(const double* lam, int total, double* slam,
-                                            bool bypass_l1) {
-  for (int i = threadIdx.x; i < total; i += blockDim.x)
-    slam[i] = bypass_l1 ? __ldcg(&lam[i]) : lam[i];
+__host__ __device__ inline bool fast_path(const GridDesc& gd) {
+  return gd.n_outer <= 2 &&
+         (gd.n_outer == 0 || gd.k[gd.outer_axes[gd.n_outer - 1]] <= kMaxFastBins);
+}
+__host__ __device__ inline int fast_bins(const GridDesc& gd) {
+  return (gd.n_outer >= 1 && fast_path(gd)) ? gd.k[gd.outer_axes[gd.n_outer - 1]] : 0;
+}
+
+template <int J, bool LOGS>
+__device__ __forceinline__ void grid_pass(const GridDesc& gd, const double* slam, double* sg,
+                                          double* pw, int64_t gwarp, int64_t nwarps) {
+  if (!fast_path(gd) || pw == nullptr) {
+    grid_pass_generic<J, LOGS>(gd, slam, sg, gwarp, nwarps);
+    return;
+  }
+  switch (gd.n_outer) {
+    case 0: grid_pass_fast<J, 0, LOGS>(gd, slam, sg, pw, gwarp, nwarps); break;
+    case 1: grid_pass_fast<J, 1, LOGS>(gd, slam, sg, pw, gwarp, nwarps); break;
+    default: grid_pass_fast<J, 2, LOGS>(gd, slam, sg, pw, gwarp, nwarps); break;
+  }
 }
 
 constexpr int kMaxMods = 8;  // modalities of a multi-modal solve
 
-// Exponent ω of the multiplicative update λ <- λ ⊙ (g/E)^ω.  ω = 1 is the MM step (monotone
-// NLL); near the fixed point its error contracts by the MM Jacobian's eigenvalues μ ∈ [0, 1),
-// over-relaxation maps them to 1 − ω(1 − μ) (still contracting for ω < 2 / (1 − μ_min)), which
-// speeds the slow modes that set the iteration count; the common-scale direction (μ = 0) is
-// left at the MM step (see solve_kernel).  Default 1.5 with a plain-MM rerun if it does not
-// converge (solve_with_fallback); GGM_MM_OMEGA overrides (BK4 has the sweep).
-static double mm_omega() {
-  const char* e = std::getenv("GGM_MM_OMEGA");
-  const double w = e ? std::atof(e) : 1.5;
-  return (w > 0.0 && w < 2.0) ? w : 1.0;
-}
+enum Scheme { kSchemeMM = 0, kSchemeSquarem = 1, kSchemeGD = 2 };
 
 struct SolveParams {
   GridDesc gd[kMaxMods];  // one per modality; offsets index the global concatenation
   int M;                  // modalities
   int T;                  // Σk over all axes
-  const double* E;
-  double* lam_out;    // converged λ (gauge 1: as iterated), Σk
-  double* g;          // marginals at lam_out, Σk
-  double* gacc;       // [3][Σk] rotating global accumulators of the block partials
-  int* status;        // [0] iterations, [1] converged flag
-  double* res_out;    // stationarity of lam_out
+  const double* E;        // spectrum of the update and the residual (G⊥-projected in the
+                          // interior regime, reading T; as given in the barrier regime / GD)
+  double floor;           // barrier ε (> 0: barrier regime, λ >= floor); 0: interior
+  double gd_eps;          // method 2: grid-minimum feasibility ε (reading Q3)
+  int scheme;
+  int pw_stride;          // doubles of private bins per block (kWarps x max k_fast)
+  double* lam_out;        // λ at exit, Σk
+  double* g;              // marginals at lam_out, Σk
+  double* gacc;           // [3][Σk + 1] rotating global accumulators of the block partials
+  int* status;            // [0] iterations, [1] converged flag
+  double* res_out;        // stationarity of lam_out
   double tol;
   int max_iter;
-  double omega;       // update exponent: λ <- λ ⊙ (g / E)^omega (1 = the MM step)
 };
 
-// Whole MM iteration in one cooperative kernel with ONE grid-wide barrier per iteration:
-// every block keeps its own copy of λ in shared memory; block partial marginals are added
-// atomically into global slot it%3; after grid.sync every block reads the same sums,
-// computes the same residual and the same update (bitwise identical in all blocks).
-// Slot (it+1)%3 is cleared by block 0 during iteration it: its last readers finished before
-// the barrier of iteration it-1, and its next writers start after the barrier of it.
-template <int J>
+// Block-wide reductions (every block runs them in the same order on the same data, so the
+// results are bitwise identical across blocks).  red: kWarps doubles of shared scratch.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) t += red[w];
+  return t;
+}
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = red[0];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) t = fmax(t, red[w]);
+  return t;
+}
+__device__ __forceinline__ double block_min(double v, double* red) {
+  return -block_max(-v, red);
+}
+
+// KKT residual at λ with marginals g (reading Q4, Lemma 6's box): |E − g| off the floor,
+// max(0, g − E) on it; the caller divides by max E.
+__device__ __forceinline__ double kkt_term(double lam, double g, double e, double floor) {
+  return (floor > 0.0 && lam <= floor * (1.0 + 1e-9)) ? fmax(0.0, g - e) : fabs(e - g);
+}
+
+// Whole solve in one cooperative kernel.  Shared memory: sg[T+1] (partials, then the reduced
+// marginals and Σ log s), slam[T] (the point the next pass evaluates), th0[T], th1[T]
+// (SQUAREM iterates in log space; GD: the accepted λ and its marginals), private bins.
+template <int J, bool LOGS>
 __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
   const int T = p.T;
-  double* sg = dsm;        // Σk block partials, then the reduced marginals
-  double* slam = sg + T;   // Σk this block's λ
+  double* sg = dsm;
+  double* slam = sg + T + 1;
+  double* th0 = slam + T;
+  double* th1 = th0 + T;
+  double* pw = p.pw_stride > 0 ? th1 + T : nullptr;  // private bins (fast pass) if allotted
   __shared__ double s_red[kWarps];
-  __shared__ double s_emax;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < T; i += blockDim.x) slam[i] = 1.0 / p.E[i];  // Alg. 1 line 5
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int i = 0; i < T; ++i) m = fmax(m, p.E[i]);
-    s_emax = m;
+  const int tid = threadIdx.x;
+  const double* __restrict__ E = p.E;
+  for (int i = tid; i < T; i += blockDim.x) {
+    const double l0 = fmax(1.0 / E[i], p.floor);  // Alg. 1 line 5
+    slam[i] = l0;
+    if (p.scheme != kSchemeMM) th0[i] = log(l0);
   }
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + wid;
+  for (int i = tid; i < p.pw_stride; i += blockDim.x) pw[i] = 0.0;
+  double emax = 0.0;
+  for (int i = tid; i < T; i += blockDim.x) emax = fmax(emax, E[i]);
+  emax = block_max(emax, s_red);
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (tid >> 5);
   const int64_t nw = (int64_t)gridDim.x * kWarps;
-  int it = 0;
-  bool done = false;
-  double res = 0.0;
   const bool single = gridDim.x == 1;
-  for (;; ++it) {
-    for (int i = threadIdx.x; i < T; i += blockDim.x) sg[i] = 0.0;
+  const int T1 = T + 1;
+  int it = 0, pass = 0, phase = 0;
+  bool done = false, stalled = false;
+  double res = 0.0, r1 = 0.0;
+  double f_acc = 0.0, mu = 1.0;  // GD: NLL of the accepted λ, step size (Alg. 1 line 6)
+  double* out_lam = slam;         // where the result lives at exit
+  double* out_g = sg;
+  for (;; ++pass) {
+    // ---------------------------------------------------------------- grid pass at slam
+    for (int i = tid; i < T1; i += blockDim.x) sg[i] = 0.0;
     if (blockIdx.x == 0 && !single)
-      for (int i = threadIdx.x; i < T; i += blockDim.x) p.gacc[(size_t)((it + 1) % 3) * T + i] = 0.0;
+      for (int i = tid; i < T1; i += blockDim.x) p.gacc[(size_t)((pass + 1) % 3) * T1 + i] = 0.0;
     __syncthreads();
     // Σ_γ of the modalities' marginals (Thm 2): each pass adds into the same sg
-    for (int m = 0; m < p.M; ++m) grid_pass<J>(p.gd[m], slam, sg, gw, nw);
+    for (int m = 0; m < p.M; ++m) grid_pass<J, LOGS>(p.gd[m], slam, sg, pw, gw, nw);
     __syncthreads();
-    double mr = 0.0;
-    if (single) {  // one block: the block partials are the marginals, no grid barrier
-      for (int i = threadIdx.x; i < T; i += blockDim.x) mr = fmax(mr, fabs(p.E[i] - sg[i]));
-    } else {
-      double* acc = p.gacc + (size_t)(it % 3) * T;
-      for (int i = threadIdx.x; i < T; i += blockDim.x) atomicAdd(&acc[i], sg[i]);
+    if (!single) {
+      double* acc = p.gacc + (size_t)(pass % 3) * T1;
+      for (int i = tid; i < T1; i += blockDim.x) atomicAdd(&acc[i], sg[i]);
       grid.sync();
-      // reduced marginals g (identical in every block), stationarity max |E - g| / max E
-      for (int i = threadIdx.x; i < T; i += blockDim.x) {
-        const double gi = __ldcg(&acc[i]);
-        sg[i] = gi;
-        mr = fmax(mr, fabs(p.E[i] - gi));
-      }
+      for (int i = tid; i < T1; i += blockDim.x) sg[i] = __ldcg(&acc[i]);
+      __syncthreads();
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
-    if (lane == 0) s_red[wid] = mr;
-    __syncthreads();
-    mr = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) mr = fmax(mr, s_red[w]);
-    res = mr / s_emax;
+    // ---------------------------------------------------------------- update
+    if (p.scheme == kSchemeGD) {
+      // Algorithm 1 as printed (readings Q1-Q3): the pass evaluated the candidate Λ' (or λ0)
+      double lin = 0.0;
+      for (int i = tid; i < T; i += blockDim.x) lin += E[i] * slam[i];
+      lin = block_sum(lin, s_red);
+      const double f = 0.5 * lin - 0.5 * sg[T];
+      const bool accept = pass == 0 || f <= f_acc;
+      if (accept) {  // Λ ← Λ' (lines 16-17): keep λ and its marginals
+        for (int i = tid; i < T; i += blockDim.x) {
+          th0[i] = slam[i];
+          th1[i] = sg[i];
+        }
+        f_acc = f;
+        if (pass > 0) ++it;
+      } else {
+        mu *= 0.5;  // NLL did not decrease (reading Q2)
+      }
+      __syncthreads();
+      out_lam = th0;
+      out_g = th1;
+      double mr = 0.0;
+      for (int i = tid; i < T; i += blockDim.x) mr = fmax(mr, fabs(E[i] - th1[i]));
+      res = block_max(mr, s_red) / emax;
+      if (res <= p.tol) {
+        done = true;
+        break;
+      }
+      if (it >= p.max_iter) break;
+      // next candidate: Λ' = Λ − μ·½(E − g), μ halved while Σ_l min Λ'_l < ε (line 11)
+      for (;;) {
+        double gmin = INFINITY;
+        for (int m = 0; m < p.M; ++m) {
+          const GridDesc& gd = p.gd[m];
+          double smin = 0.0;
+          for (int a = 0; a < gd.L; ++a) {
+            double mn = INFINITY;
+            for (int i = tid; i < gd.k[a]; i += blockDim.x) {
+              const int c = gd.off[a] + i;
+              mn = fmin(mn, th0[c] - mu * 0.5 * (E[c] - th1[c]));
+            }
+            smin += block_min(mn, s_red);
+          }
+          gmin = fmin(gmin, smin);
+        }
+        if (gmin >= p.gd_eps) break;
+        mu *= 0.5;
+        if (mu < 1e-300) break;
+      }
+      if (mu < 1e-300) {
+        stalled = true;
+        break;
+      }
+      for (int i = tid; i < T; i += blockDim.x) slam[i] = th0[i] - mu * 0.5 * (E[i] - th1[i]);
+      __syncthreads();
+      continue;
+    }
+    double mr = 0.0;
+    for (int i = tid; i < T; i += blockDim.x) mr = fmax(mr, kkt_term(slam[i], sg[i], E[i], p.floor));
+    res = block_max(mr, s_red) / emax;
     if (res <= p.tol) {
       done = true;
       break;
     }
     if (it == p.max_iter) break;
-    // majorise-minimise update λ <- λ ⊙ g / E
-    if (p.omega == 1.0) {
-      for (int i = threadIdx.x; i < T; i += blockDim.x) slam[i] = slam[i] * sg[i] / p.E[i];
-    } else {
-      // log-space step δ_i = log(g_i / E_i); its mean m is the common-scale direction, which
-      // the MM step already solves exactly (the map is invariant to λ -> cλ), so only
-      // δ − m is over-relaxed: λ_i <- λ_i exp(m + ω (δ_i − m)).  The block reduction runs in
-      // the same order in every block (bitwise-identical λ copies).
-      double part = 0.0;
-      for (int i = threadIdx.x; i < T; i += blockDim.x) {
-        const double d = log(sg[i] / p.E[i]);
-        sg[i] = d;
-        part += d;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      __syncthreads();  // every warp has read s_red (the stationarity max)
-      if (lane == 0) s_red[wid] = part;
+    ++it;
+    if (p.scheme == kSchemeMM) {
+      // majorise-minimise step, clamped on the box (a separable majoriser minimised per
+      // coordinate)
+      for (int i = tid; i < T; i += blockDim.x) slam[i] = fmax(p.floor, slam[i] * sg[i] / E[i]);
       __syncthreads();
-      double m = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) m += s_red[w];
-      m /= T;
-      for (int i = threadIdx.x; i < T; i += blockDim.x)
-        slam[i] = slam[i] * exp(m + p.omega * (sg[i] - m));
+      continue;
+    }
+    // SQUAREM (interior regime, floor = 0), log space θ = log λ, map F(θ) = θ + log(g/E)
+    if (phase == 0) {  // slam = exp(θ0): θ1 = F(θ0)
+      for (int i = tid; i < T; i += blockDim.x) {
+        const double t1 = th0[i] + log(sg[i] / E[i]);
+        th1[i] = t1;
+        slam[i] = exp(t1);
+      }
+      phase = 1;
+    } else if (phase == 1) {  // slam = exp(θ1): θ2 = F(θ1), extrapolate
+      r1 = res;
+      double nr = 0.0, nv = 0.0;
+      for (int i = tid; i < T; i += blockDim.x) {
+        const double t0 = th0[i], t1 = th1[i];
+        const double t2 = t1 + log(sg[i] / E[i]);
+        sg[i] = t2;
+        const double rr = t1 - t0, v = t2 - 2.0 * t1 + t0;
+        nr += rr * rr;
+        nv += v * v;
+      }
+      nr = block_sum(nr, s_red);
+      nv = block_sum(nv, s_red);
+      double al = nv > 0.0 ? -sqrt(nr / nv) : -1.0;
+      al = fmin(-1.0, fmax(al, -1e3));
+      for (int i = tid; i < T; i += blockDim.x) {
+        const double t0 = th0[i], t1 = th1[i], t2 = sg[i];
+        const double tp = t0 - 2.0 * al * (t1 - t0) + al * al * (t2 - 2.0 * t1 + t0);
+        th0[i] = t2;  // fallback: the plain iterate θ2
+        th1[i] = tp;
+        slam[i] = exp(tp);
+      }
+      phase = 2;
+    } else {  // slam = exp(θ'): stabilising step θ0 = F(θ') if no worse than θ1, else θ2
+      const bool take = res <= r1;
+      for (int i = tid; i < T; i += blockDim.x) {
+        if (take) th0[i] = th1[i] + log(sg[i] / E[i]);
+        slam[i] = exp(th0[i]);
+      }
+      phase = 0;
     }
     __syncthreads();
   }
   if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i < T; i += blockDim.x) {
-      p.lam_out[i] = slam[i];
-      p.g[i] = sg[i];
+    for (int i = tid; i < T; i += blockDim.x) {
+      p.lam_out[i] = out_lam[i];
+      p.g[i] = out_g[i];
     }
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       p.status[0] = it;
       p.status[1] = done ? 1 : 0;
+      p.status[2] = stalled ? 1 : 0;
+      p.status[3] = pass + 1;
       *p.res_out = res;
     }
   }
 }
 
-// Stand-alone single pass (ggm_grid_marginals / final NLL): partials into [Σk][grid].
+// Stand-alone single pass (ggm_grid_marginals): partials into [Σk][grid].
 template <int J>
 __global__ void __launch_bounds__(kThreads, 1) marginal_pass_kernel(GridDesc gd, const double* lam,
                                                                      double* partial) {
   extern __shared__ double dsm[];
   double* sg = dsm;
-  double* slam = sg + gd.total;
-  for (int i = threadIdx.x; i < gd.total; i += blockDim.x) sg[i] = 0.0;
-  load_lambda(lam, gd.total, slam, false);
+  double* slam = sg + gd.total + 1;
+  double* pw = slam + gd.total;
+  for (int i = threadIdx.x; i <= gd.total; i += blockDim.x) sg[i] = 0.0;
+  for (int i = threadIdx.x; i < gd.total; i += blockDim.x) slam[i] = lam[i];
+  for (int i = threadIdx.x; i < kWarps * fast_bins(gd); i += blockDim.x) pw[i] = 0.0;
   __syncthreads();
-  grid_pass<J>(gd, slam, sg, (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
-               (int64_t)gridDim.x * kWarps);
+  grid_pass<J, false>(gd, slam, sg, pw, (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
+                      (int64_t)gridDim.x * kWarps);
   __syncthreads();
   for (int i = threadIdx.x; i < gd.total; i += blockDim.x)
     partial[(size_t)i * gridDim.x + blockIdx.x] = sg[i];
@@ -321,8 +551,7 @@ __global__ void reduce_partials(const double* partial, int nblk, int total, doub
   if (e >= total) return;
   double sum = 0.0;
   for (int b = lane; b < nblk; b += 32) sum += partial[(size_t)e * nblk + b];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  sum = warp_sum(sum);
   if (lane == 0) g[e] = sum;
 }
 
@@ -340,28 +569,8 @@ __global__ void logsum_kernel(GridDesc gd, const double* lam, double* logsum) {
     }
     for (int m = lane; m < kin; m += 32) acc += log(base + lam[gd.off[gd.inner] + m]);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  acc = warp_sum(acc);
   if (lane == 0) atomicAdd(logsum, acc);
-}
-
-// Final: choose result buffer, canonical gauge, write λ out; compute grid_min, floor.
-__global__ void finalize_kernel(GridDesc gd, const double* lam_res, int gauge, double* lam_out,
-                                double* scalars /* [0]=smin */) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double mins[kMaxAxes];
-  double smin = 0.0;
-  for (int a = 0; a < gd.L; ++a) {
-    double m = lam_res[gd.off[a]];
-    for (int i = 1; i < gd.k[a]; ++i) m = fmin(m, lam_res[gd.off[a] + i]);
-    mins[a] = m;
-    smin += m;
-  }
-  for (int a = 0; a < gd.L; ++a) {
-    const double shift = gauge == 0 ? (-mins[a] + smin / gd.L) : 0.0;
-    for (int i = 0; i < gd.k[a]; ++i) lam_out[gd.off[a] + i] = lam_res[gd.off[a] + i] + shift;
-  }
-  scalars[0] = smin;
 }
 
 __global__ void check_E(const double* E, int total, int* bad) {
@@ -371,14 +580,10 @@ __global__ void check_E(const double* E, int total, int* bad) {
   }
 }
 
-__global__ void init_lambda(const double* E, int total, double* lam) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
-    lam[i] = 1.0 / E[i];  // Algorithm 1 line 5
-}
-
 static ggm_status make_desc(int L, const int* k, GridDesc* gd) {
   if (L < 1 || L > kMaxAxes) return fail(GGM_ERR_INVALID_ARGUMENT, "L=%d not in [1,%d]", L, kMaxAxes);
   if (!k) return fail(GGM_ERR_INVALID_ARGUMENT, "k is NULL");
+  memset(gd, 0, sizeof(*gd));
   gd->L = L;
   gd->off[0] = 0;
   int inner = 0;
@@ -425,19 +630,19 @@ static ggm_status make_desc_mod(int L, const int* ax, const int* kg, const int* 
   return GGM_OK;
 }
 
-static int pick_J(int kin) { return kin <= 128 ? 4 : kin <= 256 ? 8 : kin <= 512 ? 16 : 32; }
-
-static size_t pass_smem(const GridDesc& gd) {
-  return (size_t)gd.total * 2 * sizeof(double) + 16;
+// points per lane of the inner axis, rounded up to an instantiated size
+static int pick_J(int kin) {
+  const int j = (kin + 31) / 32;
+  static const int sizes[] = {1, 2, 4, 7, 10, 13, 16, 32};
+  for (int s : sizes)
+    if (j <= s) return s;
+  return 32;
 }
 
-template <int J>
-static cudaError_t set_attrs(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(solve_kernel<J>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(marginal_pass_kernel<J>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#define GGM_FOR_J(X) X(1) X(2) X(4) X(7) X(10) X(13) X(16) X(32)
+
+static size_t pass_smem(const GridDesc& gd) {
+  return ((size_t)gd.total * 2 + 1 + (size_t)kWarps * fast_bins(gd)) * sizeof(double) + 16;
 }
 
 static int grid_blocks(const GridDesc& gd) {
@@ -448,37 +653,359 @@ static int grid_blocks(const GridDesc& gd) {
 
 // Blocks for the cooperative solve: enough warps that each owns >= ~8 outer rows (a grid
 // barrier costs microseconds; small grids run in one block).
-static int solve_blocks(const GridDesc& gd, double extra_pts = 0.0) {
-  const double pts = (double)gd.rows * gd.k[gd.inner] + extra_pts;
+static int solve_blocks(double pts) {
   const int64_t want = (int64_t)std::ceil(pts / (kWarps * 8.0 * 32.0 * 16.0));
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, num_sms()));
+}
+
+template <int J>
+static cudaError_t launch_pass_j(const GridDesc& gd, const double* lam, double* partial, int nblk,
+                                 size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(marginal_pass_kernel<J>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  marginal_pass_kernel<J><<<nblk, kThreads, smem, s>>>(gd, lam, partial);
+  return cudaGetLastError();
 }
 
 static cudaError_t launch_pass(const GridDesc& gd, const double* lam, double* partial, int nblk,
                                cudaStream_t s) {
   const size_t smem = pass_smem(gd);
-  const int J = pick_J(gd.k[gd.inner]);
-  cudaError_t e;
-  switch (J) {
-    case 4: e = set_attrs<4>(smem); if (e) return e; marginal_pass_kernel<4><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
-    case 8: e = set_attrs<8>(smem); if (e) return e; marginal_pass_kernel<8><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
-    case 16: e = set_attrs<16>(smem); if (e) return e; marginal_pass_kernel<16><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
-    default: e = set_attrs<32>(smem); if (e) return e; marginal_pass_kernel<32><<<nblk, kThreads, smem, s>>>(gd, lam, partial); break;
+  switch (pick_J(gd.k[gd.inner])) {
+#define GGM_CASE(j) \
+  case j: return launch_pass_j<j>(gd, lam, partial, nblk, smem, s);
+    GGM_FOR_J(GGM_CASE)
+#undef GGM_CASE
   }
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
-template <int J>
-static cudaError_t launch_solve(const SolveParams& sp, int nblk, size_t smem, cudaStream_t s) {
-  cudaError_t e = set_attrs<J>(smem);
+template <int J, bool LOGS>
+static cudaError_t launch_solve_j(const SolveParams& sp, int nblk, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(solve_kernel<J, LOGS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<J>, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<J, LOGS>, kThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
   void* args[] = {const_cast<SolveParams*>(&sp)};
-  return cudaLaunchCooperativeKernel((void*)solve_kernel<J>, dim3(nblk), dim3(kThreads), args, smem,
-                                     s);
+  return cudaLaunchCooperativeKernel((void*)solve_kernel<J, LOGS>, dim3(nblk), dim3(kThreads), args,
+                                     smem, s);
+}
+
+static cudaError_t launch_solve(const SolveParams& sp, int J, int nblk, size_t smem,
+                                cudaStream_t s) {
+  const bool logs = sp.scheme == kSchemeGD;
+  switch (J) {
+#define GGM_CASE(j)                                                                   \
+  case j:                                                                             \
+    return logs ? launch_solve_j<j, true>(sp, nblk, smem, s)                          \
+                : launch_solve_j<j, false>(sp, nblk, smem, s);
+    GGM_FOR_J(GGM_CASE)
+#undef GGM_CASE
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ host-side gauge algebra
+// Axis space: one coordinate per axis.  The modalities' incidence rows span G^⊥ in axis
+// space; G_F (the gauge freedom with the axes outside `free_axes` pinned) is the null space
+// of the incidence rows plus the unit rows of the pinned axes.
+using Vec = std::vector<double>;
+
+static std::vector<Vec> null_basis(int nax, const std::vector<Vec>& rows) {
+  std::vector<Vec> R;  // orthonormalised rows
+  for (const Vec& r0 : rows) {
+    Vec v = r0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (const Vec& r : R) {
+        double d = 0.0;
+        for (int a = 0; a < nax; ++a) d += r[a] * v[a];
+        for (int a = 0; a < nax; ++a) v[a] -= d * r[a];
+      }
+    double nv = 0.0;
+    for (double x : v) nv += x * x;
+    if (nv > 1e-20) {
+      nv = std::sqrt(nv);
+      for (double& x : v) x /= nv;
+      R.push_back(v);
+    }
+  }
+  std::vector<Vec> N;
+  for (int e = 0; e < nax; ++e) {
+    Vec v(nax, 0.0);
+    v[e] = 1.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (const Vec& r : R) {
+        double d = 0.0;
+        for (int a = 0; a < nax; ++a) d += r[a] * v[a];
+        for (int a = 0; a < nax; ++a) v[a] -= d * r[a];
+      }
+      for (const Vec& r : N) {
+        double d = 0.0;
+        for (int a = 0; a < nax; ++a) d += r[a] * v[a];
+        for (int a = 0; a < nax; ++a) v[a] -= d * r[a];
+      }
+    }
+    double nv = 0.0;
+    for (double x : v) nv += x * x;
+    if (nv > 1e-12) {
+      nv = std::sqrt(nv);
+      for (double& x : v) x /= nv;
+      N.push_back(v);
+    }
+  }
+  return N;
+}
+
+struct ModelAxes {
+  int nax;
+  std::vector<int> k, off;             // per global axis
+  std::vector<std::vector<int>> mods;  // axes of each modality
+  std::vector<Vec> incidence() const {
+    std::vector<Vec> rows;
+    for (const auto& m : mods) {
+      Vec r(nax, 0.0);
+      for (int a : m) r[a] = 1.0;
+      rows.push_back(r);
+    }
+    return rows;
+  }
+  std::vector<Vec> gauge_free(const std::vector<int>& pinned) const {
+    std::vector<Vec> rows = incidence();
+    for (int a : pinned) {
+      Vec r(nax, 0.0);
+      r[a] = 1.0;
+      rows.push_back(r);
+    }
+    return null_basis(nax, rows);
+  }
+  // per-axis shifts c that remove from x (Σk coordinates, per-axis sums D) its component in
+  // the lift of span N (orthogonal projection in the Σk space: weights k_l in axis space)
+  Vec lifted_shift(const std::vector<Vec>& N, const Vec& D) const {
+    std::vector<Vec> U;  // k-weighted orthonormalisation of N
+    for (const Vec& n0 : N) {
+      Vec v = n0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (const Vec& u : U) {
+          double d = 0.0;
+          for (int a = 0; a < nax; ++a) d += k[a] * u[a] * v[a];
+          for (int a = 0; a < nax; ++a) v[a] -= d * u[a];
+        }
+      double nv = 0.0;
+      for (int a = 0; a < nax; ++a) nv += k[a] * v[a] * v[a];
+      if (nv > 1e-20) {
+        nv = std::sqrt(nv);
+        for (double& x : v) x /= nv;
+        U.push_back(v);
+      }
+    }
+    Vec c(nax, 0.0);
+    for (const Vec& u : U) {
+      double d = 0.0;
+      for (int a = 0; a < nax; ++a) d += u[a] * D[a];
+      for (int a = 0; a < nax; ++a) c[a] += d * u[a];
+    }
+    return c;
+  }
+};
+
+// Reading T: relative gauge component of the per-axis traces (single modality: max |tr_l −
+// mean| / mean; several: |P_G tr|_max / mean tr).
+static double trace_inconsistency(const ModelAxes& ax, const Vec& hE) {
+  Vec tr(ax.nax, 0.0);
+  double mean = 0.0;
+  for (int a = 0; a < ax.nax; ++a) {
+    for (int i = ax.off[a]; i < ax.off[a + 1]; ++i) tr[a] += hE[i];
+    mean += tr[a] / ax.nax;
+  }
+  if (!(mean > 0.0)) return 0.0;
+  const std::vector<Vec> N = ax.gauge_free({});
+  double ti = 0.0;
+  for (int a = 0; a < ax.nax; ++a) {
+    double pa = 0.0;
+    for (const Vec& n : N) {
+      double d = 0.0;
+      for (int b = 0; b < ax.nax; ++b) d += n[b] * tr[b];
+      pa += d * n[a];
+    }
+    ti = std::max(ti, std::fabs(pa));
+  }
+  return ti / mean;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Common driver of ggm_solve_eigvals / ggm_solve_eigvals_multi.
+static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double* E,
+                               const ggm_solve_opts& o, double* lambda, ggm_solve_info* info,
+                               cudaStream_t s) {
+  const int T = sp.T;
+  if (!(o.tol > 0.0) || o.max_iter < 0 || !(o.eps_scale >= 0.0) || !(o.trace_tol >= 0.0))
+    return fail(GGM_ERR_INVALID_ARGUMENT, "invalid solve options");
+  if (o.method < 0 || o.method > 2) return fail(GGM_ERR_INVALID_ARGUMENT, "method=%d", o.method);
+  if (o.gauge != 0 && o.gauge != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "gauge=%d", o.gauge);
+  // scratch: lam_res, g, Eu, gacc[3][T+1], scalars, status
+  const size_t bytes = sizeof(double) * (3 * (size_t)T + 3 * ((size_t)T + 1) + 8) + 64;
+  DevBuf buf;
+  GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
+  double* lam_res = static_cast<double*>(buf.p);
+  double* g = lam_res + T;
+  double* Eu = g + T;
+  double* gacc = Eu + T;
+  double* scal = gacc + 3 * ((size_t)T + 1);  // [1] logsum, [2] residual
+  int* istat = reinterpret_cast<int*>(scal + 4);  // [0] it, [1] converged, [2] stalled, [3] passes, [6] bad
+  GGM_CUDA_TRY(cudaMemsetAsync(gacc, 0, sizeof(double) * (3 * ((size_t)T + 1) + 8) + 64, s));
+  check_E<<<4, 256, 0, s>>>(E, T, istat + 6);
+  GGM_CUDA_TRY(cudaGetLastError());
+  int hbad = 0;
+  Vec hE(T);
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hbad, istat + 6, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(hE.data(), E, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hbad) return fail(GGM_ERR_DOMAIN, "E must be finite and > 0 (Thm 4, P:742)");
+
+  // reading T: interior (projected spectrum) or barrier regime
+  double emin_inv = 0.0;
+  for (int i = 0; i < T; ++i) emin_inv = std::max(emin_inv, 1.0 / hE[i]);
+  const double eps = o.eps_scale * emin_inv;
+  const double ti = trace_inconsistency(ax, hE);
+  const bool barrier = o.method != 2 && ti > o.trace_tol;
+  Vec hEu = hE;
+  if (!barrier && o.method != 2) {  // E_eff = P_{G⊥} E
+    Vec tr(ax.nax, 0.0);
+    for (int a = 0; a < ax.nax; ++a)
+      for (int i = ax.off[a]; i < ax.off[a + 1]; ++i) tr[a] += hE[i];
+    const Vec c = ax.lifted_shift(ax.gauge_free({}), tr);
+    for (int a = 0; a < ax.nax; ++a)
+      for (int i = ax.off[a]; i < ax.off[a + 1]; ++i) hEu[i] -= c[a];
+    for (int i = 0; i < T; ++i)
+      if (!(hEu[i] > 0.0)) return fail(GGM_ERR_DOMAIN, "projected spectrum not positive");
+  }
+  GGM_CUDA_TRY(cudaMemcpyAsync(Eu, hEu.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
+
+  int J = 1, kfmax = 0;
+  double pts = 0.0;
+  for (int m = 0; m < sp.M; ++m) {
+    J = std::max(J, pick_J(sp.gd[m].k[sp.gd[m].inner]));
+    kfmax = std::max(kfmax, fast_bins(sp.gd[m]));
+    pts += (double)sp.gd[m].rows * sp.gd[m].k[sp.gd[m].inner];
+  }
+  // shared memory: sg[T+1], slam[T], th0[T], th1[T], private bins; if that does not fit,
+  // the plain MM step with sg and slam only and the generic pass
+  const size_t smem_full = ((size_t)4 * T + 1 + (size_t)kWarps * kfmax) * sizeof(double) + 16;
+  const bool fits = smem_full <= 200 * 1024;
+  sp.pw_stride = fits ? kWarps * kfmax : 0;
+  const size_t smem_launch = fits ? smem_full : ((size_t)2 * T + 1) * sizeof(double) + 16;
+  if (!fits && o.method == 2)
+    return fail(GGM_ERR_UNSUPPORTED, "method 2: sum(k)=%d too large for the solve kernel", T);
+  sp.E = o.method == 2 ? E : Eu;
+  sp.floor = barrier ? eps : 0.0;
+  sp.gd_eps = eps;
+  sp.scheme = o.method == 2 ? kSchemeGD : (o.method == 1 || barrier || !fits) ? kSchemeMM : kSchemeSquarem;
+  sp.lam_out = lam_res;
+  sp.g = g;
+  sp.gacc = gacc;
+  sp.status = istat;
+  sp.res_out = scal + 2;
+  sp.tol = o.tol;
+  sp.max_iter = o.max_iter;
+  if (smem_launch > 227 * 1024)
+    return fail(GGM_ERR_UNSUPPORTED, "sum(k)=%d too large for the solve kernel", T);
+  const int nblk = solve_blocks(pts);
+  cudaError_t ce = launch_solve(sp, J, nblk, smem_launch, s);
+  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+  int hstat[4] = {0, 0, 0, 0};
+  GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  int extra = 0;
+  if (!hstat[1] && sp.scheme == kSchemeSquarem) {  // accelerated run failed: plain MM
+    extra = hstat[0];
+    sp.scheme = kSchemeMM;
+    ce = launch_solve(sp, J, nblk, smem_launch, s);
+    if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
+    GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
+  }
+  // Σ log s of the result (grid invariant: gauge shifts do not change it)
+  for (int m = 0; m < sp.M; ++m) logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(sp.gd[m], lam_res, scal + 1);
+  GGM_CUDA_TRY(cudaGetLastError());
+  Vec hL(T);
+  double hscal[3] = {0, 0, 0};
+  GGM_CUDA_TRY(cudaMemcpyAsync(hL.data(), lam_res, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+
+  // gauge (reading G / G2), among the axes with no coordinate on the floor
+  std::vector<int> pinned;
+  int nfloor = 0;
+  for (int a = 0; a < ax.nax; ++a) {
+    bool on = false;
+    for (int i = ax.off[a]; i < ax.off[a + 1]; ++i)
+      if (barrier && hL[i] <= eps * (1.0 + 1e-9)) {
+        on = true;
+        ++nfloor;
+      }
+    if (on) pinned.push_back(a);
+  }
+  const std::vector<Vec> N = ax.gauge_free(pinned);
+  Vec shift(ax.nax, 0.0);
+  if (!N.empty()) {
+    if (o.gauge == 0) {  // λ_l − (P_{G_F} μ)_l, μ_l = min λ_l
+      Vec mu(ax.nax);
+      for (int a = 0; a < ax.nax; ++a) {
+        double mn = hL[ax.off[a]];
+        for (int i = ax.off[a]; i < ax.off[a + 1]; ++i) mn = std::min(mn, hL[i]);
+        mu[a] = mn;
+      }
+      for (const Vec& n : N) {
+        double d = 0.0;
+        for (int a = 0; a < ax.nax; ++a) d += n[a] * mu[a];
+        for (int a = 0; a < ax.nax; ++a) shift[a] += d * n[a];
+      }
+    } else {  // (λ − 1/E) ⊥ lift(G_F)
+      Vec D(ax.nax, 0.0);
+      for (int a = 0; a < ax.nax; ++a)
+        for (int i = ax.off[a]; i < ax.off[a + 1]; ++i) D[a] += hL[i] - 1.0 / hE[i];
+      shift = ax.lifted_shift(N, D);
+    }
+  }
+  Vec out(T);
+  for (int a = 0; a < ax.nax; ++a)
+    for (int i = ax.off[a]; i < ax.off[a + 1]; ++i) out[i] = hL[i] - shift[a];
+  GGM_CUDA_TRY(cudaMemcpyAsync(lambda, out.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (info) {
+    double lin = 0.0;
+    for (int i = 0; i < T; ++i) lin += hE[i] * out[i];
+    double gmin = INFINITY;
+    for (const auto& m : ax.mods) {
+      double sm = 0.0;
+      for (int a : m) {
+        double mn = out[ax.off[a]];
+        for (int i = ax.off[a]; i < ax.off[a + 1]; ++i) mn = std::min(mn, out[i]);
+        sm += mn;
+      }
+      gmin = std::min(gmin, sm);
+    }
+    info->iterations = hstat[0] + extra;
+    info->stationarity = hscal[2];
+    info->nll = 0.5 * lin - 0.5 * hscal[1];
+    info->grid_min = gmin;
+    info->floor_active = nfloor > 0 ? 1 : 0;
+    info->trace_inconsistency = ti;
+  }
+  GGM_CUDA_TRY(cudaFreeAsync(buf.p, s));
+  buf.p = nullptr;
+  if (!hstat[1])
+    return fail(GGM_ERR_NO_CONVERGENCE, "no convergence in %d iterations (residual %.3e)%s",
+                o.max_iter, hscal[2], hstat[2] ? " (step size underflow)" : "");
+  return GGM_OK;
 }
 
 }  // namespace gs
@@ -494,14 +1021,8 @@ extern "C" void ggm_solve_opts_default(ggm_solve_opts* o) {
   o->eps_scale = 1e-10;
   o->method = 0;
   o->gauge = 0;
+  o->trace_tol = 1e-8;
 }
-
-struct DevBuf {
-  void* p = nullptr;
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-};
 
 extern "C" ggm_status ggm_grid_marginals(int L, const int* k, const double* lambda, double* g,
                                          double* logsum_out, void* stream) {
@@ -530,37 +1051,6 @@ extern "C" ggm_status ggm_grid_marginals(int L, const int* k, const double* lamb
   return GGM_OK;
 }
 
-// The solve kernel with update exponent sp.omega; an over-relaxed run (omega > 1) that does
-// not converge is repeated with the plain MM step (omega = 1, monotone NLL), and its
-// iterations are returned in *extra.
-static ggm_status solve_with_fallback(SolveParams sp, int J, int nblk, size_t smem,
-                                      cudaStream_t s, const int* istat, int* extra) {
-  auto launch = [&]() -> cudaError_t {
-    switch (J) {
-      case 4: return launch_solve<4>(sp, nblk, smem, s);
-      case 8: return launch_solve<8>(sp, nblk, smem, s);
-      case 16: return launch_solve<16>(sp, nblk, smem, s);
-      default: return launch_solve<32>(sp, nblk, smem, s);
-    }
-  };
-  *extra = 0;
-  cudaError_t ce = launch();
-  if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
-  if (sp.omega != 1.0) {
-    int h[2] = {0, 0};
-    GGM_CUDA_TRY(cudaMemcpyAsync(h, istat, sizeof(h), cudaMemcpyDeviceToHost, s));
-    GGM_CUDA_TRY(cudaStreamSynchronize(s));
-    if (!h[1]) {
-      *extra = h[0];
-      sp.omega = 1.0;
-      ce = launch();
-      if (ce != cudaSuccess)
-        return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
-    }
-  }
-  return GGM_OK;
-}
-
 extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
                                         const ggm_solve_opts* opts, double* lambda,
                                         ggm_solve_info* info, void* stream) {
@@ -571,90 +1061,19 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
   ggm_solve_opts o;
   ggm_solve_opts_default(&o);
   if (opts) o = *opts;
-  if (!(o.tol > 0.0) || o.max_iter < 0 || !(o.eps_scale >= 0.0))
-    return fail(GGM_ERR_INVALID_ARGUMENT, "invalid solve options");
-  if (o.method != 0)
-    return fail(GGM_ERR_UNSUPPORTED, "method %d not implemented on the GPU (use 0)", o.method);
-  if (o.gauge != 0 && o.gauge != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "gauge=%d", o.gauge);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int nblk = solve_blocks(gd);
-  const size_t T = gd.total;
-  // scratch: lam_res, g, gacc[3T], scalars[4] (smin, logsum, res), status[4]
-  const size_t bytes = sizeof(double) * (5 * T + 8) + 64;
-  DevBuf buf;
-  GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
-  double* lam_res = static_cast<double*>(buf.p);
-  double* g = lam_res + T;
-  double* gacc = g + T;
-  double* scal = gacc + 3 * T;  // [0] smin, [1] logsum, [2] residual
-  int* istat = reinterpret_cast<int*>(scal + 4);  // [0] iterations, [1] converged, [3] bad
-  GGM_CUDA_TRY(cudaMemsetAsync(gacc, 0, sizeof(double) * (3 * T + 8) + 64, s));
-  check_E<<<4, 256, 0, s>>>(E, gd.total, istat + 3);
-  GGM_CUDA_TRY(cudaGetLastError());
-  int hbad = 0;
-  GGM_CUDA_TRY(cudaMemcpyAsync(&hbad, istat + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  if (hbad) return fail(GGM_ERR_DOMAIN, "E must be finite and > 0 (Thm 4, P:742)");
-
   SolveParams sp;
+  memset(&sp, 0, sizeof(sp));
   sp.gd[0] = gd;
   sp.M = 1;
   sp.T = gd.total;
-  sp.E = E;
-  sp.lam_out = lam_res;
-  sp.g = g;
-  sp.gacc = gacc;
-  sp.status = istat;
-  sp.res_out = scal + 2;
-  sp.tol = o.tol;
-  sp.max_iter = o.max_iter;
-  sp.omega = mm_omega();
-  const size_t smem = pass_smem(gd);
-  int extra_it = 0;
-  ggm_status sst = solve_with_fallback(sp, pick_J(gd.k[gd.inner]), nblk, smem, s, istat, &extra_it);
-  if (sst != GGM_OK) return sst;
-  int hstat[2] = {0, 0};
-  GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
-  finalize_kernel<<<1, 32, 0, s>>>(gd, lam_res, o.gauge, lambda, scal);
-  logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(gd, lam_res, scal + 1);
-  GGM_CUDA_TRY(cudaGetLastError());
-  // residual of the returned λ (its marginals are in g)
-  double hres = 0.0;
-  {
-    double hscal[3];
-    GGM_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, s));
-    GGM_CUDA_TRY(cudaStreamSynchronize(s));
-    hres = hscal[2];
-    if (info) {
-      std::vector<double> hE(T), hL(T);
-      GGM_CUDA_TRY(cudaMemcpy(hE.data(), E, T * sizeof(double), cudaMemcpyDeviceToHost));
-      GGM_CUDA_TRY(cudaMemcpy(hL.data(), lam_res, T * sizeof(double), cudaMemcpyDeviceToHost));
-      double lin = 0.0;
-      for (size_t i = 0; i < T; ++i) lin += hE[i] * hL[i];
-      std::vector<double> tr(L, 0.0);
-      double mean = 0.0;
-      for (int a = 0; a < L; ++a) {
-        for (int i = gd.off[a]; i < gd.off[a + 1]; ++i) tr[a] += hE[i];
-        mean += tr[a] / L;
-      }
-      double ti = 0.0;
-      for (int a = 0; a < L; ++a) ti = std::max(ti, std::fabs(tr[a] - mean));
-      info->iterations = hstat[0] + extra_it;
-      info->stationarity = hres;
-      info->nll = 0.5 * lin - 0.5 * hscal[1];
-      info->grid_min = hscal[0];
-      double emax = 0.0;
-      for (size_t i = 0; i < T; ++i) emax = std::max(emax, 1.0 / hE[i]);
-      info->floor_active = hscal[0] <= o.eps_scale * emax ? 1 : 0;
-      info->trace_inconsistency = mean > 0 ? ti / mean : 0.0;
-    }
-  }
-  GGM_CUDA_TRY(cudaFreeAsync(buf.p, s));
-  buf.p = nullptr;
-  if (!hstat[1])
-    return fail(GGM_ERR_NO_CONVERGENCE, "no convergence in %d iterations (residual %.3e)",
-                o.max_iter, hres);
-  return GGM_OK;
+  ModelAxes ax;
+  ax.nax = L;
+  ax.k.assign(k, k + L);
+  ax.off.assign(gd.off, gd.off + L + 1);
+  std::vector<int> all(L);
+  for (int a = 0; a < L; ++a) all[a] = a;
+  ax.mods.push_back(all);
+  return solve_common(sp, ax, E, o, lambda, info, static_cast<cudaStream_t>(stream));
 }
 
 // ------------------------------------------------------------------ multi-modal solve
@@ -662,8 +1081,7 @@ extern "C" ggm_status ggm_solve_eigvals(int L, const int* k, const double* E,
 // ½(E_l − Σ_{γ∋l} g^γ_l).  The majorise-minimise step is unchanged (one Jensen majoriser
 // per modality, summed): λ ← λ ⊙ (Σ_γ g^γ) / E, so the same persistent kernel runs with one
 // grid pass per modality per iteration.  Gauge (reading G2): shifts c with Σ_{l∈γ} c_l = 0
-// for every γ leave all grid sums unchanged; gauge 0 subtracts the G-component of the axis
-// minima (for one modality: the min-balanced gauge of ggm_solve_eigvals).
+// for every γ leave all grid sums unchanged; reading T with that gauge space.
 extern "C" ggm_status ggm_solve_eigvals_multi(int A, const int* k, const double* E, int M,
                                               const int* mod_ptr, const int* mod_axes,
                                               const ggm_solve_opts* opts, double* lambda,
@@ -679,145 +1097,29 @@ extern "C" ggm_status ggm_solve_eigvals_multi(int A, const int* k, const double*
   const int T = offg[A];
   SolveParams sp;
   memset(&sp, 0, sizeof(sp));
-  double pts = 0.0;
-  int J = 4;
+  ModelAxes ax;
+  ax.nax = A;
+  ax.k.assign(k, k + A);
+  ax.off = offg;
   for (int g = 0; g < M; ++g) {
     const int L = mod_ptr[g + 1] - mod_ptr[g];
-    const int* ax = mod_axes + mod_ptr[g];
+    const int* axl = mod_axes + mod_ptr[g];
     std::vector<int> here(A, 0);
     for (int a = 0; a < L; ++a) {
-      if (ax[a] < 0 || ax[a] >= A) return fail(GGM_ERR_INVALID_ARGUMENT, "axis id out of range");
-      if (here[ax[a]]++) return fail(GGM_ERR_INVALID_ARGUMENT, "repeated axis in a modality (P:181)");
-      seen[ax[a]] = 1;
+      if (axl[a] < 0 || axl[a] >= A) return fail(GGM_ERR_INVALID_ARGUMENT, "axis id out of range");
+      if (here[axl[a]]++) return fail(GGM_ERR_INVALID_ARGUMENT, "repeated axis in a modality (P:181)");
+      seen[axl[a]] = 1;
     }
-    ggm_status st = make_desc_mod(L, ax, k, offg.data(), T, &sp.gd[g]);
+    ggm_status st = make_desc_mod(L, axl, k, offg.data(), T, &sp.gd[g]);
     if (st != GGM_OK) return st;
-    pts += (double)sp.gd[g].rows * sp.gd[g].k[sp.gd[g].inner];
-    J = std::max(J, pick_J(sp.gd[g].k[sp.gd[g].inner]));
+    ax.mods.push_back(std::vector<int>(axl, axl + L));
   }
   for (int a = 0; a < A; ++a)
     if (!seen[a]) return fail(GGM_ERR_INVALID_ARGUMENT, "axis %d occurs in no modality", a);
   ggm_solve_opts o;
   ggm_solve_opts_default(&o);
   if (opts) o = *opts;
-  if (!(o.tol > 0.0) || o.max_iter < 0 || !(o.eps_scale >= 0.0))
-    return fail(GGM_ERR_INVALID_ARGUMENT, "invalid solve options");
-  if (o.method != 0)
-    return fail(GGM_ERR_UNSUPPORTED, "method %d not implemented on the GPU (use 0)", o.method);
-  if (o.gauge != 0 && o.gauge != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "gauge=%d", o.gauge);
   sp.M = M;
   sp.T = T;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const size_t bytes = sizeof(double) * (5 * (size_t)T + 8) + 64;
-  DevBuf buf;
-  GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
-  double* lam_res = static_cast<double*>(buf.p);
-  double* g = lam_res + T;
-  double* gacc = g + T;
-  double* scal = gacc + 3 * (size_t)T;  // [1] logsum, [2] residual
-  int* istat = reinterpret_cast<int*>(scal + 4);
-  GGM_CUDA_TRY(cudaMemsetAsync(gacc, 0, sizeof(double) * (3 * (size_t)T + 8) + 64, s));
-  check_E<<<4, 256, 0, s>>>(E, T, istat + 3);
-  GGM_CUDA_TRY(cudaGetLastError());
-  int hbad = 0;
-  GGM_CUDA_TRY(cudaMemcpyAsync(&hbad, istat + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  if (hbad) return fail(GGM_ERR_DOMAIN, "E must be finite and > 0 (Thm 4, P:742)");
-  sp.E = E;
-  sp.lam_out = lam_res;
-  sp.g = g;
-  sp.gacc = gacc;
-  sp.status = istat;
-  sp.res_out = scal + 2;
-  sp.tol = o.tol;
-  sp.max_iter = o.max_iter;
-  sp.omega = mm_omega();
-  const int nblk = solve_blocks(sp.gd[0], pts - (double)sp.gd[0].rows * sp.gd[0].k[sp.gd[0].inner]);
-  const size_t smem = (size_t)T * 2 * sizeof(double) + 16;
-  int extra_it = 0;
-  ggm_status sst = solve_with_fallback(sp, J, nblk, smem, s, istat, &extra_it);
-  if (sst != GGM_OK) return sst;
-  for (int m = 0; m < M; ++m) logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(sp.gd[m], lam_res, scal + 1);
-  GGM_CUDA_TRY(cudaGetLastError());
-  int hstat[2] = {0, 0};
-  double hscal[3] = {0, 0, 0};
-  std::vector<double> hL(T), hE(T);
-  GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaMemcpyAsync(hL.data(), lam_res, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaMemcpyAsync(hE.data(), E, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  // gauge space G = null(incidence): orthonormal basis R of the row space by Gram-Schmidt;
-  // P_G x = x - Σ_r (r·x) r
-  std::vector<std::vector<double>> R;
-  for (int gm = 0; gm < M; ++gm) {
-    std::vector<double> v(A, 0.0);
-    for (int q = mod_ptr[gm]; q < mod_ptr[gm + 1]; ++q) v[mod_axes[q]] = 1.0;
-    for (int pass = 0; pass < 2; ++pass)
-      for (const auto& r : R) {
-        double dt = 0.0;
-        for (int a = 0; a < A; ++a) dt += r[a] * v[a];
-        for (int a = 0; a < A; ++a) v[a] -= dt * r[a];
-      }
-    double nv = 0.0;
-    for (double x : v) nv += x * x;
-    if (nv > 1e-20) {
-      nv = std::sqrt(nv);
-      for (double& x : v) x /= nv;
-      R.push_back(v);
-    }
-  }
-  auto proj_G = [&](const std::vector<double>& x) {
-    std::vector<double> y = x;
-    for (const auto& r : R) {
-      double dt = 0.0;
-      for (int a = 0; a < A; ++a) dt += r[a] * x[a];
-      for (int a = 0; a < A; ++a) y[a] -= dt * r[a];
-    }
-    return y;
-  };
-  std::vector<double> mins(A), tr(A, 0.0);
-  for (int a = 0; a < A; ++a) {
-    double mn = hL[offg[a]];
-    for (int i = offg[a]; i < offg[a + 1]; ++i) {
-      mn = std::min(mn, hL[i]);
-      tr[a] += hE[i];
-    }
-    mins[a] = mn;
-  }
-  const std::vector<double> shift = o.gauge == 0 ? proj_G(mins) : std::vector<double>(A, 0.0);
-  std::vector<double> out(T);
-  for (int a = 0; a < A; ++a)
-    for (int i = offg[a]; i < offg[a + 1]; ++i) out[i] = hL[i] - shift[a];
-  GGM_CUDA_TRY(cudaMemcpyAsync(lambda, out.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
-  GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  if (info) {
-    double lin = 0.0, emax = 0.0;
-    for (int i = 0; i < T; ++i) {
-      lin += hE[i] * hL[i];
-      emax = std::max(emax, 1.0 / hE[i]);
-    }
-    double gmin = INFINITY;
-    for (int gm = 0; gm < M; ++gm) {
-      double sm = 0.0;
-      for (int q = mod_ptr[gm]; q < mod_ptr[gm + 1]; ++q) sm += mins[mod_axes[q]];
-      gmin = std::min(gmin, sm);
-    }
-    const std::vector<double> ptr = proj_G(tr);
-    double trmean = 0.0, ti = 0.0;
-    for (int a = 0; a < A; ++a) trmean += tr[a] / A;
-    for (int a = 0; a < A; ++a) ti = std::max(ti, std::fabs(ptr[a]));
-    info->iterations = hstat[0] + extra_it;
-    info->stationarity = hscal[2];
-    info->nll = 0.5 * lin - 0.5 * hscal[1];
-    info->grid_min = gmin;
-    info->floor_active = gmin <= o.eps_scale * emax ? 1 : 0;
-    info->trace_inconsistency = trmean > 0 ? ti / trmean : 0.0;
-  }
-  GGM_CUDA_TRY(cudaFreeAsync(buf.p, s));
-  buf.p = nullptr;
-  if (!hstat[1])
-    return fail(GGM_ERR_NO_CONVERGENCE, "no convergence in %d iterations (residual %.3e)",
-                o.max_iter, hscal[2]);
-  return GGM_OK;
+  return solve_common(sp, ax, E, o, lambda, info, static_cast<cudaStream_t>(stream));
 }

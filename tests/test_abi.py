@@ -87,7 +87,7 @@ def test_solve_and_gram_validation(G):
     assert L.ggm_gram_eig_workspace(2, shape, 2, 1, C.byref(nb)) == 1      # bad axis
     o = G._ggm.SolveOpts()
     L.ggm_solve_opts_default(C.byref(o))
-    assert o.tol == 1e-7 and o.max_iter == 20000 and o.gauge == 0
+    assert o.tol == 1e-7 and o.max_iter == 20000 and o.gauge == 0 and o.trace_tol == 1e-8
 
 
 def test_product_path_has_no_oracle_import():

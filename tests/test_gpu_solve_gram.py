@@ -167,23 +167,112 @@ def test_gram_eig_axes_rank_error(G):
     assert e.value.status_name == "GGM_ERR_RANK"
 
 
-def test_solve_overrelaxation_fallback(G, monkeypatch):
-    """An over-relaxed run that does not converge within max_iter is repeated with the plain
-    MM step (BK4): same fixed point, iterations = both runs."""
+def test_solve_methods_same_grid(G):
+    """Method 0 (SQUAREM-accelerated majorise-minimise) and method 1 (the plain MM step)
+    reach the same grid at C2 (BK4), method 0 in fewer passes; a method-0 run that
+    cannot converge within max_iter reports GGM_ERR_NO_CONVERGENCE."""
     cfg = gen.config("C2")
     X = torch.from_numpy(cfg["X"]).cuda()
     Ec = torch.cat([G.ggm_gram_eig(X, a, k)[1] for a, k in enumerate(cfg["k"])])
-    monkeypatch.setenv("GGM_MM_OMEGA", "1")
-    lam1, info1 = G.ggm_solve_eigvals(Ec, cfg["k"], max_iter=200)
-    monkeypatch.setenv("GGM_MM_OMEGA", "1.99")   # oscillates: no convergence in 30 iterations
-    lam2, info2 = G.ggm_solve_eigvals(Ec, cfg["k"], max_iter=30)
-    assert info2["iterations"] == 30 + info1["iterations"]
-    # the rerun is the plain MM run (cross-block fp64 atomics: summation order varies)
-    np.testing.assert_allclose(lam2.cpu().numpy(), lam1.cpu().numpy(), rtol=1e-10)
-    monkeypatch.delenv("GGM_MM_OMEGA")
-    lam3, info3 = G.ggm_solve_eigvals(Ec, cfg["k"])
-    s = [O.grid_sums(_split(l.cpu().numpy(), cfg["k"])) for l in (lam1, lam3)]
+    lam1, info1 = G.ggm_solve_eigvals(Ec, cfg["k"], method=1)
+    lam0, info0 = G.ggm_solve_eigvals(Ec, cfg["k"], method=0)
+    assert info0["iterations"] < info1["iterations"]
+    s = [O.grid_sums(_split(l.cpu().numpy(), cfg["k"])) for l in (lam1, lam0)]
     np.testing.assert_allclose(s[1], s[0], rtol=1e-5)
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_solve_eigvals(Ec, cfg["k"], max_iter=3)
+    assert e.value.status == 4
+
+
+def _truncated(seed, shape=(9, 7, 6), ks=(4, 3, 5)):
+    x = gen.small_tensor(seed, shape)
+    return [O.gram_eig(x, l, k)[1] for l, k in enumerate(ks)], list(ks)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("gauge", [0, 1])
+def test_solve_barrier_truncated_tensor(G, seed, gauge):
+    """Reading T: a truncated 3-axis tensor (unequal traces) has its MLE on the barrier
+    λ >= ε (Lemma 6).  GPU λ and floor set equal the oracle's active-set
+    Newton; floor_active on both sides."""
+    Es, ks = _truncated(seed)
+    lo, oinfo = O.solve_eigvals(Es, gauge=gauge)
+    assert oinfo["floor_active"]
+    lam, info = G.ggm_solve_eigvals(_cat(Es), ks, gauge=gauge, tol=1e-9)
+    lg = _split(lam.cpu().numpy(), ks)
+    assert info["floor_active"] == 1
+    eps = oinfo["eps"]
+    for a, b in zip(lg, lo):
+        on_o = b <= eps * (1 + 1e-9)
+        on_g = a <= eps * (1 + 1e-9)
+        assert np.array_equal(on_o, on_g)
+        np.testing.assert_allclose(a, b, rtol=EIG_REL, atol=1e-3 * eps)
+    np.testing.assert_allclose(O.grid_sums(lg), O.grid_sums(lo), rtol=EIG_REL)
+    assert O.kkt_residual(Es, lg, eps * (1 + 1e-9)) <= 1e-6
+
+
+def test_solve_barrier_matrix_unequal_ranks(G):
+    """A matrix with k0 != k1: barrier regime on both sides, same λ."""
+    x = gen.small_tensor(41, (30, 20))
+    Es = [O.gram_eig(x, 0, 12)[1], O.gram_eig(x, 1, 6)[1]]
+    lo, oinfo = O.solve_eigvals(Es)
+    lam, info = G.ggm_solve_eigvals(_cat(Es), (12, 6), tol=1e-9)
+    lg = _split(lam.cpu().numpy(), (12, 6))
+    assert info["floor_active"] == 1 and oinfo["floor_active"]
+    for a, b in zip(lg, lo):
+        np.testing.assert_allclose(a, b, rtol=EIG_REL, atol=1e-3 * oinfo["eps"])
+
+
+@pytest.mark.parametrize("shape", [(20, 10), (6, 5, 4), (12, 9, 7)])
+def test_solve_gauge1_matches_oracle(G, shape):
+    """Gauge 1 = Algorithm 1's gauge, (λ − 1/E) ⊥ G (L >= 2), against the oracle's gauge 1."""
+    x = gen.small_tensor(sum(shape) + 5, shape)
+    ks = [min(d, int(np.prod(shape)) // d) for d in shape]
+    Es = [O.gram_eig(x, l, k)[1] for l, k in enumerate(ks)]
+    lo, _ = O.solve_eigvals(Es, tol=1e-13, gauge=1)
+    lam, info = G.ggm_solve_eigvals(_cat(Es), ks, gauge=1, tol=1e-9)
+    lg = _split(lam.cpu().numpy(), ks)
+    for a, b in zip(lg, lo):
+        np.testing.assert_allclose(a, b, rtol=EIG_REL, atol=EIG_REL * max(np.abs(b).max(), 1e-30))
+    d = [float(np.sum(l - 1.0 / e)) for l, e in zip(lg, Es)]
+    np.testing.assert_allclose(d, d[0], rtol=1e-6, atol=1e-9 * max(abs(v) for v in d))
+    assert info["floor_active"] == 0
+
+
+def test_solve_method2_algorithm1_matches_oracle(G):
+    """Method 2 = Algorithm 1 as printed (readings Q1-Q3) vs oracle.paper_gd_solve: the same
+    deterministic iteration (μ halving on infeasible / non-decreasing steps) reaches the same λ
+    (gauge 1 is what gradient descent preserves)."""
+    rng = np.random.default_rng(4)
+    Es = [rng.uniform(1.0, 2.0, 3), rng.uniform(1.0, 2.0, 2)]
+    Es[1] *= Es[0].sum() / Es[1].sum()
+    lo, oi = O.paper_gd_solve(Es, tol=1e-8)
+    lam, info = G.ggm_solve_eigvals(_cat(Es), (3, 2), method=2, gauge=1, tol=1e-8)
+    lg = _split(lam.cpu().numpy(), (3, 2))
+    for a, b in zip(lg, lo):
+        np.testing.assert_allclose(a, b, rtol=1e-6)
+    assert abs(info["iterations"] - oi["iterations"]) <= 2
+    assert info["stationarity"] <= 1e-8
+
+
+def test_solve_method2_trace_inconsistent_does_not_converge(G):
+    """Algorithm 1 as printed bounds only the grid minimum (reading Q3), so with unequal
+    traces the NLL decreases without bound along the gauge: no convergence (the barrier MLE
+    needs method 0/1)."""
+    Es, ks = _truncated(2)
+    with pytest.raises(G.GGMError) as e:
+        G.ggm_solve_eigvals(_cat(Es), ks, method=2, max_iter=2000)
+    assert e.value.status == 4
+
+
+def test_solve_multi_barrier(G):
+    """Reading T with the multi-modal gauge space: one modality through the multi-modal entry
+    equals the single-modality barrier solve."""
+    Es, ks = _truncated(3)
+    lam1, _ = G.ggm_solve_eigvals(_cat(Es), ks, tol=1e-9)
+    lam2, info = G.ggm_solve_eigvals_multi(_cat(Es), ks, [[0, 1, 2]], tol=1e-9)
+    assert info["floor_active"] == 1
+    np.testing.assert_allclose(lam2.cpu().numpy(), lam1.cpu().numpy(), rtol=1e-7)
 
 
 def test_gram_eig_axes_with_rsi_axis(G):
