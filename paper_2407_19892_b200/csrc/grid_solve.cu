@@ -93,99 +93,107 @@ __device__ __forceinline__ double reduce4(const double (&p)[4], int lane) {
 // every L <= 3, i.e. every BASELINE config).  slam: λ (Σk, fp64, shared); sg: this block's
 // marginal partials (Σk [+1: Σ log s when LOGS], shared, zeroed by the caller); pw: kWarps x
 // k_fast private bins (shared, zero on entry, zero again on exit).
+// A warp's rows are cut into segments of constant slow index (at most k_fast rows, the fast
+// index running fi, fi+1, ... without wrap) and each segment into groups of four rows that
+// are evaluated together: 4 x J independent point chains, no per-row branches, one
+// reduce-scatter per group, four distinct private bins.
+template <int J, bool LOGS>
+__device__ __forceinline__ void point_row(const double (&lv)[J], double (&acc)[J], double base,
+                                          double& lsum, int lane, int kin, double& pa,
+                                          double& pb) {
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const double s = base + lv[jj];
+    const double r = rcp_f64(s);
+    if (LOGS && lane + 32 * jj < kin) lsum += log(s);
+    acc[jj] += r;
+    if (jj & 1)
+      pb = jj == 1 ? r : pb + r;
+    else
+      pa = jj == 0 ? r : pa + r;
+  }
+  if (J == 1) pb = 0.0;
+}
+
 template <int J, int NOUT, bool LOGS>
 __device__ void grid_pass_fast(const GridDesc& gd, const double* slam, double* sg, double* pw,
                                int64_t gwarp, int64_t nwarps) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int kin = gd.k[gd.inner];
   const int oin = gd.off[gd.inner];
-  const int af = NOUT >= 1 ? gd.outer_axes[NOUT - 1] : 0;  // fastest outer axis
-  const int as = NOUT == 2 ? gd.outer_axes[0] : 0;         // slowest outer axis
-  const int kf = NOUT >= 1 ? gd.k[af] : 1, ks = NOUT == 2 ? gd.k[as] : 1;
-  const double* lf = slam + (NOUT >= 1 ? gd.off[af] : 0);
-  const double* ls = slam + (NOUT == 2 ? gd.off[as] : 0);
-  double* bins = pw + wid * kf;
+  // slots past the inner axis hold a huge λ: their 1/s ~ 1e-300 is negligible against any
+  // marginal, so the point loop runs without per-slot predicates (the Σ log s pass, LOGS,
+  // keeps them)
   double lv[J], acc[J];
 #pragma unroll
   for (int jj = 0; jj < J; ++jj) {
     const int m = lane + 32 * jj;
-    lv[jj] = (m < kin) ? slam[oin + m] : 1.0;
+    lv[jj] = (m < kin) ? slam[oin + m] : 1e300;
     acc[jj] = 0.0;
   }
   double lsum = 0.0;
-  const int64_t per = (gd.rows + nwarps - 1) / nwarps;
-  const int64_t r0 = gwarp * per;
-  const int64_t r1 = min(gd.rows, r0 + per);
-  int fi = NOUT >= 1 ? (int)(r0 % kf) : 0;
-  int si = NOUT == 2 ? (int)((r0 / kf) % ks) : 0;
-  double slow_acc = 0.0;
-  int slow_idx = si;
-  for (int64_t row = r0; row < r1; row += 4) {
-    double p[4];
-    int fq[4];
+  if (NOUT == 0) {  // one axis: a single row
+    if (gwarp == 0) {
+      double pa, pb;
+      point_row<J, LOGS>(lv, acc, 0.0, lsum, lane, kin, pa, pb);
+    }
+  } else {
+    const int af = gd.outer_axes[NOUT - 1];  // fastest outer axis
+    const int as = NOUT == 2 ? gd.outer_axes[0] : af;
+    const int kf = gd.k[af], ks = NOUT == 2 ? gd.k[as] : 1;
+    const int off_s = gd.off[as];
+    const double* lf = slam + gd.off[af];
+    const double* ls = slam + off_s;
+    double* bins = pw + wid * kf;
+    // balanced contiguous row ranges (every warp of the grid busy; a range's segment tails
+    // of < 4 rows take the one-row path)
+    const int64_t r0 = gwarp * gd.rows / nwarps;
+    const int64_t r1 = (gwarp + 1) * gd.rows / nwarps;
+    int fi = (int)(r0 % kf);
+    int si = NOUT == 2 ? (int)((r0 / kf) % ks) : 0;
+    for (int64_t row = r0; row < r1;) {
+      const int seg = (int)min(r1 - row, (int64_t)(kf - fi));
+      const double bs = NOUT == 2 ? ls[si] : 0.0;
+      double sacc = 0.0;
+      int q0 = 0;
+      for (; q0 + 4 <= seg; q0 += 4) {
+        double p[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool live = row + q < r1;
-      if (NOUT == 2 && live && si != slow_idx) {  // flush the slow axis (once per kf rows)
-        const double t = warp_sum(slow_acc);
-        if (lane == 0) atomicAdd(&sg[gd.off[as] + slow_idx], t);
-        slow_acc = 0.0;
-        slow_idx = si;
-      }
-      double base = 0.0;
-      if (NOUT >= 1) base += lf[fi];
-      if (NOUT == 2) base += ls[si];
-      double pq = 0.0;
-      if (live) {
-        // pairwise row partial (short dependency chain) up to 16 points per lane; a running
-        // sum above that (register pressure)
-        constexpr int JP = J <= 16 ? J : 1;
-        double part[JP];
-#pragma unroll
-        for (int jj = 0; jj < JP; ++jj) part[jj] = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) {
-          const int m = lane + 32 * jj;
-          if (m < kin) {
-            const double s = base + lv[jj];
-            const double r = rcp_f64(s);
-            if (LOGS) lsum += log(s);
-            acc[jj] += r;
-            part[J <= 16 ? jj : 0] += r;
-          }
+        for (int q = 0; q < 4; ++q) {
+          double pa, pb;
+          const double base = NOUT == 2 ? lf[fi + q0 + q] + bs : lf[fi + q0 + q];
+          point_row<J, LOGS>(lv, acc, base, lsum, lane, kin, pa, pb);
+          p[q] = pa + pb;
         }
-#pragma unroll
-        for (int w = 1; w < JP; w <<= 1)
-#pragma unroll
-          for (int jj = 0; jj + w < JP; jj += 2 * w) part[jj] += part[jj + w];
-        pq = part[0];
-      }
-      p[q] = pq;
-      fq[q] = fi;
-      if (NOUT == 2) slow_acc += pq;
-      if (NOUT >= 1 && live) {  // odometer: fastest outer axis first
-        if (++fi == kf) {
-          fi = 0;
-          if (NOUT == 2 && ++si == ks) si = 0;
+        if (NOUT == 2) sacc += (p[0] + p[1]) + (p[2] + p[3]);
+        const double tot = reduce4(p, lane);
+        if ((lane & 7) == 0) {
+          double* bq = bins + fi + q0 + (lane >> 3);  // four distinct bins (no wrap)
+          *bq += tot;
         }
+        __syncwarp();
+      }
+      for (; q0 < seg; ++q0) {  // segment tail: one row at a time
+        double pa, pb;
+        const double base = NOUT == 2 ? lf[fi + q0] + bs : lf[fi + q0];
+        point_row<J, LOGS>(lv, acc, base, lsum, lane, kin, pa, pb);
+        const double pr = pa + pb;
+        if (NOUT == 2) sacc += pr;
+        const double tot = warp_sum(pr);
+        if (lane == 0) bins[fi + q0] += tot;
+        __syncwarp();
+      }
+      if (NOUT == 2) {  // flush the slow axis once per segment
+        const double t = warp_sum(sacc);
+        if (lane == 0) atomicAdd(&sg[off_s + si], t);
+      }
+      row += seg;
+      fi += seg;
+      if (fi == kf) {
+        fi = 0;
+        if (NOUT == 2 && ++si == ks) si = 0;
       }
     }
-    if (NOUT >= 1) {
-      const double tot = reduce4(p, lane);
-      const int q = lane >> 3;
-      const int f = q == 0 ? fq[0] : q == 1 ? fq[1] : q == 2 ? fq[2] : fq[3];
-      if ((lane & 7) == 0 && row + q < r1) {
-        if (kf >= 4)
-          bins[f] += tot;  // four consecutive rows: four distinct fast indices
-        else
-          atomicAdd(&bins[f], tot);
-      }
-      __syncwarp();  // the next group's lanes may update the same bins
-    }
-  }
-  if (NOUT == 2) {
-    const double t = warp_sum(slow_acc);
-    if (lane == 0 && r0 < r1) atomicAdd(&sg[gd.off[as] + slow_idx], t);
   }
 #pragma unroll
   for (int jj = 0; jj < J; ++jj) {
@@ -197,6 +205,8 @@ __device__ void grid_pass_fast(const GridDesc& gd, const double* slam, double* s
     if (lane == 0) atomicAdd(&sg[gd.total], lsum);
   }
   if (NOUT >= 1) {  // fold the private bins into the block partials, clear them
+    const int af = gd.outer_axes[NOUT - 1];
+    const int kf = gd.k[af];
     __syncthreads();
     for (int f = threadIdx.x; f < kf; f += blockDim.x) {
       double t = 0.0;
@@ -311,6 +321,10 @@ struct SolveParams {
   double* res_out;        // stationarity of lam_out
   double tol;
   int max_iter;
+  int red_mode;           // cross-block reduction: 0 = fp64 atomics into gacc; 1 = partial
+                          // rows in part[], column sums by all blocks into gred, 2 barriers
+  double* part;           // [gridDim][Σk + 1]
+  double* gred;           // [Σk + 1]
 };
 
 // Block-wide reductions (every block runs them in the same order on the same data, so the
@@ -350,7 +364,7 @@ __device__ __forceinline__ double kkt_term(double lam, double g, double e, doubl
 // marginals and Σ log s), slam[T] (the point the next pass evaluates), th0[T], th1[T]
 // (SQUAREM iterates in log space; GD: the accepted λ and its marginals), private bins.
 template <int J, bool LOGS>
-__global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p) {
+__global__ void __launch_bounds__(kThreads, J <= 7 ? 2 : 1) solve_kernel(const SolveParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
   const int T = p.T;
@@ -390,11 +404,31 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveParams p)
     // Σ_γ of the modalities' marginals (Thm 2): each pass adds into the same sg
     for (int m = 0; m < p.M; ++m) grid_pass<J, LOGS>(p.gd[m], slam, sg, pw, gw, nw);
     __syncthreads();
-    if (!single) {
+    if (!single && p.red_mode == 0) {
       double* acc = p.gacc + (size_t)(pass % 3) * T1;
-      for (int i = tid; i < T1; i += blockDim.x) atomicAdd(&acc[i], sg[i]);
+      for (int i = tid; i < T1; i += blockDim.x) {
+        const double v = sg[i];
+        if (v != 0.0) atomicAdd(&acc[i], v);  // e.g. the slow axis: a block touches few entries
+      }
       grid.sync();
       for (int i = tid; i < T1; i += blockDim.x) sg[i] = __ldcg(&acc[i]);
+      __syncthreads();
+    } else if (!single) {
+      // block partials as columns of part[] (entry-major: part[i][block]), one barrier,
+      // entry i summed in a fixed order by one warp of block i mod gridDim (coalesced), a
+      // second barrier, every block reads the sums
+      const int nb = gridDim.x;
+      for (int i = tid; i < T1; i += blockDim.x) __stcg(&p.part[(size_t)i * nb + blockIdx.x], sg[i]);
+      grid.sync();
+      const int lane = tid & 31, w = tid >> 5;
+      for (int c = blockIdx.x + w * nb; c < T1; c += kWarps * nb) {
+        double t = 0.0;
+        for (int b = lane; b < nb; b += 32) t += __ldcg(&p.part[(size_t)c * nb + b]);
+        t = warp_sum(t);
+        if (lane == 0) __stcg(&p.gred[c], t);
+      }
+      grid.sync();
+      for (int i = tid; i < T1; i += blockDim.x) sg[i] = __ldcg(&p.gred[i]);
       __syncthreads();
     }
     // ---------------------------------------------------------------- update
@@ -588,11 +622,15 @@ static ggm_status make_desc(int L, const int* k, GridDesc* gd) {
   gd->off[0] = 0;
   int inner = 0;
   double prod = 1.0;
+  static const bool inner_min = [] {  // A/B hook: smallest axis inner (tools/solve_probe.py)
+    const char* e = std::getenv("GGM_SOLVE_INNER");
+    return e && e[0] == 'm' && e[1] == 'i';
+  }();
   for (int a = 0; a < L; ++a) {
     if (k[a] < 1) return fail(GGM_ERR_INVALID_ARGUMENT, "k[%d]=%d < 1", a, k[a]);
     gd->k[a] = k[a];
     gd->off[a + 1] = gd->off[a] + k[a];
-    if (k[a] > k[inner]) inner = a;
+    if (inner_min ? k[a] < k[inner] : k[a] > k[inner]) inner = a;
     prod *= k[a];
   }
   if (prod >= 1099511627776.0) return fail(GGM_ERR_INVALID_ARGUMENT, "grid too large (>= 2^40)");
@@ -655,7 +693,7 @@ static int grid_blocks(const GridDesc& gd) {
 // barrier costs microseconds; small grids run in one block).
 static int solve_blocks(double pts) {
   const int64_t want = (int64_t)std::ceil(pts / (kWarps * 8.0 * 32.0 * 16.0));
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, num_sms()));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, 2 * num_sms()));
 }
 
 template <int J>
@@ -689,6 +727,7 @@ static cudaError_t launch_solve_j(const SolveParams& sp, int nblk, size_t smem, 
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<J, LOGS>, kThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  nblk = std::min(nblk, std::min(per_sm, 2) * num_sms());  // co-resident (part[] has 2 x sms rows)
   void* args[] = {const_cast<SolveParams*>(&sp)};
   return cudaLaunchCooperativeKernel((void*)solve_kernel<J, LOGS>, dim3(nblk), dim3(kThreads), args,
                                      smem, s);
@@ -851,8 +890,9 @@ static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double
     return fail(GGM_ERR_INVALID_ARGUMENT, "invalid solve options");
   if (o.method < 0 || o.method > 2) return fail(GGM_ERR_INVALID_ARGUMENT, "method=%d", o.method);
   if (o.gauge != 0 && o.gauge != 1) return fail(GGM_ERR_INVALID_ARGUMENT, "gauge=%d", o.gauge);
-  // scratch: lam_res, g, Eu, gacc[3][T+1], scalars, status
-  const size_t bytes = sizeof(double) * (3 * (size_t)T + 3 * ((size_t)T + 1) + 8) + 64;
+  // scratch: lam_res, g, Eu, gacc[3][T+1], scalars, status, part[sms][T+1], gred[T+1]
+  const size_t bytes = sizeof(double) * (3 * (size_t)T + 3 * ((size_t)T + 1) + 8) + 64 +
+                       sizeof(double) * (2 * (size_t)num_sms() + 1) * ((size_t)T + 1) + 256;
   DevBuf buf;
   GGM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, s));
   double* lam_res = static_cast<double*>(buf.p);
@@ -861,6 +901,13 @@ static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double
   double* gacc = Eu + T;
   double* scal = gacc + 3 * ((size_t)T + 1);  // [1] logsum, [2] residual
   int* istat = reinterpret_cast<int*>(scal + 4);  // [0] it, [1] converged, [2] stalled, [3] passes, [6] bad
+  sp.part = reinterpret_cast<double*>(reinterpret_cast<char*>(buf.p) +
+                                      align_up(sizeof(double) * (3 * (size_t)T + 3 * ((size_t)T + 1) + 8) + 64, 256));
+  sp.gred = sp.part + 2 * (size_t)num_sms() * ((size_t)T + 1);
+  {
+    const char* e = std::getenv("GGM_SOLVE_RED");  // A/B hook (tools/solve_probe.py)
+    sp.red_mode = e ? std::atoi(e) : 0;
+  }
   GGM_CUDA_TRY(cudaMemsetAsync(gacc, 0, sizeof(double) * (3 * ((size_t)T + 1) + 8) + 64, s));
   check_E<<<4, 256, 0, s>>>(E, T, istat + 6);
   GGM_CUDA_TRY(cudaGetLastError());
