@@ -5,6 +5,12 @@ n = 1,000,000 and n = 30,000, rank 100, top-10 per row; BJ:11), row-sharded over
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config C5|C4]
 
+--gpus N > 1 without WORLD_SIZE in the environment re-launches this script under
+`torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1` (one rank per GPU,
+NCCL; NCCL_DEBUG=INFO for the communicator lines, on stderr); under torchrun WORLD_SIZE must
+equal N.  --dry-run exercises the same launcher and multi-rank plumbing on CPU (gloo) with an
+injected per-shard compute function (tests/test_bench_launcher.py); it measures nothing.
+
 A step = one pass of the hot path over the workload: for every axis, ggm_sparse_precision
 (BK1 prep/split -> BK2 fused tcgen05 recomposition + top-t -> CSR) on this rank's rows; at
 N > 1 also the NCCL all-gather of the CSR shards.  Inputs (V, λ) are resident in HBM when the
@@ -99,6 +105,37 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _maybe_launch(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (one process per GPU)
+    and return its exit code; None when this process is already the (or a) rank."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+        return None
+    if args.gpus <= 1:
+        return None
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
 def _dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -110,6 +147,75 @@ def _load_workload(name):
     from synth import gen
     c = gen.config(name)
     return c["axes"], c["t"]
+
+
+def _load_injected():
+    spec = os.environ.get("BENCH_DRYRUN_COMPUTE", "")
+    if ":" not in spec:
+        raise SystemExit("--dry-run needs BENCH_DRYRUN_COMPUTE=module:function (a CPU per-shard "
+                         "compute (V, lam, begin, end, t) -> (row_ptr, col, val))")
+    import importlib
+    mod, fn = spec.split(":", 1)
+    return getattr(importlib.import_module(mod), fn)
+
+
+def run_dry(args):
+    """The launcher and the multi-rank plumbing of a step on CPU (gloo): row shards of two
+    synthetic axes through an injected compute function, the CSR gather of parallel.py, the
+    barrier + max-over-ranks timing and rank 0's single JSON line.  No number it prints is a
+    measurement of this repository's kernels."""
+    import torch
+    import torch.distributed as dist
+    from paper_2407_19892_b200.parallel import gather_topk_csr, shard_rows
+    from synth import gen
+    world, rank, _ = _dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    compute = _load_injected()
+    t = 10
+    axes = []
+    for seed, n in ((5, args.dry_n), (6, max(args.dry_n // 10, 16))):
+        V, lam = gen.small_factor(seed, n, 16)
+        axes.append((torch.from_numpy(V), torch.from_numpy(lam)))
+
+    def step():
+        out = []
+        for V, lam in axes:
+            n = V.shape[0]
+            b, e = shard_rows(n, world, rank)
+            _, col, val = compute(V, lam, b, e, t)
+            out.append(gather_topk_csr(col, val, min(t, n - 1), n))
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = step()
+    dt = time.perf_counter() - t0
+    tt = torch.tensor([dt], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item()) / max(args.steps, 1) * 1e3
+    if rank == 0:
+        dump = os.environ.get("BENCH_DRYRUN_DUMP")
+        if dump:
+            np.savez(dump, **{f"{w}{a}": x.numpy() for a, r in enumerate(res)
+                              for w, x in zip(("rp", "col", "val"), r)})
+        ent = float(sum(V.shape[0] ** 2 for V, _ in axes))
+        print(json.dumps({"metric": METRIC, "value": ent / (ms * 1e-3), "unit": UNIT,
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                          "dry_run": True, "backend": "gloo" if world > 1 else "none",
+                          "config": {"workload": f"dry run: axes n={[int(V.shape[0]) for V, _ in axes]}"
+                                                 ", k=16, top-10 (launcher test only)"}}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
 def run_reference(args):
@@ -321,7 +427,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stages", action="store_true",
                     help="skip the a1-a4 stage timings (gram_eig + solve on C2/C3)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo launcher + plumbing check with an injected compute (tests)")
+    ap.add_argument("--dry-n", type=int, default=2000)
     args = ap.parse_args()
+    rc = _maybe_launch(args)
+    if rc is not None:
+        return rc
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -334,7 +448,12 @@ def main():
     world, rank, local = _dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator lines (nranks = N)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        print(f"bench.py: rank {rank}/{world} on cuda:{local} "
+              f"({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
     if not G.device_supported():
         raise SystemExit("libggm: device is not sm_100a")
 
