@@ -421,6 +421,8 @@ struct FusedParams {
   int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
   int screen;        // kSym: hi*hi screening MMAs only (candidates re-evaluated exactly)
   int pair;          // CTA-pair kernel (host-side selection; the kernel's template PAIR)
+  int unit_step;         // units unit_lo, unit_lo + unit_step, ... < unit_hi (1: contiguous;
+                         // nranks: the rank-strided share of the distributed symmetric scheme)
   int unit_lo, unit_hi;  // units processed by this launch (a rank's share in the sharded
                          // symmetric scheme; [0, all units) otherwise)
 #ifdef GGM_EPI_DEBUG
@@ -481,9 +483,15 @@ __device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& ub) 
 // Visit the kSym window [ub, ub + W) starting at X = the last unit of this wave (all CTAs of
 // a wave contain X in their windows), so concurrently running CTAs stream the same column
 // blocks in lockstep and share them through L2.
-__device__ __forceinline__ int sym_start(const FusedParams& p, int u, int ub, int u0, int ustep,
+__host__ __device__ __forceinline__ int unit_count(const FusedParams& p) {
+  return (p.unit_hi - p.unit_lo + p.unit_step - 1) / p.unit_step;
+}
+__host__ __device__ __forceinline__ int unit_of(const FusedParams& p, int uj) {
+  return p.unit_lo + uj * p.unit_step;
+}
+__device__ __forceinline__ int sym_start(const FusedParams& p, int uj, int ub, int u0, int ustep,
                                          int W) {
-  const int X = min(p.unit_hi - 1, u - u0 + ustep - 1);
+  const int X = unit_of(p, min(unit_count(p) - 1, uj - u0 + ustep - 1));
   const int delta = (X - ub + p.NB) % p.NB;
   return delta >= W ? 0 : delta;
 }
@@ -493,13 +501,14 @@ struct TileIter {
   int K0, K1;
   bool h1;
   int s, ub, W, o;  // kSym: o = window offset of the current tile
-  __device__ __forceinline__ void start(const FusedParams& p, int u, int ub_, int u0, int ustep) {
+  __device__ __forceinline__ void start(const FusedParams& p, int u, int uj, int ub_, int u0,
+                                        int ustep) {
     ub = ub_;
     s = 0;
     h1 = true;
     if (KIND >= kSym) {
       W = sym_window(ub, p.NB);
-      o = sym_start(p, u, ub, u0, ustep, W);
+      o = sym_start(p, uj, ub, u0, ustep, W);
       place(p);
     } else {
       const int j = KIND == kPlain ? (u % p.C) * p.TPC : 0;
@@ -812,7 +821,8 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     asm volatile("bar.sync 5, 256;" ::: "memory");
   }
   int tpar = 0;
-  for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
+  for (int uj = u0; uj < unit_count(p); uj += ustep) {
+    const int u = unit_of(p, uj);
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;  // this CTA's 128-row block
@@ -826,7 +836,7 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     top.init(t);
     double macc = 0.0;
     TileIter<KIND, PAIR> ti;
-    ti.start(p, u, ub, u0, ustep);
+    ti.start(p, u, uj, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s, ti.next(p)) {
       const int Kh = h ? ti.K1 : ti.K0;
       const bool live = (h == 0 || ti.h1) && GGM_DBG(p) != 2;
@@ -992,14 +1002,15 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   MagList<MAXT> top;
-  for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
+  for (int uj = u0; uj < unit_count(p); uj += ustep) {
+    const int u = unit_of(p, uj);
     int ub;
     const int ntiles = unit_tiles<kSeed, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
     const int64_t gi = (int64_t)rb * kRowsPerBlock + g.r;
     top.init(t);
     TileIter<kSeed, PAIR> ti;
-    ti.start(p, u, ub, u0, ustep);
+    ti.start(p, u, uj, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s, ti.next(p)) {
       const int Kh = g.second() ? ti.K1 : ti.K0;
       const int64_t cb = (int64_t)Kh * kRowsPerBlock + g.col_off();
@@ -1123,7 +1134,8 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #ifdef GGM_MMA_PROF
   long long pe_t0 = clock64(), pe_w = 0, pe_n = 0;
 #endif
-  for (int u = p.unit_lo + u0; u < p.unit_hi; u += ustep) {
+  for (int uj = u0; uj < unit_count(p); uj += ustep) {
+    const int u = unit_of(p, uj);
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1131,7 +1143,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
     const bool valid = gi < n;
     const float bi = valid ? __ldg(thr + gi) : INFINITY;  // row bound (accumulator units)
     TileIter<KIND, PAIR> ti;
-    ti.start(p, u, ub, u0, ustep);
+    ti.start(p, u, uj, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s) {
       const int Kh = second ? ti.K1 : ti.K0;
       const bool live = (!second || ti.h1) && dbg != 2;
@@ -1346,7 +1358,6 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int units = p.unit_hi;
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
   const int u0 = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
   const int ustep = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
@@ -1408,7 +1419,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
       int stage = 0;
       uint32_t phase = 0;
       int a_iter = 0;
-      for (int u = p.unit_lo + u0; u < units; u += ustep) {
+      for (int uj = u0; uj < unit_count(p); uj += ustep) {
+        const int u = unit_of(p, uj);
         int ub;
         const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1428,7 +1440,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
           ++a_iter;
         }
         TileIter<KIND, PAIR> ti;
-        ti.start(p, u, ub, u0, ustep);
+        ti.start(p, u, uj, ub, u0, ustep);
         for (int s = 0; s < ntiles; ++s, ti.next(p)) {
           if (PAIR) {
             // this CTA's half of the B tile: operand block K0 + rank, hi (+ lo) per K atom
@@ -1545,7 +1557,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
             else if (slot < p.KS + p.TS) tm[a] |= 1u << ks;
           }
         }
-        for (int u = p.unit_lo + u0; u < units; u += ustep) {
+        for (int uj = u0; uj < unit_count(p); uj += ustep) {
+          const int u = unit_of(p, uj);
           int ub;
           const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
           PROF_W(pr_ta, mbar_wait(afull, a_iter & 1));
@@ -1616,7 +1629,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
         }
       } else
 #endif
-      for (int u = p.unit_lo + u0; u < units; u += ustep) {
+      for (int uj = u0; uj < unit_count(p); uj += ustep) {
+        const int u = unit_of(p, uj);
         int ub;
         const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         if (resident) {
@@ -2265,9 +2279,10 @@ static ggm_status launch_fused(const FusedParams& fp_in, int t, int64_t ablocks,
     fp.unit_lo = 0;
     fp.unit_hi = fp.kind == kPlain ? fp.RB * fp.C : fp.RB;
   }
+  if (fp.unit_step < 1) fp.unit_step = 1;
   if (fp.unit_hi <= fp.unit_lo) return GGM_OK;  // empty shard
   const size_t smem = fused_smem_bytes(fp.KA, fp.resident, fp.pair);
-  const int units = fp.unit_hi - fp.unit_lo;
+  const int units = unit_count(fp);
   TMaps tm;
   memset(&tm, 0, sizeof(tm));
   cudaError_t ce;
@@ -2452,10 +2467,12 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   return GGM_OK;
 }
 
-// Phase 4: the symmetric main kernel over units [unit_lo, unit_hi) (all units on one GPU, a
-// contiguous share per rank in the distributed form); candidates -> w.ckey / w.cval.
+// Phase 4: the symmetric main kernel over units unit_lo, unit_lo + unit_step, ... < unit_hi
+// (all units on one GPU; rank r of N takes units r, r + N, ... in the distributed form, so
+// every rank gets the same mix of bound levels — contiguous shares left the last ranks with
+// most of the candidate emission, tools/sim_ranks.py); candidates -> w.ckey / w.cval.
 static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int unit_lo,
-                           int unit_hi, cudaStream_t s) {
+                           int unit_hi, cudaStream_t s, int unit_step = 1) {
   fp.kind = kSym;
   fp.RB = (int)pl.NBu;
   fp.thr = pl.screen ? w.thr_s : w.thr_p;
@@ -2467,6 +2484,7 @@ static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int un
   fp.cand_total = pl.cand_total;
   fp.unit_lo = unit_lo;
   fp.unit_hi = unit_hi;
+  fp.unit_step = unit_step;
   if (unit_hi <= unit_lo) return GGM_OK;
   return launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
 }
@@ -2906,8 +2924,9 @@ static ggm_status sym_shard_impl(
   st = sym_prepare(pl, w, V, lambda, n, k, fp, s, -1, -1, thr_all);
   if (st != GGM_OK) return st;
   tm.mark(1);
-  const int ulo = (int)sym_unit_lo(pl, rank, nranks), uhi = (int)sym_unit_lo(pl, rank + 1, nranks);
-  st = sym_main(pl, w, fp, ulo, uhi, s);
+  // this rank's block pairs: units rank, rank + nranks, ... (the merge ownership of rows
+  // below stays the contiguous bound-order ranges)
+  st = sym_main(pl, w, fp, rank, (int)pl.NBu, s, nranks);
   if (st != GGM_OK) return st;
   tm.mark(2);
   DevScalars hs;
@@ -2961,7 +2980,7 @@ static ggm_status sym_shard_impl(
   GGM_CUDA_TRY(cudaStreamSynchronize(s));
   tm.finish();
   double evaluated = 0.0;  // entries evaluated by this rank's units
-  for (int64_t b = ulo; b < uhi; ++b) {
+  for (int64_t b = rank; b < pl.NBu; b += nranks) {  // this rank's units (rank-strided)
     const int64_t NBu = pl.NBu;
     const int64_t W = (NBu & 1) ? (NBu + 1) / 2 : NBu / 2 + (b < NBu / 2 ? 1 : 0);
     evaluated += pl.pair ? (double)W * 2 * kRowsPerBlock * kTileN

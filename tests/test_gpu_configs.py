@@ -9,7 +9,7 @@ import torch
 
 import oracle as O
 from synth import gen
-from parity_util import check_topk
+from parity_util import assert_exact_fraction, check_topk
 
 pytestmark = pytest.mark.gpu
 
@@ -80,14 +80,38 @@ def test_data_config_pipeline(G, name, rows_per_axis):
         rows = np.arange(n) if rows_per_axis is None else _sample_rows(n, rows_per_axis, a,
                                                                        (0, n - 1))
         prp, pc, pv = _csr_rows(rp, col, val, rows)
-        st = check_topk(prp, pc, pv, Vo[a], lo[a], rows, t)
+        # C1/C3 (values O(1e-2..0.6)): the strict relative-only gate; C2's 3e-4 eigengaps
+        # carry the fp32 spectrum's rounding into ψ at ~1e-5 relative (the GPU pipeline's own
+        # V vs the oracle's fp64 V), so C2 keeps the literal gate here and is held to the
+        # strict gate kernel-level in test_c2_kernel_strict
+        st = check_topk(prp, pc, pv, Vo[a], lo[a], rows, t, strict=name != "C2")
         assert st["exact"] + st["excused"] == len(rows)
+        assert_exact_fraction(st, 0.99 if name != "C2" else 0.9, f"{name} axis {a}")
+
+
+def _shard_sample(n, P, per_shard, seed):
+    """Rows of every P-way shard: per_shard random rows plus each shard's first and last row,
+    and the 256-row tile boundaries (b·256 - 1, b·256) that fall in the sample's shards."""
+    from paper_2407_19892_b200.parallel import shard_rows
+    rng = np.random.default_rng(seed)
+    rows = set()
+    for r in range(P):
+        b, e = shard_rows(n, P, r)
+        rows.update(rng.choice(np.arange(b, e), size=min(per_shard, e - b), replace=False).tolist())
+        rows.update((b, e - 1))
+        for tb in range((b + 255) // 256 * 256, e, 256 * 37):   # every 37th tile boundary
+            rows.update((tb - 1, tb))
+    return np.array(sorted(x for x in rows if 0 <= x < n), dtype=np.int64)
 
 
 @pytest.mark.parametrize("name", ["C4", "C5"])
 def test_factor_config_sampled_rows_and_shards(G, name):
-    """C4/C5 at full size: sampled rows (incl. 2/4/8-way shard boundaries) vs the oracle, and
-    simulated ranks (P disjoint row ranges) bitwise equal to the single call."""
+    """C4/C5 at full size in the bench's launch configuration (automatic scheme: the
+    symmetric screening scheme for the large axes): sampled rows vs the oracle with the
+    strict relative-only gate and the exact-match fraction (reading TOL; §8(c) c3: C5 axis A
+    8,192 rows = 1,024 per 8-way shard incl. shard and tile boundaries, axis B all 30,000
+    rows), and simulated ranks (P disjoint row ranges, plain scheme) bitwise equal to the
+    single plain call."""
     cfg = gen.config(name)
     t = cfg["t"]
     from paper_2407_19892_b200.parallel import shard_rows
@@ -100,15 +124,15 @@ def test_factor_config_sampled_rows_and_shards(G, name):
         rp = plan.row_ptr.cpu().numpy()
         col = plan.col.cpu().numpy()
         val = plan.val.cpu().numpy()
-        bounds = []
-        for P in (2, 4, 8):
-            for r in range(P):
-                b, e = shard_rows(n, P, r)
-                bounds += [b, e - 1]
-        rows = _sample_rows(n, 256 if n > 100_000 else 512, 7 + ax, bounds + [0, n - 1])
+        if n <= 30_000:
+            rows = np.arange(n)
+        else:
+            rows = _shard_sample(n, 8, 1024 if name == "C5" else 512, 7 + ax)
         prp, pc, pv = _csr_rows(rp, col, val, rows)
-        st = check_topk(prp, pc, pv, V, lam, rows, t)
+        st = check_topk(prp, pc, pv, V, lam, rows, t, strict=True)
         assert st["exact"] + st["excused"] == len(rows)
+        assert_exact_fraction(st, 0.999, f"{name} axis {ax}")
+        assert st["max_rel_err"] <= 1e-5, st
         # simulated ranks: concatenated row shards (plain scheme) == one plain full-axis call,
         # bitwise (the automatic full-axis call above may use the symmetric scheme, whose
         # transposed-direction entries accumulate the two cross-term MMAs in swapped order)
@@ -125,3 +149,25 @@ def test_factor_config_sampled_rows_and_shards(G, name):
                 vals.append(sp.val.cpu().numpy())
             assert np.array_equal(np.concatenate(cols), col)
             assert np.array_equal(np.concatenate(vals), val)
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_c2_kernel_strict(G, axis):
+    """C2 (10,000 cells x 2,000 genes, k = 50, t = 10; BJ:8): the sparse kernel on the
+    oracle's spectrum (fp32 V, the same bits on both sides) over ALL rows of the axis, strict
+    relative-only gate and exact-match fraction (reading TOL: the literal 1e-6 floor excuses
+    every cell-axis row at C2 magnitudes, so it is not the gate here)."""
+    cfg = gen.config("C2")
+    X, ks, t = cfg["X"], cfg["k"], cfg["t"]
+    Vo, Eo = O.gram_eig(X, axis, ks[axis])
+    _, Eother = O.gram_eig(X, 1 - axis, ks[1 - axis])
+    lo, _ = O.solve_eigvals([Eo, Eother] if axis == 0 else [Eother, Eo], tol=1e-12)
+    V = Vo.astype(np.float32)
+    lam = lo[axis]
+    n = V.shape[0]
+    rp, col, val = G.ggm_sparse_precision(torch.from_numpy(V).cuda(), torch.from_numpy(lam).cuda(),
+                                          0, n, topk=t)
+    st = check_topk(rp.cpu().numpy(), col.cpu().numpy(), val.cpu().numpy(), V, lam,
+                    np.arange(n), t, strict=True)
+    assert st["exact"] + st["excused"] == n
+    assert_exact_fraction(st, 0.999, f"C2 axis {axis}")
