@@ -555,14 +555,18 @@ def ggm_sparse_precision(V: torch.Tensor, lam: torch.Tensor, row_begin: int = 0,
         row_end = n
     plan = SparsePlan(n, k, row_begin, row_end, mode, topk, tau, col_chunks, capacity,
                       device=V.device, symmetric=symmetric)
-    try:
-        nnz = plan.run(V, lam, stream)
-    except GGMError as e:
-        if e.status != 5:
-            raise
-        plan = SparsePlan(n, k, row_begin, row_end, mode, topk, tau, col_chunks,
-                          max(e.required, 1), device=V.device, symmetric=symmetric)
-        nnz = plan.run(V, lam, stream)
+    for attempt in range(3):
+        try:
+            nnz = plan.run(V, lam, stream)
+            break
+        except GGMError as e:
+            if e.status != 5 or attempt == 2:
+                raise
+            # two-call protocol; the slack covers entries within rounding of tau whose side of
+            # the threshold depends on the scheme the larger workspace selects
+            plan = SparsePlan(n, k, row_begin, row_end, mode, topk, tau, col_chunks,
+                              max(int(e.required * 1.01) + 4096, 1), device=V.device,
+                              symmetric=symmetric)
     return plan.row_ptr, plan.col[:nnz], plan.val[:nnz]
 
 

@@ -1086,6 +1086,124 @@ __device__ __forceinline__ float sel32(const uint32_t* v, uint32_t e) {
   return __uint_as_float((e & 1u) ? a[1] : a[0]);
 }
 
+// Epilogue role of the row-mass pass (kSymList, mode 2; degree down-weighting of the overall
+// rules): w_i = Σ_{j≠i} |ψ_ij| over each unordered block pair (I, J) computed once —
+// row sums of the tile into rows I (in-thread, registers), column sums into rows J (off the
+// diagonal block) by a reduce-scatter transpose per 32x32 chunk, the four quadrant warps of a
+// column slice combined in shared memory, one fp64 red per column per tile.  16 warps (4 per
+// lane quadrant, 64 columns each); the TMEM buffer is released as soon as the warp's last
+// chunk is in registers, before its sums run.
+template <bool PAIR, int EPW>
+__device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tmem_base,
+                                              uint64_t* tfull, uint64_t* tempty, int warp,
+                                              int lane, float* scratch_all, int u0, int ustep,
+                                              int rank) {
+  using G = EpiGeom<EPW>;
+  const G g(warp, lane);
+  const float sd = ldexpf(1.f, -p.sc->exp2);
+  const double sd2 = (double)sd * (double)sd;
+  const int64_t n = p.n;
+  const uint32_t trow = tmem_base + ((uint32_t)(g.q * 32) << 16) + (uint32_t)(g.part * G::W);
+  const int coff = g.col_off();
+  const bool second = g.second();
+  const uint32_t tfull_a0 = smem_u32(&tfull[0]), tfull_a1 = smem_u32(&tfull[1]);
+  const bool remote_rel = PAIR && rank != 0;
+  const uint32_t tempty_a0 = remote_rel ? mbar_map_cluster(&tempty[0], 0) : smem_u32(&tempty[0]);
+  const uint32_t tempty_a1 = remote_rel ? mbar_map_cluster(&tempty[1], 0) : smem_u32(&tempty[1]);
+  // column-sum slices: [tile parity][part][G::W] floats
+  for (int b = (warp - kFirstEpiWarp) * 32 + lane; b < 2 * G::P * G::W; b += EPW * 32)
+    scratch_all[b] = 0.f;
+  asm volatile("bar.sync 5, %0;" ::"r"(EPW * 32) : "memory");
+  int buf = 0, tpar = 0;
+  uint32_t tphase = 0;
+  for (int uj = u0; uj < unit_count(p); uj += ustep) {
+    const int u = unit_of(p, uj);
+    int ub;
+    const int ntiles = unit_tiles<kSymList, PAIR>(p, u, ub);
+    const int rb = PAIR ? 2 * ub + rank : ub;
+    const int64_t lr = (int64_t)rb * kRowsPerBlock + g.r;
+    const bool valid = lr < p.rows;
+    const int64_t gi = p.row_begin + lr;
+    double macc = 0.0;
+    TileIter<kSymList, PAIR> ti;
+    ti.start(p, u, uj, ub, u0, ustep);
+    for (int s = 0; s < ntiles; ++s) {
+      const int Kh = second ? ti.K1 : ti.K0;
+      const bool live = !second || ti.h1;
+      // the diagonal (super) block holds both (i, j) and (j, i): row sums only
+      const bool diag_blk = PAIR ? (ti.K0 >> 1) == ub : Kh == rb;
+      const int64_t cb = (int64_t)Kh * kRowsPerBlock + coff;
+      const bool need_mask = (gi >= cb && gi < cb + G::W) || cb + G::W > n;
+      ti.next(p);
+      mbar_wait_a(buf ? tfull_a1 : tfull_a0, tphase);
+      tc_fence_after();
+      const uint32_t taddr = trow + (uint32_t)(buf * kTileN);
+      const uint32_t cur = buf;
+      buf ^= 1;
+      tphase ^= (uint32_t)(buf == 0);
+      float* cacc = scratch_all + (tpar * G::P + g.part) * G::W;
+#pragma unroll
+      for (int c = 0; c < G::NC; ++c) {
+        uint32_t v[32];
+        if (live) {
+          tmem_ld32_nowait(taddr + c * 32, v);
+          tmem_wait_ld(v);
+        }
+        if (c == G::NC - 1) {  // the warp's slice is in registers: release the buffer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            const uint32_t ta = cur ? tempty_a1 : tempty_a0;
+            if (remote_rel)
+              mbar_arrive_cluster_a(ta);
+            else
+              mbar_arrive_a(ta);
+          }
+        }
+        if (!live) continue;
+        const int64_t col0 = cb + c * 32;
+        uint32_t excl = 0;  // diagonal (j == i, not an edge: Q8) and padding columns (j >= n)
+        if (need_mask) {
+          const int64_t dd = gi - col0;
+          if ((uint64_t)dd < 32ull) excl |= 1u << dd;
+          const int64_t nn = n - col0;
+          if (nn < 32) excl |= nn <= 0 ? 0xffffffffu : (0xffffffffu << nn);
+        }
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+        if (excl == 0) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s4[e & 3] += fabsf(__uint_as_float(v[e]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            s4[e & 3] += ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(v[e]));
+        }
+        if (valid) macc += (double)((s4[0] + s4[1]) + (s4[2] + s4[3]));
+        if (!diag_blk) {
+          const float cs = col_abs_sums32(v, valid ? excl : 0xffffffffu, lane);
+          atomicAdd(cacc + c * 32 + lane, cs);
+        }
+      }
+      if (!diag_blk && live) {
+        // the part's 4 quadrant warps have added their column sums: quadrant 0 flushes
+        // (and clears) them; the other parity slice takes the next tile meanwhile
+        asm volatile("bar.sync %0, 128;" ::"r"(8 + g.part) : "memory");
+        if (g.q == 0) {
+#pragma unroll
+          for (int c = 0; c < G::NC; ++c) {
+            const int64_t j = cb + c * 32 + lane;
+            const float x = cacc[c * 32 + lane];
+            cacc[c * 32 + lane] = 0.f;
+            if (j < n && x != 0.f) atomicAdd(p.mass_out + j, (double)x * sd2);
+          }
+        }
+      }
+      tpar ^= 1;
+    }
+    if (valid) atomicAdd(p.mass_out + lr, macc * sd2);  // every column slice adds its part
+  }
+}
+
 // Epilogue role, candidate form (kSym): every row i carries a lower bound b_i of its t-th
 // magnitude (the seed pass); rows and columns are in bound order.  Entry ψ_ij of a tile is
 // emitted as a candidate of row i if |ψ| >= b_i (row direction) and, for off-diagonal
@@ -1327,7 +1445,9 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #define GGM_SYM_EPW 16
 #endif
 __host__ __device__ constexpr int epw_of(int KIND, int MAXT) {
-  return KIND == kSym ? GGM_SYM_EPW : (KIND == kSeed && MAXT <= 10) ? GGM_SEED_EPW : 8;
+  return KIND == kSym ? GGM_SYM_EPW
+         : KIND == kSymList ? 16
+         : (KIND == kSeed && MAXT <= 10) ? GGM_SEED_EPW : 8;
 }
 
 template <int MAXT, int KIND, bool PAIR, int EPW = epw_of(KIND, MAXT)>
@@ -1401,6 +1521,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
     else if (KIND == kSeed)
       epilogue_seed<MAXT, PAIR, EPW>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep,
                                      rank);
+    else if (KIND == kSymList)
+      epilogue_mass<PAIR, EPW>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep, rank);
     else
       epilogue_role<MAXT, KIND, PAIR>(p, tmem_base, tfull, tempty, warp, lane, scratch, u0, ustep,
                                       rank);
