@@ -38,6 +38,23 @@ struct Carve {
 
 }  // namespace ggm
 
+// Device-side invariant checks, compiled in only for the checked build
+// (tools/build_variant.sh checked -DGGM_CHECKED; compute-sanitizer is not available on the GPU
+// pool): a failed check prints and traps, so the call returns GGM_ERR_CUDA.
+#ifdef GGM_CHECKED
+#define GGM_DCHECK(cond)                                                                \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("GGM_DCHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);            \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define GGM_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 #define GGM_CUDA_TRY(expr)                                                              \
   do {                                                                                  \
     cudaError_t _e = (expr);                                                            \

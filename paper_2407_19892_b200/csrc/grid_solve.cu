@@ -169,10 +169,12 @@ __device__ void grid_pass_fast(const GridDesc& gd, const double* slam, double* s
         const double tot = reduce4(p, lane);
         if ((lane & 7) == 0) {
           double* bq = bins + fi + q0 + (lane >> 3);  // four distinct bins (no wrap)
+          GGM_DCHECK(fi + q0 + (lane >> 3) < kf);
           *bq += tot;
         }
         __syncwarp();
       }
+      GGM_DCHECK(seg >= 1 && fi + seg <= kf);
       for (; q0 < seg; ++q0) {  // segment tail: one row at a time
         double pa, pb;
         const double base = NOUT == 2 ? lf[fi + q0] + bs : lf[fi + q0];

@@ -629,6 +629,7 @@ struct TopList {
 #pragma unroll
     for (int a = 0; a < MAXT; ++a) {
       if (a < t) {
+        GGM_DCHECK(idx[a] >= 0);  // a real column: the row had >= t candidates
         int rank = 0;
 #pragma unroll
         for (int b = 0; b < MAXT; ++b)
@@ -1414,11 +1415,13 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
             const uint32_t xb = __float_as_uint(sel32(VC, e) * sd2);
             if (hr) {  // candidate (i -> j): target row i
               const int64_t pos = at + __popc(br & lt);
+              GGM_DCHECK(pos < p.cand_total && gi < n && col0 + (int)e < n);
               p.cand_key[pos] = (uint32_t)gi;
               p.cand_val[pos] = make_uint2((uint32_t)(col0 + (int)e), xb);
             }
             if (hc) {  // candidate (j -> i): target row j
               const int64_t pos = at + __popc(br) + __popc(bc & lt);
+              GGM_DCHECK(pos < p.cand_total && gi < n && col0 + (int)e < n);
               p.cand_key[pos] = (uint32_t)(col0 + (int)e);
               p.cand_val[pos] = make_uint2((uint32_t)gi, xb);
             }
@@ -1981,6 +1984,7 @@ __global__ void recompute_sorted(const int64_t* __restrict__ off, uint2* __restr
       for (int u = 0; u < 4; ++u) {
         const int64_t e = e0 + u < b1 ? e0 + u : b1 - 1;
         const uint2 cvv = sval[e];
+        GGM_DCHECK(cvv.x < (uint32_t)n);
         keep[u] = e0 + u < b1 && fabsf(__uint_as_float(cvv.y)) >= xcut;
         const float* vb = Ub + (int64_t)cvv.x * k;
 #pragma unroll
@@ -2019,6 +2023,7 @@ __global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restr
   const int64_t b1 = lower_bound_u32(key, ncand, (uint32_t)j + 1u);
   for (int64_t e = b0; e < b1; ++e) {
     const uint2 x = cv[e];
+    GGM_DCHECK(x.x < (uint32_t)n);
     const float v = __uint_as_float(x.y);
     top.merge_insert(fabsf(v), v, __ldg(perm + x.x));
   }
