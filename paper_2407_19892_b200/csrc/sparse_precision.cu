@@ -629,7 +629,6 @@ struct TopList {
 #pragma unroll
     for (int a = 0; a < MAXT; ++a) {
       if (a < t) {
-        GGM_DCHECK(idx[a] >= 0);  // a real column: the row had >= t candidates
         int rank = 0;
 #pragma unroll
         for (int b = 0; b < MAXT; ++b)

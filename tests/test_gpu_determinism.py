@@ -1,8 +1,9 @@
 """Repeatability of every kernel family (a race-detection stand-in: compute-sanitizer is not
 available on the GPU pool): the same inputs through the C ABI three times give
 bitwise-identical CSR outputs (the candidate pools fill in a scheduling-dependent order, but
-the sort by target row + the (|ψ| desc, j asc) merge are order-free), and the eigenvalue
-solve (cross-block fp64 reductions in a scheduling-dependent order) agrees to 1e-12."""
+the sort by target row + the (|ψ| desc, j asc) merge are order-free), the down-weighted
+overall rules the same edges (values to 1e-6: fp64 row masses summed in a scheduling-dependent
+order), and the eigenvalue solve (cross-block fp64 reductions) agrees to 1e-12."""
 import numpy as np
 import pytest
 import torch
@@ -19,7 +20,7 @@ def G():
     return G
 
 
-def _rep(fn, reps=3):
+def _rep(fn, reps=3, val_rtol=0.0):
     outs = []
     for _ in range(reps):
         r = fn()
@@ -27,7 +28,10 @@ def _rep(fn, reps=3):
         outs.append([x.cpu().numpy().copy() for x in r])
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
-            assert np.array_equal(a, b)
+            if val_rtol and a.dtype == np.float32:
+                np.testing.assert_allclose(a, b, rtol=val_rtol, atol=0)
+            else:
+                assert np.array_equal(a, b)
     return outs[0]
 
 
@@ -48,7 +52,10 @@ def test_threshold_and_overall_repeatable(G):
     rp, c, v = G.ggm_sparse_precision(Vd, ld, 0, n, topk=10)
     tau = float(np.quantile(np.abs(v.cpu().numpy()), 0.5))
     _rep(lambda: G.ggm_sparse_precision(Vd, ld, 0, n, mode=1, tau=tau))
-    _rep(lambda: G.ggm_sparse_precision_overall(Vd, ld, 10 * n, downweight=True, min_edges=1))
+    # down-weighting: the row masses are fp64 sums in a scheduling-dependent order, so the
+    # values scaled back by sqrt(w_i w_j) may differ in the last float bit; the edge set not
+    _rep(lambda: G.ggm_sparse_precision_overall(Vd, ld, 10 * n, downweight=True, min_edges=1),
+         val_rtol=1e-6)
 
 
 def test_solve_repeatable(G):
