@@ -317,11 +317,30 @@ def stage_timings(G, torch):
         _, info = G.ggm_solve_eigvals(Ec, ks)
         solve_ms = (time.perf_counter() - t0) * 1e3
         pts = float(np.prod(ks))
+        kms = info["kernel_ms"]
         out[name] = {"gram_eig_ms": gram_ms, "solve_ms": solve_ms,
-                     "solve_iterations": info["iterations"],
+                     "solve_iterations": info["iterations"], "solve_passes": info["passes"],
+                     "solve_kernel_ms": kms,
                      "stationarity": info["stationarity"],
-                     "grid_points_per_s": pts * max(info["iterations"], 1) / (solve_ms * 1e-3),
+                     "grid_points_per_s": pts * info["passes"] / (kms * 1e-3),
                      "grid_points": pts}
+        if name == "C3":
+            # BK4 roofline (BK4): FP64-pipe bound, 5 FP64-pipe instructions per grid
+            # point (s = base + λ, two Newton FMAs, two accumulating adds) + 1 MUFU seed; peak
+            # = 64 FP64 lanes/clk/SM x SMs x the max SM clock / 5
+            peaks, _ = _peaks()
+            f_max = peaks.get("sm_max_mhz", 1965.0) * 1e6
+            import torch as _t
+            sms = _t.cuda.get_device_properties(0).multi_processor_count
+            peak_pts = 64.0 * sms * f_max / 5.0
+            ach = pts * info["passes"] / (kms * 1e-3)
+            out["roofline_bk4"] = {
+                "bound": "alu", "kernel": "solve_kernel (BK4, C3 grid 400x300x200)",
+                "achieved": ach / 1e12, "peak": peak_pts / 1e12, "unit": "Tpoints/s",
+                "frac": ach / peak_pts, "traffic": None,
+                "basis": "grid points x passes / CUDA-event kernel time; peak: FP64 pipe "
+                         "(64 lanes/clk/SM) at sm_max_mhz / 5 FP64 instructions per point",
+                "passes": info["passes"], "kernel_ms": kms}
     # at-scale spectrum: a 40,000 x 40,000 unfolding (beyond the dense
     # Gram path) of known spectrum, X = U diag(s) W^T, k = 50, randomized subspace iteration
     d = m = 40_000

@@ -249,6 +249,9 @@ typedef struct {
   double grid_min;            /* min_j s_j = Σ_l min λ_l */
   double trace_inconsistency; /* max_l |tr E_l − mean| / mean (reading T) */
   int floor_active;           /* 1 if some λ is on the floor ε (barrier regime) */
+  int passes;                 /* grid passes evaluated (all methods; method 2 also counts
+                                 rejected step sizes) */
+  double kernel_ms;           /* device time of the solve kernel(s), CUDA events on `stream` */
 } ggm_solve_info;
 
 void ggm_solve_opts_default(ggm_solve_opts *opts);

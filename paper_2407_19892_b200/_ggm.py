@@ -61,7 +61,7 @@ class SolveOpts(C.Structure):
 class SolveInfo(C.Structure):
     _fields_ = [("iterations", C.c_int), ("stationarity", C.c_double), ("nll", C.c_double),
                 ("grid_min", C.c_double), ("trace_inconsistency", C.c_double),
-                ("floor_active", C.c_int)]
+                ("floor_active", C.c_int), ("passes", C.c_int), ("kernel_ms", C.c_double)]
 
 
 class SparsifyOpts(C.Structure):

@@ -968,19 +968,33 @@ static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double
   if (smem_launch > 227 * 1024)
     return fail(GGM_ERR_UNSUPPORTED, "sum(k)=%d too large for the solve kernel", T);
   const int nblk = solve_blocks(pts);
+  // CUDA events around the solve kernel(s) on the launch stream (info->kernel_ms)
+  cudaEvent_t ev[2];
+  GGM_CUDA_TRY(cudaEventCreate(&ev[0]));
+  GGM_CUDA_TRY(cudaEventCreate(&ev[1]));
+  GGM_CUDA_TRY(cudaEventRecord(ev[0], s));
   cudaError_t ce = launch_solve(sp, J, nblk, smem_launch, s);
   if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
   int hstat[4] = {0, 0, 0, 0};
   GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
   GGM_CUDA_TRY(cudaStreamSynchronize(s));
   int extra = 0;
+  int passes = hstat[3];
   if (!hstat[1] && sp.scheme == kSchemeSquarem) {  // accelerated run failed: plain MM
     extra = hstat[0];
     sp.scheme = kSchemeMM;
     ce = launch_solve(sp, J, nblk, smem_launch, s);
     if (ce != cudaSuccess) return fail(GGM_ERR_CUDA, "solve_kernel launch: %s", cudaGetErrorString(ce));
     GGM_CUDA_TRY(cudaMemcpyAsync(hstat, istat, sizeof(hstat), cudaMemcpyDeviceToHost, s));
+    GGM_CUDA_TRY(cudaStreamSynchronize(s));
+    passes += hstat[3];
   }
+  GGM_CUDA_TRY(cudaEventRecord(ev[1], s));
+  GGM_CUDA_TRY(cudaEventSynchronize(ev[1]));
+  float kms = 0.f;
+  GGM_CUDA_TRY(cudaEventElapsedTime(&kms, ev[0], ev[1]));
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
   // Σ log s of the result (grid invariant: gauge shifts do not change it)
   for (int m = 0; m < sp.M; ++m) logsum_kernel<<<num_sms() * 4, 256, 0, s>>>(sp.gd[m], lam_res, scal + 1);
   GGM_CUDA_TRY(cudaGetLastError());
@@ -1048,6 +1062,8 @@ static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double
     info->grid_min = gmin;
     info->floor_active = nfloor > 0 ? 1 : 0;
     info->trace_inconsistency = ti;
+    info->passes = passes;
+    info->kernel_ms = kms;
   }
   GGM_CUDA_TRY(cudaFreeAsync(buf.p, s));
   buf.p = nullptr;
