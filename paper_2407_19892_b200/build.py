@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-Xptxas", "-warn-spills"]
 
-SOURCES = ["ggm_api.cu", "sparse_precision.cu", "grid_solve.cu", "gram_eig.cu", "wald.cu"]
+SOURCES = ["ggm_api.cu", "sparse_precision.cu", "grid_solve.cu", "gram_eig.cu", "gram_tc.cu", "wald.cu"]
 HEADERS = ["ggm_internal.h", "ptx_sm100.cuh"]
 
 

@@ -21,6 +21,13 @@ void count_launches(int n);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// gram_tc.cu: G (dim x dim fp64, row-major upper = column-major lower) += Cᵀ C on the
+// tensor cores (fp32-accurate 3 x fp16 split); C = rows samples x dim, element (c, g) at
+// C[c·rs + g·cs].
+size_t gram_tc_workspace(int64_t max_rows, int64_t dim);
+ggm_status gram_tc_accumulate(const double* C, int64_t rows, int64_t dim, int64_t rs, int64_t cs,
+                              double* G, void* ws, cudaStream_t s);
+
 // Bump allocator over a caller-provided workspace (256-byte aligned slices).
 struct Carve {
   char* base;

@@ -950,11 +950,20 @@ struct CsrDense {
   int64_t dim, chunk;
   bool rows_side;  // Gram = A^T A (m x m) accumulated over row chunks (m <= d)
   int lwork;
+  bool tc;         // chunk Grams on the tensor cores (gram_tc.cu) instead of fp64 DSYRK
 };
+// Tensor-core chunk Grams (fp32-accurate 3 x fp16 products, fp64 across 4,096-sample slices)
+// for large Grams: d·m·min(d, m) >= 1e11 flops (PBMC scale: 6e12); below that the fp64
+// DSYRK costs milliseconds.  GGM_GRAM_TC=1 / 0 forces the choice (tests).
+static bool use_gram_tc(int64_t d, int64_t m) {
+  if (const char* e = getenv("GGM_GRAM_TC")) return e[0] == '1';
+  return (double)d * (double)m * (double)std::min(d, m) >= 1e11;
+}
 ggm_status csr_dense_plan(int64_t d, int64_t m, int k, CsrDense* cd) {
   cd->rows_side = m <= d;
   cd->dim = cd->rows_side ? m : d;
   cd->chunk = std::max<int64_t>(1, kChunkElems / (cd->rows_side ? m : d));
+  cd->tc = use_gram_tc(d, m);
   cusolverDnHandle_t h = g_handles.solver;
   if (!h && cusolverDnCreate(&g_handles.solver) != CUSOLVER_STATUS_SUCCESS)
     return fail(GGM_ERR_CUDA, "cusolverDnCreate failed");
@@ -968,6 +977,7 @@ ggm_status csr_dense_plan(int64_t d, int64_t m, int k, CsrDense* cd) {
 struct CsrDenseWork {
   double *G, *w, *work, *chunk, *V64, *Vasc, *Ek, *fro;
   int* info;
+  void* tcws;  // gram_tc operand (cd.tc)
 };
 size_t csr_dense_carve(int64_t d, int64_t m, int k, const CsrDense& cd, void* ws, CsrDenseWork* w) {
   Carve c(ws);
@@ -980,6 +990,7 @@ size_t csr_dense_carve(int64_t d, int64_t m, int k, const CsrDense& cd, void* ws
   w->Ek = c.take<double>(k);
   w->fro = c.take<double>(4);
   w->info = c.take<int>(4);
+  w->tcws = c.take<uint8_t>(cd.tc ? gram_tc_workspace(cd.chunk, cd.dim) : 0);
   return c.used();
 }
 
@@ -1029,18 +1040,29 @@ static ggm_status csr_gram_dense(int64_t d, int64_t m, int64_t nnz, const int64_
   const int dim = (int)cd.dim;
   // Gram of the shorter side over dense chunks
   const int64_t total = cd.rows_side ? d : m;
+  if (cd.tc) GGM_CUDA_TRY(cudaMemsetAsync(dw.G, 0, sizeof(double) * (size_t)dim * dim, s));
   for (int64_t c0 = 0; c0 < total; c0 += cd.chunk) {
     const int64_t c1 = std::min(total, c0 + cd.chunk);
     const double beta = c0 == 0 ? 0.0 : 1.0;
-    cublasStatus_t bs;
-    if (cd.rows_side) {  // chunk: (c1-c0) x m; G += chunk^T chunk
+    cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
+    if (cd.rows_side) {  // chunk: (c1-c0) x m column-major; G += chunk^T chunk
       csr_rows_dense<<<grid_of(32 * (c1 - c0)), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, c0, c1, m, dw.chunk);
-      bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, dim, (int)(c1 - c0), &one,
-                       dw.chunk, (int)(c1 - c0), &beta, dw.G, dim);
-    } else {             // chunk: d x (c1-c0); G += chunk chunk^T
+      if (cd.tc) {
+        st = gram_tc_accumulate(dw.chunk, c1 - c0, dim, 1, c1 - c0, dw.G, dw.tcws, s);
+        if (st != GGM_OK) return st;
+      } else {
+        bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, dim, (int)(c1 - c0), &one,
+                         dw.chunk, (int)(c1 - c0), &beta, dw.G, dim);
+      }
+    } else {             // chunk: d x (c1-c0) column-major; G += chunk chunk^T
       csr_cols_dense<<<grid_of(32 * d), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, d, c0, c1, dw.chunk);
-      bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, dim, (int)(c1 - c0), &one,
-                       dw.chunk, (int)d, &beta, dw.G, dim);
+      if (cd.tc) {
+        st = gram_tc_accumulate(dw.chunk, c1 - c0, dim, d, 1, dw.G, dw.tcws, s);
+        if (st != GGM_OK) return st;
+      } else {
+        bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, dim, (int)(c1 - c0), &one,
+                         dw.chunk, (int)d, &beta, dw.G, dim);
+      }
     }
     GGM_CUDA_TRY(cudaGetLastError());
     if (bs != CUBLAS_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cublasDsyrk failed (%d)", (int)bs);

@@ -54,10 +54,12 @@ def main():
             parts.append(thr)
         thr_all = torch.stack(parts).min(dim=0).values
         del parts
-        ncand = []
+        ncand, stages = [], []
+        G.set_timing(True)
         for r in range(N):
             ms, out = ev_ms(lambda: plans[r].run(VA, lA, thr_all=thr_all))
             runs.append(ms)
+            stages.append([round(x, 3) for x in G.last_timing()])
             key, val, counts, perm = out
             shards.append((key.clone(), val.clone(), list(counts), perm))
             ncand.append(int(sum(counts)))
@@ -94,7 +96,7 @@ def main():
         res[N] = {"axisA_seed_ms": seeds, "axisA_units_ms": runs, "axisA_merge_ms": merges,
                   "axisB_rows_ms": rowsB, "max_rank_compute_ms": comp,
                   "projected_comm_ms": comm, "projected_step_ms": comp + comm,
-                  "candidates_per_rank": ncand}
+                  "candidates_per_rank": ncand, "axisA_stages_prep_main_tail_ms": stages}
         print(json.dumps({"N": N, **res[N]}), flush=True)
     if 1 in res:
         t1 = res[1]["projected_step_ms"]
