@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ggm_internal.h"
 #include "ptx_sm100.cuh"
@@ -36,9 +37,9 @@ namespace gt {
 constexpr int kAtomBytes = 128 * 128;        // 128 rows x 64 fp16
 constexpr int kStages = 2;
 constexpr int kStageBytes = 6 * kAtomBytes;  // A hi | A lo | B hi (2 blocks) | B lo (2 blocks)
-constexpr int kSliceAtoms = 64;              // fp32 TMEM accumulation over 4,096 samples
 constexpr int kThreads = 192;
 constexpr int kTileN = 256;
+constexpr int kDefaultSliceAtoms = 16;
 
 struct Scal {
   unsigned int absmax_bits;
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(256) split_T(const double* __restrict__ C, int
 
 struct GtParams {
   const uint8_t* op;
+  int slice_atoms;   // fp32 TMEM accumulation over slice_atoms x 64 samples
   int natoms, nblk;  // atoms of this chunk; 128-column blocks (even)
   int ntiles, nslices;
   int64_t dim;
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc_kernel(const GtParams p) 
         const int slice = u / p.ntiles;
         int I, J2;
         tile_of(u % p.ntiles, p.nblk, I, J2);
-        const int a0 = slice * kSliceAtoms, a1 = min(p.natoms, a0 + kSliceAtoms);
+        const int a0 = slice * p.slice_atoms, a1 = min(p.natoms, a0 + p.slice_atoms);
         for (int a = a0; a < a1; ++a) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * kStageBytes;
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc_kernel(const GtParams p) 
     uint32_t phase = 0, tphase = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       const int slice = u / p.ntiles;
-      const int a0 = slice * kSliceAtoms, a1 = min(p.natoms, a0 + kSliceAtoms);
+      const int a0 = slice * p.slice_atoms, a1 = min(p.natoms, a0 + p.slice_atoms);
       mbar_wait(&tempty[buf], tphase ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)(buf * kTileN);
@@ -301,7 +303,12 @@ ggm_status gram_tc_accumulate(const double* C, int64_t rows, int64_t dim, int64_
   p.nblk = nblk;
   p.ntiles = 0;
   for (int I = 0; I < nblk; ++I) p.ntiles += nblk / 2 - I / 2;
-  p.nslices = (natoms + kSliceAtoms - 1) / kSliceAtoms;
+  static const int slice = [] {
+    const char* e = getenv("GGM_GRAM_TC_SLICE");  // A/B hook: atoms per fp32 slice
+    return e ? std::max(1, atoi(e)) : kDefaultSliceAtoms;
+  }();
+  p.slice_atoms = slice;
+  p.nslices = (natoms + slice - 1) / slice;
   p.dim = dim;
   p.G = G;
   p.sc = sc;

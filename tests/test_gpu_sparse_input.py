@@ -159,7 +159,9 @@ def test_gram_tc_multi_slice_vs_oracle_and_fp64(G, monkeypatch, shape, npn):
     """The tensor-core chunk Gram (gram_tc.cu) over several 4,096-sample slices, ragged
     sample counts (not multiples of 64) and Gram sides (not multiples of 128, odd block
     counts), both orientations (cells x genes and genes x cells): eigenvalues within 1e-5 of
-    the oracle (north_star), top eigenvectors aligned, and within 1e-6 of the fp64 DSYRK path;
+    the oracle (north_star), top eigenvectors aligned, and within 5e-6 of the fp64 DSYRK path
+    (the tensor cores' fp32 accumulation is biased ~1.6e-7 per K-step of a slice: 2.6e-6 at the
+    16-atom slices, tools/gram_tc_probe.py);
     the selected ψ of a top-10 graph built from the spectrum within the 1e-4 gate."""
     X = _sparse_counts(11 + shape[0], *shape, keep=0.2)
     rp, c, v = _csr(X)
@@ -170,7 +172,7 @@ def test_gram_tc_multi_slice_vs_oracle_and_fp64(G, monkeypatch, shape, npn):
     V0, E0, tr0, _, _ = G.ggm_gram_eig_csr(rp, c, v, shape[1], k, nonparanormal=npn)
     Vo, Eo = (O.gram_eig_nonparanormal(X, 0, k) if npn else O.gram_eig(X, 0, k))
     assert np.allclose(E1.cpu().numpy(), Eo, rtol=1e-5)
-    assert np.allclose(E1.cpu().numpy(), E0.cpu().numpy(), rtol=1e-6)
+    assert np.allclose(E1.cpu().numpy(), E0.cpu().numpy(), rtol=5e-6)   # fp32-slice bias, BK5c
     d = np.abs(np.sum(V1.cpu().numpy().astype(np.float64)[:, :4] * Vo[:, :4], axis=0))
     assert np.all(1.0 - d < 1e-4)
     # downstream: per-row top-10 of V diag(1/E) V^T from either spectrum (a stand-in for the
