@@ -27,6 +27,14 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 size_t gram_tc_workspace(int64_t max_rows, int64_t dim);
 ggm_status gram_tc_accumulate(const double* C, int64_t rows, int64_t dim, int64_t rs, int64_t cs,
                               double* G, void* ws, cudaStream_t s);
+ggm_status gram_tc_csr_scale(const int64_t* rp, const double* sval, int64_t nrows, void* ws,
+                             cudaStream_t s);
+ggm_status gram_tc_accumulate_csr(const int64_t* rp, const int32_t* col, const double* sval,
+                                  int64_t d, bool rows_side, int64_t r0, int64_t r1, int64_t dim,
+                                  double* G, void* ws, cudaStream_t s);
+ggm_status gram_tc_csr_rank1(const int64_t* rp, const int32_t* col, const double* sval,
+                             const double* z, int64_t d, bool rows_side, int64_t dim,
+                             int64_t ncols, double* G, double* scratch, cudaStream_t s);
 
 // Bump allocator over a caller-provided workspace (256-byte aligned slices).
 struct Carve {

@@ -1040,32 +1040,38 @@ static ggm_status csr_gram_dense(int64_t d, int64_t m, int64_t nnz, const int64_
   const int dim = (int)cd.dim;
   // Gram of the shorter side over dense chunks
   const int64_t total = cd.rows_side ? d : m;
-  if (cd.tc) GGM_CUDA_TRY(cudaMemsetAsync(dw.G, 0, sizeof(double) * (size_t)dim * dim, s));
+  if (cd.tc) {
+    GGM_CUDA_TRY(cudaMemsetAsync(dw.G, 0, sizeof(double) * (size_t)dim * dim, s));
+    st = gram_tc_csr_scale(row_ptr, cw.sval, d, dw.tcws, s);
+    if (st != GGM_OK) return st;
+  }
   for (int64_t c0 = 0; c0 < total; c0 += cd.chunk) {
     const int64_t c1 = std::min(total, c0 + cd.chunk);
     const double beta = c0 == 0 ? 0.0 : 1.0;
     cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
-    if (cd.rows_side) {  // chunk: (c1-c0) x m column-major; G += chunk^T chunk
+    if (cd.tc) {  // operand straight from the CSR (no dense chunk), tensor-core Gram
+      st = gram_tc_accumulate_csr(row_ptr, col, cw.sval, d, cd.rows_side, c0, c1, dim, dw.G,
+                                  dw.tcws, s);
+      if (st != GGM_OK) return st;
+    } else if (cd.rows_side) {  // chunk: (c1-c0) x m column-major; G += chunk^T chunk
       csr_rows_dense<<<grid_of(32 * (c1 - c0)), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, c0, c1, m, dw.chunk);
-      if (cd.tc) {
-        st = gram_tc_accumulate(dw.chunk, c1 - c0, dim, 1, c1 - c0, dw.G, dw.tcws, s);
-        if (st != GGM_OK) return st;
-      } else {
+      {
         bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, dim, (int)(c1 - c0), &one,
                          dw.chunk, (int)(c1 - c0), &beta, dw.G, dim);
       }
     } else {             // chunk: d x (c1-c0) column-major; G += chunk chunk^T
       csr_cols_dense<<<grid_of(32 * d), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, d, c0, c1, dw.chunk);
-      if (cd.tc) {
-        st = gram_tc_accumulate(dw.chunk, c1 - c0, dim, d, 1, dw.G, dw.tcws, s);
-        if (st != GGM_OK) return st;
-      } else {
+      {
         bs = cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, dim, (int)(c1 - c0), &one,
                          dw.chunk, (int)d, &beta, dw.G, dim);
       }
     }
     GGM_CUDA_TRY(cudaGetLastError());
     if (bs != CUBLAS_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cublasDsyrk failed (%d)", (int)bs);
+  }
+  if (cd.tc) {  // the exact rank-one terms of S + z 1^T (fp64; z = 0 for raw data)
+    st = gram_tc_csr_rank1(row_ptr, col, cw.sval, cw.z, d, cd.rows_side, dim, m, dw.G, dw.work, s);
+    if (st != GGM_OK) return st;
   }
   if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, dim, dw.G, dim, dw.w,
                        dw.work, cd.lwork, dw.info) != CUSOLVER_STATUS_SUCCESS)
@@ -1076,12 +1082,54 @@ static ggm_status csr_gram_dense(int64_t d, int64_t m, int64_t nnz, const int64_
     // V = A W_k diag(1/σ): rows chunk by chunk into Vasc (d x k, ascending order), then
     // reverse + scale
     const double* Zk = dw.G + (size_t)(dim - k) * dim;
-    for (int64_t r0 = 0; r0 < d; r0 += cd.chunk) {
-      const int64_t r1 = std::min(d, r0 + cd.chunk);
-      csr_rows_dense<<<grid_of(32 * (r1 - r0)), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, r0, r1, m, dw.chunk);
-      if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)(r1 - r0), k, dim, &one, dw.chunk,
-                      (int)(r1 - r0), Zk, dim, &zero, dw.Vasc + r0, (int)d) != CUBLAS_STATUS_SUCCESS)
-        return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+    if (nnz < INT32_MAX && d < INT32_MAX) {
+      // in the sparse rank-one form: A Z = S Z + z (1ᵀ Z) (cuSPARSE SpMM + one rank-one
+      // update, fp64; no dense chunks)
+      if (!g_sparse.h && cusparseCreate(&g_sparse.h) != CUSPARSE_STATUS_SUCCESS)
+        return fail(GGM_ERR_CUDA, "cusparseCreate failed");
+      cusparseSetStream(g_sparse.h, s);
+      rp_to_i32<<<grid_of(d + 1), 256, 0, s>>>(row_ptr, d + 1, cw.rp32);
+      GGM_CUDA_TRY(cudaGetLastError());
+      cusparseSpMatDescr_t A = nullptr;
+      cusparseDnMatDescr_t Bz = nullptr, Cv = nullptr;
+      if (cusparseCreateCsr(&A, d, m, nnz, cw.rp32, const_cast<int32_t*>(col), cw.sval,
+                            CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO,
+                            CUDA_R_64F) != CUSPARSE_STATUS_SUCCESS ||
+          cusparseCreateDnMat(&Bz, m, k, dim, const_cast<double*>(Zk), CUDA_R_64F,
+                              CUSPARSE_ORDER_COL) != CUSPARSE_STATUS_SUCCESS ||
+          cusparseCreateDnMat(&Cv, d, k, d, dw.Vasc, CUDA_R_64F, CUSPARSE_ORDER_COL) !=
+              CUSPARSE_STATUS_SUCCESS)
+        return fail(GGM_ERR_CUDA, "cuSPARSE descriptors failed");
+      size_t bb = 0;
+      cusparseSpMM_bufferSize(g_sparse.h, CUSPARSE_OPERATION_NON_TRANSPOSE,
+                              CUSPARSE_OPERATION_NON_TRANSPOSE, &one, A, Bz, &zero, Cv, CUDA_R_64F,
+                              CUSPARSE_SPMM_ALG_DEFAULT, &bb);
+      void* spbuf = nullptr;
+      GGM_CUDA_TRY(cudaMallocAsync(&spbuf, std::max<size_t>(bb, 256), s));
+      const cusparseStatus_t ss = cusparseSpMM(
+          g_sparse.h, CUSPARSE_OPERATION_NON_TRANSPOSE, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, A,
+          Bz, &zero, Cv, CUDA_R_64F, CUSPARSE_SPMM_ALG_DEFAULT, spbuf);
+      cusparseDestroySpMat(A);
+      cusparseDestroyDnMat(Bz);
+      cusparseDestroyDnMat(Cv);
+      GGM_CUDA_TRY(cudaFreeAsync(spbuf, s));
+      if (ss != CUSPARSE_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cusparseSpMM failed");
+      if (nonparanormal) {  // + z (1ᵀ Z): column sums of Z into the (now free) DSYEVD work
+        fill_f64<<<grid_of(m), 256, 0, s>>>(cw.ones, m, 1.0);
+        if (cublasDgemv(hb, CUBLAS_OP_T, (int)m, k, &one, Zk, dim, cw.ones, 1, &zero, dw.work,
+                        1) != CUBLAS_STATUS_SUCCESS ||
+            cublasDger(hb, (int)d, k, &one, cw.z, 1, dw.work, 1, dw.Vasc, (int)d) !=
+                CUBLAS_STATUS_SUCCESS)
+          return fail(GGM_ERR_CUDA, "rank-one projection term failed");
+      }
+    } else {
+      for (int64_t r0 = 0; r0 < d; r0 += cd.chunk) {
+        const int64_t r1 = std::min(d, r0 + cd.chunk);
+        csr_rows_dense<<<grid_of(32 * (r1 - r0)), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, r0, r1, m, dw.chunk);
+        if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)(r1 - r0), k, dim, &one, dw.chunk,
+                        (int)(r1 - r0), Zk, dim, &zero, dw.Vasc + r0, (int)d) != CUBLAS_STATUS_SUCCESS)
+          return fail(GGM_ERR_CUDA, "cublasDgemm failed");
+      }
     }
     reverse_scale<<<dim3(std::max<int64_t>(1, std::min<int64_t>((d + 255) / 256, 64)), k), 256, 0, s>>>(
         dw.w, dim, dw.Vasc, d, k, dw.Ek, dw.V64);

@@ -267,38 +267,129 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc_kernel(const GtParams p) 
   }
 }
 
+// ---------------------------------------------------------------- CSR operands (no dense chunk)
+// The unfolding is A = S + z 1ᵀ (S sparse on the data's pattern, z the value of a row's zeros:
+// 0 for raw data, the COCA image of 0 for the nonparanormal skeptic; the sparse rank-one form
+// of P:1003-1012).  The tensor cores form only the Gram of S (operand: zero fill + scatter of
+// the stored entries, straight from the CSR); the rank-one terms are added exactly in fp64
+// afterwards (gram_tc_csr_rank1) — they carry the large common offset of COCA data, whose
+// share of the fp32 accumulation bias would otherwise land on the small eigenvalues.
+// rows_side: samples = CSR rows [r0, r1), Gram side = the m CSR columns; else samples = CSR
+// columns [r0, r1), Gram side = the d CSR rows.
+__device__ __forceinline__ void split16(float x, __half& h, __half& l) {
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+}
+__device__ __forceinline__ size_t op_off(int64_t b, int64_t a, int r, int e, int natoms) {
+  return ((size_t)b * natoms + a) * 2 * kAtomBytes + (size_t)r * 128 +
+         (size_t)((((e >> 3) ^ (r & 7)) << 4) + ((e & 7) << 1));
+}
+
+__global__ void csr_absmax(const int64_t* __restrict__ rp, const double* __restrict__ sval,
+                           int64_t nrows, Scal* sc) {
+  float m = 0.f;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nrows;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t q = rp[i] + (threadIdx.x & 31); q < rp[i + 1]; q += 32)
+      m = fmaxf(m, (float)fabs(sval[q]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&sc->absmax_bits, __float_as_uint(m));
+}
+
+// scatter: one warp per CSR row; rows_side: CSR row = sample, col = Gram row; else CSR row =
+// Gram row, col = sample (only columns in [r0, r1), columns ascending within a row)
+__global__ void csr_scatter(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const double* __restrict__ sval, bool rows_side, int64_t r0, int64_t r1, int64_t nrows, int natoms,
+                            const Scal* __restrict__ sc, uint8_t* __restrict__ op) {
+  const double s = ldexp(1.0, sc->exp2);
+  const int lane = threadIdx.x & 31;
+  const int64_t ibeg = rows_side ? r0 : 0, iend = rows_side ? r1 : nrows;
+  for (int64_t i = ibeg + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < iend;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t lo = rp[i];
+    const int64_t hi = rp[i + 1];
+    if (!rows_side) {  // first stored entry with col >= r0
+      int64_t a0 = lo, b0 = hi;
+      while (a0 < b0) {
+        const int64_t mid = (a0 + b0) >> 1;
+        if (col[mid] < r0) a0 = mid + 1; else b0 = mid;
+      }
+      lo = a0;
+    }
+    for (int64_t q = lo + lane; q < hi; q += 32) {
+      const int64_t c = col[q];
+      if (!rows_side && c >= r1) break;
+      const int64_t smp = rows_side ? i - r0 : c - r0;  // sample index within the chunk
+      const int64_t g = rows_side ? c : i;              // Gram-side index
+      __half h, l;
+      split16((float)(sval[q] * s), h, l);
+      const size_t off = op_off(g >> 7, smp >> 6, (int)(g & 127), (int)(smp & 63), natoms);
+      *reinterpret_cast<__half*>(op + off) = h;
+      *reinterpret_cast<__half*>(op + kAtomBytes + off) = l;
+    }
+  }
+}
+
+// rank-one terms: rows_side (A = S + z 1ᵀ, rows = samples): AᵀA = SᵀS + u1ᵀ + 1uᵀ + (zᵀz)11ᵀ,
+// u = Sᵀz; else (rows = Gram side): AAᵀ = SSᵀ + r zᵀ + z rᵀ + n zzᵀ, r = S1, n = #columns.
+__global__ void rank1_vec(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                          const double* __restrict__ sval, const double* __restrict__ z,
+                          int64_t d, bool rows_side, double* __restrict__ u, double* __restrict__ zz) {
+  const int lane = threadIdx.x & 31;
+  double zacc = 0.0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < d;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double zi = z[i];
+    if (lane == 0) zacc += zi * zi;
+    double rs = 0.0;
+    for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) {
+      if (rows_side)
+        atomicAdd(&u[col[q]], sval[q] * zi);
+      else
+        rs += sval[q];
+    }
+    if (!rows_side) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+      if (lane == 0) u[i] = rs;
+    }
+  }
+  if (lane == 0) atomicAdd(zz, zacc);
+}
+__global__ void rank1_apply(double* __restrict__ G, int64_t dim, const double* __restrict__ u,
+                            const double* __restrict__ z, const double* __restrict__ zz,
+                            bool rows_side, double ncols) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < dim * dim;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / dim, j = t - i * dim;
+    if (j < i) continue;  // row-major upper triangle (column-major lower)
+    G[t] += rows_side ? u[i] + u[j] + *zz : u[i] * z[j] + z[i] * u[j] + ncols * z[i] * z[j];
+  }
+}
+
 }  // namespace gt
 
-// Workspace bytes of gram_tc_accumulate for chunks of up to max_rows samples.
-size_t gram_tc_workspace(int64_t max_rows, int64_t dim) {
+namespace {
+size_t tc_ws(int64_t max_rows, int64_t dim) {
   const int64_t natoms = (max_rows + 63) / 64;
   int64_t nblk = (dim + 127) / 128;
   nblk += nblk & 1;
   return align_up(sizeof(gt::Scal), 256) + (size_t)nblk * natoms * 2 * gt::kAtomBytes + 1024;
 }
-
-// G (dim x dim, fp64, row-major upper triangle) += Cᵀ C for the chunk C (rows samples x dim
-// columns, element (c, g) at C[c·rs + g·cs], one dense block of rows·dim doubles) on `s`.
-// ws: gram_tc_workspace(rows, dim) bytes.
-ggm_status gram_tc_accumulate(const double* C, int64_t rows, int64_t dim, int64_t rs, int64_t cs,
-                              double* G, void* ws, cudaStream_t s) {
+uint8_t* tc_op(void* ws) {
+  uint8_t* op = static_cast<uint8_t*>(ws) + align_up(sizeof(gt::Scal), 256);
+  return op + ((1024u - (reinterpret_cast<uintptr_t>(op) & 1023u)) & 1023u);
+}
+// the Gram kernel over an operand of `rows` samples already in ws
+ggm_status tc_run(int64_t rows, int64_t dim, double* G, void* ws, cudaStream_t s) {
   using namespace gt;
-  if (rows <= 0) return GGM_OK;
-  Scal* sc = static_cast<Scal*>(ws);
-  uint8_t* op = static_cast<uint8_t*>(ws) + align_up(sizeof(Scal), 256);
-  op += (1024u - (reinterpret_cast<uintptr_t>(op) & 1023u)) & 1023u;
   const int natoms = (int)((rows + 63) / 64);
   int nblk = (int)((dim + 127) / 128);
   nblk += nblk & 1;
-  const int sms = num_sms();
-  GGM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(Scal), s));
-  chunk_absmax<<<(int)std::min<int64_t>((rows * dim + 255) / 256, sms * 8), 256, 0, s>>>(
-      C, rows * dim, sc);
-  chunk_scale<<<1, 1, 0, s>>>(sc);
-  split_T<<<dim3(natoms, nblk), 256, 0, s>>>(C, rows, dim, rs, cs, natoms, sc, op);
-  GGM_CUDA_TRY(cudaGetLastError());
   GtParams p;
-  p.op = op;
+  p.op = tc_op(ws);
   p.natoms = natoms;
   p.nblk = nblk;
   p.ntiles = 0;
@@ -311,7 +402,7 @@ ggm_status gram_tc_accumulate(const double* C, int64_t rows, int64_t dim, int64_
   p.nslices = (natoms + slice - 1) / slice;
   p.dim = dim;
   p.G = G;
-  p.sc = sc;
+  p.sc = static_cast<const Scal*>(ws);
   const size_t smem = (size_t)kStages * kStageBytes + 1024 + 256;
   static bool attr = false;
   if (!attr) {
@@ -320,9 +411,91 @@ ggm_status gram_tc_accumulate(const double* C, int64_t rows, int64_t dim, int64_
     attr = true;
   }
   const int units = p.ntiles * p.nslices;
-  gram_tc_kernel<<<std::max(1, std::min(units, sms)), kThreads, smem, s>>>(p);
+  gram_tc_kernel<<<std::max(1, std::min(units, num_sms())), kThreads, smem, s>>>(p);
+  GGM_CUDA_TRY(cudaGetLastError());
+  return GGM_OK;
+}
+}  // namespace
+
+// Workspace bytes of gram_tc_accumulate / gram_tc_accumulate_csr for chunks of up to
+// max_rows samples.
+size_t gram_tc_workspace(int64_t max_rows, int64_t dim) { return tc_ws(max_rows, dim); }
+
+// G (dim x dim, fp64, row-major upper triangle) += Cᵀ C for the chunk C (rows samples x dim
+// columns, element (c, g) at C[c·rs + g·cs], one dense block of rows·dim doubles) on `s`.
+// ws: gram_tc_workspace(rows, dim) bytes.
+ggm_status gram_tc_accumulate(const double* C, int64_t rows, int64_t dim, int64_t rs, int64_t cs,
+                              double* G, void* ws, cudaStream_t s) {
+  using namespace gt;
+  if (rows <= 0) return GGM_OK;
+  Scal* sc = static_cast<Scal*>(ws);
+  const int natoms = (int)((rows + 63) / 64);
+  int nblk = (int)((dim + 127) / 128);
+  nblk += nblk & 1;
+  const int sms = num_sms();
+  GGM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(Scal), s));
+  chunk_absmax<<<(int)std::min<int64_t>((rows * dim + 255) / 256, sms * 8), 256, 0, s>>>(
+      C, rows * dim, sc);
+  chunk_scale<<<1, 1, 0, s>>>(sc);
+  split_T<<<dim3(natoms, nblk), 256, 0, s>>>(C, rows, dim, rs, cs, natoms, sc, tc_op(ws));
   GGM_CUDA_TRY(cudaGetLastError());
   count_launches(4);
+  return tc_run(rows, dim, G, ws, s);
+}
+
+// The scale of a whole CSR unfolding (values sval + z at stored entries, z elsewhere), once
+// per call before the chunk loop of gram_tc_accumulate_csr.
+ggm_status gram_tc_csr_scale(const int64_t* rp, const double* sval, int64_t nrows, void* ws,
+                             cudaStream_t s) {
+  using namespace gt;
+  Scal* sc = static_cast<Scal*>(ws);
+  GGM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(Scal), s));
+  csr_absmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((nrows * 32 + 255) / 256, num_sms() * 8)),
+               256, 0, s>>>(rp, sval, nrows, sc);
+  chunk_scale<<<1, 1, 0, s>>>(sc);
+  GGM_CUDA_TRY(cudaGetLastError());
+  count_launches(2);
+  return GGM_OK;
+}
+
+// G += Cᵀ C for the samples [r0, r1) of a CSR unfolding (d rows, values sval + z, zeros z),
+// operand written straight from the CSR (no dense chunk).  rows_side: samples = rows, the
+// Gram side = the dim = m columns; else samples = columns, the Gram side = the dim = d rows.
+ggm_status gram_tc_accumulate_csr(const int64_t* rp, const int32_t* col, const double* sval,
+                                  int64_t d, bool rows_side, int64_t r0, int64_t r1, int64_t dim,
+                                  double* G, void* ws, cudaStream_t s) {
+  using namespace gt;
+  const int64_t rows = r1 - r0;
+  if (rows <= 0) return GGM_OK;
+  const int natoms = (int)((rows + 63) / 64);
+  int nblk = (int)((dim + 127) / 128);
+  nblk += nblk & 1;
+  const int sms = num_sms();
+  const Scal* sc = static_cast<const Scal*>(ws);
+  uint8_t* op = tc_op(ws);
+  GGM_CUDA_TRY(cudaMemsetAsync(op, 0, (size_t)nblk * natoms * 2 * kAtomBytes, s));
+  const int64_t nr = rows_side ? rows : d;
+  csr_scatter<<<(int)std::max<int64_t>(1, std::min<int64_t>((nr * 32 + 255) / 256, sms * 16)), 256, 0,
+                s>>>(rp, col, sval, rows_side, r0, r1, d, natoms, sc, op);
+  GGM_CUDA_TRY(cudaGetLastError());
+  count_launches(3);
+  return tc_run(rows, dim, G, ws, s);
+}
+
+// After the chunk loop: the exact rank-one terms of A = S + z 1ᵀ (fp64).  scratch: dim + 1
+// doubles.  ncols: the number of CSR columns (samples) when !rows_side.
+ggm_status gram_tc_csr_rank1(const int64_t* rp, const int32_t* col, const double* sval,
+                             const double* z, int64_t d, bool rows_side, int64_t dim,
+                             int64_t ncols, double* G, double* scratch, cudaStream_t s) {
+  using namespace gt;
+  const int sms = num_sms();
+  GGM_CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(double) * (dim + 1), s));
+  rank1_vec<<<(int)std::max<int64_t>(1, std::min<int64_t>((d * 32 + 255) / 256, sms * 16)), 256, 0,
+              s>>>(rp, col, sval, z, d, rows_side, scratch, scratch + dim);
+  rank1_apply<<<(int)std::max<int64_t>(1, std::min<int64_t>((dim * dim + 255) / 256, sms * 16)), 256, 0,
+                s>>>(G, dim, scratch, z, scratch + dim, rows_side, (double)ncols);
+  GGM_CUDA_TRY(cudaGetLastError());
+  count_launches(2);
   return GGM_OK;
 }
 
