@@ -386,17 +386,35 @@ def sparse_spectrum_timing(G, torch):
     rp, col, val = torch.cat(rps), torch.cat(cols), torch.cat(vals)
     del rps, cols, vals
     out = {"shape": [d, m], "nnz": int(val.numel()), "k": 50,
-           "method": "exact Gram of the 2,200 side over 1 GiB dense chunks (fp64 DSYRK) + "
-                     "DSYEVD; COCA as S + z 1^T (P:1003-1012)"}
+           "method": "exact Gram of the 2,200 side: tensor-core chunk Grams (gram_tc.cu, "
+                     "3 x fp16 split, fp32 over 4,096-sample slices, fp64 across) of S from "
+                     "the CSR + exact fp64 rank-one terms of S + z 1^T (COCA, P:1003-1012) + "
+                     "DSYEVD; the long side by a CSR row projection"}
+    peaks, _ = _peaks()
+    gram_flops = float(d) * m * m   # the symmetric half of 2 d m^2 (algorithmic)
 
     def run(tag, rp_, col_, val_, mm):
         for npn in (False, True):
             G.ggm_gram_eig_csr(rp_, col_, val_, mm, 50, nonparanormal=npn)  # warm-up
             torch.cuda.synchronize()
+            G.set_timing(True)
             t0 = time.perf_counter()
             G.ggm_gram_eig_csr(rp_, col_, val_, mm, 50, nonparanormal=npn)
             torch.cuda.synchronize()
-            out[f"{tag}_{'coca' if npn else 'raw'}_ms"] = (time.perf_counter() - t0) * 1e3
+            key = f"{tag}_{'coca' if npn else 'raw'}"
+            out[key + "_ms"] = (time.perf_counter() - t0) * 1e3
+            gms, ems, pms = G.last_timing()
+            out[key + "_stages_ms"] = {"gram": gms, "eigensolve": ems, "projection_store": pms}
+            if npn is False and tag == "cell_axis":
+                peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
+                ach = gram_flops / (gms * 1e-3) / 1e12
+                out["roofline_gram"] = {
+                    "bound": "tensor", "kernel": "gram_tc (scatter + tcgen05 Gram + fp64 red)",
+                    "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None,
+                    "basis": "d m^2 flops (symmetric half of the 1,248,980 x 2,200 Gram) / "
+                             "CUDA-event time of the Gram stage incl. the CSR scatter; peak: "
+                             "bf16 sustained / 3 (3-term fp16 split)"}
 
     run("cell_axis", rp, col, val, m)
     # gene axis: the same matrix as gene-major CSR (2,200 rows of 1,248,980 cells)

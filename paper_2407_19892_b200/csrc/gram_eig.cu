@@ -946,6 +946,47 @@ __global__ void csr_cols_dense(const int64_t* __restrict__ rp, const int32_t* __
   }
 }
 
+// Z (m x k column-major, leading dimension ld) -> row-major m x k
+__global__ void transpose_cm(const double* __restrict__ Z, int64_t ld, int64_t m, int k,
+                             double* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * k;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / k;
+    const int j = (int)(t - g * k);
+    out[t] = Z[g + (int64_t)j * ld];
+  }
+}
+// column sums of Z (m x k column-major): one warp per column
+__global__ void colsum_cm(const double* __restrict__ Z, int64_t ld, int64_t m, int k,
+                          double* __restrict__ out) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= k) return;
+  double acc = 0.0;
+  for (int64_t g = threadIdx.x & 31; g < m; g += 32) acc += Z[g + (int64_t)j * ld];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) out[j] = acc;
+}
+// V[i, :] = Σ_q sval[q] W[col[q], :] (+ z_i colsum) for every CSR row i; V column-major d x k,
+// W row-major m x k.  One warp per row, lanes over the k columns.
+__global__ void csr_project_rows(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 const double* __restrict__ sval, const double* __restrict__ z,
+                                 int64_t d, int k, const double* __restrict__ W,
+                                 const double* __restrict__ colsum, double* __restrict__ V) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < d;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = rp[i], e = rp[i + 1];
+    for (int j0 = 0; j0 < k; j0 += 32) {
+      const int j = j0 + lane;
+      double acc = 0.0;
+      if (j < k)
+        for (int64_t q = b; q < e; ++q) acc += sval[q] * W[(int64_t)col[q] * k + j];
+      if (j < k) V[i + (int64_t)j * d] = colsum ? acc + z[i] * colsum[j] : acc;
+    }
+  }
+}
+
 struct CsrDense {
   int64_t dim, chunk;
   bool rows_side;  // Gram = A^T A (m x m) accumulated over row chunks (m <= d)
@@ -1040,6 +1081,13 @@ static ggm_status csr_gram_dense(int64_t d, int64_t m, int64_t nnz, const int64_
   const int dim = (int)cd.dim;
   // Gram of the shorter side over dense chunks
   const int64_t total = cd.rows_side ? d : m;
+  // stage times when ggm_set_timing(1): Gram (incl. the operand scatter), eigensolve,
+  // projection + store (ggm_last_timing slots 0, 1, 2)
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  const bool timed = timing_enabled();
+  if (timed)
+    for (auto& e : tev) cudaEventCreate(&e);
+  if (timed) cudaEventRecord(tev[0], s);
   if (cd.tc) {
     GGM_CUDA_TRY(cudaMemsetAsync(dw.G, 0, sizeof(double) * (size_t)dim * dim, s));
     st = gram_tc_csr_scale(row_ptr, cw.sval, d, dw.tcws, s);
@@ -1073,55 +1121,26 @@ static ggm_status csr_gram_dense(int64_t d, int64_t m, int64_t nnz, const int64_
     st = gram_tc_csr_rank1(row_ptr, col, cw.sval, cw.z, d, cd.rows_side, dim, m, dw.G, dw.work, s);
     if (st != GGM_OK) return st;
   }
+  if (timed) cudaEventRecord(tev[1], s);
   if (cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, dim, dw.G, dim, dw.w,
                        dw.work, cd.lwork, dw.info) != CUSOLVER_STATUS_SUCCESS)
     return fail(GGM_ERR_CUDA, "cusolverDnDsyevd failed");
+  if (timed) cudaEventRecord(tev[2], s);
   if (!cd.rows_side) {
     take_topk<<<k, 256, 0, s>>>(dw.w, dw.G, dim, k, dw.Ek, dw.V64);
   } else {
     // V = A W_k diag(1/σ): rows chunk by chunk into Vasc (d x k, ascending order), then
     // reverse + scale
     const double* Zk = dw.G + (size_t)(dim - k) * dim;
-    if (nnz < INT32_MAX && d < INT32_MAX) {
-      // in the sparse rank-one form: A Z = S Z + z (1ᵀ Z) (cuSPARSE SpMM + one rank-one
-      // update, fp64; no dense chunks)
-      if (!g_sparse.h && cusparseCreate(&g_sparse.h) != CUSPARSE_STATUS_SUCCESS)
-        return fail(GGM_ERR_CUDA, "cusparseCreate failed");
-      cusparseSetStream(g_sparse.h, s);
-      rp_to_i32<<<grid_of(d + 1), 256, 0, s>>>(row_ptr, d + 1, cw.rp32);
+    if (k <= 1024) {
+      // in the sparse rank-one form: A Z = S Z + z (1ᵀ Z), one warp per row over its stored
+      // entries (Z transposed to row-major first; fp64; no dense chunks)
+      transpose_cm<<<grid_of((int64_t)m * k), 256, 0, s>>>(Zk, dim, m, k, dw.work);
+      if (nonparanormal) colsum_cm<<<(k + 7) / 8, 256, 0, s>>>(Zk, dim, m, k, dw.work + (size_t)m * k);
+      csr_project_rows<<<grid_of(32 * d), 256, 0, s>>>(row_ptr, col, cw.sval, cw.z, d, k, dw.work,
+                                                       nonparanormal ? dw.work + (size_t)m * k : nullptr,
+                                                       dw.Vasc);
       GGM_CUDA_TRY(cudaGetLastError());
-      cusparseSpMatDescr_t A = nullptr;
-      cusparseDnMatDescr_t Bz = nullptr, Cv = nullptr;
-      if (cusparseCreateCsr(&A, d, m, nnz, cw.rp32, const_cast<int32_t*>(col), cw.sval,
-                            CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO,
-                            CUDA_R_64F) != CUSPARSE_STATUS_SUCCESS ||
-          cusparseCreateDnMat(&Bz, m, k, dim, const_cast<double*>(Zk), CUDA_R_64F,
-                              CUSPARSE_ORDER_COL) != CUSPARSE_STATUS_SUCCESS ||
-          cusparseCreateDnMat(&Cv, d, k, d, dw.Vasc, CUDA_R_64F, CUSPARSE_ORDER_COL) !=
-              CUSPARSE_STATUS_SUCCESS)
-        return fail(GGM_ERR_CUDA, "cuSPARSE descriptors failed");
-      size_t bb = 0;
-      cusparseSpMM_bufferSize(g_sparse.h, CUSPARSE_OPERATION_NON_TRANSPOSE,
-                              CUSPARSE_OPERATION_NON_TRANSPOSE, &one, A, Bz, &zero, Cv, CUDA_R_64F,
-                              CUSPARSE_SPMM_ALG_DEFAULT, &bb);
-      void* spbuf = nullptr;
-      GGM_CUDA_TRY(cudaMallocAsync(&spbuf, std::max<size_t>(bb, 256), s));
-      const cusparseStatus_t ss = cusparseSpMM(
-          g_sparse.h, CUSPARSE_OPERATION_NON_TRANSPOSE, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, A,
-          Bz, &zero, Cv, CUDA_R_64F, CUSPARSE_SPMM_ALG_DEFAULT, spbuf);
-      cusparseDestroySpMat(A);
-      cusparseDestroyDnMat(Bz);
-      cusparseDestroyDnMat(Cv);
-      GGM_CUDA_TRY(cudaFreeAsync(spbuf, s));
-      if (ss != CUSPARSE_STATUS_SUCCESS) return fail(GGM_ERR_CUDA, "cusparseSpMM failed");
-      if (nonparanormal) {  // + z (1ᵀ Z): column sums of Z into the (now free) DSYEVD work
-        fill_f64<<<grid_of(m), 256, 0, s>>>(cw.ones, m, 1.0);
-        if (cublasDgemv(hb, CUBLAS_OP_T, (int)m, k, &one, Zk, dim, cw.ones, 1, &zero, dw.work,
-                        1) != CUBLAS_STATUS_SUCCESS ||
-            cublasDger(hb, (int)d, k, &one, cw.z, 1, dw.work, 1, dw.Vasc, (int)d) !=
-                CUBLAS_STATUS_SUCCESS)
-          return fail(GGM_ERR_CUDA, "rank-one projection term failed");
-      }
     } else {
       for (int64_t r0 = 0; r0 < d; r0 += cd.chunk) {
         const int64_t r1 = std::min(d, r0 + cd.chunk);
@@ -1137,6 +1156,16 @@ static ggm_status csr_gram_dense(int64_t d, int64_t m, int64_t nnz, const int64_
   GGM_CUDA_TRY(cudaGetLastError());
   sign_and_store<<<k, 256, 0, s>>>(dw.V64, d, k, V);
   GGM_CUDA_TRY(cudaGetLastError());
+  if (timed) {
+    cudaEventRecord(tev[3], s);
+    cudaEventSynchronize(tev[3]);
+    for (int q = 0; q < 3; ++q) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[q], tev[q + 1]);
+      record_timing(q, ms);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
   GGM_CUDA_TRY(cudaMemcpyAsync(E, dw.Ek, sizeof(double) * k, cudaMemcpyDeviceToDevice, s));
   std::vector<double> hE(k);
   int hinfo = 0;
