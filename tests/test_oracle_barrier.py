@@ -172,3 +172,46 @@ def test_gauge1_multi_modal_reduces():
     b, _ = O.solve_eigvals_multi(E, [[0, 1, 2]], gauge=1)
     for x, y in zip(a, b):
         np.testing.assert_allclose(x, y, rtol=1e-10)
+
+
+# ------------------------------------------------------- helpers pinned directly
+
+def test_marginals_sq2d_brute_force_and_hessian():
+    """marginals_sq2d (the Newton oracle's Hessian blocks): the 1-D and 2-D marginals of
+    1/s² equal explicit loops over the grid, and ½ of them is the finite-difference Jacobian
+    of the gradient ½(E − g) (∂g_li/∂λ_mj = −Σ 1/s² over the grid points with j_l=i, j_m=j)."""
+    rng = np.random.default_rng(3)
+    lams = [rng.uniform(0.3, 2.0, k) for k in (3, 4, 2)]
+    diag, pair = O.marginals_sq2d(lams)
+    for a in range(3):
+        for i in range(len(lams[a])):
+            want = 0.0
+            for j0 in range(3):
+                for j1 in range(4):
+                    for j2 in range(2):
+                        idx = (j0, j1, j2)
+                        if idx[a] != i:
+                            continue
+                        want += 1.0 / (lams[0][j0] + lams[1][j1] + lams[2][j2]) ** 2
+            assert diag[a][i] == pytest.approx(want, rel=1e-13)
+    E = [rng.uniform(1, 2, len(l)) for l in lams]
+    h = 1e-6
+    for (a, b), M in pair.items():
+        for i in range(len(lams[a])):
+            for j in range(len(lams[b])):
+                lp = [l.copy() for l in lams]
+                lm = [l.copy() for l in lams]
+                lp[b][j] += h
+                lm[b][j] -= h
+                dg = (O.gradient(E, lp)[a][i] - O.gradient(E, lm)[a][i]) / (2 * h)
+                assert dg == pytest.approx(0.5 * M[i, j], rel=1e-6)
+
+
+def test_trace_inconsistency_closed_forms():
+    """trace_inconsistency = max_l |tr E_l − mean| / mean (reading T): equal traces → 0;
+    traces (6, 1.5) → mean 3.75, max deviation 2.25 → 0.6; the multi-modal form with one
+    modality is the same number."""
+    assert O.trace_inconsistency([np.array([1.0, 2.0]), np.array([3.0])]) == 0.0
+    E = [np.array([3.0, 2.0, 1.0]), np.array([1.0, 0.5])]
+    assert O.trace_inconsistency(E) == pytest.approx(0.6, rel=1e-15)
+    assert O.trace_inconsistency_multi(E, [[0, 1]]) == pytest.approx(0.6, rel=1e-12)

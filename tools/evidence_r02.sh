@@ -1,0 +1,19 @@
+# Round-2 evidence (one gpurun session): bench lines (C5 default, C4), launch list of the C5
+# step, full captures of BK2 (C5 axis A main launch and C4 main launch), BK4 (C3 solve) and
+# the tensor-core Gram (one PBMC-scale chunk launch).
+set -u
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/r02_smi.txt
+timeout 900 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err; echo "bench rc=$?"
+timeout 600 python bench.py --config C4 --no-stages > gpurun_out/r02_bench_c4.json 2> gpurun_out/r02_bench_c4.err; echo "bench C4 rc=$?"
+B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-stages"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/r02_launches.csv $B > gpurun_out/r02_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fused_recon_topk \
+  --launch-skip 1 --launch-count 1 -o gpurun_out/r02_bk2 $B > gpurun_out/r02_ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_recon_topk \
+  --launch-skip 1 --launch-count 1 -o gpurun_out/r02_bk2_c4 $B --config C4 > gpurun_out/r02_ncu_c4.log 2>&1; echo "ncu C4 rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:solve_kernel -c 1 \
+  -o gpurun_out/r02_bk4 python tools/solve_probe.py --ncu > gpurun_out/r02_ncu_bk4.log 2>&1; echo "ncu bk4 rc=$?"
+timeout 900 ncu --set full --clock-control none -k regex:gram_tc_kernel -c 1 \
+  -o gpurun_out/r02_gramtc python tools/pbmc_probe.py > gpurun_out/r02_ncu_gramtc.log 2>&1; echo "ncu gram_tc rc=$?"
