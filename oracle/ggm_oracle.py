@@ -22,7 +22,11 @@ Pinning (tests/test_oracle_pins.py, ``-m "not gpu"``):
                             sets); KKT conditions on truncated tensors; SciPy L-BFGS-B on
                             the box and the clamped majorise-minimise iteration reach the
                             same grid / λ (tests/test_oracle_barrier.py)
-  canonical gauge           grid invariance; PSD; closed form on shifted inputs
+  marginals_sq2d            explicit grid loops; ½ of it = finite-difference Jacobian of the
+                            gradient (the Newton Hessian blocks)
+  trace_inconsistency       closed forms (equal traces → 0; (6, 1.5) → 0.6), = the
+                            multi-modal form for one modality
+  canonical gauge          grid invariance; PSD; closed form on shifted inputs
   psi_rows / top_t / thr    dense V diag(λ) V^T + brute-force sort on tiny inputs;
                             rank-1 closed form; identity-factor all-tie case
   nonparanormal (COCA)      the paper's worked example (ranks, Φ^-1 values, sparse part
