@@ -659,12 +659,28 @@ __device__ __forceinline__ float max32_abs(const float (&v)[32]) {
 
 // Column sums of |v| over the warp's 32 rows for its 32 columns (reduce-scatter transpose:
 // 31 shuffles); lane L returns the sum of column L.  Masked entries (bit e of ex) count 0.
+// The absolute values are folded into the first stage's adds (FADD |a| + |b|), and the
+// masking select runs only for lanes with masked entries (diagonal / padding tiles).
 __device__ __forceinline__ float col_abs_sums32(const uint32_t (&vr)[32], uint32_t ex, int lane) {
-  float a[32];
+  float v[32];
 #pragma unroll
-  for (int e = 0; e < 32; ++e) a[e] = ((ex >> e) & 1u) ? 0.f : fabsf(__uint_as_float(vr[e]));
+  for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(vr[e]);
+  if (ex != 0u) {
 #pragma unroll
-  for (int st = 16; st >= 1; st >>= 1) {
+    for (int e = 0; e < 32; ++e) v[e] = ((ex >> e) & 1u) ? 0.f : v[e];
+  }
+  float a[16];
+  {
+    const bool up = (lane & 16) != 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float keep = up ? v[e + 16] : v[e];
+      const float send = up ? v[e] : v[e + 16];
+      a[e] = fabsf(keep) + fabsf(__shfl_xor_sync(0xffffffffu, send, 16));
+    }
+  }
+#pragma unroll
+  for (int st = 8; st >= 1; st >>= 1) {
     const bool up = (lane & st) != 0;
 #pragma unroll
     for (int e = 0; e < st; ++e) {
