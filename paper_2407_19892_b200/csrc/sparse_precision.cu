@@ -99,6 +99,7 @@ struct DevScalars {
   unsigned int rn_max_bits;       // kSym: float bits of max_i ||U_i||
 };
 constexpr int kCandChunk = 4096;
+constexpr int kWindowSplit = 4;  // kSym/kSymList CTA-pair units per row block (sub-windows)
 constexpr int64_t kSymAutoN = 16384;  // automatic symmetric scheme from this axis length (measured crossover 8192-16384)  // candidate-pool reservation granularity (entries)
 
 // ------------------------------------------------------------------ BK1a
@@ -421,6 +422,9 @@ struct FusedParams {
   int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
   int screen;        // kSym: hi*hi screening MMAs only (candidates re-evaluated exactly)
   int pair;          // CTA-pair kernel (host-side selection; the kernel's template PAIR)
+  int wsplit;            // kSym / kSymList CTA pairs: each row block's window is cut into
+                         // wsplit consecutive sub-windows, one unit each (unit u: sub-window
+                         // u / NB of row block u % NB) — finer units balance the last wave
   int unit_step;         // units unit_lo, unit_lo + unit_step, ... < unit_hi (1: contiguous;
                          // nranks: the rank-strided share of the distributed symmetric scheme)
   int unit_lo, unit_hi;  // units processed by this launch (a rank's share in the sharded
@@ -478,7 +482,11 @@ __device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& ub) 
   ub = u;
   if (KIND == kSeed) return p.SS;  // the sample: the first SS column tiles
   // kSym: window over p.NB blocks (128-column blocks, or 256-column super blocks for pairs)
-  return PAIR ? sym_window(ub, p.NB) : (sym_window(ub, p.NB) + 1) / 2;
+  if (!PAIR) return (sym_window(ub, p.NB) + 1) / 2;
+  const int part = u / p.NB;
+  ub = u - part * p.NB;
+  const int W = sym_window(ub, p.NB);
+  return (part + 1) * W / p.wsplit - part * W / p.wsplit;
 }
 // Visit the kSym window [ub, ub + W) starting at X = the last unit of this wave (all CTAs of
 // a wave contain X in their windows), so concurrently running CTAs stream the same column
@@ -490,10 +498,10 @@ __host__ __device__ __forceinline__ int unit_of(const FusedParams& p, int uj) {
   return p.unit_lo + uj * p.unit_step;
 }
 __device__ __forceinline__ int sym_start(const FusedParams& p, int uj, int ub, int u0, int ustep,
-                                         int W) {
-  const int X = unit_of(p, min(unit_count(p) - 1, uj - u0 + ustep - 1));
+                                         int w0, int w1) {
+  const int X = unit_of(p, min(unit_count(p) - 1, uj - u0 + ustep - 1)) % p.NB;
   const int delta = (X - ub + p.NB) % p.NB;
-  return delta >= W ? 0 : delta;
+  return (delta >= w0 && delta < w1) ? delta : w0;
 }
 // Incremental enumeration (no integer division per tile).
 template <int KIND, bool PAIR>
@@ -501,6 +509,7 @@ struct TileIter {
   int K0, K1;
   bool h1;
   int s, ub, W, o;  // kSym: o = window offset of the current tile
+  int w0, w1;       // kSym: this unit's sub-window [w0, w1) of the window
   __device__ __forceinline__ void start(const FusedParams& p, int u, int uj, int ub_, int u0,
                                         int ustep) {
     ub = ub_;
@@ -508,7 +517,10 @@ struct TileIter {
     h1 = true;
     if (KIND >= kSym) {
       W = sym_window(ub, p.NB);
-      o = sym_start(p, uj, ub, u0, ustep, W);
+      const int part = PAIR ? u / p.NB : 0;
+      w0 = PAIR ? part * W / p.wsplit : 0;
+      w1 = PAIR ? (part + 1) * W / p.wsplit : W;
+      o = sym_start(p, uj, ub, u0, ustep, w0, w1);
       place(p);
     } else {
       const int j = KIND == kPlain ? (u % p.C) * p.TPC : 0;
@@ -537,7 +549,7 @@ struct TileIter {
     ++s;
     if (KIND >= kSym) {
       o += PAIR ? 1 : 2;
-      if (o >= W) o -= W;
+      if (o >= w1) o -= w1 - w0;
       place(p);
     } else {
       K0 += 2;
@@ -2417,9 +2429,12 @@ static cudaError_t launch_fused_p(const TMaps& tm, const FusedParams& fp, int t,
 static ggm_status launch_fused(const FusedParams& fp_in, int t, int64_t ablocks, int64_t bblocks,
                                cudaStream_t s) {
   FusedParams fp = fp_in;
+  if (fp.wsplit < 1 || !fp.pair) fp.wsplit = 1;
   if (fp.unit_hi <= 0) {  // default: all units of this kind
     fp.unit_lo = 0;
-    fp.unit_hi = fp.kind == kPlain ? fp.RB * fp.C : fp.RB;
+    fp.unit_hi = fp.kind == kPlain ? fp.RB * fp.C
+                 : fp.kind >= kSym ? fp.RB * fp.wsplit
+                                   : fp.RB;
   }
   if (fp.unit_step < 1) fp.unit_step = 1;
   if (fp.unit_hi <= fp.unit_lo) return GGM_OK;  // empty shard
@@ -2624,10 +2639,11 @@ static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int un
   fp.cand_key = w.ckey;
   fp.cand_val = w.cval;
   fp.cand_total = pl.cand_total;
+  fp.wsplit = pl.pair ? kWindowSplit : 1;
   fp.unit_lo = unit_lo;
-  fp.unit_hi = unit_hi;
+  fp.unit_hi = unit_hi * fp.wsplit;  // unit_hi counts row blocks; units = sub-windows
   fp.unit_step = unit_step;
-  if (unit_hi <= unit_lo) return GGM_OK;
+  if (fp.unit_hi <= unit_lo) return GGM_OK;
   return launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
 }
 
@@ -3122,10 +3138,11 @@ static ggm_status sym_shard_impl(
   GGM_CUDA_TRY(cudaStreamSynchronize(s));
   tm.finish();
   double evaluated = 0.0;  // entries evaluated by this rank's units
-  for (int64_t b = rank; b < pl.NBu; b += nranks) {  // this rank's units (rank-strided)
-    const int64_t NBu = pl.NBu;
+  const int64_t ws = pl.pair ? kWindowSplit : 1;
+  for (int64_t u = rank; u < pl.NBu * ws; u += nranks) {  // this rank's units (rank-strided)
+    const int64_t NBu = pl.NBu, part = u / NBu, b = u % NBu;
     const int64_t W = (NBu & 1) ? (NBu + 1) / 2 : NBu / 2 + (b < NBu / 2 ? 1 : 0);
-    evaluated += pl.pair ? (double)W * 2 * kRowsPerBlock * kTileN
+    evaluated += pl.pair ? (double)((part + 1) * W / ws - part * W / ws) * 2 * kRowsPerBlock * kTileN
                          : (double)((W + 1) / 2) * kRowsPerBlock * kTileN;
   }
   g_stats[0] = 2;
@@ -3667,6 +3684,7 @@ extern "C" ggm_status ggm_sparse_precision_overall(
       // each unordered block pair once: row sums + column sums (half the plain MMA work)
       fp.kind = kSymList;
       fp.RB = (int)pl.NBu;
+      fp.wsplit = kWindowSplit;  // (only CTA pairs split windows)
     }
     st = launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
     if (st != GGM_OK) return st;
