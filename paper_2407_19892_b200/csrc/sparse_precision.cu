@@ -85,7 +85,8 @@ constexpr int kMaxResidentAtoms = 2;
 // A (128 rows x KA atoms x hi/lo) stays resident in shared memory when KA <= 2 (k <= 128)
 constexpr int kScratchBytes = 32 * 1024;  // epilogue shared scratch (per CTA)
 constexpr int kScratchFloats = 32 * 32;   // per warp at 8 epilogue warps (half at 16)
-constexpr int kSeedFrac = 64;  // seed pass: the n/64 largest-norm columns (see make_plan)
+constexpr int kSeedFrac = 32;       // seed pass: the n/32 largest-norm columns (see make_plan)
+constexpr int kSeedMinTiles = 48;  // ... but at least 48 tiles while that is <= 1/8 of the axis
 
 __host__ __device__ inline size_t block_bytes(int KA) { return (size_t)2 * KA * kAtomBytes; }
 
@@ -97,10 +98,14 @@ struct DevScalars {
   unsigned long long coo_count;
   unsigned long long cand_alloc;  // kSym: entries reserved from the candidate pool
   unsigned int rn_max_bits;       // kSym: float bits of max_i ||U_i||
+  unsigned long long cand_emitted;  // kSym: candidates written (<= cand_alloc)
 };
-constexpr int kCandChunk = 4096;
+// candidate-pool reservation granularity (entries): one chunk must hold the worst case of
+// one 32x32 warp chunk in both directions, so a fresh reservation always fits
+constexpr int kCandChunk = 2048;
+static_assert(kCandChunk >= 2 * 32 * 32, "a warp chunk's candidates must fit one reservation");
 constexpr int kWindowSplit = 4;  // kSym/kSymList CTA-pair units per row block (sub-windows)
-constexpr int64_t kSymAutoN = 16384;  // automatic symmetric scheme from this axis length (measured crossover 8192-16384)  // candidate-pool reservation granularity (entries)
+constexpr int64_t kSymAutoN = 16384;  // automatic symmetric scheme from this axis length (measured crossover 8192-16384)
 
 // ------------------------------------------------------------------ BK1a
 __global__ void absmax_check(const float* __restrict__ V, const double* __restrict__ lam,
@@ -1277,6 +1282,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   CandCursor cc{0, kCandChunk};
+  unsigned long long emitted = 0;  // candidates this warp wrote (warp-uniform)
 #ifdef GGM_MMA_PROF
   long long pe_t0 = clock64(), pe_w = 0, pe_n = 0;
 #endif
@@ -1431,6 +1437,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         if (cc.used + total > kCandChunk) continue;
         int64_t at = cc.base + cc.used;
         cc.used += total;
+        emitted += (unsigned long long)total;
         uint32_t mh = mr | mc;
         while (__any_sync(0xffffffffu, mh != 0)) {
           const uint32_t e = mh ? (uint32_t)(__ffs(mh) - 1) : 0u;
@@ -1459,6 +1466,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       }
     }
   }
+  if (lane == 0 && emitted) atomicAdd(&scw->cand_emitted, emitted);
 #ifdef GGM_MMA_PROF
   if (lane == 0 && (blockIdx.x & 15) == 0 && (warp == kFirstEpiWarp || warp == kFirstEpiWarp + EPW - 1))
     printf("EPIPROF cta %d warp %d tiles %lld total %lld wait_tfull %lld\n", (int)blockIdx.x, warp,
@@ -1925,112 +1933,117 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n,
   return lo;
 }
 
-// Re-evaluation on the pool sorted by target row: one warp per target row j keeps row j of
-// U (bound order) in registers and streams its candidates' source rows (coalesced 128-B
-// loads, no permutation lookups); fp32 x fp32 products are exact in fp64 and summed in a
-// fixed order, so ψ_ij and ψ_ji come out bit-identical.
+// Re-evaluation of the screened candidates (pool sorted by target row): U in bound order,
+// rows padded to kp = k rounded up to 4 floats (16-byte aligned float4 slices),
+// kRecGroup lanes per candidate; fp32 x fp32 products are exact in fp64 and summed in a
+// fixed order (lane slices, then a kRecGroup-lane butterfly), so ψ_ij and ψ_ji come out
+// bit-identical.
 constexpr int kRecMaxK = 128;
-// Only candidates that can still reach the row's exact top t are re-evaluated: with M_j =
-// screen_margin(j) in ψ units (the screening error bound of every pair of row j) and s_t the
-// t-th largest screened magnitude of the row's candidates, an exact top-t entry c has
-// |ψ1(c)| >= T - M_j >= s_t - 2 M_j (T the exact t-th magnitude, s_t <= T + M_j).  The
-// others get value 0 and cannot displace the re-evaluated ones in merge_sym.  On a rank's
-// partial list (distributed scheme) s_t is smaller than on the full row: still conservative.
-// rows' candidate ranges of the key-sorted pool: off[j] = first index with key >= j
-__global__ void cand_row_offsets(const uint32_t* __restrict__ skey, int64_t ncand, int64_t n,
-                                 int64_t* __restrict__ off) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    off[j] = lower_bound_u32(skey, ncand, (uint32_t)j);
+constexpr int kRecGroup = 8;                      // lanes per candidate
+__host__ __device__ inline int rec_stride(int k) { return (k + 3) & ~3; }
+// number of real candidates of the key-sorted pool (unused reservations carry key
+// UINT32_MAX and sort last): *cnt = first index with key >= n
+__global__ void pool_count(const uint32_t* __restrict__ skey, int64_t ncand, int64_t n,
+                           int64_t* __restrict__ cnt) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cnt = lower_bound_u32(skey, ncand, (uint32_t)n);
 }
-// U = V diag(sqrt(λ)) in bound order (fp32), the re-evaluation operand: ψ_ij = Σ_r U_ir U_jr
+// U = V diag(sqrt(λ)) in bound order (fp32, row stride rec_stride(k), zero padded), the
+// re-evaluation operand: ψ_ij = Σ_r U_ir U_jr.  One warp per row (one permutation lookup),
+// sqrt(λ) staged in shared memory once per block.
 __global__ void gather_u_bound(const float* __restrict__ V, const double* __restrict__ lam,
                                const int32_t* __restrict__ perm, int64_t n, int k,
                                float* __restrict__ Ub) {
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * k;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = q / k;
-    const int c = (int)(q - p * k);
-    Ub[q] = (float)((double)V[(int64_t)perm[p] * k + c] * sqrt(lam[c]));
+  __shared__ double sl[kRecMaxK];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) sl[c] = sqrt(lam[c]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int kp = rec_stride(k);
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const float* v = V + (int64_t)perm[p] * k;
+    for (int c = lane; c < kp; c += 32) Ub[p * kp + c] = c < k ? (float)((double)v[c] * sl[c]) : 0.f;
   }
 }
-__global__ void recompute_sorted(const int64_t* __restrict__ off, uint2* __restrict__ sval,
-                                 int64_t n, const float* __restrict__ Ub, int k, int t,
-                                 const float* __restrict__ rn, const int32_t* __restrict__ perm,
-                                 const unsigned int* __restrict__ rn_max_bits,
-                                 const DevScalars* __restrict__ sc) {
+// Exact value of every pool candidate: candidate-parallel over the key-sorted pool (uniform
+// work, no per-row chains), kRecGroup lanes per candidate, 2 x 32/kRecGroup candidates per
+// warp in flight.  Slots at or beyond *cnt (unused reservations, key UINT32_MAX) are
+// skipped.  ψ = Σ_c U_jc U_ic over the lane slices in a fixed order, then a kRecGroup-lane
+// butterfly: the same products in the same order for (j, i) and (i, j).
+template <int R>  // float4 slices per lane: 32 R >= kp
+__global__ void __launch_bounds__(256) recompute_sorted(const uint32_t* __restrict__ skey,
+                                                        uint2* __restrict__ sval,
+                                                        const int64_t* __restrict__ cnt, int64_t n,
+                                                        const float* __restrict__ Ub, int k) {
   const int lane = threadIdx.x & 31;
-  constexpr int R = kRecMaxK / 32;
-  const float umax = __uint_as_float(*rn_max_bits);
-  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
-       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t b0 = off[j];
-    const int64_t b1 = off[j + 1];
-    if (b0 >= b1) continue;
-    // x = s_t - 2 M_j (no filter when the row has at most t candidates)
-    float xcut = -1.f;
-    constexpr int NV = 8;  // screened magnitudes held per lane (rows with <= 256 candidates)
-    if (b1 - b0 > t && b1 - b0 <= 32 * NV) {
-      float av[NV];
+  const int g = lane % kRecGroup;   // slice of the candidate's rows
+  const int cs = lane / kRecGroup;  // candidate slot of this step
+  constexpr int CPW = 32 / kRecGroup;
+  constexpr int U = 2;
+  const int kp = rec_stride(k);
+  const int64_t ncand = *cnt;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t e0 = warp * (U * CPW); e0 < ncand; e0 += nwarps * (U * CPW)) {
+    float4 xa[U][R], xb[U][R];
 #pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        const int64_t e = b0 + lane + 32 * q;
-        av[q] = e < b1 ? fabsf(__uint_as_float(sval[e].y)) : -1.f;
+    for (int u = 0; u < U; ++u) {
+      const int64_t ei = e0 + u * CPW + cs;
+      const bool ok = ei < ncand;
+      const uint32_t j = ok ? skey[ei] : 0u;
+      const uint32_t i = ok ? sval[ei].x : 0u;
+      GGM_DCHECK(!ok || (j < (uint32_t)n && i < (uint32_t)n));
+      const float4* ua = reinterpret_cast<const float4*>(Ub + (int64_t)j * kp);
+      const float4* vb = reinterpret_cast<const float4*>(Ub + (int64_t)i * kp);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int c = 32 * r + 4 * g;
+        const bool in = ok && c < kp;
+        xa[u][r] = in ? __ldg(ua + c / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        xb[u][r] = in ? __ldg(vb + c / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      float cur = INFINITY;
-      int have = 0;
-      while (have < t) {  // t-th largest with multiplicity, by rounds of warp maxima
-        float mx = -1.f;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) mx = fmaxf(mx, av[q] < cur ? av[q] : -1.f);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        int cnt = 0;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) cnt += av[q] == mx;
-        have += __reduce_add_sync(0xffffffffu, cnt);
-        cur = mx;
-        if (mx < 0.f) break;
-      }
-      const float sf = ldexpf(1.f, sc->exp2);  // ψ units = accumulator units / s^2
-      const float mj = ldexpf(screen_margin(rn[perm[j]] * sf, umax * sf, k), -2 * sc->exp2);
-      xcut = cur - 2.f * mj;
     }
-    const float* ua = Ub + j * k;
-    double xa[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int c = lane + 32 * r;
-      xa[r] = c < k ? (double)ua[c] : 0.0;
-    }
-    // four candidates per step: their source-row loads are in flight together
-    for (int64_t e0 = b0; e0 < b1; e0 += 4) {
-      float xb[4][R];
-      bool keep[4];
+    for (int u = 0; u < U; ++u) {
+      double acc = 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t e = e0 + u < b1 ? e0 + u : b1 - 1;
-        const uint2 cvv = sval[e];
-        GGM_DCHECK(cvv.x < (uint32_t)n);
-        keep[u] = e0 + u < b1 && fabsf(__uint_as_float(cvv.y)) >= xcut;
-        const float* vb = Ub + (int64_t)cvv.x * k;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int c = lane + 32 * r;
-          xb[u][r] = (keep[u] && c < k) ? __ldg(vb + c) : 0.f;
-        }
+      for (int r = 0; r < R; ++r) {  // exact fp32 x fp32 products
+        acc = fma((double)xa[u][r].x, (double)xb[u][r].x, acc);
+        acc = fma((double)xa[u][r].y, (double)xb[u][r].y, acc);
+        acc = fma((double)xa[u][r].z, (double)xb[u][r].z, acc);
+        acc = fma((double)xa[u][r].w, (double)xb[u][r].w, acc);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        double acc = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc += xa[r] * (double)xb[u][r];  // exact fp32 x fp32 products
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0 && e0 + u < b1) sval[e0 + u].y = __float_as_uint(keep[u] ? (float)acc : 0.f);
-      }
+      for (int o = kRecGroup / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const int64_t ei = e0 + u * CPW + cs;
+      if (g == 0 && ei < ncand) sval[ei].y = __float_as_uint((float)acc);
     }
   }
+}
+
+// R = ceil(kp / 32) instantiations (no FMAs on padding slices); one resident wave of blocks
+// (the kernel is grid-stride: later waves would each take a full stride share)
+template <int R>
+static void launch_recompute_r(const uint32_t* skey, uint2* sval, const int64_t* cnt, int64_t n,
+                               const float* Ub, int k, int sms, cudaStream_t s) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, recompute_sorted<R>, 256, 0) !=
+            cudaSuccess || per_sm < 1)
+      per_sm = 2;
+  }
+  recompute_sorted<R><<<sms * per_sm, 256, 0, s>>>(skey, sval, cnt, n, Ub, k);
+}
+static void launch_recompute(const uint32_t* skey, uint2* sval, const int64_t* cnt, int64_t n,
+                             const float* Ub, int k, int sms, cudaStream_t s) {
+  const int R = (rec_stride(k) + 31) / 32;
+  if (R <= 1)
+    launch_recompute_r<1>(skey, sval, cnt, n, Ub, k, sms, s);
+  else if (R == 2)
+    launch_recompute_r<2>(skey, sval, cnt, n, Ub, k, sms, s);
+  else if (R == 3)
+    launch_recompute_r<3>(skey, sval, cnt, n, Ub, k, sms, s);
+  else
+    launch_recompute_r<4>(skey, sval, cnt, n, Ub, k, sms, s);
 }
 
 template <int MAXT>
@@ -2221,11 +2234,23 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   // least one).  |ψ_ij| <= ||U_i|| ||U_j||, so large-norm columns hold most rows' largest
   // entries: on C5 factors the t-th largest over this 1/64 sample leaves ~21 candidates per
   // row where a strided 1/8 sample left ~89 (any sample gives a valid bound).
+  // Size: n/kSeedFrac columns, but at least kSeedMinTiles tiles (12,288 columns) while that
+  // stays <= 1/8 of the axis; never fewer than 8 tiles.  The seed is a plain pass over
+  // n x sample entries; a larger sample tightens b_i, which cuts the main kernel's rare-path
+  // visits (chunks with an entry above a bound): C4 (n = 2e5, k = 64) main 4.77 -> 3.95 ms
+  // for +0.23 ms of seed at 49 vs 13 tiles; C5 (n = 1e6) main 96.9 -> 93.9 ms for +2.2 ms
+  // at 1/32 vs 1/64 (profiles/r02_logs/r02u_seed_sweep.log).
   {
-    int64_t frac = g_seed_frac_override > 0 ? g_seed_frac_override : kSeedFrac;
-    if (const char* e = getenv("GGM_SEED_FRAC")) frac = std::max(1, atoi(e));  // tuning only
-    // at least 8 tiles (2048 columns): small axes get a proportionally larger sample
-    const int64_t tiles = std::max<int64_t>(8, (n / frac + kTileN - 1) / kTileN);
+    int64_t tiles;
+    if (g_seed_frac_override > 0 || getenv("GGM_SEED_FRAC")) {
+      int64_t frac = g_seed_frac_override;
+      if (const char* e = getenv("GGM_SEED_FRAC")) frac = std::max(1, atoi(e));  // tuning only
+      tiles = std::max<int64_t>(8, (n / frac + kTileN - 1) / kTileN);
+    } else {
+      tiles = (n / kSeedFrac + kTileN - 1) / kTileN;
+      tiles = std::max<int64_t>(tiles, std::min<int64_t>(kSeedMinTiles, pl->NT / 8));
+      tiles = std::max<int64_t>(8, tiles);
+    }
     pl->SS = (int)std::max<int64_t>(1, std::min<int64_t>(pl->NT, tiles));
   }
   // pool: an uninformative sample leaves ~ t x (n / sample size) candidates per row; hold
@@ -2281,7 +2306,7 @@ struct Work {
   float* thr_s;        // kSym screening: thr_p lowered by the hi*hi error bound [NB*128]
   float* thr_cmin;     // kSym: minimum of the effective bounds over each 32-column chunk
   float* Ub;           // kSym screening: U = V diag(sqrt λ) in bound order (re-evaluation)
-  int64_t* roff;       // kSym screening: candidate row offsets of the sorted pool [n+1]
+  int64_t* roff;       // kSym screening: number of real candidates of the sorted pool [1]
   int32_t* ids;        // kSym: 0..n-1
   int32_t* perm;       // kSym: permuted index -> original id [n]
   float* rn;           // kSym: row norms ||U_i|| [n]
@@ -2314,8 +2339,8 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->thr_p = cv.take<float>(nb * kRowsPerBlock);
   w->thr_s = cv.take<float>(pl.screen ? nb * kRowsPerBlock : 0);
   w->thr_cmin = cv.take<float>(nb * kRowsPerBlock / 32);
-  w->Ub = cv.take<float>(pl.screen ? (size_t)pl.n * pl.k : 0);
-  w->roff = cv.take<int64_t>(pl.screen ? (size_t)pl.n + 1 : 0);
+  w->Ub = cv.take<float>(pl.screen ? (size_t)pl.n * rec_stride(pl.k) : 0);
+  w->roff = cv.take<int64_t>(pl.screen ? 1 : 0);
   w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->rn = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
@@ -2609,7 +2634,7 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
       pl.screen ? w.thr_s : w.thr_p, nthr / 32, w.thr_cmin);
   count_launches(1);
   if (pl.screen) {
-    gather_u_bound<<<(int)std::min<int64_t>((n * k + 255) / 256, sms * 16), 256, 0, s>>>(
+    gather_u_bound<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
         V, lambda, w.perm, n, k, w.Ub);
     count_launches(1);
   }
@@ -2785,10 +2810,8 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
         GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval,
                                                      w.sval, ncand, 0, ebits, s));
         if (pl.screen) {  // exact values of every screened candidate (no top-t filter)
-          cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
-              w.skey, ncand, n, w.roff);
-          recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-              w.roff, w.sval, n, w.Ub, k, INT_MAX, w.rn, w.perm, &w.sc->rn_max_bits, w.sc);
+          pool_count<<<1, 32, 0, s>>>(w.skey, ncand, n, w.roff);
+          launch_recompute(w.skey, w.sval, w.roff, n, w.Ub, k, sms, s);
           count_launches(2);
         }
         sym_threshold_coo<<<(int)std::min<int64_t>((ncand + 255) / 256, sms * 16), 256, 0, s>>>(
@@ -2797,7 +2820,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
         count_launches(1);
       }
       g_stats[0] = 2;
-      g_stats[2] = (double)ncand;
+      g_stats[2] = (double)hs.cand_emitted;
       return mode1_tail();
     }
     if (hovf) {
@@ -2850,10 +2873,8 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                    ncand, 0, ebits, s));
       if (pl.screen) {  // exact values of the screened candidates
-        cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
-            w.skey, ncand, n, w.roff);
-        recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-            w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits, w.sc);
+        pool_count<<<1, 32, 0, s>>>(w.skey, ncand, n, w.roff);
+        launch_recompute(w.skey, w.sval, w.roff, n, w.Ub, k, sms, s);
         count_launches(2);
       }
     }
@@ -2879,7 +2900,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     }
     g_stats[0] = 2;
     g_stats[1] = evaluated;
-    g_stats[2] = (double)ncand;
+    g_stats[2] = (double)hs.cand_emitted;  // written; the sort above covers ncand reserved slots
     g_stats[3] = 0;
     *nnz_out = pl.rows * pl.t;
     return GGM_OK;
@@ -3102,10 +3123,8 @@ static ggm_status sym_shard_impl(
     GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                  ncand, 0, ebits, s));
     if (pl.screen) {  // exact values before the buckets leave this rank
-      cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
-          w.skey, ncand, n, w.roff);
-      recompute_sorted<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-          w.roff, w.sval, n, w.Ub, k, pl.t, w.rn, w.perm, &w.sc->rn_max_bits, w.sc);
+      pool_count<<<1, 32, 0, s>>>(w.skey, ncand, n, w.roff);
+      launch_recompute(w.skey, w.sval, w.roff, n, w.Ub, k, sms, s);
       count_launches(2);
     }
   }

@@ -1,10 +1,11 @@
 #!/bin/bash
 # Per-role wait-time breakdown of the BK2 main kernel (variant built with -DGGM_MMA_PROF).
 cat > /tmp/mp.py <<'PY'
+# MP_N / MP_K select the axis (default C5 axis A; C4: MP_N=200000 MP_K=64)
 import sys, os
 sys.path.insert(0, os.getcwd())
 import torch, paper_2407_19892_b200 as G
-n, k = 1_000_000, 100
+n, k = int(os.environ.get('MP_N', 1_000_000)), int(os.environ.get('MP_K', 100))
 g = torch.Generator(device="cuda").manual_seed(0)
 V = torch.linalg.qr(torch.randn(n, k, device="cuda", generator=g, dtype=torch.float64))[0].float().contiguous()
 lam = torch.exp(torch.randn(k, device="cuda", dtype=torch.float64, generator=g)).sort(descending=True).values
