@@ -1941,11 +1941,46 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n,
 constexpr int kRecMaxK = 128;
 constexpr int kRecGroup = 8;                      // lanes per candidate
 __host__ __device__ inline int rec_stride(int k) { return (k + 3) & ~3; }
-// number of real candidates of the key-sorted pool (unused reservations carry key
-// UINT32_MAX and sort last): *cnt = first index with key >= n
-__global__ void pool_count(const uint32_t* __restrict__ skey, int64_t ncand, int64_t n,
-                           int64_t* __restrict__ cnt) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *cnt = lower_bound_u32(skey, ncand, (uint32_t)n);
+// Only candidates that can still reach the row's exact top t are re-evaluated: with M_j =
+// screen_margin(j) in ψ units (the screening error bound of every pair of row j) and s_t the
+// t-th largest screened magnitude of the row's candidates, an exact top-t entry c has
+// |ψ1(c)| >= T - M_j >= s_t - 2 M_j (T the exact t-th magnitude, s_t <= T + M_j).  The
+// others get value 0 and cannot displace the re-evaluated ones in merge_sym.  On a rank's
+// partial list (distributed scheme) s_t is smaller than on the full row: still conservative.
+// rows' candidate ranges of the key-sorted pool: off[j] = first index with key >= j (off[n]
+// = the number of real candidates; unused reservations carry key UINT32_MAX, sorted last)
+__global__ void cand_row_offsets(const uint32_t* __restrict__ skey, int64_t ncand, int64_t n,
+                                 int64_t* __restrict__ off) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    off[j] = lower_bound_u32(skey, ncand, (uint32_t)j);
+}
+// cut[j] = s_t - 2 M_j, or -1 (keep all) for rows with at most t candidates: one thread per
+// row, a magnitude-only top-t list over the row's screened values
+template <int MAXT>
+__global__ void rec_cut(const int64_t* __restrict__ off, const uint2* __restrict__ sval,
+                        int64_t n, int t, int k, const float* __restrict__ rn,
+                        const int32_t* __restrict__ perm,
+                        const unsigned int* __restrict__ rn_max_bits,
+                        const DevScalars* __restrict__ sc, float* __restrict__ cut) {
+  const float umax = __uint_as_float(*rn_max_bits);
+  const float sf = ldexpf(1.f, sc->exp2);  // ψ units = accumulator units / s^2
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = off[j], b1 = off[j + 1];
+    if (b1 - b0 <= t) {
+      cut[j] = -1.f;
+      continue;
+    }
+    MagList<MAXT> top;
+    top.init(t);
+    for (int64_t e = b0; e < b1; ++e) {
+      const float a = fabsf(__uint_as_float(sval[e].y));
+      if (a > top.m[0]) top.insert(a);
+    }
+    const float mj = ldexpf(screen_margin(rn[perm[j]] * sf, umax * sf, k), -2 * sc->exp2);
+    cut[j] = top.m[0] - 2.f * mj;
+  }
 }
 // U = V diag(sqrt(λ)) in bound order (fp32, row stride rec_stride(k), zero padded), the
 // re-evaluation operand: ψ_ij = Σ_r U_ir U_jr.  One warp per row (one permutation lookup),
@@ -1964,40 +1999,44 @@ __global__ void gather_u_bound(const float* __restrict__ V, const double* __rest
     for (int c = lane; c < kp; c += 32) Ub[p * kp + c] = c < k ? (float)((double)v[c] * sl[c]) : 0.f;
   }
 }
-// Exact value of every pool candidate: candidate-parallel over the key-sorted pool (uniform
+// Exact values of the pool candidates: candidate-parallel over the key-sorted pool (uniform
 // work, no per-row chains), kRecGroup lanes per candidate, 2 x 32/kRecGroup candidates per
-// warp in flight.  Slots at or beyond *cnt (unused reservations, key UINT32_MAX) are
-// skipped.  ψ = Σ_c U_jc U_ic over the lane slices in a fixed order, then a kRecGroup-lane
+// warp in flight; candidates below their row's cut (nullptr: none) get 0 without loads.
+// Slots at or beyond off[n] (unused reservations) are skipped.  ψ = Σ_c U_jc U_ic over the lane slices in a fixed order, then a kRecGroup-lane
 // butterfly: the same products in the same order for (j, i) and (i, j).
 template <int R>  // float4 slices per lane: 32 R >= kp
 __global__ void __launch_bounds__(256) recompute_sorted(const uint32_t* __restrict__ skey,
                                                         uint2* __restrict__ sval,
-                                                        const int64_t* __restrict__ cnt, int64_t n,
-                                                        const float* __restrict__ Ub, int k) {
+                                                        const int64_t* __restrict__ off, int64_t n,
+                                                        const float* __restrict__ Ub, int k,
+                                                        const float* __restrict__ cut) {
   const int lane = threadIdx.x & 31;
   const int g = lane % kRecGroup;   // slice of the candidate's rows
   const int cs = lane / kRecGroup;  // candidate slot of this step
   constexpr int CPW = 32 / kRecGroup;
   constexpr int U = 2;
   const int kp = rec_stride(k);
-  const int64_t ncand = *cnt;
+  const int64_t ncand = off[n];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t e0 = warp * (U * CPW); e0 < ncand; e0 += nwarps * (U * CPW)) {
     float4 xa[U][R], xb[U][R];
+    bool keep[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t ei = e0 + u * CPW + cs;
       const bool ok = ei < ncand;
       const uint32_t j = ok ? skey[ei] : 0u;
-      const uint32_t i = ok ? sval[ei].x : 0u;
+      const uint2 cvv = ok ? sval[ei] : make_uint2(0u, 0u);
+      const uint32_t i = cvv.x;
       GGM_DCHECK(!ok || (j < (uint32_t)n && i < (uint32_t)n));
+      keep[u] = ok && (cut == nullptr || fabsf(__uint_as_float(cvv.y)) >= cut[j]);
       const float4* ua = reinterpret_cast<const float4*>(Ub + (int64_t)j * kp);
       const float4* vb = reinterpret_cast<const float4*>(Ub + (int64_t)i * kp);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int c = 32 * r + 4 * g;
-        const bool in = ok && c < kp;
+        const bool in = keep[u] && c < kp;
         xa[u][r] = in ? __ldg(ua + c / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
         xb[u][r] = in ? __ldg(vb + c / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -2015,7 +2054,7 @@ __global__ void __launch_bounds__(256) recompute_sorted(const uint32_t* __restri
 #pragma unroll
       for (int o = kRecGroup / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       const int64_t ei = e0 + u * CPW + cs;
-      if (g == 0 && ei < ncand) sval[ei].y = __float_as_uint((float)acc);
+      if (g == 0 && ei < ncand) sval[ei].y = __float_as_uint(keep[u] ? (float)acc : 0.f);
     }
   }
 }
@@ -2023,29 +2062,17 @@ __global__ void __launch_bounds__(256) recompute_sorted(const uint32_t* __restri
 // R = ceil(kp / 32) instantiations (no FMAs on padding slices); one resident wave of blocks
 // (the kernel is grid-stride: later waves would each take a full stride share)
 template <int R>
-static void launch_recompute_r(const uint32_t* skey, uint2* sval, const int64_t* cnt, int64_t n,
-                               const float* Ub, int k, int sms, cudaStream_t s) {
+static void launch_recompute_r(const uint32_t* skey, uint2* sval, const int64_t* off, int64_t n,
+                               const float* Ub, int k, const float* cut, int sms,
+                               cudaStream_t s) {
   static int per_sm = 0;
   if (per_sm == 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, recompute_sorted<R>, 256, 0) !=
             cudaSuccess || per_sm < 1)
       per_sm = 2;
   }
-  recompute_sorted<R><<<sms * per_sm, 256, 0, s>>>(skey, sval, cnt, n, Ub, k);
+  recompute_sorted<R><<<sms * per_sm, 256, 0, s>>>(skey, sval, off, n, Ub, k, cut);
 }
-static void launch_recompute(const uint32_t* skey, uint2* sval, const int64_t* cnt, int64_t n,
-                             const float* Ub, int k, int sms, cudaStream_t s) {
-  const int R = (rec_stride(k) + 31) / 32;
-  if (R <= 1)
-    launch_recompute_r<1>(skey, sval, cnt, n, Ub, k, sms, s);
-  else if (R == 2)
-    launch_recompute_r<2>(skey, sval, cnt, n, Ub, k, sms, s);
-  else if (R == 3)
-    launch_recompute_r<3>(skey, sval, cnt, n, Ub, k, sms, s);
-  else
-    launch_recompute_r<4>(skey, sval, cnt, n, Ub, k, sms, s);
-}
-
 template <int MAXT>
 __global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restrict__ cv,
                           int64_t ncand, int64_t n, int t, const int32_t* __restrict__ perm,
@@ -2306,7 +2333,8 @@ struct Work {
   float* thr_s;        // kSym screening: thr_p lowered by the hi*hi error bound [NB*128]
   float* thr_cmin;     // kSym: minimum of the effective bounds over each 32-column chunk
   float* Ub;           // kSym screening: U = V diag(sqrt λ) in bound order (re-evaluation)
-  int64_t* roff;       // kSym screening: number of real candidates of the sorted pool [1]
+  int64_t* roff;       // kSym screening: candidate row offsets of the sorted pool [n+1]
+  float* rcut;         // kSym screening: per-row re-evaluation cuts [n]
   int32_t* ids;        // kSym: 0..n-1
   int32_t* perm;       // kSym: permuted index -> original id [n]
   float* rn;           // kSym: row norms ||U_i|| [n]
@@ -2340,7 +2368,8 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->thr_s = cv.take<float>(pl.screen ? nb * kRowsPerBlock : 0);
   w->thr_cmin = cv.take<float>(nb * kRowsPerBlock / 32);
   w->Ub = cv.take<float>(pl.screen ? (size_t)pl.n * rec_stride(pl.k) : 0);
-  w->roff = cv.take<int64_t>(pl.screen ? 1 : 0);
+  w->roff = cv.take<int64_t>(pl.screen ? (size_t)pl.n + 1 : 0);
+  w->rcut = cv.take<float>(pl.screen ? (size_t)pl.n : 0);
   w->ids = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->perm = cv.take<int32_t>(pl.sym ? (size_t)pl.n : 0);
   w->rn = cv.take<float>(pl.sym ? (size_t)pl.n : 0);
@@ -2552,6 +2581,43 @@ static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t
   fp.dbg = d ? atoi(d) : 0;
 #endif
   return fp;
+}
+
+// exact re-evaluation of a key-sorted pool of ncand slots: row offsets, per-row cuts, then
+// the values.  The cuts pay only when rows hold many more candidates than t (the top-32
+// lists of the overall rules: re-evaluation 133 -> 38 + 10 ms at n = 10^6); at ~2t per row
+// (C4/C5 top-10) they keep nearly every candidate and cost a pass (C5: 2.09 vs 2.42 +
+// 0.10 ms), so they run when the pool averages more than kRecCutRatio t per row.  t <= 0:
+// every candidate (threshold mode).
+constexpr int kRecCutRatio = 4;
+static void recompute_pool(const Work& w, int64_t ncand, int64_t n, int k, int t, int sms,
+                           cudaStream_t s) {
+  cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
+      w.skey, ncand, n, w.roff);
+  const float* cut = nullptr;
+  bool use_cut = t > 0 && ncand > (int64_t)kRecCutRatio * t * n;
+  if (const char* e = getenv("GGM_REC_CUT")) use_cut = t > 0 && atoi(e) != 0;  // tests: both forms
+  if (use_cut) {
+    const int blocks = (int)std::min<int64_t>((n + 127) / 128, sms * 16);
+    if (t <= 10)
+      rec_cut<10><<<blocks, 128, 0, s>>>(w.roff, w.sval, n, t, k, w.rn, w.perm, &w.sc->rn_max_bits, w.sc, w.rcut);
+    else if (t <= 16)
+      rec_cut<16><<<blocks, 128, 0, s>>>(w.roff, w.sval, n, t, k, w.rn, w.perm, &w.sc->rn_max_bits, w.sc, w.rcut);
+    else
+      rec_cut<32><<<blocks, 128, 0, s>>>(w.roff, w.sval, n, t, k, w.rn, w.perm, &w.sc->rn_max_bits, w.sc, w.rcut);
+    cut = w.rcut;
+    count_launches(1);
+  }
+  const int R = (rec_stride(k) + 31) / 32;
+  if (R <= 1)
+    launch_recompute_r<1>(w.skey, w.sval, w.roff, n, w.Ub, k, cut, sms, s);
+  else if (R == 2)
+    launch_recompute_r<2>(w.skey, w.sval, w.roff, n, w.Ub, k, cut, sms, s);
+  else if (R == 3)
+    launch_recompute_r<3>(w.skey, w.sval, w.roff, n, w.Ub, k, cut, sms, s);
+  else
+    launch_recompute_r<4>(w.skey, w.sval, w.roff, n, w.Ub, k, cut, sms, s);
+  count_launches(2);
 }
 
 // Symmetric scheme, phases 1-3 (replicated on every rank of the distributed form): rows in
@@ -2810,9 +2876,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
         GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval,
                                                      w.sval, ncand, 0, ebits, s));
         if (pl.screen) {  // exact values of every screened candidate (no top-t filter)
-          pool_count<<<1, 32, 0, s>>>(w.skey, ncand, n, w.roff);
-          launch_recompute(w.skey, w.sval, w.roff, n, w.Ub, k, sms, s);
-          count_launches(2);
+          recompute_pool(w, ncand, n, k, 0, sms, s);
         }
         sym_threshold_coo<<<(int)std::min<int64_t>((ncand + 255) / 256, sms * 16), 256, 0, s>>>(
             w.skey, w.sval, ncand, n, w.perm, opts->tau, capacity, &w.sc->coo_count, w.key_in,
@@ -2873,9 +2937,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                    ncand, 0, ebits, s));
       if (pl.screen) {  // exact values of the screened candidates
-        pool_count<<<1, 32, 0, s>>>(w.skey, ncand, n, w.roff);
-        launch_recompute(w.skey, w.sval, w.roff, n, w.Ub, k, sms, s);
-        count_launches(2);
+        recompute_pool(w, ncand, n, k, pl.t, sms, s);
       }
     }
     if (pl.t <= 5)
@@ -3123,9 +3185,7 @@ static ggm_status sym_shard_impl(
     GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                  ncand, 0, ebits, s));
     if (pl.screen) {  // exact values before the buckets leave this rank
-      pool_count<<<1, 32, 0, s>>>(w.skey, ncand, n, w.roff);
-      launch_recompute(w.skey, w.sval, w.roff, n, w.Ub, k, sms, s);
-      count_launches(2);
+      recompute_pool(w, ncand, n, k, pl.t, sms, s);
     }
   }
   // destination buckets: rank r owns bound-order rows [lo_r, lo_{r+1}); unused pool slots

@@ -115,3 +115,24 @@ def test_symmetric_screening_rank_edges(G, k):
     assert st["scheme"] in ("symmetric", "plain")
     res = check_topk(rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy(), V, lam, np.arange(n), t)
     assert res["exact"] + res["excused"] == n
+
+
+@pytest.mark.parametrize("n,k,t,ss", [(5000, 100, 10, None), (4000, 64, 32, "2"), (3000, 16, 5, "256")])
+def test_recompute_cut_forms_agree(G, monkeypatch, n, k, t, ss):
+    """Symmetric screening merge: re-evaluation of every candidate vs only those above the
+    per-row cut s_t - 2 M_j (GGM_REC_CUT=0/1 force the two forms; the default picks by pool
+    size).  The kept candidates get the same fp64 values, the others cannot reach the top t:
+    identical CSR."""
+    if ss is not None:
+        monkeypatch.setenv("GGM_SEED_FRAC", ss)
+    V, lam = gen.small_factor(4000 + n + t, n, k)
+    outs = []
+    for form in ("0", "1"):
+        monkeypatch.setenv("GGM_REC_CUT", form)
+        rp, c, v, st = _run(G, V, lam, 0, n, topk=t, symmetric=1)
+        assert st["scheme"] == "symmetric" and not st["recomputed"]
+        outs.append((rp, c, v))
+    for a, b in zip(outs[0], outs[1]):
+        np.testing.assert_array_equal(a, b)
+    res = check_topk(*outs[1], V, lam, np.arange(n), t)
+    assert res["exact"] + res["excused"] == n
