@@ -128,6 +128,19 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[3
       : "=r"(r[0]),"=r"(r[1]),"=r"(r[2]),"=r"(r[3]),"=r"(r[4]),"=r"(r[5]),"=r"(r[6]),"=r"(r[7]),"=r"(r[8]),"=r"(r[9]),"=r"(r[10]),"=r"(r[11]),"=r"(r[12]),"=r"(r[13]),"=r"(r[14]),"=r"(r[15]),"=r"(r[16]),"=r"(r[17]),"=r"(r[18]),"=r"(r[19]),"=r"(r[20]),"=r"(r[21]),"=r"(r[22]),"=r"(r[23]),"=r"(r[24]),"=r"(r[25]),"=r"(r[26]),"=r"(r[27]),"=r"(r[28]),"=r"(r[29]),"=r"(r[30]),"=r"(r[31])
       : "r"(taddr));
 }
+// 16 lanes x 32 columns in the 16x256b fragment layout (.x4: four 8-column groups): thread
+// t gets lanes base + t/4 and base + t/4 + 8, columns 8g + 2(t%4) + {0,1}; register 4g + m
+// holds (lane t/4 + 8(m >> 1), column 8g + 2(t%4) + (m & 1)) (tools/probes/
+// tmem_layout_probe.cu).  Valid after tmem_wait_ld on the enclosing 32-register array.
+__device__ __forceinline__ void tmem_ld16x256_x4_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 // One lane of the (converged) warp returns true: single-thread tcgen05 instructions are
 // issued under it while the rest of the role runs warp-uniformly (operands in uniform
 // registers, no per-instruction R2UR/ELECT loop).

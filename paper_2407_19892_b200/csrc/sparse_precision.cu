@@ -1133,6 +1133,7 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
                                               int rank) {
   using G = EpiGeom<EPW>;
   const G g(warp, lane);
+  const int lq = lane & 3, lg = lane >> 2;  // 16x256b fragment coordinates
   const float sd = ldexpf(1.f, -p.sc->exp2);
   const double sd2 = (double)sd * (double)sd;
   const int64_t n = p.n;
@@ -1143,10 +1144,8 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
   const bool remote_rel = PAIR && rank != 0;
   const uint32_t tempty_a0 = remote_rel ? mbar_map_cluster(&tempty[0], 0) : smem_u32(&tempty[0]);
   const uint32_t tempty_a1 = remote_rel ? mbar_map_cluster(&tempty[1], 0) : smem_u32(&tempty[1]);
-  // column-sum slices: [tile parity][part][G::W] floats
-  for (int b = (warp - kFirstEpiWarp) * 32 + lane; b < 2 * G::P * G::W; b += EPW * 32)
-    scratch_all[b] = 0.f;
-  asm volatile("bar.sync 5, %0;" ::"r"(EPW * 32) : "memory");
+  // column-sum partials: [tile parity][part][quadrant][G::W] floats, plain stores (every
+  // live off-diagonal tile overwrites its slot), combined after the part's barrier
   int buf = 0, tpar = 0;
   uint32_t tphase = 0;
   for (int uj = u0; uj < unit_count(p); uj += ustep) {
@@ -1154,9 +1153,11 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
     int ub;
     const int ntiles = unit_tiles<kSymList, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
-    const int64_t lr = (int64_t)rb * kRowsPerBlock + g.r;
+    // this thread's rows (16x256b layout): lr = rbase + lg + 8 j; its row-sum row: j = lq
+    const int64_t rbase = (int64_t)rb * kRowsPerBlock + g.q * 32;
+    const bool rows_valid = rbase + 32 <= p.rows;
+    const int64_t lr = rbase + lg + 8 * lq;
     const bool valid = lr < p.rows;
-    const int64_t gi = p.row_begin + lr;
     double macc = 0.0;
     TileIter<kSymList, PAIR> ti;
     ti.start(p, u, uj, ub, u0, ustep);
@@ -1166,7 +1167,8 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
       // the diagonal (super) block holds both (i, j) and (j, i): row sums only
       const bool diag_blk = PAIR ? (ti.K0 >> 1) == ub : Kh == rb;
       const int64_t cb = (int64_t)Kh * kRowsPerBlock + coff;
-      const bool need_mask = (gi >= cb && gi < cb + G::W) || cb + G::W > n;
+      const int64_t gr0 = p.row_begin + rbase;  // the warp's rows: [gr0, gr0 + 32)
+      const bool need_mask = (gr0 < cb + G::W && cb < gr0 + 32) || cb + G::W > n;
       ti.next(p);
       mbar_wait_a(buf ? tfull_a1 : tfull_a0, tphase);
       tc_fence_after();
@@ -1174,12 +1176,19 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
       const uint32_t cur = buf;
       buf ^= 1;
       tphase ^= (uint32_t)(buf == 0);
-      float* cacc = scratch_all + (tpar * G::P + g.part) * G::W;
+      float* cpart = scratch_all + (size_t)(tpar * G::P + g.part) * 4 * G::W;  // [quadrant][W]
+      float racc = 0.f;  // this tile's row sum (fp32 over 2 chunks, then fp64)
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) {
+        // 32 rows x 32 columns in the 16x256b layout (two 16-lane loads): this thread holds
+        // rows lg + 8j (j = 0..3; v[16(j >> 1) + 4cg + 2(j & 1) + b]) at columns
+        // 8cg + 2lq + b (cg = 0..3, b = 0..1), so both the row and the column sums start
+        // with thread-local adds and end in short reduce-scatters (3 + 7 shuffles instead of
+        // the 31-shuffle transpose of the 32x32b layout)
         uint32_t v[32];
         if (live) {
-          tmem_ld32_nowait(taddr + c * 32, v);
+          tmem_ld16x256_x4_nowait(taddr + c * 32, v);
+          tmem_ld16x256_x4_nowait(taddr + ((uint32_t)16 << 16) + c * 32, v + 16);
           tmem_wait_ld(v);
         }
         if (c == G::NC - 1) {  // the warp's slice is in registers: release the buffer
@@ -1195,43 +1204,76 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
         }
         if (!live) continue;
         const int64_t col0 = cb + c * 32;
-        uint32_t excl = 0;  // diagonal (j == i, not an edge: Q8) and padding columns (j >= n)
-        if (need_mask) {
-          const int64_t dd = gi - col0;
-          if ((uint64_t)dd < 32ull) excl |= 1u << dd;
-          const int64_t nn = n - col0;
-          if (nn < 32) excl |= nn <= 0 ? 0xffffffffu : (0xffffffffu << nn);
-        }
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-        if (excl == 0) {
+        if (need_mask || !rows_valid) {
+          // diagonal (j == i, not an edge: Q8), padding columns (j >= n), rows past the axis
 #pragma unroll
-          for (int e = 0; e < 32; ++e) s4[e & 3] += fabsf(__uint_as_float(v[e]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            s4[e & 3] += ((excl >> e) & 1u) ? 0.f : fabsf(__uint_as_float(v[e]));
-        }
-        if (valid) macc += (double)((s4[0] + s4[1]) + (s4[2] + s4[3]));
-        if (!diag_blk) {
-          const float cs = col_abs_sums32(v, valid ? excl : 0xffffffffu, lane);
-          atomicAdd(cacc + c * 32 + lane, cs);
-        }
-      }
-      if (!diag_blk && live) {
-        // the part's 4 quadrant warps have added their column sums: quadrant 0 flushes
-        // (and clears) them; the other parity slice takes the next tile meanwhile
-        asm volatile("bar.sync %0, 128;" ::"r"(8 + g.part) : "memory");
-        if (g.q == 0) {
-#pragma unroll
-          for (int c = 0; c < G::NC; ++c) {
-            const int64_t j = cb + c * 32 + lane;
-            const float x = cacc[c * 32 + lane];
-            cacc[c * 32 + lane] = 0.f;
-            if (j < n && x != 0.f) atomicAdd(p.mass_out + j, (double)x * sd2);
+          for (int x = 0; x < 32; ++x) {
+            const int j = 2 * (x >> 4) + ((x >> 1) & 1);
+            const int64_t col = col0 + 8 * ((x >> 2) & 3) + 2 * lq + (x & 1);
+            const int64_t lrj = rbase + lg + 8 * j;
+            if (col == p.row_begin + lrj || col >= n || lrj >= p.rows) v[x] = 0u;
           }
         }
+        float rs[4], cs8[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int o = 16 * (j >> 1) + 2 * (j & 1);
+          float a = fabsf(__uint_as_float(v[o])) + fabsf(__uint_as_float(v[o + 1]));
+#pragma unroll
+          for (int cg = 1; cg < 4; ++cg)
+            a += fabsf(__uint_as_float(v[o + 4 * cg])) + fabsf(__uint_as_float(v[o + 4 * cg + 1]));
+          rs[j] = a;
+        }
+#pragma unroll
+        for (int cg = 0; cg < 4; ++cg)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int o = 4 * cg + b;
+            cs8[2 * cg + b] = (fabsf(__uint_as_float(v[o])) + fabsf(__uint_as_float(v[o + 2]))) +
+                              (fabsf(__uint_as_float(v[o + 16])) + fabsf(__uint_as_float(v[o + 18])));
+          }
+        {  // row sums: reduce-scatter over lq (lanes ^2, ^1) -> this lane: row lg + 8 lq
+          const bool up2 = (lq & 2) != 0;
+          float a0 = (up2 ? rs[2] : rs[0]) + __shfl_xor_sync(0xffffffffu, up2 ? rs[0] : rs[2], 2);
+          float a1 = (up2 ? rs[3] : rs[1]) + __shfl_xor_sync(0xffffffffu, up2 ? rs[1] : rs[3], 2);
+          const bool up1 = (lq & 1) != 0;
+          const float r = (up1 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, up1 ? a0 : a1, 1);
+          racc += r;
+        }
+        if (!diag_blk) {  // column sums: reduce-scatter over lg (lanes ^16, ^8, ^4)
+          float a4[4];
+          const bool u16 = (lg & 4) != 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            a4[e] = (u16 ? cs8[e + 4] : cs8[e]) + __shfl_xor_sync(0xffffffffu, u16 ? cs8[e] : cs8[e + 4], 16);
+          const bool u8 = (lg & 2) != 0;
+          float a2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            a2[e] = (u8 ? a4[e + 2] : a4[e]) + __shfl_xor_sync(0xffffffffu, u8 ? a4[e] : a4[e + 2], 8);
+          const bool u4 = (lg & 1) != 0;
+          const float cs = (u4 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, u4 ? a2[0] : a2[1], 4);
+          // this lane: column 8 (lg >> 1) + 2 lq + (lg & 1) of the chunk
+          cpart[g.q * G::W + c * 32 + 8 * (lg >> 1) + 2 * lq + (lg & 1)] = cs;
+        }
       }
-      tpar ^= 1;
+      macc += (double)racc;
+      if (!diag_blk && live) {
+        // the part's 4 quadrant warps have stored their column partials: each warp combines
+        // and flushes 16 of the part's W columns (balanced; no shared-memory atomics); the
+        // other parity slice takes the next tile meanwhile
+        asm volatile("bar.sync %0, 128;" ::"r"(8 + g.part) : "memory");
+        constexpr int CPW = G::W / 4;  // columns flushed per warp
+        for (int cc = lane; cc < CPW; cc += 32) {
+          const int col = g.q * CPW + cc;
+          const float x = (cpart[col] + cpart[G::W + col]) + (cpart[2 * G::W + col] + cpart[3 * G::W + col]);
+          const int64_t j = cb + col;
+          if (j < n && x != 0.f) atomicAdd(p.mass_out + j, (double)x * sd2);
+        }
+        // the slot parity alternates between barrier tiles only: a slot is rewritten two
+        // barriers after it was read (a diagonal tile in between has no barrier)
+        tpar ^= 1;
+      }
     }
     if (valid) atomicAdd(p.mass_out + lr, macc * sd2);  // every column slice adds its part
   }
