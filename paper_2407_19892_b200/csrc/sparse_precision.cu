@@ -414,7 +414,8 @@ struct FusedParams {
   unsigned long long* coo_count;
   int64_t capacity;
   float* thr_out;          // kSeed: per-row t-th largest sampled |ψ| (accumulator units)
-  double* mass_out;        // mode 2 (plain): row masses Σ_{j≠i} |ψ_ij| (atomic partials)
+  double* mass_out;        // mode 2: row masses Σ_{j≠i} |ψ_ij| in accumulator units (atomic
+                           // partials; times 2^-2e by scale_pow2 after the pass)
   unsigned long long* hist_out;  // mode 3 (plain): counts of upper entries (j > i) with
                                  // |ψ| > τ in 256 log buckets b = min(255, (bits|ψ| - bits τ) >> hshift)
   int hshift;
@@ -924,14 +925,14 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
             const int64_t j = cb + c * 32 + lane;
             const float v = acc[c * 32 + lane];
             acc[c * 32 + lane] = 0.f;
-            if (j < p.n && v != 0.f) atomicAdd(p.mass_out + j, (double)v * (double)sd2);
+            if (j < p.n && v != 0.f) atomicAdd(p.mass_out + j, (double)v);
           }
         }
         tpar ^= 1;
       }
     }
-    if (p.mode == 2) {  // both column halves add their partial row mass (unscaled ψ units)
-      if (valid) atomicAdd(p.mass_out + lr, macc * (double)sd2);
+    if (p.mode == 2) {  // both column halves add their partial row mass (accumulator units)
+      if (valid) atomicAdd(p.mass_out + lr, macc);
       continue;
     }
     if (p.mode != 0) continue;  // modes 1, 3: nothing per row
@@ -1134,8 +1135,6 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
   using G = EpiGeom<EPW>;
   const G g(warp, lane);
   const int lq = lane & 3, lg = lane >> 2;  // 16x256b fragment coordinates
-  const float sd = ldexpf(1.f, -p.sc->exp2);
-  const double sd2 = (double)sd * (double)sd;
   const int64_t n = p.n;
   const uint32_t trow = tmem_base + ((uint32_t)(g.q * 32) << 16) + (uint32_t)(g.part * G::W);
   const int coff = g.col_off();
@@ -1159,6 +1158,7 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
     const int64_t lr = rbase + lg + 8 * lq;
     const bool valid = lr < p.rows;
     double macc = 0.0;
+    float racc = 0.f;  // row sums of up to 16 tiles (fp32), then into macc (fp64)
     TileIter<kSymList, PAIR> ti;
     ti.start(p, u, uj, ub, u0, ustep);
     for (int s = 0; s < ntiles; ++s) {
@@ -1177,7 +1177,6 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
       buf ^= 1;
       tphase ^= (uint32_t)(buf == 0);
       float* cpart = scratch_all + (size_t)(tpar * G::P + g.part) * 4 * G::W;  // [quadrant][W]
-      float racc = 0.f;  // this tile's row sum (fp32 over 2 chunks, then fp64)
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) {
         // 32 rows x 32 columns in the 16x256b layout (two 16-lane loads): this thread holds
@@ -1257,7 +1256,10 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
           cpart[g.q * G::W + c * 32 + 8 * (lg >> 1) + 2 * lq + (lg & 1)] = cs;
         }
       }
-      macc += (double)racc;
+      if ((s & 15) == 15) {
+        macc += (double)racc;
+        racc = 0.f;
+      }
       if (!diag_blk && live) {
         // the part's 4 quadrant warps have stored their column partials: each warp combines
         // and flushes 16 of the part's W columns (balanced; no shared-memory atomics); the
@@ -1268,14 +1270,14 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
           const int col = g.q * CPW + cc;
           const float x = (cpart[col] + cpart[G::W + col]) + (cpart[2 * G::W + col] + cpart[3 * G::W + col]);
           const int64_t j = cb + col;
-          if (j < n && x != 0.f) atomicAdd(p.mass_out + j, (double)x * sd2);
+          if (j < n && x != 0.f) atomicAdd(p.mass_out + j, (double)x);
         }
         // the slot parity alternates between barrier tiles only: a slot is rewritten two
         // barriers after it was read (a diagonal tile in between has no barrier)
         tpar ^= 1;
       }
     }
-    if (valid) atomicAdd(p.mass_out + lr, macc * sd2);  // every column slice adds its part
+    if (valid) atomicAdd(p.mass_out + lr, macc + (double)racc);  // every column slice adds its part
   }
 }
 
@@ -3349,6 +3351,13 @@ extern "C" ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t* cand_key,
 namespace ggm {
 namespace sp {
 
+// x *= 2^-2e (the row masses from accumulator units to ψ units; a power of two: exact)
+__global__ void scale_pow2(double* __restrict__ x, int64_t n, const DevScalars* __restrict__ sc) {
+  const double f = ldexp(1.0, -2 * sc->exp2);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= f;
+}
 __global__ void scale_rows(const float* __restrict__ V, const double* __restrict__ w, int64_t n,
                            int k, float* __restrict__ Vs, double* __restrict__ sq) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * (int64_t)k;
@@ -3809,7 +3818,8 @@ extern "C" ggm_status ggm_sparse_precision_overall(
     }
     st = launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
     if (st != GGM_OK) return st;
-    launches += 4;
+    scale_pow2<<<blocks(n), 256, 0, s>>>(w.w, n, sw.sc);  // accumulator -> ψ units (exact)
+    launches += 5;
   }
   scale_rows<<<blocks(n * (int64_t)k), 256, 0, s>>>(V, op.downweight ? w.w : nullptr, n, k, w.Vs, w.sq);
   GGM_CUDA_TRY(cudaGetLastError());

@@ -139,3 +139,19 @@ def test_overall_spec_rank1_example(G):
     rp, c, val = _run(G, v, [2.0], 1)
     assert rp.tolist() == [0, 1, 2, 2] and c.tolist() == [1, 0]
     assert np.allclose(val, [1.0, 1.0], rtol=1e-6)
+
+
+@pytest.mark.parametrize("plain", [False, True])
+@pytest.mark.parametrize("n,k,N,m", [(1000, 64, 3000, 0), (2053, 100, 20530, 3), (129, 128, 64, 1)])
+def test_overall_mass_epilogues(G, monkeypatch, plain, n, k, N, m):
+    """Row masses of the down-weighting from the symmetric 16x256b-fragment epilogue
+    (default) and from the plain list epilogue (GGM_OVERALL_PLAIN_MASS=1): both against the
+    oracle, on axes whose length is not a multiple of the 32-row warp slice."""
+    if plain:
+        monkeypatch.setenv("GGM_OVERALL_PLAIN_MASS", "1")
+    else:
+        monkeypatch.delenv("GGM_OVERALL_PLAIN_MASS", raising=False)
+    V, lam = gen.small_factor(n * 11 + k + N, n, k)
+    rp, c, v = _run(G, V, lam, N, True, m)
+    st = check_overall(rp, c, v, V, lam, N, True, m)
+    assert st["excused"] <= max(2, st["edges"] // 500), st
