@@ -416,12 +416,15 @@ ggm_status ggm_sparse_precision_overall(int64_t n, int k, const float *V, const 
                                         int64_t capacity, int64_t *nnz_out, void *workspace,
                                         size_t workspace_bytes, void *stream);
 
-/* Candidate path of this thread's last ggm_sparse_precision_overall call: 0 = the per-row
- * top-t1 lists held the top N pairs (no saturated row), 2 = lists + the saturated rows'
- * block, 1 = histogram + full threshold pass; -1 before any call.  *saturated (optional) =
- * rows whose t1-th listed score reached L3.  ms (optional, filled when ggm_set_timing(1)
- * was on): device time of the phases (row masses + scaling, top-t1 lists, bound L3 +
- * saturation, candidate pass, ranking + CSR). */
+/* Candidate path of this thread's last ggm_sparse_precision_overall call: 3 = a global
+ * threshold τ from a uniform pair sample + one symmetric pass with per-row bounds
+ * min(top-m bound, τ), exact once >= n_edges pairs exceed τ (default from n >= 65,536;
+ * otherwise, or when its checks fail, the lists paths): 0 = the per-row top-t1 lists held
+ * the top N pairs (no saturated row), 2 = lists + the saturated rows' block, 1 = histogram
+ * + full threshold pass; -1 before any call.  *saturated (optional) = rows whose t1-th
+ * listed score reached L3 (0 on path 3).  ms (optional, filled when ggm_set_timing(1) was
+ * on): device time of the phases (row masses + scaling, top-t1 lists or the path-3 sample +
+ * pass, bound L3 + saturation, candidate pass, ranking + CSR). */
 int ggm_overall_last_path(int64_t *saturated, float ms[5]);
 
 /* ------------------------------------------------------------------------------------

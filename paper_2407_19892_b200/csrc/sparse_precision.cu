@@ -239,6 +239,50 @@ __global__ void fill_tau(float* __restrict__ thr, int64_t n, float tau,
        i += (int64_t)gridDim.x * blockDim.x)
     thr[i] = ts;
 }
+__global__ void cap_tau(float* __restrict__ thr, int64_t n, float tau,
+                        const DevScalars* __restrict__ sc) {
+  const float ts = ldexpf(tau, 2 * sc->exp2);  // ψ units -> accumulator units
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    thr[i] = fminf(thr[i], ts);
+}
+// overall rules, global-threshold pass: the pairs (i < j, original ids) of the exact
+// candidates with |ψ| > τ, once each (both directions are candidates: bounds <= τ), as pair
+// keys i*n + j and signed values; *count counts all (only the first cap are written)
+__global__ void sym_upper_pairs(const uint32_t* __restrict__ skey, const uint2* __restrict__ sval,
+                                int64_t ncand, int64_t n, const int32_t* __restrict__ perm,
+                                float tau, int64_t cap, unsigned long long* count,
+                                uint64_t* __restrict__ pkey, float* __restrict__ score) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ncand; base += stride) {
+    const int64_t e = base + threadIdx.x;
+    bool keep = false;
+    int64_t i = 0, j = 0;
+    float v = 0.f;
+    if (e < ncand) {
+      const uint32_t t = skey[e];
+      if (t != 0xFFFFFFFFu) {
+        const uint2 x = sval[e];
+        v = __uint_as_float(x.y);
+        i = perm[t];
+        j = perm[x.x];
+        keep = i < j && fabsf(v) > tau;
+      }
+    }
+    const uint32_t bm = __ballot_sync(0xffffffffu, keep);
+    unsigned long long b0 = 0;
+    if (lane == 0 && bm) b0 = atomicAdd(count, (unsigned long long)__popc(bm));
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (keep) {
+      const int64_t pos = (int64_t)b0 + __popc(bm & ((1u << lane) - 1u));
+      if (pos < cap) {
+        pkey[pos] = (uint64_t)i * (uint64_t)n + (uint64_t)j;
+        score[pos] = v;
+      }
+    }
+  }
+}
 // symmetric threshold mode: candidates with |ψ| > τ (exact values) -> COO (original row * n +
 // original column, ψ); count in *count (entries beyond capacity are counted, not written)
 __global__ void sym_threshold_coo(const uint32_t* __restrict__ skey, const uint2* __restrict__ sval,
@@ -2235,6 +2279,14 @@ struct SeedFracScope {
   explicit SeedFracScope(int f) : saved(g_seed_frac_override) { g_seed_frac_override = f; }
   ~SeedFracScope() { g_seed_frac_override = saved; }
 };
+// extra symmetric candidate-pool entries for the next plans on this thread (the overall
+// rules' global-threshold pass: every directed entry above τ on top of the top-m lists)
+static thread_local int64_t g_cand_extra = 0;
+struct CandExtraScope {
+  int64_t saved;
+  explicit CandExtraScope(int64_t e) : saved(g_cand_extra) { g_cand_extra = e; }
+  ~CandExtraScope() { g_cand_extra = saved; }
+};
 
 static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end,
                             const ggm_sparsify_opts* o, int64_t capacity, Plan* pl) {
@@ -2333,7 +2385,7 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
     // room for the output capacity + 25 % (overflow -> exact plain recomputation)
     const int64_t want = pl->mode == 1 ? std::max<int64_t>(capacity + capacity / 4, int64_t(1) << 20)
                                        : n * per_row;
-    pl->cand_total = pl->sym ? want + (int64_t)sms * 16 * kCandChunk * 2 : 0;
+    pl->cand_total = pl->sym ? want + g_cand_extra + (int64_t)sms * 16 * kCandChunk * 2 : 0;
   }
   pl->sort_temp_bytes = 0;
   if (pl->sym) {
@@ -2674,7 +2726,7 @@ static void recompute_pool(const Work& w, int64_t ncand, int64_t n, int k, int t
 static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, const double* lambda,
                               int64_t n, int k, const FusedParams& fp, cudaStream_t s,
                               int seed_ulo = -1, int seed_uhi = -1,
-                              const float* thr_all = nullptr) {
+                              const float* thr_all = nullptr, float tau_cap = 0.f) {
   const int sms = num_sms();
   ggm_status st;
     // (1) rows in descending ||U_i|| order (CUB sort of the row norms), split in that order
@@ -2724,6 +2776,10 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
     seed_bounds<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(
         w.thr, w.rn_s, &w.sc->rn_max_bits, n, k, w.sc);
     count_launches(1);
+    if (tau_cap > 0.f) {  // bound_i = min(top-t bound_i, τ): also every entry above τ
+      cap_tau<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, n, tau_cap, w.sc);
+      count_launches(1);
+    }
   }
   // (3) order rows (= columns) by their bound: sort (bound, original id) -> the final
   // permutation and the permuted bounds; re-split in that order, so the 32 columns of
@@ -3548,6 +3604,90 @@ using namespace ggm::sp;
 
 namespace {
 
+// Overall rules, path 3 (one symmetric pass for the whole candidate set): per-row bounds
+// min(top-m seed bound, τ), so the pool holds every directed entry above τ and each row's
+// top-m candidates.  After the exact re-evaluation: the pairs (i < j) with |ψ| > τ ->
+// pkey/score (all counted in *d_count, the first cap written) and each row's exact top m ->
+// row_ptr/col/val (stride m).  GGM_ERR_CAPACITY: the pool overflowed (the caller falls back).
+static ggm_status sym_tau_topm(int64_t n, int k, const float* V, const double* lambda, int m,
+                               float tau, int64_t extra, void* ws, size_t ws_bytes,
+                               uint64_t* pkey, float* score, int64_t cap,
+                               unsigned long long* d_count, int64_t* npairs, int64_t* row_ptr,
+                               int32_t* col, float* val, cudaStream_t s) {
+  ggm_sparsify_opts so{};
+  so.mode = 0;
+  so.topk = m;
+  so.symmetric = 1;
+  Plan pl;
+  ggm_status st;
+  {
+    CandExtraScope ce(extra);
+    st = make_plan(n, k, 0, n, &so, n * (int64_t)m, &pl);
+  }
+  if (st != GGM_OK) return st;
+  if (!pl.sym) return fail(GGM_ERR_UNSUPPORTED, "overall path 3 needs the symmetric scheme");
+  reset_launches();
+  Work w;
+  if (ws_bytes < carve(pl, ws, &w)) return fail(GGM_ERR_INVALID_ARGUMENT, "overall path 3 workspace");
+  const int sms = num_sms();
+  GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
+  absmax_check<<<(int)std::max<int64_t>(1, std::min<int64_t>((n * k + 255) / 256, sms * 8)), 256, 0, s>>>(
+      V, lambda, n, k, w.sc);
+  scale_finalize<<<1, 1, 0, s>>>(w.sc);
+  count_launches(2);
+  FusedParams fp = base_params(pl, w, n, 0);
+  fp.tau = 0.f;
+  st = sym_prepare(pl, w, V, lambda, n, k, fp, s, -1, -1, nullptr, tau);
+  if (st != GGM_OK) return st;
+  st = sym_main(pl, w, fp, 0, (int)pl.NBu, s);
+  if (st != GGM_OK) return st;
+  DevScalars hs;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
+  if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
+  if (hs.cand_overflow) return fail(GGM_ERR_CAPACITY, "overall path 3: candidate pool overflow");
+  const int64_t ncand = (int64_t)std::min<unsigned long long>(hs.cand_alloc, pl.cand_total);
+  GGM_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
+  if (ncand > 0) {
+    size_t tb = pl.sort_temp_bytes;
+    int ebits = 1;
+    while ((int64_t(1) << ebits) <= n) ++ebits;
+    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
+                                                 ncand, 0, ebits, s));
+    if (pl.screen) recompute_pool(w, ncand, n, k, 0, sms, s);  // every candidate exact
+    sym_upper_pairs<<<(int)std::min<int64_t>((ncand + 255) / 256, sms * 16), 256, 0, s>>>(
+        w.skey, w.sval, ncand, n, w.perm, tau, cap, d_count, pkey, score);
+    count_launches(1);
+  }
+  if (m <= 5)
+    launch_merge_sym_t<5>(w, pl, ncand, row_ptr, col, val, s);
+  else if (m <= 10)
+    launch_merge_sym_t<10>(w, pl, ncand, row_ptr, col, val, s);
+  else if (m <= 16)
+    launch_merge_sym_t<16>(w, pl, ncand, row_ptr, col, val, s);
+  else
+    launch_merge_sym_t<32>(w, pl, ncand, row_ptr, col, val, s);
+  count_launches(1);
+  unsigned long long hc = 0;
+  GGM_CUDA_TRY(cudaMemcpyAsync(&hc, d_count, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  GGM_CUDA_TRY(cudaStreamSynchronize(s));
+  GGM_CUDA_TRY(cudaGetLastError());
+  *npairs = (int64_t)hc;
+  return GGM_OK;
+}
+
+// path 3 sample: rows (s n)/R + n/(2R), s < R (a stratified sample of the axis)
+__global__ void sample_rows(int32_t* __restrict__ ids, int64_t R, int64_t n) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
+       q += (int64_t)gridDim.x * blockDim.x)
+    ids[q] = (int32_t)(q * n / R + n / (2 * R) < n ? q * n / R + n / (2 * R) : n - 1);
+}
+constexpr int64_t kOverallSampleRows = 16384;  // path 3: rows of the pair sample
+constexpr int64_t kOverallPath3MinN = 65536;   // path 3 by default from this axis length
+constexpr double kOverallTauMargin = 1.25;      // τ: sampled rank of 1.25 N pairs (2.5 N directed)
+static int64_t overall_path3_extra(int64_t N) { return 4 * N; }
+
 constexpr int kOverallSeedFrac = 8;  // seed sample of the top-t1 lists pass (see make_plan)
 thread_local int g_overall_path = -1;  // 0: lists only, 1: histogram + threshold, 2: block
 thread_local int64_t g_overall_sat = 0;  // saturated rows at L3
@@ -3633,7 +3773,27 @@ ggm_status overall_plan(int64_t n, int k, const ggm_overall_opts* o, int64_t can
   so.tau = 0.f;
   st = ggm_sparse_precision_workspace(n, k, 0, n, &so, cand_capacity, &b);
   if (st != GGM_OK) return st;
-  op->ws_sub = std::max(mx, b);
+  mx = std::max(mx, b);
+  {  // path 3: the sample's top-T lists and the global-threshold pass (if it applies)
+    const int64_t R = std::min<int64_t>(n, kOverallSampleRows);
+    if (R >= 3) {
+      ggm_sparsify_opts s3{};
+      s3.mode = 0;
+      s3.topk = (int)std::min<int64_t>(GGM_MAX_TOPK, R - 1);
+      if (ggm_sparse_precision_workspace(R, k, 0, R, &s3, R * s3.topk, &b) == GGM_OK)
+        mx = std::max(mx, b);
+    }
+    ggm_sparsify_opts s4{};
+    s4.mode = 0;
+    s4.topk = std::max(op->m, 1);
+    s4.symmetric = 1;
+    Plan pl;
+    Work wk;
+    CandExtraScope ce(overall_path3_extra(op->N));
+    if (make_plan(n, k, 0, n, &s4, n * (int64_t)s4.topk, &pl) == GGM_OK && pl.sym)
+      mx = std::max(mx, carve(pl, nullptr, &wk));
+  }
+  op->ws_sub = mx;
   size_t c = 0, t = 0;
   const int64_t L = op->n * op->t1 + cand_capacity + 2 * op->E_max;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, t, (const float*)nullptr, (float*)nullptr,
@@ -3826,6 +3986,75 @@ extern "C" ggm_status ggm_sparse_precision_overall(
   ++launches;
   // (2) per-row top-t1 of Ψ'
   ph.mark(1);
+  // Path 3 (default from kOverallPath3MinN rows; GGM_OVERALL_PATH=3 forces it): a global
+  // threshold τ from a uniform pair sample (the top-T lists of R stratified sample rows
+  // among themselves: (R(R-1))/(n(n-1)) of all pairs; directed counts / 2 never exceed the
+  // sample's pair counts, so τ errs low), set at the sampled rank of 2.5 N directed entries
+  // (~1.25 N pairs above it); then ONE symmetric pass with bounds min(top-m bound, τ) gives
+  // every pair above τ and each row's top m.  Exact when >= N pairs exceed τ (checked);
+  // otherwise, or when the sample / pool / capacities do not fit, the lists path below runs.
+  const char* force = std::getenv("GGM_OVERALL_PATH");  // test hook: "1" hist, "2" block, "3"
+  int lst = op.t1;  // stride of the per-row lists used by the min-edges rule
+  int64_t nc = 0;
+  bool done3 = false;
+  if (force ? force[0] == '3' : n >= kOverallPath3MinN) {
+    const int64_t C = op.cand_cap + n * op.t1;  // pair-candidate arrays
+    const int64_t R = std::min<int64_t>(n, kOverallSampleRows);
+    const int T = (int)std::min<int64_t>(GGM_MAX_TOPK, R - 1);
+    float tau = 0.f;
+    if (R >= 3 && R * T <= op.cand_cap) {
+      const float* F = w.Vs;
+      if (R < n) {
+        sample_rows<<<blocks(R), 256, 0, s>>>(w.rid, R, n);
+        gather_rows<<<blocks(R * k), 256, 0, s>>>(w.Vs, w.rid, R, k, w.Vsub);
+        F = w.Vsub;
+        launches += 2;
+      }
+      ggm_sparsify_opts so{};
+      so.mode = 0;
+      so.topk = T;
+      int64_t nnz = 0;
+      if (ggm_sparse_precision(R, k, F, lambda, 0, R, &so, w.rp3, w.col3, w.val3, op.cand_cap,
+                               &nnz, w.sub, op.ws_sub, stream) == GGM_OK) {
+        launches += ggm_last_launches();
+        const double pr = (double)R * (double)(R - 1) / ((double)n * (double)(n - 1));
+        // directed entries of the sample: 2 x its pairs above the level
+        const int64_t K = (int64_t)std::ceil(2.0 * kOverallTauMargin * (double)op.N * pr);
+        if (K >= 64 && K <= R * T) {
+          abs_copy<<<blocks(R * T), 256, 0, s>>>(w.val3, R * T, w.ak);
+          size_t tb = op.cub_tmp;
+          GGM_CUDA_TRY(cub::DeviceRadixSort::SortKeysDescending(w.cub, tb, w.ak, w.ak_s, R * T, 0, 32, s));
+          GGM_CUDA_TRY(cudaMemcpyAsync(&tau, w.ak_s + K - 1, sizeof(float), cudaMemcpyDeviceToHost, s));
+          GGM_CUDA_TRY(cudaStreamSynchronize(s));
+          launches += 2;
+        }
+      }
+    }
+    if (std::getenv("GGM_DEBUG_OVERALL"))
+      fprintf(stderr, "overall path 3: sample R=%lld T=%d cand_cap %lld -> tau %g\n", (long long)R, T,
+              (long long)op.cand_cap, (double)tau);
+    if (tau > 0.f) {
+      int64_t np = 0;
+      const ggm_status st3 = sym_tau_topm(n, k, w.Vs, lambda, std::max(op.m, 1), tau,
+                                          overall_path3_extra(op.N), w.sub, op.ws_sub, w.pk,
+                                          w.sc, C, w.cnt, &np, w.rp1, w.col1, w.val1, s);
+      launches += ggm_last_launches();
+      if (std::getenv("GGM_DEBUG_OVERALL"))
+        fprintf(stderr, "overall path 3: R=%lld T=%d tau=%g status=%d pairs=%lld (N=%lld, cap %lld)\n",
+                (long long)R, T, (double)tau, (int)st3, (long long)np, (long long)op.N, (long long)C);
+      if (st3 == GGM_ERR_DOMAIN) return st3;
+      if (st3 == GGM_OK && np >= op.N && np <= C) {
+        done3 = true;
+        nc = np;
+        lst = std::max(op.m, 1);
+        g_overall_path = 3;
+        g_overall_sat = 0;
+        ph.mark(2);
+        ph.mark(3);
+      }
+    }
+  }
+  if (!done3) {
   {
     ggm_sparsify_opts so{};
     so.mode = 0;
@@ -3891,8 +4120,7 @@ extern "C" ggm_status ggm_sparse_precision_overall(
   unsigned int nsat = 0;
   GGM_CUDA_TRY(cudaMemcpyAsync(&nsat, w.min_bits, sizeof(nsat), cudaMemcpyDeviceToHost, s));
   GGM_CUDA_TRY(cudaStreamSynchronize(s));
-  int64_t nc = nu1;
-  const char* force = std::getenv("GGM_OVERALL_PATH");  // test hook: "1" hist, "2" block
+  nc = nu1;
   g_overall_path = L3 <= 0.f ? 1 : (nsat == 0 ? 0 : (2 * (int64_t)nsat <= n ? 2 : 1));
   if (force && L3 > 0.f && (force[0] == '1' || force[0] == '2')) g_overall_path = force[0] - '0';
   g_overall_sat = nsat;
@@ -4015,6 +4243,7 @@ extern "C" ggm_status ggm_sparse_precision_overall(
       launches += 1;
     }
   }
+  }  // lists path
   // (4) candidates ranked by (score desc, i, j): stable sorts by pair key, then by |score|
   ph.mark(4);
   const int64_t Ntop = std::min<int64_t>(op.N, nc);
@@ -4033,8 +4262,8 @@ extern "C" ggm_status ggm_sparse_precision_overall(
   take_top<<<blocks(Ntop), 256, 0, s>>>(w.idx2, Ntop, w.pk, w.sc, w.uk, w.uv);
   int64_t nu = Ntop;
   if (op.m > 0) {
-    min_edge_pairs<<<blocks(n), 256, 0, s>>>(w.col1, w.val1, n, op.t1, op.m, w.uk + Ntop);
-    min_edge_vals<<<blocks(n * op.m), 256, 0, s>>>(w.col1, w.val1, w.uk + Ntop, n, op.t1, op.m, w.uv + Ntop);
+    min_edge_pairs<<<blocks(n), 256, 0, s>>>(w.col1, w.val1, n, lst, op.m, w.uk + Ntop);
+    min_edge_vals<<<blocks(n * op.m), 256, 0, s>>>(w.col1, w.val1, w.uk + Ntop, n, lst, op.m, w.uv + Ntop);
     nu += n * op.m;
   }
   launches += 5 + (op.m > 0 ? 2 : 0);

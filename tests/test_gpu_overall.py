@@ -29,14 +29,15 @@ def _run(G, V, lam, N, dw=False, m=0, **kw):
     return rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy()
 
 
-@pytest.fixture(params=["auto", "hist", "block"])
+@pytest.fixture(params=["auto", "hist", "block", "gthr"])
 def path(request, monkeypatch):
     """auto: the driver's choice; hist / block: force the histogram + threshold passes or
-    the saturated-block pass (whenever the lists give a bound)."""
+    the saturated-block pass (whenever the lists give a bound); gthr: force the sampled
+    global-threshold pass (path 3; falls back to the lists when its checks fail)."""
     if request.param == "auto":
         monkeypatch.delenv("GGM_OVERALL_PATH", raising=False)
     else:
-        monkeypatch.setenv("GGM_OVERALL_PATH", "1" if request.param == "hist" else "2")
+        monkeypatch.setenv("GGM_OVERALL_PATH", {"hist": "1", "block": "2", "gthr": "3"}[request.param])
     return request.param
 
 
@@ -109,6 +110,7 @@ def test_overall_at_scale_properties(G):
     ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
     rp, c, v = G.ggm_sparse_precision_overall(Vd, ld, N, min_edges=m)
     print("overall path, saturated rows:", G.overall_last_path())
+    assert G.overall_last_path()[0] == 3  # the sampled global-threshold pass at this size
     rp, c, v = rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy()
     rows = np.repeat(np.arange(n), np.diff(rp))
     up = rows < c
