@@ -445,7 +445,8 @@ def overall_timing(G, torch, V, lam):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     path, sat = G.overall_last_path()
-    return {"path": {0: "lists", 1: "histogram+threshold", 2: "lists+saturated block"}.get(path, path),
+    return {"path": {0: "lists", 1: "histogram+threshold", 2: "lists+saturated block",
+                     3: "sampled global threshold + one symmetric pass"}.get(path, path),
             "saturated_rows": sat, "phases_ms": G.overall_last_timing(), "n": int(n), "n_edges": 10 * int(n), "downweight": True, "min_edges": 1,
             "edges_kept": int(c.numel()) // 2, "ms": ms, "entries_per_s": float(n) * n / (ms * 1e-3),
             "launches": G.last_launches()}
