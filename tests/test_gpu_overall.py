@@ -68,11 +68,18 @@ def test_overall_all_zero_offdiagonal(G, path):
     assert len(c) == 0 and np.all(rp == 0)
 
 
+@pytest.mark.parametrize("force3", [False, True])
 @pytest.mark.parametrize("dw", [False, True])
-def test_overall_hub_vertices(G, dw):
+def test_overall_hub_vertices(G, monkeypatch, dw, force3):
     """40 hub rows with 8x the norm: without down-weighting the top pairs concentrate on the
     hubs, their lists saturate and the histogram + threshold path runs; with it, the
-    scores are rebalanced (the over-focus the paper describes)."""
+    scores are rebalanced (the over-focus the paper describes).  force3: the
+    sampled global-threshold path on the same input (the hubs make its sample lists
+    saturate: the estimate errs low, more pairs pass τ, the result is unchanged)."""
+    if force3:
+        monkeypatch.setenv("GGM_OVERALL_PATH", "3")
+    else:
+        monkeypatch.delenv("GGM_OVERALL_PATH", raising=False)
     n, k, N = 4000, 48, 40000
     V, lam = gen.small_factor(77, n, k)
     V = V.copy()
@@ -81,7 +88,9 @@ def test_overall_hub_vertices(G, dw):
     st = check_overall(rp, c, v, V, lam, N, dw, 1)
     assert st["excused"] <= max(2, st["edges"] // 500), st
     path, sat = G.overall_last_path()
-    if not dw:
+    if force3:
+        assert path == 3, (path, sat)
+    elif not dw:
         assert path != 0 and sat > 0, (path, sat)
 
 
