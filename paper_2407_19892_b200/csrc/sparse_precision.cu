@@ -104,7 +104,10 @@ struct DevScalars {
 // one 32x32 warp chunk in both directions, so a fresh reservation always fits
 constexpr int kCandChunk = 2048;
 static_assert(kCandChunk >= 2 * 32 * 32, "a warp chunk's candidates must fit one reservation");
-constexpr int kWindowSplit = 4;  // kSym/kSymList CTA-pair units per row block (sub-windows)
+#ifndef GGM_WSPLIT
+#define GGM_WSPLIT 8
+#endif
+constexpr int kWindowSplit = GGM_WSPLIT;  // kSym/kSymList CTA-pair units per row block (sub-windows)
 constexpr int64_t kSymAutoN = 16384;  // automatic symmetric scheme from this axis length (measured crossover 8192-16384)
 
 // ------------------------------------------------------------------ BK1a
