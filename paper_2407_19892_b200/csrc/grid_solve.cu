@@ -43,7 +43,13 @@ namespace ggm {
 namespace gs {
 
 constexpr int kMaxAxes = 8;
-constexpr int kThreads = 512;
+#ifndef GGM_SOLVE_THREADS
+#define GGM_SOLVE_THREADS 512
+#endif
+#ifndef GGM_SOLVE_MINB
+#define GGM_SOLVE_MINB 1
+#endif
+constexpr int kThreads = GGM_SOLVE_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxFastBins = 1024;  // private per-warp bins: kWarps x k_fast doubles
 
@@ -366,7 +372,7 @@ __device__ __forceinline__ double kkt_term(double lam, double g, double e, doubl
 // marginals and Σ log s), slam[T] (the point the next pass evaluates), th0[T], th1[T]
 // (SQUAREM iterates in log space; GD: the accepted λ and its marginals), private bins.
 template <int J, bool LOGS>
-__global__ void __launch_bounds__(kThreads, J <= 7 ? 2 : 1) solve_kernel(const SolveParams p) {
+__global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SOLVE_MINB) solve_kernel(const SolveParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
   const int T = p.T;
