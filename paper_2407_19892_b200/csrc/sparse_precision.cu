@@ -104,6 +104,8 @@ struct DevScalars {
 // one 32x32 warp chunk in both directions, so a fresh reservation always fits
 constexpr int kCandChunk = 2048;
 static_assert(kCandChunk >= 2 * 32 * 32, "a warp chunk's candidates must fit one reservation");
+constexpr int kRecCutRatio = 4;  // re-evaluation cuts when the pool averages > 4t per row
+constexpr int kRecCutMinT = 16;  // cuts (and the screened values they need) from t = 16
 #ifndef GGM_WSPLIT
 #define GGM_WSPLIT 8
 #endif
@@ -474,6 +476,8 @@ struct FusedParams {
   uint2* cand_val;         //       (source row i, ψ bits)
   int64_t cand_total;      //       pool capacity; warps reserve kCandChunk-entry chunks
   int screen;        // kSym: hi*hi screening MMAs only (candidates re-evaluated exactly)
+  int cand_vals;     // kSym: 1 = store each candidate's value (no screening: the final value;
+                     // screening: the screened value, read only by the re-evaluation cuts)
   int pair;          // CTA-pair kernel (host-side selection; the kernel's template PAIR)
   int wsplit;            // kSym / kSymList CTA pairs: each row block's window is cut into
                          // wsplit consecutive sub-windows, one unit each (unit u: sub-window
@@ -1537,7 +1541,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
           const uint32_t br = __ballot_sync(0xffffffffu, hr);
           const uint32_t bc = __ballot_sync(0xffffffffu, hc);
           if (mh) {
-            const uint32_t xb = __float_as_uint(sel32(VC, e) * sd2);
+            const uint32_t xb = p.cand_vals ? __float_as_uint(sel32(VC, e) * sd2) : 0u;
             if (hr) {  // candidate (i -> j): target row i
               const int64_t pos = at + __popc(br & lt);
               GGM_DCHECK(pos < p.cand_total && gi < n && col0 + (int)e < n);
@@ -2249,6 +2253,8 @@ struct Plan {
   int64_t NBu;   // kSym/kSeed units over the axis: NB or ceil(NB/2)
   int sym;       // symmetric scheme (kSeed + kSym + merge_sym)
   int screen;    // symmetric scheme: hi*hi screening + exact re-evaluation of candidates
+  int rec_cut;   // screening, mode 0: per-row re-evaluation cuts allowed (1: when the pool
+                 // is candidate-heavy, 2: always — GGM_REC_CUT=1); needs the screened values
   int SS;        // seed column-tile stride
   int64_t NB;    // 128-row blocks of the axis
   int64_t cand_total;  // kSym: candidate pool capacity (entries)
@@ -2350,6 +2356,14 @@ static ggm_status make_plan(int64_t n, int k, int64_t row_begin, int64_t row_end
   const bool sym_ok = (o->mode == 0 || o->mode == 1) && full_axis && pl->resident;
   pl->sym = sym_ok && (o->symmetric == 1 || (o->symmetric == 0 && n >= kSymAutoN)) ? 1 : 0;
   pl->screen = pl->sym && k <= 128 && !getenv("GGM_NO_SCREEN") ? 1 : 0;
+  // re-evaluation cuts pay only on candidate-heavy pools (the top-32 lists of the overall
+  // rules, ~10t candidates per row); at top-10 (~2t per row) they keep nearly every
+  // candidate, and without them the epilogue skips each candidate's screened value
+  pl->rec_cut = 0;
+  if (pl->screen && pl->mode == 0) {
+    pl->rec_cut = pl->t >= kRecCutMinT ? 1 : 0;
+    if (const char* e = getenv("GGM_REC_CUT")) pl->rec_cut = atoi(e) != 0 ? 2 : 0;  // tests: both forms
+  }
   // candidates: ~ t x 16 / 2 per row expected (seed samples 1/16 of the columns, half of
   // each row's columns come from the transposed direction); regions hold 2x that on average
   // pool: 2x the expected candidates + one chunk per epilogue warp of partially used space
@@ -2686,16 +2700,16 @@ static FusedParams base_params(const Plan& pl, const Work& w, int64_t n, int64_t
 // the values.  The cuts pay only when rows hold many more candidates than t (the top-32
 // lists of the overall rules: re-evaluation 133 -> 38 + 10 ms at n = 10^6); at ~2t per row
 // (C4/C5 top-10) they keep nearly every candidate and cost a pass (C5: 2.09 vs 2.42 +
-// 0.10 ms), so they run when the pool averages more than kRecCutRatio t per row.  t <= 0:
-// every candidate (threshold mode).
-constexpr int kRecCutRatio = 4;
-static void recompute_pool(const Work& w, int64_t ncand, int64_t n, int k, int t, int sms,
-                           cudaStream_t s) {
+// 0.10 ms), so they run when the pool averages more than kRecCutRatio t per row (cut_mode
+// 1, plans with t >= kRecCutMinT, whose epilogue stores the screened values; 2: always;
+// 0: never).  t <= 0: every candidate (threshold mode).
+static void recompute_pool(const Work& w, int64_t ncand, int64_t n, int k, int t, int cut_mode,
+                           int sms, cudaStream_t s) {
   cand_row_offsets<<<(int)std::min<int64_t>((n + 256) / 256, sms * 16), 256, 0, s>>>(
       w.skey, ncand, n, w.roff);
   const float* cut = nullptr;
-  bool use_cut = t > 0 && ncand > (int64_t)kRecCutRatio * t * n;
-  if (const char* e = getenv("GGM_REC_CUT")) use_cut = t > 0 && atoi(e) != 0;  // tests: both forms
+  const bool use_cut =
+      t > 0 && (cut_mode == 2 || (cut_mode == 1 && ncand > (int64_t)kRecCutRatio * t * n));
   if (use_cut) {
     const int blocks = (int)std::min<int64_t>((n + 127) / 128, sms * 16);
     if (t <= 10)
@@ -2829,6 +2843,7 @@ static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int un
   fp.thr = pl.screen ? w.thr_s : w.thr_p;
   fp.thr_min = w.thr_cmin;
   fp.screen = pl.screen;
+  fp.cand_vals = (!pl.screen || pl.rec_cut) ? 1 : 0;
   fp.perm = w.perm;
   fp.cand_key = w.ckey;
   fp.cand_val = w.cval;
@@ -2979,7 +2994,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
         GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval,
                                                      w.sval, ncand, 0, ebits, s));
         if (pl.screen) {  // exact values of every screened candidate (no top-t filter)
-          recompute_pool(w, ncand, n, k, 0, sms, s);
+          recompute_pool(w, ncand, n, k, 0, 0, sms, s);
         }
         sym_threshold_coo<<<(int)std::min<int64_t>((ncand + 255) / 256, sms * 16), 256, 0, s>>>(
             w.skey, w.sval, ncand, n, w.perm, opts->tau, capacity, &w.sc->coo_count, w.key_in,
@@ -3040,7 +3055,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                    ncand, 0, ebits, s));
       if (pl.screen) {  // exact values of the screened candidates
-        recompute_pool(w, ncand, n, k, pl.t, sms, s);
+        recompute_pool(w, ncand, n, k, pl.t, pl.rec_cut, sms, s);
       }
     }
     if (pl.t <= 5)
@@ -3288,7 +3303,7 @@ static ggm_status sym_shard_impl(
     GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                  ncand, 0, ebits, s));
     if (pl.screen) {  // exact values before the buckets leave this rank
-      recompute_pool(w, ncand, n, k, pl.t, sms, s);
+      recompute_pool(w, ncand, n, k, pl.t, pl.rec_cut, sms, s);
     }
   }
   // destination buckets: rank r owns bound-order rows [lo_r, lo_{r+1}); unused pool slots
@@ -3658,7 +3673,7 @@ static ggm_status sym_tau_topm(int64_t n, int k, const float* V, const double* l
     while ((int64_t(1) << ebits) <= n) ++ebits;
     GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, w.ckey, w.skey, w.cval, w.sval,
                                                  ncand, 0, ebits, s));
-    if (pl.screen) recompute_pool(w, ncand, n, k, 0, sms, s);  // every candidate exact
+    if (pl.screen) recompute_pool(w, ncand, n, k, 0, 0, sms, s);  // every candidate exact
     sym_upper_pairs<<<(int)std::min<int64_t>((ncand + 255) / 256, sms * 16), 256, 0, s>>>(
         w.skey, w.sval, ncand, n, w.perm, tau, cap, d_count, pkey, score);
     count_launches(1);
