@@ -1414,7 +1414,11 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #endif
       tc_fence_after();
       const uint32_t taddr = trow + (uint32_t)(buf * kTileN);
-#ifdef GGM_EPI_BLOCK
+#ifndef GGM_EPI_STREAM
+      // both 32-column chunks loaded back to back, one wait, then the buffer is released
+      // before either filter runs (the streamed form — load, filter, load, release — holds
+      // the buffer through the first chunk's filter: C4 main 3.80 vs 3.75 ms,
+      // profiles/r02_logs/r02d_ab_epiblock.log)
       uint32_t v[G::NC][32];
       if (live) {
 #pragma unroll
@@ -1477,7 +1481,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) {
         const int col0 = cb + c * 32;
-#ifndef GGM_EPI_BLOCK
+#ifdef GGM_EPI_STREAM
         uint32_t vc[32];
         tmem_ld32_nowait(taddr + c * 32, vc);
         tmem_wait_ld(vc);
