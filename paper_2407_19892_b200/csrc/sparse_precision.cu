@@ -135,6 +135,23 @@ __global__ void absmax_check(const float* __restrict__ V, const double* __restri
   const int64_t total = n * (int64_t)k;
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  if (staged && (k & 3) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0) {
+    // float4 form: 4 consecutive columns of one row per load (k ≡ 0 mod 4, aligned V)
+    const float4* V4 = reinterpret_cast<const float4*>(V);
+    const int64_t total4 = total >> 2;
+    const int k4 = k >> 2;
+    const int cstep4 = (int)(step % k4);
+    int c4 = (int)(i0 % k4);
+    for (int64_t idx = i0; idx < total4; idx += step) {
+      const float4 v = __ldg(V4 + idx);
+      if (!isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w)) bad = 1;
+      const int c = 4 * c4;
+      m = fmaxf(m, fmaxf(fmaxf((float)(fabs((double)v.x) * sl[c]), (float)(fabs((double)v.y) * sl[c + 1])),
+                         fmaxf((float)(fabs((double)v.z) * sl[c + 2]), (float)(fabs((double)v.w) * sl[c + 3]))));
+      c4 += cstep4;
+      if (c4 >= k4) c4 -= k4;
+    }
+  } else {
   const int cstep = (int)(step % k);
   int c = (int)(i0 % k);  // column of idx, advanced incrementally (no division per element)
   for (int64_t idx = i0; idx < total; idx += step) {
@@ -151,6 +168,7 @@ __global__ void absmax_check(const float* __restrict__ V, const double* __restri
     m = fmaxf(m, u);
     c += cstep;
     if (c >= k) c -= k;
+  }
   }
   if (bad) atomicOr(&sc->flags, 1);
 #pragma unroll
@@ -170,6 +188,39 @@ __global__ void row_norms(const float* __restrict__ V, const double* __restrict_
                           int k, float* __restrict__ rn, unsigned int* __restrict__ rn_max_bits) {
   const int lane = threadIdx.x & 31;
   float wmax = 0.f;
+  if ((k & 3) == 0 && k <= 1024 && (reinterpret_cast<uintptr_t>(V) & 15) == 0) {
+    // float4 form: 8 lanes per row, 4 rows per warp step (λ staged in shared memory)
+    __shared__ double sl[1024];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) sl[c] = lam[c];
+    __syncthreads();
+    const int l8 = lane & 7, k4 = k >> 2;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wstep = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i0 = w0 * 4; i0 < n; i0 += wstep * 4) {
+      const int64_t i = i0 + (lane >> 3);
+      double acc = 0.0;
+      if (i < n) {
+        const float4* v4 = reinterpret_cast<const float4*>(V + i * k);
+        for (int j = l8; j < k4; j += 8) {
+          const float4 x = __ldg(v4 + j);
+          const double* l = sl + 4 * j;
+          acc += l[0] * (double)x.x * (double)x.x + l[1] * (double)x.y * (double)x.y +
+                 l[2] * (double)x.z * (double)x.z + l[3] * (double)x.w * (double)x.w;
+        }
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (i < n) {
+        const float f = (float)sqrt(acc);
+        if (l8 == 0) rn[i] = f;
+        wmax = fmaxf(wmax, f);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0) atomicMax(rn_max_bits, __float_as_uint(wmax));
+    return;
+  }
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
        i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     double acc = 0.0;
@@ -361,7 +412,7 @@ __device__ __forceinline__ void split2(double x, __half& h, __half& l) {
 // One thread per (row, 16-byte chunk): the 8 elements are split once and both the hi-array
 // and the lo-array chunk are written (sqrt(λ) staged in shared memory; 32-bit index math).
 constexpr int kSplitMaxK = 1024;
-__global__ void split_tile(const float* __restrict__ V, const double* __restrict__ lam,
+__global__ void split_tile_generic(const float* __restrict__ V, const double* __restrict__ lam,
                            int64_t n, int k, int KA, int KS, int TS, int64_t row0,
                            int64_t nrows_pad, const DevScalars* __restrict__ sc,
                            uint8_t* __restrict__ dst, const int32_t* __restrict__ perm = nullptr) {
@@ -428,6 +479,107 @@ __global__ void split_tile(const float* __restrict__ V, const double* __restrict
     *reinterpret_cast<uint4*>(dst + base + (size_t)a * kAtomBytes) = *reinterpret_cast<const uint4*>(oh);
     *reinterpret_cast<uint4*>(dst + base + (size_t)(KA + a) * kAtomBytes) =
         *reinterpret_cast<const uint4*>(ol);
+  }
+}
+
+// Fast form (8·KA ≤ 256 chunks per row, i.e. k ≤ 2048): a block is `rpb` rows × 8·KA
+// chunks, so every thread keeps one fixed chunk and its 8 source columns, scales
+// sqrt(λ_c)·s (as an fp32 pair sh + sl, |sl| ≤ 2⁻²⁴ sh) and tail positions in registers
+// across its grid-stride rows.  The split runs in fp32: p = fl(v·sh) with its exact
+// FMA error, hi = fp16(p), lo = fp16((p − hi) + err + v·sl), so hi + lo carries x = v·sqrt(λ)·s
+// to ~2⁻²² relative as before and |x − hi| ≤ 2⁻¹¹(1 + 2⁻¹²)|x| (inside the 1.1 slack of the
+// screening margins) — without the fp64 conversions of the generic form.  Full slots of a
+// k ≡ 0 (mod 4) factor are read with two float4 loads.
+__global__ void split_tile_fast(const float* __restrict__ V, const double* __restrict__ lam,
+                                int64_t n, int k, int KA, int KS, int TS, int64_t row0,
+                                int64_t nrows_pad, const DevScalars* __restrict__ sc,
+                                uint8_t* __restrict__ dst, const int32_t* __restrict__ perm) {
+  const int cpr = KA * 8;
+  const int rpb = blockDim.x / cpr;
+  const int ch = threadIdx.x % cpr, rsub = threadIdx.x / cpr;
+  if (rsub >= rpb) return;
+  const double s = ldexp(1.0, sc->exp2);
+  const int slot = ch >> 1;
+  const int r = k - 16 * KS;
+  int src[8], seg[8];
+  float sh[8], sl[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int pos = (ch & 1) * 8 + e;
+    src[e] = -1;
+    seg[e] = 0;
+    if (slot < KS || TS == 0) {
+      const int c = slot * 16 + pos;
+      if (c < k) src[e] = c;
+    } else if (slot < KS + TS) {
+      const int q = (slot - KS) * 16 + pos;
+      if (q < 3 * r) {
+        seg[e] = q / r;
+        src[e] = 16 * KS + q % r;
+      }
+    }
+    const double d = src[e] >= 0 ? sqrt(lam[src[e]]) * s : 0.0;
+    sh[e] = (float)d;
+    sl[e] = (float)(d - (double)sh[e]);
+  }
+  const int c0 = slot * 16 + (ch & 1) * 8;
+  const bool vec = (slot < KS || TS == 0) && (k & 3) == 0 && c0 + 8 <= k;
+  const int a = ch >> 3, c8 = ch & 7;
+  for (int64_t row = (int64_t)blockIdx.x * rpb + rsub; row < nrows_pad;
+       row += (int64_t)gridDim.x * rpb) {
+    int64_t g = row0 + row;
+    const bool real = g < n;
+    if (perm && real) g = perm[g];  // symmetric scheme: rows in bound order
+    float x[8];
+    if (real && vec) {
+      const float4* vp = reinterpret_cast<const float4*>(V + g * k + c0);
+      const float4 x0 = __ldg(vp), x1 = __ldg(vp + 1);
+      x[0] = x0.x; x[1] = x0.y; x[2] = x0.z; x[3] = x0.w;
+      x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = (real && src[e] >= 0) ? __ldg(V + g * k + src[e]) : 0.f;
+    }
+    __align__(16) __half oh[8];
+    __align__(16) __half ol[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float pr = x[e] * sh[e];
+      const float err = fmaf(x[e], sh[e], -pr);
+      const __half h = __float2half_rn(pr);
+      const __half l = __float2half_rn((pr - __half2float(h)) + fmaf(x[e], sl[e], err));
+      // plain slots: hi / lo; packed tail: B (hi array) [hi | lo | hi], A (lo array) [hi | hi | lo]
+      oh[e] = seg[e] == 1 ? l : h;
+      ol[e] = (seg[e] == 2 || (seg[e] == 0 && !(slot >= KS && TS > 0))) ? l : h;
+      if (src[e] < 0) {
+        oh[e] = __float2half(0.f);
+        ol[e] = __float2half(0.f);
+      }
+    }
+    const int64_t b = row / kRowsPerBlock;
+    const int rr = (int)(row % kRowsPerBlock);
+    const size_t base = (size_t)b * block_bytes(KA) + (size_t)rr * 128 + (size_t)((c8 ^ (rr & 7)) * 16);
+    *reinterpret_cast<uint4*>(dst + base + (size_t)a * kAtomBytes) = *reinterpret_cast<const uint4*>(oh);
+    *reinterpret_cast<uint4*>(dst + base + (size_t)(KA + a) * kAtomBytes) =
+        *reinterpret_cast<const uint4*>(ol);
+  }
+}
+
+// Operand split of rows [row0, row0 + nrows_pad) (padding rows past n are zero): the fast
+// form when a row's chunks fit one 256-thread block, the generic grid-stride form otherwise.
+static void launch_split(cudaStream_t st, int sms, const float* V, const double* lam, int64_t n,
+                         int k, int KA, int KS, int TS, int64_t row0, int64_t nrows_pad,
+                         const DevScalars* sc, uint8_t* dst, const int32_t* perm = nullptr) {
+  const int cpr = KA * 8;
+  if (cpr <= 256) {
+    const int rpb = 256 / cpr;
+    const int64_t blocks = (nrows_pad + rpb - 1) / rpb;
+    split_tile_fast<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, sms * 16)), cpr * rpb,
+                      0, st>>>(V, lam, n, k, KA, KS, TS, row0, nrows_pad, sc, dst, perm);
+  } else {
+    const int64_t tot = nrows_pad * cpr;
+    split_tile_generic<<<(int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, sms * 16)),
+                         256, 0, st>>>(V, lam, n, k, KA, KS, TS, row0, nrows_pad, sc, dst, perm);
   }
 }
 
@@ -2092,9 +2244,21 @@ __global__ void gather_u_bound(const float* __restrict__ V, const double* __rest
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int kp = rec_stride(k);
+  const bool vec = (k & 3) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0;
   for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n;
        p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const float* v = V + (int64_t)perm[p] * k;
+    if (vec) {  // k ≡ 0 (mod 4): kp = k, float4 rows
+      const float4* v4 = reinterpret_cast<const float4*>(v);
+      float4* u4 = reinterpret_cast<float4*>(Ub + p * kp);
+      for (int j = lane; j < (k >> 2); j += 32) {
+        const float4 x = __ldg(v4 + j);
+        const double* l = sl + 4 * j;
+        u4[j] = make_float4((float)((double)x.x * l[0]), (float)((double)x.y * l[1]),
+                            (float)((double)x.z * l[2]), (float)((double)x.w * l[3]));
+      }
+      continue;
+    }
     for (int c = lane; c < kp; c += 32) Ub[p * kp + c] = c < k ? (float)((double)v[c] * sl[c]) : 0.f;
   }
 }
@@ -2773,8 +2937,7 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   } else {
     {
       const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
+      launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
           w.Bop, w.perm_n);
       count_launches(1);
     }
@@ -2827,8 +2990,7 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   }
   {
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-    split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop,
+    launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop,
         w.perm);
   }
   count_launches(3);
@@ -2903,16 +3065,14 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     scale_finalize<<<1, 1, 0, s>>>(w.sc);
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     if (!pl.sym) {  // (the symmetric scheme splits in norm order below)
-      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-          V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
+      launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
           w.Bop);
       count_launches(1);
     }
     count_launches(2);
     if (!pl.alias) {
       const int64_t totA = (int64_t)pl.nAblocks * kRowsPerBlock * pl.KA * 16;  // rows padded
-      split_tile<<<(int)std::min<int64_t>((totA + 255) / 256, sms * 16), 256, 0, s>>>(
-          V, lambda, n, k, pl.KA, pl.KS, pl.TS, row_begin, (int64_t)pl.nAblocks * kRowsPerBlock,
+      launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, row_begin, (int64_t)pl.nAblocks * kRowsPerBlock,
           w.sc, w.Aop);
       count_launches(1);
     }
@@ -2972,8 +3132,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       if (hovf) {
         // pool exhausted: the plain threshold pass (exact) from an un-permuted split
         const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-        split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-            V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
+        launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
         count_launches(1);
         Plan bp = pl;
         bp.sym = 0;
@@ -3014,8 +3173,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       // from an un-permuted split
       {
         const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-        split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-            V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
+        launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
         count_launches(1);
       }
       Plan bp = pl;
@@ -3988,8 +4146,7 @@ extern "C" ggm_status ggm_sparse_precision_overall(
     absmax_check<<<blocks(n * (int64_t)k), 256, 0, s>>>(V, lambda, n, k, sw.sc);
     scale_finalize<<<1, 1, 0, s>>>(sw.sc);
     const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-    split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-        V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
+    launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
     FusedParams fp = base_params(pl, sw, n, 0);
     fp.mass_out = w.w;
     if (pl.resident && !std::getenv("GGM_OVERALL_PLAIN_MASS")) {
@@ -4197,8 +4354,7 @@ extern "C" ggm_status ggm_sparse_precision_overall(
       absmax_check<<<blocks(rows * (int64_t)k), 256, 0, s>>>(F, lambda, rows, k, sw.sc);
       scale_finalize<<<1, 1, 0, s>>>(sw.sc);
       const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-      split_tile<<<(int)std::min<int64_t>((totB + 255) / 256, sms * 16), 256, 0, s>>>(
-          F, lambda, rows, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
+      launch_split(s, sms, F, lambda, rows, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
       FusedParams fp = base_params(pl, sw, rows, 0);
       fp.tau = x0;
       fp.hist_out = w.hist;
