@@ -638,6 +638,9 @@ struct FusedParams {
                          // nranks: the rank-strided share of the distributed symmetric scheme)
   int unit_lo, unit_hi;  // units processed by this launch (a rank's share in the sharded
                          // symmetric scheme; [0, all units) otherwise)
+  int pm_n, pm_r;        // kSym part-major share (pm_n > 0, pm_n | wsplit): rank pm_r of pm_n
+                         // takes sub-windows pm_r, pm_r + pm_n, ... of EVERY row block, in
+                         // row-block order (unit_lo/hi/step unused)
 #ifdef GGM_EPI_DEBUG
   int dbg;  // timing experiments only (GGM_DEBUG_EPI): 1 = TMEM loads only, 2 = no epilogue work
 #endif
@@ -700,15 +703,30 @@ __device__ __forceinline__ int unit_tiles(const FusedParams& p, int u, int& ub) 
 // Visit the kSym window [ub, ub + W) starting at X = the last unit of this wave (all CTAs of
 // a wave contain X in their windows), so concurrently running CTAs stream the same column
 // blocks in lockstep and share them through L2.
+template <int KIND>
 __host__ __device__ __forceinline__ int unit_count(const FusedParams& p) {
+  if (KIND == kSym && p.pm_n > 0) return (p.wsplit / p.pm_n) * p.NB;
   return (p.unit_hi - p.unit_lo + p.unit_step - 1) / p.unit_step;
 }
+// Folded part-major share (pm_n ranks, wsplit sub-windows per row block, Q = wsplit / pm_n
+// slots per row block and rank): sub-window j is paired with wsplit-1-j (the near-diagonal
+// sub-windows emit fewer candidates than the far ones: C5, N = 8, 2.10M vs 2.88M per rank
+// unfolded), rank r owns the pairs j = r, r + pm_n, ...; with one slot (Q = 1) it takes j on
+// even and wsplit-1-j on odd row blocks.  Local unit uj = lp·NB + ub (row blocks in order).
+template <int KIND>
 __host__ __device__ __forceinline__ int unit_of(const FusedParams& p, int uj) {
+  if (KIND == kSym && p.pm_n > 0) {
+    const int lp = uj / p.NB, ub = uj - lp * p.NB;
+    const int j = p.pm_r + p.pm_n * (lp >> 1);
+    const bool far = ((lp + ub) & 1) != 0;
+    return (far ? p.wsplit - 1 - j : j) * p.NB + ub;
+  }
   return p.unit_lo + uj * p.unit_step;
 }
+template <int KIND>
 __device__ __forceinline__ int sym_start(const FusedParams& p, int uj, int ub, int u0, int ustep,
                                          int w0, int w1) {
-  const int X = unit_of(p, min(unit_count(p) - 1, uj - u0 + ustep - 1)) % p.NB;
+  const int X = unit_of<KIND>(p, min(unit_count<KIND>(p) - 1, uj - u0 + ustep - 1)) % p.NB;
   const int delta = (X - ub + p.NB) % p.NB;
   return (delta >= w0 && delta < w1) ? delta : w0;
 }
@@ -729,7 +747,7 @@ struct TileIter {
       const int part = PAIR ? u / p.NB : 0;
       w0 = PAIR ? part * W / p.wsplit : 0;
       w1 = PAIR ? (part + 1) * W / p.wsplit : W;
-      o = sym_start(p, uj, ub, u0, ustep, w0, w1);
+      o = sym_start<KIND>(p, uj, ub, u0, ustep, w0, w1);
       place(p);
     } else {
       const int j = KIND == kPlain ? (u % p.C) * p.TPC : 0;
@@ -934,6 +952,13 @@ __device__ __forceinline__ void release_tmem(uint64_t* bar) {
 struct CandCursor {
   int64_t base, used;  // current reservation [base, base + kCandChunk) of the pool
 };
+// Marks the unused tail of the warp's reservation (key UINT32_MAX sorts after every row), so
+// the pool needs no up-front fill: the host sorts only the reserved prefix [0, cand_alloc).
+// A cursor without a live reservation (initial, or pool exhausted) has used == kCandChunk.
+__device__ __forceinline__ void close_chunk(const FusedParams& p, const CandCursor& cc, int lane) {
+  for (int64_t q = cc.base + cc.used + lane; q < cc.base + kCandChunk; q += 32)
+    p.cand_key[q] = 0xFFFFFFFFu;
+}
 template <int MAXT, int KIND>
 __device__ __forceinline__ void epi_chunk(const FusedParams& p, const uint32_t (&vr)[32],
                                           uint32_t tchunk, int64_t col0, int64_t gi, int64_t lr,
@@ -1058,8 +1083,8 @@ __device__ __forceinline__ void epilogue_role(const FusedParams& p, uint32_t tme
     asm volatile("bar.sync 5, 256;" ::: "memory");
   }
   int tpar = 0;
-  for (int uj = u0; uj < unit_count(p); uj += ustep) {
-    const int u = unit_of(p, uj);
+  for (int uj = u0; uj < unit_count<KIND>(p); uj += ustep) {
+    const int u = unit_of<KIND>(p, uj);
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;  // this CTA's 128-row block
@@ -1239,8 +1264,8 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
   int buf = 0;
   uint32_t tphase = 0;
   MagList<MAXT> top;
-  for (int uj = u0; uj < unit_count(p); uj += ustep) {
-    const int u = unit_of(p, uj);
+  for (int uj = u0; uj < unit_count<kSeed>(p); uj += ustep) {
+    const int u = unit_of<kSeed>(p, uj);
     int ub;
     const int ntiles = unit_tiles<kSeed, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1257,8 +1282,17 @@ __device__ __forceinline__ void epilogue_seed(const FusedParams& p, uint32_t tme
       const uint32_t taddr = tmem_base + ((uint32_t)(g.q * 32) << 16) +
                              (uint32_t)(buf * kTileN + g.part * G::W);
       uint32_t v[G::NC][32];
+#ifndef GGM_EPI_LD32
+      if constexpr (G::NC == 2) {  // one x64 load (as the candidate epilogue)
+        tmem_ld64_nowait(taddr, v[0], v[G::NC - 1]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+      }
+#else
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+#endif
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) tmem_wait_ld(v[c]);
       tc_fence_before();
@@ -1350,8 +1384,8 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
   // live off-diagonal tile overwrites its slot), combined after the part's barrier
   int buf = 0, tpar = 0;
   uint32_t tphase = 0;
-  for (int uj = u0; uj < unit_count(p); uj += ustep) {
-    const int u = unit_of(p, uj);
+  for (int uj = u0; uj < unit_count<kSymList>(p); uj += ustep) {
+    const int u = unit_of<kSymList>(p, uj);
     int ub;
     const int ntiles = unit_tiles<kSymList, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1533,8 +1567,8 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #ifdef GGM_MMA_PROF
   long long pe_t0 = clock64(), pe_w = 0, pe_n = 0;
 #endif
-  for (int uj = u0; uj < unit_count(p); uj += ustep) {
-    const int u = unit_of(p, uj);
+  for (int uj = u0; uj < unit_count<KIND>(p); uj += ustep) {
+    const int u = unit_of<KIND>(p, uj);
     int ub;
     const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
     const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1573,8 +1607,19 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       // profiles/r02_logs/r02d_ab_epiblock.log)
       uint32_t v[G::NC][32];
       if (live) {
+#ifndef GGM_EPI_LD32
+        // one 32x32b.x64 load for the warp's 64 columns (C4 main 3.78 -> 3.74 ms against two
+        // x32 loads, same session: profiles/r02_logs/r02ab_ld64.log)
+        if constexpr (G::NC == 2) {
+          tmem_ld64_nowait(taddr, v[0], v[G::NC - 1]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+        }
+#else
 #pragma unroll
         for (int c = 0; c < G::NC; ++c) tmem_ld32_nowait(taddr + c * 32, v[c]);
+#endif
 #pragma unroll
         for (int c = 0; c < G::NC; ++c) tmem_wait_ld(v[c]);
       }
@@ -1676,6 +1721,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         const int total = __reduce_add_sync(0xffffffffu, __popc(mr) + __popc(mc));
         if (total == 0) continue;
         if (cc.used + total > kCandChunk) {  // reserve a fresh chunk of the pool
+          close_chunk(p, cc, lane);
           unsigned long long b0 = 0;
           if (lane == 0) b0 = atomicAdd(&scw->cand_alloc, (unsigned long long)kCandChunk);
           cc.base = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
@@ -1717,6 +1763,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
       }
     }
   }
+  close_chunk(p, cc, lane);
   if (lane == 0 && emitted) atomicAdd(&scw->cand_emitted, emitted);
 #ifdef GGM_MMA_PROF
   if (lane == 0 && (blockIdx.x & 15) == 0 && (warp == kFirstEpiWarp || warp == kFirstEpiWarp + EPW - 1))
@@ -1830,8 +1877,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
       int stage = 0;
       uint32_t phase = 0;
       int a_iter = 0;
-      for (int uj = u0; uj < unit_count(p); uj += ustep) {
-        const int u = unit_of(p, uj);
+      for (int uj = u0; uj < unit_count<KIND>(p); uj += ustep) {
+        const int u = unit_of<KIND>(p, uj);
         int ub;
         const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         const int rb = PAIR ? 2 * ub + rank : ub;
@@ -1968,8 +2015,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
             else if (slot < p.KS + p.TS) tm[a] |= 1u << ks;
           }
         }
-        for (int uj = u0; uj < unit_count(p); uj += ustep) {
-          const int u = unit_of(p, uj);
+        for (int uj = u0; uj < unit_count<KIND>(p); uj += ustep) {
+          const int u = unit_of<KIND>(p, uj);
           int ub;
           const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
           PROF_W(pr_ta, mbar_wait(afull, a_iter & 1));
@@ -2040,8 +2087,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
         }
       } else
 #endif
-      for (int uj = u0; uj < unit_count(p); uj += ustep) {
-        const int u = unit_of(p, uj);
+      for (int uj = u0; uj < unit_count<KIND>(p); uj += ustep) {
+        const int u = unit_of<KIND>(p, uj);
         int ub;
         const int ntiles = unit_tiles<KIND, PAIR>(p, u, ub);
         if (resident) {
@@ -2340,7 +2387,8 @@ template <int MAXT>
 __global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restrict__ cv,
                           int64_t ncand, int64_t n, int t, const int32_t* __restrict__ perm,
                           int64_t row_begin, int64_t row_end, int64_t* row_id,
-                          int64_t* row_ptr, int32_t* col, float* val) {
+                          int64_t* row_ptr, int32_t* col, float* val,
+                          const int64_t* __restrict__ off = nullptr) {
   // row j (bound-order index): top t of its candidates (source in bound order, value) by
   // (|ψ| desc, original column id asc), ascending columns.  row_id == nullptr: written at
   // the original row id (single GPU, full axis); else at j - row_begin, with its original id
@@ -2349,8 +2397,9 @@ __global__ void merge_sym(const uint32_t* __restrict__ key, const uint2* __restr
   if (j >= row_end) return;
   TopList<MAXT> top;
   top.init(t);
-  const int64_t b0 = lower_bound_u32(key, ncand, (uint32_t)j);
-  const int64_t b1 = lower_bound_u32(key, ncand, (uint32_t)j + 1u);
+  // the row's bucket: from the re-evaluation's row offsets when given, else two binary searches
+  const int64_t b0 = off ? off[j] : lower_bound_u32(key, ncand, (uint32_t)j);
+  const int64_t b1 = off ? off[j + 1] : lower_bound_u32(key, ncand, (uint32_t)j + 1u);
   for (int64_t e = b0; e < b1; ++e) {
     const uint2 x = cv[e];
     GGM_DCHECK(x.x < (uint32_t)n);
@@ -2772,9 +2821,12 @@ static ggm_status launch_fused(const FusedParams& fp_in, int t, int64_t ablocks,
                                    : fp.RB;
   }
   if (fp.unit_step < 1) fp.unit_step = 1;
-  if (fp.unit_hi <= fp.unit_lo) return GGM_OK;  // empty shard
+  if (fp.pm_n > 0 && (fp.kind != kSym || fp.wsplit % fp.pm_n != 0 || (fp.wsplit & 1) ||
+                     (fp.wsplit / fp.pm_n != 1 && (fp.wsplit / fp.pm_n) % 2 != 0)))
+    fp.pm_n = 0;
+  if (fp.pm_n == 0 && fp.unit_hi <= fp.unit_lo) return GGM_OK;  // empty shard
   const size_t smem = fused_smem_bytes(fp.KA, fp.resident, fp.pair);
-  const int units = unit_count(fp);
+  const int units = unit_count<kSym>(fp);
   TMaps tm;
   memset(&tm, 0, sizeof(tm));
   cudaError_t ce;
@@ -2799,8 +2851,10 @@ static void launch_merge_sym_t(const Work& w, const Plan& pl, int64_t ncand, int
                                int32_t* col, float* val, cudaStream_t s) {
   const int threads = 128;
   const int blocks = (int)((pl.n + threads - 1) / threads);
+  // screening plans with candidates computed the pool's row offsets (recompute_pool)
   merge_sym<MAXT><<<blocks, threads, 0, s>>>(w.skey, w.sval, ncand, pl.n, pl.t, w.perm, 0, pl.n,
-                                             nullptr, row_ptr, col, val);
+                                             nullptr, row_ptr, col, val,
+                                             (pl.screen && ncand > 0) ? w.roff : nullptr);
 }
 
 static thread_local double g_stats[6] = {0, 0, 0, 0, 0, 0};
@@ -2918,7 +2972,6 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   const int64_t nthr = 2 * pl.NBu * kRowsPerBlock;
   fill_f32<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, nthr,
                                                                              INFINITY);
-  GGM_CUDA_TRY(cudaMemsetAsync(w.ckey, 0xFF, sizeof(uint32_t) * pl.cand_total, s));
   row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
       V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
   iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
@@ -2935,10 +2988,23 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   } else if (thr_all) {
     GGM_CUDA_TRY(cudaMemcpyAsync(w.thr, thr_all, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
   } else {
-    {
-      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
-      launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
-          w.Bop, w.perm_n);
+    const int64_t nrows_pad = (int64_t)pl.nBblocks * kRowsPerBlock;
+    if (seed_ulo >= 0) {
+      // a rank's seed share reads only its own row units (A) and the first SS column tiles
+      // (B): split just those rows (the replicated full split cost 0.24 ms per rank at C5)
+      const int64_t R = pl.pair ? 2 * kRowsPerBlock : kRowsPerBlock;
+      const int64_t b_hi = std::min<int64_t>(nrows_pad, (int64_t)pl.SS * kTileN);
+      int64_t a_lo = std::min<int64_t>(nrows_pad, seed_ulo * R);
+      const int64_t a_hi = std::min<int64_t>(nrows_pad, seed_uhi * R);
+      launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, b_hi, w.sc, w.Bop, w.perm_n);
+      a_lo = std::max(a_lo, b_hi);
+      if (a_hi > a_lo)
+        launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, a_lo, a_hi - a_lo, w.sc,
+                     w.Bop + (size_t)(a_lo / kRowsPerBlock) * block_bytes(pl.KA), w.perm_n);
+      count_launches(2);
+    } else {
+      launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, nrows_pad, w.sc, w.Bop,
+                   w.perm_n);
       count_launches(1);
     }
     // (2) seed: per row, the t-th largest hi·hi chunk maximum over the first SS column
@@ -3003,7 +3069,7 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
 // every rank gets the same mix of bound levels — contiguous shares left the last ranks with
 // most of the candidate emission, tools/sim_ranks.py); candidates -> w.ckey / w.cval.
 static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int unit_lo,
-                           int unit_hi, cudaStream_t s, int unit_step = 1) {
+                           int unit_hi, cudaStream_t s, int unit_step = 1, int pm_n = 0) {
   fp.kind = kSym;
   fp.RB = (int)pl.NBu;
   fp.thr = pl.screen ? w.thr_s : w.thr_p;
@@ -3018,7 +3084,9 @@ static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int un
   fp.unit_lo = unit_lo;
   fp.unit_hi = unit_hi * fp.wsplit;  // unit_hi counts row blocks; units = sub-windows
   fp.unit_step = unit_step;
-  if (fp.unit_hi <= unit_lo) return GGM_OK;
+  fp.pm_n = pm_n;
+  fp.pm_r = unit_lo;
+  if (pm_n == 0 && fp.unit_hi <= unit_lo) return GGM_OK;
   return launch_fused(fp, pl.t, a_blocks(pl, 0), pl.nBblocks, s);
 }
 
@@ -3311,6 +3379,21 @@ static ggm_status sym_shard_plan(int64_t n, int k, const ggm_sparsify_opts* opts
   return GGM_OK;
 }
 
+// Part-major share of the distributed symmetric units (0: rank-strided); GGM_SYM_ASSIGN=strided
+// forces the rank-strided form (A/B, tests).
+static int sym_part_major(const Plan& pl, int nranks) {
+  const char* e = getenv("GGM_SYM_ASSIGN");
+  if (e && strcmp(e, "strided") == 0) return 0;
+  const int q = nranks > 0 ? kWindowSplit / nranks : 0;
+  return (nranks > 1 && pl.pair && kWindowSplit % 2 == 0 && kWindowSplit % nranks == 0 &&
+          (q == 1 || q % 2 == 0)) ? nranks : 0;
+}
+// owner rank of unit (sub-window part, row block b) under the folded part-major share
+static int sym_pm_owner(int part, int64_t b, int nranks) {
+  const int j = std::min(part, kWindowSplit - 1 - part);
+  if (kWindowSplit / nranks == 1) return (b & 1) ? kWindowSplit - 1 - part : part;
+  return j % nranks;
+}
 static int64_t sym_unit_rows(const Plan& pl) { return pl.pair ? 2 * kRowsPerBlock : kRowsPerBlock; }
 static int64_t sym_unit_lo(const Plan& pl, int rank, int nranks) {
   return pl.NBu * (int64_t)rank / nranks;
@@ -3445,9 +3528,14 @@ static ggm_status sym_shard_impl(
   st = sym_prepare(pl, w, V, lambda, n, k, fp, s, -1, -1, thr_all);
   if (st != GGM_OK) return st;
   tm.mark(1);
-  // this rank's block pairs: units rank, rank + nranks, ... (the merge ownership of rows
-  // below stays the contiguous bound-order ranges)
-  st = sym_main(pl, w, fp, rank, (int)pl.NBu, s, nranks);
+  // this rank's block pairs (the merge ownership of rows below stays the contiguous
+  // bound-order ranges): folded part-major when nranks divides the sub-window count (a
+  // rank owns sub-windows j and wsplit-1-j of EVERY row block, row blocks in order, so the
+  // CTAs of a wave stream overlapping column windows through L2 as at N = 1; unit_of), else
+  // rank-strided units rank, rank + nranks, ...; both give every rank the same mix of bound
+  // levels (C5, N = 8 per-rank main 11.9-13.3 ms strided, 11.3-12.8 unfolded part-major)
+  const int pm = sym_part_major(pl, nranks);
+  st = sym_main(pl, w, fp, rank, (int)pl.NBu, s, nranks, pm);
   if (st != GGM_OK) return st;
   tm.mark(2);
   DevScalars hs;
@@ -3498,8 +3586,9 @@ static ggm_status sym_shard_impl(
   tm.finish();
   double evaluated = 0.0;  // entries evaluated by this rank's units
   const int64_t ws = pl.pair ? kWindowSplit : 1;
-  for (int64_t u = rank; u < pl.NBu * ws; u += nranks) {  // this rank's units (rank-strided)
+  for (int64_t u = 0; u < pl.NBu * ws; ++u) {  // this rank's units
     const int64_t NBu = pl.NBu, part = u / NBu, b = u % NBu;
+    if (pm ? (sym_pm_owner((int)part, b, nranks) != rank) : (u % nranks != rank)) continue;
     const int64_t W = (NBu & 1) ? (NBu + 1) / 2 : NBu / 2 + (b < NBu / 2 ? 1 : 0);
     evaluated += pl.pair ? (double)((part + 1) * W / ws - part * W / ws) * 2 * kRowsPerBlock * kTileN
                          : (double)((W + 1) / 2) * kRowsPerBlock * kTileN;

@@ -91,3 +91,23 @@ def test_rows_begin_partition(G):
         b = [G.sym_rows_begin(n, k, t, r, P) for r in range(P + 1)]
         assert b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
         assert all(x % 256 == 0 for x in b[:-1])
+
+
+@pytest.mark.parametrize("assign", ["part", "strided"])
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_unit_assignments_equal_single_call(G, monkeypatch, assign, P):
+    """Both shares of the block-pair units (folded part-major: sub-windows j and 7 - j of every
+    row block for the pairs j owned by the rank, the default when P divides the sub-window
+    count; rank-strided units r, r + P, ..., GGM_SYM_ASSIGN=strided) cover every unit exactly
+    once: bitwise the single call (P = 8 is in test_simulated_ranks_equal_single_call)."""
+    n, k, t = 6000, 64, 10
+    if assign == "strided":
+        monkeypatch.setenv("GGM_SYM_ASSIGN", "strided")
+    V, lam = gen.small_factor(77 + P, n, k)
+    Vd = torch.from_numpy(V).cuda()
+    ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
+    rp, c, v = G.ggm_sparse_precision(Vd, ld, 0, n, mode=0, topk=t, symmetric=1)
+    torch.cuda.synchronize()
+    c2, v2 = _simulate(G, Vd, ld, t, P, seeded=True)
+    assert np.array_equal(c.cpu().numpy(), c2)
+    np.testing.assert_array_equal(v.cpu().numpy(), v2)

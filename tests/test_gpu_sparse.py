@@ -52,6 +52,24 @@ def test_topk_streaming_large_k(G):
     check_topk(rp, c, v, V, lam, np.arange(n), t)
 
 
+@pytest.mark.parametrize("k", [2048, 2051, 2304])
+def test_topk_very_large_k_generic_split(G, k):
+    """k > 2048: more than 256 16-byte chunks per operand row, so the operand split takes its
+    generic grid-stride form (the fast form keeps one chunk per thread of a 256-thread block);
+    k = 2051 also exercises the unaligned (k mod 4 != 0) scalar loads; k = 2048 is the fast
+    form at one row per block."""
+    n, t = 2600, 5
+    V, lam = gen.small_factor(11, n, k)
+    rp, c, v = _run(G, V, lam, 0, n, mode=0, topk=t)
+    rows = np.unique(np.concatenate([np.arange(0, 200), np.arange(n - 100, n)]))
+    segs = [(rp[i], rp[i + 1]) for i in rows]
+    rps = np.concatenate([[0], np.cumsum([b - a for a, b in segs])])
+    cs = np.concatenate([c[a:b] for a, b in segs])
+    vs = np.concatenate([v[a:b] for a, b in segs])
+    st = check_topk(rps, cs, vs, V, lam, rows, t)
+    assert st["exact"] + st["excused"] == len(rows)
+
+
 def test_all_ties_identity_factor(G):
     """V = first k columns of I: all off-diagonals are exactly 0 ⇒ the t smallest j != i."""
     n, k, t = 700, 8, 10

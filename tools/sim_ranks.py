@@ -3,7 +3,8 @@ in turn (no rank waits on another): axis A (n = 10^6) distributed symmetric sche
 seed pass + this rank's block pairs + merge of its rows; axis B (n = 30,000) plain row shards.
 Prints, per N, the max-over-ranks compute time and a projected step time = that + the
 collectives' bytes at an assumed NVLink/NCCL bus bandwidth (a projection, not a measurement of
-N GPUs: DESIGN.md §5).  Usage: python tools/sim_ranks.py [N ...]"""
+N GPUs: DESIGN.md §5).  Usage: python tools/sim_ranks.py [N ...] [--symB]  (--symB: axis B by the distributed
+symmetric scheme too at N > 1)"""
 import json
 import os
 import sys
@@ -35,7 +36,7 @@ def ev_ms(fn, reps=3):
 
 
 def main():
-    Ns = [int(x) for x in sys.argv[1:]] or [1, 2, 4, 8]
+    Ns = [int(x) for x in sys.argv[1:] if x.isdigit()] or [1, 2, 4, 8]
     cfg = gen.config("C5")
     t = cfg["t"]
     (VA, lA), (VB, lB) = [(torch.from_numpy(V).cuda(), torch.from_numpy(l).cuda())
@@ -43,13 +44,17 @@ def main():
     nA, k = VA.shape
     nB = VB.shape[0]
     res = {}
-    for N in Ns:
+    symB = "--symB" in sys.argv   # axis B by the distributed symmetric scheme as well
+
+    def sym_axis(V, lam, N):
+        """Per-rank seed / units / merge times (ms) of the distributed symmetric scheme."""
+        n = V.shape[0]
         seeds, runs, merges, plans, shards = [], [], [], [], []
         for r in range(N):
-            plans.append(G.SymShardPlan(nA, k, t, r, N))
+            plans.append(G.SymShardPlan(n, k, t, r, N))
         parts = []
         for r in range(N):
-            ms, thr = ev_ms(lambda: plans[r].seed(VA, lA).clone())
+            ms, thr = ev_ms(lambda: plans[r].seed(V, lam).clone())
             seeds.append(ms)
             parts.append(thr)
         thr_all = torch.stack(parts).min(dim=0).values
@@ -57,7 +62,7 @@ def main():
         ncand, stages = [], []
         G.set_timing(True)
         for r in range(N):
-            ms, out = ev_ms(lambda: plans[r].run(VA, lA, thr_all=thr_all))
+            ms, out = ev_ms(lambda: plans[r].run(V, lam, thr_all=thr_all))
             runs.append(ms)
             stages.append([round(x, 3) for x in G.last_timing()])
             key, val, counts, perm = out
@@ -70,17 +75,25 @@ def main():
                 ks.append(key[off:off + counts[d]])
                 vs.append(val[off:off + counts[d]])
             rk, rv = torch.cat(ks), torch.cat(vs)
-            b, e = G.sym_rows_begin(nA, k, t, d, N), G.sym_rows_begin(nA, k, t, d + 1, N)
-            ms, _ = ev_ms(lambda: G.sym_merge(nA, t, rk, rv, shards[0][3], b, e))
+            b, e = G.sym_rows_begin(n, k, t, d, N), G.sym_rows_begin(n, k, t, d + 1, N)
+            ms, _ = ev_ms(lambda: G.sym_merge(n, t, rk, rv, shards[0][3], b, e))
             merges.append(ms)
         del shards
         torch.cuda.empty_cache()
-        rowsB = []
-        for r in range(N):
-            b, e = shard_rows(nB, N, r)
-            p = G.SparsePlan(nB, k, b, e, topk=t)
-            ms, _ = ev_ms(lambda: p.run(VB, lB))
-            rowsB.append(ms)
+        return seeds, runs, merges, ncand, stages
+
+    for N in Ns:
+        seeds, runs, merges, ncand, stages = sym_axis(VA, lA, N)
+        rowsB, ncB = [], [0]
+        if symB and N > 1:
+            sB, rB, mB, ncB, _ = sym_axis(VB, lB, N)
+            rowsB = [a + b + c for a, b, c in zip(sB, rB, mB)]
+        else:
+            for r in range(N):
+                b, e = shard_rows(nB, N, r)
+                p = G.SparsePlan(nB, k, b, e, topk=t)
+                ms, _ = ev_ms(lambda: p.run(VB, lB))
+                rowsB.append(ms)
         perA = [a + b + c for a, b, c in zip(seeds, runs, merges)]
         comp = max(perA) + max(rowsB)
         # collectives per step at N > 1: all-reduce(MIN) of nA floats, all-to-all of the
@@ -90,6 +103,8 @@ def main():
                    12.0 * max(ncand) * (N - 1) / N,
                    (8.0 * nA * t + 8.0 * nA) * (N - 1) / N,
                    8.0 * nB * t * (N - 1) / N]
+            if symB:  # axis B's seed all-reduce and candidate all-to-all
+                byt += [4.0 * nB * 2 * (N - 1) / N, 12.0 * max(ncB) * (N - 1) / N]
             comm = sum(b / (BUS_GBS * 1e9) * 1e3 + LAT_MS for b in byt)
         else:
             comm = 0.0
