@@ -438,12 +438,15 @@ def overall_timing(G, torch, V, lam):
     kw = dict(downweight=True, min_edges=1)
     _, _, _, (ccap, cap) = G.ggm_sparse_precision_overall(V, lam, 10 * n, return_caps=True, **kw)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    rp, c, v = G.ggm_sparse_precision_overall(V, lam, 10 * n, cand_capacity=ccap, capacity=cap, **kw)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms = float("inf")
+    for _ in range(2):  # best of two calls (the first may still grow the caching allocator)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rp, c, v = G.ggm_sparse_precision_overall(V, lam, 10 * n, cand_capacity=ccap,
+                                                  capacity=cap, **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = min(ms, e0.elapsed_time(e1))
     path, sat = G.overall_last_path()
     return {"path": {0: "lists", 1: "histogram+threshold", 2: "lists+saturated block",
                      3: "sampled global threshold + one symmetric pass"}.get(path, path),

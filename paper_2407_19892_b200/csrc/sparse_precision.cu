@@ -3055,7 +3055,6 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
     count_launches(1);
   }
   {
-    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop,
         w.perm);
   }
@@ -3131,7 +3130,6 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 8));
     absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
     scale_finalize<<<1, 1, 0, s>>>(w.sc);
-    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     if (!pl.sym) {  // (the symmetric scheme splits in norm order below)
       launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc,
           w.Bop);
@@ -3139,7 +3137,6 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     }
     count_launches(2);
     if (!pl.alias) {
-      const int64_t totA = (int64_t)pl.nAblocks * kRowsPerBlock * pl.KA * 16;  // rows padded
       launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, row_begin, (int64_t)pl.nAblocks * kRowsPerBlock,
           w.sc, w.Aop);
       count_launches(1);
@@ -3199,7 +3196,6 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
     if (pl.mode == 1) {
       if (hovf) {
         // pool exhausted: the plain threshold pass (exact) from an un-permuted split
-        const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
         launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
         count_launches(1);
         Plan bp = pl;
@@ -3240,7 +3236,6 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
       // the candidate pool filled up: recompute the whole axis with the plain scheme (exact)
       // from an un-permuted split
       {
-        const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
         launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, w.sc, w.Bop);
         count_launches(1);
       }
@@ -4234,7 +4229,6 @@ extern "C" ggm_status ggm_sparse_precision_overall(
     GGM_CUDA_TRY(cudaMemsetAsync(w.w, 0, sizeof(double) * n, s));
     absmax_check<<<blocks(n * (int64_t)k), 256, 0, s>>>(V, lambda, n, k, sw.sc);
     scale_finalize<<<1, 1, 0, s>>>(sw.sc);
-    const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
     launch_split(s, sms, V, lambda, n, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
     FusedParams fp = base_params(pl, sw, n, 0);
     fp.mass_out = w.w;
@@ -4442,7 +4436,6 @@ extern "C" ggm_status ggm_sparse_precision_overall(
       GGM_CUDA_TRY(cudaMemsetAsync(w.hist, 0, 256 * sizeof(unsigned long long), s));
       absmax_check<<<blocks(rows * (int64_t)k), 256, 0, s>>>(F, lambda, rows, k, sw.sc);
       scale_finalize<<<1, 1, 0, s>>>(sw.sc);
-      const int64_t totB = (int64_t)pl.nBblocks * kRowsPerBlock * pl.KA * 16;
       launch_split(s, sms, F, lambda, rows, k, pl.KA, pl.KS, pl.TS, 0, (int64_t)pl.nBblocks * kRowsPerBlock, sw.sc, sw.Bop);
       FusedParams fp = base_params(pl, sw, rows, 0);
       fp.tau = x0;
