@@ -1675,6 +1675,20 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #endif
 #define VC vc
 #endif
+#if !defined(GGM_EPI_STREAM) && !defined(GGM_EPI_VOTE_PER_CHUNK)
+      // one vote for the warp's whole slice (both chunks' maxima, independent chains): the
+      // common tile has no entry above any bound and leaves after a single __any_sync
+      float mpre[G::NC];
+      if (!need_mask) {
+        bool hit = false;
+#pragma unroll
+        for (int c = 0; c < G::NC; ++c) {
+          mpre[c] = max32_abs(reinterpret_cast<const float(&)[32]>(v[c]));
+          hit |= mpre[c] >= bi || mpre[c] >= cmin[c];
+        }
+        if (!__any_sync(0xffffffffu, valid && hit)) continue;
+      }
+#endif
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) {
         const int col0 = cb + c * 32;
@@ -1684,7 +1698,11 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         tmem_wait_ld(vc);
         if (c == G::NC - 1) release_cur();  // the last chunk is in registers
 #endif
+#if !defined(GGM_EPI_STREAM) && !defined(GGM_EPI_VOTE_PER_CHUNK)
+        float m = need_mask ? 0.f : mpre[c];
+#else
         float m = max32_abs(reinterpret_cast<const float(&)[32]>(VC));
+#endif
         uint32_t excl = 0;  // diagonal (Q8) and padding columns
         if (need_mask) {
           const int dd = gi - col0;
