@@ -1590,12 +1590,6 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #pragma unroll
       for (int c = 0; c < G::NC; ++c)
         cmin[c] = emit_cols ? __ldg(thr_min + (cb >> 5) + c) : INFINITY;
-#ifdef GGM_EPI_PREFETCH_THR
-      // the rare path's per-column bounds of this tile (two 128-byte lines) into L1 while
-      // the warp waits for the accumulator
-      if (emit_cols && lane < G::NC && cb + 32 * lane < n)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(thr + cb + 32 * lane));
-#endif
 #ifdef GGM_MMA_PROF
       const long long pe_c = clock64();
 #endif
