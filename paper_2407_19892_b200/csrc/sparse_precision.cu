@@ -1590,6 +1590,14 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #pragma unroll
       for (int c = 0; c < G::NC; ++c)
         cmin[c] = emit_cols ? __ldg(thr_min + (cb >> 5) + c) : INFINITY;
+#ifndef GGM_EPI_THR_LDG
+      // the tile's column bounds, one per lane and chunk (coalesced, before the wait); the rare
+      // path broadcasts them with shuffles instead of re-reading them from global memory
+      // (C4 main 3.77 -> 3.71 ms, profiles/r02_logs/r02h_ab_thrshfl.log)
+      float thl[G::NC];
+#pragma unroll
+      for (int c = 0; c < G::NC; ++c) thl[c] = emit_cols ? __ldg(thr + cb + 32 * c + lane) : INFINITY;
+#endif
 #ifdef GGM_MMA_PROF
       const long long pe_c = clock64();
 #endif
@@ -1724,6 +1732,16 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
           for (int e = 0; e < 32; ++e) mr |= (fabsf(__uint_as_float(VC[e])) >= bi ? 1u : 0u) << e;
           mr &= ~excl;
         }
+#ifndef GGM_EPI_THR_LDG
+        if (__any_sync(0xffffffffu, ch)) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float th = __shfl_sync(0xffffffffu, thl[c], e);
+            mc |= (ch && fabsf(__uint_as_float(VC[e])) >= th ? 1u : 0u) << e;
+          }
+          mc &= ~excl;
+        }
+#else
         if (ch) {
           const float4* t4 = reinterpret_cast<const float4*>(thr + col0);
 #pragma unroll
@@ -1736,6 +1754,7 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
           }
           mc &= ~excl;
         }
+#endif
         const int total = __reduce_add_sync(0xffffffffu, __popc(mr) + __popc(mc));
         if (total == 0) continue;
         if (cc.used + total > kCandChunk) {  // reserve a fresh chunk of the pool

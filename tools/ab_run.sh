@@ -1,9 +1,8 @@
 set -u
 mkdir -p gpurun_out
-python -c "import __graft_entry__" 
-for cfg in "200000 64" "1000000 100"; do
-  set -- $cfg
-  echo "#### n=$1 k=$2"
-  MP_N=$1 MP_K=$2 VARIANTS="mmaprof_dbg" DBGS="2 4 3 0" bash tools/mma_prof.sh 2>&1 | grep -v "cta 64"
-done > gpurun_out/r02h_mmaprof.log 2>&1
-cat gpurun_out/r02h_mmaprof.log
+V=${V:-thrshfl}
+for i in 1 2 3; do
+  timeout 300 python tools/sym_ab.py
+  GGM_LIB_PATH=tools/variants/$V.so TAG=$V timeout 300 python tools/sym_ab.py
+done > gpurun_out/r02h_ab_$V.log 2>&1
+cat gpurun_out/r02h_ab_$V.log
