@@ -109,6 +109,13 @@ constexpr int kRecCutMinT = 16;  // cuts (and the screened values they need) fro
 #ifndef GGM_WSPLIT
 #define GGM_WSPLIT 8
 #endif
+// rare path, transposed direction: entries are tested against the minimum bound of their
+// GGM_CMASK_W-column group (8; 32 = the chunk minimum) or, GGM_CMASK_W = 1, their own
+// column's bound (profiles/r02_logs/ab_cmask*.log)
+#ifndef GGM_CMASK_W
+#define GGM_CMASK_W 8
+#endif
+static_assert(GGM_CMASK_W == 1 || GGM_CMASK_W == 8 || GGM_CMASK_W == 32, "GGM_CMASK_W: 1, 8 or 32");
 constexpr int kWindowSplit = GGM_WSPLIT;  // kSym/kSymList CTA-pair units per row block (sub-windows)
 constexpr int64_t kSymAutoN = 16384;  // automatic symmetric scheme from this axis length (measured crossover 8192-16384)
 
@@ -372,11 +379,11 @@ __global__ void sym_threshold_coo(const uint32_t* __restrict__ skey, const uint2
 }
 
 __global__ void chunk_min32(const float* __restrict__ thr, int64_t nchunks,
-                            float* __restrict__ out) {
+                            float* __restrict__ out, int width = 32) {
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
        c += (int64_t)gridDim.x * blockDim.x) {
     float m = INFINITY;
-    for (int e = 0; e < 32; ++e) m = fminf(m, thr[c * 32 + e]);
+    for (int e = 0; e < width; ++e) m = fminf(m, thr[c * width + e]);
     out[c] = m;
   }
 }
@@ -623,6 +630,8 @@ struct FusedParams {
   const float* thr;        // kSym: per-(permuted) column lower bound of that row's t-th
                            //       magnitude (accumulator units, +inf = padding)
   const float* thr_min;    // kSym: min of thr over each 32-column chunk (bound order)
+  const float* thr_min8;   // kSym: min of thr over each 8-column group (the rare path's
+                           // column-direction mask)
   const int32_t* perm;     // kSym: permuted index -> original row/column id
   uint32_t* cand_key;      // kSym: candidate pool: target row j (UINT32_MAX = unused slot)
   uint2* cand_val;         //       (source row i, ψ bits)
@@ -1590,10 +1599,9 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
 #pragma unroll
       for (int c = 0; c < G::NC; ++c)
         cmin[c] = emit_cols ? __ldg(thr_min + (cb >> 5) + c) : INFINITY;
-#ifndef GGM_EPI_THR_LDG
-      // the tile's column bounds, one per lane and chunk (coalesced, before the wait); the rare
-      // path broadcasts them with shuffles instead of re-reading them from global memory
-      // (C4 main 3.77 -> 3.71 ms, profiles/r02_logs/r02h_ab_thrshfl.log)
+#if GGM_CMASK_W == 1
+      // the tile's column bounds, one per lane and chunk (coalesced, before the wait): the
+      // exact column mask broadcasts them with shuffles
       float thl[G::NC];
 #pragma unroll
       for (int c = 0; c < G::NC; ++c) thl[c] = emit_cols ? __ldg(thr + cb + 32 * c + lane) : INFINITY;
@@ -1732,8 +1740,8 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
           for (int e = 0; e < 32; ++e) mr |= (fabsf(__uint_as_float(VC[e])) >= bi ? 1u : 0u) << e;
           mr &= ~excl;
         }
-#ifndef GGM_EPI_THR_LDG
-        if (__any_sync(0xffffffffu, ch)) {
+#if GGM_CMASK_W == 1
+        if (__any_sync(0xffffffffu, ch)) {  // exact: entry (i, j) against bound b_j
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const float th = __shfl_sync(0xffffffffu, thl[c], e);
@@ -1743,14 +1751,20 @@ __device__ __forceinline__ void epilogue_emit(const FusedParams& p, uint32_t tme
         }
 #else
         if (ch) {
-          const float4* t4 = reinterpret_cast<const float4*>(thr + col0);
+          // against the minimum bound of the entry's GGM_CMASK_W-column group (columns are in
+          // bound order, so the groups' bounds are nearly equal): a superset of the exact
+          // transposed-direction candidates, made exact by the re-evaluation and the merge
+#if GGM_CMASK_W == 8
+          const float4 g8 = __ldg(reinterpret_cast<const float4*>(p.thr_min8 + (col0 >> 3)));
+#endif
 #pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) {
-            const float4 th = __ldg(t4 + q4);
-            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 0])) >= th.x ? 1u : 0u) << (4 * q4 + 0);
-            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 1])) >= th.y ? 1u : 0u) << (4 * q4 + 1);
-            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 2])) >= th.z ? 1u : 0u) << (4 * q4 + 2);
-            mc |= (fabsf(__uint_as_float(VC[4 * q4 + 3])) >= th.w ? 1u : 0u) << (4 * q4 + 3);
+          for (int e = 0; e < 32; ++e) {
+#if GGM_CMASK_W == 8
+            const float th = e < 8 ? g8.x : e < 16 ? g8.y : e < 24 ? g8.z : g8.w;
+#else
+            const float th = cmin[c];
+#endif
+            mc |= (fabsf(__uint_as_float(VC[e])) >= th ? 1u : 0u) << e;
           }
           mc &= ~excl;
         }
@@ -2699,6 +2713,7 @@ struct Work {
   float* thr_p;        // kSym: bounds in permuted (sorted) order [NB*128]
   float* thr_s;        // kSym screening: thr_p lowered by the hi*hi error bound [NB*128]
   float* thr_cmin;     // kSym: minimum of the effective bounds over each 32-column chunk
+  float* thr_cmin8;    // kSym: ... over each 8-column group
   float* Ub;           // kSym screening: U = V diag(sqrt λ) in bound order (re-evaluation)
   int64_t* roff;       // kSym screening: candidate row offsets of the sorted pool [n+1]
   float* rcut;         // kSym screening: per-row re-evaluation cuts [n]
@@ -2734,6 +2749,7 @@ static size_t carve(const Plan& pl, void* ws, Work* w) {
   w->thr_p = cv.take<float>(nb * kRowsPerBlock);
   w->thr_s = cv.take<float>(pl.screen ? nb * kRowsPerBlock : 0);
   w->thr_cmin = cv.take<float>(nb * kRowsPerBlock / 32);
+  w->thr_cmin8 = cv.take<float>(nb * kRowsPerBlock / 8);
   w->Ub = cv.take<float>(pl.screen ? (size_t)pl.n * rec_stride(pl.k) : 0);
   w->roff = cv.take<int64_t>(pl.screen ? (size_t)pl.n + 1 : 0);
   w->rcut = cv.take<float>(pl.screen ? (size_t)pl.n : 0);
@@ -3085,6 +3101,9 @@ static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, con
   }
   chunk_min32<<<(int)std::min<int64_t>((nthr / 32 + 255) / 256, sms * 8), 256, 0, s>>>(
       pl.screen ? w.thr_s : w.thr_p, nthr / 32, w.thr_cmin);
+  chunk_min32<<<(int)std::min<int64_t>((nthr / 8 + 255) / 256, sms * 8), 256, 0, s>>>(
+      pl.screen ? w.thr_s : w.thr_p, nthr / 8, w.thr_cmin8, 8);
+  count_launches(1);
   count_launches(1);
   if (pl.screen) {
     gather_u_bound<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
@@ -3110,6 +3129,7 @@ static ggm_status sym_main(const Plan& pl, const Work& w, FusedParams fp, int un
   fp.RB = (int)pl.NBu;
   fp.thr = pl.screen ? w.thr_s : w.thr_p;
   fp.thr_min = w.thr_cmin;
+  fp.thr_min8 = w.thr_cmin8;
   fp.screen = pl.screen;
   fp.cand_vals = (!pl.screen || pl.rec_cut) ? 1 : 0;
   fp.perm = w.perm;
