@@ -310,14 +310,17 @@ typedef struct {
   int symmetric;  /* scheme selection, over the FULL axis (row_begin = 0, row_end = n) with
                      A resident (otherwise always plain):
                      0 = automatic (symmetric for full axes with n >= 16384), 1 = symmetric, 2 = plain.
-                     Symmetric scheme (Ψ = Ψ^T): a seed pass over the n/64 columns of
-                     largest ||U_j|| (hi·hi products) gives each row i a lower bound b_i of
+                     Symmetric scheme (Ψ = Ψ^T): a seed pass over the n/32 columns of
+                     largest ||U_j|| (at least 48 256-column tiles while that is <= 1/8 of
+                     the axis; hi·hi products) gives each row i a lower bound b_i of
                      its t-th |ψ| (t-th largest 32-column chunk maximum, minus the hi·hi
                      rounding bound 2^-10·1.1·||U_i||·max_j||U_j||); rows are reordered by b_i; each
                      unordered 128x128 block pair is then evaluated once (cyclic window per
                      row block) and entry ψ_ij is kept as a candidate of row i if
-                     |ψ| >= b_i and of row j if |ψ| >= b_j; a CUB sort by row and a merge
-                     select each row's top t by (|ψ| desc, j asc).  For k <= 128 the main
+                     |ψ| >= b_i and of row j if |ψ| >= the smallest bound of j's 8-column
+                     group (a superset of |ψ| >= b_j; bounds in a group are nearly equal);
+                     a CUB sort by row and a merge select each row's top t by
+                     (|ψ| desc, j asc) — extra candidates below b_j never reach row j's top t.  For k <= 128 the main
                      pass computes hi·hi only, with every threshold lowered by its error
                      bound, and the candidates are re-evaluated exactly (fp64 sums of the
                      fp32 inputs) before the selection.  Mode 1 uses τ as every row's bound
@@ -340,8 +343,12 @@ ggm_status ggm_sparse_precision(int64_t n, int k, const float *V, const double *
  *
  * ggm_sparse_precision_sym_shard: runs the replicated phases (row norms, seed pass, the two
  * orderings and splits — deterministic, so every rank derives the same permutation) and
- * this rank's contiguous share of the symmetric units (units = 256-row blocks of the
- * bound-ordered axis, [NBu·rank/nranks, NBu·(rank+1)/nranks)).  Outputs this rank's
+ * this rank's share of the symmetric units (a unit = one of the 8 sub-windows of a 256-row
+ * block's column window in the bound-ordered axis).  nranks in {2, 4, 8}: folded
+ * part-major — rank r owns sub-windows j and 7 − j of every row block for the j ≡ r (mod
+ * nranks) (at nranks = 8: j = r on even, 7 − r on odd row blocks); other nranks:
+ * rank-strided units r, r + nranks, ...  (GGM_SYM_ASSIGN=strided forces the latter).
+ * Every unit is evaluated by exactly one rank.  Outputs this rank's
  * candidates sorted by target row, as two device arrays: cand_key[e] = target row (bound
  * order index), cand_val[2e..2e+1] = (source row, bound order index; ψ as float bits);
  * counts[r] (host) = number of candidates whose target row rank r owns (contiguous in the

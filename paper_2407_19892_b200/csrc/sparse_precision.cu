@@ -1530,8 +1530,8 @@ __device__ __forceinline__ void epilogue_mass(const FusedParams& p, uint32_t tme
 // Epilogue role, candidate form (kSym): every row i carries a lower bound b_i of its t-th
 // magnitude (the seed pass); rows and columns are in bound order.  Entry ψ_ij of a tile is
 // emitted as a candidate of row i if |ψ| >= b_i (row direction) and, for off-diagonal
-// blocks, of row j if |ψ| >= b_j (transposed direction, each unordered block pair being
-// evaluated once).  No per-row list is kept: the whole 128-column block of the warp is
+// blocks, of row j if |ψ| >= min of the bounds of j's 8-column group (transposed direction,
+// each unordered block pair being evaluated once; a superset of |ψ| >= b_j, GGM_CMASK_W).  No per-row list is kept: the whole 128-column block of the warp is
 // loaded into registers and the TMEM buffer released before the filter runs; a final merge
 // selects each row's top t among its candidates.  Fast path per 32 columns: one FMNMX3
 // chain + two compares (row bound; chunk minimum of the column bounds).
