@@ -380,7 +380,12 @@ ggm_status ggm_sparse_precision_sym_shard(int64_t n, int k, const float *V,
  * the row blocks (rows in descending-norm order) and +inf for all other rows; the caller
  * combines the ranks' arrays by an element-wise minimum (one all-reduce MIN) and passes the
  * result to ggm_sparse_precision_sym_shard_seeded, which skips the seed pass and is
- * otherwise identical to ggm_sparse_precision_sym_shard.  Same workspace size.
+ * otherwise identical to ggm_sparse_precision_sym_shard.  Same workspace size.  When the
+ * seeded call gets the same workspace (and V, λ, n, k, topk, mode, nranks) as this rank's
+ * ggm_sym_seed_shard call, it also reuses the scale, row norms and norm order that call left
+ * there (host-side stamp per workspace address, consumed once; any other library call on
+ * that workspace discards it) — V and λ must not change in between, as thr_all already
+ * requires.
  * ggm_sym_seed_shard synchronizes `stream`. */
 ggm_status ggm_sym_seed_shard(int64_t n, int k, const float *V, const double *lambda,
                               const ggm_sparsify_opts *opts, int rank, int nranks,

@@ -33,6 +33,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "ggm_internal.h"
@@ -2922,6 +2924,44 @@ extern "C" void ggm_last_stats(double out[6]) {
   for (int i = 0; i < 6; ++i) out[i] = g_stats[i];
 }
 
+// Seed-call reuse (distributed symmetric scheme): ggm_sym_seed_shard leaves the scale, the
+// row norms and the norm order in its workspace; the seeded shard call on the SAME workspace
+// and inputs (its thr_all came from those seed calls) skips recomputing them.  Host-side
+// stamps keyed by the workspace address; any other call on that workspace, or different
+// inputs, recompute everything.
+struct SeedStamp {
+  const float* V;
+  const double* lambda;
+  int64_t n;
+  int k, t, mode, nranks;
+};
+static std::mutex g_seed_mu;
+static std::unordered_map<const void*, SeedStamp> g_seed_reg;
+static void seed_stamp_set(const void* ws, const SeedStamp& st) {
+  std::lock_guard<std::mutex> g(g_seed_mu);
+  g_seed_reg[ws] = st;
+}
+static bool seed_stamp_take(const void* ws, const SeedStamp& st) {  // one-shot match
+  std::lock_guard<std::mutex> g(g_seed_mu);
+  auto it = g_seed_reg.find(ws);
+  if (it == g_seed_reg.end()) return false;
+  const SeedStamp o = it->second;
+  g_seed_reg.erase(it);
+  return o.V == st.V && o.lambda == st.lambda && o.n == st.n && o.k == st.k && o.t == st.t &&
+         o.mode == st.mode && o.nranks == st.nranks;
+}
+static void seed_stamp_forget(const void* ws) {
+  std::lock_guard<std::mutex> g(g_seed_mu);
+  g_seed_reg.erase(ws);
+}
+// zero the per-call counters of a workspace whose scale and norm maximum are reused
+__global__ void reset_pool_counters(DevScalars* sc) {
+  sc->cand_overflow = 0;
+  sc->coo_count = 0;
+  sc->cand_alloc = 0;
+  sc->cand_emitted = 0;
+}
+
 extern "C" ggm_status ggm_sparse_precision_workspace(int64_t n, int k, int64_t row_begin,
                                                      int64_t row_end,
                                                      const ggm_sparsify_opts* opts,
@@ -3018,22 +3058,29 @@ static void recompute_pool(const Work& w, int64_t ncand, int64_t n, int k, int t
 static ggm_status sym_prepare(const Plan& pl, const Work& w, const float* V, const double* lambda,
                               int64_t n, int k, const FusedParams& fp, cudaStream_t s,
                               int seed_ulo = -1, int seed_uhi = -1,
-                              const float* thr_all = nullptr, float tau_cap = 0.f) {
+                              const float* thr_all = nullptr, float tau_cap = 0.f,
+                              bool norms_ready = false) {
   const int sms = num_sms();
   ggm_status st;
     // (1) rows in descending ||U_i|| order (CUB sort of the row norms), split in that order
+    // (norms_ready: the row norms, their maximum and the norm order are already in the
+    // workspace from this rank's seed-share call on the same inputs)
   const int64_t nthr = 2 * pl.NBu * kRowsPerBlock;
   fill_f32<<<(int)std::min<int64_t>((nthr + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, nthr,
                                                                              INFINITY);
-  row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
-      V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
-  iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
-  {
-    size_t tb = pl.sort_temp_bytes;
-    GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.sort_tmp, tb, w.rn, w.rn_s, w.ids,
-                                                           w.perm_n, (int)n, 0, 32, s));
+  if (!norms_ready) {
+    row_norms<<<(int)std::min<int64_t>((n * 32 + 255) / 256, sms * 16), 256, 0, s>>>(
+        V, lambda, n, k, w.rn, &w.sc->rn_max_bits);
+    iota_i32<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.ids, n);
+    {
+      size_t tb = pl.sort_temp_bytes;
+      GGM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(w.sort_tmp, tb, w.rn, w.rn_s, w.ids,
+                                                             w.perm_n, (int)n, 0, 32, s));
+    }
+    count_launches(4);
+  } else {
+    count_launches(1);
   }
-  count_launches(4);
   if (pl.mode == 1) {
     // threshold mode: every row's bound is τ itself (accumulator units); no seed pass
     fill_tau<<<(int)std::min<int64_t>((n + 255) / 256, sms * 8), 256, 0, s>>>(w.thr, n, fp.tau, w.sc);
@@ -3152,6 +3199,7 @@ extern "C" ggm_status ggm_sparse_precision(int64_t n, int k, const float* V, con
                                            int32_t* col, float* val, int64_t capacity,
                                            int64_t* nnz_out, void* workspace,
                                            size_t workspace_bytes, void* stream) {
+  seed_stamp_forget(workspace);
   if (!V || !lambda || !row_ptr || !nnz_out || !workspace)
     return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
   if (opts && opts->mode != 0 && opts->mode != 1)
@@ -3503,6 +3551,7 @@ extern "C" ggm_status ggm_sym_seed_shard(int64_t n, int k, const float* V, const
     return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
   if (nranks < 1 || nranks > GGM_MAX_RANKS || rank < 0 || rank >= nranks)
     return fail(GGM_ERR_INVALID_ARGUMENT, "rank %d / nranks %d invalid", rank, nranks);
+  seed_stamp_forget(workspace);
   Plan pl;
   ggm_status st = sym_shard_plan(n, k, opts, &pl);
   if (st != GGM_OK) return st;
@@ -3535,6 +3584,7 @@ extern "C" ggm_status ggm_sym_seed_shard(int64_t n, int k, const float* V, const
   GGM_CUDA_TRY(cudaMemcpy(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost));
   if (hs.flags & 1) return fail(GGM_ERR_DOMAIN, "V contains non-finite values");
   if (hs.flags & 2) return fail(GGM_ERR_DOMAIN, "lambda must be finite and > 0 (P:65)");
+  seed_stamp_set(workspace, SeedStamp{V, lambda, n, k, opts->topk, opts->mode, nranks});
   return GGM_OK;
 }
 
@@ -3568,8 +3618,16 @@ static ggm_status sym_shard_impl(
   EventTimer tm(timing_enabled(), s);
   tm.mark(0);
   const int sms = num_sms();
-  GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
-  {
+  // seeded call on the workspace of this rank's seed share with the same inputs: the scale,
+  // the domain flags, the row norms and the norm order are reused (seed_stamp_take)
+  const bool reuse =
+      thr_all && seed_stamp_take(workspace, SeedStamp{V, lambda, n, k, opts->topk, opts->mode, nranks});
+  if (!thr_all) seed_stamp_forget(workspace);
+  if (reuse) {
+    reset_pool_counters<<<1, 1, 0, s>>>(w.sc);
+    count_launches(1);
+  } else {
+    GGM_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(DevScalars), s));
     const int64_t total = n * (int64_t)k;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sms * 8));
     absmax_check<<<grid, 256, 0, s>>>(V, lambda, n, k, w.sc);
@@ -3577,7 +3635,7 @@ static ggm_status sym_shard_impl(
     count_launches(2);
   }
   FusedParams fp = base_params(pl, w, n, 0);
-  st = sym_prepare(pl, w, V, lambda, n, k, fp, s, -1, -1, thr_all);
+  st = sym_prepare(pl, w, V, lambda, n, k, fp, s, -1, -1, thr_all, 0.f, reuse);
   if (st != GGM_OK) return st;
   tm.mark(1);
   // this rank's block pairs (the merge ownership of rows below stays the contiguous
@@ -4252,6 +4310,7 @@ extern "C" ggm_status ggm_sparse_precision_overall(
     int64_t n, int k, const float* V, const double* lambda, const ggm_overall_opts* opts,
     int64_t cand_capacity, int64_t* row_ptr, int32_t* col, float* val, int64_t capacity,
     int64_t* nnz_out, void* workspace, size_t workspace_bytes, void* stream) {
+  seed_stamp_forget(workspace);
   if (!V || !lambda || !row_ptr || !nnz_out || !workspace)
     return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
   OverallPlan op;

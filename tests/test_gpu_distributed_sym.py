@@ -22,17 +22,21 @@ def G():
     return G
 
 
-def _simulate(G, V, lam, t, P, seeded=False):
+def _simulate(G, V, lam, t, P, seeded=False, same_plans=False):
+    """same_plans: every rank seeds and runs on ONE workspace (as bench.py and parallel.py
+    do), so the seeded call reuses the seed call's scale, norms and norm order."""
     n, k = V.shape
     thr_all = None
+    plans = [G.SymShardPlan(n, k, t, r, P) for r in range(P)] if same_plans else None
     if seeded:  # sharded seed pass: every rank's share, combined by an element-wise minimum
-        parts = [G.SymShardPlan(n, k, t, r, P).seed(V, lam) for r in range(P)]
+        parts = [(plans[r] if same_plans else G.SymShardPlan(n, k, t, r, P)).seed(V, lam).clone()
+                 for r in range(P)]
         thr_all = torch.stack(parts).min(dim=0).values
         for r, part in enumerate(parts):
             assert torch.isinf(part).any() or P == 1
     shards = []
     for r in range(P):
-        plan = G.SymShardPlan(n, k, t, r, P)
+        plan = plans[r] if same_plans else G.SymShardPlan(n, k, t, r, P)
         key, val, counts, perm = plan.run(V, lam, thr_all=thr_all)
         torch.cuda.synchronize()
         shards.append((key.clone(), val.clone(), counts, perm.clone()))
@@ -109,5 +113,20 @@ def test_unit_assignments_equal_single_call(G, monkeypatch, assign, P):
     rp, c, v = G.ggm_sparse_precision(Vd, ld, 0, n, mode=0, topk=t, symmetric=1)
     torch.cuda.synchronize()
     c2, v2 = _simulate(G, Vd, ld, t, P, seeded=True)
+    assert np.array_equal(c.cpu().numpy(), c2)
+    np.testing.assert_array_equal(v.cpu().numpy(), v2)
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_seeded_call_reusing_the_seed_workspace(G, P):
+    """The seeded shard call on the workspace of the same rank's seed call (same V, λ) reuses
+    its scale, row norms and norm order: bitwise the single call."""
+    n, k, t = 20000, 100, 10
+    V, lam = gen.small_factor(555 + P, n, k)
+    Vd = torch.from_numpy(V).cuda()
+    ld = torch.from_numpy(np.asarray(lam, np.float64)).cuda()
+    rp, c, v = G.ggm_sparse_precision(Vd, ld, 0, n, mode=0, topk=t, symmetric=1)
+    torch.cuda.synchronize()
+    c2, v2 = _simulate(G, Vd, ld, t, P, seeded=True, same_plans=True)
     assert np.array_equal(c.cpu().numpy(), c2)
     np.testing.assert_array_equal(v.cpu().numpy(), v2)

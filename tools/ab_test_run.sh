@@ -1,6 +1,5 @@
-# GPU box: symmetric-scheme tests on the default build, then the A/B against variant $V.
+# GPU box: distributed-scheme tests, then the per-rank shares (sim_ranks N = 1 2 4 8).
 set -u
 mkdir -p gpurun_out
-V=${V:?variant}
-timeout 900 python -m pytest tests/test_gpu_sparse.py tests/test_gpu_sym_stress.py tests/test_gpu_distributed_sym.py tests/test_gpu_overall.py tests/test_gpu_configs.py tests/test_gpu_determinism.py -x -q > gpurun_out/ab_tests_default.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/ab_tests_default.log
-V=$V bash tools/ab_run.sh
+timeout 900 python -m pytest tests/test_gpu_distributed_sym.py tests/test_gpu_sparse.py tests/test_gpu_overall.py -x -q > gpurun_out/r02k_pytest.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/r02k_pytest.log
+timeout 800 python tools/sim_ranks.py 1 2 4 8 > gpurun_out/r02k_simranks.log 2>&1; echo "sim rc=$?"; tail -4 gpurun_out/r02k_simranks.log
