@@ -3727,6 +3727,7 @@ extern "C" ggm_status ggm_sym_merge(int64_t n, int t, const uint32_t* cand_key,
                                     int64_t row_begin, int64_t row_end, int64_t* row_id,
                                     int32_t* col, float* val, void* workspace,
                                     size_t workspace_bytes, void* stream) {
+  seed_stamp_forget(workspace);
   if (!perm || !row_id || !col || !val || (ncand > 0 && (!cand_key || !cand_val)) || !workspace)
     return fail(GGM_ERR_INVALID_ARGUMENT, "null pointer argument");
   if (n < 2 || row_begin < 0 || row_end > n || row_begin > row_end || ncand < 0)
