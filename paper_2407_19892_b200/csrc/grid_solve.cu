@@ -51,6 +51,13 @@ constexpr int kMaxAxes = 8;
 #endif
 constexpr int kThreads = GGM_SOLVE_THREADS;
 constexpr int kWarps = kThreads / 32;
+#ifndef GGM_SOLVE_RED_GROUPS
+#define GGM_SOLVE_RED_GROUPS 4
+#endif
+// red_mode 2 (default): accumulator copies, block b adds into copy b mod kRedGroups.  C3 solve
+// kernel: 4 copies 1.003 ms, 8 1.015, 16 1.052, one accumulator (red_mode 0) 1.065
+// (profiles/r02_logs/r02k_redgroups.log, r02k_red2.log)
+constexpr int kRedGroups = GGM_SOLVE_RED_GROUPS;
 constexpr int kMaxFastBins = 1024;  // private per-warp bins: kWarps x k_fast doubles
 
 struct GridDesc {
@@ -406,13 +413,37 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
   for (;; ++pass) {
     // ---------------------------------------------------------------- grid pass at slam
     for (int i = tid; i < T1; i += blockDim.x) sg[i] = 0.0;
-    if (blockIdx.x == 0 && !single)
+    if (blockIdx.x == 0 && !single && p.red_mode != 2)
       for (int i = tid; i < T1; i += blockDim.x) p.gacc[(size_t)((pass + 1) % 3) * T1 + i] = 0.0;
+    if (!single && p.red_mode == 2) {  // zero the next pass's group accumulators (all blocks)
+      double* nb = p.part + (size_t)((pass + 1) % 3) * kRedGroups * T1;
+      for (int64_t e = (int64_t)blockIdx.x * blockDim.x + tid; e < (int64_t)kRedGroups * T1;
+           e += (int64_t)gridDim.x * blockDim.x)
+        nb[e] = 0.0;
+    }
     __syncthreads();
     // Σ_γ of the modalities' marginals (Thm 2): each pass adds into the same sg
     for (int m = 0; m < p.M; ++m) grid_pass<J, LOGS>(p.gd[m], slam, sg, pw, gw, nw);
     __syncthreads();
-    if (!single && p.red_mode == 0) {
+    if (!single && p.red_mode == 2) {
+      // grouped fp64 atomics: block b adds into accumulator copy b mod kRedGroups (1/kRedGroups
+      // of the same-address contention of one accumulator), every block sums the copies in a
+      // fixed order after the barrier
+      double* accb = p.part + (size_t)(pass % 3) * kRedGroups * T1;
+      double* acc = accb + (size_t)(blockIdx.x % kRedGroups) * T1;
+      for (int i = tid; i < T1; i += blockDim.x) {
+        const double v = sg[i];
+        if (v != 0.0) atomicAdd(&acc[i], v);
+      }
+      grid.sync();
+      for (int i = tid; i < T1; i += blockDim.x) {
+        double t = 0.0;
+#pragma unroll
+        for (int gq = 0; gq < kRedGroups; ++gq) t += __ldcg(&accb[(size_t)gq * T1 + i]);
+        sg[i] = t;
+      }
+      __syncthreads();
+    } else if (!single && p.red_mode == 0) {
       double* acc = p.gacc + (size_t)(pass % 3) * T1;
       for (int i = tid; i < T1; i += blockDim.x) {
         const double v = sg[i];
@@ -914,9 +945,11 @@ static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double
   sp.gred = sp.part + 2 * (size_t)num_sms() * ((size_t)T + 1);
   {
     const char* e = std::getenv("GGM_SOLVE_RED");  // A/B hook (tools/solve_probe.py)
-    sp.red_mode = e ? std::atoi(e) : 0;
+    sp.red_mode = e ? std::atoi(e) : 2;
   }
   GGM_CUDA_TRY(cudaMemsetAsync(gacc, 0, sizeof(double) * (3 * ((size_t)T + 1) + 8) + 64, s));
+  if (sp.red_mode == 2)  // the first pass's group accumulators (3 x kRedGroups copies fit part[])
+    GGM_CUDA_TRY(cudaMemsetAsync(sp.part, 0, sizeof(double) * 3 * kRedGroups * ((size_t)T + 1), s));
   check_E<<<4, 256, 0, s>>>(E, T, istat + 6);
   GGM_CUDA_TRY(cudaGetLastError());
   int hbad = 0;

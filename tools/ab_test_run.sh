@@ -1,5 +1,9 @@
-# GPU box: distributed-scheme tests, then the per-rank shares (sim_ranks N = 1 2 4 8).
+# GPU box: BK4 accumulator-copy count (default 8 vs 16 / 4), C3 solve kernel time.
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_distributed_sym.py tests/test_gpu_sparse.py tests/test_gpu_overall.py -x -q > gpurun_out/r02k_pytest.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/r02k_pytest.log
-timeout 800 python tools/sim_ranks.py 1 2 4 8 > gpurun_out/r02k_simranks.log 2>&1; echo "sim rc=$?"; tail -4 gpurun_out/r02k_simranks.log
+for i in 1 2 3; do
+  TAG=g8 timeout 300 python tools/solve_ab.py
+  GGM_LIB_PATH=tools/variants/red16.so TAG=g16 timeout 300 python tools/solve_ab.py
+  GGM_LIB_PATH=tools/variants/red4.so TAG=g4 timeout 300 python tools/solve_ab.py
+done 2>&1 | grep "C3" > gpurun_out/r02k_redgroups.log
+cat gpurun_out/r02k_redgroups.log
