@@ -313,9 +313,11 @@ def stage_timings(G, torch):
         Ec = torch.cat(Es)
         G.ggm_solve_eigvals(Ec, ks)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        _, info = G.ggm_solve_eigvals(Ec, ks)
-        solve_ms = (time.perf_counter() - t0) * 1e3
+        solve_ms = float("inf")
+        for _ in range(3):                        # whole call incl. host work: best of 3
+            t0 = time.perf_counter()
+            _, info = G.ggm_solve_eigvals(Ec, ks)
+            solve_ms = min(solve_ms, (time.perf_counter() - t0) * 1e3)
         pts = float(np.prod(ks))
         kms = info["kernel_ms"]
         out[name] = {"gram_eig_ms": gram_ms, "solve_ms": solve_ms,

@@ -711,7 +711,14 @@ def sym_merge(n: int, t: int, key: torch.Tensor, val: torch.Tensor, perm: torch.
               row_begin: int, row_end: int, stream=None):
     """Merge received candidates of bound-order rows [row_begin, row_end): returns
     (row_id int64 [rows], col int32 [rows*t_eff], val float32 [rows*t_eff])."""
+    _require_cuda(key, torch.int32, "key")
+    _require_cuda(val, torch.int32, "val")
+    _require_cuda(perm, torch.int32, "perm")
     ncand = int(key.numel())
+    if val.numel() != 2 * ncand:
+        raise ValueError("val must hold two int32 words per candidate key")
+    if perm.numel() != int(n) or not (0 <= int(row_begin) <= int(row_end) <= int(n)):
+        raise ValueError("perm length != n or row range outside [0, n]")
     dev = perm.device
     te = min(int(t), int(n) - 1)
     rows = int(row_end) - int(row_begin)

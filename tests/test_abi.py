@@ -90,6 +90,21 @@ def test_solve_and_gram_validation(G):
     assert o.tol == 1e-7 and o.max_iter == 20000 and o.gauge == 0 and o.trace_tol == 1e-8
 
 
+def test_binding_rejects_host_tensors(G):
+    """The Python binding refuses CPU / wrong-dtype tensors before any pointer reaches the
+    library (a host pointer handed to a kernel would fault the context)."""
+    import torch
+    key = torch.zeros(4, dtype=torch.int32)
+    val = torch.zeros(4, 2, dtype=torch.int32)
+    perm = torch.arange(8, dtype=torch.int32)
+    with pytest.raises(ValueError):
+        G.sym_merge(8, 2, key, val, perm, 0, 8)
+    with pytest.raises(ValueError):
+        G.ggm_solve_eigvals(torch.ones(5, dtype=torch.float64), [3, 2])
+    with pytest.raises(ValueError):
+        G.ggm_sparse_precision(torch.zeros(8, 3), torch.ones(3, dtype=torch.float64))
+
+
 def test_product_path_has_no_oracle_import():
     """The CUDA path never imports the oracle (or any CPU fallback)."""
     pkg = os.path.join(ROOT, "paper_2407_19892_b200")
