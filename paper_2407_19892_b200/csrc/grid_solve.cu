@@ -130,7 +130,7 @@ __device__ __forceinline__ void point_row(const double (&lv)[J], double (&acc)[J
 
 template <int J, int NOUT, bool LOGS>
 __device__ void grid_pass_fast(const GridDesc& gd, const double* slam, double* sg, double* pw,
-                               int64_t gwarp, int64_t nwarps) {
+                               int64_t gwarp, int64_t nwarps, double* accw = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int kin = gd.k[gd.inner];
   const int oin = gd.off[gd.inner];
@@ -210,10 +210,15 @@ __device__ void grid_pass_fast(const GridDesc& gd, const double* slam, double* s
       }
     }
   }
+  if (NOUT >= 1 && accw != nullptr) {  // per-warp rows, folded below (no fp64 smem CAS loops)
 #pragma unroll
-  for (int jj = 0; jj < J; ++jj) {
-    const int m = lane + 32 * jj;
-    if (m < kin) atomicAdd(&sg[oin + m], acc[jj]);
+    for (int jj = 0; jj < J; ++jj) accw[wid * 32 * J + lane + 32 * jj] = acc[jj];
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      const int m = lane + 32 * jj;
+      if (m < kin) atomicAdd(&sg[oin + m], acc[jj]);
+    }
   }
   if (LOGS) {
     lsum = warp_sum(lsum);
@@ -231,6 +236,12 @@ __device__ void grid_pass_fast(const GridDesc& gd, const double* slam, double* s
       }
       sg[gd.off[af] + f] += t;
     }
+    if (accw != nullptr)
+      for (int m = threadIdx.x; m < kin; m += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < kWarps; ++w) t += accw[w * 32 * J + m];
+        sg[oin + m] += t;
+      }
     __syncthreads();
   }
 }
@@ -303,15 +314,16 @@ __host__ __device__ inline int fast_bins(const GridDesc& gd) {
 
 template <int J, bool LOGS>
 __device__ __forceinline__ void grid_pass(const GridDesc& gd, const double* slam, double* sg,
-                                          double* pw, int64_t gwarp, int64_t nwarps) {
+                                          double* pw, int64_t gwarp, int64_t nwarps,
+                                          double* accw = nullptr) {
   if (!fast_path(gd) || pw == nullptr) {
     grid_pass_generic<J, LOGS>(gd, slam, sg, gwarp, nwarps);
     return;
   }
   switch (gd.n_outer) {
     case 0: grid_pass_fast<J, 0, LOGS>(gd, slam, sg, pw, gwarp, nwarps); break;
-    case 1: grid_pass_fast<J, 1, LOGS>(gd, slam, sg, pw, gwarp, nwarps); break;
-    default: grid_pass_fast<J, 2, LOGS>(gd, slam, sg, pw, gwarp, nwarps); break;
+    case 1: grid_pass_fast<J, 1, LOGS>(gd, slam, sg, pw, gwarp, nwarps, accw); break;
+    default: grid_pass_fast<J, 2, LOGS>(gd, slam, sg, pw, gwarp, nwarps, accw); break;
   }
 }
 
@@ -329,6 +341,7 @@ struct SolveParams {
   double gd_eps;          // method 2: grid-minimum feasibility ε (reading Q3)
   int scheme;
   int pw_stride;          // doubles of private bins per block (kWarps x max k_fast)
+  int accw;               // 1: kWarps x 32 J doubles after the bins hold per-warp inner marginals
   double* lam_out;        // λ at exit, Σk
   double* g;              // marginals at lam_out, Σk
   double* gacc;           // [3][Σk + 1] rotating global accumulators of the block partials
@@ -388,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
   double* th0 = slam + T;
   double* th1 = th0 + T;
   double* pw = p.pw_stride > 0 ? th1 + T : nullptr;  // private bins (fast pass) if allotted
+  double* accw = pw != nullptr && p.accw ? pw + p.pw_stride : nullptr;  // per-warp inner rows
   __shared__ double s_red[kWarps];
   const int tid = threadIdx.x;
   const double* __restrict__ E = p.E;
@@ -423,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
     }
     __syncthreads();
     // Σ_γ of the modalities' marginals (Thm 2): each pass adds into the same sg
-    for (int m = 0; m < p.M; ++m) grid_pass<J, LOGS>(p.gd[m], slam, sg, pw, gw, nw);
+    for (int m = 0; m < p.M; ++m) grid_pass<J, LOGS>(p.gd[m], slam, sg, pw, gw, nw, accw);
     __syncthreads();
     if (!single && p.red_mode == 2) {
       // grouped fp64 atomics: block b adds into accumulator copy b mod kRedGroups (1/kRedGroups
@@ -987,9 +1001,21 @@ static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double
   }
   // shared memory: sg[T+1], slam[T], th0[T], th1[T], private bins; if that does not fit,
   // the plain MM step with sg and slam only and the generic pass
-  const size_t smem_full = ((size_t)4 * T + 1 + (size_t)kWarps * kfmax) * sizeof(double) + 16;
+  // per-warp inner-marginal rows (kWarps x 32 J doubles) in place of fp64 shared atomics,
+  // which compile to CAS loops (ATOMS.CAST.SPIN.64) contended by the block's 16 warps:
+  // C3 kernel 1.004 -> 0.970 ms (profiles/r02_logs/r02end_ab_accw.log); -DGGM_SOLVE_NOACCW
+  // restores the atomics
+#ifndef GGM_SOLVE_NOACCW
+  const size_t accw_d = (size_t)kWarps * 32 * J;
+#else
+  const size_t accw_d = 0;
+#endif
+  const size_t smem_base = ((size_t)4 * T + 1 + (size_t)kWarps * kfmax) * sizeof(double) + 16;
+  const bool accw_fits = accw_d > 0 && smem_base + accw_d * sizeof(double) <= 200 * 1024;
+  const size_t smem_full = smem_base + (accw_fits ? accw_d * sizeof(double) : 0);
   const bool fits = smem_full <= 200 * 1024;
   sp.pw_stride = fits ? kWarps * kfmax : 0;
+  sp.accw = fits && accw_fits ? 1 : 0;
   const size_t smem_launch = fits ? smem_full : ((size_t)2 * T + 1) * sizeof(double) + 16;
   if (!fits && o.method == 2)
     return fail(GGM_ERR_UNSUPPORTED, "method 2: sum(k)=%d too large for the solve kernel", T);
