@@ -342,6 +342,7 @@ struct SolveParams {
   int scheme;
   int pw_stride;          // doubles of private bins per block (kWarps x max k_fast)
   int accw;               // 1: kWarps x 32 J doubles after the bins hold per-warp inner marginals
+  int sE_off;             // >= 0: E cached at this offset (doubles) of dynamic shared memory
   double* lam_out;        // λ at exit, Σk
   double* g;              // marginals at lam_out, Σk
   double* gacc;           // [3][Σk + 1] rotating global accumulators of the block partials
@@ -404,7 +405,14 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
   double* accw = pw != nullptr && p.accw ? pw + p.pw_stride : nullptr;  // per-warp inner rows
   __shared__ double s_red[kWarps];
   const int tid = threadIdx.x;
-  const double* __restrict__ E = p.E;
+  // E (read by every update) cached in shared memory when the host allotted it
+  const double* E = p.E;
+  if (p.sE_off >= 0) {
+    double* se = dsm + p.sE_off;
+    for (int i = tid; i < T; i += blockDim.x) se[i] = p.E[i];
+    __syncthreads();
+    E = se;
+  }
   for (int i = tid; i < T; i += blockDim.x) {
     const double l0 = fmax(1.0 / E[i], p.floor);  // Alg. 1 line 5
     slam[i] = l0;
@@ -542,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
       continue;
     }
     double mr = 0.0;
+    #pragma unroll 2
     for (int i = tid; i < T; i += blockDim.x) mr = fmax(mr, kkt_term(slam[i], sg[i], E[i], p.floor));
     res = block_max(mr, s_red) / emax;
     if (res <= p.tol) {
@@ -553,12 +562,14 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
     if (p.scheme == kSchemeMM) {
       // majorise-minimise step, clamped on the box (a separable majoriser minimised per
       // coordinate)
+      #pragma unroll 2
       for (int i = tid; i < T; i += blockDim.x) slam[i] = fmax(p.floor, slam[i] * sg[i] / E[i]);
       __syncthreads();
       continue;
     }
     // SQUAREM (interior regime, floor = 0), log space θ = log λ, map F(θ) = θ + log(g/E)
     if (phase == 0) {  // slam = exp(θ0): θ1 = F(θ0)
+      #pragma unroll 2
       for (int i = tid; i < T; i += blockDim.x) {
         const double t1 = th0[i] + log(sg[i] / E[i]);
         th1[i] = t1;
@@ -568,6 +579,7 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
     } else if (phase == 1) {  // slam = exp(θ1): θ2 = F(θ1), extrapolate
       r1 = res;
       double nr = 0.0, nv = 0.0;
+      #pragma unroll 2
       for (int i = tid; i < T; i += blockDim.x) {
         const double t0 = th0[i], t1 = th1[i];
         const double t2 = t1 + log(sg[i] / E[i]);
@@ -590,6 +602,7 @@ __global__ void __launch_bounds__(kThreads, J <= 7 ? 2 * GGM_SOLVE_MINB : GGM_SO
       phase = 2;
     } else {  // slam = exp(θ'): stabilising step θ0 = F(θ') if no worse than θ1, else θ2
       const bool take = res <= r1;
+      #pragma unroll 2
       for (int i = tid; i < T; i += blockDim.x) {
         if (take) th0[i] = th1[i] + log(sg[i] / E[i]);
         slam[i] = exp(th0[i]);
@@ -1012,11 +1025,16 @@ static ggm_status solve_common(SolveParams sp, const ModelAxes& ax, const double
 #endif
   const size_t smem_base = ((size_t)4 * T + 1 + (size_t)kWarps * kfmax) * sizeof(double) + 16;
   const bool accw_fits = accw_d > 0 && smem_base + accw_d * sizeof(double) <= 200 * 1024;
-  const size_t smem_full = smem_base + (accw_fits ? accw_d * sizeof(double) : 0);
-  const bool fits = smem_full <= 200 * 1024;
+  const size_t smem_pw = smem_base + (accw_fits ? accw_d * sizeof(double) : 0);
+  const bool fits = smem_pw <= 200 * 1024;
   sp.pw_stride = fits ? kWarps * kfmax : 0;
   sp.accw = fits && accw_fits ? 1 : 0;
-  const size_t smem_launch = fits ? smem_full : ((size_t)2 * T + 1) * sizeof(double) + 16;
+  // E in shared memory after everything else, when it fits
+  const size_t se_at = fits ? smem_pw : ((size_t)2 * T + 1) * sizeof(double) + 16;
+  const bool se_fits = se_at + (size_t)T * sizeof(double) <= 200 * 1024;
+  sp.sE_off = se_fits ? (int)(align_up(se_at, 16) / sizeof(double)) : -1;
+  const size_t smem_full = se_fits ? align_up(se_at, 16) + (size_t)T * sizeof(double) : smem_pw;
+  const size_t smem_launch = (fits || se_fits) ? smem_full : ((size_t)2 * T + 1) * sizeof(double) + 16;
   if (!fits && o.method == 2)
     return fail(GGM_ERR_UNSUPPORTED, "method 2: sum(k)=%d too large for the solve kernel", T);
   sp.E = o.method == 2 ? E : Eu;
